@@ -1,0 +1,400 @@
+"""Pins of the CPU oracle against things other than itself.
+
+Independent references used here: closed forms, scipy.linalg.expm /
+expm_frechet, numpy eigendecompositions, scipy.integrate.solve_ivp on Eq. 6
+written in matrix form, and mathematical invariants.  No CUDA involved.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.integrate
+import scipy.linalg
+
+from paper_2511_13330_b200 import inputs as qi
+
+
+def vec(rho):
+    """column stacking: vec(rho)[i + d j] = rho[i, j]   (A5)"""
+    return rho.reshape(-1, order="F")
+
+
+def unvec(v, d):
+    return v.reshape(d, d, order="F")
+
+
+def rand_c(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def rand_herm(rng, d):
+    a = rand_c(rng, d, d)
+    return (a + a.conj().T) / 2
+
+
+def rand_rho(rng, d):
+    a = rand_c(rng, d, d)
+    r = a @ a.conj().T
+    return r / np.trace(r)
+
+
+def eq6_numpy(H, C, rho):
+    """Eq. 6 in matrix form, written independently of the oracle."""
+    out = -1j * (H @ rho - rho @ H)
+    for c in C:
+        cd = c.conj().T
+        out += c @ rho @ cd - 0.5 * (cd @ c @ rho + rho @ cd @ c)
+    return out
+
+
+# ---------------------------------------------------------------- layout / Eq. 8
+def test_vectorization_convention(oracle):
+    # vec([[a,b],[c,d]]) = (a,c,b,d) and vec(H rho) = (I (x) H) vec(rho)
+    assert np.array_equal(vec(np.array([[1, 2], [3, 4]])), [1, 3, 2, 4])
+    rng = np.random.default_rng(1)
+    H = rand_herm(rng, 3)
+    L0, _ = oracle.build_liouvillian(H, np.zeros((0, 3, 3)), np.zeros((0, 3, 3)))
+    rho = rand_c(rng, 3, 3)
+    assert np.allclose(L0 @ vec(rho), vec(-1j * (H @ rho - rho @ H)), atol=1e-14)
+
+
+@pytest.mark.parametrize("d", [2, 3, 8])
+def test_eq8_matches_eq6(oracle, d):
+    rng = np.random.default_rng(d)
+    H = rand_herm(rng, d)
+    C = rand_c(rng, 3, d, d) * 0.3
+    Hc = np.stack([rand_herm(rng, d)])
+    L0, Lc = oracle.build_liouvillian(H, Hc, C)
+    rho = rand_rho(rng, d)
+    want = eq6_numpy(H, C, rho)
+    assert np.abs(L0 @ vec(rho) - vec(want)).max() < 1e-13
+    assert np.abs(unvec(L0 @ vec(rho), d) - oracle.lindblad_rhs(H, C, rho)).max() < 1e-13
+    # control Liouvillian has no dissipator: L_j vec(rho) = vec(-i[H_j, rho])
+    assert np.abs(Lc[0] @ vec(rho) - vec(-1j * (Hc[0] @ rho - rho @ Hc[0]))).max() < 1e-13
+    # spectrum of a Lindblad generator: Re(lambda) <= 0
+    assert np.linalg.eigvals(L0).real.max() < 1e-9
+
+
+def test_liouvillian_zero(oracle):
+    L0, Lc = oracle.build_liouvillian(np.zeros((2, 2)), np.zeros((1, 2, 2)), np.zeros((0, 2, 2)))
+    assert not L0.any() and not Lc.any()
+
+
+# ---------------------------------------------------------------- expm (Eq. 14), P-11
+@pytest.mark.parametrize("n,scale", [(4, 1e-3), (4, 3.0), (16, 0.7), (64, 0.05), (64, 0.9), (64, 12.0)])
+def test_expm_vs_scipy(oracle, n, scale):
+    rng = np.random.default_rng(n)
+    A = rand_c(rng, n, n)
+    A *= scale / np.abs(A).sum(0).max()
+    E = oracle.expm(A)
+    R = scipy.linalg.expm(A)
+    assert np.linalg.norm(E - R) / np.linalg.norm(R) < 5e-14
+
+
+def test_expm_closed_forms(oracle):
+    assert np.array_equal(oracle.expm(np.zeros((5, 5), complex)), np.eye(5))
+    dg = np.array([0.1, -2.0, 3.5 + 1j, -0.7j])
+    assert np.allclose(oracle.expm(np.diag(dg)), np.diag(np.exp(dg)), rtol=1e-14, atol=0)
+    assert np.array_equal(oracle.expm(np.array([[0, 1], [0, 0]], complex)), [[1, 1], [0, 1]])
+    # e^{-iHt} for Hermitian H via the eigendecomposition (independent of any expm)
+    rng = np.random.default_rng(7)
+    H = rand_herm(rng, 8)
+    w, Q = np.linalg.eigh(H)
+    want = (Q * np.exp(-1j * w * 1.7)) @ Q.conj().T
+    assert np.abs(oracle.expm(-1j * 1.7 * H) - want).max() < 1e-13
+
+
+# ---------------------------------------------------------------- Frechet, P-9
+def test_frechet_vs_scipy(oracle):
+    rng = np.random.default_rng(3)
+    for n, s in [(4, 0.5), (16, 1.3), (64, 0.4)]:
+        A = rand_c(rng, n, n)
+        A *= s / np.abs(A).sum(0).max()
+        E = rand_c(rng, n, n)
+        L, X = oracle.frechet(A, E)
+        Xs, Ls = scipy.linalg.expm_frechet(A, E)
+        assert np.linalg.norm(L - Ls) / np.linalg.norm(Ls) < 1e-13
+        assert np.linalg.norm(X - Xs) / np.linalg.norm(Xs) < 1e-13
+        # commuting case L(A, A) = A e^A
+        L2, _ = oracle.frechet(A, A)
+        assert np.linalg.norm(L2 - A @ Xs) / np.linalg.norm(L2) < 1e-13
+
+
+# ---------------------------------------------------------------- RK4 oracle (O8)
+def test_rk4_precession_and_order(oracle):
+    b, T = 2.0, math.pi
+    H0 = (b / 2) * qi.SZ
+    L0, Lc = oracle.build_liouvillian(H0, np.zeros((1, 2, 2)), np.zeros((0, 2, 2)))
+    rho0 = np.array([[0.5, 0.5], [0.5, 0.5]], complex)
+    errs = []
+    for sub in (8, 16):
+        Lam = oracle.rk4(L0, Lc, T, 4, sub, u=np.zeros((4, 1)))
+        rho = unvec(Lam @ vec(rho0), 2)
+        errs.append(abs(rho[0, 1] - 0.5 * np.exp(-1j * b * T)))
+    Lam = oracle.rk4(L0, Lc, T, 4, 256, u=np.zeros((4, 1)))
+    assert abs(unvec(Lam @ vec(rho0), 2)[0, 1] - 0.5 * np.exp(-1j * b * T)) < 1e-8
+    assert 4 - 0.3 < math.log2(errs[0] / errs[1]) < 4 + 0.3
+
+
+# ---------------------------------------------------------------- P-1, P-2, P-12
+def test_p1_identity(oracle):
+    L0, Lc = oracle.build_liouvillian(np.zeros((8, 8)), np.zeros((2, 8, 8)), np.zeros((0, 8, 8)))
+    Lam = oracle.propagate(L0, Lc, np.zeros((16, 2)), 10.0, 16)
+    assert np.array_equal(Lam, np.eye(64))
+
+
+def test_p2_constant_controls(oracle):
+    p = qi.cfg0()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    T = 25.0
+    uc = np.array([0.1, 0.2])
+    L = L0 + uc[0] * Lc[0] + uc[1] * Lc[1]
+    ref = scipy.linalg.expm(T * L)
+    lam1 = oracle.propagate(L0, Lc, np.tile(uc, (1, 1)), T, 1)
+    lam8 = oracle.propagate(L0, Lc, np.tile(uc, (8, 1)), T, 8)
+    assert np.linalg.norm(lam1 - ref) / np.linalg.norm(ref) < 1e-12
+    assert np.linalg.norm(lam8 - lam1) / np.linalg.norm(ref) < 1e-12
+
+
+def test_p12_ordering_and_semigroup(oracle):
+    p = qi.cfg0()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    u = np.array([[0.3, 0.0], [0.0, 0.3]])          # slice 0 (earlier) then slice 1 (later)
+    h = 3.0
+    A = scipy.linalg.expm(h * (L0 + 0.3 * Lc[0]))
+    B = scipy.linalg.expm(h * (L0 + 0.3 * Lc[1]))
+    assert np.linalg.norm(A @ B - B @ A) > 1e-3        # non-commuting fixture
+    Lam = oracle.propagate(L0, Lc, u, 2 * h, 2)
+    assert np.linalg.norm(Lam - B @ A) < 1e-12
+    assert np.linalg.norm(Lam - A @ B) > 1e-3
+    # [0, T] = [T/2, T] o [0, T/2]
+    N = 32
+    full = oracle.propagate(L0, Lc, p.u[0, :N], 12.5, N)
+    first = oracle.propagate(L0, Lc, p.u[0, :N], 12.5, N, k1=N // 2)
+    second = oracle.propagate(L0, Lc, p.u[0, :N], 12.5, N, k0=N // 2)
+    assert np.linalg.norm(second @ first - full) / np.linalg.norm(full) < 1e-13
+    # ordered product helper: earlier on the right
+    assert np.allclose(oracle.ordered_product(np.stack([A, B])), B @ A, atol=1e-14)
+
+
+# ---------------------------------------------------------------- P-3, P-4, P-5, P-13
+def hilbert_magnus4(H1, H2, h):
+    """Hilbert-space 4th-order Magnus generator for one slice (test's own Hilbert-space form)."""
+    A1, A2 = -1j * H1, -1j * H2
+    return 0.5 * h * (A1 + A2) - math.sqrt(3) * h * h / 12 * (A1 @ A2 - A2 @ A1)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_p3_zero_dissipation(oracle, mode):
+    p = qi.cfg0()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, np.zeros((0, 8, 8)))
+    N, T = 64, 25.0
+    h = T / N
+    rng = np.random.default_rng(11)
+    if mode == 0:
+        u = p.u[0, :N]
+        nodes = np.stack([u, u], axis=1)
+    else:
+        nodes = rng.uniform(0, qi.U_MAX, (N, 2, 2))
+        u = nodes
+    Lam = oracle.propagate(L0, Lc, u, T, N, mode=mode)
+    U = np.eye(8, dtype=complex)
+    for k in range(N):
+        H1 = p.H0[0] + nodes[k, 0, 0] * p.Hc[0] + nodes[k, 0, 1] * p.Hc[1]
+        H2 = p.H0[0] + nodes[k, 1, 0] * p.Hc[0] + nodes[k, 1, 1] * p.Hc[1]
+        U = scipy.linalg.expm(hilbert_magnus4(H1, H2, h)) @ U
+    assert np.abs(U.conj().T @ U - np.eye(8)).max() < 1e-13
+    want = np.kron(U.conj(), U)
+    assert np.linalg.norm(Lam - want) / np.linalg.norm(want) < 1e-12
+
+
+def test_p4_p5_p13_invariants(oracle):
+    p = qi.cfg0()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(L0, Lc, p.u[0], p.T, p.N)
+    d = 8
+    vI = vec(np.eye(d))
+    assert np.abs(vI.conj() @ Lam - vI.conj()).max() < 1e-13               # P-4 trace
+    idx = np.arange(64)
+    i, j = idx % d, idx // d
+    swap = j + d * i                                                          # (i,j) -> (j,i)
+    assert np.abs(Lam - Lam[np.ix_(swap, swap)].conj()).max() < 1e-13         # P-5 Hermiticity
+    # P-13 coherence-order blocks: m(i) = magnetisation of basis state i
+    m = np.array([sum(1 if ((s >> (2 - q)) & 1) == 0 else -1 for q in range(3)) for s in range(d)])
+    q = m[i] - m[j]
+    off = q[:, None] != q[None, :]
+    assert np.count_nonzero(Lam[off]) == 0
+    assert np.count_nonzero(L0[off]) == 0 and np.count_nonzero(Lc[:, off]) == 0
+    sizes = sorted(np.bincount(q + 6)[np.bincount(q + 6) > 0].tolist(), reverse=True)
+    assert sizes == [20, 15, 15, 6, 6, 1, 1]
+
+
+# ---------------------------------------------------------------- P-6 single-spin closed forms
+def _spin_lam(oracle, H0, Hx, C, T, N, W=0.0):
+    L0, Lc = oracle.build_liouvillian(H0, Hx[None], C)
+    return oracle.propagate(L0, Lc, np.full((N, 1), W), T, N)
+
+
+def test_p6_precession_and_decay(oracle):
+    b, t1, t2, T = 0.9, 50.0, 20.0, 7.3
+    C = np.stack([qi.SMINUS / math.sqrt(t1), qi.SZ * math.sqrt(1 / (2 * t2))])
+    Lam = _spin_lam(oracle, (b / 2) * qi.SZ, 0.5 * qi.SX, C, T, 4)
+    rho0 = np.array([[0.6, 0.3 - 0.2j], [0.3 + 0.2j, 0.4]])
+    rho = unvec(Lam @ vec(rho0), 2)
+    assert abs(rho[0, 1] - rho0[0, 1] * np.exp(-1j * b * T - T / t2 - T / (2 * t1))) < 1e-14
+    assert abs(rho[0, 0] - rho0[0, 0] * np.exp(-T / t1)) < 1e-14
+
+
+def test_p6_rabi_with_dephasing(oracle):
+    W, t2, T = 1.3, 4.0, 6.0
+    C = np.stack([qi.SZ * math.sqrt(1 / (2 * t2))])
+    Lam = _spin_lam(oracle, np.zeros((2, 2)), 0.5 * qi.SX, C, T, 16, W=W)
+    rho = unvec(Lam @ vec(np.array([[1, 0], [0, 0]], complex)), 2)
+    kap = 1 / (2 * t2)
+    mu = math.sqrt(W * W - kap * kap)
+    want = math.exp(-kap * T) * (math.cos(mu * T) + kap / mu * math.sin(mu * T))
+    assert abs((rho[0, 0] - rho[1, 1]).real - want) < 1e-13
+
+
+# ---------------------------------------------------------------- P-7 order 4 (A1, A2)
+def _smooth_case():
+    p = qi.cfg0()
+    C = qi.collapse_ops(3, t1=200.0, t2=50.0)        # stronger dissipation: exercise the dissipator
+    prm = qi.sine_params(9, 2, nterm=4)
+    prm[:, :, 1] *= 4.0                                # faster controls: visible time dependence
+    return p, C, prm
+
+
+def _ivp_reference(p, C, prm, T, rho0, oracle):
+    def rhs(t, y):
+        u = oracle.sines_eval(prm, qi.U_MAX, t)
+        H = p.H0[0] + u[0] * p.Hc[0] + u[1] * p.Hc[1]
+        return eq6_numpy(H, C, y.reshape(8, 8)).reshape(-1)
+    sol = scipy.integrate.solve_ivp(rhs, (0, T), rho0.reshape(-1).astype(complex), method="DOP853",
+                                    rtol=1e-13, atol=1e-15)
+    return sol.y[:, -1].reshape(8, 8)
+
+
+def test_p7_magnus4_order(oracle):
+    p, C, prm = _smooth_case()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, C)
+    T = 12.0
+    rho0 = rand_rho(np.random.default_rng(5), 8)
+    ref = _ivp_reference(p, C, prm, T, rho0, oracle)
+    errs = {}
+    for order in (4, 2):
+        e = []
+        for N in (8, 16, 32):
+            u = oracle.sines_nodes(prm, qi.U_MAX, N, T)
+            Lam = oracle.propagate(L0, Lc, u, T, N, mode=1, order=order)
+            e.append(np.abs(unvec(Lam @ vec(rho0), 8) - ref).max())
+        errs[order] = e
+    o4 = [math.log2(errs[4][i] / errs[4][i + 1]) for i in range(2)]
+    o2 = [math.log2(errs[2][i] / errs[2][i + 1]) for i in range(2)]
+    assert all(3.7 < o < 4.3 for o in o4), o4
+    assert all(1.7 < o < 2.3 for o in o2), o2
+
+
+def test_p7_magnus4_sign_is_detected(oracle):
+    """The flipped commutator sign must NOT give order 4 (sign detector, A2)."""
+    p, C, prm = _smooth_case()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, C)
+    T = 12.0
+    rho0 = rand_rho(np.random.default_rng(5), 8)
+    ref = _ivp_reference(p, C, prm, T, rho0, oracle)
+    e = []
+    for N in (8, 16, 32):
+        h = T / N
+        u = oracle.sines_nodes(prm, qi.U_MAX, N, T)
+        Lam = np.eye(64, dtype=complex)
+        for k in range(N):
+            A1 = L0 + u[k, 0, 0] * Lc[0] + u[k, 0, 1] * Lc[1]
+            A2 = L0 + u[k, 1, 0] * Lc[0] + u[k, 1, 1] * Lc[1]
+            Om = 0.5 * h * (A1 + A2) + math.sqrt(3) * h * h / 12 * (A1 @ A2 - A2 @ A1)
+            Lam = scipy.linalg.expm(Om) @ Lam
+        e.append(np.abs(unvec(Lam @ vec(rho0), 8) - ref).max())
+    assert math.log2(e[1] / e[2]) < 3.0
+
+
+def test_p7_pwc_matches_rk4(oracle):
+    p = qi.cfg0()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    N, T = 8, 4.0
+    u = p.u[0, :N]
+    Lam = oracle.propagate(L0, Lc, u, T, N)
+    e1 = np.abs(oracle.rk4(L0, Lc, T, N, 32, u=u) - Lam).max()
+    e2 = np.abs(oracle.rk4(L0, Lc, T, N, 64, u=u) - Lam).max()
+    assert e2 < 1e-8 and 14 < e1 / e2 < 18
+
+
+# ---------------------------------------------------------------- P-10 fidelity
+def test_p10_fidelity(oracle):
+    V = qi.haar_unitary(8, 0)
+    assert abs(oracle.fidelity(np.kron(V.conj(), V), V) - 1.0) < 1e-14
+    U = qi.haar_unitary(8, 1)
+    want = abs(np.trace(V.conj().T @ U)) ** 2 / 64
+    assert abs(oracle.fidelity(np.kron(U.conj(), U), V) - want) < 1e-15
+    # CPTP Lambda: F in [0, 1]
+    p = qi.cfg0()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    F = oracle.fidelity(oracle.propagate(L0, Lc, p.u[0, :32], 12.5, 32), V)
+    assert 0.0 <= F <= 1.0
+
+
+# ---------------------------------------------------------------- P-8 gradient vs FD
+def _fd(oracle, L0, Lc, u, T, N, V, mode, eps=1e-6, entries=None):
+    g = np.zeros(u.shape)
+    flat = list(np.ndindex(*u.shape)) if entries is None else entries
+    for ix in flat:
+        up, um = u.copy(), u.copy()
+        up[ix] += eps
+        um[ix] -= eps
+        Fp = oracle.fidelity(oracle.propagate(L0, Lc, up, T, N, mode=mode), V)
+        Fm = oracle.fidelity(oracle.propagate(L0, Lc, um, T, N, mode=mode), V)
+        g[ix] = (Fp - Fm) / (2 * eps)
+    return g
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_p8_gradient_vs_fd_d8(oracle, mode):
+    p = qi.cfg0()
+    C = qi.collapse_ops(3, t1=300.0, t2=60.0)
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, C)
+    N, T = 6, 9.0
+    rng = np.random.default_rng(21 + mode)
+    u = p.u[0, :N] if mode == 0 else rng.uniform(0, qi.U_MAX, (N, 2, 2)) * 5
+    F, g, Lam = oracle.gradient(L0, Lc, u, T, N, p.V, mode=mode)
+    assert abs(F - oracle.fidelity(oracle.propagate(L0, Lc, u, T, N, mode=mode), p.V)) < 1e-15
+    gfd = _fd(oracle, L0, Lc, u, T, N, p.V, mode)
+    assert np.linalg.norm(g - gfd) / np.linalg.norm(gfd) < 1e-6
+
+
+def test_p8_gradient_d2_and_small_T(oracle):
+    C = np.stack([qi.SMINUS / math.sqrt(30.0), qi.SZ * math.sqrt(1 / 20.0)])
+    L0, Lc = oracle.build_liouvillian(0.4 * qi.SZ, (0.5 * qi.SX)[None], C)
+    V = qi.haar_unitary(2, 3)
+    u = np.random.default_rng(2).uniform(0, 2, (5, 1))
+    F, g, _ = oracle.gradient(L0, Lc, u, 3.0, 5, V)
+    gfd = _fd(oracle, L0, Lc, u, 3.0, 5, V, 0)
+    assert np.linalg.norm(g - gfd) / np.linalg.norm(gfd) < 1e-6
+    # T -> 0: gradient -> 0 linearly in h
+    _, g1, _ = oracle.gradient(L0, Lc, u, 1e-4, 5, V)
+    _, g2, _ = oracle.gradient(L0, Lc, u, 2e-4, 5, V)
+    assert np.abs(g1).max() < 1e-4 and abs(np.linalg.norm(g2) / np.linalg.norm(g1) - 2) < 1e-3
+
+
+# ---------------------------------------------------------------- controls of configs[3] (A11)
+def test_sines_controls_clip_and_nodes(oracle):
+    prm = qi.sine_params(3, 2)
+    ts = np.linspace(0, 2000, 4001)
+    vals = np.array([oracle.sines_eval(prm, qi.U_MAX, t) for t in ts])
+    assert vals.min() >= 0.0 and vals.max() <= qi.U_MAX
+    clipped = np.mean((vals == 0.0) | (vals == qi.U_MAX))
+    assert 0.0 < clipped < 0.2
+    # node sampling = function at t_k + (1/2 -+ sqrt(3)/6) h
+    N, T = 10, 50.0
+    nodes = oracle.sines_nodes(prm, qi.U_MAX, N, T)
+    h = T / N
+    k = 7
+    assert np.allclose(nodes[k, 0], oracle.sines_eval(prm, qi.U_MAX, k * h + (0.5 - math.sqrt(3) / 6) * h))
+    assert np.allclose(nodes[k, 1], oracle.sines_eval(prm, qi.U_MAX, k * h + (0.5 + math.sqrt(3) / 6) * h))
