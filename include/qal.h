@@ -1,0 +1,198 @@
+/*
+ * qal.h -- C ABI of libqal.so, the B200 (sm_100a) hot path of the Qalibrate
+ * method (arxiv 2511.13330): time-sliced Magnus superoperator propagator of the
+ * Lindblad equation, gate fidelity and its gradient.
+ *
+ * Citation keys: "P:n" = PAPER.md line n (section / equation named beside it);
+ * "A#" = a reading listed in DESIGN.md "Readings of the paper".
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Matrices are ROW-MAJOR; complex numbers are interleaved {re, im} doubles
+ *    (== torch.complex128 == cuDoubleComplex).  vec(rho) is column stacking,
+ *    vec(rho)[i + d*j] = rho[i][j] (A5; the convention under which Eq. 8, P:107,
+ *    holds).
+ *  - Every array pointer is a DEVICE pointer owned by the caller.  The library
+ *    never allocates, frees or retains device memory in these calls (except
+ *    the per-process function attribute setup done once per device).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All work is enqueued on it; no call synchronises the host.
+ *  - Arguments are validated synchronously BEFORE any launch; a call that
+ *    returns an error code has enqueued nothing and written nothing.
+ *  - Numeric failures that can only be seen on the device (a non-finite slice
+ *    generator) are reported per pulse in the optional `status` array
+ *    (device int[batch]; 0 = ok, QAL_ERR_NONFINITE otherwise).  `status` is
+ *    overwritten, not accumulated.
+ *  - Determinism: identical inputs and shapes give bit-identical outputs; no
+ *    reduction uses atomics and every tree has a fixed shape keyed to the
+ *    slice count and chunk size only (A16).
+ *  - Supported sizes: d = 8 (superoperator n = d*d = 64, the three-spin
+ *    exchange-only qubit of P:59).  Other d return QAL_ERR_UNSUPPORTED.
+ *    Controls: 1 <= n_ctrl <= QAL_MAX_CTRL.
+ */
+#ifndef QAL_H
+#define QAL_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } qal_c128;
+
+enum {
+    QAL_OK = 0,
+    QAL_ERR_NULL = -1,        /* a required pointer is NULL                          */
+    QAL_ERR_DIM = -2,         /* inconsistent sizes (chunk does not divide count ...) */
+    QAL_ERR_EMPTY = -3,       /* batch, slice count or product length is zero        */
+    QAL_ERR_NONFINITE = -4,   /* non-finite scalar argument, or device status flag   */
+    QAL_ERR_UNSUPPORTED = -5, /* d / n / n_ctrl / mode outside what is implemented   */
+    QAL_ERR_WORKSPACE = -6,   /* ws NULL or ws_bytes < qal_workspace_bytes(...)       */
+    QAL_ERR_CUDA = -7         /* a CUDA launch failed (cudaGetLastError)              */
+};
+
+enum {
+    QAL_CTRL_PWC = 0,   /* u[batch][count][J]: value held on the whole slice        */
+    QAL_CTRL_NODES = 1  /* u[batch][count][2][J]: values at the two Gauss-Legendre nodes   */
+                        /* tau_{k,1,2} = t_k + (1/2 -+ sqrt(3)/6) h of slice k (A1, A2)     */
+};
+
+enum {                   /* op codes for qal_workspace_bytes */
+    QAL_OP_ORDERED_PRODUCT = 1,
+    QAL_OP_FIDELITY = 2,      /* qal_fidelity_grad with grad == NULL */
+    QAL_OP_FIDELITY_GRAD = 3  /* qal_fidelity_grad with grad != NULL */
+};
+
+#define QAL_MAX_CTRL 8
+#define QAL_ABI_VERSION 1
+
+int qal_abi_version(void);
+const char *qal_status_string(int code);
+
+/*
+ * Eq. 8 from Eq. 6: the Liouvillian superoperator is linear
+ * in H, so L(t) = L0 + sum_j u_j(t) L_j with
+ *   L0 = -i (I (x) H0 - H0^T (x) I) + sum_c [ conj(c) (x) c - 1/2 I (x) c^dag c
+ *                                              - 1/2 (c^dag c)^T (x) I ]
+ *   L_j = -i (I (x) H_j - H_j^T (x) I)
+ * where the collapse operators c carry sqrt(rate) (A6: sigma-_i / sqrt(T1),
+ * sigma_z_i sqrt(1/(2 T2))).
+ *   d        Hilbert dimension (8).  n = d*d.
+ *   batch    number of drift Hamiltonians H0 (per-pulse Zeeman offsets), >= 1.
+ *   H0       [batch][d][d]   Hc [n_ctrl][d][d]   C [n_cops][d][d] (n_cops >= 0; C may be
+ *            NULL iff n_cops == 0).
+ *   want_comm  if nonzero also write the bilinear commutator basis of the
+ *            4th-order Magnus generator (A2):
+ *            Lcomm[b][j]            = [L0_b, L_j]          j = 0..J-1
+ *            Lcomm[b][J + p(a,c)]   = [L_a, L_c]           a < c, lexicographic pairs
+ *            i.e. n_comm = J + J(J-1)/2 matrices per batch entry.
+ *   Outputs L0 [batch][n][n], Lc [n_ctrl][n][n], Lcomm [batch][n_comm][n][n] (or NULL
+ *   when want_comm == 0).
+ */
+int qal_build_liouvillian(int d, int batch, const qal_c128 *H0, int n_ctrl, const qal_c128 *Hc,
+                          int n_cops, const qal_c128 *C, int want_comm, qal_c128 *L0, qal_c128 *Lc,
+                          qal_c128 *Lcomm, void *stream);
+
+/*
+ * Eqs. 13-15, generalised to the 4th-order Magnus method (A1, A2):
+ * for every slice k of the uniform grid t_k = k h, h = T / n_slices,
+ *   A_a   = L0 + sum_j u_j(tau_{k,a}) L_j                                   (a = 1, 2)
+ *   Omega = (h/2)(A_1 + A_2) - (sqrt(3) h^2 / 12) [A_1, A_2]               (order 4)
+ *   Omega = (h/2)(A_1 + A_2)                                               (order 2)
+ *   U_k   = expm(Omega)     (Eq. 14; scaling and squaring around a Taylor
+ *                            polynomial whose truncation bound is <= 2^-53, A15)
+ * and the left fold of every `chunk` consecutive slices (Eq. 15, later slice on
+ * the LEFT, A4): chunk_prod[b][c] = U_{k0+(c+1)chunk-1} ... U_{k0+c chunk}.
+ *   n            64.
+ *   n_slices, T  define the grid (h = T / n_slices).  The call processes the
+ *                `count` slices k0 .. k0+count-1 (0 <= k0, k0+count <= n_slices);
+ *                u points at the row of slice k0.
+ *   magnus_order 2 or 4.  ctrl_mode QAL_CTRL_PWC or QAL_CTRL_NODES.
+ *   u            PWC: [batch][count][J]; NODES: [batch][count][2][J] (f64).
+ *   L0           [batch or 1][n][n]; L0_batch_stride = n*n or 0 (shared).
+ *   Lc           [J][n][n].
+ *   Lcomm        as written by qal_build_liouvillian; required iff
+ *                (ctrl_mode == NODES && magnus_order == 4), else ignored;
+ *                Lcomm_batch_stride = n_comm*n*n or 0.
+ *   U_out        optional [batch][count][n][n]: every U_k.
+ *   chunk        >= 1, must divide count.  chunk_prod optional
+ *                [batch][count/chunk][n][n].  At least one of U_out / chunk_prod.
+ *   status       optional device int[batch].
+ *   ws, ws_bytes unused (pass NULL, 0); reserved.
+ */
+int qal_magnus_expm_slices(int n, int batch, int n_slices, double T, int k0, int count,
+                           int magnus_order, int ctrl_mode, int n_ctrl, const double *u,
+                           const qal_c128 *L0, long long L0_batch_stride, const qal_c128 *Lc,
+                           const qal_c128 *Lcomm, long long Lcomm_batch_stride, qal_c128 *U_out,
+                           int chunk, qal_c128 *chunk_prod, int *status, void *ws, size_t ws_bytes,
+                           void *stream);
+
+/*
+ * Eq. 15 with the tree reduction of P:141: out[b] = U[b][count-1] ... U[b][0]
+ * (later factor on the LEFT, A4), evaluated as a balanced binary tree whose shape
+ * depends on `count` only (pairs (2i, 2i+1) -> U[2i+1] U[2i] per level; an odd
+ * last element is carried up unchanged).
+ *   U    [batch][count][n][n], time order.  out [batch][n][n].  count >= 1.
+ *   ws   >= qal_workspace_bytes(QAL_OP_ORDERED_PRODUCT, n, batch, count, 0, 0) bytes of
+ *        device memory (may be NULL when that is 0, i.e. count <= 2).
+ */
+int qal_ordered_product(int n, int batch, int count, const qal_c128 *U, qal_c128 *out, void *ws,
+                        size_t ws_bytes, void *stream);
+
+/*
+ * Gate (process) fidelity to a target unitary V (A8, replaces Eqs. 16-17 on
+ * this path):
+ *   F[b] = Re Tr(S_V^dag Lambda[b]) / d^2,  S_V = conj(V) (x) V
+ * (the superoperator of rho -> V rho V^dag under column stacking).  S_V is never
+ * formed: S_V[i+dj, k+dl] = conj(V[j][l]) V[i][k].  Fixed-order reduction.
+ *   Lambda [batch][n][n], V [d][d], F [batch] (f64).
+ */
+int qal_fidelity(int d, int batch, const qal_c128 *Lambda, const qal_c128 *V, double *F,
+                 void *stream);
+
+/*
+ * The whole hot path for a batch of pulses: propagator (as above, full grid,
+ * k0 = 0, count = n_slices), fidelity and, if grad != NULL, the gradient of F
+ * with respect to every control value (A14; P:185 motivates the adjoint form):
+ *   dF/du_{k,j} = Re Tr(G_k dU_k/du_{k,j}) / d^2,
+ *   G_k = P_k S_V^dag U_{N-1} ... U_{k+1},  P_k = U_{k-1} ... U_0,
+ * evaluated with ONE adjoint Frechet derivative per slice,
+ *   W_k = L_exp(Omega_k, G_k)    (so that Re Tr(G_k L(Omega_k, E)) = Re Tr(W_k E)),
+ * and dF/du_{k,j} = Re Tr(W_k dOmega_k/du_{k,j}) / d^2.  grad has the layout of u.
+ *   F       [batch] out.  grad [batch][...] out or NULL.  Lambda optional out
+ *           [batch][n][n].
+ *   ws      >= qal_workspace_bytes(grad ? QAL_OP_FIDELITY_GRAD : QAL_OP_FIDELITY, n, batch,
+ *           n_slices, n_ctrl, ctrl_mode) bytes.
+ * Other arguments as for qal_magnus_expm_slices.
+ */
+int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order, int ctrl_mode,
+                      int n_ctrl, const double *u, const qal_c128 *L0, long long L0_batch_stride,
+                      const qal_c128 *Lc, const qal_c128 *Lcomm, long long Lcomm_batch_stride,
+                      const qal_c128 *V, double *F, double *grad, qal_c128 *Lambda, int *status,
+                      void *ws, size_t ws_bytes, void *stream);
+
+/* Device workspace (bytes) an op needs; 0 when none.  `flags` = ctrl_mode for the
+ * fidelity ops, 0 otherwise. */
+size_t qal_workspace_bytes(int op, int n, int batch, int n_slices, int n_ctrl, int flags);
+
+/* Chunk size qal_fidelity_grad uses for the forward fold of a fidelity-only call
+ * (a function of n_slices and batch only; exported so callers can reproduce it). */
+int qal_default_chunk(int batch, int n_slices);
+
+/*
+ * FP64 roofline probe (bench only): kind 0 = DMMA.8x8x4 loop, kind 1 = DFMA
+ * loop; `blocks` CTAs of 256 threads, `iters` inner iterations.  Returns the FP64
+ * flop count one launch performs in *flops (host pointer).  `sink` is a device
+ * double that is written only to defeat dead-code elimination.
+ */
+int qal_fp64_peak_probe(int kind, int blocks, int iters, double *flops, double *sink, void *stream);
+
+/* Number of kernels the last call on this host thread enqueued (launch accounting
+ * for bench.py's gpu_launches); reset by every qal_* call that launches. */
+int qal_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QAL_H */

@@ -1,0 +1,282 @@
+// qal_api.cu -- the C ABI of libqal.so (include/qal.h): synchronous argument
+// validation, then kernel launches on the caller's stream.  No allocation.
+#include <cmath>
+#include <cstdint>
+
+#include "../../include/qal.h"
+#include "qal_dev.cuh"
+#include "qal_internal.h"
+
+namespace qal {
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cached[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 1;
+  }
+  return cached[dev];
+}
+
+int& launch_counter() {
+  static thread_local int c = 0;
+  return c;
+}
+
+}  // namespace qal
+
+using namespace qal;
+
+namespace {
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? QAL_OK : QAL_ERR_CUDA; }
+inline const double2* D2(const qal_c128* p) { return reinterpret_cast<const double2*>(p); }
+inline double2* D2(qal_c128* p) { return reinterpret_cast<double2*>(p); }
+inline int ncomm_of(int J) { return J + J * (J - 1) / 2; }
+
+size_t tree_ws_bytes(int batch, int count) {
+  if (count <= 2) return 0;
+  const size_t c1 = (size_t)(count + 1) / 2, c2 = (c1 + 1) / 2;
+  return (size_t)batch * (c1 + c2) * MAT_BYTES;
+}
+
+// Balanced tree over `count` natural matrices per pulse -> out.
+int run_tree(int batch, int count, const double2* U, double2* out, void* ws, cudaStream_t st) {
+  if (count == 1) return cuda_rc(cudaMemcpyAsync(out, U, (size_t)batch * MAT_BYTES, cudaMemcpyDeviceToDevice, st));
+  const size_t c1 = (size_t)(count + 1) / 2;
+  double2* bufA = reinterpret_cast<double2*>(ws);
+  double2* bufB = bufA ? bufA + (size_t)batch * c1 * PLANE_C : nullptr;
+  const double2* in = U;
+  int cnt = count;
+  int lvl = 0;
+  while (cnt > 1) {
+    const int half = (cnt + 1) / 2;
+    double2* dst = (half == 1) ? out : ((lvl & 1) ? bufB : bufA);
+    cudaError_t e = launch_tree_level(batch, cnt, in, dst, st);
+    if (e != cudaSuccess) return QAL_ERR_CUDA;
+    in = dst;
+    cnt = half;
+    ++lvl;
+  }
+  return QAL_OK;
+}
+
+bool finite(double x) { return std::isfinite(x); }
+
+struct Common {
+  Basis B;
+  SliceGrid G;
+};
+
+int check_basis(int n_or_d_ok, int batch, int n_slices, double T, int order, int mode, int J, const double* u,
+                const qal_c128* L0, long long L0s, const qal_c128* Lc, const qal_c128* Lcomm, long long Lcs,
+                Common& c) {
+  if (!n_or_d_ok) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1 || n_slices < 1) return QAL_ERR_EMPTY;
+  if (!finite(T) || T <= 0.0) return QAL_ERR_NONFINITE;
+  if (order != 2 && order != 4) return QAL_ERR_UNSUPPORTED;
+  if (mode != QAL_CTRL_PWC && mode != QAL_CTRL_NODES) return QAL_ERR_UNSUPPORTED;
+  if (J < 1 || J > QAL_MAX_CTRL) return QAL_ERR_UNSUPPORTED;
+  if (!u || !L0 || !Lc) return QAL_ERR_NULL;
+  if (L0s != 0 && L0s != (long long)PLANE_C) return QAL_ERR_DIM;
+  const bool comm = (mode == QAL_CTRL_NODES && order == 4);
+  if (comm && !Lcomm) return QAL_ERR_NULL;
+  if (comm && Lcs != 0 && Lcs != (long long)ncomm_of(J) * PLANE_C) return QAL_ERR_DIM;
+  const double h = T / n_slices;
+  c.B.L0 = D2(L0);
+  c.B.L0_stride = L0s;
+  c.B.Lc = D2(Lc);
+  c.B.Lcomm = comm ? D2(Lcomm) : nullptr;
+  c.B.Lcomm_stride = comm ? Lcs : 0;
+  c.B.J = J;
+  c.B.ncomm = comm ? ncomm_of(J) : 0;
+  c.G.h = h;
+  c.G.c4 = (order == 4) ? std::sqrt(3.0) * h * h / 12.0 : 0.0;
+  c.G.mode = mode;
+  c.G.u = u;
+  c.G.count = n_slices;
+  return QAL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qal_abi_version(void) { return QAL_ABI_VERSION; }
+
+const char* qal_status_string(int code) {
+  switch (code) {
+    case QAL_OK: return "ok";
+    case QAL_ERR_NULL: return "required pointer is NULL";
+    case QAL_ERR_DIM: return "inconsistent dimensions";
+    case QAL_ERR_EMPTY: return "empty input";
+    case QAL_ERR_NONFINITE: return "non-finite value";
+    case QAL_ERR_UNSUPPORTED: return "unsupported size or mode";
+    case QAL_ERR_WORKSPACE: return "workspace too small";
+    case QAL_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+int qal_last_launch_count(void) { return launch_counter(); }
+
+int qal_default_chunk(int batch, int n_slices) {
+  if (batch < 1 || n_slices < 1) return 1;
+  int c = 1;
+  while (c * 2 <= 64 && n_slices % (c * 2) == 0) c *= 2;
+  const long long want = 4LL * num_sms();
+  while (c > 1 && (long long)batch * (n_slices / c) < want) c /= 2;
+  return c;
+}
+
+size_t qal_workspace_bytes(int op, int n, int batch, int n_slices, int n_ctrl, int flags) {
+  (void)n_ctrl;
+  (void)flags;
+  if (n != 64 || batch < 1 || n_slices < 1) return 0;
+  switch (op) {
+    case QAL_OP_ORDERED_PRODUCT: return tree_ws_bytes(batch, n_slices);
+    case QAL_OP_FIDELITY: {
+      const int ch = qal_default_chunk(batch, n_slices);
+      const int nch = n_slices / ch;
+      return (size_t)batch * nch * MAT_BYTES + tree_ws_bytes(batch, nch) + (size_t)batch * MAT_BYTES;
+    }
+    case QAL_OP_FIDELITY_GRAD:
+      return 3 * (size_t)batch * n_slices * MAT_BYTES + (size_t)batch * MAT_BYTES + grad_scratch_bytes();
+    default: return 0;
+  }
+}
+
+int qal_build_liouvillian(int d, int batch, const qal_c128* H0, int n_ctrl, const qal_c128* Hc, int n_cops,
+                          const qal_c128* C, int want_comm, qal_c128* L0, qal_c128* Lc, qal_c128* Lcomm,
+                          void* stream) {
+  launch_counter() = 0;
+  if (d != 8) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1) return QAL_ERR_EMPTY;
+  if (n_ctrl < 0 || n_ctrl > QAL_MAX_CTRL || n_cops < 0) return QAL_ERR_DIM;
+  if (!H0 || !L0) return QAL_ERR_NULL;
+  if (n_ctrl > 0 && (!Hc || !Lc)) return QAL_ERR_NULL;
+  if (n_cops > 0 && !C) return QAL_ERR_NULL;
+  if (want_comm && (n_ctrl < 1 || !Lcomm)) return n_ctrl < 1 ? QAL_ERR_DIM : QAL_ERR_NULL;
+  cudaError_t e = launch_liouvillian(batch, D2(H0), n_ctrl, D2(Hc), n_cops, D2(C), D2(L0), D2(Lc), S(stream));
+  if (e != cudaSuccess) return QAL_ERR_CUDA;
+  if (want_comm) e = launch_commutators(batch, n_ctrl, D2(L0), D2(Lc), D2(Lcomm), S(stream));
+  return cuda_rc(e);
+}
+
+int qal_magnus_expm_slices(int n, int batch, int n_slices, double T, int k0, int count, int magnus_order,
+                           int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0,
+                           long long L0_batch_stride, const qal_c128* Lc, const qal_c128* Lcomm,
+                           long long Lcomm_batch_stride, qal_c128* U_out, int chunk, qal_c128* chunk_prod,
+                           int* status, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  launch_counter() = 0;
+  Common c;
+  int rc = check_basis(n == 64, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0, L0_batch_stride, Lc,
+                       Lcomm, Lcomm_batch_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!U_out && !chunk_prod) return QAL_ERR_NULL;
+  if (chunk < 1 || count % chunk != 0) return QAL_ERR_DIM;
+  c.G.count = count;
+  FwdOut O;
+  O.U_nat = D2(U_out);
+  O.U_img = nullptr;
+  O.chunk_nat = D2(chunk_prod);
+  O.chunk = chunk_prod ? chunk : 1;
+  O.status = status;
+  if (!chunk_prod && count % O.chunk) return QAL_ERR_DIM;
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, S(stream)) != cudaSuccess) return QAL_ERR_CUDA;
+  return cuda_rc(launch_expm_fold(batch, c.B, c.G, O, S(stream)));
+}
+
+int qal_ordered_product(int n, int batch, int count, const qal_c128* U, qal_c128* out, void* ws, size_t ws_bytes,
+                        void* stream) {
+  launch_counter() = 0;
+  if (n != 64) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1 || count < 1) return QAL_ERR_EMPTY;
+  if (!U || !out) return QAL_ERR_NULL;
+  const size_t need = tree_ws_bytes(batch, count);
+  if (need > 0 && (!ws || ws_bytes < need)) return QAL_ERR_WORKSPACE;
+  return run_tree(batch, count, D2(U), D2(out), ws, S(stream));
+}
+
+int qal_fidelity(int d, int batch, const qal_c128* Lambda, const qal_c128* V, double* F, void* stream) {
+  launch_counter() = 0;
+  if (d != 8) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1) return QAL_ERR_EMPTY;
+  if (!Lambda || !V || !F) return QAL_ERR_NULL;
+  return cuda_rc(launch_fidelity(batch, D2(Lambda), D2(V), F, S(stream)));
+}
+
+int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order, int ctrl_mode, int n_ctrl,
+                      const double* u, const qal_c128* L0, long long L0_batch_stride, const qal_c128* Lc,
+                      const qal_c128* Lcomm, long long Lcomm_batch_stride, const qal_c128* V, double* F,
+                      double* grad, qal_c128* Lambda, int* status, void* ws, size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  Common c;
+  int rc = check_basis(d == 8, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0, L0_batch_stride, Lc,
+                       Lcomm, Lcomm_batch_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (!V || !F) return QAL_ERR_NULL;
+  const size_t need = qal_workspace_bytes(grad ? QAL_OP_FIDELITY_GRAD : QAL_OP_FIDELITY, 64, batch, n_slices,
+                                          n_ctrl, ctrl_mode);
+  if (!ws || ws_bytes < need) return QAL_ERR_WORKSPACE;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+  char* w = reinterpret_cast<char*>(ws);
+  if (!grad) {
+    const int ch = qal_default_chunk(batch, n_slices);
+    const int nch = n_slices / ch;
+    double2* parts = reinterpret_cast<double2*>(w);
+    w += (size_t)batch * nch * MAT_BYTES;
+    double2* lam_tmp = reinterpret_cast<double2*>(w);
+    w += (size_t)batch * MAT_BYTES;
+    double2* lam = Lambda ? D2(Lambda) : lam_tmp;
+    FwdOut O{nullptr, nullptr, parts, ch, status};
+    if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+    int l = launch_counter();
+    rc = run_tree(batch, nch, parts, lam, w, st);
+    l += launch_counter();
+    if (rc != QAL_OK) return rc;
+    rc = cuda_rc(launch_fidelity(batch, lam, D2(V), F, st));
+    launch_counter() += l;
+    return rc;
+  }
+  // gradient path: U_k images (parallel over slices) -> prefix chain P_k -> fidelity ->
+  // suffix chain X_{k+1} -> one adjoint Frechet derivative per slice
+  const size_t seq = (size_t)batch * n_slices * IMG;
+  double* U_img = reinterpret_cast<double*>(w);
+  double* P_img = U_img + seq;
+  double* X_img = P_img + seq;
+  double2* lam_tmp = reinterpret_cast<double2*>(X_img + seq);
+  double* scratch = reinterpret_cast<double*>(lam_tmp + (size_t)batch * PLANE_C);
+  double2* lam = Lambda ? D2(Lambda) : lam_tmp;
+  int total = 0;
+  FwdOut O{nullptr, U_img, nullptr, 1, status};
+  if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+  total += launch_counter();
+  if (launch_prefix_chain(batch, n_slices, U_img, P_img, lam, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_fidelity(batch, lam, D2(V), F, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_suffix_chain(batch, n_slices, U_img, D2(V), X_img, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_grad_slices(batch, c.B, c.G, P_img, X_img, grad, status, scratch, st) != cudaSuccess)
+    return QAL_ERR_CUDA;
+  return QAL_OK;
+}
+
+int qal_fp64_peak_probe(int kind, int blocks, int iters, double* flops, double* sink, void* stream) {
+  launch_counter() = 0;
+  if (kind != 0 && kind != 1) return QAL_ERR_UNSUPPORTED;
+  if (blocks < 1 || iters < 1) return QAL_ERR_EMPTY;
+  if (!flops || !sink) return QAL_ERR_NULL;
+  *flops = (kind == 0) ? (double)blocks * 8.0 * iters * 8.0 * 512.0 : (double)blocks * 256.0 * iters * 8.0 * 2.0;
+  return cuda_rc(launch_fp64_probe(kind, blocks, iters, sink, S(stream)));
+}
+
+}  // extern "C"

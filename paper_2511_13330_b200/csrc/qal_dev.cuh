@@ -1,0 +1,352 @@
+// qal_dev.cuh -- device building blocks of libqal.so (sm_100a only).
+//
+// One CTA of 8 warps owns one 64x64 complex128 matrix product at a time:
+//   * warp w owns the 8-row STRIP r = 8w..8w+7 of every operand and result;
+//     lane (g = lane/4, t = lane%4) holds the 16 complex entries
+//         strip[i] = M[8w + g][4i + t],   i = 0..15.
+//   * C = A B is evaluated with FP64 tensor-core MMAs (mma.sync m8n8k4 f64 ->
+//     SASS DMMA.8x8x4), 4 real MMAs per complex 8x8x4 step (planar re/im).
+//     A comes from registers (the strip layout IS the m8n8k4 A-fragment layout
+//     for k-step i), B from a shared-memory IMAGE of the whole matrix.
+//   * The image stores the columns of every 8-column tile permuted,
+//         phys(c) = (c & ~7) | ((c & 3) << 1) | ((c >> 2) & 1),
+//     so that the accumulator of a product comes out in the strip layout: a
+//     result feeds the next product as its A operand with no shuffles.  Rows
+//     alternate an XOR-8 swizzle of the physical column, which makes the
+//     B-fragment loads (LDS.64) and strip loads/stores (LDS/STS.128) free of
+//     bank conflicts without padding (image = 2 x 32 KB, re plane then im plane).
+//   * Strips that only their owner thread needs again (powers X^2, X^3 in the
+//     Taylor evaluation) are parked in Tensor Memory with tcgen05.st / tcgen05.ld:
+//     TMEM is 256 KB/SM of otherwise idle on-chip storage on this FP64 path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qal {
+
+constexpr int NT = 256;           // threads per CTA (8 warps)
+constexpr int PLANE = 64 * 64;    // doubles per re / im plane
+constexpr int IMG = 2 * PLANE;    // doubles per matrix image (64 KB)
+
+struct Lane {
+  int w, g, t, r, lane;
+};
+
+__device__ __forceinline__ Lane lane_id() {
+  Lane L;
+  L.lane = threadIdx.x & 31;
+  L.w = threadIdx.x >> 5;
+  L.g = L.lane >> 2;
+  L.t = L.lane & 3;
+  L.r = 8 * L.w + L.g;
+  return L;
+}
+
+struct Strip {
+  double re[16], im[16];
+};
+
+// Compiler-only fence: keeps the operand loads of the NEXT product from being hoisted
+// into the current DMMA loop (they would need another 64 live registers).
+#define QAL_FENCE() asm volatile("" ::: "memory")
+
+// ---------------------------------------------------------------- layout
+__device__ __forceinline__ int phys_col(int r, int c) {
+  return ((c & ~7) | ((c & 3) << 1) | ((c >> 2) & 1)) ^ ((r & 1) << 3);
+}
+__device__ __forceinline__ int img_off(int r, int c) { return r * 64 + phys_col(r, c); }
+
+// offset of the (even) strip pair (2j, 2j+1) of lane L in an image plane
+__device__ __forceinline__ int pair_off(const Lane& L, int j) {
+  return L.r * 64 + ((8 * j + 2 * L.t) ^ ((L.g & 1) << 3));
+}
+
+__device__ __forceinline__ void zero(Strip& s) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { s.re[i] = 0.0; s.im[i] = 0.0; }
+}
+
+__device__ __forceinline__ void copy(Strip& d, const Strip& s) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { d.re[i] = s.re[i]; d.im[i] = s.im[i]; }
+}
+
+// strip <-> image (shared or global; generic pointers, 16-byte accesses)
+__device__ __forceinline__ void load_img(Strip& s, const double* __restrict__ img, const Lane& L) {
+  QAL_FENCE();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int o = pair_off(L, j);
+    double2 a = *reinterpret_cast<const double2*>(img + o);
+    double2 b = *reinterpret_cast<const double2*>(img + PLANE + o);
+    s.re[2 * j] = a.x; s.re[2 * j + 1] = a.y;
+    s.im[2 * j] = b.x; s.im[2 * j + 1] = b.y;
+  }
+}
+__device__ __forceinline__ void store_img(double* __restrict__ img, const Strip& s, const Lane& L) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int o = pair_off(L, j);
+    *reinterpret_cast<double2*>(img + o) = make_double2(s.re[2 * j], s.re[2 * j + 1]);
+    *reinterpret_cast<double2*>(img + PLANE + o) = make_double2(s.im[2 * j], s.im[2 * j + 1]);
+  }
+}
+
+// strip <-> natural row-major complex128 matrix in global memory
+__device__ __forceinline__ void load_nat(Strip& s, const double2* __restrict__ M, const Lane& L) {
+  QAL_FENCE();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    double2 v = __ldg(M + L.r * 64 + 4 * i + L.t);
+    s.re[i] = v.x; s.im[i] = v.y;
+  }
+}
+__device__ __forceinline__ void store_nat(double2* __restrict__ M, const Strip& s, const Lane& L) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) M[L.r * 64 + 4 * i + L.t] = make_double2(s.re[i], s.im[i]);
+}
+
+// whole natural matrix -> shared image (cooperative, all 256 threads)
+__device__ __forceinline__ void block_nat_to_img(double* __restrict__ img, const double2* __restrict__ M) {
+#pragma unroll 4
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const int r = e >> 6, c = e & 63;
+    double2 v = __ldg(M + e);
+    const int o = img_off(r, c);
+    img[o] = v.x;
+    img[PLANE + o] = v.y;
+  }
+}
+// whole image (global) -> shared image (cooperative 16-byte copy)
+__device__ __forceinline__ void block_img_copy(double* __restrict__ dst, const double* __restrict__ src) {
+  const double2* s = reinterpret_cast<const double2*>(src);
+  double2* d = reinterpret_cast<double2*>(dst);
+#pragma unroll 4
+  for (int e = threadIdx.x; e < IMG / 2; e += NT) d[e] = s[e];
+}
+
+__device__ __forceinline__ bool is_diag(const Lane& L, int i) { return L.r == 4 * i + L.t; }
+
+// ---------------------------------------------------------------- FP64 tensor core
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// acc += A * B, A = strip (registers, A-fragment layout), B = shared image.
+__device__ __forceinline__ void mma_acc(Strip& acc, const Strip& a, const double* __restrict__ Bs,
+                                        const Lane& L) {
+  const int todd = L.t & 1;
+  // row 4q+t of B; physical tile of output tile j is j ^ (t & 1)
+  const double* bE = Bs + L.t * 64 + L.g + 8 * todd;  // even j: tile j + todd
+  const double* bO = Bs + L.t * 64 + L.g - 8 * todd;  // odd  j: tile j - todd
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const double ar = a.re[q], ai = a.im[q], nai = -a.im[q];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double* p = ((j & 1) ? bO : bE) + q * 256 + 8 * j;
+      const double br = p[0], bi = p[PLANE];
+      dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br);
+      dmma(acc.re[2 * j], acc.re[2 * j + 1], nai, bi);
+      dmma(acc.im[2 * j], acc.im[2 * j + 1], ar, bi);
+      dmma(acc.im[2 * j], acc.im[2 * j + 1], ai, br);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Tensor Memory scratch
+// 512 columns x 128 lanes x 32 bit.  Warp w reaches lanes 32(w%4)..+31; warps w and
+// w+4 use different column halves.  Slot s (0..3) of a warp: 64 columns (re 32, im 32).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void tmem_alloc512(uint32_t* slot_smem) {
+  // whole warp 0 executes
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot_smem)));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base));
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t tmem_slot_addr(uint32_t base, const Lane& L, int slot) {
+  return base + (static_cast<uint32_t>(32 * (L.w & 3)) << 16) + static_cast<uint32_t>(slot * 128 + (L.w >> 2) * 64);
+}
+
+#define QAL_R32(v)                                                                                   \
+  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), \
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),  \
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), \
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+#define QAL_W32(v)                                                                                       \
+  "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),         \
+      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), \
+      "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),           \
+      "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),           \
+      "=r"(v[30]), "=r"(v[31])
+
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      QAL_R32(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : QAL_W32(v)
+      : "r"(addr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_store_half(uint32_t addr, const double (&x)[16]) {
+  uint32_t v[32];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[2 * i] = static_cast<uint32_t>(__double2loint(x[i]));
+    v[2 * i + 1] = static_cast<uint32_t>(__double2hiint(x[i]));
+  }
+  tmem_st32(addr, v);
+}
+__device__ __forceinline__ void tmem_load_half(uint32_t addr, double (&x)[16]) {
+  QAL_FENCE();
+  uint32_t v[32];
+  tmem_ld32(addr, v);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i]));
+}
+__device__ __forceinline__ void tmem_store(uint32_t addr, const Strip& s) {
+  tmem_store_half(addr, s.re);
+  tmem_store_half(addr + 32, s.im);
+  tmem_wait_st();
+}
+
+// acc += a * M  where M is a strip parked in TMEM (loaded in halves to bound registers)
+__device__ __forceinline__ void tmem_axpy(Strip& acc, double a, uint32_t addr) {
+  double x[16];
+  tmem_load_half(addr, x);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc.re[i] = fma(a, x[i], acc.re[i]);
+  tmem_load_half(addr + 32, x);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc.im[i] = fma(a, x[i], acc.im[i]);
+}
+
+// ---------------------------------------------------------------- TMA bulk copies
+// 1-D bulk tensor copies (cp.async.bulk, the TMA engine) global -> shared, completion
+// tracked by an mbarrier transaction count.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// one thread: copy a 64 KB matrix image global -> shared, arriving on `bar`
+__device__ __forceinline__ void tma_load_img(double* dst, const double* src, uint64_t* bar) {
+  mbar_expect_tx(bar, IMG * 8);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) bulk_g2s(dst + p * (IMG / 4), src + p * (IMG / 4), IMG * 2, bar);
+}
+
+// ---------------------------------------------------------------- reductions
+// max over columns of sum_r |M[r][c]| (the induced 1-norm) of the CTA's matrix given
+// by its strips.  Fixed order; two __syncthreads.  red: >= 8*64 + 8 doubles of smem.
+__device__ __forceinline__ double norm1(const Strip& s, double* red, const Lane& L) {
+  double cs[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) cs[i] = hypot(s.re[i], s.im[i]);
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], off);
+  if (L.g == 0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) red[L.w * 64 + 4 * i + L.t] = cs[i];
+  }
+  __syncthreads();
+  if (L.w == 0) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { a += red[w * 64 + L.lane]; b += red[w * 64 + 32 + L.lane]; }
+    double m = fmax(a, b);
+    if (!(a == a) || !(b == b)) m = __longlong_as_double(0x7ff8000000000000LL);  // keep NaN
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      double o = __shfl_xor_sync(0xffffffffu, m, off);
+      m = (o != o || o > m) ? o : m;
+    }
+    if (L.lane == 0) red[512] = m;
+  }
+  __syncthreads();
+  return red[512];
+}
+
+// sum over the CTA of one double per thread, fixed order (warp tree, then warps in
+// order).  red: >= 8 doubles of smem + 1; two __syncthreads.
+__device__ __forceinline__ double block_sum(double v, double* red, const Lane& L) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if (L.lane == 0) red[L.w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w];
+    red[8] = s;
+  }
+  __syncthreads();
+  return red[8];
+}
+
+// ---------------------------------------------------------------- expm helpers
+// Taylor degree / scaling choice (A15): the truncation bound
+//   sum_{k>m} theta^k / k! <= 2^-53 e^-theta
+// holds for ||X||_1 <= theta_m (thresholds computed offline).
+constexpr double THETA8 = 0.0693960458639;
+constexpr double THETA12 = 0.3269045734215;
+constexpr double THETA16 = 0.7873811561929;
+
+__device__ __forceinline__ void choose_ms(double nrm, int& m, int& s) {
+  s = 0;
+  if (!(nrm <= 1e300)) { m = 16; s = 0; return; }  // non-finite: flagged by caller
+  if (nrm <= THETA8) { m = 8; return; }
+  if (nrm <= THETA12) { m = 12; return; }
+  m = 16;
+  while (nrm > THETA16 && s < 1000) { nrm *= 0.5; ++s; }
+}
+
+// Taylor coefficients 1/i!, correctly rounded (Fraction(1, i!) -> double)
+__constant__ double c_inv_fact[19] = {1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664,
+                                      0.008333333333333333, 0.001388888888888889, 0.0001984126984126984,
+                                      2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07,
+                                      2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10,
+                                      1.1470745597729725e-11, 7.647163731819816e-13, 4.779477332387385e-14,
+                                      2.8114572543455206e-15, 1.5619206968586225e-16};
+__device__ __forceinline__ double inv_fact(int i) { return c_inv_fact[i]; }
+
+}  // namespace qal

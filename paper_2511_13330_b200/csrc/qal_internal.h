@@ -1,0 +1,62 @@
+// qal_internal.h -- launcher interface between qal_api.cu and the kernel TUs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace qal {
+
+constexpr int MAXJ = 8;
+constexpr size_t MAT_BYTES = 64 * 64 * 16;   // one 64x64 complex128 matrix / image
+constexpr size_t PLANE_C = 64 * 64;          // complex elements per matrix
+
+// Generator basis of the Magnus slice (a3): Omega_k = sum_m alpha_m(k) B_m with
+// B = {L0_b, L_1..L_J, [L0_b, L_j] (J), [L_a, L_c] (a<c)}.
+struct Basis {
+  const double2* L0;
+  long long L0_stride;      // complex elements between pulses (0 = shared)
+  const double2* Lc;        // [J][64][64]
+  const double2* Lcomm;     // [.][ncomm][64][64] or nullptr
+  long long Lcomm_stride;   // complex elements between pulses (0 = shared)
+  int J;
+  int ncomm;                // 0 when the commutator basis is not used
+};
+
+struct SliceGrid {
+  double h;                 // T / n_slices
+  double c4;                // sqrt(3) h^2 / 12 for order 4, 0 for order 2
+  int mode;                 // QAL_CTRL_PWC / QAL_CTRL_NODES
+  const double* u;          // [batch][count][nodes][J]
+  int count;                // slices per pulse in this call
+};
+
+struct FwdOut {
+  double2* U_nat;           // [batch][count] natural, or nullptr
+  double* U_img;            // [batch][count] images (internal), or nullptr
+  double2* chunk_nat;       // [batch][count/chunk] natural, or nullptr
+  int chunk;
+  int* status;              // [batch] or nullptr
+};
+
+int num_sms();
+int& launch_counter();
+
+cudaError_t launch_expm_fold(int batch, const Basis& B, const SliceGrid& G, const FwdOut& O, cudaStream_t st);
+cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* out, cudaStream_t st);
+cudaError_t launch_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st);
+cudaError_t launch_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops,
+                               const double2* C, double2* L0, double2* Lc, cudaStream_t st);
+cudaError_t launch_commutators(int batch, int J, const double2* L0, const double2* Lc, double2* Lcomm,
+                               cudaStream_t st);
+// prefix P_{k+1} = U_k P_k (P_0 = I) and suffix X_k = X_{k+1} U_k (X_N = S_V^dag) over
+// per-pulse image sequences; see qal_grad.cu
+cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P_img, double2* Lam_nat,
+                                cudaStream_t st);
+cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const double2* V, double* X_img,
+                                cudaStream_t st);
+cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, const double* P_img,
+                               const double* X_img, double* grad, int* status, double* scratch,
+                               cudaStream_t st);
+size_t grad_scratch_bytes();
+cudaError_t launch_fp64_probe(int kind, int blocks, int iters, double* sink, cudaStream_t st);
+
+}  // namespace qal

@@ -1,0 +1,237 @@
+// qal_product.cu -- K1 (Liouvillian + commutator basis), K4 (ordered-product tree
+// level), K5 (fidelity), K0 (FP64 peak probe).
+#include "qal_dev.cuh"
+#include "qal_internal.h"
+
+namespace qal {
+
+// ------------------------------------------------------------------ K4
+// One tree level of Eq. 15: out[b][i] = in[b][2i+1] in[b][2i] (later factor
+// on the LEFT); an odd last element is carried up unchanged.  One CTA per output.
+__global__ void __launch_bounds__(NT, 2) k_tree_level(int batch, int cnt, const double2* __restrict__ in,
+                                                      double2* __restrict__ out) {
+  extern __shared__ __align__(128) double smem[];
+  const Lane L = lane_id();
+  const int half = (cnt + 1) / 2;
+  const int b = blockIdx.x / half, i = blockIdx.x % half;
+  const double2* src = in + (size_t)b * cnt * PLANE;
+  double2* dst = out + ((size_t)b * half + i) * PLANE;
+  if (2 * i + 1 == cnt) {  // carry
+    for (int e = threadIdx.x; e < PLANE; e += NT) dst[e] = src[(size_t)(cnt - 1) * PLANE + e];
+    return;
+  }
+  block_nat_to_img(smem, src + (size_t)(2 * i) * PLANE);
+  Strip A, acc;
+  load_nat(A, src + (size_t)(2 * i + 1) * PLANE, L);
+  __syncthreads();
+  zero(acc);
+  mma_acc(acc, A, smem, L);
+  store_nat(dst, acc, L);
+}
+
+cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* out, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_tree_level, cudaFuncAttributeMaxDynamicSharedMemorySize, IMG * 8);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int half = (cnt + 1) / 2;
+  k_tree_level<<<batch * half, NT, IMG * 8, st>>>(batch, cnt, in, out);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K5
+// F[b] = Re Tr(S_V^dag Lambda_b) / d^2 with S_V[i+dj, k+dl] = conj(V[j][l]) V[i][k] (A8):
+// F = Re sum V[j][l] conj(V[i][k]) Lambda[i+dj][k+dl] / d^2.  d = 8.  One CTA per pulse.
+__global__ void __launch_bounds__(NT) k_fidelity(const double2* __restrict__ Lam, const double2* __restrict__ V,
+                                                 double* __restrict__ F) {
+  __shared__ double2 Vs[64];
+  __shared__ double red[16];
+  const Lane L = lane_id();
+  if (threadIdx.x < 64) Vs[threadIdx.x] = V[threadIdx.x];
+  __syncthreads();
+  const double2* M = Lam + (size_t)blockIdx.x * PLANE;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const int a = e >> 6, c = e & 63;
+    const int i = a & 7, j = a >> 3, k = c & 7, l = c >> 3;
+    const double2 vjl = Vs[j * 8 + l], vik = Vs[i * 8 + k], x = M[e];
+    // w = vjl * conj(vik)
+    const double wr = vjl.x * vik.x + vjl.y * vik.y;
+    const double wi = vjl.y * vik.x - vjl.x * vik.y;
+    acc += wr * x.x - wi * x.y;
+  }
+  const double s = block_sum(acc, red, L);
+  if (threadIdx.x == 0) F[blockIdx.x] = s / 64.0;
+}
+
+cudaError_t launch_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st) {
+  k_fidelity<<<batch, NT, 0, st>>>(Lam, V, F);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K1
+// Eq. 8, column stacking (A5): with a = p d + r, c = s d + q (p, s: column index of
+// rho; r, q: row index),
+//   (I (x) H)[a][c] = delta_ps H[r][q],   (H^T (x) I)[a][c] = H[s][p] delta_rq,
+//   (conj(C) (x) C)[a][c] = conj(C[p][s]) C[r][q].
+// blockIdx.y = 0 -> L0 of pulse blockIdx.z (drift + all dissipators); y = 1 + j -> L_j.
+__global__ void __launch_bounds__(NT) k_liouvillian(const double2* __restrict__ H0, const double2* __restrict__ Hc,
+                                                    int ncops, const double2* __restrict__ C,
+                                                    double2* __restrict__ L0, double2* __restrict__ Lc, int yoff) {
+  constexpr int d = 8;
+  __shared__ double2 H[64], S[64];   // H and S = sum_c C^dag C
+  __shared__ double2 Cs[64];
+  const int y = blockIdx.y + yoff, b = blockIdx.z;
+  const bool drift = (y == 0);
+  const double2* Hsrc = drift ? H0 + (size_t)b * 64 : Hc + (size_t)(y - 1) * 64;
+  if (threadIdx.x < 64) {
+    H[threadIdx.x] = Hsrc[threadIdx.x];
+    S[threadIdx.x] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  if (drift) {
+    for (int cc = 0; cc < ncops; ++cc) {
+      if (threadIdx.x < 64) Cs[threadIdx.x] = C[(size_t)cc * 64 + threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x < 64) {  // S[r][q] += sum_m conj(C[m][r]) C[m][q]
+        const int r = threadIdx.x >> 3, q = threadIdx.x & 7;
+        double sr = 0.0, si = 0.0;
+        for (int m = 0; m < d; ++m) {
+          const double2 x = Cs[m * 8 + r], z = Cs[m * 8 + q];
+          sr += x.x * z.x + x.y * z.y;
+          si += x.x * z.y - x.y * z.x;
+        }
+        S[threadIdx.x].x += sr;
+        S[threadIdx.x].y += si;
+      }
+      __syncthreads();
+    }
+  }
+  double2* out = drift ? L0 + (size_t)b * PLANE : Lc + (size_t)(y - 1) * PLANE;
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const int a = e >> 6, c = e & 63;
+    const int p = a >> 3, r = a & 7, s = c >> 3, q = c & 7;
+    // Hamiltonian part: -i (delta_ps H[r][q] - H[s][p] delta_rq)
+    double hr = 0.0, hi = 0.0;
+    if (p == s) { hr += H[r * 8 + q].x; hi += H[r * 8 + q].y; }
+    if (r == q) { hr -= H[s * 8 + p].x; hi -= H[s * 8 + p].y; }
+    double vr = hi, vi = -hr;  // -i (hr + i hi) = hi - i hr
+    if (drift) {
+      for (int cc = 0; cc < ncops; ++cc) {
+        const double2 cps = C[(size_t)cc * 64 + p * 8 + s], crq = C[(size_t)cc * 64 + r * 8 + q];
+        // conj(cps) * crq
+        vr += cps.x * crq.x + cps.y * crq.y;
+        vi += cps.x * crq.y - cps.y * crq.x;
+      }
+      if (p == s) { vr -= 0.5 * S[r * 8 + q].x; vi -= 0.5 * S[r * 8 + q].y; }
+      if (r == q) { vr -= 0.5 * S[s * 8 + p].x; vi -= 0.5 * S[s * 8 + p].y; }
+    }
+    out[e] = make_double2(vr, vi);
+  }
+}
+
+cudaError_t launch_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops, const double2* C,
+                               double2* L0, double2* Lc, cudaStream_t st) {
+  // drift part of every pulse (y = 0, z = pulse), then the J control parts once
+  k_liouvillian<<<dim3(1, 1, batch), NT, 0, st>>>(H0, Hc, ncops, C, L0, Lc, 0);
+  ++launch_counter();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || J == 0) return e;
+  k_liouvillian<<<dim3(1, J, 1), NT, 0, st>>>(H0, Hc, ncops, C, L0, Lc, 1);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// [X, Y] = X Y - Y X for the commutator basis of the order-4 generator (a3, A2):
+// blockIdx.y = j < J:   [L0_b, L_j];   j >= J: pair (a, c), a < c, lexicographic.
+__global__ void __launch_bounds__(NT, 1) k_commutators(int J, const double2* __restrict__ L0,
+                                                       const double2* __restrict__ Lc,
+                                                       double2* __restrict__ Lcomm) {
+  extern __shared__ __align__(128) double smem[];
+  double* SX = smem;
+  double* SY = smem + IMG;
+  const Lane L = lane_id();
+  const int b = blockIdx.x, m = blockIdx.y;
+  const int ncomm = J + J * (J - 1) / 2;
+  const double2 *Xp, *Yp;
+  if (m < J) {
+    Xp = L0 + (size_t)b * PLANE;
+    Yp = Lc + (size_t)m * PLANE;
+  } else {
+    int p = J, a = 0, c = 1;
+    for (int aa = 0; aa < J; ++aa)
+      for (int cc = aa + 1; cc < J; ++cc, ++p)
+        if (p == m) { a = aa; c = cc; }
+    Xp = Lc + (size_t)a * PLANE;
+    Yp = Lc + (size_t)c * PLANE;
+  }
+  block_nat_to_img(SX, Xp);
+  block_nat_to_img(SY, Yp);
+  Strip A, acc;
+  __syncthreads();
+  zero(acc);
+  load_nat(A, Xp, L);
+  mma_acc(acc, A, SY, L);  // X Y
+  load_nat(A, Yp, L);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { A.re[i] = -A.re[i]; A.im[i] = -A.im[i]; }
+  mma_acc(acc, A, SX, L);  // - Y X
+  store_nat(Lcomm + ((size_t)b * ncomm + m) * PLANE, acc, L);
+}
+
+cudaError_t launch_commutators(int batch, int J, const double2* L0, const double2* Lc, double2* Lcomm,
+                               cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_commutators, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * IMG * 8);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ncomm = J + J * (J - 1) / 2;
+  k_commutators<<<dim3(batch, ncomm), NT, 2 * IMG * 8, st>>>(J, L0, Lc, Lcomm);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K0
+__global__ void __launch_bounds__(NT) k_probe_dmma(double* sink, int iters) {
+  double acc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+  const double a = 1e-3 * threadIdx.x, b = 1.0 + 1e-6 * threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(acc[2 * i], acc[2 * i + 1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i];
+  if (s == 1234.5) *sink = s;
+}
+__global__ void __launch_bounds__(NT) k_probe_dfma(double* sink, int iters) {
+  double a[8];
+  const double b = 1.0000001, c = 1e-9;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 1234.5) *sink = s;
+}
+
+cudaError_t launch_fp64_probe(int kind, int blocks, int iters, double* sink, cudaStream_t st) {
+  if (kind == 0) k_probe_dmma<<<blocks, NT, 0, st>>>(sink, iters);
+  else k_probe_dfma<<<blocks, NT, 0, st>>>(sink, iters);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+}  // namespace qal

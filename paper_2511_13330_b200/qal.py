@@ -1,0 +1,231 @@
+"""Thin ctypes binding of libqal.so (include/qal.h), same names as the C ABI.
+
+Argument marshalling only: torch tensors (device memory) are passed as raw
+pointers together with the current CUDA stream; every step of the hot path runs
+in the library's sm_100a kernels.  There is no CPU fallback: if the library or a
+GPU is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqal.so")
+
+QAL_OK = 0
+QAL_CTRL_PWC = 0
+QAL_CTRL_NODES = 1
+QAL_OP_ORDERED_PRODUCT = 1
+QAL_OP_FIDELITY = 2
+QAL_OP_FIDELITY_GRAD = 3
+QAL_MAX_CTRL = 8
+
+_EXPORTS = {
+    "qal_abi_version": (ctypes.c_int, []),
+    "qal_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "qal_last_launch_count": (ctypes.c_int, []),
+    "qal_default_chunk": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "qal_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int] * 6),
+    "qal_build_liouvillian": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_magnus_expm_slices": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                               ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_ordered_product": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_fidelity": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_fidelity_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p]),
+}
+
+_lib = None
+
+
+class QalError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load libqal.so and declare every exported symbol (fails loudly if absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise QalError(f"libqal.so not built ({path}); run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _EXPORTS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != QAL_OK:
+        raise QalError(f"{what}: {load().qal_status_string(rc).decode()} ({rc})")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t, dtype, name):
+    if t is None:
+        return None
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise QalError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise QalError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise QalError(f"{name} must be contiguous")
+    return t
+
+
+def abi_version() -> int:
+    return load().qal_abi_version()
+
+
+def last_launch_count() -> int:
+    return load().qal_last_launch_count()
+
+
+def default_chunk(batch: int, n_slices: int) -> int:
+    return load().qal_default_chunk(batch, n_slices)
+
+
+def workspace_bytes(op: int, n: int, batch: int, n_slices: int, n_ctrl: int = 0, flags: int = 0) -> int:
+    return load().qal_workspace_bytes(op, n, batch, n_slices, n_ctrl, flags)
+
+
+def n_comm(J: int) -> int:
+    return J + J * (J - 1) // 2
+
+
+def qal_build_liouvillian(H0, Hc, C, want_comm=False, stream=None):
+    """Eq. 8: returns (L0 [B][n][n], Lc [J][n][n], Lcomm [B][ncomm][n][n] or None)."""
+    c128 = torch.complex128
+    H0 = _dev(H0, c128, "H0")
+    Hc = _dev(Hc, c128, "Hc")
+    C = _dev(C, c128, "C") if C is not None and C.shape[0] > 0 else None
+    d = H0.shape[-1]
+    B = H0.shape[0]
+    J = Hc.shape[0]
+    n = d * d
+    dev = H0.device
+    L0 = torch.empty((B, n, n), dtype=c128, device=dev)
+    Lc = torch.empty((J, n, n), dtype=c128, device=dev)
+    Lcomm = torch.empty((B, n_comm(J), n, n), dtype=c128, device=dev) if want_comm else None
+    rc = load().qal_build_liouvillian(d, B, _ptr(H0), J, _ptr(Hc), 0 if C is None else C.shape[0], _ptr(C),
+                                      int(bool(want_comm)), _ptr(L0), _ptr(Lc), _ptr(Lcomm), _stream(stream))
+    _check(rc, "qal_build_liouvillian")
+    return L0, Lc, Lcomm
+
+
+def qal_magnus_expm_slices(L0, Lc, u, T, n_slices, *, k0=0, count=None, magnus_order=4,
+                           ctrl_mode=QAL_CTRL_PWC, Lcomm=None, want_U=False, chunk=None, status=None,
+                           stream=None):
+    """Eqs. 13-15: per-slice U_k and/or chunk products.  Returns (U or None, chunk_prod or None)."""
+    c128 = torch.complex128
+    L0 = _dev(L0, c128, "L0")
+    Lc = _dev(Lc, c128, "Lc")
+    u = _dev(u, torch.float64, "u")
+    B = u.shape[0]
+    J = Lc.shape[0]
+    n = L0.shape[-1]
+    count = n_slices - k0 if count is None else count
+    dev = u.device
+    U = torch.empty((B, count, n, n), dtype=c128, device=dev) if want_U else None
+    P = None
+    if chunk is not None:
+        P = torch.empty((B, count // chunk, n, n), dtype=c128, device=dev)
+    L0s = 0 if L0.shape[0] == 1 else n * n
+    Lcs = 0
+    if Lcomm is not None:
+        Lcomm = _dev(Lcomm, c128, "Lcomm")
+        Lcs = 0 if Lcomm.shape[0] == 1 else n_comm(J) * n * n
+    rc = load().qal_magnus_expm_slices(n, B, n_slices, float(T), k0, count, magnus_order, ctrl_mode, J, _ptr(u),
+                                       _ptr(L0), L0s, _ptr(Lc), _ptr(Lcomm), Lcs, _ptr(U),
+                                       1 if chunk is None else chunk, _ptr(P), _ptr(status), None, 0,
+                                       _stream(stream))
+    _check(rc, "qal_magnus_expm_slices")
+    return U, P
+
+
+def qal_ordered_product(U, stream=None):
+    """Eq. 15 / P:141 balanced tree: U [B][count][n][n] -> U[count-1] ... U[0]."""
+    U = _dev(U, torch.complex128, "U")
+    B, count, n = U.shape[0], U.shape[1], U.shape[2]
+    out = torch.empty((B, n, n), dtype=U.dtype, device=U.device)
+    wsb = workspace_bytes(QAL_OP_ORDERED_PRODUCT, n, B, count)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=U.device)
+    rc = load().qal_ordered_product(n, B, count, _ptr(U), _ptr(out), _ptr(ws), wsb, _stream(stream))
+    _check(rc, "qal_ordered_product")
+    return out
+
+
+def qal_fidelity(Lam, V, stream=None):
+    """A8: F[b] = Re Tr(S_V^dag Lambda_b) / d^2."""
+    Lam = _dev(Lam, torch.complex128, "Lambda")
+    V = _dev(V, torch.complex128, "V")
+    F = torch.empty(Lam.shape[0], dtype=torch.float64, device=Lam.device)
+    rc = load().qal_fidelity(V.shape[0], Lam.shape[0], _ptr(Lam), _ptr(V), _ptr(F), _stream(stream))
+    _check(rc, "qal_fidelity")
+    return F
+
+
+def qal_fidelity_grad(L0, Lc, u, T, n_slices, V, *, magnus_order=4, ctrl_mode=QAL_CTRL_PWC, Lcomm=None,
+                      want_grad=True, want_Lambda=False, status=None, ws=None, stream=None):
+    """The whole hot path: returns (F [B], grad (layout of u) or None, Lambda or None)."""
+    c128 = torch.complex128
+    L0 = _dev(L0, c128, "L0")
+    Lc = _dev(Lc, c128, "Lc")
+    u = _dev(u, torch.float64, "u")
+    V = _dev(V, c128, "V")
+    B = u.shape[0]
+    J = Lc.shape[0]
+    n = L0.shape[-1]
+    d = V.shape[0]
+    dev = u.device
+    F = torch.empty(B, dtype=torch.float64, device=dev)
+    g = torch.empty_like(u) if want_grad else None
+    Lam = torch.empty((B, n, n), dtype=c128, device=dev) if want_Lambda else None
+    op = QAL_OP_FIDELITY_GRAD if want_grad else QAL_OP_FIDELITY
+    wsb = workspace_bytes(op, n, B, n_slices, J, ctrl_mode)
+    if ws is None or ws.numel() < wsb:
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    L0s = 0 if L0.shape[0] == 1 else n * n
+    Lcs = 0
+    if Lcomm is not None:
+        Lcomm = _dev(Lcomm, c128, "Lcomm")
+        Lcs = 0 if Lcomm.shape[0] == 1 else n_comm(J) * n * n
+    rc = load().qal_fidelity_grad(d, B, n_slices, float(T), magnus_order, ctrl_mode, J, _ptr(u), _ptr(L0), L0s,
+                                  _ptr(Lc), _ptr(Lcomm), Lcs, _ptr(V), _ptr(F), _ptr(g), _ptr(Lam),
+                                  _ptr(status), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "qal_fidelity_grad")
+    return F, g, Lam
+
+
+def qal_fp64_peak_probe(kind: int, blocks: int, iters: int, sink, stream=None) -> float:
+    """Launch the FP64 probe (K0); returns the flop count of the launch."""
+    fl = ctypes.c_double(0.0)
+    rc = load().qal_fp64_peak_probe(kind, blocks, iters, ctypes.byref(fl), _ptr(sink), _stream(stream))
+    _check(rc, "qal_fp64_peak_probe")
+    return fl.value
