@@ -1,0 +1,286 @@
+#!/usr/bin/env python
+"""bench.py -- Magnus slices/s of the Qalibrate hot path on B200 (BASELINE.json metric).
+
+Default workload (one "step" = every SURVEY 8(a) row once over one batch):
+  configs[2]: 4096 pulses x 1024 PWC slices (T = 200 ns, d = 8, n = 64, complex128) per GPU,
+  quasistatic Zeeman offsets per pulse; a2 Liouvillian build, a3-a5 Magnus-4 expm + ordered
+  product, a6 fidelity, a7 gradient w.r.t. all 2 x 1024 controls of every pulse.
+  value = slices/s summed over all ranks (weak scaling: every rank owns 4096 distinct pulses).
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+        (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Magnus slices/s (c128 64×64 expm+product) and % FP64 roofline at 1/2/4/8 GPU"
+UNIT = "slices/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pulses", type=int, default=4096, help="pulses per GPU (configs[2]: 4096)")
+    ap.add_argument("--slices", type=int, default=1024)
+    ap.add_argument("--sub-batch", type=int, default=296)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-slices", type=int, default=1024)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) leg
+def oracle_sample(prob, n_sample):
+    """The oracle as it stands (O1-O7: forward + per-direction gradient) on the first n_sample
+    slices of pulse 0 with the workload's slice width; returns (slices/s, seconds, threads)."""
+    import oracle
+    L0, Lc = oracle.build_liouvillian(prob.H0[0], prob.Hc, prob.C)
+    h = prob.T / prob.N
+    u = prob.u[0, :n_sample]
+    t0 = time.perf_counter()
+    oracle.gradient(L0, Lc, u, h * n_sample, n_sample, prob.V)
+    dt = time.perf_counter() - t0
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return n_sample / dt, dt, threads
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2511_13330_b200 import inputs as qi
+    oracle.build()
+    prob = qi.cfg2(batch=1, N=args.slices, T=200.0 * args.slices / 1024)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, dt, threads = oracle_sample(prob, args.cpu_sample_slices)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    sample = (f"oracle (O1-O7, sequential C, OpenMP over gradient directions) on slices 0..{args.cpu_sample_slices - 1}"
+              f" of pulse 0 of configs[2] (h = 200/1024 ns), forward + gradient, per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(d for _, d in vals),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[2] bounded sample (oracle)", "slices_per_step": args.cpu_sample_slices},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our leg
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_13330_b200 import _build, driver, inputs as qi, qal
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _build.build()
+    qal.load()
+
+    B, N = args.pulses, args.slices
+    T = 200.0 * N / 1024
+    prob = qi.cfg2(batch=B, N=N, T=T, first_pulse=rank * B)       # rank owns pulses [rank B, (rank+1) B)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    H0, Hc, C, u, V = to(prob.H0), to(prob.Hc), to(prob.C), to(prob.u), to(prob.V)
+    eng = driver.PulseBatch(H0, Hc, C, u, V, T, sub_batch=args.sub_batch)
+
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tf = driver.fp64_peak(sink, blocks=2 * nsm)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        eng.step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: device-resident inputs
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qal.qal_profile_begin(counters)
+    ev0.record()
+    launches = 0
+    for _ in range(args.steps):
+        eng.step()
+        launches += eng.launches
+    ev1.record()
+    torch.cuda.synchronize()
+    stages = qal.qal_profile_end()
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    prods = counters.cpu().tolist()
+
+    slices_total = world * B * N * args.steps
+    value = slices_total / (ms_max * 1e-3)
+
+    # ---------------- e2e: host (pinned) inputs -> device -> host results, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hu = torch.from_numpy(prob.u).pin_memory()
+        hH0 = torch.from_numpy(prob.H0).pin_memory()
+        hF = torch.empty(B, dtype=torch.float64).pin_memory()
+        hg = torch.empty_like(hu).pin_memory()
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            eng.u.copy_(hu, non_blocking=True)
+            eng.H0.copy_(hH0, non_blocking=True)
+            eng.step()
+            hF.copy_(eng.F, non_blocking=True)
+            hg.copy_(eng.grad, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        t2 = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e = {"value": slices_total / (t2.item() * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(hu.numel() * 8 + hH0.numel() * 16),
+               "d2h_bytes_per_step": int(hF.numel() * 8 + hg.numel() * 8)}
+
+    # ---------------- roofline of the dominant kernel (largest device time in the window)
+    dom = max(stages, key=lambda s: stages[s][0])
+    dom_ms, dom_launch = stages[dom]
+    dom_idx = qal.STAGES.index(dom)
+    dom_flops_per_launch = driver.stage_flops(prods[dom_idx]) / max(dom_launch, 1)
+    achieved = dom_flops_per_launch / (dom_ms / max(dom_launch, 1) * 1e-3) / 1e12
+    traffic = load_traffic().get(qal.KERNELS[dom])
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": traffic, "kernel": qal.KERNELS[dom],
+                "peak_source": "measured FP64 DMMA.8x8x4 peak (K0 probe, this run, this GPU); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "flops_per_launch": dom_flops_per_launch, "ms_per_launch": dom_ms / max(dom_launch, 1)}
+    step_flops = sum(driver.stage_flops(p) for p in prods) / args.steps
+    split = {s: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                 "products_per_step": prods[i] / args.steps,
+                 "tflops": (driver.stage_flops(prods[i]) / (v[0] * 1e-3) / 1e12) if v[0] > 0 else None}
+             for i, (s, v) in enumerate(stages.items()) if v[1] > 0}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        v, dt, threads = oracle_sample(prob, args.cpu_sample_slices)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"oracle forward + gradient on slices 0..{args.cpu_sample_slices - 1} of pulse 0 "
+                         f"of this workload ({dt:.1f} s), OpenMP over gradient directions"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "configs[2]: pulses x 1024 PWC slices, T=200 ns, d=8 (64x64 c128 "
+                                       "superoperators), forward + fidelity + gradient",
+                           "pulses_per_gpu": B, "slices": N, "sub_batch": eng.sub,
+                           "l2": f"inputs larger than L2 (gradient workspace {eng.ws_bytes / 2**30:.1f} GiB)",
+                           "parallelism": f"batch-sharded x{world}"},
+                "pulses_per_s": world * B * args.steps / (ms_max * 1e-3),
+                "pct_fp64_roofline": step_flops / (ms_max / args.steps * 1e-3) / 1e12 / peak_tf,
+                "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "gpu": torch.cuda.get_device_name(dev)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -188,6 +188,22 @@ int qal_default_chunk(int batch, int n_slices);
  */
 int qal_fp64_peak_probe(int kind, int blocks, int iters, double *flops, double *sink, void *stream);
 
+/*
+ * Stage profiling (bench.py's roofline and the expm-vs-product split, the Fig. 2
+ * analog of P:167-171).  Between qal_profile_begin and qal_profile_end every kernel
+ * the library enqueues is bracketed by CUDA events on its launch stream and, if
+ * `dev_counters` (device unsigned long long[QAL_NSTAGE], zeroed by the caller) is
+ * not NULL, each kernel adds the number of 64x64 complex matrix products it actually
+ * executed (the (m, s) choice is per slice) to dev_counters[stage].
+ * qal_profile_end synchronises the recorded events and writes, per stage, the summed
+ * device milliseconds and the number of launches (host arrays of QAL_NSTAGE).
+ * Not thread-safe; one profiling window per process at a time.
+ */
+enum { QAL_ST_LIOUV = 0, QAL_ST_COMM = 1, QAL_ST_EXPM = 2, QAL_ST_TREE = 3, QAL_ST_FID = 4,
+       QAL_ST_PREFIX = 5, QAL_ST_SUFFIX = 6, QAL_ST_GRAD = 7, QAL_NSTAGE = 8 };
+int qal_profile_begin(unsigned long long *dev_counters);
+int qal_profile_end(double *ms, int *launches);
+
 /* Number of kernels the last call on this host thread enqueued (launch accounting
  * for bench.py's gpu_launches); reset by every qal_* call that launches. */
 int qal_last_launch_count(void);

@@ -2,6 +2,7 @@
 // validation, then kernel launches on the caller's stream.  No allocation.
 #include <cmath>
 #include <cstdint>
+#include <vector>
 
 #include "../../include/qal.h"
 #include "qal_dev.cuh"
@@ -25,6 +26,54 @@ int num_sms() {
 int& launch_counter() {
   static thread_local int c = 0;
   return c;
+}
+
+namespace {
+struct ProfRec {
+  int stage;
+  cudaEvent_t e0, e1;
+};
+struct ProfState {
+  bool on = false;
+  unsigned long long* ctr = nullptr;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<ProfRec> recs;
+  cudaEvent_t pending = nullptr;
+};
+ProfState& prof() {
+  static ProfState p;
+  return p;
+}
+cudaEvent_t prof_event() {
+  ProfState& P = prof();
+  if (P.used == P.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    P.pool.push_back(e);
+  }
+  return P.pool[P.used++];
+}
+}  // namespace
+
+unsigned long long* prof_counter(int stage) {
+  ProfState& P = prof();
+  return (P.on && P.ctr) ? P.ctr + stage : nullptr;
+}
+void prof_pre(int stage, cudaStream_t st) {
+  (void)stage;
+  ProfState& P = prof();
+  if (!P.on) return;
+  P.pending = prof_event();
+  cudaEventRecord(P.pending, st);
+}
+void prof_post(int stage, cudaStream_t st) {
+  ProfState& P = prof();
+  if (!P.on || !P.pending) return;
+  cudaEvent_t e1 = prof_event();
+  cudaEventRecord(e1, st);
+  P.recs.push_back({stage, P.pending, e1});
+  P.pending = nullptr;
 }
 
 }  // namespace qal
@@ -241,13 +290,9 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
     double2* lam = Lambda ? D2(Lambda) : lam_tmp;
     FwdOut O{nullptr, nullptr, parts, ch, status};
     if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
-    int l = launch_counter();
     rc = run_tree(batch, nch, parts, lam, w, st);
-    l += launch_counter();
     if (rc != QAL_OK) return rc;
-    rc = cuda_rc(launch_fidelity(batch, lam, D2(V), F, st));
-    launch_counter() += l;
-    return rc;
+    return cuda_rc(launch_fidelity(batch, lam, D2(V), F, st));
   }
   // gradient path: U_k images (parallel over slices) -> prefix chain P_k -> fidelity ->
   // suffix chain X_{k+1} -> one adjoint Frechet derivative per slice
@@ -258,16 +303,45 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
   double2* lam_tmp = reinterpret_cast<double2*>(X_img + seq);
   double* scratch = reinterpret_cast<double*>(lam_tmp + (size_t)batch * PLANE_C);
   double2* lam = Lambda ? D2(Lambda) : lam_tmp;
-  int total = 0;
   FwdOut O{nullptr, U_img, nullptr, 1, status};
   if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
-  total += launch_counter();
   if (launch_prefix_chain(batch, n_slices, U_img, P_img, lam, st) != cudaSuccess) return QAL_ERR_CUDA;
   if (launch_fidelity(batch, lam, D2(V), F, st) != cudaSuccess) return QAL_ERR_CUDA;
   if (launch_suffix_chain(batch, n_slices, U_img, D2(V), X_img, st) != cudaSuccess) return QAL_ERR_CUDA;
   if (launch_grad_slices(batch, c.B, c.G, P_img, X_img, grad, status, scratch, st) != cudaSuccess)
     return QAL_ERR_CUDA;
   return QAL_OK;
+}
+
+int qal_profile_begin(unsigned long long* dev_counters) {
+  ProfState& P = prof();
+  P.on = true;
+  P.ctr = dev_counters;
+  P.recs.clear();
+  P.used = 0;
+  P.pending = nullptr;
+  return QAL_OK;
+}
+
+int qal_profile_end(double* ms, int* launches) {
+  ProfState& P = prof();
+  if (!ms || !launches) return QAL_ERR_NULL;
+  for (int i = 0; i < NSTAGE; ++i) { ms[i] = 0.0; launches[i] = 0; }
+  int rc = QAL_OK;
+  for (const ProfRec& r : P.recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&t, r.e0, r.e1) != cudaSuccess) {
+      rc = QAL_ERR_CUDA;
+      continue;
+    }
+    ms[r.stage] += t;
+    launches[r.stage] += 1;
+  }
+  P.on = false;
+  P.ctr = nullptr;
+  P.recs.clear();
+  P.used = 0;
+  return rc;
 }
 
 int qal_fp64_peak_probe(int kind, int blocks, int iters, double* flops, double* sink, void* stream) {

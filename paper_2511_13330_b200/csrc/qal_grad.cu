@@ -35,7 +35,8 @@ __device__ __forceinline__ void set_identity(Strip& s, const Lane& L) {
 // ------------------------------------------------------------------ prefix chain
 // P_0 = I, P_{k+1} = U_k P_k; writes P_img[b][k] = P_k (k < N) and Lam[b] = P_N.
 __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __restrict__ U_img,
-                                                        double* __restrict__ P_img, double2* __restrict__ Lam) {
+                                                        double* __restrict__ P_img, double2* __restrict__ Lam,
+                                                        unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* SP = smem;
   double* SU[2] = {smem + IMG, smem + 2 * IMG};
@@ -73,13 +74,15 @@ __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __r
     if (k + 1 < N) store_img(P + (size_t)(k + 1) * IMG, acc, L);
     else store_nat(Lam + (size_t)b * PLANE, acc, L);
   }
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, (unsigned long long)N);
 }
 
 // ------------------------------------------------------------------ suffix chain
 // X_N = S_V^dag, X_k = X_{k+1} U_k; writes X_img[b][k-1] = X_k for k = 1..N.
 // S_V^dag[a][c] = V[j][l] conj(V[i][k]) with a = k + 8 l, c = i + 8 j (A8, column stacking).
 __global__ void __launch_bounds__(NT, 1) k_suffix_chain(int N, const double* __restrict__ U_img,
-                                                        const double2* __restrict__ V, double* __restrict__ X_img) {
+                                                        const double2* __restrict__ V, double* __restrict__ X_img,
+                                                        unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* SU[2] = {smem, smem + IMG};
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * IMG);
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(NT, 1) k_suffix_chain(int N, const double* __r
     copy(A, acc);
     store_img(X + (size_t)(k - 1) * IMG, A, L);
   }
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, (unsigned long long)(N - 1));
 }
 
 // ------------------------------------------------------------------ gradient slices
@@ -128,7 +132,8 @@ __device__ __forceinline__ int n_traces(const Basis& B) { return B.J + B.ncomm; 
 __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, SliceGrid G,
                                                        const double* __restrict__ P_img,
                                                        const double* __restrict__ X_img, double* __restrict__ grad,
-                                                       int* __restrict__ status, double* __restrict__ scratch) {
+                                                       int* __restrict__ status, double* __restrict__ scratch,
+                                                       unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* S1 = smem;            // X_{k+1}, then dX = G / 2^s, then dX^4, then dE
   double* S2 = smem + IMG;      // X = Omega / 2^s
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
   const int items = batch * N;
   const int K = n_traces(B);
   uint32_t phase = 0;
+  unsigned long long nprod = 0;
   Strip A, acc;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
@@ -211,6 +217,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
     store_img(S1, acc, L);                        // S1 = dX^4
     // Horner with derivative: H = B_{tb-1} + c_m X^4, dH = dB_{tb-1} + c_m dX^4
     const int tb = m / 4;
+    nprod += 1 + 3 + 6 + 3 * (tb - 1) + 3 * s;   // G, powers, their derivatives, Horner, squarings
     const double cm = inv_fact(m);
     ps_block(A, tb - 1, sX, tm, L);
     load_img(acc, S3, L);
@@ -310,6 +317,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
       }
     }
   }
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, nprod);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -325,7 +333,9 @@ cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_prefix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, P_img, Lam);
+  prof_pre(ST_PREFIX, st);
+  k_prefix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, P_img, Lam, prof_counter(ST_PREFIX));
+  prof_post(ST_PREFIX, st);
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -338,7 +348,9 @@ cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const dou
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_suffix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, V, X_img);
+  prof_pre(ST_SUFFIX, st);
+  k_suffix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, V, X_img, prof_counter(ST_SUFFIX));
+  prof_post(ST_SUFFIX, st);
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -353,7 +365,10 @@ cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, co
   }
   const int items = batch * G.count;
   const int grid = items < num_sms() ? items : num_sms();
-  k_grad_slices<<<grid, NT, GRAD_SMEM_BYTES, st>>>(batch, B, G, P_img, X_img, grad, status, scratch);
+  prof_pre(ST_GRAD, st);
+  k_grad_slices<<<grid, NT, GRAD_SMEM_BYTES, st>>>(batch, B, G, P_img, X_img, grad, status, scratch,
+                                                    prof_counter(ST_GRAD));
+  prof_post(ST_GRAD, st);
   ++launch_counter();
   return cudaGetLastError();
 }

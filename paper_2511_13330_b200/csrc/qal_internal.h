@@ -40,6 +40,12 @@ struct FwdOut {
 int num_sms();
 int& launch_counter();
 
+// profiling window (qal_profile_begin/end): stage ids as in qal.h
+enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, NSTAGE };
+unsigned long long* prof_counter(int stage);   // device counter slot or nullptr
+void prof_pre(int stage, cudaStream_t st);      // record start event (no-op when off)
+void prof_post(int stage, cudaStream_t st);     // record end event
+
 cudaError_t launch_expm_fold(int batch, const Basis& B, const SliceGrid& G, const FwdOut& O, cudaStream_t st);
 cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* out, cudaStream_t st);
 cudaError_t launch_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st);

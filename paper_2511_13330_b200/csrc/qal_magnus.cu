@@ -56,7 +56,8 @@ __device__ __forceinline__ int expm_ps(Strip& A, Strip& acc, int m, int s, doubl
   return prods;
 }
 
-__global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGrid G, FwdOut O) {
+__global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGrid G, FwdOut O,
+                                                    unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* SX = smem;
   double* SX4 = smem + IMG;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGr
   const int nchunk = G.count / O.chunk;
   const int items = batch * nchunk;
   Strip A, acc;
+  unsigned long long nprod = 0;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / nchunk, c = item % nchunk;
     if (threadIdx.x == 0) bad_sh = 0;
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGr
       for (int i = 0; i < 16; ++i) { A.re[i] *= sc; A.im[i] *= sc; }
       store_img(SX, A, L);
       __syncthreads();
-      expm_ps(A, acc, m, s, SX, SX4, tm, L);
+      nprod += expm_ps(A, acc, m, s, SX, SX4, tm, L);
       const size_t slot = (size_t)b * G.count + k;
       if (O.U_nat) store_nat(O.U_nat + slot * PLANE, A, L);
       if (O.U_img) store_img(O.U_img + slot * IMG, A, L);
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGr
         } else {
           zero(acc); mma_acc(acc, A, SP, L);  // P <- U_k P
           copy(A, acc);
+          ++nprod;
           __syncthreads();
           store_img(SP, A, L);
         }
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGr
     // status[] is zeroed by the host API before the launch; only failures are written
     if (O.status && threadIdx.x == 0 && bad_sh) O.status[b] = -4;
   }
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, nprod);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -124,7 +128,9 @@ cudaError_t launch_expm_fold(int batch, const Basis& B, const SliceGrid& G, cons
   }
   const int items = batch * (G.count / O.chunk);
   const int grid = items < num_sms() ? items : num_sms();
-  k_expm_fold<<<grid, NT, FWD_SMEM_BYTES, st>>>(batch, B, G, O);
+  prof_pre(ST_EXPM, st);
+  k_expm_fold<<<grid, NT, FWD_SMEM_BYTES, st>>>(batch, B, G, O, prof_counter(ST_EXPM));
+  prof_post(ST_EXPM, st);
   ++launch_counter();
   return cudaGetLastError();
 }

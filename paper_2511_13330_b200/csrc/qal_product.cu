@@ -9,7 +9,7 @@ namespace qal {
 // One tree level of Eq. 15: out[b][i] = in[b][2i+1] in[b][2i] (later factor
 // on the LEFT); an odd last element is carried up unchanged.  One CTA per output.
 __global__ void __launch_bounds__(NT, 2) k_tree_level(int batch, int cnt, const double2* __restrict__ in,
-                                                      double2* __restrict__ out) {
+                                                      double2* __restrict__ out, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   const Lane L = lane_id();
   const int half = (cnt + 1) / 2;
@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(NT, 2) k_tree_level(int batch, int cnt, const 
   zero(acc);
   mma_acc(acc, A, smem, L);
   store_nat(dst, acc, L);
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, 1ull);
 }
 
 cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* out, cudaStream_t st) {
@@ -37,7 +38,9 @@ cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* ou
     attr = true;
   }
   const int half = (cnt + 1) / 2;
-  k_tree_level<<<batch * half, NT, IMG * 8, st>>>(batch, cnt, in, out);
+  prof_pre(ST_TREE, st);
+  k_tree_level<<<batch * half, NT, IMG * 8, st>>>(batch, cnt, in, out, prof_counter(ST_TREE));
+  prof_post(ST_TREE, st);
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -68,7 +71,9 @@ __global__ void __launch_bounds__(NT) k_fidelity(const double2* __restrict__ Lam
 }
 
 cudaError_t launch_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st) {
+  prof_pre(ST_FID, st);
   k_fidelity<<<batch, NT, 0, st>>>(Lam, V, F);
+  prof_post(ST_FID, st);
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -137,11 +142,15 @@ __global__ void __launch_bounds__(NT) k_liouvillian(const double2* __restrict__ 
 cudaError_t launch_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops, const double2* C,
                                double2* L0, double2* Lc, cudaStream_t st) {
   // drift part of every pulse (y = 0, z = pulse), then the J control parts once
+  prof_pre(ST_LIOUV, st);
   k_liouvillian<<<dim3(1, 1, batch), NT, 0, st>>>(H0, Hc, ncops, C, L0, Lc, 0);
+  prof_post(ST_LIOUV, st);
   ++launch_counter();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || J == 0) return e;
+  prof_pre(ST_LIOUV, st);
   k_liouvillian<<<dim3(1, J, 1), NT, 0, st>>>(H0, Hc, ncops, C, L0, Lc, 1);
+  prof_post(ST_LIOUV, st);
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -150,7 +159,7 @@ cudaError_t launch_liouvillian(int batch, const double2* H0, int J, const double
 // blockIdx.y = j < J:   [L0_b, L_j];   j >= J: pair (a, c), a < c, lexicographic.
 __global__ void __launch_bounds__(NT, 1) k_commutators(int J, const double2* __restrict__ L0,
                                                        const double2* __restrict__ Lc,
-                                                       double2* __restrict__ Lcomm) {
+                                                       double2* __restrict__ Lcomm, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* SX = smem;
   double* SY = smem + IMG;
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(NT, 1) k_commutators(int J, const double2* __r
   for (int i = 0; i < 16; ++i) { A.re[i] = -A.re[i]; A.im[i] = -A.im[i]; }
   mma_acc(acc, A, SX, L);  // - Y X
   store_nat(Lcomm + ((size_t)b * ncomm + m) * PLANE, acc, L);
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, 2ull);
 }
 
 cudaError_t launch_commutators(int batch, int J, const double2* L0, const double2* Lc, double2* Lcomm,
@@ -192,7 +202,9 @@ cudaError_t launch_commutators(int batch, int J, const double2* L0, const double
     attr = true;
   }
   const int ncomm = J + J * (J - 1) / 2;
-  k_commutators<<<dim3(batch, ncomm), NT, 2 * IMG * 8, st>>>(J, L0, Lc, Lcomm);
+  prof_pre(ST_COMM, st);
+  k_commutators<<<dim3(batch, ncomm), NT, 2 * IMG * 8, st>>>(J, L0, Lc, Lcomm, prof_counter(ST_COMM));
+  prof_post(ST_COMM, st);
   ++launch_counter();
   return cudaGetLastError();
 }

@@ -1,0 +1,160 @@
+"""Host-side driver: device buffers, sub-batching and multi-GPU partitioning around
+the C ABI (B3 in SURVEY.md).  Plumbing only -- every arithmetic step of the hot path
+runs inside libqal.so.
+
+* PulseBatch  -- configs[2]-style batches: per-pulse drift, shared controls basis;
+                 the batch is processed in sub-batches whose gradient workspace fits
+                 HBM; across ranks the pulses are partitioned (no data-path collective).
+* time_shard_propagator -- configs[3]-style long horizons: rank r owns the slice range
+                 [r N/G, (r+1) N/G), folds it into one partial (same chunk/tree shape
+                 for every G), all-gathers the G partials and combines them in order
+                 (later rank on the LEFT, Eq. 15).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import qal
+
+C128 = torch.complex128
+F64 = torch.float64
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class PulseBatch:
+    """Forward + gradient for a batch of pulses with per-pulse drift Hamiltonians.
+
+    Inputs are device tensors: H0 [B][d][d], Hc [J][d][d], C [K][d][d], u [B][N][J], V [d][d].
+    ``step()`` runs the whole hot path (a2 Liouvillian, a3-a5 propagator, a6 fidelity,
+    a7 gradient) and leaves F [B] and grad [B][N][J] in preallocated device buffers.
+    """
+
+    def __init__(self, H0, Hc, C, u, V, T, *, sub_batch=None, want_grad=True, magnus_order=4, stream=None):
+        self.H0, self.Hc, self.C, self.u, self.V = H0, Hc, C, u, V
+        self.B, self.N, self.J = u.shape[0], u.shape[1], Hc.shape[0]
+        self.d = V.shape[0]
+        self.n = self.d * self.d
+        self.T = float(T)
+        self.order = magnus_order
+        self.want_grad = want_grad
+        dev = u.device
+        self.stream = stream
+        self.sub = self.B if sub_batch is None else min(sub_batch, self.B)
+        self.L0 = torch.empty((self.B, self.n, self.n), dtype=C128, device=dev)
+        self.Lc = torch.empty((self.J, self.n, self.n), dtype=C128, device=dev)
+        self.F = torch.empty(self.B, dtype=F64, device=dev)
+        self.grad = torch.empty_like(u) if want_grad else None
+        self.status = torch.zeros(self.B, dtype=torch.int32, device=dev)
+        op = qal.QAL_OP_FIDELITY_GRAD if want_grad else qal.QAL_OP_FIDELITY
+        self.ws_bytes = qal.workspace_bytes(op, self.n, self.sub, self.N, self.J, 0)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.launches = 0
+
+    def _s(self):
+        s = torch.cuda.current_stream() if self.stream is None else self.stream
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def step(self):
+        lib = qal.load()
+        st = self._s()
+        nc = 0 if self.C is None else self.C.shape[0]
+        rc = lib.qal_build_liouvillian(self.d, self.B, _p(self.H0), self.J, _p(self.Hc), nc, _p(self.C), 0,
+                                       _p(self.L0), _p(self.Lc), None, st)
+        qal._check(rc, "qal_build_liouvillian")
+        launches = lib.qal_last_launch_count()
+        plane = self.n * self.n
+        for b0 in range(0, self.B, self.sub):
+            nb = min(self.sub, self.B - b0)
+            rc = lib.qal_fidelity_grad(
+                self.d, nb, self.N, self.T, self.order, qal.QAL_CTRL_PWC, self.J,
+                ctypes.c_void_p(self.u.data_ptr() + b0 * self.N * self.J * 8),
+                ctypes.c_void_p(self.L0.data_ptr() + b0 * plane * 16), plane, _p(self.Lc), None, 0, _p(self.V),
+                ctypes.c_void_p(self.F.data_ptr() + b0 * 8),
+                ctypes.c_void_p(self.grad.data_ptr() + b0 * self.N * self.J * 8) if self.want_grad else None,
+                None, ctypes.c_void_p(self.status.data_ptr() + b0 * 4), _p(self.ws), self.ws_bytes, st)
+            qal._check(rc, "qal_fidelity_grad")
+            launches += lib.qal_last_launch_count()
+        self.launches = launches
+        return self.F, self.grad
+
+
+def shard_range(total: int, world: int, rank: int):
+    """Contiguous equal shard [lo, hi) of `total` units for `rank` (total % world == 0)."""
+    if total % world:
+        raise ValueError(f"{total} units do not split over {world} ranks")
+    per = total // world
+    return rank * per, (rank + 1) * per
+
+
+def time_shard_chunk(n_slices: int, world_max: int = 8) -> int:
+    """Chunk size keyed to N only (A16): every rank's range is a union of whole subtrees
+    for any G <= world_max dividing N, so the product is bit-identical across G."""
+    c = 1
+    while c < 64 and n_slices % (2 * c) == 0 and n_slices // (2 * c) >= world_max:
+        c *= 2
+    return c
+
+
+def ordered_combine(parts, stream=None):
+    """Lambda = Q_{G-1} ... Q_0 from the stacked per-rank partials [G][n][n] (qal_ordered_product)."""
+    return qal.qal_ordered_product(parts.unsqueeze(0).contiguous(), stream=stream)[0]
+
+
+def time_shard_propagator(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, magnus_order=4, group=None,
+                          stream=None):
+    """configs[3]: this rank's slices [k0, k0 + len(u_local)) -> local tree partial -> all-gather ->
+    ordered combine.  Returns Lambda (identical on every rank)."""
+    import torch.distributed as dist
+
+    count = u_local.shape[1]
+    chunk = time_shard_chunk(n_slices)
+    _, parts = qal.qal_magnus_expm_slices(L0, Lc, u_local, T, n_slices, k0=k0, count=count,
+                                          magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcomm=Lcomm,
+                                          chunk=chunk, stream=stream)
+    Q = qal.qal_ordered_product(parts, stream=stream)[0]          # local partial, [n][n]
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return Q
+    world = dist.get_world_size(group)
+    gathered = torch.empty((world,) + tuple(Q.shape), dtype=Q.dtype, device=Q.device)
+    dist.all_gather_into_tensor(torch.view_as_real(gathered).reshape(-1), torch.view_as_real(Q).reshape(-1),
+                                group=group)
+    return ordered_combine(gathered, stream=stream)
+
+
+def fp64_peak(sink, blocks, seconds=0.2, kind=0):
+    """Measured FP64 peak (K0 probe, DMMA.8x8x4 by default) in TFLOP/s on the current device."""
+    iters = 2000
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qal.qal_fp64_peak_probe(kind, blocks, iters, sink)      # warm-up
+    torch.cuda.synchronize()
+    start.record()
+    fl = qal.qal_fp64_peak_probe(kind, blocks, iters, sink)
+    end.record()
+    end.synchronize()
+    ms = start.elapsed_time(end)
+    iters = max(1, int(iters * seconds * 1e3 / max(ms, 1e-3)))
+    best = 0.0
+    for _ in range(3):
+        start.record()
+        fl = qal.qal_fp64_peak_probe(kind, blocks, iters, sink)
+        end.record()
+        end.synchronize()
+        best = max(best, fl / (start.elapsed_time(end) * 1e-3) / 1e12)
+    return best
+
+
+MATMUL_FLOPS_64 = 8.0 * 64 ** 3     # one 64x64 complex product (ZGEMM convention)
+
+
+def stage_flops(products: int) -> float:
+    return products * MATMUL_FLOPS_64
+
+
+__all__ = ["PulseBatch", "shard_range", "time_shard_chunk", "time_shard_propagator", "ordered_combine",
+           "fp64_peak", "MATMUL_FLOPS_64", "stage_flops", "math"]

@@ -22,6 +22,11 @@ QAL_OP_ORDERED_PRODUCT = 1
 QAL_OP_FIDELITY = 2
 QAL_OP_FIDELITY_GRAD = 3
 QAL_MAX_CTRL = 8
+STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
+          "grad_slices"]
+KERNELS = {"liouvillian": "k_liouvillian", "commutators": "k_commutators", "expm_fold": "k_expm_fold",
+           "tree": "k_tree_level", "fidelity": "k_fidelity", "prefix_chain": "k_prefix_chain",
+           "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices"}
 
 _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
@@ -47,6 +52,8 @@ _EXPORTS = {
                                           ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_profile_begin": (ctypes.c_int, [ctypes.c_void_p]),
+    "qal_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p]),
 }
@@ -221,6 +228,20 @@ def qal_fidelity_grad(L0, Lc, u, T, n_slices, V, *, magnus_order=4, ctrl_mode=QA
                                   _ptr(status), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "qal_fidelity_grad")
     return F, g, Lam
+
+
+def qal_profile_begin(dev_counters=None):
+    """Open a stage-profiling window (events around every library kernel)."""
+    _check(load().qal_profile_begin(_ptr(dev_counters)), "qal_profile_begin")
+
+
+def qal_profile_end():
+    """Close the window: {stage: (device ms summed, launches)} (synchronises the events)."""
+    n = len(STAGES)
+    ms = (ctypes.c_double * n)()
+    la = (ctypes.c_int * n)()
+    _check(load().qal_profile_end(ms, la), "qal_profile_end")
+    return {STAGES[i]: (ms[i], la[i]) for i in range(n)}
 
 
 def qal_fp64_peak_probe(kind: int, blocks: int, iters: int, sink, stream=None) -> float:
