@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"],
+                    help="cfg2: batch fwd+grad (default, weak scaling); cfg3: 2^20-slice horizon, time-sharded")
     return ap.parse_args()
 
 
@@ -234,7 +236,9 @@ def run_ours(args):
     dom_idx = qal.STAGES.index(dom)
     dom_flops_per_launch = driver.stage_flops(prods[dom_idx]) / max(dom_launch, 1)
     achieved = dom_flops_per_launch / (dom_ms / max(dom_launch, 1) * 1e-3) / 1e12
-    traffic = load_traffic().get(qal.KERNELS[dom])
+    tr = load_traffic().get(qal.KERNELS[dom])
+    units_per_launch = {"grad_slices": eng.sub * N, "expm_fold": eng.sub * N}.get(dom)
+    traffic = (tr["dram_bytes_per_unit"] * units_per_launch) if (tr and units_per_launch) else None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved / peak_tf, "traffic": traffic, "kernel": qal.KERNELS[dom],
                 "peak_source": "measured FP64 DMMA.8x8x4 peak (K0 probe, this run, this GPU); "
@@ -275,10 +279,102 @@ def run_ours(args):
     return 0
 
 
+def run_cfg3(args):
+    """configs[3]: one pulse, N = 2^20 NODES slices over 10 us, time-sharded over the ranks
+    (strong scaling): a1 device sampler -> a2 basis (+ commutators) -> a3-a5 local chunk fold +
+    tree -> all-gather of the G partials -> ordered combine -> a6 fidelity."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_13330_b200 import _build, driver, inputs as qi, qal
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _build.build()
+    qal.load()
+    prob = qi.cfg3()
+    N, T = prob.N, prob.T
+    k0, k1 = driver.shard_range(N, world, rank)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    H0, Hc, C, V, prm = to(prob.H0), to(prob.Hc), to(prob.C), to(prob.V), to(prob.sines)
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
+
+    state = {}
+
+    def step():
+        u = qal.qal_sample_controls_sines(prm, prob.u_max, N, T, k0, k1 - k0)
+        L0, Lc, Lcomm = qal.qal_build_liouvillian(H0, Hc, C, want_comm=True)
+        Lam = driver.time_shard_propagator(L0, Lc, Lcomm, u.unsqueeze(0), T, N, k0, ctrl_mode=qal.QAL_CTRL_NODES)
+        state["F"] = qal.qal_fidelity(Lam.unsqueeze(0), V)
+        state["Lam"] = Lam
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qal.qal_profile_begin(counters)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    stages = qal.qal_profile_end()
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    prods = counters.cpu().tolist()
+    value = N * args.steps / (ms_max * 1e-3)
+    dom = "expm_fold"
+    dom_ms, dom_l = stages[dom]
+    ach = driver.stage_flops(prods[qal.STAGES.index(dom)]) / (dom_ms * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
+                "traffic": None, "kernel": "k_expm_fold",
+                "peak_source": "measured FP64 DMMA.8x8x4 peak (K0 probe, this run)",
+                "flops_per_launch": driver.stage_flops(prods[qal.STAGES.index(dom)]) / max(dom_l, 1),
+                "ms_per_launch": dom_ms / max(dom_l, 1)}
+    split = {s: {"ms_per_step": v[0] / args.steps, "products_per_step": prods[i] / args.steps}
+             for i, (s, v) in enumerate(stages.items()) if v[1] > 0}
+    if rank == 0:
+        step_flops = sum(driver.stage_flops(p) for p in prods) / args.steps
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "configs[3]: 1 pulse, N=2^20 Magnus-4 NODES slices over 10 us, "
+                                       "time-sharded, all-gather of G partials + ordered combine",
+                           "slices": N, "chunk": driver.time_shard_chunk(N), "parallelism": f"time-sharded x{world}",
+                           "l2": "chunk partials 1 GiB > L2"},
+                "pct_fp64_roofline": step_flops / (ms_max / args.steps * 1e-3) / 1e12 / peak_tf,
+                "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split,
+                "F": state["F"].item(), "clocks": clk, "gpu": torch.cuda.get_device_name(dev)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "cfg3":
+        return run_cfg3(args)
     return run_ours(args)
 
 

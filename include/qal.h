@@ -152,6 +152,17 @@ int qal_fidelity(int d, int batch, const qal_c128 *Lambda, const qal_c128 *V, do
                  void *stream);
 
 /*
+ * Control table of configs[3] (a1, NODES mode; A11): the smooth random controls
+ *   s_j(t) = sum_m a_{jm} sin(2 pi f_{jm} t + phi_{jm}) / sqrt(sum_m a_{jm}^2 / 2)
+ *   u_j(t) = clip(u_max/2 (1 + s_j(t)/2), 0, u_max)
+ * sampled at the two Gauss-Legendre nodes tau_{k,1,2} = t_k + (1/2 -+ sqrt(3)/6) h of the
+ * slices k0 .. k0+count-1 of the grid t_k = k h, h = T / n_slices.
+ *   prm    device [n_ctrl][nterm][3] = (a, f [GHz], phi).   u_out device [count][2][n_ctrl].
+ */
+int qal_sample_controls_sines(int n_ctrl, int nterm, const double *prm, double u_max, int n_slices,
+                              double T, int k0, int count, double *u_out, void *stream);
+
+/*
  * The whole hot path for a batch of pulses: propagator (as above, full grid,
  * k0 = 0, count = n_slices), fidelity and, if grad != NULL, the gradient of F
  * with respect to every control value (A14; P:185 motivates the adjoint form):

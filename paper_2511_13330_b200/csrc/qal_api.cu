@@ -115,7 +115,7 @@ int run_tree(int batch, int count, const double2* U, double2* out, void* ws, cud
   return QAL_OK;
 }
 
-bool finite(double x) { return std::isfinite(x); }
+bool is_fin(double x) { return std::isfinite(x); }
 
 struct Common {
   Basis B;
@@ -127,7 +127,7 @@ int check_basis(int n_or_d_ok, int batch, int n_slices, double T, int order, int
                 Common& c) {
   if (!n_or_d_ok) return QAL_ERR_UNSUPPORTED;
   if (batch < 1 || n_slices < 1) return QAL_ERR_EMPTY;
-  if (!finite(T) || T <= 0.0) return QAL_ERR_NONFINITE;
+  if (!is_fin(T) || T <= 0.0) return QAL_ERR_NONFINITE;
   if (order != 2 && order != 4) return QAL_ERR_UNSUPPORTED;
   if (mode != QAL_CTRL_PWC && mode != QAL_CTRL_NODES) return QAL_ERR_UNSUPPORTED;
   if (J < 1 || J > QAL_MAX_CTRL) return QAL_ERR_UNSUPPORTED;
@@ -311,6 +311,17 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
   if (launch_grad_slices(batch, c.B, c.G, P_img, X_img, grad, status, scratch, st) != cudaSuccess)
     return QAL_ERR_CUDA;
   return QAL_OK;
+}
+
+int qal_sample_controls_sines(int n_ctrl, int nterm, const double* prm, double u_max, int n_slices, double T,
+                              int k0, int count, double* u_out, void* stream) {
+  launch_counter() = 0;
+  if (n_ctrl < 1 || n_ctrl > QAL_MAX_CTRL || nterm < 1) return QAL_ERR_UNSUPPORTED;
+  if (n_slices < 1 || count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!is_fin(T) || T <= 0.0 || !is_fin(u_max)) return QAL_ERR_NONFINITE;
+  if (!prm || !u_out) return QAL_ERR_NULL;
+  return cuda_rc(launch_sample_sines(n_ctrl, nterm, prm, u_max, T / n_slices, k0, count, u_out, S(stream)));
 }
 
 int qal_profile_begin(unsigned long long* dev_counters) {

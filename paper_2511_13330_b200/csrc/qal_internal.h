@@ -63,6 +63,8 @@ cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, co
                                const double* X_img, double* grad, int* status, double* scratch,
                                cudaStream_t st);
 size_t grad_scratch_bytes();
+cudaError_t launch_sample_sines(int J, int nterm, const double* prm, double umax, double h, int k0, int count,
+                               double* out, cudaStream_t st);
 cudaError_t launch_fp64_probe(int kind, int blocks, int iters, double* sink, cudaStream_t st);
 
 }  // namespace qal

@@ -209,6 +209,41 @@ cudaError_t launch_commutators(int batch, int J, const double2* L0, const double
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ a1 (NODES controls)
+// configs[3] controls (A11) at the Gauss-Legendre nodes of slices k0..k0+count-1.
+__global__ void __launch_bounds__(NT) k_sample_sines(int J, int nterm, const double* __restrict__ prm, double umax,
+                                                     double h, int k0, int count, double* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * NT + threadIdx.x;
+  if (idx >= (long long)count * 2 * J) return;
+  const int j = (int)(idx % J);
+  const int a = (int)((idx / J) % 2);
+  const long long k = idx / (2 * J) + k0;
+  // explicit round-to-nearest operations (no FMA contraction): the phase 2 pi f t reaches
+  // ~3e3 rad at t = 10 us, where a contracted multiply-add would move u by ~1e-13
+  const double c = __ddiv_rn(__dsqrt_rn(3.0), 6.0);
+  const double tk = __dmul_rn((double)k, h);
+  const double t = __dadd_rn(tk, __dmul_rn(a == 0 ? __dsub_rn(0.5, c) : __dadd_rn(0.5, c), h));
+  const double* p = prm + (size_t)j * nterm * 3;
+  double s = 0.0, a2 = 0.0;
+  for (int m = 0; m < nterm; ++m) {
+    const double arg = __dadd_rn(__dmul_rn(__dmul_rn(2.0 * 3.141592653589793, p[3 * m + 1]), t), p[3 * m + 2]);
+    s = __dadd_rn(s, __dmul_rn(p[3 * m], sin(arg)));
+    a2 = __dadd_rn(a2, __dmul_rn(p[3 * m], p[3 * m]));
+  }
+  s = __ddiv_rn(s, __dsqrt_rn(__ddiv_rn(a2, 2.0)));
+  const double v = __dmul_rn(__dmul_rn(0.5, umax), __dadd_rn(1.0, __dmul_rn(0.5, s)));
+  out[idx] = v < 0.0 ? 0.0 : (v > umax ? umax : v);
+}
+
+cudaError_t launch_sample_sines(int J, int nterm, const double* prm, double umax, double h, int k0, int count,
+                               double* out, cudaStream_t st) {
+  const long long total = (long long)count * 2 * J;
+  const int grid = (int)((total + NT - 1) / NT);
+  k_sample_sines<<<grid, NT, 0, st>>>(J, nterm, prm, umax, h, k0, count, out);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K0
 __global__ void __launch_bounds__(NT) k_probe_dmma(double* sink, int iters) {
   double acc[16];

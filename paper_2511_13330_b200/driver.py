@@ -95,36 +95,59 @@ def shard_range(total: int, world: int, rank: int):
 def time_shard_chunk(n_slices: int, world_max: int = 8) -> int:
     """Chunk size keyed to N only (A16): every rank's range is a union of whole subtrees
     for any G <= world_max dividing N, so the product is bit-identical across G."""
+    base = n_slices
+    for g in (world_max, 4, 2, 1):
+        if n_slices % g == 0:
+            base = n_slices // g
+            break
     c = 1
-    while c < 64 and n_slices % (2 * c) == 0 and n_slices // (2 * c) >= world_max:
+    while c < 64 and base % (2 * c) == 0:
         c *= 2
     return c
 
 
-def ordered_combine(parts, stream=None):
-    """Lambda = Q_{G-1} ... Q_0 from the stacked per-rank partials [G][n][n] (qal_ordered_product)."""
-    return qal.qal_ordered_product(parts.unsqueeze(0).contiguous(), stream=stream)[0]
+def gather_partials(Q, group=None):
+    """All-gather every rank's partial product [n][n] -> [G][n][n] in rank order (NCCL over
+    NVLink on GPUs, gloo on CPU).  Complex tensors travel as their real view."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return Q.unsqueeze(0)
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(Q.shape), dtype=Q.dtype, device=Q.device)
+    dist.all_gather_into_tensor(torch.view_as_real(out).reshape(-1), torch.view_as_real(Q.contiguous()).reshape(-1),
+                                group=group)
+    return out
+
+
+def ordered_combine(parts, product=None, stream=None):
+    """Lambda = Q_{G-1} ... Q_0 (Eq. 15, later rank on the LEFT) from the gathered partials [G][n][n],
+    with the same balanced-tree shape as qal_ordered_product.  `product(list_or_tensor)` may be
+    swapped for tests; the default is the library's tree kernel."""
+    if product is None:
+        return qal.qal_ordered_product(parts.unsqueeze(0).contiguous(), stream=stream)[0]
+    return product(parts)
+
+
+def local_partial(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, magnus_order=4, stream=None):
+    """This rank's partial Q = U_{k0+count-1} ... U_{k0}: chunk fold (chunk keyed to N only) + tree."""
+    count = u_local.shape[1]
+    chunk = time_shard_chunk(n_slices)
+    if count % chunk:
+        raise ValueError(f"slice range {count} is not a multiple of the chunk {chunk}")
+    _, parts = qal.qal_magnus_expm_slices(L0, Lc, u_local, T, n_slices, k0=k0, count=count,
+                                          magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcomm=Lcomm,
+                                          chunk=chunk, stream=stream)
+    return qal.qal_ordered_product(parts, stream=stream)[0]
 
 
 def time_shard_propagator(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, magnus_order=4, group=None,
                           stream=None):
-    """configs[3]: this rank's slices [k0, k0 + len(u_local)) -> local tree partial -> all-gather ->
-    ordered combine.  Returns Lambda (identical on every rank)."""
-    import torch.distributed as dist
-
-    count = u_local.shape[1]
-    chunk = time_shard_chunk(n_slices)
-    _, parts = qal.qal_magnus_expm_slices(L0, Lc, u_local, T, n_slices, k0=k0, count=count,
-                                          magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcomm=Lcomm,
-                                          chunk=chunk, stream=stream)
-    Q = qal.qal_ordered_product(parts, stream=stream)[0]          # local partial, [n][n]
-    if group is None and not (dist.is_available() and dist.is_initialized()):
-        return Q
-    world = dist.get_world_size(group)
-    gathered = torch.empty((world,) + tuple(Q.shape), dtype=Q.dtype, device=Q.device)
-    dist.all_gather_into_tensor(torch.view_as_real(gathered).reshape(-1), torch.view_as_real(Q).reshape(-1),
-                                group=group)
-    return ordered_combine(gathered, stream=stream)
+    """configs[3]: this rank's slices [k0, k0 + count) -> local partial -> all-gather -> ordered
+    combine.  Returns Lambda (identical on every rank)."""
+    Q = local_partial(L0, Lc, Lcomm, u_local, T, n_slices, k0, ctrl_mode=ctrl_mode, magnus_order=magnus_order,
+                      stream=stream)
+    return ordered_combine(gather_partials(Q, group), stream=stream)
 
 
 def fp64_peak(sink, blocks, seconds=0.2, kind=0):
@@ -157,4 +180,4 @@ def stage_flops(products: int) -> float:
 
 
 __all__ = ["PulseBatch", "shard_range", "time_shard_chunk", "time_shard_propagator", "ordered_combine",
-           "fp64_peak", "MATMUL_FLOPS_64", "stage_flops", "math"]
+           "gather_partials", "local_partial", "fp64_peak", "MATMUL_FLOPS_64", "stage_flops", "math"]

@@ -52,6 +52,9 @@ _EXPORTS = {
                                           ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_sample_controls_sines": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_double,
+                                                  ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_void_p, ctypes.c_void_p]),
     "qal_profile_begin": (ctypes.c_int, [ctypes.c_void_p]),
     "qal_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -228,6 +231,18 @@ def qal_fidelity_grad(L0, Lc, u, T, n_slices, V, *, magnus_order=4, ctrl_mode=QA
                                   _ptr(status), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "qal_fidelity_grad")
     return F, g, Lam
+
+
+def qal_sample_controls_sines(prm, u_max, n_slices, T, k0=0, count=None, stream=None):
+    """a1 (NODES, A11): controls at the GL nodes of slices k0..k0+count-1 -> [count][2][J] f64."""
+    prm = _dev(prm, torch.float64, "prm")
+    J, nterm = prm.shape[0], prm.shape[1]
+    count = n_slices - k0 if count is None else count
+    out = torch.empty((count, 2, J), dtype=torch.float64, device=prm.device)
+    rc = load().qal_sample_controls_sines(J, nterm, _ptr(prm), float(u_max), n_slices, float(T), k0, count,
+                                          _ptr(out), _stream(stream))
+    _check(rc, "qal_sample_controls_sines")
+    return out
 
 
 def qal_profile_begin(dev_counters=None):

@@ -1,0 +1,122 @@
+"""Full-size parity at BASELINE.json sizes, in the launch configuration bench.py times:
+sampled outputs the oracle computes one by one, and properties that hold at any size."""
+import numpy as np
+import pytest
+
+from paper_2511_13330_b200 import inputs as qi
+
+pytestmark = pytest.mark.gpu
+
+
+def relfro(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def qal(torch_cuda):
+    from paper_2511_13330_b200 import _build, qal as q
+    _build.build()
+    q.load()
+    return q
+
+
+def to(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.fixture(scope="module")
+def cfg2_full(torch_cuda, qal):
+    """configs[2] at full size through driver.PulseBatch with bench.py's sub-batch (296)."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg2()
+    eng = driver.PulseBatch(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C), to(torch, p.u), to(torch, p.V),
+                            p.T, sub_batch=296)
+    F, g = eng.step()
+    torch.cuda.synchronize()
+    return p, F.cpu().numpy(), g.cpu().numpy(), eng.status.cpu().numpy()
+
+
+@pytest.mark.parametrize("pulse", [0, 295, 296, 2047, 4095])
+def test_cfg2_full_size_sampled_pulses(cfg2_full, oracle, pulse):
+    p, F, g, status = cfg2_full
+    assert status[pulse] == 0
+    L0, Lc = oracle.build_liouvillian(p.H0[pulse], p.Hc, p.C)
+    Fr, gr, _ = oracle.gradient(L0, Lc, p.u[pulse], p.T, p.N, p.V)
+    assert abs(F[pulse] - Fr) / abs(Fr) <= 1e-10
+    assert relfro(g[pulse], gr) <= 1e-8
+
+
+def test_cfg2_full_size_properties(cfg2_full):
+    _, F, g, status = cfg2_full
+    assert np.all(status == 0)
+    assert np.all(np.isfinite(F)) and np.all(np.isfinite(g))
+    assert np.all((F > 0.0) & (F < 1.0))          # process fidelity of a CPTP map lies in [0, 1]
+
+
+@pytest.fixture(scope="module")
+def cfg3_full(torch_cuda, qal):
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg3()
+    L0, Lc, Lcomm = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C), want_comm=True)
+    u = qal.qal_sample_controls_sines(to(torch, p.sines), p.u_max, p.N, p.T)
+    return p, L0, Lc, Lcomm, u
+
+
+def test_cfg3_full_horizon_properties_and_bit_identity_across_G(cfg3_full, qal, torch_cuda):
+    """N = 2^20: trace / Hermiticity preservation (P-4, P-5), exact coherence-order zeros (P-13),
+    and the time-sharded product for G = 2, 4, 8 bit-identical to G = 1 (A16)."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p, L0, Lc, Lcomm, u = cfg3_full
+    N = p.N
+    lam = {}
+    for G in (1, 2, 4, 8):
+        parts = []
+        for r in range(G):
+            k0, k1 = driver.shard_range(N, G, r)
+            parts.append(driver.local_partial(L0, Lc, Lcomm, u[k0:k1].unsqueeze(0).contiguous(), p.T, N, k0,
+                                              ctrl_mode=1))
+        lam[G] = driver.ordered_combine(torch.stack(parts)).cpu().numpy()
+    for G in (2, 4, 8):
+        assert np.array_equal(lam[G], lam[1]), G
+    Lam = lam[1]
+    vecI = np.eye(8).reshape(-1, order="F")
+    assert np.max(np.abs(vecI @ Lam - vecI)) <= 1e-10
+    idx = np.arange(64)
+    sw = (idx // 8) + 8 * (idx % 8)
+    assert np.max(np.abs(Lam - Lam[sw][:, sw].conj())) <= 1e-10
+    m = np.array([bin(i).count("1") for i in range(8)])   # number of down spins
+    q = np.array([m[a // 8] - m[a % 8] for a in range(64)])  # coherence order of vec index a = i + 8 j
+    off = q[:, None] != q[None, :]
+    assert np.all(Lam[off] == 0.0)
+
+
+@pytest.mark.parametrize("chunk_index", [0, 7777, 16383])
+def test_cfg3_full_horizon_sampled_chunks(cfg3_full, qal, oracle, chunk_index):
+    """The chunk partials bench.py folds (chunk 64 of the 2^20-slice grid) vs the oracle."""
+    p, L0, Lc, Lcomm, u = cfg3_full
+    from paper_2511_13330_b200 import driver
+    chunk = driver.time_shard_chunk(p.N)
+    k0 = chunk_index * chunk
+    _, P = qal.qal_magnus_expm_slices(L0, Lc, u[k0:k0 + chunk].unsqueeze(0).contiguous(), p.T, p.N, k0=k0,
+                                      count=chunk, ctrl_mode=1, Lcomm=Lcomm, chunk=chunk)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    uref = oracle.sines_nodes(p.sines, p.u_max, p.N, p.T, k0, k0 + chunk)
+    ref = oracle_range(oracle, rL0, rLc, uref, p.T, p.N, k0, chunk)
+    assert relfro(P[0, 0].cpu().numpy(), ref) <= 1e-10
+
+
+def oracle_range(oracle, L0, Lc, u_rows, T, N, k0, count):
+    """oracle.propagate indexes u by absolute slice; hand it a table whose row k0+i is u_rows[i]."""
+    full = np.zeros((k0 + count,) + u_rows.shape[1:])
+    full[k0:] = u_rows
+    return oracle.propagate(L0, Lc, full, T, N, mode=1, k0=k0, k1=k0 + count)

@@ -288,3 +288,14 @@ def test_determinism_bit_identical(torch_cuda, qal, cfg0_ref):
     L0, Lc, _ = build_basis(torch, qal, p)
     outs = [qal.qal_fidelity_grad(L0, Lc, dev(torch, p.u), p.T, p.N, dev(torch, p.V)) for _ in range(2)]
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+# ------------------------------------------------------------------ a1, NODES controls on the device
+@pytest.mark.parametrize("k0,count", [(0, 4096), ((1 << 20) - 777, 777), (123456, 1)])
+def test_sines_sampler_matches_oracle(torch_cuda, qal, oracle, k0, count):
+    torch = torch_cuda
+    p = qi.cfg3()
+    got = qal.qal_sample_controls_sines(dev(torch, p.sines), p.u_max, p.N, p.T, k0, count).cpu().numpy()
+    ref = oracle.sines_nodes(p.sines, p.u_max, p.N, p.T, k0, k0 + count)
+    assert got.shape == ref.shape
+    assert np.max(np.abs(got - ref)) <= 1e-13 * p.u_max
