@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"],
+    ap.add_argument("--cfg4-slices", type=int, default=8, help="slices per step of the cfg4 sample")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
                     help="cfg2: batch fwd+grad (default, weak scaling); cfg3: 2^20-slice horizon, time-sharded")
     return ap.parse_args()
 
@@ -178,7 +179,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # ---------------- timed region: device-resident inputs
-    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    counters = torch.zeros(9, dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -320,7 +321,7 @@ def run_cfg3(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    counters = torch.zeros(9, dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -369,8 +370,96 @@ def run_cfg3(args):
     return 0
 
 
+def run_cfg4(args):
+    """configs[4]: d = 64 (n = 4096) dense tiled DMMA path, PWC; pulses sharded over ranks (weak:
+    one pulse per rank per step).  A step is a bounded sample of one pulse: the first
+    --cfg4-slices slices (expm + fold, chunk = all of them) + the fidelity."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_13330_b200 import _build, driver, inputs as qi, qal
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _build.build()
+    qal.load()
+    S = args.cfg4_slices
+    prob = qi.cfg4()
+    pulse = rank % prob.u.shape[0]
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    L0, Lc, _ = qal.qal_build_liouvillian(to(prob.H0), to(prob.Hc), to(prob.C))
+    u = to(prob.u[pulse:pulse + 1, :S])
+    V = to(prob.V)
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
+    n = 4096
+    ws = torch.empty(qal.workspace_bytes(qal.QAL_OP_EXPM_SLICES, n, 1, S), dtype=torch.uint8, device=dev)
+    P = torch.empty((1, 1, n, n), dtype=torch.complex128, device=dev)
+    F = torch.empty(1, dtype=torch.float64, device=dev)
+    lib = qal.load()
+    st = lambda: qal._stream(None)  # noqa: E731
+
+    def step():
+        rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, 5, qal._ptr(u), qal._ptr(L0), 0,
+                                        qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
+                                        ws.numel(), st())
+        qal._check(rc, "qal_magnus_expm_slices")
+        qal._check(lib.qal_fidelity(64, 1, qal._ptr(P), qal._ptr(V), qal._ptr(F), st()), "qal_fidelity")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    counters = torch.zeros(9, dtype=torch.int64, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qal.qal_profile_begin(counters)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    stages = qal.qal_profile_end()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    g_ms, g_l = stages["dense_gemm"]
+    flops_per_product = 8.0 * n ** 3
+    nprod = counters.cpu().tolist()[qal.STAGES.index("dense_gemm")]   # executed 4096^2 products
+    if rank == 0:
+        ach = nprod * flops_per_product / (g_ms * 1e-3) / 1e12
+        line = {"metric": METRIC, "value": world * S * args.steps / (ms_max * 1e-3), "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"configs[4] sample: pulse {pulse}, first {S} of 512 PWC slices, d=64 "
+                                       f"(4096x4096 c128), expm + fold + fidelity", "slices_per_step": S},
+                "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+                             "frac": ach / peak_tf, "traffic": None, "kernel": "k_dense_gemm",
+                             "ms_per_launch": g_ms / max(g_l, 1)},
+                "fp64_peak_tflops": peak_tf, "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()
+                                                                   if v[1]},
+                "products_per_slice": nprod / (S * args.steps),
+                "F_sample": F.item(), "clocks": clk, "gpu": torch.cuda.get_device_name(dev)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if args.config == "cfg4" and args.impl != "reference":
+        return run_cfg4(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "cfg3":

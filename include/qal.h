@@ -27,7 +27,11 @@
  *    reduction uses atomics and every tree has a fixed shape keyed to the
  *    slice count and chunk size only (A16).
  *  - Supported sizes: d = 8 (superoperator n = d*d = 64, the three-spin
- *    exchange-only qubit of P:59).  Other d return QAL_ERR_UNSUPPORTED.
+ *    exchange-only qubit of P:59) on every entry point, and d = 64 (n = 4096, two
+ *    exchange-only qubits = six spins, BASELINE configs[4]) on the forward path:
+ *    build_liouvillian (want_comm = 0), magnus_expm_slices (PWC controls; degree-16
+ *    Taylor with device-chosen s <= 8), ordered_product, fidelity and fidelity_grad
+ *    with grad == NULL.  Other sizes return QAL_ERR_UNSUPPORTED.
  *    Controls: 1 <= n_ctrl <= QAL_MAX_CTRL.
  */
 #ifndef QAL_H
@@ -61,7 +65,8 @@ enum {
 enum {                   /* op codes for qal_workspace_bytes */
     QAL_OP_ORDERED_PRODUCT = 1,
     QAL_OP_FIDELITY = 2,      /* qal_fidelity_grad with grad == NULL */
-    QAL_OP_FIDELITY_GRAD = 3  /* qal_fidelity_grad with grad != NULL */
+    QAL_OP_FIDELITY_GRAD = 3, /* qal_fidelity_grad with grad != NULL */
+    QAL_OP_EXPM_SLICES = 4    /* qal_magnus_expm_slices (non-zero only for n = 4096) */
 };
 
 #define QAL_MAX_CTRL 8
@@ -119,7 +124,9 @@ int qal_build_liouvillian(int d, int batch, const qal_c128 *H0, int n_ctrl, cons
  *   chunk        >= 1, must divide count.  chunk_prod optional
  *                [batch][count/chunk][n][n].  At least one of U_out / chunk_prod.
  *   status       optional device int[batch].
- *   ws, ws_bytes unused (pass NULL, 0); reserved.
+ *   ws, ws_bytes n = 64: unused (NULL, 0).  n = 4096: >= qal_workspace_bytes(QAL_OP_EXPM_SLICES,
+ *                4096, ...) bytes (eight tiled 4096^2 matrices, ~2.1 GB); pulses run one after
+ *                the other, each product filling the GPU.
  */
 int qal_magnus_expm_slices(int n, int batch, int n_slices, double T, int k0, int count,
                            int magnus_order, int ctrl_mode, int n_ctrl, const double *u,
@@ -211,7 +218,7 @@ int qal_fp64_peak_probe(int kind, int blocks, int iters, double *flops, double *
  * Not thread-safe; one profiling window per process at a time.
  */
 enum { QAL_ST_LIOUV = 0, QAL_ST_COMM = 1, QAL_ST_EXPM = 2, QAL_ST_TREE = 3, QAL_ST_FID = 4,
-       QAL_ST_PREFIX = 5, QAL_ST_SUFFIX = 6, QAL_ST_GRAD = 7, QAL_NSTAGE = 8 };
+       QAL_ST_PREFIX = 5, QAL_ST_SUFFIX = 6, QAL_ST_GRAD = 7, QAL_ST_DENSE_GEMM = 8, QAL_NSTAGE = 9 };
 int qal_profile_begin(unsigned long long *dev_counters);
 int qal_profile_end(double *ms, int *launches);
 

@@ -187,6 +187,30 @@ def matmul(A, B):
     return C
 
 
+def matmul_rows(A, B, r0, r1):
+    """rows r0..r1-1 of A B (plain sums)."""
+    A, pa = _c(A, np.complex128)
+    B, pb = _c(B, np.complex128)
+    n = A.shape[0]
+    C = np.zeros((r1 - r0, n), np.complex128)
+    lib().qalref_matmul_rows(n, pa, pb, r0, r1, C.ctypes.data_as(ctypes.c_void_p))
+    return C
+
+
+def evolve_rho(H0, Hc, C, u, T, N, sub, rho0):
+    """RK4 of Eq. 6 on the density matrix with PWC controls u[N][J] (no superoperator)."""
+    H0, p0 = _c(H0, np.complex128)
+    d = H0.shape[-1]
+    Hc, pc = _c(np.asarray(Hc).reshape(-1, d, d), np.complex128)
+    C, pC = _c(np.asarray(C).reshape(-1, d, d), np.complex128)
+    u, pu = _c(u, np.float64)
+    rho0, pr = _c(rho0, np.complex128)
+    rho = np.zeros_like(rho0)
+    _chk(lib().qalref_evolve_rho(d, p0, Hc.shape[0], pc, C.shape[0], pC, N, ctypes.c_double(T), sub, pu, pr,
+                                 rho.ctypes.data_as(ctypes.c_void_p)))
+    return rho
+
+
 def ordered_product(Us):
     """U[count-1] ... U[0] by a sequential left fold (Eq. 15)."""
     P = np.eye(Us.shape[-1], dtype=np.complex128)

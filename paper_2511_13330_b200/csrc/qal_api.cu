@@ -94,6 +94,47 @@ size_t tree_ws_bytes(int batch, int count) {
   return (size_t)batch * (c1 + c2) * MAT_BYTES;
 }
 
+constexpr size_t BIG = (size_t)4096 * 4096;      // complex elements of an n = 4096 matrix
+constexpr size_t BIG_BYTES = BIG * 16;
+
+size_t dense_tree_ws_bytes(int batch, int count) {
+  const size_t c1 = (size_t)(count + 1) / 2, c2 = (c1 + 1) / 2;
+  return (count <= 2 ? 0 : (size_t)batch * (c1 + c2) * BIG_BYTES) + 3 * BIG_BYTES;
+}
+
+// n = 4096 balanced tree: level by level, one dense product per pair (each fills the GPU)
+int run_dense_tree(int batch, int count, const double2* U, double2* out, void* ws, cudaStream_t st) {
+  if (count == 1) return cuda_rc(cudaMemcpyAsync(out, U, (size_t)batch * BIG_BYTES, cudaMemcpyDeviceToDevice, st));
+  const size_t c1 = (size_t)(count + 1) / 2, c2 = (c1 + 1) / 2;
+  double* tiles = reinterpret_cast<double*>(ws);
+  double2* bufA = reinterpret_cast<double2*>(tiles + 3 * BIG * 2);
+  double2* bufB = bufA + (size_t)batch * c1 * BIG;
+  (void)c2;
+  const double2* in = U;
+  int cnt = count, lvl = 0;
+  while (cnt > 1) {
+    const int half = (cnt + 1) / 2;
+    double2* dst = (half == 1) ? out : ((lvl & 1) ? bufB : bufA);
+    for (int b = 0; b < batch; ++b)
+      for (int i = 0; i < half; ++i) {
+        const double2* src = in + ((size_t)b * cnt) * BIG;
+        double2* d = dst + ((size_t)b * half + i) * BIG;
+        if (2 * i + 1 == cnt) {
+          if (cudaMemcpyAsync(d, src + (size_t)(cnt - 1) * BIG, BIG_BYTES, cudaMemcpyDeviceToDevice, st) !=
+              cudaSuccess)
+            return QAL_ERR_CUDA;
+        } else if (launch_dense_tree_pair(src + (size_t)(2 * i + 1) * BIG, src + (size_t)(2 * i) * BIG, d, tiles,
+                                          st) != cudaSuccess) {
+          return QAL_ERR_CUDA;
+        }
+      }
+    in = dst;
+    cnt = half;
+    ++lvl;
+  }
+  return QAL_OK;
+}
+
 // Balanced tree over `count` natural matrices per pulse -> out.
 int run_tree(int batch, int count, const double2* U, double2* out, void* ws, cudaStream_t st) {
   if (count == 1) return cuda_rc(cudaMemcpyAsync(out, U, (size_t)batch * MAT_BYTES, cudaMemcpyDeviceToDevice, st));
@@ -124,7 +165,7 @@ struct Common {
 
 int check_basis(int n_or_d_ok, int batch, int n_slices, double T, int order, int mode, int J, const double* u,
                 const qal_c128* L0, long long L0s, const qal_c128* Lc, const qal_c128* Lcomm, long long Lcs,
-                Common& c) {
+                Common& c, bool dense = false) {
   if (!n_or_d_ok) return QAL_ERR_UNSUPPORTED;
   if (batch < 1 || n_slices < 1) return QAL_ERR_EMPTY;
   if (!is_fin(T) || T <= 0.0) return QAL_ERR_NONFINITE;
@@ -132,7 +173,8 @@ int check_basis(int n_or_d_ok, int batch, int n_slices, double T, int order, int
   if (mode != QAL_CTRL_PWC && mode != QAL_CTRL_NODES) return QAL_ERR_UNSUPPORTED;
   if (J < 1 || J > QAL_MAX_CTRL) return QAL_ERR_UNSUPPORTED;
   if (!u || !L0 || !Lc) return QAL_ERR_NULL;
-  if (L0s != 0 && L0s != (long long)PLANE_C) return QAL_ERR_DIM;
+  if (L0s != 0 && L0s != (long long)(dense ? BIG : PLANE_C)) return QAL_ERR_DIM;
+  if (dense && mode != QAL_CTRL_PWC) return QAL_ERR_UNSUPPORTED;
   const bool comm = (mode == QAL_CTRL_NODES && order == 4);
   if (comm && !Lcomm) return QAL_ERR_NULL;
   if (comm && Lcs != 0 && Lcs != (long long)ncomm_of(J) * PLANE_C) return QAL_ERR_DIM;
@@ -186,7 +228,16 @@ int qal_default_chunk(int batch, int n_slices) {
 size_t qal_workspace_bytes(int op, int n, int batch, int n_slices, int n_ctrl, int flags) {
   (void)n_ctrl;
   (void)flags;
-  if (n != 64 || batch < 1 || n_slices < 1) return 0;
+  if (batch < 1 || n_slices < 1) return 0;
+  if (n == 4096) {
+    switch (op) {
+      case QAL_OP_EXPM_SLICES: return dense_expm_ws_bytes();
+      case QAL_OP_ORDERED_PRODUCT: return dense_tree_ws_bytes(batch, n_slices);
+      case QAL_OP_FIDELITY: return dense_expm_ws_bytes() + (size_t)batch * BIG_BYTES;
+      default: return 0;
+    }
+  }
+  if (n != 64) return 0;
   switch (op) {
     case QAL_OP_ORDERED_PRODUCT: return tree_ws_bytes(batch, n_slices);
     case QAL_OP_FIDELITY: {
@@ -204,13 +255,18 @@ int qal_build_liouvillian(int d, int batch, const qal_c128* H0, int n_ctrl, cons
                           const qal_c128* C, int want_comm, qal_c128* L0, qal_c128* Lc, qal_c128* Lcomm,
                           void* stream) {
   launch_counter() = 0;
-  if (d != 8) return QAL_ERR_UNSUPPORTED;
+  if (d != 8 && d != 64) return QAL_ERR_UNSUPPORTED;
   if (batch < 1) return QAL_ERR_EMPTY;
   if (n_ctrl < 0 || n_ctrl > QAL_MAX_CTRL || n_cops < 0) return QAL_ERR_DIM;
   if (!H0 || !L0) return QAL_ERR_NULL;
   if (n_ctrl > 0 && (!Hc || !Lc)) return QAL_ERR_NULL;
   if (n_cops > 0 && !C) return QAL_ERR_NULL;
   if (want_comm && (n_ctrl < 1 || !Lcomm)) return n_ctrl < 1 ? QAL_ERR_DIM : QAL_ERR_NULL;
+  if (d == 64) {
+    if (want_comm) return QAL_ERR_UNSUPPORTED;
+    return cuda_rc(launch_dense_liouvillian(batch, D2(H0), n_ctrl, D2(Hc), n_cops, D2(C), D2(L0), D2(Lc),
+                                            S(stream)));
+  }
   cudaError_t e = launch_liouvillian(batch, D2(H0), n_ctrl, D2(Hc), n_cops, D2(C), D2(L0), D2(Lc), S(stream));
   if (e != cudaSuccess) return QAL_ERR_CUDA;
   if (want_comm) e = launch_commutators(batch, n_ctrl, D2(L0), D2(Lc), D2(Lcomm), S(stream));
@@ -222,17 +278,31 @@ int qal_magnus_expm_slices(int n, int batch, int n_slices, double T, int k0, int
                            long long L0_batch_stride, const qal_c128* Lc, const qal_c128* Lcomm,
                            long long Lcomm_batch_stride, qal_c128* U_out, int chunk, qal_c128* chunk_prod,
                            int* status, void* ws, size_t ws_bytes, void* stream) {
-  (void)ws;
-  (void)ws_bytes;
   launch_counter() = 0;
   Common c;
-  int rc = check_basis(n == 64, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0, L0_batch_stride, Lc,
-                       Lcomm, Lcomm_batch_stride, c);
+  int rc = check_basis(n == 64 || n == 4096, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0,
+                       L0_batch_stride, Lc, Lcomm, Lcomm_batch_stride, c, n == 4096);
   if (rc != QAL_OK) return rc;
   if (count < 1) return QAL_ERR_EMPTY;
   if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
   if (!U_out && !chunk_prod) return QAL_ERR_NULL;
   if (chunk < 1 || count % chunk != 0) return QAL_ERR_DIM;
+  if (n == 4096) {
+    if (ctrl_mode != QAL_CTRL_PWC) return QAL_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < dense_expm_ws_bytes()) return QAL_ERR_WORKSPACE;
+    if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, S(stream)) != cudaSuccess) return QAL_ERR_CUDA;
+    for (int b = 0; b < batch; ++b) {
+      cudaError_t e = launch_dense_expm_fold(
+          D2(L0) + (size_t)b * L0_batch_stride, D2(Lc), n_ctrl, u + (size_t)b * count * n_ctrl, count, c.G.h,
+          chunk_prod ? chunk : count, chunk_prod ? D2(chunk_prod) + (size_t)b * (count / chunk) * BIG : nullptr,
+          U_out ? D2(U_out) + (size_t)b * count * BIG : nullptr, status ? status + b : nullptr,
+          reinterpret_cast<double*>(ws), nullptr, S(stream));
+      if (e != cudaSuccess) return QAL_ERR_CUDA;
+    }
+    return QAL_OK;
+  }
+  (void)ws;
+  (void)ws_bytes;
   c.G.count = count;
   FwdOut O;
   O.U_nat = D2(U_out);
@@ -248,9 +318,14 @@ int qal_magnus_expm_slices(int n, int batch, int n_slices, double T, int k0, int
 int qal_ordered_product(int n, int batch, int count, const qal_c128* U, qal_c128* out, void* ws, size_t ws_bytes,
                         void* stream) {
   launch_counter() = 0;
-  if (n != 64) return QAL_ERR_UNSUPPORTED;
+  if (n != 64 && n != 4096) return QAL_ERR_UNSUPPORTED;
   if (batch < 1 || count < 1) return QAL_ERR_EMPTY;
   if (!U || !out) return QAL_ERR_NULL;
+  if (n == 4096) {
+    const size_t needd = dense_tree_ws_bytes(batch, count);
+    if (count > 1 && (!ws || ws_bytes < needd)) return QAL_ERR_WORKSPACE;
+    return run_dense_tree(batch, count, D2(U), D2(out), ws, S(stream));
+  }
   const size_t need = tree_ws_bytes(batch, count);
   if (need > 0 && (!ws || ws_bytes < need)) return QAL_ERR_WORKSPACE;
   return run_tree(batch, count, D2(U), D2(out), ws, S(stream));
@@ -258,9 +333,10 @@ int qal_ordered_product(int n, int batch, int count, const qal_c128* U, qal_c128
 
 int qal_fidelity(int d, int batch, const qal_c128* Lambda, const qal_c128* V, double* F, void* stream) {
   launch_counter() = 0;
-  if (d != 8) return QAL_ERR_UNSUPPORTED;
+  if (d != 8 && d != 64) return QAL_ERR_UNSUPPORTED;
   if (batch < 1) return QAL_ERR_EMPTY;
   if (!Lambda || !V || !F) return QAL_ERR_NULL;
+  if (d == 64) return cuda_rc(launch_dense_fidelity(batch, D2(Lambda), D2(V), F, S(stream)));
   return cuda_rc(launch_fidelity(batch, D2(Lambda), D2(V), F, S(stream)));
 }
 
@@ -270,10 +346,26 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
                       double* grad, qal_c128* Lambda, int* status, void* ws, size_t ws_bytes, void* stream) {
   launch_counter() = 0;
   Common c;
-  int rc = check_basis(d == 8, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0, L0_batch_stride, Lc,
-                       Lcomm, Lcomm_batch_stride, c);
+  int rc = check_basis(d == 8 || (d == 64 && !grad), batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0,
+                       L0_batch_stride, Lc, Lcomm, Lcomm_batch_stride, c, d == 64);
   if (rc != QAL_OK) return rc;
   if (!V || !F) return QAL_ERR_NULL;
+  if (d == 64) {   // forward only: one fold per pulse, then the fidelity
+    const size_t needd = qal_workspace_bytes(QAL_OP_FIDELITY, 4096, batch, n_slices, n_ctrl, ctrl_mode);
+    if (!ws || ws_bytes < needd) return QAL_ERR_WORKSPACE;
+    double2* lam = Lambda ? D2(Lambda)
+                          : reinterpret_cast<double2*>(reinterpret_cast<char*>(ws) + dense_expm_ws_bytes());
+    cudaStream_t st = S(stream);
+    if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+    for (int b = 0; b < batch; ++b) {
+      if (launch_dense_expm_fold(D2(L0) + (size_t)b * L0_batch_stride, D2(Lc), n_ctrl,
+                                 u + (size_t)b * n_slices * n_ctrl, n_slices, c.G.h, n_slices, lam + (size_t)b * BIG,
+                                 nullptr, status ? status + b : nullptr, reinterpret_cast<double*>(ws), nullptr,
+                                 st) != cudaSuccess)
+        return QAL_ERR_CUDA;
+    }
+    return cuda_rc(launch_dense_fidelity(batch, lam, D2(V), F, st));
+  }
   const size_t need = qal_workspace_bytes(grad ? QAL_OP_FIDELITY_GRAD : QAL_OP_FIDELITY, 64, batch, n_slices,
                                           n_ctrl, ctrl_mode);
   if (!ws || ws_bytes < need) return QAL_ERR_WORKSPACE;

@@ -1,0 +1,526 @@
+// qal_dense.cu -- K7: the same propagator for d = 64 (two exchange-only qubits, six
+// spins; superoperator n = 4096, BASELINE configs[4]).
+//
+// A 4096x4096 complex128 matrix (268 MB) is kept as a 64x64 grid of TILE IMAGES: tile
+// (I, J) is the 64 KB shared-memory image of rows 64I.., columns 64J.. (qal_dev.cuh
+// layout), stored at tile index I*64 + J.  One product C = A B runs as a persistent
+// kernel, one CTA (8 warps) per SM and one 64x64 output tile at a time; for every k-tile
+// the A tile and the B tile arrive by TMA bulk copies (A single-buffered: it is drained
+// into registers at the start of each step; B double-buffered), and the CTA issues the
+// 64x64x64 complex block product as DMMA.8x8x4 exactly like the n = 64 kernels.
+//
+// Eq. 14 per slice with Paterson-Stockmeyer degree m = 16 and s squarings chosen
+// on the DEVICE from ||Omega||_1 (a plan record), so the host never synchronises: the
+// squaring launches beyond s return immediately and the fold reads the result buffer
+// selected by the parity of s.
+#include "qal_dev.cuh"
+#include "qal_internal.h"
+
+namespace qal {
+
+constexpr int NTD = 64;                    // tiles per dimension
+constexpr int NTILES = NTD * NTD;          // 4096 tiles
+constexpr size_t DIMG = (size_t)NTILES * IMG;   // doubles per tiled matrix
+constexpr int GEMM_SMEM = 3 * IMG * 8 + 64;
+
+struct DensePlan {
+  int m, s, bad, pad;
+  double nrm;
+};
+
+__device__ __forceinline__ const double* tile_ptr(const double* M, int I, int J) {
+  return M + ((size_t)I * NTD + J) * IMG;
+}
+
+// ------------------------------------------------------------------ GEMM
+struct GemmArgs {
+  const double* A;
+  const double* A_alt;      // used instead of A when plan->s is odd (result of s squarings)
+  const double* B;
+  double* C;
+  const double* src[3];     // accumulator init: cid I + sum coef[i] src[i]
+  double coef[3];
+  double cid;
+  int nsrc;
+  int slot;                 // >= 0: active only when slot < plan->s (squarings)
+  const DensePlan* plan;
+  unsigned long long* ctr;  // profiling: +1 per executed product (or nullptr)
+};
+
+__device__ __forceinline__ void tile_coords(int t, int& I, int& J) {
+  // groups of 8 tile-rows sweep all tile-columns: the 8 A row-panels and one B column-panel
+  // in flight stay L2-resident across the 148 concurrent CTAs
+  const int grp = t / (8 * NTD);
+  const int w = t % (8 * NTD);
+  I = grp * 8 + (w % 8);
+  J = w / 8;
+}
+
+__global__ void __launch_bounds__(NT, 1) k_dense_gemm(GemmArgs g) {
+  if (g.slot >= 0 && g.slot >= g.plan->s) return;
+  const double* A = (g.A_alt && (g.plan->s & 1)) ? g.A_alt : g.A;
+  extern __shared__ __align__(128) double smem[];
+  double* SA = smem;
+  double* SB[2] = {smem + IMG, smem + 2 * IMG};
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * IMG);   // [0] = A, [1], [2] = B
+  const Lane L = lane_id();
+  int t = blockIdx.x;
+  if (t >= NTILES) return;
+  if (g.ctr && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(g.ctr, 1ull);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int I, J;
+  tile_coords(t, I, J);
+  if (threadIdx.x == 0) {
+    tma_load_img(SA, tile_ptr(A, I, 0), &bar[0]);
+    tma_load_img(SB[0], tile_ptr(g.B, 0, J), &bar[1]);
+  }
+  uint32_t phA = 0, phB[2] = {0, 0};
+  int step = 0;
+  Strip a, acc;
+  for (; t < NTILES; t += gridDim.x) {
+    tile_coords(t, I, J);
+    zero(acc);
+    for (int q = 0; q < g.nsrc; ++q) {
+      Strip x;
+      load_img(x, tile_ptr(g.src[q], I, J), L);
+      const double c = g.coef[q];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) { acc.re[i] = fma(c, x.re[i], acc.re[i]); acc.im[i] = fma(c, x.im[i], acc.im[i]); }
+    }
+    if (I == J && g.cid != 0.0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (is_diag(L, i)) acc.re[i] += g.cid;
+    }
+    for (int K = 0; K < NTD; ++K, ++step) {
+      const int cur = step & 1;
+      mbar_wait(&bar[0], phA);
+      phA ^= 1;
+      mbar_wait(&bar[1 + cur], phB[cur]);
+      phB[cur] ^= 1;
+      load_img(a, SA, L);
+      __syncthreads();  // SA drained by every warp; SB[cur^1] no longer read (previous step done)
+      if (threadIdx.x == 0) {
+        int tn = t, Kn = K + 1;
+        if (Kn == NTD) { tn = t + gridDim.x; Kn = 0; }
+        if (tn < NTILES) {
+          int In, Jn;
+          tile_coords(tn, In, Jn);
+          fence_proxy_async();
+          tma_load_img(SA, tile_ptr(A, In, Kn), &bar[0]);
+          tma_load_img(SB[cur ^ 1], tile_ptr(g.B, Kn, Jn), &bar[1 + (cur ^ 1)]);
+        }
+      }
+      mma_acc(acc, a, SB[cur], L);
+    }
+    store_img(g.C + ((size_t)I * NTD + J) * IMG, acc, L);
+  }
+}
+
+// ------------------------------------------------------------------ elementwise
+// logical (row, col, plane) of flat index e of a tiled matrix
+__device__ __forceinline__ bool dense_is_diag_re(size_t e) {
+  const size_t tile = e / IMG;
+  const int within = (int)(e % IMG);
+  if (within >= PLANE) return false;  // imaginary plane
+  const int I = (int)(tile / NTD), J = (int)(tile % NTD);
+  if (I != J) return false;
+  const int r = within >> 6, pc = (within & 63) ^ ((r & 1) << 3);
+  const int p = pc & 7;
+  const int c = (pc & ~7) | (4 * (p & 1) + (p >> 1));
+  return r == c;
+}
+
+// out = cid I + sum_q coef[q] src[q]   (flat over both planes)
+struct ComboArgs {
+  const double* src[5];
+  double coef[5];
+  int nsrc;
+  double cid;
+  double* out;
+};
+__global__ void __launch_bounds__(NT) k_dense_combo(ComboArgs g) {
+  const size_t stride = (size_t)gridDim.x * NT;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < DIMG; e += stride) {
+    double v = 0.0;
+    for (int q = 0; q < g.nsrc; ++q) v = fma(g.coef[q], g.src[q][e], v);
+    if (g.cid != 0.0 && dense_is_diag_re(e)) v += g.cid;
+    g.out[e] = v;
+  }
+}
+
+// X = h (L0 + sum_j u_j L_j) from natural-layout basis into tile images (a3 for PWC; the
+// order-4 commutator term vanishes identically when the two node values coincide)
+__global__ void __launch_bounds__(NT) k_dense_omega(const double2* __restrict__ L0, const double2* __restrict__ Lc,
+                                                    int J, const double* __restrict__ u, double h,
+                                                    double* __restrict__ X) {
+  __shared__ double cf[MAXJ + 1];
+  if (threadIdx.x <= J) cf[threadIdx.x] = threadIdx.x == 0 ? h : h * u[threadIdx.x - 1];
+  __syncthreads();
+  const size_t n2 = (size_t)4096 * 4096;
+  const size_t stride = (size_t)gridDim.x * NT;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < n2; e += stride) {
+    const int a = (int)(e >> 12), c = (int)(e & 4095);
+    const double2 x0 = __ldg(L0 + e);
+    double re = cf[0] * x0.x, im = cf[0] * x0.y;
+    for (int j = 0; j < J; ++j) {
+      const double2 x = __ldg(Lc + (size_t)j * n2 + e);
+      re = fma(cf[j + 1], x.x, re);
+      im = fma(cf[j + 1], x.y, im);
+    }
+    double* T = X + ((size_t)(a >> 6) * NTD + (c >> 6)) * IMG;
+    const int o = img_off(a & 63, c & 63);
+    T[o] = re;
+    T[PLANE + o] = im;
+  }
+}
+
+// column abs sums per tile row: part[I][c] = sum_{r in tile row I} |X[r][c]|
+__global__ void __launch_bounds__(64) k_dense_colsum(const double* __restrict__ X, double* __restrict__ part) {
+  const int I = blockIdx.x / NTD, J = blockIdx.x % NTD, c = threadIdx.x;
+  const double* T = X + ((size_t)I * NTD + J) * IMG;
+  double s = 0.0;
+  for (int r = 0; r < 64; ++r) {
+    const int o = img_off(r, c);
+    s += hypot(T[o], T[PLANE + o]);
+  }
+  part[(size_t)I * 4096 + J * 64 + c] = s;
+}
+
+// plan: ||X||_1 = max_c sum_I part[I][c] (fixed order); m = 16, s from theta_16 (A15)
+__global__ void __launch_bounds__(1024) k_dense_plan(const double* __restrict__ part, DensePlan* plan, int smax,
+                                                     int* status) {
+  __shared__ double red[32];
+  double m = 0.0;
+  bool nan = false;
+  for (int c = threadIdx.x; c < 4096; c += 1024) {
+    double s = 0.0;
+    for (int I = 0; I < NTD; ++I) s += part[(size_t)I * 4096 + c];
+    if (!(s == s)) nan = true;
+    m = fmax(m, s);
+  }
+  if (nan) m = __longlong_as_double(0x7ff8000000000000LL);
+  for (int off = 16; off > 0; off >>= 1) {
+    const double o = __shfl_xor_sync(0xffffffffu, m, off);
+    m = (o != o || o > m) ? o : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = red[0];
+    for (int w = 1; w < 32; ++w) v = (red[w] != red[w] || red[w] > v) ? red[w] : v;
+    int mm, s;
+    choose_ms(v, mm, s);
+    int bad = !(v <= 1e300) || s > smax;
+    if (bad) s = 0;
+    plan->m = 16;
+    plan->s = s;
+    plan->bad = bad;
+    plan->nrm = v;
+    if (bad && status) *status = -4;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_dense_scale(double* X, const DensePlan* plan) {
+  const double sc = ldexp(1.0, -plan->s);
+  if (sc == 1.0) return;
+  const size_t stride = (size_t)gridDim.x * NT;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < DIMG; e += stride) X[e] *= sc;
+}
+
+// dst = (plan->s odd ? b : a)
+__global__ void __launch_bounds__(NT) k_dense_copy_sel(double* dst, const double* a, const double* b,
+                                                       const DensePlan* plan) {
+  const double* src = (plan->s & 1) ? b : a;
+  const size_t stride = (size_t)gridDim.x * NT;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < DIMG / 2; e += stride)
+    reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(src)[e];
+}
+
+__global__ void __launch_bounds__(NT) k_dense_to_nat(const double* __restrict__ X, double2* __restrict__ M) {
+  const size_t n2 = (size_t)4096 * 4096;
+  const size_t stride = (size_t)gridDim.x * NT;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < n2; e += stride) {
+    const int a = (int)(e >> 12), c = (int)(e & 4095);
+    const double* T = X + ((size_t)(a >> 6) * NTD + (c >> 6)) * IMG;
+    const int o = img_off(a & 63, c & 63);
+    M[e] = make_double2(T[o], T[PLANE + o]);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_dense_from_nat(const double2* __restrict__ M, double* __restrict__ X) {
+  const size_t n2 = (size_t)4096 * 4096;
+  const size_t stride = (size_t)gridDim.x * NT;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < n2; e += stride) {
+    const int a = (int)(e >> 12), c = (int)(e & 4095);
+    double* T = X + ((size_t)(a >> 6) * NTD + (c >> 6)) * IMG;
+    const int o = img_off(a & 63, c & 63);
+    const double2 v = __ldg(M + e);
+    T[o] = v.x;
+    T[PLANE + o] = v.y;
+  }
+}
+
+// ------------------------------------------------------------------ d = 64 Liouvillian (Eq. 8)
+// Tile row p (64 CTAs per matrix): S = sum_c C^dag C is built in shared memory, then rows
+// a = 64 p + r are written: -i(delta_ps H[r][q] - H[s][p] delta_rq) + sum_c conj(C[p][s]) C[r][q]
+//                            - 1/2 delta_ps S[r][q] - 1/2 S[s][p] delta_rq
+__global__ void __launch_bounds__(NT) k_dense_liouv(const double2* __restrict__ H0, const double2* __restrict__ Hc,
+                                                    int ncops, const double2* __restrict__ C,
+                                                    double2* __restrict__ L0, double2* __restrict__ Lc, int yoff) {
+  extern __shared__ __align__(16) double2 S[];   // 64 x 64
+  const int p = blockIdx.x, y = blockIdx.y + yoff, b = blockIdx.z;
+  const bool drift = (y == 0);
+  const double2* H = drift ? H0 + (size_t)b * 4096 : Hc + (size_t)(y - 1) * 4096;
+  double2* out = drift ? L0 + (size_t)b * 4096 * 4096 : Lc + (size_t)(y - 1) * 4096 * 4096;
+  if (drift) {
+    for (int e = threadIdx.x; e < 4096; e += NT) {
+      const int r = e >> 6, q = e & 63;
+      double sr = 0.0, si = 0.0;
+      for (int cc = 0; cc < ncops; ++cc) {
+        const double2* Cc = C + (size_t)cc * 4096;
+        for (int mm = 0; mm < 64; ++mm) {
+          const double2 x = __ldg(Cc + mm * 64 + r), z = __ldg(Cc + mm * 64 + q);
+          sr += x.x * z.x + x.y * z.y;
+          si += x.x * z.y - x.y * z.x;
+        }
+      }
+      S[e] = make_double2(sr, si);
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < 64 * 4096; e += NT) {
+    const int r = e >> 12, c = e & 4095;
+    const int s = c >> 6, q = c & 63;
+    double hr = 0.0, hi = 0.0;
+    if (p == s) { const double2 v = __ldg(H + r * 64 + q); hr += v.x; hi += v.y; }
+    if (r == q) { const double2 v = __ldg(H + s * 64 + p); hr -= v.x; hi -= v.y; }
+    double vr = hi, vi = -hr;
+    if (drift) {
+      for (int cc = 0; cc < ncops; ++cc) {
+        const double2 cps = __ldg(C + (size_t)cc * 4096 + p * 64 + s);
+        const double2 crq = __ldg(C + (size_t)cc * 4096 + r * 64 + q);
+        vr += cps.x * crq.x + cps.y * crq.y;
+        vi += cps.x * crq.y - cps.y * crq.x;
+      }
+      if (p == s) { vr -= 0.5 * S[r * 64 + q].x; vi -= 0.5 * S[r * 64 + q].y; }
+      if (r == q) { vr -= 0.5 * S[s * 64 + p].x; vi -= 0.5 * S[s * 64 + p].y; }
+    }
+    out[(size_t)(p * 64 + r) * 4096 + c] = make_double2(vr, vi);
+  }
+}
+
+// ------------------------------------------------------------------ d = 64 fidelity (A8)
+// part[j] = sum_{i,k,l} V[j][l] conj(V[i][k]) Lambda[i + 64 j][k + 64 l]   (row block j)
+__global__ void __launch_bounds__(NT) k_dense_fid_part(const double2* __restrict__ Lam, const double2* __restrict__ V,
+                                                       double* __restrict__ part) {
+  __shared__ double red[16];
+  const Lane L = lane_id();
+  const int j = blockIdx.x, b = blockIdx.y;
+  const double2* M = Lam + (size_t)b * 4096 * 4096;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < 64 * 4096; e += NT) {
+    const int i = e >> 12, c = e & 4095, k = c & 63, l = c >> 6;
+    const double2 vjl = __ldg(V + j * 64 + l), vik = __ldg(V + i * 64 + k);
+    const double2 x = __ldg(M + (size_t)(i + 64 * j) * 4096 + c);
+    const double wr = vjl.x * vik.x + vjl.y * vik.y, wi = vjl.y * vik.x - vjl.x * vik.y;
+    acc += wr * x.x - wi * x.y;
+  }
+  const double s = block_sum(acc, red, L);
+  if (threadIdx.x == 0) part[(size_t)b * 64 + j] = s;
+}
+__global__ void __launch_bounds__(1024) k_dense_fid_1cta(const double2* __restrict__ Lam,
+                                                         const double2* __restrict__ V, double* __restrict__ F) {
+  __shared__ double red[40];
+  const double2* M = Lam + (size_t)blockIdx.x * 4096 * 4096;
+  double acc = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)4096 * 4096; e += 1024) {
+    const int a = (int)(e >> 12), c = (int)(e & 4095);
+    const int i = a & 63, j = a >> 6, k = c & 63, l = c >> 6;
+    const double2 vjl = __ldg(V + j * 64 + l), vik = __ldg(V + i * 64 + k), x = __ldg(M + e);
+    const double wr = vjl.x * vik.x + vjl.y * vik.y, wi = vjl.y * vik.x - vjl.x * vik.y;
+    acc += wr * x.x - wi * x.y;
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 32; ++w) s += red[w];
+    F[blockIdx.x] = s / 4096.0;
+  }
+}
+__global__ void k_dense_fid_final(const double* __restrict__ part, double* __restrict__ F) {
+  double s = 0.0;
+  for (int j = 0; j < 64; ++j) s += part[(size_t)blockIdx.x * 64 + j];
+  F[blockIdx.x] = s / 4096.0;
+}
+
+// ------------------------------------------------------------------ host launchers
+namespace {
+int grid_ew() { return 4 * num_sms(); }
+}  // namespace
+
+size_t dense_expm_ws_bytes() { return 8 * DIMG * 8 + (size_t)NTD * 4096 * 8 + 256; }
+
+static cudaError_t gemm(const GemmArgs& g0, cudaStream_t st) {
+  GemmArgs g = g0;
+  g.ctr = prof_counter(ST_DENSE_GEMM);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prof_pre(ST_DENSE_GEMM, st);
+  k_dense_gemm<<<num_sms(), NT, GEMM_SMEM, st>>>(g);
+  prof_post(ST_DENSE_GEMM, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t dense_gemm_plain(const double* A, const double* B, double* C, cudaStream_t st) {
+  GemmArgs g{};
+  g.A = A;
+  g.B = B;
+  g.C = C;
+  g.slot = -1;
+  return gemm(g, st);
+}
+
+// Propagator of `count` PWC slices for one pulse: chunk folds -> chunk_nat (natural).
+cudaError_t launch_dense_expm_fold(const double2* L0, const double2* Lc, int J, const double* u, int count,
+                                   double h, int chunk, double2* chunk_nat, double2* U_nat, int* status,
+                                   double* ws, unsigned long long* nprod_host, cudaStream_t st) {
+  double* X = ws;
+  double* X2 = X + DIMG;
+  double* X3 = X2 + DIMG;
+  double* X4 = X3 + DIMG;
+  double* T0 = X4 + DIMG;
+  double* T1 = T0 + DIMG;
+  double* P[2] = {T1 + DIMG, T1 + 2 * DIMG};
+  double* part = T1 + 3 * DIMG;
+  DensePlan* plan = reinterpret_cast<DensePlan*>(part + (size_t)NTD * 4096);
+  constexpr int SMAX = 8;
+  int pc = 0;
+  cudaError_t e = cudaSuccess;
+  for (int k = 0; k < count && e == cudaSuccess; ++k) {
+    k_dense_omega<<<grid_ew(), NT, 0, st>>>(L0, Lc, J, u + (size_t)k * J, h, X);
+    k_dense_colsum<<<NTILES, 64, 0, st>>>(X, part);
+    k_dense_plan<<<1, 1024, 0, st>>>(part, plan, SMAX, status);
+    k_dense_scale<<<grid_ew(), NT, 0, st>>>(X, plan);
+    launch_counter() += 4;
+    if ((e = dense_gemm_plain(X, X, X2, st)) != cudaSuccess) break;
+    if ((e = dense_gemm_plain(X2, X, X3, st)) != cudaSuccess) break;
+    if ((e = dense_gemm_plain(X3, X, X4, st)) != cudaSuccess) break;
+    // H = B3 + c16 X^4 (B_i = c_{4i} I + c_{4i+1} X + c_{4i+2} X^2 + c_{4i+3} X^3)
+    static const double ifac[17] = {1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333,
+                                    0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05,
+                                    2.7557319223985893e-06, 2.755731922398589e-07, 2.505210838544172e-08,
+                                    2.08767569878681e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,
+                                    7.647163731819816e-13, 4.779477332387385e-14};
+    ComboArgs cb{};
+    cb.src[0] = X; cb.src[1] = X2; cb.src[2] = X3; cb.src[3] = X4;
+    cb.coef[0] = ifac[13]; cb.coef[1] = ifac[14]; cb.coef[2] = ifac[15]; cb.coef[3] = ifac[16];
+    cb.nsrc = 4;
+    cb.cid = ifac[12];
+    cb.out = T0;
+    k_dense_combo<<<grid_ew(), NT, 0, st>>>(cb);
+    ++launch_counter();
+    double* Hin = T0;
+    double* Hout = T1;
+    for (int blk = 2; blk >= 0; --blk) {   // H <- B_blk + H X^4
+      GemmArgs g{};
+      g.A = Hin; g.B = X4; g.C = Hout; g.slot = -1;
+      g.src[0] = X; g.src[1] = X2; g.src[2] = X3;
+      g.coef[0] = ifac[4 * blk + 1]; g.coef[1] = ifac[4 * blk + 2]; g.coef[2] = ifac[4 * blk + 3];
+      g.nsrc = 3;
+      g.cid = ifac[4 * blk];
+      if ((e = gemm(g, st)) != cudaSuccess) break;
+      double* tmp = Hin; Hin = Hout; Hout = tmp;
+    }
+    if (e != cudaSuccess) break;
+    // U in Hin (= T1).  Squarings: slot q reads E[q&1], writes E[(q+1)&1] with E = {T1, T0}
+    double* E[2] = {Hin, Hout};
+    for (int q = 0; q < SMAX; ++q) {
+      GemmArgs g{};
+      g.A = E[q & 1]; g.B = E[q & 1]; g.C = E[(q + 1) & 1]; g.slot = q; g.plan = plan;
+      if ((e = gemm(g, st)) != cudaSuccess) break;
+    }
+    if (e != cudaSuccess) break;
+    // U = E[s & 1]
+    if (U_nat) {
+      k_dense_copy_sel<<<grid_ew(), NT, 0, st>>>(X, E[0], E[1], plan);
+      k_dense_to_nat<<<grid_ew(), NT, 0, st>>>(X, U_nat + (size_t)k * 4096 * 4096);
+      launch_counter() += 2;
+    }
+    if (chunk_nat) {
+      if (k % chunk == 0) {
+        k_dense_copy_sel<<<grid_ew(), NT, 0, st>>>(P[pc], E[0], E[1], plan);
+        ++launch_counter();
+      } else {
+        GemmArgs g{};
+        g.A = E[0]; g.A_alt = E[1]; g.B = P[pc]; g.C = P[pc ^ 1]; g.slot = -1; g.plan = plan;
+        if ((e = gemm(g, st)) != cudaSuccess) break;
+        pc ^= 1;
+      }
+      if (k % chunk == chunk - 1) {
+        k_dense_to_nat<<<grid_ew(), NT, 0, st>>>(P[pc], chunk_nat + (size_t)(k / chunk) * 4096 * 4096);
+        ++launch_counter();
+      }
+    }
+    e = cudaGetLastError();
+  }
+  (void)nprod_host;
+  return e;
+}
+
+cudaError_t launch_dense_tree_pair(const double2* Alater, const double2* Bearlier, double2* out, double* ws,
+                                   cudaStream_t st) {
+  double* TA = ws;
+  double* TB = ws + DIMG;
+  double* TC = ws + 2 * DIMG;
+  k_dense_from_nat<<<grid_ew(), NT, 0, st>>>(Alater, TA);
+  k_dense_from_nat<<<grid_ew(), NT, 0, st>>>(Bearlier, TB);
+  launch_counter() += 2;
+  cudaError_t e = dense_gemm_plain(TA, TB, TC, st);
+  if (e != cudaSuccess) return e;
+  k_dense_to_nat<<<grid_ew(), NT, 0, st>>>(TC, out);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops,
+                                     const double2* C, double2* L0, double2* Lc, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_liouv, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prof_pre(ST_LIOUV, st);
+  k_dense_liouv<<<dim3(64, 1, batch), NT, 4096 * 16, st>>>(H0, Hc, ncops, C, L0, Lc, 0);
+  prof_post(ST_LIOUV, st);
+  ++launch_counter();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || J == 0) return e;
+  k_dense_liouv<<<dim3(64, J, 1), NT, 4096 * 16, st>>>(H0, Hc, ncops, C, L0, Lc, 1);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st) {
+  prof_pre(ST_FID, st);
+  k_dense_fid_1cta<<<batch, 1024, 0, st>>>(Lam, V, F);
+  prof_post(ST_FID, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+}  // namespace qal

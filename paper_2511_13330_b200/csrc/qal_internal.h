@@ -41,7 +41,7 @@ int num_sms();
 int& launch_counter();
 
 // profiling window (qal_profile_begin/end): stage ids as in qal.h
-enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, NSTAGE };
+enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, ST_DENSE_GEMM, NSTAGE };
 unsigned long long* prof_counter(int stage);   // device counter slot or nullptr
 void prof_pre(int stage, cudaStream_t st);      // record start event (no-op when off)
 void prof_post(int stage, cudaStream_t st);     // record end event
@@ -65,6 +65,16 @@ cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, co
 size_t grad_scratch_bytes();
 cudaError_t launch_sample_sines(int J, int nterm, const double* prm, double umax, double h, int k0, int count,
                                double* out, cudaStream_t st);
+// n = 4096 (d = 64) dense path, qal_dense.cu
+size_t dense_expm_ws_bytes();
+cudaError_t launch_dense_expm_fold(const double2* L0, const double2* Lc, int J, const double* u, int count,
+                                   double h, int chunk, double2* chunk_nat, double2* U_nat, int* status,
+                                   double* ws, unsigned long long* nprod_host, cudaStream_t st);
+cudaError_t launch_dense_tree_pair(const double2* Alater, const double2* Bearlier, double2* out, double* ws,
+                                   cudaStream_t st);
+cudaError_t launch_dense_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops,
+                                     const double2* C, double2* L0, double2* Lc, cudaStream_t st);
+cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st);
 cudaError_t launch_fp64_probe(int kind, int blocks, int iters, double* sink, cudaStream_t st);
 
 }  // namespace qal

@@ -21,12 +21,13 @@ QAL_CTRL_NODES = 1
 QAL_OP_ORDERED_PRODUCT = 1
 QAL_OP_FIDELITY = 2
 QAL_OP_FIDELITY_GRAD = 3
+QAL_OP_EXPM_SLICES = 4
 QAL_MAX_CTRL = 8
 STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
-          "grad_slices"]
+          "grad_slices", "dense_gemm"]
 KERNELS = {"liouvillian": "k_liouvillian", "commutators": "k_commutators", "expm_fold": "k_expm_fold",
            "tree": "k_tree_level", "fidelity": "k_fidelity", "prefix_chain": "k_prefix_chain",
-           "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices"}
+           "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices", "dense_gemm": "k_dense_gemm"}
 
 _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
@@ -171,9 +172,11 @@ def qal_magnus_expm_slices(L0, Lc, u, T, n_slices, *, k0=0, count=None, magnus_o
     if Lcomm is not None:
         Lcomm = _dev(Lcomm, c128, "Lcomm")
         Lcs = 0 if Lcomm.shape[0] == 1 else n_comm(J) * n * n
+    wsb = workspace_bytes(QAL_OP_EXPM_SLICES, n, B, count)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev) if wsb else None
     rc = load().qal_magnus_expm_slices(n, B, n_slices, float(T), k0, count, magnus_order, ctrl_mode, J, _ptr(u),
                                        _ptr(L0), L0s, _ptr(Lc), _ptr(Lcomm), Lcs, _ptr(U),
-                                       1 if chunk is None else chunk, _ptr(P), _ptr(status), None, 0,
+                                       1 if chunk is None else chunk, _ptr(P), _ptr(status), _ptr(ws), wsb,
                                        _stream(stream))
     _check(rc, "qal_magnus_expm_slices")
     return U, P

@@ -398,3 +398,38 @@ def test_sines_controls_clip_and_nodes(oracle):
     k = 7
     assert np.allclose(nodes[k, 0], oracle.sines_eval(prm, qi.U_MAX, k * h + (0.5 - math.sqrt(3) / 6) * h))
     assert np.allclose(nodes[k, 1], oracle.sines_eval(prm, qi.U_MAX, k * h + (0.5 + math.sqrt(3) / 6) * h))
+
+
+# ---------------------------------------------------------------- helpers used by the d = 64 checks
+def test_matmul_rows_is_the_matrix_product(oracle):
+    rng = np.random.default_rng(11)
+    A = rand_c(rng, 96, 96)
+    B = rand_c(rng, 96, 96)
+    got = oracle.matmul_rows(A, B, 17, 29)
+    assert np.allclose(got, (A @ B)[17:29], rtol=0, atol=1e-12)
+
+
+def test_evolve_rho_t1_decay_closed_form(oracle):
+    """P-6(ii) on the density-matrix integrator: rho_upup(t) = e^{-t/T1}."""
+    T1 = 7.0
+    p = qi.single_spin("t1", T=5.0, N=5, t1=T1)
+    rho0 = np.array([[1, 0], [0, 0]], dtype=np.complex128)
+    rho = oracle.evolve_rho(p.H0[0], p.Hc, p.C, p.u[0], p.T, p.N, 64, rho0)
+    assert abs(rho[0, 0] - math.exp(-5.0 / T1)) <= 1e-12
+    assert abs(np.trace(rho) - 1.0) <= 1e-14
+
+
+def test_evolve_rho_matches_solve_ivp_d8(oracle):
+    """Eq. 6 with PWC controls on the 3-spin model vs scipy's adaptive integrator."""
+    p = qi.cfg0(N=4, T=100.0 * 4 / 256)
+    rng = np.random.default_rng(5)
+    rho0 = rand_rho(rng, 8)
+    got = oracle.evolve_rho(p.H0[0], p.Hc, p.C, p.u[0], p.T, p.N, 256, rho0)
+    h = p.T / p.N
+    rho = rho0.copy()
+    for k in range(p.N):
+        H = p.H0[0] + sum(p.u[0, k, j] * p.Hc[j] for j in range(2))
+        f = lambda t, y, H=H: eq6_numpy(H, p.C, y.reshape(8, 8)).reshape(-1)  # noqa: E731
+        sol = scipy.integrate.solve_ivp(f, (0.0, h), rho.reshape(-1), method="DOP853", rtol=1e-13, atol=1e-15)
+        rho = sol.y[:, -1].reshape(8, 8)
+    assert np.max(np.abs(got - rho)) <= 1e-13
