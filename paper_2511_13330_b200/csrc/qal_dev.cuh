@@ -73,7 +73,6 @@ __device__ __forceinline__ void copy(Strip& d, const Strip& s) {
 
 // strip <-> image (shared or global; generic pointers, 16-byte accesses)
 __device__ __forceinline__ void load_img(Strip& s, const double* __restrict__ img, const Lane& L) {
-  QAL_FENCE();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int o = pair_off(L, j);
@@ -92,9 +91,21 @@ __device__ __forceinline__ void store_img(double* __restrict__ img, const Strip&
   }
 }
 
+// img <- x + a * y (strip-wise, no temporary strip)
+__device__ __forceinline__ void store_img_axpy(double* __restrict__ img, const Strip& x, double a, const Strip& y,
+                                               const Lane& L) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int o = pair_off(L, j);
+    *reinterpret_cast<double2*>(img + o) =
+        make_double2(fma(a, y.re[2 * j], x.re[2 * j]), fma(a, y.re[2 * j + 1], x.re[2 * j + 1]));
+    *reinterpret_cast<double2*>(img + PLANE + o) =
+        make_double2(fma(a, y.im[2 * j], x.im[2 * j]), fma(a, y.im[2 * j + 1], x.im[2 * j + 1]));
+  }
+}
+
 // strip <-> natural row-major complex128 matrix in global memory
 __device__ __forceinline__ void load_nat(Strip& s, const double2* __restrict__ M, const Lane& L) {
-  QAL_FENCE();
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     double2 v = __ldg(M + L.r * 64 + 4 * i + L.t);
@@ -127,6 +138,10 @@ __device__ __forceinline__ void block_img_copy(double* __restrict__ dst, const d
 
 __device__ __forceinline__ bool is_diag(const Lane& L, int i) { return L.r == 4 * i + L.t; }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // ---------------------------------------------------------------- FP64 tensor core
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -135,33 +150,53 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // acc += A * B, A = strip (registers, A-fragment layout), B = shared image.
+// B fragments are fetched one k-step ahead with volatile shared loads (explicit 2-stage
+// software pipeline, 32 registers): ptxas keeps them in program order instead of hoisting
+// the whole 256-load stream and spilling (the kernels run at 255 registers).
+__device__ __forceinline__ double lds_v(uint32_t a) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void mma_acc(Strip& acc, const Strip& a, const double* __restrict__ Bs,
                                         const Lane& L) {
   const int todd = L.t & 1;
   // row 4q+t of B; physical tile of output tile j is j ^ (t & 1)
-  const double* bE = Bs + L.t * 64 + L.g + 8 * todd;  // even j: tile j + todd
-  const double* bO = Bs + L.t * 64 + L.g - 8 * todd;  // odd  j: tile j - todd
+  const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);  // even j: tile j + todd
+  const uint32_t bO = smem_u32(Bs + L.t * 64 + L.g - 8 * todd);  // odd  j: tile j - todd
+  double br[2][8], bi[2][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t p = ((j & 1) ? bO : bE) + 8u * (8 * j);
+    br[0][j] = lds_v(p);
+    bi[0][j] = lds_v(p + 8u * PLANE);
+  }
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
+    const int cur = q & 1;
+    if (q + 1 < 16) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t p = ((j & 1) ? bO : bE) + 8u * ((q + 1) * 256 + 8 * j);
+        br[cur ^ 1][j] = lds_v(p);
+        bi[cur ^ 1][j] = lds_v(p + 8u * PLANE);
+      }
+    }
     const double ar = a.re[q], ai = a.im[q], nai = -a.im[q];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const double* p = ((j & 1) ? bO : bE) + q * 256 + 8 * j;
-      const double br = p[0], bi = p[PLANE];
-      dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br);
-      dmma(acc.re[2 * j], acc.re[2 * j + 1], nai, bi);
-      dmma(acc.im[2 * j], acc.im[2 * j + 1], ar, bi);
-      dmma(acc.im[2 * j], acc.im[2 * j + 1], ai, br);
+      dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br[cur][j]);
+      dmma(acc.re[2 * j], acc.re[2 * j + 1], nai, bi[cur][j]);
+      dmma(acc.im[2 * j], acc.im[2 * j + 1], ar, bi[cur][j]);
+      dmma(acc.im[2 * j], acc.im[2 * j + 1], ai, br[cur][j]);
     }
   }
+  QAL_FENCE();
 }
 
 // ---------------------------------------------------------------- Tensor Memory scratch
 // 512 columns x 128 lanes x 32 bit.  Warp w reaches lanes 32(w%4)..+31; warps w and
 // w+4 use different column halves.  Slot s (0..3) of a warp: 64 columns (re 32, im 32).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 __device__ __forceinline__ void tmem_alloc512(uint32_t* slot_smem) {
   // whole warp 0 executes
@@ -218,7 +253,6 @@ __device__ __forceinline__ void tmem_store_half(uint32_t addr, const double (&x)
   tmem_st32(addr, v);
 }
 __device__ __forceinline__ void tmem_load_half(uint32_t addr, double (&x)[16]) {
-  QAL_FENCE();
   uint32_t v[32];
   tmem_ld32(addr, v);
   tmem_wait_ld();
@@ -231,15 +265,17 @@ __device__ __forceinline__ void tmem_store(uint32_t addr, const Strip& s) {
   tmem_wait_st();
 }
 
-// acc += a * M  where M is a strip parked in TMEM (loaded in halves to bound registers)
+// acc += a * M  where M is a strip parked in TMEM (both halves in flight, one wait)
 __device__ __forceinline__ void tmem_axpy(Strip& acc, double a, uint32_t addr) {
-  double x[16];
-  tmem_load_half(addr, x);
+  uint32_t v[32], w[32];
+  tmem_ld32(addr, v);
+  tmem_ld32(addr + 32, w);
+  tmem_wait_ld();
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc.re[i] = fma(a, x[i], acc.re[i]);
-  tmem_load_half(addr + 32, x);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) acc.im[i] = fma(a, x[i], acc.im[i]);
+  for (int i = 0; i < 16; ++i) {
+    acc.re[i] = fma(a, __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i])), acc.re[i]);
+    acc.im[i] = fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[i]);
+  }
 }
 
 // ---------------------------------------------------------------- TMA bulk copies

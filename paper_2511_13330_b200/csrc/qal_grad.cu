@@ -23,7 +23,7 @@ namespace qal {
 
 constexpr int CHAIN_SMEM_BYTES = 3 * IMG * 8 + 64;
 constexpr int GRAD_SMEM_BYTES = 3 * IMG * 8 + (8 * 64 + 16) * 8 + 64;
-constexpr int GRAD_SCRATCH_STRIPS = 4;
+constexpr int GRAD_SCRATCH_STRIPS = 6;
 constexpr int QAL_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;   // traces per slice (<= 44)
 static_assert(9 * QAL_TR_MAX <= 8 * 64 + 16, "trace reduction buffer");
 
@@ -134,134 +134,214 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
                                                        const double* __restrict__ X_img, double* __restrict__ grad,
                                                        int* __restrict__ status, double* __restrict__ scratch,
                                                        unsigned long long* ctr) {
+  // Dual-number evaluation of the forward Taylor scheme (T8 / T18 + s squarings) at X = Omega/2^s
+  // in the direction dX = G/2^s: every product (P, dP)(Q, dQ) = (PQ, dP Q + P dQ) with the
+  // right factors Q, dQ as shared images (SV = values, SD = derivatives) and the left factors
+  // as strips (TMEM slots / L2 scratch).  The result dE is W = L_exp(Omega, G).
   extern __shared__ __align__(128) double smem[];
-  double* S1 = smem;            // X_{k+1}, then dX = G / 2^s, then dX^4, then dE
-  double* S2 = smem + IMG;      // X = Omega / 2^s
-  double* S3 = smem + 2 * IMG;  // X^4, then E (squarings)
+  double* SD = smem;            // P_k (TMA), then dX, dA3 / dW, dB5 / dR, dA9, dE
+  double* SV = smem + IMG;      // X, A3 / W, B5 / R, A9, E
+  double* SN = smem + 2 * IMG;  // X_{k+1} of this item (TMA, prefetched during the previous item)
   double* red = smem + 3 * IMG;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 8 * 64 + 16);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 8 * 64 + 16);   // [0] = P_k -> SD, [1] = X_{k+1} -> SN
   __shared__ uint32_t tmem_base_sh;
   const Lane L = lane_id();
   if (L.w == 0) tmem_alloc512(&tmem_base_sh);
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tm = tmem_slot_addr(tmem_base_sh, L, 0);   // slots: X^2, X^3, dX^2, dX^3
+  const uint32_t tm = tmem_slot_addr(tmem_base_sh, L, 0);
+  const uint32_t T0 = tm, T1 = tm + 128, T2 = tm + 256, T3 = tm + 384;   // A2, dA2, A3|Y, dA3|dY
   double* scr = scratch + (size_t)blockIdx.x * GRAD_SCRATCH_STRIPS * IMG;
-  double* sX = scr;             // strips parked in global (L2): X, dX, H, dH
-  double* sdX = scr + IMG;
-  double* sH = scr + 2 * IMG;
-  double* sdH = scr + 3 * IMG;
+  double* gX = scr;
+  double* gdX = scr + IMG;
+  double* gA6 = scr + 2 * IMG;
+  double* gdA6 = scr + 3 * IMG;
+  double* gE = scr + 4 * IMG;     // squarings only (s > 0)
+  double* gdE = scr + 5 * IMG;
   const int N = G.count;
   const int items = batch * N;
   const int K = n_traces(B);
-  uint32_t phase = 0;
+  uint32_t ph0 = 0, ph1 = 0;
   unsigned long long nprod = 0;
   Strip A, acc;
+  if (threadIdx.x == 0 && blockIdx.x < items) tma_load_img(SN, X_img + (size_t)blockIdx.x * IMG, &bar[1]);
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
-    __syncthreads();  // previous item done with S1
+    __syncthreads();  // previous item done with SD, SV
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      tma_load_img(S1, X_img + ((size_t)b * N + k) * IMG, bar);
+      tma_load_img(SD, P_img + ((size_t)b * N + k) * IMG, &bar[0]);
     }
     // X = Omega_k / 2^s
     build_omega(A, B, G, b, k, L);
     const double nrm = norm1(A, red, L);
     int m, s;
-    choose_ms(nrm, m, s);
+    choose_scheme(nrm, m, s);
     if (!(nrm <= 1e300) && threadIdx.x == 0 && status) status[b] = -4;
     const double sc = ldexp(1.0, -s);
 #pragma unroll
     for (int i = 0; i < 16; ++i) { A.re[i] *= sc; A.im[i] *= sc; }
-    store_img(S2, A, L);
-    store_img(sX, A, L);
-    // G = P_k X_{k+1}
-    load_img(A, P_img + ((size_t)b * N + k) * IMG, L);
-    mbar_wait(bar, phase);
-    phase ^= 1;
+    store_img(SV, A, L);
+    store_img(gX, A, L);
+    // G = P_k X_{k+1};  dX = G / 2^s
+    mbar_wait(&bar[0], ph0);
+    ph0 ^= 1;
+    load_img(A, SD, L);
+    mbar_wait(&bar[1], ph1);
+    ph1 ^= 1;
     zero(acc);
-    mma_acc(acc, A, S1, L);
+    mma_acc(acc, A, SN, L);
 #pragma unroll
     for (int i = 0; i < 16; ++i) { acc.re[i] *= sc; acc.im[i] *= sc; }
-    __syncthreads();  // all reads of S1 (X_{k+1}) done; S2 complete
-    store_img(S1, acc, L);
-    store_img(sdX, acc, L);
-    __syncthreads();  // dX complete
-    // powers and their derivatives
-    load_img(A, sX, L);
-    zero(acc); mma_acc(acc, A, S2, L);            // X^2
-    tmem_store(tm, acc);
-    zero(acc); mma_acc(acc, A, S1, L);            // X dX
-    load_img(A, sdX, L);
-    mma_acc(acc, A, S2, L);                       // + dX X = dX^2
-    tmem_store(tm + 256, acc);
-    tmem_load(A, tm);
-    zero(acc); mma_acc(acc, A, S2, L);            // X^3
-    tmem_store(tm + 128, acc);
-    zero(acc); mma_acc(acc, A, S1, L);            // X^2 dX
-    tmem_load(A, tm + 256);
-    mma_acc(acc, A, S2, L);                       // + dX^2 X = dX^3
-    tmem_store(tm + 384, acc);
-    tmem_load(A, tm + 128);
-    zero(acc); mma_acc(acc, A, S2, L);            // X^4
-    store_img(S3, acc, L);
-    zero(acc); mma_acc(acc, A, S1, L);            // X^3 dX
-    tmem_load(A, tm + 384);
-    mma_acc(acc, A, S2, L);                       // + dX^3 X = dX^4
-    __syncthreads();                              // all reads of S1, S2 done; S3 = X^4
-    store_img(S1, acc, L);                        // S1 = dX^4
-    // Horner with derivative: H = B_{tb-1} + c_m X^4, dH = dB_{tb-1} + c_m dX^4
-    const int tb = m / 4;
-    nprod += 1 + 3 + 6 + 3 * (tb - 1) + 3 * s;   // G, powers, their derivatives, Horner, squarings
-    const double cm = inv_fact(m);
-    ps_block(A, tb - 1, sX, tm, L);
-    load_img(acc, S3, L);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) { A.re[i] = fma(cm, acc.re[i], A.re[i]); A.im[i] = fma(cm, acc.im[i], A.im[i]); }
-    store_img(sH, A, L);
-    dps_block(A, tb - 1, sdX, tm + 256, L);
-    {
-      Strip d4;
-      load_img(d4, S1, L);  // own rows of dX^4 (written by this thread)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) { A.re[i] = fma(cm, d4.re[i], A.re[i]); A.im[i] = fma(cm, d4.im[i], A.im[i]); }
+    __syncthreads();  // reads of SD (P_k), SN (X_{k+1}) done; SV (X) complete
+    store_img(SD, acc, L);
+    store_img(gdX, acc, L);
+    __syncthreads();  // SD = dX complete
+    // (A2, dA2)
+    load_img(A, SV, L);
+    zero(acc); mma_acc(acc, A, SV, L);                 // A2 = X X
+    tmem_store(T0, acc);
+    zero(acc); mma_acc(acc, A, SD, L);                 // X dX
+    load_img(A, SD, L);
+    mma_acc(acc, A, SV, L);                            // + dX X
+    tmem_store(T1, acc);
+    int np = 1 + 1 + 2;
+    if (m == 8) {
+      // (W, dW) = c1 (X, dX) + c2 (A2, dA2) shared;  (Y, dY) = (A2, dA2)(W, dW)
+      __syncthreads();                                 // reads of SV (X), SD (dX) done
+      zero(acc); add_img(acc, c_t8[0], gX, L); add_tm(acc, c_t8[1], T0); store_img(SV, acc, L);
+      zero(acc); add_img(acc, c_t8[0], gdX, L); add_tm(acc, c_t8[1], T1); store_img(SD, acc, L);
+      __syncthreads();
+      tmem_load(A, T0);
+      zero(acc); mma_acc(acc, A, SV, L);               // Y = A2 W
+      tmem_store(T2, acc);
+      zero(acc); mma_acc(acc, A, SD, L);               // A2 dW
+      tmem_load(A, T1);
+      mma_acc(acc, A, SV, L);                          // + dA2 W = dY
+      tmem_store(T3, acc);
+      __syncthreads();                                 // reads of SV (W), SD (dW) done
+      // (R, dR) = (Y, dY) + c5 (A2, dA2) shared
+      zero(acc); add_tm(acc, 1.0, T2); add_tm(acc, c_t8[4], T0); store_img(SV, acc, L);
+      zero(acc); add_tm(acc, 1.0, T3); add_tm(acc, c_t8[4], T1); store_img(SD, acc, L);
+      __syncthreads();
+      // dT = c6 dY + c7 dA2 + dX + dL R + L dR,   L = Y + c3 A2 + c4 X
+      zero(acc);
+      add_tm(acc, c_t8[5], T3); add_tm(acc, c_t8[6], T1); add_img(acc, 1.0, gdX, L);
+      zero(A); add_tm(A, 1.0, T3); add_tm(A, c_t8[2], T1); add_img(A, c_t8[3], gdX, L);   // dL
+      mma_acc(acc, A, SV, L);
+      zero(A); add_tm(A, 1.0, T2); add_tm(A, c_t8[2], T0); add_img(A, c_t8[3], gX, L);    // L
+      mma_acc(acc, A, SD, L);
+      if (s > 0) store_img(gdE, acc, L);
+      np += 1 + 2 + 2;
+      if (s > 0) {                                     // T = c6 Y + c7 A2 + X + I + L R
+        zero(acc);
+        add_tm(acc, c_t8[5], T2); add_tm(acc, c_t8[6], T0); add_img(acc, 1.0, gX, L); add_diag(acc, 1.0, L);
+        mma_acc(acc, A, SV, L);
+        store_img(gE, acc, L);
+        ++np;
+      }
+    } else {
+      // (A3, dA3) = (A2, dA2)(X, dX)
+      tmem_load(A, T0);
+      zero(acc); mma_acc(acc, A, SV, L);               // A3
+      tmem_store(T2, acc);
+      zero(acc); mma_acc(acc, A, SD, L);               // A2 dX
+      tmem_load(A, T1);
+      mma_acc(acc, A, SV, L);                          // + dA2 X = dA3
+      tmem_store(T3, acc);
+      __syncthreads();                                 // reads of SV (X), SD (dX) done
+      tmem_load(A, T2); store_img(SV, A, L);
+      tmem_load(A, T3); store_img(SD, A, L);
+      __syncthreads();
+      // (A6, dA6) = (A3, dA3)(A3, dA3)
+      tmem_load(A, T2);
+      zero(acc); mma_acc(acc, A, SV, L);               // A6
+      store_img(gA6, acc, L);
+      zero(acc); mma_acc(acc, A, SD, L);               // A3 dA3
+      tmem_load(A, T3);
+      mma_acc(acc, A, SV, L);                          // + dA3 A3
+      store_img(gdA6, acc, L);
+      __syncthreads();                                 // reads of SV (A3), SD (dA3) done
+      // (B5, dB5) shared
+      zero(acc);
+      add_img(acc, c_t18[T18_B5][1], gX, L); add_tm(acc, c_t18[T18_B5][2], T0); add_img(acc, 1.0, gA6, L);
+      store_img(SV, acc, L);
+      zero(acc);
+      add_img(acc, c_t18[T18_B5][1], gdX, L); add_tm(acc, c_t18[T18_B5][2], T1); add_img(acc, 1.0, gdA6, L);
+      store_img(SD, acc, L);
+      __syncthreads();
+      // dA9 = dB4 + dB1 B5 + B1 dB5
+      zero(acc);
+      add_img(acc, c_t18[T18_B4][1], gdX, L); add_tm(acc, c_t18[T18_B4][2], T1);
+      add_tm(acc, c_t18[T18_B4][3], T3); add_img(acc, c_t18[T18_B4][4], gdA6, L);
+      zero(A);
+      add_img(A, c_t18[T18_B1][1], gdX, L); add_tm(A, c_t18[T18_B1][2], T1); add_tm(A, c_t18[T18_B1][3], T3);
+      mma_acc(acc, A, SV, L);
+      zero(A);
+      add_img(A, c_t18[T18_B1][1], gX, L); add_tm(A, c_t18[T18_B1][2], T0); add_tm(A, c_t18[T18_B1][3], T2);
+      mma_acc(acc, A, SD, L);
+      store_img(SN, acc, L);                           // dA9 (SN idle since G)
+      // A9 = B4 + B1 B5   (A still holds B1)
+      zero(acc);
+      add_diag(acc, c_t18[T18_B4][0], L);
+      add_img(acc, c_t18[T18_B4][1], gX, L); add_tm(acc, c_t18[T18_B4][2], T0);
+      add_tm(acc, c_t18[T18_B4][3], T2); add_img(acc, c_t18[T18_B4][4], gA6, L);
+      mma_acc(acc, A, SV, L);
+      __syncthreads();                                 // reads of SV (B5), SD (dB5) done
+      store_img(SV, acc, L);                           // A9
+      __syncthreads();                                 // A9 (SV), dA9 (SN) complete
+      // dT = dB2 + dL A9 + L dA9,  L = B3 + A9
+      zero(acc);
+      add_img(acc, c_t18[T18_B2][1], gdX, L); add_tm(acc, c_t18[T18_B2][2], T1);
+      add_tm(acc, c_t18[T18_B2][3], T3); add_img(acc, c_t18[T18_B2][4], gdA6, L);
+      load_img(A, SN, L);                              // dL = dB3 + dA9
+      add_img(A, c_t18[T18_B3][1], gdX, L); add_tm(A, c_t18[T18_B3][2], T1);
+      add_tm(A, c_t18[T18_B3][3], T3); add_img(A, c_t18[T18_B3][4], gdA6, L);
+      mma_acc(acc, A, SV, L);
+      load_img(A, SV, L);                              // L = B3 + A9
+      add_diag(A, c_t18[T18_B3][0], L);
+      add_img(A, c_t18[T18_B3][1], gX, L); add_tm(A, c_t18[T18_B3][2], T0);
+      add_tm(A, c_t18[T18_B3][3], T2); add_img(A, c_t18[T18_B3][4], gA6, L);
+      mma_acc(acc, A, SN, L);
+      if (s > 0) store_img(gdE, acc, L);
+      np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
+      if (s > 0) {                                     // T = B2 + L A9
+        zero(acc);
+        add_diag(acc, c_t18[T18_B2][0], L);
+        add_img(acc, c_t18[T18_B2][1], gX, L); add_tm(acc, c_t18[T18_B2][2], T0);
+        add_tm(acc, c_t18[T18_B2][3], T2); add_img(acc, c_t18[T18_B2][4], gA6, L);
+        mma_acc(acc, A, SV, L);
+        store_img(gE, acc, L);
+        ++np;
+      }
     }
-    store_img(sdH, A, L);
-    __syncthreads();                              // S1 = dX^4 complete
-    for (int blk = tb - 2; blk >= 0; --blk) {
-      dps_block(acc, blk, sdX, tm + 256, L);      // dH <- dB + dH X^4 + H dX^4
-      load_img(A, sdH, L);
-      mma_acc(acc, A, S3, L);
-      load_img(A, sH, L);
-      mma_acc(acc, A, S1, L);
-      store_img(sdH, acc, L);
-      ps_block(acc, blk, sX, tm, L);              // H <- B + H X^4
-      mma_acc(acc, A, S3, L);
-      store_img(sH, acc, L);
-    }
-    // squarings: E <- E^2, dE <- dE E + E dE
+    // squarings: (E, dE) <- (E E, dE E + E dE)
     for (int q = 0; q < s; ++q) {
       __syncthreads();
-      load_img(A, sH, L);
-      store_img(S3, A, L);
-      load_img(acc, sdH, L);
-      store_img(S1, acc, L);
+      load_img(A, gE, L);
+      store_img(SV, A, L);
+      load_img(acc, gdE, L);
+      store_img(SD, acc, L);
       __syncthreads();
-      zero(acc); mma_acc(acc, A, S1, L);          // E dE
-      load_img(A, sdH, L);
-      mma_acc(acc, A, S3, L);                     // + dE E
-      store_img(sdH, acc, L);
-      load_img(A, sH, L);
-      zero(acc); mma_acc(acc, A, S3, L);          // E^2
-      store_img(sH, acc, L);
+      zero(acc); mma_acc(acc, A, SD, L);               // E dE
+      load_img(A, gdE, L);
+      mma_acc(acc, A, SV, L);                          // + dE E
+      store_img(gdE, acc, L);
+      load_img(A, gE, L);
+      zero(acc); mma_acc(acc, A, SV, L);               // E E
+      store_img(gE, acc, L);
+      np += 3;
     }
+    nprod += np;
     // W = dE = L(Omega, G).  traces T_m = Re Tr(W B_m) = sum_{r,c} Re(W[r][c] B_m[c][r])
-    load_img(A, sdH, L);
+    if (s > 0) load_img(A, gdE, L);
+    else copy(A, acc);
     for (int mm = 0; mm < K; ++mm) {
       const double2* Bm = (mm < B.J) ? B.Lc + (size_t)mm * PLANE
                                      : B.Lcomm + (size_t)b * B.Lcomm_stride + (size_t)(mm - B.J) * PLANE;
@@ -276,7 +356,11 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       if (L.lane == 0) red[L.w * QAL_TR_MAX + mm] = v;
     }
-    __syncthreads();
+    __syncthreads();  // also: every product of this item is done -> SN is free
+    if (threadIdx.x == 0 && item + (int)gridDim.x < items) {
+      fence_proxy_async();
+      tma_load_img(SN, X_img + (size_t)(item + gridDim.x) * IMG, &bar[1]);   // next item's X_{k+1}
+    }
     if (threadIdx.x < K) {
       double t = 0.0;
 #pragma unroll
