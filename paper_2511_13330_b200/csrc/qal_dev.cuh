@@ -104,6 +104,44 @@ __device__ __forceinline__ void store_img_axpy(double* __restrict__ img, const S
   }
 }
 
+// ---------------------------------------------------------------- L2 residency hints
+// Per-CTA scratch strips are re-read within microseconds: keep them in L2 (evict_last);
+// the per-slice operand images are streamed once (evict_first).
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void load_img_l2(Strip& s, const double* __restrict__ img, const Lane& L, uint64_t pol) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int o = pair_off(L, j);
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(s.re[2 * j]), "=d"(s.re[2 * j + 1])
+                 : "l"(img + o), "l"(pol));
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(s.im[2 * j]), "=d"(s.im[2 * j + 1])
+                 : "l"(img + PLANE + o), "l"(pol));
+  }
+}
+__device__ __forceinline__ void store_img_l2(double* __restrict__ img, const Strip& s, const Lane& L, uint64_t pol) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int o = pair_off(L, j);
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + o), "d"(s.re[2 * j]),
+                 "d"(s.re[2 * j + 1]), "l"(pol)
+                 : "memory");
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + PLANE + o), "d"(s.im[2 * j]),
+                 "d"(s.im[2 * j + 1]), "l"(pol)
+                 : "memory");
+  }
+}
+
 // strip <-> natural row-major complex128 matrix in global memory
 __device__ __forceinline__ void load_nat(Strip& s, const double2* __restrict__ M, const Lane& L) {
 #pragma unroll
@@ -295,6 +333,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -307,6 +353,13 @@ __device__ __forceinline__ void tma_load_img(double* dst, const double* src, uin
   mbar_expect_tx(bar, IMG * 8);
 #pragma unroll
   for (int p = 0; p < 4; ++p) bulk_g2s(dst + p * (IMG / 4), src + p * (IMG / 4), IMG * 2, bar);
+}
+// same for an image that is read exactly once (streamed; L2 evict_first)
+__device__ __forceinline__ void tma_load_img_stream(double* dst, const double* src, uint64_t* bar) {
+  const uint64_t pol = l2_evict_first();
+  mbar_expect_tx(bar, IMG * 8);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) bulk_g2s_hint(dst + p * (IMG / 4), src + p * (IMG / 4), IMG * 2, bar, pol);
 }
 
 // ---------------------------------------------------------------- reductions

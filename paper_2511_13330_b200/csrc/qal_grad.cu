@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __r
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) tma_load_img(SU[0], U, &bar[0]);
+  if (threadIdx.x == 0) tma_load_img_stream(SU[0], U, &bar[0]);
   Strip A, acc;
   set_identity(A, L);
   store_img(SP, A, L);
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __r
     __syncthreads();  // SP written; buffer cur^1 (read at step k-1) is free
     if (threadIdx.x == 0 && k + 1 < N) {
       fence_proxy_async();
-      tma_load_img(SU[cur ^ 1], U + (size_t)(k + 1) * IMG, &bar[cur ^ 1]);
+      tma_load_img_stream(SU[cur ^ 1], U + (size_t)(k + 1) * IMG, &bar[cur ^ 1]);
     }
     mbar_wait(&bar[cur], ph[cur]);
     ph[cur] ^= 1;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __r
     mma_acc(acc, A, SP, L);   // U_k P_k
     __syncthreads();          // all reads of SP done
     store_img(SP, acc, L);
-    if (k + 1 < N) store_img(P + (size_t)(k + 1) * IMG, acc, L);
+    if (k + 1 < N) store_img_l2(P + (size_t)(k + 1) * IMG, acc, L, l2_evict_first());
     else store_nat(Lam + (size_t)b * PLANE, acc, L);
   }
   if (ctr && threadIdx.x == 0) atomicAdd(ctr, (unsigned long long)N);
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(NT, 1) k_suffix_chain(int N, const double* __r
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0 && N > 1) tma_load_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * IMG, &bar[(N - 1) & 1]);
+  if (threadIdx.x == 0 && N > 1) tma_load_img_stream(SU[(N - 1) & 1], U + (size_t)(N - 1) * IMG, &bar[(N - 1) & 1]);
   Strip A, acc;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
@@ -113,14 +113,14 @@ __global__ void __launch_bounds__(NT, 1) k_suffix_chain(int N, const double* __r
     __syncthreads();  // buffer cur^1 (read at step k+1) is free
     if (threadIdx.x == 0 && k - 1 >= 1) {
       fence_proxy_async();
-      tma_load_img(SU[cur ^ 1], U + (size_t)(k - 1) * IMG, &bar[cur ^ 1]);
+      tma_load_img_stream(SU[cur ^ 1], U + (size_t)(k - 1) * IMG, &bar[cur ^ 1]);
     }
     mbar_wait(&bar[cur], ph[cur]);
     ph[cur] ^= 1;
     zero(acc);
     mma_acc(acc, A, SU[cur], L);  // X_{k+1} U_k
     copy(A, acc);
-    store_img(X + (size_t)(k - 1) * IMG, A, L);
+    store_img_l2(X + (size_t)(k - 1) * IMG, A, L, l2_evict_first());
   }
   if (ctr && threadIdx.x == 0) atomicAdd(ctr, (unsigned long long)(N - 1));
 }
@@ -167,16 +167,17 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
   const int N = G.count;
   const int items = batch * N;
   const int K = n_traces(B);
+  const uint64_t keep = l2_evict_last();
   uint32_t ph0 = 0, ph1 = 0;
   unsigned long long nprod = 0;
   Strip A, acc;
-  if (threadIdx.x == 0 && blockIdx.x < items) tma_load_img(SN, X_img + (size_t)blockIdx.x * IMG, &bar[1]);
+  if (threadIdx.x == 0 && blockIdx.x < items) tma_load_img_stream(SN, X_img + (size_t)blockIdx.x * IMG, &bar[1]);
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
     __syncthreads();  // previous item done with SD, SV
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      tma_load_img(SD, P_img + ((size_t)b * N + k) * IMG, &bar[0]);
+      tma_load_img_stream(SD, P_img + ((size_t)b * N + k) * IMG, &bar[0]);
     }
     // X = Omega_k / 2^s
     build_omega(A, B, G, b, k, L);
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
 #pragma unroll
     for (int i = 0; i < 16; ++i) { A.re[i] *= sc; A.im[i] *= sc; }
     store_img(SV, A, L);
-    store_img(gX, A, L);
+    store_img_l2(gX, A, L, keep);
     // G = P_k X_{k+1};  dX = G / 2^s
     mbar_wait(&bar[0], ph0);
     ph0 ^= 1;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
     for (int i = 0; i < 16; ++i) { acc.re[i] *= sc; acc.im[i] *= sc; }
     __syncthreads();  // reads of SD (P_k), SN (X_{k+1}) done; SV (X) complete
     store_img(SD, acc, L);
-    store_img(gdX, acc, L);
+    store_img_l2(gdX, acc, L, keep);
     __syncthreads();  // SD = dX complete
     // (A2, dA2)
     load_img(A, SV, L);
@@ -215,8 +216,8 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
     if (m == 8) {
       // (W, dW) = c1 (X, dX) + c2 (A2, dA2) shared;  (Y, dY) = (A2, dA2)(W, dW)
       __syncthreads();                                 // reads of SV (X), SD (dX) done
-      zero(acc); add_img(acc, c_t8[0], gX, L); add_tm(acc, c_t8[1], T0); store_img(SV, acc, L);
-      zero(acc); add_img(acc, c_t8[0], gdX, L); add_tm(acc, c_t8[1], T1); store_img(SD, acc, L);
+      zero(acc); add_img_l2(acc, c_t8[0], gX, L, keep); add_tm(acc, c_t8[1], T0); store_img(SV, acc, L);
+      zero(acc); add_img_l2(acc, c_t8[0], gdX, L, keep); add_tm(acc, c_t8[1], T1); store_img(SD, acc, L);
       __syncthreads();
       tmem_load(A, T0);
       zero(acc); mma_acc(acc, A, SV, L);               // Y = A2 W
@@ -232,18 +233,18 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
       __syncthreads();
       // dT = c6 dY + c7 dA2 + dX + dL R + L dR,   L = Y + c3 A2 + c4 X
       zero(acc);
-      add_tm(acc, c_t8[5], T3); add_tm(acc, c_t8[6], T1); add_img(acc, 1.0, gdX, L);
-      zero(A); add_tm(A, 1.0, T3); add_tm(A, c_t8[2], T1); add_img(A, c_t8[3], gdX, L);   // dL
+      add_tm(acc, c_t8[5], T3); add_tm(acc, c_t8[6], T1); add_img_l2(acc, 1.0, gdX, L, keep);
+      zero(A); add_tm(A, 1.0, T3); add_tm(A, c_t8[2], T1); add_img_l2(A, c_t8[3], gdX, L, keep);   // dL
       mma_acc(acc, A, SV, L);
-      zero(A); add_tm(A, 1.0, T2); add_tm(A, c_t8[2], T0); add_img(A, c_t8[3], gX, L);    // L
+      zero(A); add_tm(A, 1.0, T2); add_tm(A, c_t8[2], T0); add_img_l2(A, c_t8[3], gX, L, keep);    // L
       mma_acc(acc, A, SD, L);
-      if (s > 0) store_img(gdE, acc, L);
+      if (s > 0) store_img_l2(gdE, acc, L, keep);
       np += 1 + 2 + 2;
       if (s > 0) {                                     // T = c6 Y + c7 A2 + X + I + L R
         zero(acc);
-        add_tm(acc, c_t8[5], T2); add_tm(acc, c_t8[6], T0); add_img(acc, 1.0, gX, L); add_diag(acc, 1.0, L);
+        add_tm(acc, c_t8[5], T2); add_tm(acc, c_t8[6], T0); add_img_l2(acc, 1.0, gX, L, keep); add_diag(acc, 1.0, L);
         mma_acc(acc, A, SV, L);
-        store_img(gE, acc, L);
+        store_img_l2(gE, acc, L, keep);
         ++np;
       }
     } else {
@@ -262,85 +263,85 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
       // (A6, dA6) = (A3, dA3)(A3, dA3)
       tmem_load(A, T2);
       zero(acc); mma_acc(acc, A, SV, L);               // A6
-      store_img(gA6, acc, L);
+      store_img_l2(gA6, acc, L, keep);
       zero(acc); mma_acc(acc, A, SD, L);               // A3 dA3
       tmem_load(A, T3);
       mma_acc(acc, A, SV, L);                          // + dA3 A3
-      store_img(gdA6, acc, L);
+      store_img_l2(gdA6, acc, L, keep);
       __syncthreads();                                 // reads of SV (A3), SD (dA3) done
       // (B5, dB5) shared
       zero(acc);
-      add_img(acc, c_t18[T18_B5][1], gX, L); add_tm(acc, c_t18[T18_B5][2], T0); add_img(acc, 1.0, gA6, L);
+      add_img_l2(acc, c_t18[T18_B5][1], gX, L, keep); add_tm(acc, c_t18[T18_B5][2], T0); add_img_l2(acc, 1.0, gA6, L, keep);
       store_img(SV, acc, L);
       zero(acc);
-      add_img(acc, c_t18[T18_B5][1], gdX, L); add_tm(acc, c_t18[T18_B5][2], T1); add_img(acc, 1.0, gdA6, L);
+      add_img_l2(acc, c_t18[T18_B5][1], gdX, L, keep); add_tm(acc, c_t18[T18_B5][2], T1); add_img_l2(acc, 1.0, gdA6, L, keep);
       store_img(SD, acc, L);
       __syncthreads();
       // dA9 = dB4 + dB1 B5 + B1 dB5
       zero(acc);
-      add_img(acc, c_t18[T18_B4][1], gdX, L); add_tm(acc, c_t18[T18_B4][2], T1);
-      add_tm(acc, c_t18[T18_B4][3], T3); add_img(acc, c_t18[T18_B4][4], gdA6, L);
+      add_img_l2(acc, c_t18[T18_B4][1], gdX, L, keep); add_tm(acc, c_t18[T18_B4][2], T1);
+      add_tm(acc, c_t18[T18_B4][3], T3); add_img_l2(acc, c_t18[T18_B4][4], gdA6, L, keep);
       zero(A);
-      add_img(A, c_t18[T18_B1][1], gdX, L); add_tm(A, c_t18[T18_B1][2], T1); add_tm(A, c_t18[T18_B1][3], T3);
+      add_img_l2(A, c_t18[T18_B1][1], gdX, L, keep); add_tm(A, c_t18[T18_B1][2], T1); add_tm(A, c_t18[T18_B1][3], T3);
       mma_acc(acc, A, SV, L);
       zero(A);
-      add_img(A, c_t18[T18_B1][1], gX, L); add_tm(A, c_t18[T18_B1][2], T0); add_tm(A, c_t18[T18_B1][3], T2);
+      add_img_l2(A, c_t18[T18_B1][1], gX, L, keep); add_tm(A, c_t18[T18_B1][2], T0); add_tm(A, c_t18[T18_B1][3], T2);
       mma_acc(acc, A, SD, L);
       store_img(SN, acc, L);                           // dA9 (SN idle since G)
       // A9 = B4 + B1 B5   (A still holds B1)
       zero(acc);
       add_diag(acc, c_t18[T18_B4][0], L);
-      add_img(acc, c_t18[T18_B4][1], gX, L); add_tm(acc, c_t18[T18_B4][2], T0);
-      add_tm(acc, c_t18[T18_B4][3], T2); add_img(acc, c_t18[T18_B4][4], gA6, L);
+      add_img_l2(acc, c_t18[T18_B4][1], gX, L, keep); add_tm(acc, c_t18[T18_B4][2], T0);
+      add_tm(acc, c_t18[T18_B4][3], T2); add_img_l2(acc, c_t18[T18_B4][4], gA6, L, keep);
       mma_acc(acc, A, SV, L);
       __syncthreads();                                 // reads of SV (B5), SD (dB5) done
       store_img(SV, acc, L);                           // A9
       __syncthreads();                                 // A9 (SV), dA9 (SN) complete
       // dT = dB2 + dL A9 + L dA9,  L = B3 + A9
       zero(acc);
-      add_img(acc, c_t18[T18_B2][1], gdX, L); add_tm(acc, c_t18[T18_B2][2], T1);
-      add_tm(acc, c_t18[T18_B2][3], T3); add_img(acc, c_t18[T18_B2][4], gdA6, L);
+      add_img_l2(acc, c_t18[T18_B2][1], gdX, L, keep); add_tm(acc, c_t18[T18_B2][2], T1);
+      add_tm(acc, c_t18[T18_B2][3], T3); add_img_l2(acc, c_t18[T18_B2][4], gdA6, L, keep);
       load_img(A, SN, L);                              // dL = dB3 + dA9
-      add_img(A, c_t18[T18_B3][1], gdX, L); add_tm(A, c_t18[T18_B3][2], T1);
-      add_tm(A, c_t18[T18_B3][3], T3); add_img(A, c_t18[T18_B3][4], gdA6, L);
+      add_img_l2(A, c_t18[T18_B3][1], gdX, L, keep); add_tm(A, c_t18[T18_B3][2], T1);
+      add_tm(A, c_t18[T18_B3][3], T3); add_img_l2(A, c_t18[T18_B3][4], gdA6, L, keep);
       mma_acc(acc, A, SV, L);
       load_img(A, SV, L);                              // L = B3 + A9
       add_diag(A, c_t18[T18_B3][0], L);
-      add_img(A, c_t18[T18_B3][1], gX, L); add_tm(A, c_t18[T18_B3][2], T0);
-      add_tm(A, c_t18[T18_B3][3], T2); add_img(A, c_t18[T18_B3][4], gA6, L);
+      add_img_l2(A, c_t18[T18_B3][1], gX, L, keep); add_tm(A, c_t18[T18_B3][2], T0);
+      add_tm(A, c_t18[T18_B3][3], T2); add_img_l2(A, c_t18[T18_B3][4], gA6, L, keep);
       mma_acc(acc, A, SN, L);
-      if (s > 0) store_img(gdE, acc, L);
+      if (s > 0) store_img_l2(gdE, acc, L, keep);
       np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
       if (s > 0) {                                     // T = B2 + L A9
         zero(acc);
         add_diag(acc, c_t18[T18_B2][0], L);
-        add_img(acc, c_t18[T18_B2][1], gX, L); add_tm(acc, c_t18[T18_B2][2], T0);
-        add_tm(acc, c_t18[T18_B2][3], T2); add_img(acc, c_t18[T18_B2][4], gA6, L);
+        add_img_l2(acc, c_t18[T18_B2][1], gX, L, keep); add_tm(acc, c_t18[T18_B2][2], T0);
+        add_tm(acc, c_t18[T18_B2][3], T2); add_img_l2(acc, c_t18[T18_B2][4], gA6, L, keep);
         mma_acc(acc, A, SV, L);
-        store_img(gE, acc, L);
+        store_img_l2(gE, acc, L, keep);
         ++np;
       }
     }
     // squarings: (E, dE) <- (E E, dE E + E dE)
     for (int q = 0; q < s; ++q) {
       __syncthreads();
-      load_img(A, gE, L);
+      load_img_l2(A, gE, L, keep);
       store_img(SV, A, L);
-      load_img(acc, gdE, L);
+      load_img_l2(acc, gdE, L, keep);
       store_img(SD, acc, L);
       __syncthreads();
       zero(acc); mma_acc(acc, A, SD, L);               // E dE
-      load_img(A, gdE, L);
+      load_img_l2(A, gdE, L, keep);
       mma_acc(acc, A, SV, L);                          // + dE E
-      store_img(gdE, acc, L);
-      load_img(A, gE, L);
+      store_img_l2(gdE, acc, L, keep);
+      load_img_l2(A, gE, L, keep);
       zero(acc); mma_acc(acc, A, SV, L);               // E E
-      store_img(gE, acc, L);
+      store_img_l2(gE, acc, L, keep);
       np += 3;
     }
     nprod += np;
     // W = dE = L(Omega, G).  traces T_m = Re Tr(W B_m) = sum_{r,c} Re(W[r][c] B_m[c][r])
-    if (s > 0) load_img(A, gdE, L);
+    if (s > 0) load_img_l2(A, gdE, L, keep);
     else copy(A, acc);
     for (int mm = 0; mm < K; ++mm) {
       const double2* Bm = (mm < B.J) ? B.Lc + (size_t)mm * PLANE
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
     __syncthreads();  // also: every product of this item is done -> SN is free
     if (threadIdx.x == 0 && item + (int)gridDim.x < items) {
       fence_proxy_async();
-      tma_load_img(SN, X_img + (size_t)(item + gridDim.x) * IMG, &bar[1]);   // next item's X_{k+1}
+      tma_load_img_stream(SN, X_img + (size_t)(item + gridDim.x) * IMG, &bar[1]);   // next item's X_{k+1}
     }
     if (threadIdx.x < K) {
       double t = 0.0;

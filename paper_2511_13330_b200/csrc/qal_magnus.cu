@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGr
       nprod += expm_fast(A, acc, m, s, SX, SX4, tm, L);
       const size_t slot = (size_t)b * G.count + k;
       if (O.U_nat) store_nat(O.U_nat + slot * PLANE, A, L);
-      if (O.U_img) store_img(O.U_img + slot * IMG, A, L);
+      if (O.U_img) store_img_l2(O.U_img + slot * IMG, A, L, l2_evict_first());
       if (O.chunk_nat) {
         if (kk == 0) {
           store_img(SP, A, L);             // P = U_k (no reader of SP is in flight)

@@ -8,11 +8,15 @@ namespace qal {
 
 // X += a * M (natural layout, strip of lane L)
 __device__ __forceinline__ void axpy_nat(Strip& X, double a, const double2* __restrict__ M, const Lane& L) {
+  const uint64_t keep = l2_evict_last();   // the basis is shared by every CTA and slice
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const double2 v = __ldg(M + L.r * 64 + 4 * i + L.t);
-    X.re[i] = fma(a, v.x, X.re[i]);
-    X.im[i] = fma(a, v.y, X.im[i]);
+    double vx, vy;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(vx), "=d"(vy)
+                 : "l"(M + L.r * 64 + 4 * i + L.t), "l"(keep));
+    X.re[i] = fma(a, vx, X.re[i]);
+    X.im[i] = fma(a, vy, X.im[i]);
   }
 }
 
@@ -124,6 +128,13 @@ __device__ __forceinline__ void add_img(Strip& acc, double a, const double* img,
   if (a == 0.0) return;
   Strip x;
   load_img(x, img, L);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { acc.re[i] = fma(a, x.re[i], acc.re[i]); acc.im[i] = fma(a, x.im[i], acc.im[i]); }
+}
+__device__ __forceinline__ void add_img_l2(Strip& acc, double a, const double* img, const Lane& L, uint64_t pol) {
+  if (a == 0.0) return;
+  Strip x;
+  load_img_l2(x, img, L, pol);
 #pragma unroll
   for (int i = 0; i < 16; ++i) { acc.re[i] = fma(a, x.re[i], acc.re[i]); acc.im[i] = fma(a, x.im[i], acc.im[i]); }
 }
