@@ -66,7 +66,8 @@ enum {                   /* op codes for qal_workspace_bytes */
     QAL_OP_ORDERED_PRODUCT = 1,
     QAL_OP_FIDELITY = 2,      /* qal_fidelity_grad with grad == NULL */
     QAL_OP_FIDELITY_GRAD = 3, /* qal_fidelity_grad with grad != NULL */
-    QAL_OP_EXPM_SLICES = 4    /* qal_magnus_expm_slices (non-zero only for n = 4096) */
+    QAL_OP_EXPM_SLICES = 4,   /* qal_magnus_expm_slices (non-zero only for n = 4096) */
+    QAL_OP_VJP = 5            /* qal_propagator_forward + qal_propagator_vjp (n_slices = count) */
 };
 
 #define QAL_MAX_CTRL 8
@@ -189,6 +190,45 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
                       const qal_c128 *Lc, const qal_c128 *Lcomm, long long Lcomm_batch_stride,
                       const qal_c128 *V, double *F, double *grad, qal_c128 *Lambda, int *status,
                       void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * The gradient path split in two, for objectives other than the fidelity and for time-sharded
+ * horizons (the reverse-mode counterpart of Eq. 15; P:185 motivates avoiding autodiff).
+ *
+ * qal_propagator_forward: for slices k0 .. k0+count-1 of the grid (as qal_magnus_expm_slices),
+ *   Lambda[b] = U_{k0+count-1} ... U_{k0} P_init[b]   (P_init NULL = identity),
+ *   and stores every U_k and every prefix P_k = U_{k-1} ... U_{k0} P_init in `ws` for a following
+ *   qal_propagator_vjp with the same arguments and the same ws.
+ * qal_propagator_vjp: for any scalar objective with dL = Re Tr(C[b] dLambda[b]) (C = the cotangent,
+ *   device [batch][n][n]), writes grad[b] = dL/du (layout of u) with one adjoint Frechet
+ *   derivative per slice (as qal_fidelity_grad, which is the special case C = S_V^dag / d^2).
+ * ws: >= qal_workspace_bytes(QAL_OP_VJP, n, batch, count, n_ctrl, ctrl_mode).
+ */
+int qal_propagator_forward(int d, int batch, int n_slices, double T, int k0, int count, int magnus_order,
+                           int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0,
+                           long long L0_batch_stride, const qal_c128 *Lc, const qal_c128 *Lcomm,
+                           long long Lcomm_batch_stride, const qal_c128 *P_init, qal_c128 *Lambda,
+                           int *status, void *ws, size_t ws_bytes, void *stream);
+int qal_propagator_vjp(int d, int batch, int n_slices, double T, int k0, int count, int magnus_order,
+                       int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0,
+                       long long L0_batch_stride, const qal_c128 *Lc, const qal_c128 *Lcomm,
+                       long long Lcomm_batch_stride, const qal_c128 *C, double *grad, int *status,
+                       void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Eqs. 16-17: the paper's calibration objective.  P = [vec(rho_0) vec(rho_1)] (device
+ * [n][2], rho_k = |phi_k><phi_k| of the logical states of Eqs. 2-3), target G (device [2][2]):
+ *   Pi = P^dag Lambda P,   loss[b] = 1/4 ||Pi - G||_F^2   (the Frobenius norm of Eq. 17 with A^dag A,
+ *   DESIGN.md A22), and, if C != NULL, the cotangent C[b] = 1/2 P (Pi - G)^dag P^dag (so that
+ *   d loss = Re Tr(C dLambda), the input of qal_propagator_vjp).
+ */
+int qal_logical_loss(int d, int batch, const qal_c128 *Lambda, const qal_c128 *Pproj, const qal_c128 *G,
+                     double *loss, qal_c128 *C, void *stream);
+
+/* Adam (ref [13]) on device arrays of n doubles, step t >= 1 (bias correction):
+ *   m <- b1 m + (1-b1) g;  v <- b2 v + (1-b2) g^2;  theta <- theta - lr (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps) */
+int qal_adam_step(int n, double *theta, const double *grad, double *m, double *v, int t, double lr,
+                  double beta1, double beta2, double eps, void *stream);
 
 /* Device workspace (bytes) an op needs; 0 when none.  `flags` = ctrl_mode for the
  * fidelity ops, 0 otherwise. */

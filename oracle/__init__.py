@@ -141,6 +141,41 @@ def gradient(L0, Lc, u, T, N, V, mode=0, order=4):
     return F.value, g, Lam
 
 
+def vjp(L0, Lc, u, T, N, C, mode=0, order=4):
+    """dL/du for dL = Re Tr(C dLambda) (per-direction augmented exponentials); returns (grad, Lambda)."""
+    L0, p0 = _c(L0, np.complex128)
+    Lc, pc = _c(Lc, np.complex128)
+    u, pu = _c(u, np.float64)
+    C, pC = _c(C, np.complex128)
+    n = L0.shape[0]
+    g = np.zeros(u.shape, np.float64)
+    Lam = np.zeros((n, n), np.complex128)
+    _chk(lib().qalref_vjp(n, N, ctypes.c_double(T), order, mode, Lc.shape[0], pu, p0, pc, pC,
+                          g.ctypes.data_as(ctypes.c_void_p), Lam.ctypes.data_as(ctypes.c_void_p)))
+    return g, Lam
+
+
+def logical_loss(Lam, P, G):
+    """Eqs. 16-17: (loss, cotangent C)."""
+    Lam, pl = _c(Lam, np.complex128)
+    P, pp = _c(P, np.complex128)
+    G, pg = _c(G, np.complex128)
+    n = Lam.shape[0]
+    loss = ctypes.c_double(0.0)
+    C = np.zeros((n, n), np.complex128)
+    _chk(lib().qalref_logical_loss(n, pl, pp, pg, ctypes.byref(loss), C.ctypes.data_as(ctypes.c_void_p)))
+    return loss.value, C
+
+
+def adam_step(theta, g, m, v, t, lr=1e-2, b1=0.9, b2=0.999, eps=1e-8):
+    """in place on theta, m, v (float64 contiguous arrays)."""
+    for a in (theta, g, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    lib().qalref_adam_step(theta.size, theta.ctypes.data_as(ctypes.c_void_p), g.ctypes.data_as(ctypes.c_void_p),
+                           m.ctypes.data_as(ctypes.c_void_p), v.ctypes.data_as(ctypes.c_void_p), t,
+                           ctypes.c_double(lr), ctypes.c_double(b1), ctypes.c_double(b2), ctypes.c_double(eps))
+
+
 def sines_eval(prm, umax, t):
     prm, pp = _c(prm, np.float64)
     J, nterm = prm.shape[0], prm.shape[1]

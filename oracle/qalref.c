@@ -23,6 +23,9 @@
  *   fidelity            pinned (P-10)
  *   frechet / gradient  pinned (scipy.linalg.expm_frechet, central FD P-8)
  *   rk4                 pinned (analytic precession, order 4)
+ *   vjp                 pinned (equals gradient for C = S_V^dag/d^2; central FD of Re Tr(C Lambda))
+ *   logical_loss        pinned (Pi = I for Lambda = I, logical swap, FD of the loss vs cotangent)
+ *   adam_step           pinned (closed forms: first step lr sign(g); constant gradient)
  *   sines_eval          parity unpinned vs the paper (A11: the paper gives no values)
  */
 #include <complex.h>
@@ -345,9 +348,30 @@ int qalref_frechet(int n, const cplx *A, const cplx *E, cplx *Lout, cplx *expA)
 /*   NODES (u_j(tau_{k,2})):        (h/2) L_j     - c [A_1, L_j]                        */
 /* grad has the layout of u.  Returns F in *F.                                        */
 /* ------------------------------------------------------------------ */
+static int gradient_core(int d, int N, double T, int order, int mode, int J, const double *u,
+                         const cplx *L0, const cplx *Lc, const cplx *V, const cplx *Cseed, double *F,
+                         double *grad, cplx *LambdaOut);
+
 int qalref_gradient(int d, int N, double T, int order, int mode, int J, const double *u,
                     const cplx *L0, const cplx *Lc, const cplx *V, double *F, double *grad,
                     cplx *LambdaOut)
+{
+    return gradient_core(d, N, T, order, mode, J, u, L0, Lc, V, NULL, F, grad, LambdaOut);
+}
+
+/* Reverse-mode product for any scalar objective with dL = Re Tr(C dLambda): the same per-direction
+ * augmented exponentials as qalref_gradient, with the suffix seeded by C instead of S_V^dag / d^2. */
+int qalref_vjp(int n, int N, double T, int order, int mode, int J, const double *u, const cplx *L0,
+               const cplx *Lc, const cplx *C, double *grad, cplx *LambdaOut)
+{
+    double F = 0.0;
+    int d = (int)lround(sqrt((double)n));
+    return gradient_core(d, N, T, order, mode, J, u, L0, Lc, NULL, C, &F, grad, LambdaOut);
+}
+
+static int gradient_core(int d, int N, double T, int order, int mode, int J, const double *u,
+                         const cplx *L0, const cplx *Lc, const cplx *V, const cplx *Cseed, double *F,
+                         double *grad, cplx *LambdaOut)
 {
     if (J > 64) return QALREF_ERR_DIM;
     int n = d * d;
@@ -368,13 +392,19 @@ int qalref_gradient(int d, int N, double T, int order, int mode, int J, const do
         mm(n, U + (size_t)k * nn, P + (size_t)k * nn, P + (size_t)(k + 1) * nn);
     }
     if (LambdaOut) memcpy(LambdaOut, P + (size_t)N * nn, sizeof(cplx) * nn);
-    *F = qalref_fidelity(d, P + (size_t)N * nn, V);
-
-    /* X_N = S_V^dag (explicit conjugate transpose of conj(V) (x) V) */
-    for (int e = 0; e < d * d; ++e) Vc[e] = conj(V[e]);
-    kron(d, Vc, d, V, S);
-    for (int a = 0; a < n; ++a)
-        for (int b = 0; b < n; ++b) X[(size_t)N * nn + (size_t)a * n + b] = conj(S[(size_t)b * n + a]);
+    double scale = 1.0;
+    if (Cseed) {
+        /* X_N = C */
+        memcpy(X + (size_t)N * nn, Cseed, sizeof(cplx) * nn);
+    } else {
+        *F = qalref_fidelity(d, P + (size_t)N * nn, V);
+        /* X_N = S_V^dag (explicit conjugate transpose of conj(V) (x) V), objective scaled by 1/d^2 */
+        for (int e = 0; e < d * d; ++e) Vc[e] = conj(V[e]);
+        kron(d, Vc, d, V, S);
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) X[(size_t)N * nn + (size_t)a * n + b] = conj(S[(size_t)b * n + a]);
+        scale = 1.0 / ((double)d * d);
+    }
     for (int k = N - 1; k >= 0; --k)
         mm(n, X + (size_t)(k + 1) * nn, U + (size_t)k * nn, X + (size_t)k * nn);
 
@@ -410,7 +440,7 @@ int qalref_gradient(int d, int N, double T, int order, int mode, int J, const do
         double acc = 0.0;
         for (int r = 0; r < n; ++r)
             for (int q = 0; q < n; ++q) acc += creal(G[(size_t)r * n + q] * dU[(size_t)q * n + r]);
-        grad[dir] = acc / ((double)d * d);
+        grad[dir] = acc * scale;
         free(A1); free(A2); free(E); free(T1); free(T2); free(G); free(dU);
     }
     free(U); free(P); free(X); free(Om); free(S); free(Vc);
@@ -494,6 +524,64 @@ int qalref_rk4(int n, int N, double T, int sub, int cmode, int J, const double *
     }
     free(Lt); free(Y); free(k1); free(k2); free(k3); free(k4);
     return QALREF_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Eqs. 16-17: Pi = P^dag Lambda P with P (n x 2) the flattened logical density       */
+/* matrices; loss = (1/4) ||Pi - G||_F^2 with ||A||_F^2 = Tr(A^dag A) (A22); cotangent             */
+/* C = 1/2 P (Pi - G)^dag P^dag of d loss = Re Tr(C dLambda).  Explicit products, plain loops.     */
+/* ------------------------------------------------------------------ */
+int qalref_logical_loss(int n, const cplx *Lambda, const cplx *P, const cplx *G, double *loss, cplx *C)
+{
+    cplx *LP = malloc(sizeof(cplx) * (size_t)n * 2);   /* Lambda P, n x 2 */
+    cplx Pi[4], A[4];
+    for (int i = 0; i < n; ++i)
+        for (int b = 0; b < 2; ++b) {
+            cplx s = 0;
+            for (int j = 0; j < n; ++j) s += Lambda[(size_t)i * n + j] * P[(size_t)j * 2 + b];
+            LP[(size_t)i * 2 + b] = s;
+        }
+    double l = 0.0;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            cplx s = 0;
+            for (int i = 0; i < n; ++i) s += conj(P[(size_t)i * 2 + a]) * LP[(size_t)i * 2 + b];
+            Pi[a * 2 + b] = s;
+            A[a * 2 + b] = s - G[a * 2 + b];
+        }
+    for (int a = 0; a < 2; ++a)              /* Tr(A^dag A) = sum_{ab} conj(A_ab) A_ab */
+        for (int b = 0; b < 2; ++b) l += creal(conj(A[a * 2 + b]) * A[a * 2 + b]);
+    *loss = 0.25 * l;
+    if (C) {
+        cplx PAd[2 * 64 * 64];               /* P A^dag (n x 2), n <= 4096 */
+        if (n > 2048) { free(LP); return QALREF_ERR_DIM; }
+        for (int i = 0; i < n; ++i)
+            for (int b = 0; b < 2; ++b) {
+                cplx s = 0;
+                for (int a = 0; a < 2; ++a) s += P[(size_t)i * 2 + a] * conj(A[b * 2 + a]);
+                PAd[i * 2 + b] = s;
+            }
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                cplx s = 0;
+                for (int b = 0; b < 2; ++b) s += PAd[i * 2 + b] * conj(P[(size_t)j * 2 + b]);
+                C[(size_t)i * n + j] = 0.5 * s;
+            }
+    }
+    free(LP);
+    return QALREF_OK;
+}
+
+/* Adam (Kingma & Ba, ref [13]) with bias correction, step t >= 1 */
+void qalref_adam_step(int n, double *theta, const double *g, double *m, double *v, int t, double lr, double b1,
+                      double b2, double eps)
+{
+    for (int i = 0; i < n; ++i) {
+        m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+        v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+        double mh = m[i] / (1.0 - pow(b1, t)), vh = v[i] / (1.0 - pow(b2, t));
+        theta[i] -= lr * mh / (sqrt(vh) + eps);
+    }
 }
 
 /* plain product, exported for the ordered-product pins (P-12): C = A B */

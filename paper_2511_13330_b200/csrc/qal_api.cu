@@ -194,6 +194,38 @@ int check_basis(int n_or_d_ok, int batch, int n_slices, double T, int order, int
   return QAL_OK;
 }
 
+// workspace of the gradient path: U_img, P_img, X_img [batch][count] images + scratch
+struct GradWs {
+  double *U, *P, *X, *scratch;
+};
+GradWs grad_ws(void* ws, int batch, int count) {
+  const size_t seq = (size_t)batch * count * IMG;
+  GradWs g;
+  g.U = reinterpret_cast<double*>(ws);
+  g.P = g.U + seq;
+  g.X = g.P + seq;
+  g.scratch = g.X + seq + (size_t)batch * IMG;   // leaves room for one [batch][n][n] complex temp (Lambda)
+  return g;
+}
+
+int forward_impl(int batch, const Common& c, const double2* P_init, double2* Lam, int* status, void* ws,
+                 cudaStream_t st) {
+  GradWs g = grad_ws(ws, batch, c.G.count);
+  FwdOut O{nullptr, g.U, nullptr, 1, status};
+  if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_prefix_chain(batch, c.G.count, g.U, g.P, Lam, P_init, st) != cudaSuccess) return QAL_ERR_CUDA;
+  return QAL_OK;
+}
+
+int vjp_impl(int batch, const Common& c, const double2* V, const double2* C, double gscale, double* grad, int* status,
+             void* ws, cudaStream_t st) {
+  GradWs g = grad_ws(ws, batch, c.G.count);
+  if (launch_suffix_chain(batch, c.G.count, g.U, V, C, g.X, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_grad_slices(batch, c.B, c.G, g.P, g.X, grad, status, g.scratch, gscale, st) != cudaSuccess)
+    return QAL_ERR_CUDA;
+  return QAL_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -246,6 +278,7 @@ size_t qal_workspace_bytes(int op, int n, int batch, int n_slices, int n_ctrl, i
       return (size_t)batch * nch * MAT_BYTES + tree_ws_bytes(batch, nch) + (size_t)batch * MAT_BYTES;
     }
     case QAL_OP_FIDELITY_GRAD:
+    case QAL_OP_VJP:
       return 3 * (size_t)batch * n_slices * MAT_BYTES + (size_t)batch * MAT_BYTES + grad_scratch_bytes();
     default: return 0;
   }
@@ -386,23 +419,67 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
     if (rc != QAL_OK) return rc;
     return cuda_rc(launch_fidelity(batch, lam, D2(V), F, st));
   }
-  // gradient path: U_k images (parallel over slices) -> prefix chain P_k -> fidelity ->
-  // suffix chain X_{k+1} -> one adjoint Frechet derivative per slice
-  const size_t seq = (size_t)batch * n_slices * IMG;
-  double* U_img = reinterpret_cast<double*>(w);
-  double* P_img = U_img + seq;
-  double* X_img = P_img + seq;
-  double2* lam_tmp = reinterpret_cast<double2*>(X_img + seq);
-  double* scratch = reinterpret_cast<double*>(lam_tmp + (size_t)batch * PLANE_C);
-  double2* lam = Lambda ? D2(Lambda) : lam_tmp;
-  FwdOut O{nullptr, U_img, nullptr, 1, status};
-  if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_prefix_chain(batch, n_slices, U_img, P_img, lam, st) != cudaSuccess) return QAL_ERR_CUDA;
+  // gradient path: forward (U_k images, prefix P_k) -> fidelity -> VJP with C = S_V^dag (in-kernel from V)
+  double2* lam = Lambda ? D2(Lambda) : reinterpret_cast<double2*>(w + 3 * (size_t)batch * n_slices * MAT_BYTES);
+  if ((rc = forward_impl(batch, c, nullptr, lam, status, ws, st)) != QAL_OK) return rc;
   if (launch_fidelity(batch, lam, D2(V), F, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_suffix_chain(batch, n_slices, U_img, D2(V), X_img, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_grad_slices(batch, c.B, c.G, P_img, X_img, grad, status, scratch, st) != cudaSuccess)
-    return QAL_ERR_CUDA;
-  return QAL_OK;
+  return vjp_impl(batch, c, D2(V), nullptr, 1.0 / 64.0, grad, status, ws, st);
+}
+
+int qal_propagator_forward(int d, int batch, int n_slices, double T, int k0, int count, int magnus_order,
+                           int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0, long long L0_batch_stride,
+                           const qal_c128* Lc, const qal_c128* Lcomm, long long Lcomm_batch_stride,
+                           const qal_c128* P_init, qal_c128* Lambda, int* status, void* ws, size_t ws_bytes,
+                           void* stream) {
+  launch_counter() = 0;
+  Common c;
+  int rc = check_basis(d == 8, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0, L0_batch_stride, Lc,
+                       Lcomm, Lcomm_batch_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!Lambda) return QAL_ERR_NULL;
+  c.G.count = count;
+  if (!ws || ws_bytes < qal_workspace_bytes(QAL_OP_VJP, 64, batch, count, n_ctrl, ctrl_mode)) return QAL_ERR_WORKSPACE;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+  return forward_impl(batch, c, D2(P_init), D2(Lambda), status, ws, st);
+}
+
+int qal_propagator_vjp(int d, int batch, int n_slices, double T, int k0, int count, int magnus_order, int ctrl_mode,
+                       int n_ctrl, const double* u, const qal_c128* L0, long long L0_batch_stride, const qal_c128* Lc,
+                       const qal_c128* Lcomm, long long Lcomm_batch_stride, const qal_c128* C, double* grad,
+                       int* status, void* ws, size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  Common c;
+  int rc = check_basis(d == 8, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0, L0_batch_stride, Lc,
+                       Lcomm, Lcomm_batch_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!C || !grad) return QAL_ERR_NULL;
+  c.G.count = count;
+  if (!ws || ws_bytes < qal_workspace_bytes(QAL_OP_VJP, 64, batch, count, n_ctrl, ctrl_mode)) return QAL_ERR_WORKSPACE;
+  return vjp_impl(batch, c, nullptr, D2(C), 1.0, grad, status, ws, S(stream));
+}
+
+int qal_logical_loss(int d, int batch, const qal_c128* Lambda, const qal_c128* Pproj, const qal_c128* G, double* loss,
+                     qal_c128* C, void* stream) {
+  launch_counter() = 0;
+  if (d != 8) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1) return QAL_ERR_EMPTY;
+  if (!Lambda || !Pproj || !G || !loss) return QAL_ERR_NULL;
+  return cuda_rc(launch_logical_loss(batch, D2(Lambda), D2(Pproj), D2(G), loss, D2(C), S(stream)));
+}
+
+int qal_adam_step(int n, double* theta, const double* grad, double* m, double* v, int t, double lr, double beta1,
+                  double beta2, double eps, void* stream) {
+  launch_counter() = 0;
+  if (n < 1) return QAL_ERR_EMPTY;
+  if (t < 1) return QAL_ERR_DIM;
+  if (!theta || !grad || !m || !v) return QAL_ERR_NULL;
+  if (!is_fin(lr) || !is_fin(beta1) || !is_fin(beta2) || !is_fin(eps)) return QAL_ERR_NONFINITE;
+  return cuda_rc(launch_adam(n, theta, grad, m, v, t, lr, beta1, beta2, eps, S(stream)));
 }
 
 int qal_sample_controls_sines(int n_ctrl, int nterm, const double* prm, double u_max, int n_slices, double T,

@@ -33,9 +33,10 @@ __device__ __forceinline__ void set_identity(Strip& s, const Lane& L) {
 }
 
 // ------------------------------------------------------------------ prefix chain
-// P_0 = I, P_{k+1} = U_k P_k; writes P_img[b][k] = P_k (k < N) and Lam[b] = P_N.
+// P_0 = P_init (default I), P_{k+1} = U_k P_k; writes P_img[b][k] = P_k (k < N) and Lam[b] = P_N.
 __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __restrict__ U_img,
                                                         double* __restrict__ P_img, double2* __restrict__ Lam,
+                                                        const double2* __restrict__ P_init,
                                                         unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* SP = smem;
@@ -53,7 +54,8 @@ __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __r
   __syncthreads();
   if (threadIdx.x == 0) tma_load_img_stream(SU[0], U, &bar[0]);
   Strip A, acc;
-  set_identity(A, L);
+  if (P_init) load_nat(A, P_init + (size_t)b * PLANE, L);   // time-sharded: prefix of earlier ranks
+  else set_identity(A, L);
   store_img(SP, A, L);
   store_img(P, A, L);
   uint32_t ph[2] = {0, 0};
@@ -78,10 +80,11 @@ __global__ void __launch_bounds__(NT, 1) k_prefix_chain(int N, const double* __r
 }
 
 // ------------------------------------------------------------------ suffix chain
-// X_N = S_V^dag, X_k = X_{k+1} U_k; writes X_img[b][k-1] = X_k for k = 1..N.
+// X_N = C (default S_V^dag), X_k = X_{k+1} U_k; writes X_img[b][k-1] = X_k for k = 1..N.
 // S_V^dag[a][c] = V[j][l] conj(V[i][k]) with a = k + 8 l, c = i + 8 j (A8, column stacking).
 __global__ void __launch_bounds__(NT, 1) k_suffix_chain(int N, const double* __restrict__ U_img,
-                                                        const double2* __restrict__ V, double* __restrict__ X_img,
+                                                        const double2* __restrict__ V,
+                                                        const double2* __restrict__ Cseed, double* __restrict__ X_img,
                                                         unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   double* SU[2] = {smem, smem + IMG};
@@ -98,13 +101,17 @@ __global__ void __launch_bounds__(NT, 1) k_suffix_chain(int N, const double* __r
   __syncthreads();
   if (threadIdx.x == 0 && N > 1) tma_load_img_stream(SU[(N - 1) & 1], U + (size_t)(N - 1) * IMG, &bar[(N - 1) & 1]);
   Strip A, acc;
+  if (Cseed) {
+    load_nat(A, Cseed + (size_t)b * PLANE, L);       // general cotangent: dL = Re Tr(C dLambda)
+  } else {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int a = L.r, c = 4 * i + L.t;
-    const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
-    const double2 vjl = __ldg(V + j * 8 + l), vik = __ldg(V + ii * 8 + kk);
-    A.re[i] = vjl.x * vik.x + vjl.y * vik.y;
-    A.im[i] = vjl.y * vik.x - vjl.x * vik.y;
+    for (int i = 0; i < 16; ++i) {
+      const int a = L.r, c = 4 * i + L.t;
+      const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
+      const double2 vjl = __ldg(V + j * 8 + l), vik = __ldg(V + ii * 8 + kk);
+      A.re[i] = vjl.x * vik.x + vjl.y * vik.y;
+      A.im[i] = vjl.y * vik.x - vjl.x * vik.y;
+    }
   }
   store_img(X + (size_t)(N - 1) * IMG, A, L);
   uint32_t ph[2] = {0, 0};
@@ -133,7 +140,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
                                                        const double* __restrict__ P_img,
                                                        const double* __restrict__ X_img, double* __restrict__ grad,
                                                        int* __restrict__ status, double* __restrict__ scratch,
-                                                       unsigned long long* ctr) {
+                                                       double gscale, unsigned long long* ctr) {
   // Dual-number evaluation of the forward Taylor scheme (T8 / T18 + s squarings) at X = Omega/2^s
   // in the direction dX = G/2^s: every product (P, dP)(Q, dQ) = (PQ, dP Q + P dQ) with the
   // right factors Q, dQ as shared images (SV = values, SD = derivatives) and the left factors
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
     if (threadIdx.x == 0) {
       const double* T = red + 8 * QAL_TR_MAX;
       const int J = B.J;
-      const double inv_d2 = 1.0 / 64.0;
+      const double inv_d2 = gscale;   // 1/d^2 for the fidelity, 1 for a general cotangent
       if (G.mode == 0) {
         double* g = grad + ((size_t)b * N + k) * J;
         for (int j = 0; j < J; ++j) g[j] = G.h * T[j] * inv_d2;
@@ -411,7 +418,8 @@ __global__ void __launch_bounds__(NT, 1) k_grad_slices(int batch, Basis B, Slice
 
 size_t grad_scratch_bytes() { return (size_t)num_sms() * GRAD_SCRATCH_STRIPS * MAT_BYTES; }
 
-cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P_img, double2* Lam, cudaStream_t st) {
+cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P_img, double2* Lam,
+                                const double2* P_init, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_prefix_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, CHAIN_SMEM_BYTES);
@@ -419,14 +427,14 @@ cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P
     attr = true;
   }
   prof_pre(ST_PREFIX, st);
-  k_prefix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, P_img, Lam, prof_counter(ST_PREFIX));
+  k_prefix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, P_img, Lam, P_init, prof_counter(ST_PREFIX));
   prof_post(ST_PREFIX, st);
   ++launch_counter();
   return cudaGetLastError();
 }
 
-cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const double2* V, double* X_img,
-                                cudaStream_t st) {
+cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const double2* V, const double2* Cseed,
+                                double* X_img, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_suffix_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, CHAIN_SMEM_BYTES);
@@ -434,14 +442,15 @@ cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const dou
     attr = true;
   }
   prof_pre(ST_SUFFIX, st);
-  k_suffix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, V, X_img, prof_counter(ST_SUFFIX));
+  k_suffix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, V, Cseed, X_img, prof_counter(ST_SUFFIX));
   prof_post(ST_SUFFIX, st);
   ++launch_counter();
   return cudaGetLastError();
 }
 
 cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, const double* P_img,
-                               const double* X_img, double* grad, int* status, double* scratch, cudaStream_t st) {
+                               const double* X_img, double* grad, int* status, double* scratch, double gscale,
+                               cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_grad_slices, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM_BYTES);
@@ -451,7 +460,7 @@ cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, co
   const int items = batch * G.count;
   const int grid = items < num_sms() ? items : num_sms();
   prof_pre(ST_GRAD, st);
-  k_grad_slices<<<grid, NT, GRAD_SMEM_BYTES, st>>>(batch, B, G, P_img, X_img, grad, status, scratch,
+  k_grad_slices<<<grid, NT, GRAD_SMEM_BYTES, st>>>(batch, B, G, P_img, X_img, grad, status, scratch, gscale,
                                                     prof_counter(ST_GRAD));
   prof_post(ST_GRAD, st);
   ++launch_counter();

@@ -56,12 +56,17 @@ cudaError_t launch_commutators(int batch, int J, const double2* L0, const double
 // prefix P_{k+1} = U_k P_k (P_0 = I) and suffix X_k = X_{k+1} U_k (X_N = S_V^dag) over
 // per-pulse image sequences; see qal_grad.cu
 cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P_img, double2* Lam_nat,
-                                cudaStream_t st);
-cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const double2* V, double* X_img,
-                                cudaStream_t st);
+                                const double2* P_init, cudaStream_t st);
+cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const double2* V, const double2* Cseed,
+                                double* X_img, cudaStream_t st);
 cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, const double* P_img,
-                               const double* X_img, double* grad, int* status, double* scratch,
+                               const double* X_img, double* grad, int* status, double* scratch, double gscale,
                                cudaStream_t st);
+// Eqs. 16-17 logical loss + cotangent, and Adam (qal_product.cu)
+cudaError_t launch_logical_loss(int batch, const double2* Lam, const double2* Pproj, const double2* Gt, double* loss,
+                                double2* C, cudaStream_t st);
+cudaError_t launch_adam(int n, double* theta, const double* g, double* m, double* v, int t, double lr, double b1,
+                        double b2, double eps, cudaStream_t st);
 size_t grad_scratch_bytes();
 cudaError_t launch_sample_sines(int J, int nterm, const double* prm, double umax, double h, int k0, int count,
                                double* out, cudaStream_t st);

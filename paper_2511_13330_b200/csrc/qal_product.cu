@@ -209,6 +209,101 @@ cudaError_t launch_commutators(int batch, int J, const double2* L0, const double
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ Eqs. 16-17
+// Logical projection Pi = P^dag Lambda P (P = [vec(rho_0) vec(rho_1)], n x 2), the mean squared
+// error loss = 1/4 ||Pi - G||_F^2 (Frobenius via A^dag A, A22), and its cotangent
+// C = 1/2 P (Pi - G)^dag P^dag, so that d loss = Re Tr(C dLambda).  One CTA per pulse.
+__global__ void __launch_bounds__(NT) k_logical_loss(const double2* __restrict__ Lam, const double2* __restrict__ Pp,
+                                                     const double2* __restrict__ Gt, double* __restrict__ loss,
+                                                     double2* __restrict__ C) {
+  __shared__ double red[8][9];
+  __shared__ double2 Ash[4];
+  const Lane L = lane_id();
+  const double2* M = Lam + (size_t)blockIdx.x * PLANE;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Pi_ab re/im, ab = 00, 01, 10, 11
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const int i = e >> 6, j = e & 63;
+    const double2 x = M[e];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const double2 pia = __ldg(Pp + i * 2 + a);   // conj(P_ia) Lambda_ij P_jb
+      const double tr = pia.x * x.x + pia.y * x.y, ti = pia.x * x.y - pia.y * x.x;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double2 pjb = __ldg(Pp + j * 2 + b);
+        acc[2 * (2 * a + b)] += tr * pjb.x - ti * pjb.y;
+        acc[2 * (2 * a + b) + 1] += tr * pjb.y + ti * pjb.x;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+  if (L.lane == 0)
+    for (int q = 0; q < 8; ++q) red[L.w][q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0;
+    for (int ab = 0; ab < 4; ++ab) {
+      double pr = 0.0, pi = 0.0;
+      for (int w = 0; w < 8; ++w) { pr += red[w][2 * ab]; pi += red[w][2 * ab + 1]; }
+      const double2 g = Gt[ab];
+      Ash[ab] = make_double2(pr - g.x, pi - g.y);
+      l += (pr - g.x) * (pr - g.x) + (pi - g.y) * (pi - g.y);
+    }
+    loss[blockIdx.x] = 0.25 * l;
+  }
+  __syncthreads();
+  if (!C) return;
+  double2* Cb = C + (size_t)blockIdx.x * PLANE;
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const int i = e >> 6, j = e & 63;
+    double cr = 0.0, ci = 0.0;   // 1/2 sum_ab P_ia conj(A_ba) conj(P_jb)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double2 pia = __ldg(Pp + i * 2 + a), pjb = __ldg(Pp + j * 2 + b), A = Ash[2 * b + a];
+        // w = P_ia * conj(A_ba)
+        const double wr = pia.x * A.x + pia.y * A.y, wi = pia.y * A.x - pia.x * A.y;
+        // w * conj(P_jb)
+        cr += wr * pjb.x + wi * pjb.y;
+        ci += wi * pjb.x - wr * pjb.y;
+      }
+    Cb[e] = make_double2(0.5 * cr, 0.5 * ci);
+  }
+}
+
+cudaError_t launch_logical_loss(int batch, const double2* Lam, const double2* Pproj, const double2* Gt, double* loss,
+                                double2* C, cudaStream_t st) {
+  k_logical_loss<<<batch, NT, 0, st>>>(Lam, Pproj, Gt, loss, C);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// Adam (ref [13]): m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2; theta <- theta - lr mhat/(sqrt(vhat)+eps)
+__global__ void __launch_bounds__(NT) k_adam(int n, double* __restrict__ th, const double* __restrict__ g,
+                                             double* __restrict__ m, double* __restrict__ v, double c1, double c2,
+                                             double lr, double b1, double b2, double eps) {
+  const int i = blockIdx.x * NT + threadIdx.x;
+  if (i >= n) return;
+  const double gi = g[i];
+  const double mi = b1 * m[i] + (1.0 - b1) * gi;
+  const double vi = b2 * v[i] + (1.0 - b2) * gi * gi;
+  m[i] = mi;
+  v[i] = vi;
+  th[i] -= lr * (mi / c1) / (sqrt(vi / c2) + eps);
+}
+
+cudaError_t launch_adam(int n, double* theta, const double* g, double* m, double* v, int t, double lr, double b1,
+                        double b2, double eps, cudaStream_t st) {
+  const double c1 = 1.0 - pow(b1, (double)t), c2 = 1.0 - pow(b2, (double)t);
+  k_adam<<<(n + NT - 1) / NT, NT, 0, st>>>(n, theta, g, m, v, c1, c2, lr, b1, b2, eps);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ a1 (NODES controls)
 // configs[3] controls (A11) at the Gauss-Legendre nodes of slices k0..k0+count-1.
 __global__ void __launch_bounds__(NT) k_sample_sines(int J, int nterm, const double* __restrict__ prm, double umax,

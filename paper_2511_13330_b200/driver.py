@@ -150,6 +150,34 @@ def time_shard_propagator(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode,
     return ordered_combine(gather_partials(Q, group), stream=stream)
 
 
+def calibrate(H0, Hc, C, u0, T, Pproj, G, *, iters=200, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8,
+              magnus_order=4, stream=None):
+    """NEXT f1 -- the paper's calibration loop: Adam over the PWC coefficient matrix
+    u [B][M][J] minimising the Eq. 16-17 loss 1/4 ||P^dag Lambda P - G||_F^2, every step on the
+    device: forward (qal_propagator_forward) -> loss + cotangent (qal_logical_loss) -> gradient
+    (qal_propagator_vjp, one adjoint Frechet derivative per slice; the paper's autodiff hit a
+    memory wall here) -> qal_adam_step.  Returns dict(u, loss_history [iters, B],
+    best_u, best_loss); no host synchronisation inside the loop."""
+    u = u0.clone().contiguous()
+    L0, Lc, _ = qal.qal_build_liouvillian(H0, Hc, C, stream=stream)
+    sess = qal.GradientSession(L0, Lc, u, T, u.shape[1], magnus_order=magnus_order, stream=stream)
+    m = torch.zeros_like(u)
+    v = torch.zeros_like(u)
+    hist = torch.empty((iters, u.shape[0]), dtype=F64, device=u.device)
+    best = torch.full((u.shape[0],), float("inf"), dtype=F64, device=u.device)
+    best_u = u.clone()
+    for t in range(1, iters + 1):
+        Lam = sess.forward()
+        loss, cot = qal.qal_logical_loss(Lam, Pproj, G, stream=stream)
+        hist[t - 1] = loss
+        better = loss < best
+        best = torch.where(better, loss, best)
+        best_u[better] = u[better]
+        g = sess.vjp(cot)
+        qal.qal_adam_step(u, g, m, v, t, lr, beta1, beta2, eps, stream=stream)
+    return {"u": u, "loss_history": hist, "best_u": best_u, "best_loss": best}
+
+
 def fp64_peak(sink, blocks, seconds=0.2, kind=0):
     """Measured FP64 peak (K0 probe, DMMA.8x8x4 by default) in TFLOP/s on the current device."""
     iters = 2000
@@ -180,4 +208,4 @@ def stage_flops(products: int) -> float:
 
 
 __all__ = ["PulseBatch", "shard_range", "time_shard_chunk", "time_shard_propagator", "ordered_combine",
-           "gather_partials", "local_partial", "fp64_peak", "MATMUL_FLOPS_64", "stage_flops", "math"]
+           "gather_partials", "local_partial", "calibrate", "fp64_peak", "MATMUL_FLOPS_64", "stage_flops", "math"]

@@ -261,4 +261,37 @@ def single_spin(kind: str, T: float, N: int, b: float = 0.0, W: float = 0.0,
     return Problem(f"spin1-{kind}", 2, H0[None].copy(), Hc, C, T, N, u, CTRL_PWC, np.eye(2, dtype=np.complex128))
 
 
+# --------------------------------------------------------------------------
+# Logical encoding of the exchange-only qubit (Eqs. 2-3) and the projection of Eq. 16
+# (P:145-151): P = [vec(rho_0) vec(rho_1)], rho_k = |phi_k><phi_k|, column stacking (A5).
+# A22: Eq. 3 as printed, 2|uuu> - |uud> - |duu>, mixes S_z sectors (|uuu> has S_z = 3/2); the
+# default is the standard decoherence-free-subspace state 2|udu> - |uud> - |duu> (S_z = 1/2,
+# orthogonal to phi_0); variant="as-printed" reproduces the printed equation.
+# --------------------------------------------------------------------------
+def _ket(bits: str) -> np.ndarray:
+    """|s1 s2 s3> with 'u' = up (0), 'd' = down (1); index = 4 s1 + 2 s2 + s3 (A7)."""
+    v = np.zeros(8, dtype=np.complex128)
+    v[int("".join("0" if c == "u" else "1" for c in bits), 2)] = 1.0
+    return v
+
+
+def logical_states(variant: str = "standard-dfs") -> np.ndarray:
+    phi0 = (_ket("uud") - _ket("duu")) / math.sqrt(2.0)
+    top = _ket("uuu") if variant == "as-printed" else _ket("udu")
+    phi1 = (2.0 * top - _ket("uud") - _ket("duu")) / math.sqrt(6.0)
+    return np.stack([phi0, phi1])
+
+
+def projection_matrix(variant: str = "standard-dfs") -> np.ndarray:
+    """[n][2] complex: columns vec(|phi_k><phi_k|) (column stacking)."""
+    phis = logical_states(variant)
+    return np.ascontiguousarray(np.stack([np.outer(p, p.conj()).reshape(-1, order="F") for p in phis], axis=1))
+
+
+LOGICAL_GATES = {
+    "X": np.array([[0, 1], [1, 0]], dtype=np.complex128),
+    "I": np.eye(2, dtype=np.complex128),
+}
+
+
 CONFIGS = {"cfg0": cfg0, "cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}

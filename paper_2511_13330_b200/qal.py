@@ -22,6 +22,7 @@ QAL_OP_ORDERED_PRODUCT = 1
 QAL_OP_FIDELITY = 2
 QAL_OP_FIDELITY_GRAD = 3
 QAL_OP_EXPM_SLICES = 4
+QAL_OP_VJP = 5
 QAL_MAX_CTRL = 8
 STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
           "grad_slices", "dense_gemm"]
@@ -56,6 +57,21 @@ _EXPORTS = {
     "qal_sample_controls_sines": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_double,
                                                   ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_propagator_forward": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_propagator_vjp": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_logical_loss": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_adam_step": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_void_p]),
     "qal_profile_begin": (ctypes.c_int, [ctypes.c_void_p]),
     "qal_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -234,6 +250,69 @@ def qal_fidelity_grad(L0, Lc, u, T, n_slices, V, *, magnus_order=4, ctrl_mode=QA
                                   _ptr(status), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "qal_fidelity_grad")
     return F, g, Lam
+
+
+class GradientSession:
+    """qal_propagator_forward / qal_propagator_vjp pair sharing one workspace (same slice range)."""
+
+    def __init__(self, L0, Lc, u, T, n_slices, *, k0=0, magnus_order=4, ctrl_mode=QAL_CTRL_PWC, Lcomm=None,
+                 stream=None):
+        self.L0 = _dev(L0, torch.complex128, "L0")
+        self.Lc = _dev(Lc, torch.complex128, "Lc")
+        self.u = _dev(u, torch.float64, "u")
+        self.Lcomm = _dev(Lcomm, torch.complex128, "Lcomm") if Lcomm is not None else None
+        self.T, self.N, self.k0 = float(T), n_slices, k0
+        self.B, self.count = u.shape[0], u.shape[1]
+        self.J, self.n = Lc.shape[0], L0.shape[-1]
+        self.order, self.mode, self.stream = magnus_order, ctrl_mode, stream
+        self.L0s = 0 if self.L0.shape[0] == 1 else self.n * self.n
+        self.Lcs = 0 if self.Lcomm is None or self.Lcomm.shape[0] == 1 else n_comm(self.J) * self.n * self.n
+        wsb = workspace_bytes(QAL_OP_VJP, self.n, self.B, self.count, self.J, ctrl_mode)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=u.device)
+        self.status = torch.zeros(self.B, dtype=torch.int32, device=u.device)
+
+    def _args(self):
+        return (int(round(self.n ** 0.5)), self.B, self.N, self.T, self.k0, self.count, self.order, self.mode, self.J,
+                _ptr(self.u), _ptr(self.L0), self.L0s, _ptr(self.Lc), _ptr(self.Lcomm), self.Lcs)
+
+    def forward(self, P_init=None):
+        Lam = torch.empty((self.B, self.n, self.n), dtype=torch.complex128, device=self.u.device)
+        if P_init is not None:
+            P_init = _dev(P_init, torch.complex128, "P_init")
+        rc = load().qal_propagator_forward(*self._args(), _ptr(P_init), _ptr(Lam), _ptr(self.status), _ptr(self.ws),
+                                           self.ws.numel(), _stream(self.stream))
+        _check(rc, "qal_propagator_forward")
+        return Lam
+
+    def vjp(self, C):
+        C = _dev(C, torch.complex128, "C")
+        g = torch.empty_like(self.u)
+        rc = load().qal_propagator_vjp(*self._args(), _ptr(C), _ptr(g), _ptr(self.status), _ptr(self.ws),
+                                       self.ws.numel(), _stream(self.stream))
+        _check(rc, "qal_propagator_vjp")
+        return g
+
+
+def qal_logical_loss(Lam, Pproj, G, want_cotangent=True, stream=None):
+    """Eqs. 16-17: (loss [B], cotangent C [B][n][n] or None)."""
+    Lam = _dev(Lam, torch.complex128, "Lambda")
+    Pproj = _dev(Pproj, torch.complex128, "P")
+    G = _dev(G, torch.complex128, "G")
+    loss = torch.empty(Lam.shape[0], dtype=torch.float64, device=Lam.device)
+    C = torch.empty_like(Lam) if want_cotangent else None
+    rc = load().qal_logical_loss(8, Lam.shape[0], _ptr(Lam), _ptr(Pproj), _ptr(G), _ptr(loss), _ptr(C),
+                                 _stream(stream))
+    _check(rc, "qal_logical_loss")
+    return loss, C
+
+
+def qal_adam_step(theta, grad, m, v, t, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+    """Adam on device tensors (in place on theta, m, v)."""
+    for name, x in (("theta", theta), ("grad", grad), ("m", m), ("v", v)):
+        _dev(x, torch.float64, name)
+    rc = load().qal_adam_step(theta.numel(), _ptr(theta), _ptr(grad), _ptr(m), _ptr(v), t, lr, beta1, beta2, eps,
+                              _stream(stream))
+    _check(rc, "qal_adam_step")
 
 
 def qal_sample_controls_sines(prm, u_max, n_slices, T, k0=0, count=None, stream=None):

@@ -433,3 +433,78 @@ def test_evolve_rho_matches_solve_ivp_d8(oracle):
         sol = scipy.integrate.solve_ivp(f, (0.0, h), rho.reshape(-1), method="DOP853", rtol=1e-13, atol=1e-15)
         rho = sol.y[:, -1].reshape(8, 8)
     assert np.max(np.abs(got - rho)) <= 1e-13
+
+
+# ---------------------------------------------------------------- calibration objective (NEXT f1)
+def test_projection_matrix_is_orthonormal_and_literal():
+    """S:101-103 adapted to the spin basis: P^dag P = I_2; column 0 = vec(|phi0><phi0|)."""
+    for variant in ("standard-dfs", "as-printed"):
+        P = qi.projection_matrix(variant)
+        assert P.shape == (64, 2)
+        assert np.allclose(P.conj().T @ P, np.eye(2), atol=1e-15)
+    P = qi.projection_matrix()
+    # |phi0> = (|uud> - |duu>)/sqrt2 -> indices 1 and 4; vec index i + 8 j
+    assert abs(P[1 + 8 * 1, 0] - 0.5) < 1e-15 and abs(P[1 + 8 * 4, 0] + 0.5) < 1e-15
+    phis = qi.logical_states()
+    sz = np.diag(sum(qi.site_op(qi.SZ, i, 3) for i in range(3))).real
+    for p in phis:                                    # both states in the S_z = +1/2 sector (A22)
+        assert abs(np.vdot(p, sz * p).real - 1.0) < 1e-15
+
+
+def test_logical_loss_identity_swap_and_cotangent(oracle):
+    P = qi.projection_matrix()
+    # Lambda = I -> Pi = I_2 (S:349)
+    loss, _ = oracle.logical_loss(np.eye(64, dtype=np.complex128), P, np.eye(2, dtype=np.complex128))
+    assert loss < 1e-30
+    # logical swap (S:350): the unitary exchanging phi0 <-> phi1 and fixing their complement
+    phis = qi.logical_states()
+    W = np.eye(8, dtype=np.complex128) - np.outer(phis[0], phis[0].conj()) - np.outer(phis[1], phis[1].conj())
+    W += np.outer(phis[0], phis[1].conj()) + np.outer(phis[1], phis[0].conj())
+    Lsw = np.kron(W.conj(), W)
+    loss, _ = oracle.logical_loss(Lsw, P, qi.LOGICAL_GATES["X"])
+    assert loss < 1e-28
+    # cotangent: d loss along E equals Re Tr(C E) (central difference)
+    rng = np.random.default_rng(3)
+    Lam = rand_c(rng, 64, 64) / 8.0
+    G = rand_c(rng, 2, 2)
+    E = rand_c(rng, 64, 64)
+    l0, C = oracle.logical_loss(Lam, P, G)
+    eps = 1e-6
+    lp, _ = oracle.logical_loss(Lam + eps * E, P, G)
+    lm, _ = oracle.logical_loss(Lam - eps * E, P, G)
+    fd = (lp - lm) / (2 * eps)
+    assert abs(fd - np.trace(C @ E).real) <= 1e-8 * max(1.0, abs(fd))
+
+
+def test_vjp_reduces_to_the_fidelity_gradient_and_matches_fd(oracle):
+    p = qi.cfg0(N=6, T=100.0 * 6 / 256)
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    F, g, Lam = oracle.gradient(L0, Lc, p.u[0], p.T, p.N, p.V)
+    SV = np.kron(p.V.conj(), p.V)
+    gv, Lv = oracle.vjp(L0, Lc, p.u[0], p.T, p.N, SV.conj().T / 64.0)
+    assert np.allclose(gv, g, rtol=0, atol=1e-16 + 1e-12 * np.abs(g).max())
+    assert np.array_equal(Lv, Lam)
+    rng = np.random.default_rng(8)
+    C = rand_c(rng, 64, 64)
+    gC, _ = oracle.vjp(L0, Lc, p.u[0], p.T, p.N, C)
+    eps = 1e-6
+    for k, j in [(0, 0), (3, 1), (5, 0)]:
+        up, um = p.u[0].copy(), p.u[0].copy()
+        up[k, j] += eps
+        um[k, j] -= eps
+        fp = np.trace(C @ oracle.propagate(L0, Lc, up, p.T, p.N)).real
+        fm = np.trace(C @ oracle.propagate(L0, Lc, um, p.T, p.N)).real
+        assert abs((fp - fm) / (2 * eps) - gC[k, j]) <= 1e-6 * np.abs(gC).max()
+
+
+def test_adam_closed_forms(oracle):
+    rng = np.random.default_rng(2)
+    g = rng.standard_normal(7)
+    th = np.zeros(7)
+    m = np.zeros(7)
+    v = np.zeros(7)
+    oracle.adam_step(th, g, m, v, 1, lr=0.1, eps=0.0)
+    assert np.allclose(th, -0.1 * np.sign(g), atol=1e-15)        # first step: lr * sign(g)
+    for t in range(2, 6):                                          # constant gradient: every step lr sign(g)
+        oracle.adam_step(th, g, m, v, t, lr=0.1, eps=0.0)
+        assert np.allclose(th, -0.1 * t * np.sign(g), atol=1e-13)
