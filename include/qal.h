@@ -215,6 +215,10 @@ int qal_propagator_vjp(int d, int batch, int n_slices, double T, int k0, int cou
                        long long Lcomm_batch_stride, const qal_c128 *C, double *grad, int *status,
                        void *ws, size_t ws_bytes, void *stream);
 
+/* Cotangent of the fidelity (A8): C = S_V^dag / d^2 (device [n][n]), so that dF = Re Tr(C dLambda).
+ * Used to seed qal_propagator_vjp on time-sharded horizons. */
+int qal_fidelity_cotangent(int d, const qal_c128 *V, qal_c128 *C, void *stream);
+
 /*
  * Eqs. 16-17: the paper's calibration objective.  P = [vec(rho_0) vec(rho_1)] (device
  * [n][2], rho_k = |phi_k><phi_k| of the logical states of Eqs. 2-3), target G (device [2][2]):

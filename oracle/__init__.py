@@ -155,6 +155,14 @@ def vjp(L0, Lc, u, T, N, C, mode=0, order=4):
     return g, Lam
 
 
+def fidelity_cotangent(V):
+    V, pv = _c(V, np.complex128)
+    d = V.shape[0]
+    C = np.zeros((d * d, d * d), np.complex128)
+    lib().qalref_fidelity_cotangent(d, pv, C.ctypes.data_as(ctypes.c_void_p))
+    return C
+
+
 def logical_loss(Lam, P, G):
     """Eqs. 16-17: (loss, cotangent C)."""
     Lam, pl = _c(Lam, np.complex128)

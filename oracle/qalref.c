@@ -526,6 +526,18 @@ int qalref_rk4(int n, int N, double T, int sub, int cmode, int J, const double *
     return QALREF_OK;
 }
 
+/* cotangent of the fidelity: C = S_V^dag / d^2 with S_V = conj(V) (x) V formed explicitly */
+void qalref_fidelity_cotangent(int d, const cplx *V, cplx *C)
+{
+    int n = d * d;
+    cplx *Vc = malloc(sizeof(cplx) * d * d), *S = malloc(sizeof(cplx) * (size_t)n * n);
+    for (int e = 0; e < d * d; ++e) Vc[e] = conj(V[e]);
+    kron(d, Vc, d, V, S);
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) C[(size_t)a * n + b] = conj(S[(size_t)b * n + a]) / ((double)d * d);
+    free(Vc); free(S);
+}
+
 /* ------------------------------------------------------------------ */
 /* Eqs. 16-17: Pi = P^dag Lambda P with P (n x 2) the flattened logical density       */
 /* matrices; loss = (1/4) ||Pi - G||_F^2 with ||A||_F^2 = Tr(A^dag A) (A22); cotangent             */

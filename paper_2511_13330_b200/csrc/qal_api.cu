@@ -463,6 +463,13 @@ int qal_propagator_vjp(int d, int batch, int n_slices, double T, int k0, int cou
   return vjp_impl(batch, c, nullptr, D2(C), 1.0, grad, status, ws, S(stream));
 }
 
+int qal_fidelity_cotangent(int d, const qal_c128* V, qal_c128* C, void* stream) {
+  launch_counter() = 0;
+  if (d != 8) return QAL_ERR_UNSUPPORTED;
+  if (!V || !C) return QAL_ERR_NULL;
+  return cuda_rc(launch_fidelity_cotangent(D2(V), D2(C), S(stream)));
+}
+
 int qal_logical_loss(int d, int batch, const qal_c128* Lambda, const qal_c128* Pproj, const qal_c128* G, double* loss,
                      qal_c128* C, void* stream) {
   launch_counter() = 0;

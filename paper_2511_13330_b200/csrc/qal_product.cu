@@ -209,6 +209,22 @@ cudaError_t launch_commutators(int batch, int J, const double2* L0, const double
   return cudaGetLastError();
 }
 
+// cotangent of the fidelity (A8): C = S_V^dag / d^2, C[a][c] = V[j][l] conj(V[i][k]) / d^2 with
+// a = k + d l, c = i + d j (so that dF = Re Tr(C dLambda)).  d = 8.
+__global__ void __launch_bounds__(NT) k_fidelity_cotangent(const double2* __restrict__ V, double2* __restrict__ C) {
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const int a = e >> 6, c = e & 63;
+    const int k = a & 7, l = a >> 3, i = c & 7, j = c >> 3;
+    const double2 vjl = V[j * 8 + l], vik = V[i * 8 + k];
+    C[e] = make_double2((vjl.x * vik.x + vjl.y * vik.y) / 64.0, (vjl.y * vik.x - vjl.x * vik.y) / 64.0);
+  }
+}
+cudaError_t launch_fidelity_cotangent(const double2* V, double2* C, cudaStream_t st) {
+  k_fidelity_cotangent<<<1, NT, 0, st>>>(V, C);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ Eqs. 16-17
 // Logical projection Pi = P^dag Lambda P (P = [vec(rho_0) vec(rho_1)], n x 2), the mean squared
 // error loss = 1/4 ||Pi - G||_F^2 (Frobenius via A^dag A, A22), and its cotangent

@@ -178,6 +178,70 @@ def calibrate(H0, Hc, C, u0, T, Pproj, G, *, iters=200, lr=1e-2, beta1=0.9, beta
     return {"u": u, "loss_history": hist, "best_u": best_u, "best_loss": best}
 
 
+def segment_seeds(Qs, C, product):
+    """Seed algebra of the time-sharded gradient (NEXT f2).  Qs: the time-ordered partial products
+    Q_0 .. Q_{S-1} of consecutive slice segments (over all ranks), C: the cotangent of the objective
+    at Lambda = Q_{S-1} ... Q_0.  For segment s with local prefixes P_k^loc (P_init = I),
+        G_k = P_k^loc X'_{k+1},   X'_{end of s} = (Q_{s-1} ... Q_0) C (Q_{S-1} ... Q_{s+1})
+    so the vjp of every segment runs on its own slices with the seed X'_s (no recomputation).
+    `product(list)` = ordered product of a time-ordered list (later on the LEFT).
+    Returns the list of seeds."""
+    S = len(Qs)
+    seeds = []
+    for s in range(S):
+        prefix = product(Qs[:s]) if s > 0 else None
+        suffix = product(Qs[s + 1:]) if s + 1 < S else None
+        chain = [x for x in (suffix, C, prefix) if x is not None]   # prefix C suffix  (time order reversed)
+        seeds.append(product(chain) if len(chain) > 1 else chain[0])
+    return seeds
+
+
+def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, cotangent, magnus_order=4,
+                          segment=1 << 16, group=None, stream=None):
+    """NEXT f2 -- gradient of an objective over a long horizon, time-sharded over the ranks and
+    segmented on each rank so the stored images fit HBM.  Rank r owns slices [k0, k0 + count).
+    1. every local segment's partial Q (chunk fold + tree), 2. all-gather the rank partials
+    (NCCL), 3. Lambda and the cotangent C = cotangent(Lambda), 4. per segment: forward (P_init = I)
+    + VJP with the seed of segment_seeds.  Returns (Lambda, grad of the local slices)."""
+    count = u_local.shape[1]
+    segment = min(segment, count)
+    if count % segment:
+        raise ValueError("segment must divide the rank's slice count")
+    nseg = count // segment
+    local = []
+    for s in range(nseg):
+        us = u_local[:, s * segment:(s + 1) * segment].contiguous()
+        local.append(local_partial(L0, Lc, Lcomm, us, T, n_slices, k0 + s * segment, ctrl_mode=ctrl_mode,
+                                   magnus_order=magnus_order, stream=stream))
+    Q_rank = local[0] if nseg == 1 else ordered_combine(torch.stack(local), stream=stream)
+    ranks = gather_partials(Q_rank, group)                                  # [G][n][n]
+    rank = _rank(group)
+    before = None if rank == 0 else ordered_combine(ranks[:rank], stream=stream)
+    after = None if rank + 1 == ranks.shape[0] else ordered_combine(ranks[rank + 1:], stream=stream)
+    Lam = ordered_combine(ranks, stream=stream)
+    C = cotangent(Lam)
+    # the rank's segments see everything before the rank inside their prefix, after it in their suffix
+    prod = lambda xs: qal.qal_ordered_product(torch.stack(list(xs)).unsqueeze(0).contiguous(),  # noqa: E731
+                                              stream=stream)[0]
+    Qs = ([before] if before is not None else []) + local + ([after] if after is not None else [])
+    seeds = segment_seeds(Qs, C, prod)
+    off = 1 if before is not None else 0
+    grad = torch.empty_like(u_local)
+    for s in range(nseg):
+        us = u_local[:, s * segment:(s + 1) * segment].contiguous()
+        sess = qal.GradientSession(L0, Lc, us, T, n_slices, k0=k0 + s * segment, magnus_order=magnus_order,
+                                   ctrl_mode=ctrl_mode, Lcomm=Lcomm, stream=stream)
+        sess.forward()
+        grad[:, s * segment:(s + 1) * segment] = sess.vjp(seeds[off + s].unsqueeze(0).contiguous())
+        del sess
+    return Lam, grad
+
+
+def _rank(group=None):
+    import torch.distributed as dist
+    return dist.get_rank(group) if (dist.is_available() and dist.is_initialized()) else 0
+
+
 def fp64_peak(sink, blocks, seconds=0.2, kind=0):
     """Measured FP64 peak (K0 probe, DMMA.8x8x4 by default) in TFLOP/s on the current device."""
     iters = 2000
@@ -208,4 +272,5 @@ def stage_flops(products: int) -> float:
 
 
 __all__ = ["PulseBatch", "shard_range", "time_shard_chunk", "time_shard_propagator", "ordered_combine",
-           "gather_partials", "local_partial", "calibrate", "fp64_peak", "MATMUL_FLOPS_64", "stage_flops", "math"]
+           "gather_partials", "local_partial", "calibrate", "segment_seeds", "time_sharded_gradient", "fp64_peak",
+           "MATMUL_FLOPS_64", "stage_flops", "math"]

@@ -67,6 +67,7 @@ _EXPORTS = {
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_fidelity_cotangent": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "qal_logical_loss": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "qal_adam_step": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -291,6 +292,15 @@ class GradientSession:
                                        self.ws.numel(), _stream(self.stream))
         _check(rc, "qal_propagator_vjp")
         return g
+
+
+def qal_fidelity_cotangent(V, stream=None):
+    """C = S_V^dag / d^2 [n][n] (dF = Re Tr(C dLambda))."""
+    V = _dev(V, torch.complex128, "V")
+    d = V.shape[0]
+    C = torch.empty((d * d, d * d), dtype=torch.complex128, device=V.device)
+    _check(load().qal_fidelity_cotangent(d, _ptr(V), _ptr(C), _stream(stream)), "qal_fidelity_cotangent")
+    return C
 
 
 def qal_logical_loss(Lam, Pproj, G, want_cotangent=True, stream=None):

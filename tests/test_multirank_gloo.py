@@ -103,3 +103,30 @@ def test_batch_shards_are_disjoint_slices_of_one_global_batch():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == [1.0, 1.0]
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_segment_seed_algebra_reproduces_the_full_horizon_gradient(oracle, mode):
+    """NEXT f2: per-segment VJPs with the seeds of driver.segment_seeds (local prefixes, earlier
+    segments folded into the suffix seed) equal the oracle's gradient over the whole horizon."""
+    from paper_2511_13330_b200 import inputs as qi
+    N, S = 12, 3
+    if mode == 0:
+        p = qi.cfg0(N=N, T=100.0 * N / 256)
+        u = p.u[0]
+    else:
+        p = qi.cfg3()
+        u = oracle.sines_nodes(p.sines, p.u_max, N, 60.0)
+        p.T = 60.0
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    h = p.T / N
+    C = oracle.fidelity_cotangent(p.V)
+    g_full, Lam = oracle.vjp(L0, Lc, u, p.T, N, C, mode=mode)
+    seg = N // S
+    Qs = [oracle.propagate(L0, Lc, u[s * seg:(s + 1) * seg], h * seg, seg, mode=mode) for s in range(S)]
+    seeds = driver.segment_seeds(Qs, C, lambda xs: oracle.ordered_product(np.stack(list(xs))))
+    g_seg = np.concatenate([oracle.vjp(L0, Lc, u[s * seg:(s + 1) * seg], h * seg, seg, seeds[s], mode=mode)[0]
+                            for s in range(S)])
+    assert np.allclose(g_seg, g_full, rtol=0, atol=1e-12 * np.abs(g_full).max())
+    F = oracle.fidelity(Lam, p.V)
+    assert abs(np.trace(C @ Lam).real - F) <= 1e-15           # the cotangent of the fidelity
