@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
     ap.add_argument("--cfg4-slices", type=int, default=8, help="slices per step of the cfg4 sample")
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg3grad", "cfg4", "hubbard3"],
                     help="cfg2: batch fwd+grad (default, weak scaling); cfg3: 2^20-slice horizon, time-sharded")
     return ap.parse_args()
 
@@ -280,6 +280,78 @@ def run_ours(args):
     return 0
 
 
+def run_cfg3grad(args):
+    """NEXT f2: fidelity gradient over the configs[3] horizon (2^20 NODES slices), time-sharded over
+    the ranks and segmented (2^16 slices) on each: slices/s of the whole forward + gradient."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_13330_b200 import _build, driver, inputs as qi, qal
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _build.build()
+    qal.load()
+    prob = qi.cfg3()
+    N, T = prob.N, prob.T
+    k0, k1 = driver.shard_range(N, world, rank)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    H0, Hc, C, V, prm = to(prob.H0), to(prob.Hc), to(prob.C), to(prob.V), to(prob.sines)
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
+
+    def step():
+        u = qal.qal_sample_controls_sines(prm, prob.u_max, N, T, k0, k1 - k0).unsqueeze(0).contiguous()
+        L0, Lc, Lcomm = qal.qal_build_liouvillian(H0, Hc, C, want_comm=True)
+        return driver.time_sharded_gradient(L0, Lc, Lcomm, u, T, N, k0, ctrl_mode=qal.QAL_CTRL_NODES,
+                                            cotangent=lambda Lm: qal.qal_fidelity_cotangent(V))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    counters = torch.zeros(9, dtype=torch.int64, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qal.qal_profile_begin(counters)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    stages = qal.qal_profile_end()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    prods = counters.cpu().tolist()
+    if rank == 0:
+        flops = sum(driver.stage_flops(x) for x in prods) / args.steps
+        line = {"metric": METRIC, "value": N * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": "configs[3] gradient (NEXT f2): 2^20 NODES slices, fidelity gradient w.r.t. "
+                                       "all 2 x 2 x 2^20 node values, time-sharded; 64-slice sub-segments, log-depth prefix/suffix "
+                                       "scans, one batched VJP"},
+                "pct_fp64_roofline": flops / (ms / args.steps * 1e-3) / 1e12 / peak_tf,
+                "products_per_slice": sum(prods) / (N * args.steps),
+                "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
+                "fp64_peak_tflops": peak_tf, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_cfg3(args):
     """configs[3]: one pulse, N = 2^20 NODES slices over 10 us, time-sharded over the ranks
     (strong scaling): a1 device sampler -> a2 basis (+ commutators) -> a3-a5 local chunk fold +
@@ -388,7 +460,7 @@ def run_cfg4(args):
     _build.build()
     qal.load()
     S = args.cfg4_slices
-    prob = qi.cfg4()
+    prob = qi.hubbard3() if args.config == "hubbard3" else qi.cfg4()
     pulse = rank % prob.u.shape[0]
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     L0, Lc, _ = qal.qal_build_liouvillian(to(prob.H0), to(prob.Hc), to(prob.C))
@@ -404,7 +476,7 @@ def run_cfg4(args):
     st = lambda: qal._stream(None)  # noqa: E731
 
     def step():
-        rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, 5, qal._ptr(u), qal._ptr(L0), 0,
+        rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, prob.J, qal._ptr(u), qal._ptr(L0), 0,
                                         qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
                                         ws.numel(), st())
         qal._check(rc, "qal_magnus_expm_slices")
@@ -441,7 +513,7 @@ def run_cfg4(args):
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"configs[4] sample: pulse {pulse}, first {S} of 512 PWC slices, d=64 "
+                "config": {"workload": f"{prob.name} sample: pulse {pulse}, first {S} of {prob.N} PWC slices, d=64 "
                                        f"(4096x4096 c128), expm + fold + fidelity", "slices_per_step": S},
                 "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
                              "frac": ach / peak_tf, "traffic": None, "kernel": "k_dense_gemm",
@@ -458,12 +530,14 @@ def run_cfg4(args):
 
 def main():
     args = parse()
-    if args.config == "cfg4" and args.impl != "reference":
+    if args.config in ("cfg4", "hubbard3") and args.impl != "reference":
         return run_cfg4(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "cfg3":
         return run_cfg3(args)
+    if args.config == "cfg3grad":
+        return run_cfg3grad(args)
     return run_ours(args)
 
 

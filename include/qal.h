@@ -149,6 +149,21 @@ int qal_ordered_product(int n, int batch, int count, const qal_c128 *U, qal_c128
                         size_t ws_bytes, void *stream);
 
 /*
+ * Log-depth scans of Eq. 15 (P:137-141 tree reduction generalised to all prefixes / suffixes;
+ * Hillis-Steele levels, later factor on the LEFT), for single long pulses whose sequential
+ * chains would leave the GPU idle:
+ *   prefix_excl[b][s] = U[b][s-1] ... U[b][0]          (identity at s = 0)
+ *   suffix_excl[b][s] = U[b][count-1] ... U[b][s+1]    (identity at s = count-1)
+ * Either output may be NULL.  U [batch][count][n][n]; ws >= 4 * batch * count * n * n * 16 bytes.
+ */
+int qal_ordered_scan(int n, int batch, int count, const qal_c128 *U, qal_c128 *prefix_excl,
+                     qal_c128 *suffix_excl, void *ws, size_t ws_bytes, void *stream);
+
+/* C[i] = A[i] B[i], i < count, with element strides strideA / strideB = n*n or 0 (broadcast). */
+int qal_batched_matmul(int n, int count, const qal_c128 *A, long long strideA, const qal_c128 *B,
+                       long long strideB, qal_c128 *C, void *stream);
+
+/*
  * Gate (process) fidelity to a target unitary V (A8, replaces Eqs. 16-17 on
  * this path):
  *   F[b] = Re Tr(S_V^dag Lambda[b]) / d^2,  S_V = conj(V) (x) V

@@ -364,6 +364,28 @@ int qal_ordered_product(int n, int batch, int count, const qal_c128* U, qal_c128
   return run_tree(batch, count, D2(U), D2(out), ws, S(stream));
 }
 
+int qal_ordered_scan(int n, int batch, int count, const qal_c128* U, qal_c128* prefix_excl, qal_c128* suffix_excl,
+                     void* ws, size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  if (n != 64) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1 || count < 1) return QAL_ERR_EMPTY;
+  if (!U || (!prefix_excl && !suffix_excl)) return QAL_ERR_NULL;
+  if (!ws || ws_bytes < 4 * (size_t)batch * count * MAT_BYTES) return QAL_ERR_WORKSPACE;
+  return cuda_rc(launch_scan(batch, count, D2(U), D2(prefix_excl), D2(suffix_excl), reinterpret_cast<double2*>(ws),
+                             S(stream)));
+}
+
+int qal_batched_matmul(int n, int count, const qal_c128* A, long long strideA, const qal_c128* B, long long strideB,
+                       qal_c128* C, void* stream) {
+  launch_counter() = 0;
+  if (n != 64) return QAL_ERR_UNSUPPORTED;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (!A || !B || !C) return QAL_ERR_NULL;
+  if ((strideA != 0 && strideA != (long long)PLANE_C) || (strideB != 0 && strideB != (long long)PLANE_C))
+    return QAL_ERR_DIM;
+  return cuda_rc(launch_batched_mm(count, D2(A), strideA, D2(B), strideB, D2(C), S(stream)));
+}
+
 int qal_fidelity(int d, int batch, const qal_c128* Lambda, const qal_c128* V, double* F, void* stream) {
   launch_counter() = 0;
   if (d != 8 && d != 64) return QAL_ERR_UNSUPPORTED;

@@ -62,6 +62,10 @@ cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const dou
 cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, const double* P_img,
                                const double* X_img, double* grad, int* status, double* scratch, double gscale,
                                cudaStream_t st);
+cudaError_t launch_scan(int batch, int cnt, const double2* U, double2* pre, double2* suf, double2* ws,
+                        cudaStream_t st);
+cudaError_t launch_batched_mm(int count, const double2* A, long long sa, const double2* B, long long sb, double2* C,
+                              cudaStream_t st);
 cudaError_t launch_fidelity_cotangent(const double2* V, double2* C, cudaStream_t st);
 // Eqs. 16-17 logical loss + cotangent, and Adam (qal_product.cu)
 cudaError_t launch_logical_loss(int batch, const double2* Lam, const double2* Pproj, const double2* Gt, double* loss,

@@ -45,6 +45,111 @@ cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* ou
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ scans (log-depth prefix/suffix)
+// One Hillis-Steele level over per-pulse sequences of `cnt` matrices (later factor on the LEFT):
+//   prefix (dir 0): out[s] = in[s] in[s-d]  (s >= d), else copy  -> after all levels: U_s ... U_0
+//   suffix (dir 1): out[s] = in[s+d] in[s]  (s+d < cnt), else copy -> U_{cnt-1} ... U_s
+__global__ void __launch_bounds__(NT, 2) k_scan_level(int cnt, int d, int dir, const double2* __restrict__ in,
+                                                      double2* __restrict__ out, unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  const Lane L = lane_id();
+  const int b = blockIdx.x / cnt, s = blockIdx.x % cnt;
+  const double2* src = in + (size_t)b * cnt * PLANE;
+  double2* dst = out + ((size_t)b * cnt + s) * PLANE;
+  const int partner = dir == 0 ? s - d : s + d;
+  if (partner < 0 || partner >= cnt) {
+    for (int e = threadIdx.x; e < PLANE; e += NT) dst[e] = src[(size_t)s * PLANE + e];
+    return;
+  }
+  const int later = dir == 0 ? s : partner, earlier = dir == 0 ? partner : s;
+  block_nat_to_img(smem, src + (size_t)earlier * PLANE);
+  Strip A, acc;
+  load_nat(A, src + (size_t)later * PLANE, L);
+  __syncthreads();
+  zero(acc);
+  mma_acc(acc, A, smem, L);
+  store_nat(dst, acc, L);
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, 1ull);
+}
+
+// exclusive outputs from the inclusive scans: pre[s] = incl_pre[s-1] (I at s = 0),
+// suf[s] = incl_suf[s+1] (I at s = cnt-1)
+__global__ void __launch_bounds__(NT) k_scan_shift(int cnt, const double2* __restrict__ ip, const double2* __restrict__ is,
+                                                   double2* __restrict__ pre, double2* __restrict__ suf) {
+  const int b = blockIdx.x / cnt, s = blockIdx.x % cnt;
+  double2* p = pre + ((size_t)b * cnt + s) * PLANE;
+  double2* q = suf + ((size_t)b * cnt + s) * PLANE;
+  const double2* ps = s > 0 ? ip + ((size_t)b * cnt + s - 1) * PLANE : nullptr;
+  const double2* qs = s + 1 < cnt ? is + ((size_t)b * cnt + s + 1) * PLANE : nullptr;
+  for (int e = threadIdx.x; e < PLANE; e += NT) {
+    const double2 id = make_double2((e >> 6) == (e & 63) ? 1.0 : 0.0, 0.0);
+    if (pre) p[e] = ps ? ps[e] : id;
+    if (suf) q[e] = qs ? qs[e] : id;
+  }
+}
+
+cudaError_t launch_scan(int batch, int cnt, const double2* U, double2* pre, double2* suf, double2* ws,
+                        cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan_level, cudaFuncAttributeMaxDynamicSharedMemorySize, IMG * 8);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const size_t seq = (size_t)batch * cnt * PLANE;
+  double2* buf[2][2] = {{ws, ws + seq}, {ws + 2 * seq, ws + 3 * seq}};   // [dir][ping-pong]
+  const double2* res[2] = {U, U};
+  for (int dir = 0; dir < 2; ++dir) {
+    if ((dir == 0 && !pre) || (dir == 1 && !suf)) continue;
+    const double2* in = U;
+    int pp = 0;
+    for (int d = 1; d < cnt; d <<= 1) {
+      prof_pre(ST_TREE, st);
+      k_scan_level<<<batch * cnt, NT, IMG * 8, st>>>(cnt, d, dir, in, buf[dir][pp], prof_counter(ST_TREE));
+      prof_post(ST_TREE, st);
+      ++launch_counter();
+      in = buf[dir][pp];
+      pp ^= 1;
+    }
+    res[dir] = in;
+  }
+  k_scan_shift<<<batch * cnt, NT, 0, st>>>(cnt, res[0], res[1], pre, suf);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// out[i] = A[i] B[i] with element strides (0 = broadcast); one CTA per product
+__global__ void __launch_bounds__(NT, 2) k_batched_mm(const double2* __restrict__ A, long long sa,
+                                                      const double2* __restrict__ B, long long sb,
+                                                      double2* __restrict__ C, unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  const Lane L = lane_id();
+  const size_t i = blockIdx.x;
+  block_nat_to_img(smem, B + i * sb);
+  Strip a, acc;
+  load_nat(a, A + i * sa, L);
+  __syncthreads();
+  zero(acc);
+  mma_acc(acc, a, smem, L);
+  store_nat(C + i * PLANE, acc, L);
+  if (ctr && threadIdx.x == 0) atomicAdd(ctr, 1ull);
+}
+
+cudaError_t launch_batched_mm(int count, const double2* A, long long sa, const double2* B, long long sb, double2* C,
+                              cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_batched_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, IMG * 8);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prof_pre(ST_TREE, st);
+  k_batched_mm<<<count, NT, IMG * 8, st>>>(A, sa, B, sb, C, prof_counter(ST_TREE));
+  prof_post(ST_TREE, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K5
 // F[b] = Re Tr(S_V^dag Lambda_b) / d^2 with S_V[i+dj, k+dl] = conj(V[j][l]) V[i][k] (A8):
 // F = Re sum V[j][l] conj(V[i][k]) Lambda[i+dj][k+dl] / d^2.  d = 8.  One CTA per pulse.

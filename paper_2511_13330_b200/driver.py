@@ -197,44 +197,51 @@ def segment_seeds(Qs, C, product):
 
 
 def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, cotangent, magnus_order=4,
-                          segment=1 << 16, group=None, stream=None):
-    """NEXT f2 -- gradient of an objective over a long horizon, time-sharded over the ranks and
-    segmented on each rank so the stored images fit HBM.  Rank r owns slices [k0, k0 + count).
-    1. every local segment's partial Q (chunk fold + tree), 2. all-gather the rank partials
-    (NCCL), 3. Lambda and the cotangent C = cotangent(Lambda), 4. per segment: forward (P_init = I)
-    + VJP with the seed of segment_seeds.  Returns (Lambda, grad of the local slices)."""
+                          sub=64, group_subsegments=2048, group=None, stream=None):
+    """NEXT f2 -- gradient of an objective over a long horizon, time-sharded over the ranks, with
+    log-depth parallelism inside each rank.  Rank r owns slices [k0, k0 + count) of ONE pulse
+    (u_local [1][count][...]):
+      1. sub-segment partials Q_s (s < S = count/sub): chunk fold, all sub-segments in parallel;
+      2. exclusive prefix / suffix products of the Q_s: Hillis-Steele scan (qal_ordered_scan);
+      3. all-gather of the rank totals (NCCL); Lambda; C = cotangent(Lambda);
+         rank seed C_r = (ranks before) C (ranks after)... as matrices: B_r C A_r with
+         B_r = Q_{r-1}..Q_0 (earlier ranks) on the left of C and A_r = Q_{G-1}..Q_{r+1} on the right
+      4. sub-segment seeds pre_s C_r suf_s (segment_seeds, batched);
+      5. the VJP of all sub-segments as one batch of short "pulses" (qal_propagator_forward / _vjp),
+         in groups so the stored images fit HBM.
+    Returns (Lambda, grad of the local slices)."""
     count = u_local.shape[1]
-    segment = min(segment, count)
-    if count % segment:
-        raise ValueError("segment must divide the rank's slice count")
-    nseg = count // segment
-    local = []
-    for s in range(nseg):
-        us = u_local[:, s * segment:(s + 1) * segment].contiguous()
-        local.append(local_partial(L0, Lc, Lcomm, us, T, n_slices, k0 + s * segment, ctrl_mode=ctrl_mode,
-                                   magnus_order=magnus_order, stream=stream))
-    Q_rank = local[0] if nseg == 1 else ordered_combine(torch.stack(local), stream=stream)
-    ranks = gather_partials(Q_rank, group)                                  # [G][n][n]
+    if count % sub:
+        raise ValueError("sub must divide the rank's slice count")
+    S = count // sub
+    _, parts = qal.qal_magnus_expm_slices(L0, Lc, u_local, T, n_slices, k0=k0, count=count,
+                                          magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcomm=Lcomm, chunk=sub,
+                                          stream=stream)
+    pre, suf = qal.qal_ordered_scan(parts, stream=stream)                        # [1][S]
+    Q_rank = qal.qal_batched_matmul(parts[:, S - 1], pre[:, S - 1], stream=stream)[0]
+    ranks = gather_partials(Q_rank, group)                                        # [G][n][n]
     rank = _rank(group)
-    before = None if rank == 0 else ordered_combine(ranks[:rank], stream=stream)
-    after = None if rank + 1 == ranks.shape[0] else ordered_combine(ranks[rank + 1:], stream=stream)
     Lam = ordered_combine(ranks, stream=stream)
     C = cotangent(Lam)
-    # the rank's segments see everything before the rank inside their prefix, after it in their suffix
-    prod = lambda xs: qal.qal_ordered_product(torch.stack(list(xs)).unsqueeze(0).contiguous(),  # noqa: E731
-                                              stream=stream)[0]
-    Qs = ([before] if before is not None else []) + local + ([after] if after is not None else [])
-    seeds = segment_seeds(Qs, C, prod)
-    off = 1 if before is not None else 0
-    grad = torch.empty_like(u_local)
-    for s in range(nseg):
-        us = u_local[:, s * segment:(s + 1) * segment].contiguous()
-        sess = qal.GradientSession(L0, Lc, us, T, n_slices, k0=k0 + s * segment, magnus_order=magnus_order,
+    if rank > 0:                     # earlier ranks sit right of the local prefix: C <- B_r C
+        C = qal.qal_batched_matmul(ordered_combine(ranks[:rank], stream=stream).unsqueeze(0), C.unsqueeze(0),
+                                   stream=stream)[0]
+    if rank + 1 < ranks.shape[0]:    # later ranks sit left of the local suffix: C <- C A_r
+        C = qal.qal_batched_matmul(C.unsqueeze(0), ordered_combine(ranks[rank + 1:], stream=stream).unsqueeze(0),
+                                   stream=stream)[0]
+    tmp = qal.qal_batched_matmul(C.unsqueeze(0), suf[0], stream=stream)          # C_r suf_s
+    seeds = qal.qal_batched_matmul(pre[0], tmp, stream=stream)                    # pre_s C_r suf_s
+    del tmp, pre, suf, parts
+    us = u_local[0].reshape((S, sub) + tuple(u_local.shape[2:]))
+    grad = torch.empty_like(us)
+    for g0 in range(0, S, group_subsegments):
+        g1 = min(S, g0 + group_subsegments)
+        sess = qal.GradientSession(L0, Lc, us[g0:g1].contiguous(), T, n_slices, k0=0, magnus_order=magnus_order,
                                    ctrl_mode=ctrl_mode, Lcomm=Lcomm, stream=stream)
         sess.forward()
-        grad[:, s * segment:(s + 1) * segment] = sess.vjp(seeds[off + s].unsqueeze(0).contiguous())
+        grad[g0:g1] = sess.vjp(seeds[g0:g1].contiguous())
         del sess
-    return Lam, grad
+    return Lam, grad.reshape(u_local.shape)
 
 
 def _rank(group=None):

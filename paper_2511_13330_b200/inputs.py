@@ -294,4 +294,87 @@ LOGICAL_GATES = {
 }
 
 
-CONFIGS = {"cfg0": cfg0, "cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
+# --------------------------------------------------------------------------
+# NEXT f3: the paper's own model -- the Hubbard Hamiltonian of Eq. 1 on a chain of
+# quantum dots, each with the 4-dim Fock space {|>, |u>, |d>, |ud>}.
+# A23 (basis): index = base-4 number with digit map {empty 0, up 1, down 2, updown 3},
+#     dot 1 most significant.  A24 (signs): Jordan-Wigner over fermionic modes ordered
+#     (dot-major, up before down), so the operators anticommute exactly.
+# A25 (unstated parameters; synthetic, rad/ns): U~ = 2pi 2.0, V_i = -2pi (0.30, 0.25, 0.30),
+#     U_C = 2pi 0.5; controls are the hoppings t_{i,i+1} in [0, 2pi 0.5].  Jump operators of P:85
+#     with the logical-subspace lowering a = phi_0 phi_1^dag: L1 = a/sqrt(T1), L2 = a^dag a/sqrt(T2).
+# --------------------------------------------------------------------------
+def fock_creation(dot: int, spin: int, n_dots: int) -> np.ndarray:
+    """c^dag_{dot, spin} (spin 0 = up, 1 = down) as a 4^N x 4^N matrix (A23, A24)."""
+    D = 4 ** n_dots
+    mode = 2 * dot + spin
+    out = np.zeros((D, D), dtype=np.complex128)
+    for idx in range(D):
+        digits = [(idx // 4 ** (n_dots - 1 - i)) % 4 for i in range(n_dots)]
+        occ = []
+        for dgt in digits:                      # digit -> (n_up, n_down)
+            occ += [1 if dgt in (1, 3) else 0, 1 if dgt in (2, 3) else 0]
+        if occ[mode]:
+            continue
+        sign = -1.0 if sum(occ[:mode]) % 2 else 1.0
+        occ[mode] = 1
+        new = 0
+        for i in range(n_dots):
+            nu, nd = occ[2 * i], occ[2 * i + 1]
+            new = new * 4 + (0 if (nu, nd) == (0, 0) else 1 if (nu, nd) == (1, 0) else 2 if (nu, nd) == (0, 1) else 3)
+        out[new, idx] = sign
+    return out
+
+
+def fock_number(dot: int, n_dots: int) -> np.ndarray:
+    n = np.zeros((4 ** n_dots,) * 2, dtype=np.complex128)
+    for s in (0, 1):
+        c = fock_creation(dot, s, n_dots)
+        n += c @ c.conj().T
+    return n
+
+
+def hubbard_terms(n_dots: int, U: float, V, UC: float):
+    """(H0, [H_j]): H0 = sum_i [U/2 n_i(n_i - 1) + V_i n_i] + sum_<ij> U_C n_i n_j and the hopping
+    terms H_j = sum_sigma (c^dag_{j sigma} c_{j+1 sigma} + h.c.) whose coefficients t_{j,j+1} are the controls."""
+    D = 4 ** n_dots
+    I = np.eye(D, dtype=np.complex128)
+    ns = [fock_number(i, n_dots) for i in range(n_dots)]
+    H0 = sum(0.5 * U * n @ (n - I) + V[i] * n for i, n in enumerate(ns))
+    H0 = H0 + sum(UC * ns[i] @ ns[i + 1] for i in range(n_dots - 1))
+    Hc = []
+    for j in range(n_dots - 1):
+        h = np.zeros((D, D), dtype=np.complex128)
+        for s in (0, 1):
+            cd_j, cd_k = fock_creation(j, s, n_dots), fock_creation(j + 1, s, n_dots)
+            h += cd_j @ cd_k.conj().T
+        Hc.append(h + h.conj().T)
+    return H0, (np.stack(Hc) if Hc else np.zeros((0, D, D), dtype=np.complex128))
+
+
+def hubbard_logical_states() -> np.ndarray:
+    """Eqs. 2-3 in the 3-dot Fock space (one electron per dot): phi_0 = (|u u d> - |d u u>)/sqrt2,
+    phi_1 (A22 standard DFS) = (2|u d u> - |u u d> - |d u u>)/sqrt6; base-4 indices per A23."""
+    def ket(s):
+        v = np.zeros(64, dtype=np.complex128)
+        v[sum((1 if c == "u" else 2) * 4 ** (2 - i) for i, c in enumerate(s))] = 1.0
+        return v
+    phi0 = (ket("uud") - ket("duu")) / math.sqrt(2.0)
+    phi1 = (2.0 * ket("udu") - ket("uud") - ket("duu")) / math.sqrt(6.0)
+    return np.stack([phi0, phi1])
+
+
+def hubbard3(seed: int = 7, N: int = 512, T: float = 100.0, batch: int = 1) -> Problem:
+    """NEXT f3: the paper's 3-dot Hubbard workload (D = 64, 4096 x 4096 superoperators, Fig. 1 /
+    P:147); T and M are unstated in the paper (A25), chosen like configs[4]."""
+    H0, Hc = hubbard_terms(3, TWO_PI * 2.0, -TWO_PI * np.array([0.30, 0.25, 0.30]), TWO_PI * 0.5)
+    phi0, phi1 = hubbard_logical_states()
+    a = np.outer(phi0, phi1.conj())
+    C = np.stack([a / math.sqrt(T1_NS), (a.conj().T @ a) / math.sqrt(T2_NS)])
+    u = np.empty((batch, N, 2))
+    for p in range(batch):
+        u[p] = TWO_PI * 0.5 * uniform(seed, "hubbard", p, 2 * N).reshape(N, 2)
+    return Problem("hubbard3", 64, H0[None].copy(), Hc, C, T, N, u, CTRL_PWC, haar_unitary(64, seed))
+
+
+CONFIGS = {"cfg0": cfg0, "cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "hubbard3": hubbard3}

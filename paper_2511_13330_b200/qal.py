@@ -67,6 +67,10 @@ _EXPORTS = {
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_ordered_scan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_batched_matmul": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
+                                           ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]),
     "qal_fidelity_cotangent": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "qal_logical_loss": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
@@ -208,6 +212,31 @@ def qal_ordered_product(U, stream=None):
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=U.device)
     rc = load().qal_ordered_product(n, B, count, _ptr(U), _ptr(out), _ptr(ws), wsb, _stream(stream))
     _check(rc, "qal_ordered_product")
+    return out
+
+
+def qal_ordered_scan(U, want_prefix=True, want_suffix=True, stream=None):
+    """Exclusive prefix / suffix products of U [B][count][n][n] (later on the LEFT)."""
+    U = _dev(U, torch.complex128, "U")
+    B, cnt, n = U.shape[0], U.shape[1], U.shape[2]
+    pre = torch.empty_like(U) if want_prefix else None
+    suf = torch.empty_like(U) if want_suffix else None
+    ws = torch.empty(4 * B * cnt * n * n * 16, dtype=torch.uint8, device=U.device)
+    rc = load().qal_ordered_scan(n, B, cnt, _ptr(U), _ptr(pre), _ptr(suf), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "qal_ordered_scan")
+    return pre, suf
+
+
+def qal_batched_matmul(A, B, stream=None):
+    """A [count|1][n][n] @ B [count|1][n][n] -> [count][n][n] (broadcast a leading 1)."""
+    A = _dev(A, torch.complex128, "A")
+    B = _dev(B, torch.complex128, "B")
+    cnt = max(A.shape[0], B.shape[0])
+    n = A.shape[-1]
+    out = torch.empty((cnt, n, n), dtype=torch.complex128, device=A.device)
+    rc = load().qal_batched_matmul(n, cnt, _ptr(A), 0 if A.shape[0] == 1 else n * n, _ptr(B),
+                                   0 if B.shape[0] == 1 else n * n, _ptr(out), _stream(stream))
+    _check(rc, "qal_batched_matmul")
     return out
 
 

@@ -132,3 +132,49 @@ def test_dense_full_pulse_invariants_and_fidelity_path(cfg4, qal, torch_cuda):
     Lam = Lg[0].cpu().numpy()
     check_cptp_invariants(Lam, 1e-10)
     assert 0.0 < F.item() < 1.0
+
+
+# ------------------------------------------------------------------ NEXT f3: 3-dot Hubbard model (Eq. 1)
+@pytest.fixture(scope="module")
+def hub(torch_cuda, qal):
+    torch = torch_cuda
+    p = qi.hubbard3(N=2, T=100.0 * 2 / 512)
+    L0, Lc, _ = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C))
+    return p, L0, Lc
+
+
+def test_hubbard_liouvillian_matches_oracle(hub, oracle):
+    p, L0, Lc = hub
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    assert np.max(np.abs(L0[0].cpu().numpy() - rL0)) <= 1e-13
+    assert np.max(np.abs(Lc.cpu().numpy() - rLc)) <= 1e-13
+
+
+def test_hubbard_zero_dissipation_is_conj_u_kron_u(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    p = qi.hubbard3(N=4, T=100.0 * 4 / 512)
+    L0, Lc, _ = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), None)
+    _, P = qal.qal_magnus_expm_slices(L0, Lc, to(torch, p.u), p.T, p.N, chunk=p.N)
+    h = p.T / p.N
+    U = np.eye(64, dtype=np.complex128)
+    for k in range(p.N):
+        Hk = p.H0[0] + sum(p.u[0, k, j] * p.Hc[j] for j in range(2))
+        U = oracle.matmul(oracle.expm(-1j * h * Hk), U)
+    assert relfro(P[0, 0].cpu().numpy(), np.kron(U.conj(), U)) <= 1e-10
+
+
+def test_hubbard_dissipative_slice_vs_rk4_on_rho(torch_cuda, qal, oracle):
+    """one slice (||Omega||_1 ~ 25: s = 5 squarings on the device) applied to a density matrix vs the
+    oracle's RK4 of Eq. 6 with 8192 sub-steps (global RK4 error ~ 2e-11)."""
+    torch = torch_cuda
+    p = qi.hubbard3(N=1, T=100.0 / 512)
+    L0, Lc, _ = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C))
+    _, P = qal.qal_magnus_expm_slices(L0, Lc, to(torch, p.u), p.T, 1, chunk=1)
+    Lam = P[0, 0].cpu().numpy()
+    phis = qi.hubbard_logical_states()
+    rho0 = 0.7 * np.outer(phis[0], phis[0].conj()) + 0.3 * np.outer(phis[1], phis[1].conj())
+    rho0 += 0.2 * (np.outer(phis[0], phis[1].conj()) + np.outer(phis[1], phis[0].conj()))
+    ref = oracle.evolve_rho(p.H0[0], p.Hc, p.C, p.u[0], p.T, 1, 8192, rho0)
+    got = (Lam @ rho0.reshape(-1, order="F")).reshape(64, 64, order="F")
+    assert relfro(got, ref) <= 1e-10
+    check_cptp_invariants(Lam, 1e-10)

@@ -44,7 +44,7 @@ def test_segmented_nodes_gradient_matches_oracle(torch_cuda, qal, oracle):
     L0, Lc, Lcomm = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C), want_comm=True)
     V = to(torch, p.V)
     Lam, g = driver.time_sharded_gradient(L0, Lc, Lcomm, to(torch, u[None]), T, N, 0, ctrl_mode=1,
-                                          cotangent=lambda Lm: qal.qal_fidelity_cotangent(V), segment=64)
+                                          cotangent=lambda Lm: qal.qal_fidelity_cotangent(V), sub=32)
     rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
     Fr, gr, Lr = oracle.gradient(rL0, rLc, u, T, N, p.V, mode=1)
     assert relfro(Lam.cpu().numpy(), Lr) <= 1e-10

@@ -299,3 +299,29 @@ def test_sines_sampler_matches_oracle(torch_cuda, qal, oracle, k0, count):
     ref = oracle.sines_nodes(p.sines, p.u_max, p.N, p.T, k0, k0 + count)
     assert got.shape == ref.shape
     assert np.max(np.abs(got - ref)) <= 1e-13 * p.u_max
+
+
+# ------------------------------------------------------------------ log-depth scans
+@pytest.mark.parametrize("count", [1, 2, 5, 13, 64])
+def test_ordered_scan_matches_oracle(torch_cuda, qal, oracle, count):
+    torch = torch_cuda
+    rng = np.random.default_rng(count)
+    U = (rng.standard_normal((2, count, 64, 64)) + 1j * rng.standard_normal((2, count, 64, 64))) / 8.0
+    pre, suf = qal.qal_ordered_scan(dev(torch, U))
+    pre, suf = pre.cpu().numpy(), suf.cpu().numpy()
+    I = np.eye(64)
+    for b in range(2):
+        for s in range(count):
+            rp = oracle.ordered_product(U[b, :s]) if s > 0 else I
+            rs = oracle.ordered_product(U[b, s + 1:]) if s + 1 < count else I
+            assert relfro(pre[b, s], rp) <= 1e-12 and relfro(suf[b, s], rs) <= 1e-12
+
+
+def test_batched_matmul_broadcast(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((1, 64, 64)) + 1j * rng.standard_normal((1, 64, 64))
+    B = rng.standard_normal((4, 64, 64)) + 1j * rng.standard_normal((4, 64, 64))
+    C = qal.qal_batched_matmul(dev(torch, A), dev(torch, B)).cpu().numpy()
+    for i in range(4):
+        assert relfro(C[i], oracle.matmul(A[0], B[i])) <= 1e-14
