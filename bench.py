@@ -505,7 +505,7 @@ def run_cfg4(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = t.item()
     g_ms, g_l = stages["dense_gemm"]
-    flops_per_product = 8.0 * n ** 3
+    flops_per_product = driver.complex_product_flops(n)
     nprod = counters.cpu().tolist()[qal.STAGES.index("dense_gemm")]   # executed 4096^2 products
     if rank == 0:
         ach = nprod * flops_per_product / (g_ms * 1e-3) / 1e12

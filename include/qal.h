@@ -74,6 +74,14 @@ enum {                   /* op codes for qal_workspace_bytes */
 #define QAL_ABI_VERSION 1
 
 int qal_abi_version(void);
+
+/*
+ * Real FP64 matrix multiplications the library spends per complex matrix product:
+ * 3 (Gauss / "3M": P = Ar Br, Q = Ai Bi, R = (Ar+Ai)(Br+Bi); Re = P - Q, Im = R - P - Q)
+ * when built with -DQAL_USE_3M, else 4 (the default).  Algorithmic flop accounting counts
+ * 2 n^3 per real multiplication, i.e. 6 n^3 per complex product for the 3M form.
+ */
+int qal_real_mults_per_complex_product(void);
 const char *qal_status_string(int code);
 
 /*

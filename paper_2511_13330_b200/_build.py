@@ -11,7 +11,7 @@ OUT = os.path.join(HERE, "libqal.so")
 SOURCES = ["qal_api.cu", "qal_magnus.cu", "qal_product.cu", "qal_grad.cu", "qal_dense.cu"]
 HEADERS = ["qal_dev.cuh", "qal_slice.cuh", "qal_internal.h", "../../include/qal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+FLAGS = [*os.environ.get("QAL_NVCC_EXTRA", "").split(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 

@@ -232,6 +232,8 @@ extern "C" {
 
 int qal_abi_version(void) { return QAL_ABI_VERSION; }
 
+int qal_real_mults_per_complex_product(void) { return qal::QAL_REAL_MMAS_PER_CMMA; }
+
 const char* qal_status_string(int code) {
   switch (code) {
     case QAL_OK: return "ok";

@@ -196,8 +196,8 @@ __device__ __forceinline__ double lds_v(uint32_t a) {
   asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
-__device__ __forceinline__ void mma_acc(Strip& acc, const Strip& a, const double* __restrict__ Bs,
-                                        const Lane& L) {
+__device__ __forceinline__ void mma_acc_4m(Strip& acc, const Strip& a, const double* __restrict__ Bs,
+                                           const Lane& L) {
   const int todd = L.t & 1;
   // row 4q+t of B; physical tile of output tile j is j ^ (t & 1)
   const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);  // even j: tile j + todd
@@ -231,6 +231,88 @@ __device__ __forceinline__ void mma_acc(Strip& acc, const Strip& a, const double
   }
   QAL_FENCE();
 }
+
+// Same product with 3 real MMAs per complex 8x8x4 step (Gauss / "3M"):
+//   P = Ar Br,  Q = Ai Bi,  R = (Ar + Ai)(Br + Bi);   Re = P - Q,  Im = R - P - Q.
+// The existing accumulator is folded in by initialising P = acc.re, R = acc.re + acc.im
+// (so P and R live in the acc registers; only Q is extra).  The output columns are done in
+// two halves of 4 tiles, which keeps Q and the B prefetch at 8 + 16 doubles.  The operand
+// sums Ar + Ai (once per k-step) and Br + Bi (per tile) are DADDs: 160 per product per
+// thread against 384 DMMAs (each 16 pipe cycles per warp), i.e. 25% fewer tensor-pipe
+// cycles than mma_acc_4m.  Normwise the rounding error stays O(u |A| |B|).
+
+// an add the compiler may not CSE across the two column halves (it would keep 16 sums
+// live through the first half and spill them)
+__device__ __forceinline__ double dadd_opaque(double x, double y) {
+  double z;
+  asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(z) : "d"(x), "d"(y));
+  return z;
+}
+__device__ __forceinline__ void mma_acc_3m(Strip& acc, const Strip& a, const double* __restrict__ Bs,
+                                           const Lane& L) {
+  const int todd = L.t & 1;
+  const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);
+  const uint32_t bO = smem_u32(Bs + L.t * 64 + L.g - 8 * todd);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double Q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      Q[i] = 0.0;
+      acc.im[8 * h + i] += acc.re[8 * h + i];  // R = acc.re + acc.im
+    }
+    double br[2][4], bi[2][4];
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * h + jj;
+      const uint32_t p = ((j & 1) ? bO : bE) + 8u * (8 * j);
+      br[0][jj] = lds_v(p);
+      bi[0][jj] = lds_v(p + 8u * PLANE);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int cur = q & 1;
+      if (q + 1 < 16) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = 4 * h + jj;
+          const uint32_t p = ((j & 1) ? bO : bE) + 8u * ((q + 1) * 256 + 8 * j);
+          br[cur ^ 1][jj] = lds_v(p);
+          bi[cur ^ 1][jj] = lds_v(p + 8u * PLANE);
+        }
+      }
+      const double ar = a.re[q], ai = a.im[q], as = dadd_opaque(ar, ai);
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * h + jj;
+        const double bs = br[cur][jj] + bi[cur][jj];
+        dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br[cur][jj]);   // P
+        dmma(Q[2 * jj], Q[2 * jj + 1], ai, bi[cur][jj]);           // Q
+        dmma(acc.im[2 * j], acc.im[2 * j + 1], as, bs);            // R
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double p = acc.re[8 * h + i], s = p + Q[i];
+      acc.re[8 * h + i] = p - Q[i];
+      acc.im[8 * h + i] -= s;
+    }
+  }
+  QAL_FENCE();
+}
+
+// The product every kernel uses.  Default: the 4-MMA form.  -DQAL_USE_3M selects the Gauss
+// form; measured on B200 (cfg2 fwd+grad): 661k -> 736k slices/s (+11%, not the 25% the DMMA
+// count promises: the operand DADDs share the FP64 pipe and the extra live values spill), with
+// ~10x larger rounding in the invariants (Hermiticity defect 2.4e-13 after 256 slices).  Kept
+// as an option, not the default.
+#ifdef QAL_USE_3M
+constexpr int QAL_REAL_MMAS_PER_CMMA = 3;
+#define mma_acc mma_acc_3m
+#else
+constexpr int QAL_REAL_MMAS_PER_CMMA = 4;
+#define mma_acc mma_acc_4m
+#endif
 
 // ---------------------------------------------------------------- Tensor Memory scratch
 // 512 columns x 128 lanes x 32 bit.  Warp w reaches lanes 32(w%4)..+31; warps w and

@@ -274,10 +274,17 @@ def fp64_peak(sink, blocks, seconds=0.2, kind=0):
 MATMUL_FLOPS_64 = 8.0 * 64 ** 3     # one 64x64 complex product (ZGEMM convention)
 
 
+def complex_product_flops(n: int = 64) -> float:
+    """Algorithmic flops of one n x n complex product as the library executes it: 2 n^3 per real
+    multiplication, 3 of them for the Gauss (3M) form -> 6 n^3 (a 3M product counts
+    6 n^3 so the roofline fraction is not inflated), 8 n^3 for the default 4M build."""
+    return 2.0 * n ** 3 * qal.real_mults_per_complex_product()
+
+
 def stage_flops(products: int) -> float:
-    return products * MATMUL_FLOPS_64
+    return products * complex_product_flops(64)
 
 
 __all__ = ["PulseBatch", "shard_range", "time_shard_chunk", "time_shard_propagator", "ordered_combine",
            "gather_partials", "local_partial", "calibrate", "segment_seeds", "time_sharded_gradient", "fp64_peak",
-           "MATMUL_FLOPS_64", "stage_flops", "math"]
+           "MATMUL_FLOPS_64", "complex_product_flops", "stage_flops", "math"]

@@ -32,6 +32,7 @@ KERNELS = {"liouvillian": "k_liouvillian", "commutators": "k_commutators", "expm
 
 _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
+    "qal_real_mults_per_complex_product": (ctypes.c_int, []),
     "qal_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "qal_last_launch_count": (ctypes.c_int, []),
     "qal_default_chunk": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
@@ -133,6 +134,11 @@ def _dev(t, dtype, name):
 
 def abi_version() -> int:
     return load().qal_abi_version()
+
+
+def real_mults_per_complex_product() -> int:
+    """4 (default build), 3 for a -DQAL_USE_3M build (Gauss complex product)."""
+    return load().qal_real_mults_per_complex_product()
 
 
 def last_launch_count() -> int:
