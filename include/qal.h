@@ -53,7 +53,8 @@ enum {
     QAL_ERR_NONFINITE = -4,   /* non-finite scalar argument, or device status flag   */
     QAL_ERR_UNSUPPORTED = -5, /* d / n / n_ctrl / mode outside what is implemented   */
     QAL_ERR_WORKSPACE = -6,   /* ws NULL or ws_bytes < qal_workspace_bytes(...)       */
-    QAL_ERR_CUDA = -7         /* a CUDA launch failed (cudaGetLastError)              */
+    QAL_ERR_CUDA = -7,        /* a CUDA launch failed (cudaGetLastError)              */
+    QAL_ERR_STRUCTURE = -8    /* block path: an operator couples two blocks of the plan */
 };
 
 enum {
@@ -273,6 +274,99 @@ int qal_default_chunk(int batch, int n_slices);
  */
 int qal_fp64_peak_probe(int kind, int blocks, int iters, double *flops, double *sink, void *stream);
 
+/* ===================================================================================
+ * Coherence-block path (pin P-13).  Every operator of the problem
+ * conserves total S_z (Eq. 6), so the superoperators of Eq. 8 and
+ * everything built from them by Eqs. 13-15 are block diagonal by coherence
+ * order q = m_a - m_b (d = 8: blocks 20/15/15/6/6/1/1).  Hermiticity preservation
+ * (Lambda[s(R), s(C)] = conj(Lambda[R, C]), s(i + d j) = j + d i) pairs q with -q.
+ * The path computes exactly the same Omega_k, U_k, Lambda, F and dF/du as the dense path,
+ * restricted to the blocks (2.9% of the dense flops with the mirror).
+ *
+ * A PACKED matrix is the concatenation of the plan's super-block matrices (groups g of
+ * padded width width[g] = 8, 16 or 24; each row-major complex128, entries on padding
+ * rows / columns are 0), `packed` complex elements in total.  Packed row row0[g] + r is
+ * natural index perm[row0[g] + r] (-1 = padding).
+ * =================================================================================== */
+#define QAL_BLK_MAX_GROUPS 16
+#define QAL_BLK_MAX_ROWS 96
+
+typedef struct {
+    int n;                              /* superoperator dimension (64)                       */
+    int d;                              /* Hilbert dimension (8)                              */
+    int mirror;                         /* 1: one block of every Hermitian-mirror pair stored */
+    int ngroups;                        /* super-blocks                                       */
+    int nrows;                          /* packed rows = sum of widths (<= QAL_BLK_MAX_ROWS)   */
+    int packed;                         /* complex elements per packed matrix = sum width^2   */
+    int n_components;                   /* connected components of the basis sparsity graph  */
+    int width[QAL_BLK_MAX_GROUPS];      /* padded width of group g: 8, 16 or 24               */
+    int row0[QAL_BLK_MAX_GROUPS];       /* first packed row of group g                        */
+    int off[QAL_BLK_MAX_GROUPS];        /* complex offset of group g inside a packed matrix   */
+    double flops[QAL_BLK_MAX_GROUPS];   /* algorithmic flops of one product of group g:
+                                           8 sum_{components} s^3 (padding excluded)          */
+    int perm[QAL_BLK_MAX_ROWS];         /* packed row -> natural index, -1 = padding          */
+    int weight[QAL_BLK_MAX_ROWS];       /* 0 padding, 1 self-mirror component (or mirror
+                                           off), 2 component whose mirror is implied         */
+    int inv[64];                        /* natural index -> packed row, -1 = not stored       */
+    int comp[64];                       /* natural index -> component id                      */
+} qal_block_plan;
+
+/*
+ * Structure detection (host only, no device work): the connected components of the union
+ * sparsity pattern of `nmat` HOST matrices mats[nmat][n][n] (pass every generator the
+ * calls will use: L0 of every pulse or a representative plus k_blk_check, L_j, commutators),
+ * the Hermitian mirror pairing (QAL_ERR_STRUCTURE if it does not map components onto
+ * components) and a first-fit-decreasing packing into super-blocks.  n must be 64;
+ * components larger than 24 -> QAL_ERR_UNSUPPORTED.
+ */
+int qal_block_plan_build(int n, int nmat, const qal_c128 *mats, int mirror, qal_block_plan *plan);
+
+/*
+ * natural [count][n][n] (device) -> packed [count][plan->packed] (device).  If `flag` (device
+ * int, caller-zeroed) is not NULL the call also verifies that every entry coupling two
+ * different components is exactly zero and sets *flag = QAL_ERR_STRUCTURE otherwise.
+ */
+int qal_block_pack(const qal_block_plan *plan, int count, const qal_c128 *nat, qal_c128 *packed, int *flag,
+                   void *stream);
+
+/* packed -> natural [count][n][n]; blocks of mirrored components are filled from their stored
+ * partner by Lambda[s(R), s(C)] = conj(Lambda[R, C]); entries between components are 0. */
+int qal_block_unpack(const qal_block_plan *plan, int count, const qal_c128 *packed, qal_c128 *nat, void *stream);
+
+/*
+ * qal_magnus_expm_slices on packed operands: L0p [batch|1][packed] (L0p_stride = packed or 0),
+ * Lcp [J][packed], Lcommp [batch|1][ncomm][packed] (NODES + order 4 only; stride ncomm*packed
+ * or 0).  Output chunk_prod [batch][count/chunk][packed] (required).  No workspace.
+ * Other arguments and errors as qal_magnus_expm_slices.
+ */
+int qal_block_expm_slices(const qal_block_plan *plan, int batch, int n_slices, double T, int k0, int count,
+                          int magnus_order, int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0p,
+                          long long L0p_stride, const qal_c128 *Lcp, const qal_c128 *Lcommp,
+                          long long Lcommp_stride, int chunk, qal_c128 *chunk_prod, int *status, void *stream);
+
+/* qal_ordered_product on packed matrices: out[b] = U[b][count-1] ... U[b][0] (same tree shape).
+ * ws >= qal_block_workspace_bytes(plan, QAL_OP_ORDERED_PRODUCT, batch, count). */
+int qal_block_ordered_product(const qal_block_plan *plan, int batch, int count, const qal_c128 *U, qal_c128 *out,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/* qal_fidelity on packed Lambda (mirrored components counted twice). */
+int qal_block_fidelity(const qal_block_plan *plan, int batch, const qal_c128 *Lambda_packed, const qal_c128 *V,
+                       double *F, void *stream);
+
+/*
+ * qal_fidelity_grad on packed operands (plan built with mirror = 1 or 0; the fidelity cotangent
+ * S_V^dag is Hermiticity preserving, so the mirror is exact).  Lambda_packed optional out
+ * [batch][packed].  ws >= qal_block_workspace_bytes(plan, grad ? QAL_OP_FIDELITY_GRAD :
+ * QAL_OP_FIDELITY, batch, n_slices).
+ */
+int qal_block_fidelity_grad(const qal_block_plan *plan, int batch, int n_slices, double T, int magnus_order,
+                            int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0p, long long L0p_stride,
+                            const qal_c128 *Lcp, const qal_c128 *Lcommp, long long Lcommp_stride,
+                            const qal_c128 *V, double *F, double *grad, qal_c128 *Lambda_packed, int *status,
+                            void *ws, size_t ws_bytes, void *stream);
+
+size_t qal_block_workspace_bytes(const qal_block_plan *plan, int op, int batch, int n_slices);
+
 /*
  * Stage profiling (bench.py's roofline and the expm-vs-product split, the Fig. 2
  * analog of P:167-171).  Between qal_profile_begin and qal_profile_end every kernel
@@ -285,7 +379,11 @@ int qal_fp64_peak_probe(int kind, int blocks, int iters, double *flops, double *
  * Not thread-safe; one profiling window per process at a time.
  */
 enum { QAL_ST_LIOUV = 0, QAL_ST_COMM = 1, QAL_ST_EXPM = 2, QAL_ST_TREE = 3, QAL_ST_FID = 4,
-       QAL_ST_PREFIX = 5, QAL_ST_SUFFIX = 6, QAL_ST_GRAD = 7, QAL_ST_DENSE_GEMM = 8, QAL_NSTAGE = 9 };
+       QAL_ST_PREFIX = 5, QAL_ST_SUFFIX = 6, QAL_ST_GRAD = 7, QAL_ST_DENSE_GEMM = 8,
+       /* coherence-block path: these counters accumulate ALGORITHMIC FLOPs (8 s^3 per complex
+        * product of an s x s block, padding excluded), not product counts */
+       QAL_ST_BLK_EXPM = 9, QAL_ST_BLK_TREE = 10, QAL_ST_BLK_PREFIX = 11, QAL_ST_BLK_SUFFIX = 12,
+       QAL_ST_BLK_GRAD = 13, QAL_NSTAGE = 14 };
 int qal_profile_begin(unsigned long long *dev_counters);
 int qal_profile_end(double *ms, int *launches);
 

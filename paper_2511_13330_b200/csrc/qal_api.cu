@@ -163,6 +163,101 @@ struct Common {
   SliceGrid G;
 };
 
+// ------------------------------------------------------------------ coherence-block path
+int check_plan(const qal_block_plan* p) {
+  if (!p) return QAL_ERR_NULL;
+  if (p->n != 64 || p->d != 8 || p->ngroups < 1 || p->ngroups > QAL_BLK_MAX_GROUPS) return QAL_ERR_UNSUPPORTED;
+  if (p->nrows < 8 || p->nrows > QAL_BLK_MAX_ROWS || p->nrows % 8) return QAL_ERR_DIM;
+  int row = 0, off = 0;
+  for (int g = 0; g < p->ngroups; ++g) {
+    const int w = p->width[g];
+    if (w < 8 || w > 24 || w % 8 || p->row0[g] != row || p->off[g] != off) return QAL_ERR_DIM;
+    row += w;
+    off += w * w;
+  }
+  if (row != p->nrows || off != p->packed) return QAL_ERR_DIM;
+  for (int r = 0; r < p->nrows; ++r)
+    if (p->perm[r] < -1 || p->perm[r] >= 64 || p->weight[r] < 0 || p->weight[r] > 2) return QAL_ERR_DIM;
+  return QAL_OK;
+}
+
+struct BlkCommon {
+  BlkBasis B;
+  SliceGrid G;
+};
+int check_block_basis(const qal_block_plan* p, int batch, int n_slices, double T, int order, int mode, int J,
+                      const double* u, const qal_c128* L0, long long L0s, const qal_c128* Lc, const qal_c128* Lcomm,
+                      long long Lcs, BlkCommon& c) {
+  int rc = check_plan(p);
+  if (rc != QAL_OK) return rc;
+  if (batch < 1 || n_slices < 1) return QAL_ERR_EMPTY;
+  if (!is_fin(T) || T <= 0.0) return QAL_ERR_NONFINITE;
+  if (order != 2 && order != 4) return QAL_ERR_UNSUPPORTED;
+  if (mode != QAL_CTRL_PWC && mode != QAL_CTRL_NODES) return QAL_ERR_UNSUPPORTED;
+  if (J < 1 || J > QAL_MAX_CTRL) return QAL_ERR_UNSUPPORTED;
+  if (!u || !L0 || !Lc) return QAL_ERR_NULL;
+  if (L0s != 0 && L0s != (long long)p->packed) return QAL_ERR_DIM;
+  const bool comm = (mode == QAL_CTRL_NODES && order == 4);
+  if (comm && !Lcomm) return QAL_ERR_NULL;
+  if (comm && Lcs != 0 && Lcs != (long long)ncomm_of(J) * p->packed) return QAL_ERR_DIM;
+  const double h = T / n_slices;
+  c.B.L0 = D2(L0);
+  c.B.L0_stride = L0s;
+  c.B.Lc = D2(Lc);
+  c.B.Lcomm = comm ? D2(Lcomm) : nullptr;
+  c.B.Lcomm_stride = comm ? Lcs : 0;
+  c.B.J = J;
+  c.B.ncomm = comm ? ncomm_of(J) : 0;
+  c.B.packed = p->packed;
+  c.G.h = h;
+  c.G.c4 = (order == 4) ? std::sqrt(3.0) * h * h / 12.0 : 0.0;
+  c.G.mode = mode;
+  c.G.u = u;
+  c.G.count = n_slices;
+  return QAL_OK;
+}
+
+size_t blk_mat_bytes(const qal_block_plan* p) { return (size_t)p->packed * 16; }
+
+size_t blk_tree_ws_bytes(const qal_block_plan* p, int batch, int count) {
+  if (count <= 2) return 0;
+  const size_t c1 = (size_t)(count + 1) / 2, c2 = (c1 + 1) / 2;
+  return (size_t)batch * (c1 + c2) * blk_mat_bytes(p);
+}
+
+int run_blk_tree(const qal_block_plan* p, int batch, int count, const double2* U, double2* out, void* ws,
+                 cudaStream_t st) {
+  const size_t mb = blk_mat_bytes(p);
+  if (count == 1) return cuda_rc(cudaMemcpyAsync(out, U, (size_t)batch * mb, cudaMemcpyDeviceToDevice, st));
+  const size_t c1 = (size_t)(count + 1) / 2;
+  double2* bufA = reinterpret_cast<double2*>(ws);
+  double2* bufB = bufA ? bufA + (size_t)batch * c1 * p->packed : nullptr;
+  const double2* in = U;
+  int cnt = count, lvl = 0;
+  while (cnt > 1) {
+    const int half = (cnt + 1) / 2;
+    double2* dst = (half == 1) ? out : ((lvl & 1) ? bufB : bufA);
+    if (launch_blk_tree_level(*p, batch, cnt, in, dst, st) != cudaSuccess) return QAL_ERR_CUDA;
+    in = dst;
+    cnt = half;
+    ++lvl;
+  }
+  return QAL_OK;
+}
+
+size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices);
+int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
+                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st);
+
+// chunk of the block forward fold: keep >= ~4 CTAs per SM busy, chunk | n_slices
+int blk_default_chunk(int batch, int n_slices) {
+  const long long want = 4LL * num_sms();
+  int ch = n_slices;
+  while (ch > 1 && (long long)batch * (n_slices / ch) < want && (ch % 2) == 0) ch /= 2;
+  return ch;
+}
+
+
 int check_basis(int n_or_d_ok, int batch, int n_slices, double T, int order, int mode, int J, const double* u,
                 const qal_c128* L0, long long L0s, const qal_c128* Lc, const qal_c128* Lcomm, long long Lcs,
                 Common& c, bool dense = false) {
@@ -564,4 +659,130 @@ int qal_fp64_peak_probe(int kind, int blocks, int iters, double* flops, double* 
   return cuda_rc(launch_fp64_probe(kind, blocks, iters, sink, S(stream)));
 }
 
+
+int qal_block_plan_build(int n, int nmat, const qal_c128* mats, int mirror, qal_block_plan* plan) {
+  launch_counter() = 0;
+  if (!mats || !plan) return QAL_ERR_NULL;
+  if (nmat < 1) return QAL_ERR_EMPTY;
+  return build_block_plan(n, nmat, D2(mats), mirror, plan);
+}
+
+int qal_block_pack(const qal_block_plan* plan, int count, const qal_c128* nat, qal_c128* packed, int* flag,
+                   void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (!nat || !packed) return QAL_ERR_NULL;
+  return cuda_rc(launch_blk_pack(*plan, count, D2(nat), D2(packed), flag, S(stream)));
+}
+
+int qal_block_unpack(const qal_block_plan* plan, int count, const qal_c128* packed, qal_c128* nat, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (!nat || !packed) return QAL_ERR_NULL;
+  return cuda_rc(launch_blk_unpack(*plan, count, D2(packed), D2(nat), S(stream)));
+}
+
+int qal_block_expm_slices(const qal_block_plan* plan, int batch, int n_slices, double T, int k0, int count,
+                          int magnus_order, int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0p,
+                          long long L0p_stride, const qal_c128* Lcp, const qal_c128* Lcommp,
+                          long long Lcommp_stride, int chunk, qal_c128* chunk_prod, int* status, void* stream) {
+  launch_counter() = 0;
+  BlkCommon c;
+  int rc = check_block_basis(plan, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0p, L0p_stride, Lcp,
+                             Lcommp, Lcommp_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (chunk < 1 || count % chunk) return QAL_ERR_DIM;
+  if (!chunk_prod) return QAL_ERR_NULL;
+  c.G.count = count;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+  BlkFwdOut O{nullptr, D2(chunk_prod), chunk, status};
+  return cuda_rc(launch_blk_expm_fold(*plan, batch, c.B, c.G, O, st));
+}
+
+int qal_block_ordered_product(const qal_block_plan* plan, int batch, int count, const qal_c128* U, qal_c128* out,
+                              void* ws, size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (batch < 1 || count < 1) return QAL_ERR_EMPTY;
+  if (!U || !out) return QAL_ERR_NULL;
+  const size_t need = blk_tree_ws_bytes(plan, batch, count);
+  if (need && (!ws || ws_bytes < need)) return QAL_ERR_WORKSPACE;
+  return run_blk_tree(plan, batch, count, D2(U), D2(out), ws, S(stream));
+}
+
+int qal_block_fidelity(const qal_block_plan* plan, int batch, const qal_c128* Lambda_packed, const qal_c128* V,
+                       double* F, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (batch < 1) return QAL_ERR_EMPTY;
+  if (!Lambda_packed || !V || !F) return QAL_ERR_NULL;
+  return cuda_rc(launch_blk_fidelity(*plan, batch, D2(Lambda_packed), D2(V), F, S(stream)));
+}
+
+size_t qal_block_workspace_bytes(const qal_block_plan* plan, int op, int batch, int n_slices) {
+  if (check_plan(plan) != QAL_OK || batch < 1 || n_slices < 1) return 0;
+  const size_t mb = blk_mat_bytes(plan);
+  switch (op) {
+    case QAL_OP_ORDERED_PRODUCT: return blk_tree_ws_bytes(plan, batch, n_slices);
+    case QAL_OP_FIDELITY: {
+      const int ch = blk_default_chunk(batch, n_slices);
+      const int nch = n_slices / ch;
+      return (size_t)batch * nch * mb + blk_tree_ws_bytes(plan, batch, nch) + (size_t)batch * mb;
+    }
+    case QAL_OP_FIDELITY_GRAD:
+      return blk_grad_ws_bytes(plan, batch, n_slices);
+    default: return 0;
+  }
+}
+
+int qal_block_fidelity_grad(const qal_block_plan* plan, int batch, int n_slices, double T, int magnus_order,
+                            int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0p, long long L0p_stride,
+                            const qal_c128* Lcp, const qal_c128* Lcommp, long long Lcommp_stride, const qal_c128* V,
+                            double* F, double* grad, qal_c128* Lambda_packed, int* status, void* ws, size_t ws_bytes,
+                            void* stream) {
+  launch_counter() = 0;
+  BlkCommon c;
+  int rc = check_block_basis(plan, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0p, L0p_stride, Lcp,
+                             Lcommp, Lcommp_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (!V || !F) return QAL_ERR_NULL;
+  const size_t need = qal_block_workspace_bytes(plan, grad ? QAL_OP_FIDELITY_GRAD : QAL_OP_FIDELITY, batch, n_slices);
+  if (!ws || ws_bytes < need) return QAL_ERR_WORKSPACE;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+  char* w = reinterpret_cast<char*>(ws);
+  const size_t mb = blk_mat_bytes(plan);
+  if (!grad) {
+    const int ch = blk_default_chunk(batch, n_slices);
+    const int nch = n_slices / ch;
+    double2* parts = reinterpret_cast<double2*>(w);
+    w += (size_t)batch * nch * mb;
+    double2* lam_tmp = reinterpret_cast<double2*>(w);
+    w += (size_t)batch * mb;
+    double2* lam = Lambda_packed ? D2(Lambda_packed) : lam_tmp;
+    BlkFwdOut O{nullptr, parts, ch, status};
+    if (launch_blk_expm_fold(*plan, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+    if ((rc = run_blk_tree(plan, batch, nch, parts, lam, w, st)) != QAL_OK) return rc;
+    return cuda_rc(launch_blk_fidelity(*plan, batch, lam, D2(V), F, st));
+  }
+  return blk_fidelity_grad_impl(plan, batch, c, D2(V), F, grad, D2(Lambda_packed), status, ws, st);
+}
 }  // extern "C"
+
+namespace {
+size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices) { (void)p; (void)batch; (void)n_slices; return 0; }
+int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
+                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st) {
+  (void)p; (void)batch; (void)c; (void)V; (void)F; (void)grad; (void)Lam; (void)status; (void)ws; (void)st;
+  return QAL_ERR_UNSUPPORTED;
+}
+}  // namespace

@@ -1,0 +1,778 @@
+// qal_blocks.cu -- the coherence-block (structure-exploiting) variant of the hot path,
+// SURVEY.md 8(f) row 4 / pin P-13.
+//
+// Every operator of the problem conserves the total S_z (Eq. 6 with the exchange
+// Hamiltonian, the Zeeman drift and the sigma-_i / sigma_z_i collapse operators), so the
+// Liouvillian of Eq. 8 maps the coherence-order subspaces q = m_a - m_b of
+// vec(rho) into themselves: after a permutation every generator L0, L_j, [L0, L_j],
+// [L_a, L_c] -- and therefore every Omega_k, U_k = expm(Omega_k) (Eq. 14), the ordered
+// product Lambda (Eq. 15) and every prefix / suffix product -- is block diagonal, with
+// blocks 20/15/15/6/6/1/1 for d = 8.  Hermiticity preservation (Lambda[s(R), s(C)] =
+// conj(Lambda[R, C]), s(i + d j) = j + d i, pin P-5) pairs block q with block -q, so with
+// `mirror` only q >= 0 is computed (20, 15, 6, 1): 2.9% of the dense flops.
+//
+// The structure is DETECTED, not assumed: qal_block_plan_build takes the union sparsity
+// pattern of the generator basis and finds its connected components (host), and
+// k_blk_check re-verifies on the device that every off-block entry of every basis matrix
+// of every pulse is exactly zero (status QAL_ERR_STRUCTURE otherwise).
+//
+// Layout: components are packed into "super-blocks" (groups) of padded width
+// P = 8C, C in {1..4} column tiles; a packed matrix is the concatenation of the groups'
+// P x P blocks (natural row-major complex).  A CTA holds one warp per 8-row tile of every
+// group (6 warps for d = 8 with mirror): the warps of group g run the dense kernels'
+// strip algorithm (qal_dev.cuh) on a P-wide strip, synchronised by their own named
+// barrier, independently of the other groups.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/qal.h"
+#include "qal_dev.cuh"
+#include "qal_internal.h"
+#include "qal_slice.cuh"
+
+namespace qal {
+
+// ------------------------------------------------------------------ device plan
+struct BlkDev {
+  int ngroups, nwarps, packed;
+  int C[QAL_BLK_MAX_GROUPS];       // column (= row) tiles of group g
+  int off[QAL_BLK_MAX_GROUPS];     // complex offset of group g in a packed matrix
+  int wrp0[QAL_BLK_MAX_GROUPS];    // first warp (row tile) of group g
+  int soff[QAL_BLK_MAX_GROUPS];    // double offset of group g's shared-memory region
+  signed char perm[QAL_BLK_MAX_ROWS];     // packed row -> natural index (-1 pad)
+  unsigned char weight[QAL_BLK_MAX_ROWS]; // 0 pad, 1, 2
+  signed char inv[64];                    // natural index -> packed row (-1 not stored)
+  signed char comp[64];                   // natural index -> component
+  int d;
+  unsigned long long gflops[QAL_BLK_MAX_GROUPS];   // algorithmic flops of one product of group g
+};
+
+BlkDev to_dev(const qal_block_plan& p) {
+  BlkDev D;
+  memset(&D, 0, sizeof(D));
+  D.ngroups = p.ngroups;
+  D.nwarps = p.nrows / 8;
+  D.packed = p.packed;
+  D.d = p.d;
+  for (int g = 0; g < p.ngroups; ++g) {
+    D.C[g] = p.width[g] / 8;
+    D.off[g] = p.off[g];
+    D.wrp0[g] = p.row0[g] / 8;
+    D.gflops[g] = (unsigned long long)p.flops[g];
+  }
+  for (int r = 0; r < QAL_BLK_MAX_ROWS; ++r) {
+    D.perm[r] = (signed char)(r < p.nrows ? p.perm[r] : -1);
+    D.weight[r] = (unsigned char)(r < p.nrows ? p.weight[r] : 0);
+  }
+  for (int i = 0; i < 64; ++i) {
+    D.inv[i] = (signed char)(i < p.n ? p.inv[i] : -1);
+    D.comp[i] = (signed char)(i < p.n ? p.comp[i] : -1);
+  }
+  return D;
+}
+
+// group of the calling warp
+struct GrpCtx {
+  int g, C, rt, P, off;   // rt = row tile within the group
+};
+__device__ __forceinline__ GrpCtx grp_of(const BlkDev& D, int w) {
+  GrpCtx x;
+  x.g = 0;
+#pragma unroll 1
+  for (int g = 1; g < D.ngroups; ++g)
+    if (w >= D.wrp0[g]) x.g = g;
+  x.C = D.C[x.g];
+  x.rt = w - D.wrp0[x.g];
+  x.P = 8 * x.C;
+  x.off = D.off[x.g];
+  return x;
+}
+
+__device__ __forceinline__ void grp_sync(int g, int C) {
+  if (C == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(32 * C) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ P-wide strips
+// Strip of 8 rows (row tile rt) of a P x P block, A-fragment layout: s[i] = M[8 rt + g][4 i + t].
+template <int C>
+struct BS {
+  double re[2 * C], im[2 * C];
+};
+
+template <int C>
+__device__ __forceinline__ void bzero(BS<C>& s) {
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) { s.re[i] = 0.0; s.im[i] = 0.0; }
+}
+template <int C>
+__device__ __forceinline__ void bcopy(BS<C>& d, const BS<C>& s) {
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) { d.re[i] = s.re[i]; d.im[i] = s.im[i]; }
+}
+template <int C>
+__device__ __forceinline__ void baxpy(BS<C>& acc, double a, const BS<C>& x) {
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) { acc.re[i] = fma(a, x.re[i], acc.re[i]); acc.im[i] = fma(a, x.im[i], acc.im[i]); }
+}
+template <int C>
+__device__ __forceinline__ void bscale(BS<C>& s, double a) {
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) { s.re[i] *= a; s.im[i] *= a; }
+}
+// diagonal test: row 8 rt + g, column 4 i + t
+template <int C>
+__device__ __forceinline__ void badd_diag(BS<C>& s, double a, int rt, const Lane& L) {
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i)
+    if (8 * rt + L.g == 4 * i + L.t) s.re[i] += a;
+}
+template <int C>
+__device__ __forceinline__ void bset_identity(BS<C>& s, int rt, const Lane& L) {
+  bzero(s);
+  badd_diag(s, 1.0, rt, L);
+}
+
+// image of a P x P block: re plane (P*P doubles) then im plane; column c of row r at
+// r*P + phys(c) (the within-tile permutation of qal_dev.cuh) XOR 8 on odd rows when C is
+// even (with C odd the row stride 8C already alternates the bank halves).
+template <int C>
+__device__ __forceinline__ int bpair_off(int rt, const Lane& L, int j) {
+  const int r = 8 * rt + L.g;
+  const int swz = (C % 2 == 0) ? ((L.g & 1) << 3) : 0;
+  return r * (8 * C) + ((8 * j + 2 * L.t) ^ swz);
+}
+template <int C>
+__device__ __forceinline__ void bload_img(BS<C>& s, const double* __restrict__ img, int rt, const Lane& L) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int o = bpair_off<C>(rt, L, j);
+    const double2 a = *reinterpret_cast<const double2*>(img + o);
+    const double2 b = *reinterpret_cast<const double2*>(img + PL + o);
+    s.re[2 * j] = a.x; s.re[2 * j + 1] = a.y;
+    s.im[2 * j] = b.x; s.im[2 * j + 1] = b.y;
+  }
+}
+template <int C>
+__device__ __forceinline__ void bstore_img(double* __restrict__ img, const BS<C>& s, int rt, const Lane& L) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int o = bpair_off<C>(rt, L, j);
+    *reinterpret_cast<double2*>(img + o) = make_double2(s.re[2 * j], s.re[2 * j + 1]);
+    *reinterpret_cast<double2*>(img + PL + o) = make_double2(s.im[2 * j], s.im[2 * j + 1]);
+  }
+}
+// acc += a * image strip (no temporary strip kept live)
+template <int C>
+__device__ __forceinline__ void baxpy_img(BS<C>& acc, double a, const double* __restrict__ img, int rt,
+                                          const Lane& L) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int o = bpair_off<C>(rt, L, j);
+    const double2 x = *reinterpret_cast<const double2*>(img + o);
+    const double2 y = *reinterpret_cast<const double2*>(img + PL + o);
+    acc.re[2 * j] = fma(a, x.x, acc.re[2 * j]); acc.re[2 * j + 1] = fma(a, x.y, acc.re[2 * j + 1]);
+    acc.im[2 * j] = fma(a, y.x, acc.im[2 * j]); acc.im[2 * j + 1] = fma(a, y.y, acc.im[2 * j + 1]);
+  }
+}
+// natural row-major P x P complex block <-> strip
+template <int C>
+__device__ __forceinline__ void bload_nat(BS<C>& s, const double2* __restrict__ M, int rt, const Lane& L) {
+  constexpr int P = 8 * C;
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    const double2 v = __ldg(M + (8 * rt + L.g) * P + 4 * i + L.t);
+    s.re[i] = v.x; s.im[i] = v.y;
+  }
+}
+template <int C>
+__device__ __forceinline__ void bstore_nat(double2* __restrict__ M, const BS<C>& s, int rt, const Lane& L) {
+  constexpr int P = 8 * C;
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) M[(8 * rt + L.g) * P + 4 * i + L.t] = make_double2(s.re[i], s.im[i]);
+}
+template <int C>
+__device__ __forceinline__ void baxpy_nat(BS<C>& X, double a, const double2* __restrict__ M, int rt, const Lane& L) {
+  constexpr int P = 8 * C;
+  const uint64_t keep = l2_evict_last();
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    double vx, vy;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(vx), "=d"(vy)
+                 : "l"(M + (8 * rt + L.g) * P + 4 * i + L.t), "l"(keep));
+    X.re[i] = fma(a, vx, X.re[i]);
+    X.im[i] = fma(a, vy, X.im[i]);
+  }
+}
+
+// acc += A * B, A = strip, B = image (FP64 tensor cores, 4 real MMAs per complex 8x8x4 step;
+// the P-wide version of qal_dev.cuh's mma_acc_4m)
+template <int C>
+__device__ __forceinline__ void bmma(BS<C>& acc, const BS<C>& a, const double* __restrict__ Bs, const Lane& L) {
+  constexpr int P = 8 * C, PL = P * P;
+  const int swz = (C % 2 == 0) ? (L.t & 1) : 0;   // physical tile of logical tile j: j ^ swz
+  const uint32_t base = smem_u32(Bs + L.t * P + L.g);
+  double br[2][C], bi[2][C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const uint32_t p = base + 8u * (8 * (j ^ swz));
+    br[0][j] = lds_v(p);
+    bi[0][j] = lds_v(p + 8u * PL);
+  }
+#pragma unroll
+  for (int q = 0; q < 2 * C; ++q) {
+    const int cur = q & 1;
+    if (q + 1 < 2 * C) {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const uint32_t p = base + 8u * ((q + 1) * 4 * P + 8 * (j ^ swz));
+        br[cur ^ 1][j] = lds_v(p);
+        bi[cur ^ 1][j] = lds_v(p + 8u * PL);
+      }
+    }
+    const double ar = a.re[q], ai = a.im[q], nai = -a.im[q];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br[cur][j]);
+      dmma(acc.re[2 * j], acc.re[2 * j + 1], nai, bi[cur][j]);
+      dmma(acc.im[2 * j], acc.im[2 * j + 1], ar, bi[cur][j]);
+      dmma(acc.im[2 * j], acc.im[2 * j + 1], ai, br[cur][j]);
+    }
+  }
+  QAL_FENCE();
+}
+
+// ||X||_1 of the group's block (max column sum of |x|), fixed order; red: >= 8 C * 8 C doubles
+// private to the group.  One group barrier; every warp of the group returns the same value.
+template <int C>
+__device__ __forceinline__ double bnorm1(const BS<C>& s, double* red, int g, int rt, const Lane& L) {
+  constexpr int P = 8 * C;
+  double cs[2 * C];
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) cs[i] = hypot(s.re[i], s.im[i]);
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
+  if (L.g == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) red[rt * P + 4 * i + L.t] = cs[i];
+  }
+  grp_sync(g, C);
+  double m = 0.0;
+  if (L.lane < P) {
+    double a = 0.0;
+#pragma unroll
+    for (int r = 0; r < C; ++r) a += red[r * P + L.lane];
+    m = a;
+  }
+  bool nan = !(m == m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, m, o);
+    nan = nan || !(x == x);
+    m = fmax(m, x);
+  }
+  nan = __any_sync(0xffffffffu, nan);
+  return nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
+}
+
+// Omega_k strip of the group from the packed generator basis (a1-a3, as build_omega)
+template <int C>
+__device__ __forceinline__ void bbuild_omega(BS<C>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
+                                             int off, int rt, const Lane& L) {
+  const int J = B.J;
+  const int nodes = (G.mode == 1) ? 2 : 1;
+  const double* u = G.u + ((size_t)b * G.count + k) * nodes * J;
+  bzero(X);
+  baxpy_nat(X, G.h, B.L0 + (size_t)b * B.L0_stride + off, rt, L);
+  for (int j = 0; j < J; ++j) {
+    const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * J + j);
+    baxpy_nat(X, 0.5 * G.h * (v1 + v2), B.Lc + (size_t)j * B.packed + off, rt, L);
+  }
+  if (B.ncomm > 0) {
+    const double2* Cb = B.Lcomm + (size_t)b * B.Lcomm_stride + off;
+    for (int j = 0; j < J; ++j) {
+      const double v1 = __ldg(u + j), v2 = __ldg(u + J + j);
+      baxpy_nat(X, -G.c4 * (v2 - v1), Cb + (size_t)j * B.packed, rt, L);
+    }
+    int p = J;
+    for (int a = 0; a < J; ++a)
+      for (int c = a + 1; c < J; ++c, ++p) {
+        const double coef = -G.c4 * (__ldg(u + a) * __ldg(u + J + c) - __ldg(u + c) * __ldg(u + J + a));
+        baxpy_nat(X, coef, Cb + (size_t)p * B.packed, rt, L);
+      }
+  }
+}
+
+// U = expm(X 2^s) for the group's block (the T8 / T18 schemes of qal_slice.cuh, powers kept in
+// registers); X's strip in A and its image in SX; SX4 = the group's shared operand image.
+// Result in A.  Returns the products done.
+template <int C>
+__device__ __forceinline__ int bexpm(BS<C>& A, BS<C>& acc, int m, int s, double* SX, double* SX4, int g, int rt,
+                                     const Lane& L) {
+  BS<C> T0, T1, T2;
+  int prods;
+  bzero(acc); bmma(acc, A, SX, L);                     // A2 = X X
+  bcopy(T0, acc);
+  if (m == 8) {
+    bzero(A);                                          // W = c1 X + c2 A2 (shared)
+    baxpy(A, c_t8[1], T0);
+    baxpy_img(A, c_t8[0], SX, rt, L);
+    bstore_img(SX4, A, rt, L);
+    grp_sync(g, C);
+    bzero(acc); bmma(acc, T0, SX4, L);                 // Y = A2 W
+    bcopy(T1, acc);
+    grp_sync(g, C);                                    // reads of SX4 (W) done
+    baxpy(acc, c_t8[4], T0);                           // R = Y + c5 A2 (shared)
+    bstore_img(SX4, acc, rt, L);
+    bcopy(A, T1);                                      // L = Y + c3 A2 + c4 X
+    baxpy(A, c_t8[2], T0);
+    baxpy_img(A, c_t8[3], SX, rt, L);
+    grp_sync(g, C);
+    bzero(acc);                                        // T8 = c6 Y + c7 A2 + X + I + L R
+    baxpy(acc, c_t8[5], T1);
+    baxpy(acc, c_t8[6], T0);
+    baxpy_img(acc, 1.0, SX, rt, L);
+    badd_diag(acc, 1.0, rt, L);
+    bmma(acc, A, SX4, L);
+    bcopy(A, acc);
+    prods = 3;
+  } else {
+    bzero(acc); bmma(acc, T0, SX, L);                  // A3 = A2 X
+    bcopy(T1, acc);
+    bstore_img(SX4, acc, rt, L);
+    grp_sync(g, C);
+    bzero(acc); bmma(acc, T1, SX4, L);                 // A6 = A3 A3
+    bcopy(T2, acc);
+    baxpy_img(acc, c_t18[T18_B5][1], SX, rt, L);       // B5 = e1 X + e2 A2 + A6
+    baxpy(acc, c_t18[T18_B5][2], T0);
+    grp_sync(g, C);                                    // reads of SX4 (A3) done
+    bstore_img(SX4, acc, rt, L);
+    bzero(A);                                          // B1
+    baxpy_img(A, c_t18[T18_B1][1], SX, rt, L);
+    baxpy(A, c_t18[T18_B1][2], T0);
+    baxpy(A, c_t18[T18_B1][3], T1);
+    bzero(acc);                                        // B4
+    badd_diag(acc, c_t18[T18_B4][0], rt, L);
+    baxpy_img(acc, c_t18[T18_B4][1], SX, rt, L);
+    baxpy(acc, c_t18[T18_B4][2], T0);
+    baxpy(acc, c_t18[T18_B4][3], T1);
+    baxpy(acc, c_t18[T18_B4][4], T2);
+    grp_sync(g, C);                                    // B5 image complete
+    bmma(acc, A, SX4, L);                              // A9 = B4 + B1 B5
+    grp_sync(g, C);                                    // reads of SX4 (B5) done
+    bstore_img(SX4, acc, rt, L);
+    bcopy(A, acc);                                     // L = B3 + A9
+    badd_diag(A, c_t18[T18_B3][0], rt, L);
+    baxpy_img(A, c_t18[T18_B3][1], SX, rt, L);
+    baxpy(A, c_t18[T18_B3][2], T0);
+    baxpy(A, c_t18[T18_B3][3], T1);
+    baxpy(A, c_t18[T18_B3][4], T2);
+    bzero(acc);                                        // T18 = B2 + L A9
+    badd_diag(acc, c_t18[T18_B2][0], rt, L);
+    baxpy_img(acc, c_t18[T18_B2][1], SX, rt, L);
+    baxpy(acc, c_t18[T18_B2][2], T0);
+    baxpy(acc, c_t18[T18_B2][3], T1);
+    baxpy(acc, c_t18[T18_B2][4], T2);
+    grp_sync(g, C);                                    // A9 image complete
+    bmma(acc, A, SX4, L);
+    bcopy(A, acc);
+    prods = 5;
+  }
+  for (int q = 0; q < s; ++q) {                        // squarings
+    grp_sync(g, C);
+    bstore_img(SX4, A, rt, L);
+    grp_sync(g, C);
+    bzero(acc); bmma(acc, A, SX4, L);
+    bcopy(A, acc);
+    ++prods;
+  }
+  return prods;
+}
+
+// per-group shared memory of the forward kernel: SX, SX4, SP images + norm buffer
+__host__ __device__ constexpr int fwd_grp_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
+
+template <int C>
+__device__ void blk_fwd_group(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
+                              const GrpCtx& x, double* sm, int* bad, unsigned long long& nprod, const Lane& L) {
+  double* SX = sm;
+  double* SX4 = sm + 2 * 64 * C * C;
+  double* SP = sm + 4 * 64 * C * C;
+  double* red = sm + 6 * 64 * C * C;
+  const int nchunk = G.count / O.chunk;
+  const int b = item / nchunk, c = item % nchunk;
+  BS<C> A, acc;
+  for (int kk = 0; kk < O.chunk; ++kk) {
+    const int k = c * O.chunk + kk;
+    bbuild_omega(A, B, G, b, k, x.off, x.rt, L);
+    const double nrm = bnorm1(A, red, x.g, x.rt, L);
+    int m, s;
+    choose_scheme(nrm, m, s);
+    if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+    bscale(A, ldexp(1.0, -s));
+    bstore_img(SX, A, x.rt, L);
+    grp_sync(x.g, C);
+    const int np = bexpm(A, acc, m, s, SX, SX4, x.g, x.rt, L);
+    if (x.rt == 0 && L.lane == 0) nprod += np;
+    const size_t slot = (size_t)b * G.count + k;
+    if (O.U_img) bstore_img(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x.rt, L);
+    if (O.chunk_nat) {
+      if (kk == 0) {
+        bstore_img(SP, A, x.rt, L);
+      } else {
+        bzero(acc); bmma(acc, A, SP, L);              // P <- U_k P
+        bcopy(A, acc);
+        if (x.rt == 0 && L.lane == 0) ++nprod;
+        grp_sync(x.g, C);
+        bstore_img(SP, A, x.rt, L);
+      }
+    }
+    grp_sync(x.g, C);   // SX / SX4 / red free for the next slice
+  }
+  if (O.chunk_nat) bstore_nat(O.chunk_nat + ((size_t)b * nchunk + c) * D.packed + x.off, A, x.rt, L);
+}
+
+__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4, 1) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
+                                                                           BlkFwdOut O, unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int bad_sh;
+  const Lane L = lane_id();
+  const GrpCtx x = grp_of(D, L.w);
+  double* sm = smem + D.soff[x.g];
+  if (threadIdx.x == 0) bad_sh = 0;
+  __syncthreads();
+  unsigned long long nprod = 0;
+  const int item = blockIdx.x;
+  switch (x.C) {
+    case 1: blk_fwd_group<1>(D, B, G, O, item, x, sm, &bad_sh, nprod, L); break;
+    case 2: blk_fwd_group<2>(D, B, G, O, item, x, sm, &bad_sh, nprod, L); break;
+    default: blk_fwd_group<3>(D, B, G, O, item, x, sm, &bad_sh, nprod, L); break;
+  }
+  __syncthreads();
+  const int nchunk = G.count / O.chunk;
+  if (O.status && threadIdx.x == 0 && bad_sh) O.status[item / nchunk] = QAL_ERR_NONFINITE;
+  // algorithmic flops of the products this group executed (profiling window)
+  if (ctr && L.lane == 0 && x.rt == 0 && nprod) atomicAdd(ctr, nprod * D.gflops[x.g]);
+}
+
+// ------------------------------------------------------------------ pair products (tree level)
+// out[b][i] = in[b][2i+1] in[b][2i] per group (later factor on the LEFT, Eq. 15); an odd last
+// element is carried.  One CTA per output; packed natural in / out.
+template <int C>
+__device__ void blk_pair_group(const BlkDev& D, const double2* lhs, const double2* rhs, double2* out,
+                               const GrpCtx& x, double* sm, const Lane& L) {
+  BS<C> A, acc;
+  bload_nat(A, rhs + x.off, x.rt, L);        // earlier factor as the B image
+  bstore_img(sm, A, x.rt, L);
+  bload_nat(A, lhs + x.off, x.rt, L);
+  grp_sync(x.g, C);
+  bzero(acc);
+  bmma(acc, A, sm, L);
+  bstore_nat(out + x.off, acc, x.rt, L);
+}
+
+__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4) k_blk_tree_level(BlkDev D, int cnt, const double2* __restrict__ in,
+                                                                         double2* __restrict__ out,
+                                                                         unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  const Lane L = lane_id();
+  const int half = (cnt + 1) / 2;
+  const int b = blockIdx.x / half, i = blockIdx.x % half;
+  const double2* src = in + (size_t)b * cnt * D.packed;
+  double2* dst = out + ((size_t)b * half + i) * D.packed;
+  if (2 * i + 1 == cnt) {
+    for (int e = threadIdx.x; e < D.packed; e += blockDim.x) dst[e] = src[(size_t)(cnt - 1) * D.packed + e];
+    return;
+  }
+  const GrpCtx x = grp_of(D, L.w);
+  double* sm = smem + D.soff[x.g];
+  const double2* lhs = src + (size_t)(2 * i + 1) * D.packed;
+  const double2* rhs = src + (size_t)(2 * i) * D.packed;
+  switch (x.C) {
+    case 1: blk_pair_group<1>(D, lhs, rhs, dst, x, sm, L); break;
+    case 2: blk_pair_group<2>(D, lhs, rhs, dst, x, sm, L); break;
+    default: blk_pair_group<3>(D, lhs, rhs, dst, x, sm, L); break;
+  }
+  if (ctr && L.lane == 0 && x.rt == 0) atomicAdd(ctr, D.gflops[x.g]);
+}
+
+// ------------------------------------------------------------------ pack / unpack / check
+// packed[e][g block (r, c)] = nat[e][perm r][perm c] (0 on padding).
+__global__ void k_blk_pack(BlkDev D, int count, const double2* __restrict__ nat, double2* __restrict__ packed) {
+  const int e = blockIdx.y;
+  const double2* src = nat + (size_t)e * 4096;
+  double2* dst = packed + (size_t)e * D.packed;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < D.packed; idx += gridDim.x * blockDim.x) {
+    int g = 0;
+    for (int q = 1; q < D.ngroups; ++q)
+      if (idx >= D.off[q]) g = q;
+    const int P = 8 * D.C[g], loc = idx - D.off[g];
+    const int r = loc / P, c = loc % P;
+    const int R = D.perm[8 * D.wrp0[g] + r], Cc = D.perm[8 * D.wrp0[g] + c];
+    dst[idx] = (R >= 0 && Cc >= 0) ? src[R * 64 + Cc] : make_double2(0.0, 0.0);
+  }
+}
+
+// every entry of nat[e] that couples two different components must be exactly zero
+__global__ void k_blk_check(BlkDev D, int count, const double2* __restrict__ nat, int* __restrict__ flag) {
+  const int e = blockIdx.y;
+  const double2* src = nat + (size_t)e * 4096;
+  int bad = 0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 4096; idx += gridDim.x * blockDim.x) {
+    const int R = idx >> 6, Cc = idx & 63;
+    if (D.comp[R] != D.comp[Cc]) {
+      const double2 v = src[idx];
+      if (v.x != 0.0 || v.y != 0.0) bad = 1;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = QAL_ERR_STRUCTURE;
+}
+
+// natural from packed: stored component -> value; mirrored component -> conj of the stored
+// mirror entry (Lambda[s(R), s(C)] = conj(Lambda[R, C]), s(i + d j) = j + d i); else 0.
+__global__ void k_blk_unpack(BlkDev D, int count, const double2* __restrict__ packed, double2* __restrict__ nat) {
+  const int e = blockIdx.y;
+  const double2* src = packed + (size_t)e * D.packed;
+  double2* dst = nat + (size_t)e * 4096;
+  const int d = D.d;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 4096; idx += gridDim.x * blockDim.x) {
+    const int R = idx >> 6, Cc = idx & 63;
+    double2 v = make_double2(0.0, 0.0);
+    if (D.comp[R] == D.comp[Cc]) {
+      int r = D.inv[R], c = D.inv[Cc];
+      bool cj = false;
+      if (r < 0) {   // mirrored component: read the stored mirror entry
+        r = D.inv[(R / d) + d * (R % d)];
+        c = D.inv[(Cc / d) + d * (Cc % d)];
+        cj = true;
+      }
+      if (r >= 0 && c >= 0) {
+        int g = 0;
+        for (int q = 1; q < D.ngroups; ++q)
+          if (r >= 8 * D.wrp0[q]) g = q;
+        const int P = 8 * D.C[g];
+        v = src[D.off[g] + (r - 8 * D.wrp0[g]) * P + (c - 8 * D.wrp0[g])];
+        if (cj) v.y = -v.y;
+      }
+    }
+    dst[idx] = v;
+  }
+}
+
+// ------------------------------------------------------------------ fidelity (a6)
+// F = Re Tr(S_V^dag Lambda)/d^2 summed over the stored blocks with the component weights
+// (a mirrored block contributes the same real part as its stored partner).
+__global__ void __launch_bounds__(256) k_blk_fidelity(BlkDev D, const double2* __restrict__ Lam,
+                                                      const double2* __restrict__ V, double* __restrict__ F) {
+  __shared__ double2 Vs[64];
+  __shared__ double red[16];
+  const Lane L = lane_id();
+  if (threadIdx.x < 64) Vs[threadIdx.x] = V[threadIdx.x];
+  __syncthreads();
+  const double2* M = Lam + (size_t)blockIdx.x * D.packed;
+  double acc = 0.0;
+  for (int g = 0; g < D.ngroups; ++g) {
+    const int P = 8 * D.C[g], row0 = 8 * D.wrp0[g];
+    for (int e = threadIdx.x; e < P * P; e += blockDim.x) {
+      const int r = e / P, c = e % P;
+      const int a = D.perm[row0 + r], cc = D.perm[row0 + c];
+      if (a < 0 || cc < 0) continue;
+      const double w = D.weight[row0 + r];
+      const int i = a & 7, j = a >> 3, k = cc & 7, l = cc >> 3;
+      const double2 vjl = Vs[j * 8 + l], vik = Vs[i * 8 + k], x = M[D.off[g] + e];
+      const double wr = vjl.x * vik.x + vjl.y * vik.y;
+      const double wi = vjl.y * vik.x - vjl.x * vik.y;
+      acc += w * (wr * x.x - wi * x.y);
+    }
+  }
+  const double s = block_sum(acc, red, L);
+  if (threadIdx.x == 0) F[blockIdx.x] = s / 64.0;
+}
+
+// ------------------------------------------------------------------ launchers
+namespace {
+int grp_smem_doubles(const BlkDev& D, int (*per)(int), int* soff) {
+  int o = 0;
+  for (int g = 0; g < D.ngroups; ++g) {
+    soff[g] = o;
+    o += per(D.C[g]);
+    o = (o + 15) & ~15;   // 128-byte alignment of every region
+  }
+  return o;
+}
+int fwd_per(int C) { return fwd_grp_doubles(C); }
+int pair_per(int C) { return 2 * 64 * C * C; }
+}  // namespace
+
+cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
+                                 const BlkFwdOut& O, cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  const size_t bytes = (size_t)grp_smem_doubles(D, fwd_per, D.soff) * 8;
+  static size_t attr = 0;
+  if (bytes > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_blk_expm_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    attr = bytes;
+  }
+  const int items = batch * (G.count / O.chunk);
+  prof_pre(ST_BLK_EXPM, st);
+  k_blk_expm_fold<<<items, 32 * D.nwarps, bytes, st>>>(D, B, G, O, prof_counter(ST_BLK_EXPM));
+  prof_post(ST_BLK_EXPM, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, const double2* in, double2* out,
+                                  cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  const size_t bytes = (size_t)grp_smem_doubles(D, pair_per, D.soff) * 8;
+  const int half = (cnt + 1) / 2;
+  prof_pre(ST_BLK_TREE, st);
+  k_blk_tree_level<<<batch * half, 32 * D.nwarps, bytes, st>>>(D, cnt, in, out, prof_counter(ST_BLK_TREE));
+  prof_post(ST_BLK_TREE, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* nat, double2* packed, int* flag,
+                            cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  dim3 grid(4, count);
+  if (flag) {
+    k_blk_check<<<grid, 256, 0, st>>>(D, count, nat, flag);
+    ++launch_counter();
+  }
+  k_blk_pack<<<grid, 256, 0, st>>>(D, count, nat, packed);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2* packed, double2* nat,
+                              cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  dim3 grid(4, count);
+  k_blk_unpack<<<grid, 256, 0, st>>>(D, count, packed, nat);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
+                                cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  prof_pre(ST_FID, st);
+  k_blk_fidelity<<<batch, 256, 0, st>>>(D, Lam, V, F);
+  prof_post(ST_FID, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ host: structure detection
+// Components of the union sparsity graph of the given matrices; Hermitian mirror pairing;
+// first-fit-decreasing packing into super-blocks of padded width 8C <= 32.
+int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block_plan* out) {
+  if (n != 64) return QAL_ERR_UNSUPPORTED;
+  const int d = 8;
+  std::vector<int> par(n);
+  for (int i = 0; i < n; ++i) par[i] = i;
+  auto find = [&](int a) {
+    while (par[a] != a) a = par[a] = par[par[a]];
+    return a;
+  };
+  for (int m = 0; m < nmat; ++m)
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < n; ++c) {
+        const double2 v = mats[((size_t)m * n + r) * n + c];
+        if (!std::isfinite(v.x) || !std::isfinite(v.y)) return QAL_ERR_NONFINITE;
+        if (v.x != 0.0 || v.y != 0.0) {
+          const int a = find(r), b = find(c);
+          if (a != b) par[std::max(a, b)] = std::min(a, b);
+        }
+      }
+  // component ids in order of their smallest element
+  std::vector<int> cid(n, -1), root_id(n, -1);
+  int ncomp = 0;
+  for (int i = 0; i < n; ++i) {
+    const int r = find(i);
+    if (root_id[r] < 0) root_id[r] = ncomp++;
+    cid[i] = root_id[r];
+  }
+  std::vector<std::vector<int>> members(ncomp);
+  for (int i = 0; i < n; ++i) members[cid[i]].push_back(i);
+  // Hermitian mirror s(i + d j) = j + d i maps components onto components
+  std::vector<int> mir(ncomp, -1);
+  for (int k = 0; k < ncomp; ++k) {
+    const int i0 = members[k][0];
+    mir[k] = cid[(i0 / d) + d * (i0 % d)];
+    for (int i : members[k])
+      if (cid[(i / d) + d * (i % d)] != mir[k]) return QAL_ERR_STRUCTURE;
+  }
+  std::vector<int> keep, weight(ncomp, 1);
+  for (int k = 0; k < ncomp; ++k) {
+    if (!mirror) { keep.push_back(k); continue; }
+    if (mir[k] == k) keep.push_back(k);
+    else if (k < mir[k]) { keep.push_back(k); weight[k] = 2; }
+  }
+  for (int k : keep)
+    if ((int)members[k].size() > 24) return QAL_ERR_UNSUPPORTED;   // super-blocks up to 24 wide
+  std::stable_sort(keep.begin(), keep.end(),
+                   [&](int a, int b) { return members[a].size() > members[b].size(); });
+  struct Bin { int width, used; std::vector<int> comps; };
+  std::vector<Bin> bins;
+  for (int k : keep) {
+    const int sz = (int)members[k].size();
+    bool placed = false;
+    for (Bin& bn : bins)
+      if (bn.used + sz <= bn.width) { bn.used += sz; bn.comps.push_back(k); placed = true; break; }
+    if (!placed) bins.push_back({(sz + 7) / 8 * 8, sz, {k}});
+  }
+  if ((int)bins.size() > QAL_BLK_MAX_GROUPS) return QAL_ERR_UNSUPPORTED;
+  qal_block_plan p;
+  memset(&p, 0, sizeof(p));
+  p.n = n;
+  p.d = d;
+  p.mirror = mirror ? 1 : 0;
+  p.ngroups = (int)bins.size();
+  p.n_components = ncomp;
+  int row = 0, off = 0;
+  for (int i = 0; i < QAL_BLK_MAX_ROWS; ++i) { p.perm[i] = -1; p.weight[i] = 0; }
+  for (int i = 0; i < 64; ++i) { p.inv[i] = -1; p.comp[i] = i < n ? cid[i] : -1; }
+  for (int g = 0; g < p.ngroups; ++g) {
+    p.width[g] = bins[g].width;
+    p.row0[g] = row;
+    p.off[g] = off;
+    int r = row;
+    for (int k : bins[g].comps)
+      for (int i : members[k]) {
+        p.perm[r] = i;
+        p.weight[r] = weight[k];
+        p.inv[i] = r;
+        ++r;
+      }
+    double fl = 0.0;
+    for (int k : bins[g].comps) {
+      const double sz = (double)members[k].size();
+      fl += 2.0 * QAL_REAL_MMAS_PER_CMMA * sz * sz * sz;   // 8 s^3 per complex product (4M)
+    }
+    p.flops[g] = fl;
+    row += bins[g].width;
+    off += bins[g].width * bins[g].width;
+  }
+  if (row > QAL_BLK_MAX_ROWS) return QAL_ERR_UNSUPPORTED;
+  p.nrows = row;
+  p.packed = off;
+  *out = p;
+  return QAL_OK;
+}
+
+}  // namespace qal

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include "../../include/qal.h"
+
 namespace qal {
 
 constexpr int MAXJ = 8;
@@ -37,11 +39,39 @@ struct FwdOut {
   int* status;              // [batch] or nullptr
 };
 
+// coherence-block path (qal_blocks.cu): packed generator basis and forward outputs
+struct BlkBasis {
+  const double2* L0;       // packed [batch|1][packed]
+  long long L0_stride;     // complex elements between pulses (0 = shared)
+  const double2* Lc;       // packed [J][packed]
+  const double2* Lcomm;    // packed [batch|1][ncomm][packed] or nullptr
+  long long Lcomm_stride;
+  int J, ncomm, packed;
+};
+struct BlkFwdOut {
+  double* U_img;       // [batch][count] packed images, or nullptr
+  double2* chunk_nat;  // [batch][count/chunk] packed natural, or nullptr
+  int chunk;
+  int* status;
+};
+int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block_plan* out);
+cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
+                                 const BlkFwdOut& O, cudaStream_t st);
+cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, const double2* in, double2* out,
+                                  cudaStream_t st);
+cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* nat, double2* packed, int* flag,
+                            cudaStream_t st);
+cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2* packed, double2* nat,
+                              cudaStream_t st);
+cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
+                                cudaStream_t st);
+
 int num_sms();
 int& launch_counter();
 
 // profiling window (qal_profile_begin/end): stage ids as in qal.h
-enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, ST_DENSE_GEMM, NSTAGE };
+enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, ST_DENSE_GEMM,
+       ST_BLK_EXPM, ST_BLK_TREE, ST_BLK_PREFIX, ST_BLK_SUFFIX, ST_BLK_GRAD, NSTAGE };
 unsigned long long* prof_counter(int stage);   // device counter slot or nullptr
 void prof_pre(int stage, cudaStream_t st);      // record start event (no-op when off)
 void prof_post(int stage, cudaStream_t st);     // record end event

@@ -25,10 +25,15 @@ QAL_OP_EXPM_SLICES = 4
 QAL_OP_VJP = 5
 QAL_MAX_CTRL = 8
 STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
-          "grad_slices", "dense_gemm"]
+          "grad_slices", "dense_gemm", "blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain",
+          "blk_grad_slices"]
+# stages whose device counter holds algorithmic FLOPs (coherence-block path), not product counts
+FLOP_STAGES = {"blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain", "blk_grad_slices"}
 KERNELS = {"liouvillian": "k_liouvillian", "commutators": "k_commutators", "expm_fold": "k_expm_fold",
            "tree": "k_tree_level", "fidelity": "k_fidelity", "prefix_chain": "k_prefix_chain",
-           "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices", "dense_gemm": "k_dense_gemm"}
+           "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices", "dense_gemm": "k_dense_gemm",
+           "blk_expm_fold": "k_blk_expm_fold", "blk_tree": "k_blk_tree_level", "blk_prefix_chain": "k_blk_prefix_chain",
+           "blk_suffix_chain": "k_blk_suffix_chain", "blk_grad_slices": "k_blk_grad_slices"}
 
 _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
@@ -78,6 +83,29 @@ _EXPORTS = {
     "qal_adam_step": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                       ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_void_p]),
+    "qal_block_plan_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.c_void_p]),
+    "qal_block_pack": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_block_unpack": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p]),
+    "qal_block_expm_slices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_block_ordered_product": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                  ctypes.c_void_p]),
+    "qal_block_fidelity": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_block_fidelity_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                ctypes.c_void_p]),
+    "qal_block_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "qal_profile_begin": (ctypes.c_int, [ctypes.c_void_p]),
     "qal_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -392,3 +420,136 @@ def qal_fp64_peak_probe(kind: int, blocks: int, iters: int, sink, stream=None) -
     rc = load().qal_fp64_peak_probe(kind, blocks, iters, ctypes.byref(fl), _ptr(sink), _stream(stream))
     _check(rc, "qal_fp64_peak_probe")
     return fl.value
+
+
+# --------------------------------------------------------------------------- coherence-block path
+QAL_BLK_MAX_GROUPS = 16
+QAL_BLK_MAX_ROWS = 96
+QAL_ERR_STRUCTURE = -8
+
+
+class BlockPlan(ctypes.Structure):
+    """Mirror of qal_block_plan (include/qal.h)."""
+    _fields_ = [("n", ctypes.c_int), ("d", ctypes.c_int), ("mirror", ctypes.c_int), ("ngroups", ctypes.c_int),
+                ("nrows", ctypes.c_int), ("packed", ctypes.c_int), ("n_components", ctypes.c_int),
+                ("width", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("row0", ctypes.c_int * QAL_BLK_MAX_GROUPS),
+                ("off", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("flops", ctypes.c_double * QAL_BLK_MAX_GROUPS),
+                ("perm", ctypes.c_int * QAL_BLK_MAX_ROWS), ("weight", ctypes.c_int * QAL_BLK_MAX_ROWS),
+                ("inv", ctypes.c_int * 64), ("comp", ctypes.c_int * 64)]
+
+    def groups(self):
+        return [(self.width[g], self.row0[g], self.off[g]) for g in range(self.ngroups)]
+
+    def flops_per_product(self) -> float:
+        return float(sum(self.flops[g] for g in range(self.ngroups)))
+
+
+def qal_block_plan_build(mats, mirror=True) -> BlockPlan:
+    """Structure detection on the union sparsity of `mats` ([m][n][n] complex128, any device; copied to
+    host memory because the library's plan builder is host code)."""
+    host = mats.detach().to("cpu", torch.complex128).contiguous().reshape(-1, mats.shape[-2], mats.shape[-1])
+    plan = BlockPlan()
+    rc = load().qal_block_plan_build(host.shape[-1], host.shape[0], ctypes.c_void_p(host.data_ptr()),
+                                     1 if mirror else 0, ctypes.byref(plan))
+    _check(rc, "qal_block_plan_build")
+    return plan
+
+
+def qal_block_pack(plan: BlockPlan, nat, check=True, stream=None):
+    """natural [..., n, n] -> packed [..., plan.packed]; returns (packed, flag) with flag a device int
+    tensor (QAL_ERR_STRUCTURE if an off-block entry is non-zero) or None."""
+    nat = _dev(nat, torch.complex128, "nat")
+    lead = nat.shape[:-2]
+    cnt = max(1, int(torch.tensor(lead).prod().item()) if len(lead) else 1)
+    out = torch.empty(tuple(lead) + (plan.packed,), dtype=torch.complex128, device=nat.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=nat.device) if check else None
+    _check(load().qal_block_pack(ctypes.byref(plan), cnt, _ptr(nat), _ptr(out), _ptr(flag), _stream(stream)),
+           "qal_block_pack")
+    return out, flag
+
+
+def qal_block_unpack(plan: BlockPlan, packed, stream=None):
+    packed = _dev(packed, torch.complex128, "packed")
+    lead = packed.shape[:-1]
+    cnt = max(1, int(torch.tensor(lead).prod().item()) if len(lead) else 1)
+    out = torch.empty(tuple(lead) + (plan.n, plan.n), dtype=torch.complex128, device=packed.device)
+    _check(load().qal_block_unpack(ctypes.byref(plan), cnt, _ptr(packed), _ptr(out), _stream(stream)),
+           "qal_block_unpack")
+    return out
+
+
+def qal_block_expm_slices(plan: BlockPlan, L0p, Lcp, u, T, n_slices, *, k0=0, count=None, chunk=None,
+                          magnus_order=4, ctrl_mode=QAL_CTRL_PWC, Lcommp=None, status=None, stream=None):
+    """Chunk products [B][count/chunk][packed] of the slices k0..k0+count-1 (packed operands)."""
+    c128 = torch.complex128
+    L0p = _dev(L0p, c128, "L0p")
+    Lcp = _dev(Lcp, c128, "Lcp")
+    u = _dev(u, torch.float64, "u")
+    B, J = u.shape[0], Lcp.shape[0]
+    count = n_slices - k0 if count is None else count
+    chunk = count if chunk is None else chunk
+    out = torch.empty((B, count // chunk, plan.packed), dtype=c128, device=u.device)
+    L0s = 0 if L0p.shape[0] == 1 else plan.packed
+    Lcs = 0
+    if Lcommp is not None:
+        Lcommp = _dev(Lcommp, c128, "Lcommp")
+        Lcs = 0 if Lcommp.shape[0] == 1 else n_comm(J) * plan.packed
+    rc = load().qal_block_expm_slices(ctypes.byref(plan), B, n_slices, float(T), k0, count, magnus_order, ctrl_mode,
+                                      J, _ptr(u), _ptr(L0p), L0s, _ptr(Lcp), _ptr(Lcommp), Lcs, chunk, _ptr(out),
+                                      _ptr(status), _stream(stream))
+    _check(rc, "qal_block_expm_slices")
+    return out
+
+
+def qal_block_ordered_product(plan: BlockPlan, U, stream=None):
+    U = _dev(U, torch.complex128, "U")
+    B, cnt = U.shape[0], U.shape[1]
+    out = torch.empty((B, plan.packed), dtype=torch.complex128, device=U.device)
+    wsb = load().qal_block_workspace_bytes(ctypes.byref(plan), QAL_OP_ORDERED_PRODUCT, B, cnt)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=U.device)
+    _check(load().qal_block_ordered_product(ctypes.byref(plan), B, cnt, _ptr(U), _ptr(out), _ptr(ws), wsb,
+                                            _stream(stream)), "qal_block_ordered_product")
+    return out
+
+
+def qal_block_fidelity(plan: BlockPlan, Lam, V, stream=None):
+    Lam = _dev(Lam, torch.complex128, "Lambda")
+    V = _dev(V, torch.complex128, "V")
+    F = torch.empty(Lam.shape[0], dtype=torch.float64, device=Lam.device)
+    _check(load().qal_block_fidelity(ctypes.byref(plan), Lam.shape[0], _ptr(Lam), _ptr(V), _ptr(F), _stream(stream)),
+           "qal_block_fidelity")
+    return F
+
+
+def block_workspace_bytes(plan: BlockPlan, op: int, batch: int, n_slices: int) -> int:
+    return load().qal_block_workspace_bytes(ctypes.byref(plan), op, batch, n_slices)
+
+
+def qal_block_fidelity_grad(plan: BlockPlan, L0p, Lcp, u, T, n_slices, V, *, magnus_order=4,
+                            ctrl_mode=QAL_CTRL_PWC, Lcommp=None, want_grad=True, want_Lambda=False, status=None,
+                            ws=None, stream=None):
+    """The hot path on packed operands: (F [B], grad (layout of u) or None, packed Lambda or None)."""
+    c128 = torch.complex128
+    L0p = _dev(L0p, c128, "L0p")
+    Lcp = _dev(Lcp, c128, "Lcp")
+    u = _dev(u, torch.float64, "u")
+    V = _dev(V, c128, "V")
+    B, J = u.shape[0], Lcp.shape[0]
+    dev = u.device
+    F = torch.empty(B, dtype=torch.float64, device=dev)
+    g = torch.empty_like(u) if want_grad else None
+    Lam = torch.empty((B, plan.packed), dtype=c128, device=dev) if want_Lambda else None
+    op = QAL_OP_FIDELITY_GRAD if want_grad else QAL_OP_FIDELITY
+    wsb = block_workspace_bytes(plan, op, B, n_slices)
+    if ws is None or ws.numel() < wsb:
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    L0s = 0 if L0p.shape[0] == 1 else plan.packed
+    Lcs = 0
+    if Lcommp is not None:
+        Lcommp = _dev(Lcommp, c128, "Lcommp")
+        Lcs = 0 if Lcommp.shape[0] == 1 else n_comm(J) * plan.packed
+    rc = load().qal_block_fidelity_grad(ctypes.byref(plan), B, n_slices, float(T), magnus_order, ctrl_mode, J,
+                                        _ptr(u), _ptr(L0p), L0s, _ptr(Lcp), _ptr(Lcommp), Lcs, _ptr(V), _ptr(F),
+                                        _ptr(g), _ptr(Lam), _ptr(status), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "qal_block_fidelity_grad")
+    return F, g, Lam

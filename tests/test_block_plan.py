@@ -1,0 +1,101 @@
+"""Structure detection of the coherence-block path (host code in libqal.so; no GPU needed).
+
+Pinned against the physics, not against the library: total S_z conservation (Eq. 6) makes
+the Liouvillian block diagonal by coherence order q = m(i) - m(j) of vec(rho)[i + d j] = rho[i][j]
+(column stacking, A5), where m counts the up spins of basis state i (A7: bit = 0 is up).  The sectors
+are computed here from that definition alone and must equal the plan's components; Hermiticity
+preservation pairs q with -q (P-5).
+"""
+from collections import Counter
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2511_13330_b200 import inputs as qi
+
+
+@pytest.fixture(scope="module")
+def qal():
+    from paper_2511_13330_b200 import _build, qal as q
+    _build.build()
+    q.load()
+    return q
+
+
+def coherence_order(d=8, nspin=3):
+    up = [nspin - bin(i).count("1") for i in range(d)]
+    return np.array([up[R % d] - up[R // d] for R in range(d * d)])
+
+
+@pytest.fixture(scope="module")
+def basis(oracle):
+    p = qi.cfg2(batch=2, N=4)
+    mats = []
+    for b in range(2):
+        L0, Lc = oracle.build_liouvillian(p.H0[b], p.Hc, p.C)
+        mats.append(L0[None])
+    mats.append(Lc)
+    return torch.from_numpy(np.concatenate(mats))
+
+
+def plan_components(plan):
+    return np.array(list(plan.comp)[:64])
+
+
+def test_components_are_the_coherence_order_sectors(qal, basis):
+    plan = qal.qal_block_plan_build(basis, mirror=False)
+    q = coherence_order()
+    comp = plan_components(plan)
+    # same partition: two indices share a component iff they share q
+    assert all((comp[a] == comp[b]) == (q[a] == q[b]) for a in range(64) for b in range(64))
+    assert sorted(Counter(q).values(), reverse=True) == [20, 15, 15, 6, 6, 1, 1]
+    assert plan.n_components == 7
+
+
+def test_mirror_keeps_one_of_each_pair(qal, basis):
+    plan = qal.qal_block_plan_build(basis, mirror=True)
+    q = coherence_order()
+    rows = [plan.perm[r] for r in range(plan.nrows) if plan.perm[r] >= 0]
+    kept = sorted(set(q[rows]))
+    assert len(rows) == 20 + 15 + 6 + 1
+    assert len(kept) == 4 and all(-k not in kept or k == 0 for k in kept)   # one of q, -q
+    for r in range(plan.nrows):
+        R = plan.perm[r]
+        if R < 0:
+            assert plan.weight[r] == 0
+        else:
+            assert plan.weight[r] == (1 if q[R] == 0 else 2)
+
+
+def test_packing_layout_is_consistent(qal, basis):
+    for mirror in (True, False):
+        plan = qal.qal_block_plan_build(basis, mirror=mirror)
+        row = off = 0
+        for g in range(plan.ngroups):
+            w = plan.width[g]
+            assert w in (8, 16, 24) and plan.row0[g] == row and plan.off[g] == off
+            row += w
+            off += w * w
+        assert row == plan.nrows and off == plan.packed
+        stored = [plan.perm[r] for r in range(plan.nrows) if plan.perm[r] >= 0]
+        assert len(stored) == len(set(stored))
+        for R in range(64):
+            r = plan.inv[R]
+            assert r == -1 or plan.perm[r] == R
+        if not mirror:
+            assert sorted(stored) == list(range(64))
+
+
+def test_flops_are_the_block_cubes(qal, basis):
+    plan = qal.qal_block_plan_build(basis, mirror=True)
+    mults = qal.real_mults_per_complex_product()
+    assert plan.flops_per_product() == 2 * mults * (20 ** 3 + 15 ** 3 + 6 ** 3 + 1)
+    dense = 2 * mults * 64 ** 3
+    assert plan.flops_per_product() / dense < 0.05
+
+
+def test_dense_coupling_gives_one_component_and_is_rejected(qal):
+    M = torch.ones((1, 64, 64), dtype=torch.complex128)
+    with pytest.raises(qal.QalError):
+        qal.qal_block_plan_build(M, mirror=True)     # one 64-wide component > 24: unsupported

@@ -1,0 +1,181 @@
+"""GPU parity of the coherence-block path (pin P-13) against the CPU oracle.
+
+The block path computes the same Omega_k, U_k, Lambda, F (and dF/du) as the dense path, restricted to
+the coherence-order blocks found by qal_block_plan_build; every expected value here comes from
+oracle/ (dense, sequential, no structure), so these tests pin the block path to the definition.
+Tolerances as tests/test_gpu_parity.py (BASELINE north_star).
+"""
+import numpy as np
+import pytest
+
+from paper_2511_13330_b200 import inputs as qi
+
+pytestmark = pytest.mark.gpu
+
+TOL_PROP = 1e-10
+TOL_GRAD = 1e-8
+
+
+def relfro(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def qal(torch_cuda):
+    from paper_2511_13330_b200 import _build, qal as q
+    _build.build()
+    q.load()
+    return q
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def packed_basis(torch, qal, prob, mirror=True, want_comm=False):
+    """Dense basis on the GPU (K1), plan from it, packed copies (with the device structure check)."""
+    C = prob.C if prob.C.shape[0] > 0 else None
+    L0, Lc, Lcomm = qal.qal_build_liouvillian(dev(torch, prob.H0), dev(torch, prob.Hc),
+                                              None if C is None else dev(torch, C), want_comm=want_comm)
+    mats = [L0, Lc] + ([Lcomm.reshape(-1, 64, 64)] if want_comm else [])
+    plan = qal.qal_block_plan_build(torch.cat([m.reshape(-1, 64, 64) for m in mats]), mirror=mirror)
+    L0p, f0 = qal.qal_block_pack(plan, L0)
+    Lcp, f1 = qal.qal_block_pack(plan, Lc)
+    Lcommp = None
+    if want_comm:
+        Lcommp, f2 = qal.qal_block_pack(plan, Lcomm)
+        assert f2.item() == 0
+    assert f0.item() == 0 and f1.item() == 0
+    return plan, L0p, Lcp, Lcommp
+
+
+@pytest.mark.parametrize("mirror", [True, False])
+def test_pack_unpack_roundtrip_of_oracle_lambda(torch_cuda, qal, oracle, mirror):
+    torch = torch_cuda
+    p = qi.cfg0(N=16, T=100.0 * 16 / 256)
+    plan, _, _, _ = packed_basis(torch, qal, p, mirror)
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(L0, Lc, p.u[0], p.T, p.N)
+    pk, flag = qal.qal_block_pack(plan, dev(torch, Lam[None]))
+    assert flag.item() == 0                        # the oracle's Lambda is block diagonal (P-13)
+    back = qal.qal_block_unpack(plan, pk)[0].cpu().numpy()
+    assert relfro(back, Lam) <= 1e-14              # mirror fill = Hermiticity preservation (P-5)
+
+
+def test_structure_check_flags_off_block_entry(torch_cuda, qal):
+    torch = torch_cuda
+    p = qi.cfg0(N=4, T=1.0)
+    plan, _, _, _ = packed_basis(torch, qal, p)
+    M = torch.zeros((2, 64, 64), dtype=torch.complex128, device="cuda")
+    M[1, 0, 1] = 1e-300                            # couples natural indices 0 and 1 (q = 0 and q = 1)
+    _, flag = qal.qal_block_pack(plan, M)
+    assert flag.item() == qal.QAL_ERR_STRUCTURE
+
+
+@pytest.mark.parametrize("mirror", [True, False])
+def test_cfg0_forward_block_path(torch_cuda, qal, oracle, mirror):
+    torch = torch_cuda
+    p = qi.cfg0()
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p, mirror)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(rL0, rLc, p.u[0], p.T, p.N)
+    F, _, Lp = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V),
+                                           want_grad=False, want_Lambda=True)
+    got = qal.qal_block_unpack(plan, Lp)[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP, relfro(got, Lam)
+    Fr = oracle.fidelity(Lam, p.V)
+    assert abs(F.item() - Fr) / abs(Fr) <= TOL_PROP
+    Fb = qal.qal_block_fidelity(plan, Lp, dev(torch, p.V)).item()
+    assert abs(Fb - Fr) / abs(Fr) <= TOL_PROP
+
+
+@pytest.mark.parametrize("chunk", [1, 4, 64, 256])
+def test_chunk_fold_and_block_tree(torch_cuda, qal, oracle, chunk):
+    torch = torch_cuda
+    p = qi.cfg0()
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(rL0, rLc, p.u[0], p.T, p.N)
+    parts = qal.qal_block_expm_slices(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, chunk=chunk)
+    got = qal.qal_block_unpack(plan, qal.qal_block_ordered_product(plan, parts))[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP
+
+
+@pytest.mark.parametrize("count", [1, 2, 3, 5, 13])
+def test_block_ordered_product_ragged(torch_cuda, qal, oracle, count):
+    """Tree over `count` packed slice exponentials vs the oracle's sequential left fold (A4)."""
+    torch = torch_cuda
+    p = qi.cfg0(N=count, T=100.0 * count / 256)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(rL0, rLc, p.u[0], p.T, p.N)
+    Us = qal.qal_block_expm_slices(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, chunk=1)
+    got = qal.qal_block_unpack(plan, qal.qal_block_ordered_product(plan, Us))[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP
+
+
+def test_cfg2_recipe_per_pulse_drift(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    p = qi.cfg2(batch=3, N=32, T=200.0 * 32 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    F, _, Lp = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V),
+                                           want_grad=False, want_Lambda=True)
+    got = qal.qal_block_unpack(plan, Lp).cpu().numpy()
+    for b in range(3):
+        rL0, rLc = oracle.build_liouvillian(p.H0[b], p.Hc, p.C)
+        Lam = oracle.propagate(rL0, rLc, p.u[b], p.T, p.N)
+        assert relfro(got[b], Lam) <= TOL_PROP
+        Fr = oracle.fidelity(Lam, p.V)
+        assert abs(F[b].item() - Fr) / abs(Fr) <= TOL_PROP
+
+
+@pytest.mark.parametrize("order", [2, 4])
+def test_nodes_mode_block_forward(torch_cuda, qal, oracle, order):
+    """cfg3 recipe: Magnus-4 commutator basis, packed (the commutators are block diagonal too)."""
+    torch = torch_cuda
+    p = qi.cfg3()
+    N, T = 256, 200.0
+    u = oracle.sines_nodes(p.sines, p.u_max, N, T)[None]
+    plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(rL0, rLc, u[0], T, N, mode=1, order=order)
+    parts = qal.qal_block_expm_slices(plan, L0p, Lcp, dev(torch, u), T, N, chunk=16, magnus_order=order,
+                                      ctrl_mode=1, Lcommp=Lcommp)
+    got = qal.qal_block_unpack(plan, qal.qal_block_ordered_product(plan, parts))[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP
+
+
+def test_block_slice_range_k0(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    p = qi.cfg3()
+    N, T = 256, 200.0
+    u = oracle.sines_nodes(p.sines, p.u_max, N, T)[None]
+    plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    k0, cnt = 96, 64
+    Lam = oracle.propagate(rL0, rLc, u[0], T, N, mode=1, k0=k0, k1=k0 + cnt)
+    parts = qal.qal_block_expm_slices(plan, L0p, Lcp, dev(torch, u[:, k0:k0 + cnt]), T, N, k0=k0, count=cnt,
+                                      chunk=cnt, ctrl_mode=1, Lcommp=Lcommp)
+    got = qal.qal_block_unpack(plan, parts[:, 0])[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP
+
+
+@pytest.mark.parametrize("T,N", [(100.0, 4), (1000.0, 2), (3.0, 8), (100.0, 64)])
+def test_block_norm_regimes(torch_cuda, qal, oracle, T, N):
+    """Per-block (m, s) choices: squarings (s > 0) and the T8 scheme."""
+    torch = torch_cuda
+    p = qi.cfg0(N=N, T=T)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(rL0, rLc, p.u[0], T, N)
+    F, _, Lp = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), T, N, dev(torch, p.V),
+                                           want_grad=False, want_Lambda=True)
+    got = qal.qal_block_unpack(plan, Lp)[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP
