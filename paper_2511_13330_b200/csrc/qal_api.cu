@@ -702,7 +702,7 @@ int qal_block_expm_slices(const qal_block_plan* plan, int batch, int n_slices, d
   c.G.count = count;
   cudaStream_t st = S(stream);
   if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
-  BlkFwdOut O{nullptr, D2(chunk_prod), chunk, status};
+  BlkFwdOut O{nullptr, D2(chunk_prod), chunk, status, nullptr};
   return cuda_rc(launch_blk_expm_fold(*plan, batch, c.B, c.G, O, st));
 }
 
@@ -769,7 +769,7 @@ int qal_block_fidelity_grad(const qal_block_plan* plan, int batch, int n_slices,
     double2* lam_tmp = reinterpret_cast<double2*>(w);
     w += (size_t)batch * mb;
     double2* lam = Lambda_packed ? D2(Lambda_packed) : lam_tmp;
-    BlkFwdOut O{nullptr, parts, ch, status};
+    BlkFwdOut O{nullptr, parts, ch, status, nullptr};
     if (launch_blk_expm_fold(*plan, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
     if ((rc = run_blk_tree(plan, batch, nch, parts, lam, w, st)) != QAL_OK) return rc;
     return cuda_rc(launch_blk_fidelity(*plan, batch, lam, D2(V), F, st));
@@ -779,10 +779,26 @@ int qal_block_fidelity_grad(const qal_block_plan* plan, int batch, int n_slices,
 }  // extern "C"
 
 namespace {
-size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices) { (void)p; (void)batch; (void)n_slices; return 0; }
+size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices) {
+  const size_t img = (size_t)p->packed * 16;
+  return 3 * (size_t)batch * n_slices * img + (size_t)batch * img + blk_grad_scratch_bytes(*p);
+}
+// forward (U_k and prefix P_k images, Lambda) -> fidelity -> suffix chain (X_{k+1}) -> gradient slices
 int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
                            double* grad, double2* Lam, int* status, void* ws, cudaStream_t st) {
-  (void)p; (void)batch; (void)c; (void)V; (void)F; (void)grad; (void)Lam; (void)status; (void)ws; (void)st;
-  return QAL_ERR_UNSUPPORTED;
+  const size_t seq = (size_t)batch * c.G.count * 2 * p->packed;   // doubles per image sequence
+  double* U = reinterpret_cast<double*>(ws);
+  double* P = U + seq;
+  double* X = P + seq;
+  double2* lam_tmp = reinterpret_cast<double2*>(X + seq);
+  double* scratch = reinterpret_cast<double*>(lam_tmp + (size_t)batch * p->packed);
+  double2* lam = Lam ? Lam : lam_tmp;
+  BlkFwdOut O{U, lam, c.G.count, status, P};
+  if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_blk_suffix_chain(*p, batch, c.G.count, U, V, X, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_blk_grad_slices(*p, batch, c.B, c.G, P, X, grad, status, scratch, st) != cudaSuccess)
+    return QAL_ERR_CUDA;
+  return QAL_OK;
 }
 }  // namespace

@@ -429,6 +429,10 @@ __device__ void blk_fwd_group(const BlkDev& D, const BlkBasis& B, const SliceGri
     if (O.U_img) bstore_img(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x.rt, L);
     if (O.chunk_nat) {
       if (kk == 0) {
+        if (O.P_img) {                                // P_0 = I
+          bset_identity(acc, x.rt, L);
+          bstore_img(O.P_img + slot * 2 * D.packed + 2 * x.off, acc, x.rt, L);
+        }
         bstore_img(SP, A, x.rt, L);
       } else {
         bzero(acc); bmma(acc, A, SP, L);              // P <- U_k P
@@ -437,6 +441,7 @@ __device__ void blk_fwd_group(const BlkDev& D, const BlkBasis& B, const SliceGri
         grp_sync(x.g, C);
         bstore_img(SP, A, x.rt, L);
       }
+      if (O.P_img && kk + 1 < O.chunk) bstore_img(O.P_img + (slot + 1) * 2 * D.packed + 2 * x.off, A, x.rt, L);
     }
     grp_sync(x.g, C);   // SX / SX4 / red free for the next slice
   }
@@ -600,6 +605,541 @@ __global__ void __launch_bounds__(256) k_blk_fidelity(BlkDev D, const double2* _
   if (threadIdx.x == 0) F[blockIdx.x] = s / 64.0;
 }
 
+// ------------------------------------------------------------------ gradient (a7), block form
+// The fidelity gradient of qal_grad.cu restricted to the blocks: G_k = P_k X_{k+1} is block
+// diagonal on the stored blocks (P_k block diagonal, and only the diagonal blocks of S_V^dag
+// enter X_{k+1} = S_V^dag U_{N-1}..U_{k+1} through Re Tr(S_V^dag Lambda)), the adjoint Frechet
+// derivative W_k = L_exp(Omega_k, G_k) of a block-diagonal Omega_k is computed block by block,
+// and dF/du = Re Tr(W_k dOmega_k/du)/d^2 sums the blocks with the component weights (a mirrored
+// block gives the same real part as its stored partner).
+
+// TMEM strips: 4C 32-bit columns per plane; warp w uses lane quarter w % 4 and the column range
+// (w / 4) * 128 + slot * 32 (slot < 4).
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t addr, const uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_st<4>(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_st<8>(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t addr, uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_ld<4>(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(addr)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(addr)
+               : "memory");
+}
+// one plane of 2C doubles = 4C words: C = 1 -> x4, C = 2 -> x8, C = 3 -> x8 + x4
+template <int C>
+__device__ __forceinline__ void tm_st_plane(uint32_t addr, const double* x) {
+  uint32_t v[4 * C];
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    v[2 * i] = static_cast<uint32_t>(__double2loint(x[i]));
+    v[2 * i + 1] = static_cast<uint32_t>(__double2hiint(x[i]));
+  }
+  if (C == 1) tm_st<4>(addr, v);
+  if (C >= 2) tm_st<8>(addr, v);
+  if (C == 3) tm_st<4>(addr + 8, v + 8);
+}
+template <int C>
+__device__ __forceinline__ void tm_ld_plane(uint32_t addr, uint32_t* v) {
+  if (C == 1) tm_ld<4>(addr, v);
+  if (C >= 2) tm_ld<8>(addr, v);
+  if (C == 3) tm_ld<4>(addr + 8, v + 8);
+}
+template <int C>
+__device__ __forceinline__ void bt_store(uint32_t addr, const BS<C>& s) {
+  tm_st_plane<C>(addr, s.re);
+  tm_st_plane<C>(addr + 4 * C, s.im);
+  tmem_wait_st();
+}
+template <int C>
+__device__ __forceinline__ void bt_load(BS<C>& s, uint32_t addr) {
+  uint32_t v[4 * C], w[4 * C];
+  tm_ld_plane<C>(addr, v);
+  tm_ld_plane<C>(addr + 4 * C, w);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    s.re[i] = __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i]));
+    s.im[i] = __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i]));
+  }
+}
+template <int C>
+__device__ __forceinline__ void bt_axpy(BS<C>& acc, double a, uint32_t addr) {
+  if (a == 0.0) return;
+  uint32_t v[4 * C], w[4 * C];
+  tm_ld_plane<C>(addr, v);
+  tm_ld_plane<C>(addr + 4 * C, w);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    acc.re[i] = fma(a, __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i])), acc.re[i]);
+    acc.im[i] = fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[i]);
+  }
+}
+// global image strip with an L2 policy
+template <int C>
+__device__ __forceinline__ void bload_img_l2(BS<C>& s, const double* __restrict__ img, int rt, const Lane& L,
+                                             uint64_t pol) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int o = bpair_off<C>(rt, L, j);
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(s.re[2 * j]), "=d"(s.re[2 * j + 1])
+                 : "l"(img + o), "l"(pol));
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(s.im[2 * j]), "=d"(s.im[2 * j + 1])
+                 : "l"(img + PL + o), "l"(pol));
+  }
+}
+template <int C>
+__device__ __forceinline__ void bstore_img_l2(double* __restrict__ img, const BS<C>& s, int rt, const Lane& L,
+                                              uint64_t pol) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int o = bpair_off<C>(rt, L, j);
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + o), "d"(s.re[2 * j]),
+                 "d"(s.re[2 * j + 1]), "l"(pol)
+                 : "memory");
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + PL + o), "d"(s.im[2 * j]),
+                 "d"(s.im[2 * j + 1]), "l"(pol)
+                 : "memory");
+  }
+}
+template <int C>
+__device__ __forceinline__ void baxpy_img_l2(BS<C>& acc, double a, const double* __restrict__ img, int rt,
+                                             const Lane& L, uint64_t pol) {
+  if (a == 0.0) return;
+  BS<C> x;
+  bload_img_l2(x, img, rt, L, pol);
+  baxpy(acc, a, x);
+}
+// one thread: bulk-copy a group image (16 P^2 bytes) global -> shared, arriving on `bar`
+__device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int C, uint64_t* bar) {
+  const uint32_t bytes = 16u * 64u * C * C;
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s_hint(dst, src, bytes, bar, l2_evict_first());
+}
+
+// --------------------------------------------------------------- suffix chain
+// X_N = S_V^dag on the stored blocks, X_k = X_{k+1} U_k; X_img[b][k-1] = X_k (k = 1..N).
+// One CTA per pulse; the groups run independently; U_k streamed by per-group TMA (double buffer).
+template <int C>
+__device__ void blk_suffix_group(const BlkDev& D, int N, const double* U, const double2* V, double* X,
+                                 const GrpCtx& x, double* sm, uint64_t* bar, unsigned long long& nprod,
+                                 const Lane& L) {
+  constexpr int P = 8 * C;
+  double* SU[2] = {sm, sm + 2 * 64 * C * C};
+  const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
+  const int go = 2 * x.off;
+  const bool leader = (x.rt == 0 && L.lane == 0);
+  const int row0 = 8 * D.wrp0[x.g];
+  BS<C> A, acc;
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    const int a = D.perm[row0 + 8 * x.rt + L.g], c = D.perm[row0 + 4 * i + L.t];
+    double re = 0.0, im = 0.0;
+    if (a >= 0 && c >= 0) {
+      const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
+      const double2 vjl = __ldg(V + j * 8 + l), vik = __ldg(V + ii * 8 + kk);
+      re = vjl.x * vik.x + vjl.y * vik.y;
+      im = vjl.y * vik.x - vjl.x * vik.y;
+    }
+    A.re[i] = re;
+    A.im[i] = im;
+  }
+  (void)P;
+  bstore_img(X + (size_t)(N - 1) * stride + go, A, x.rt, L);
+  if (leader && N > 1) tma_grp_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * stride + go, C, &bar[(N - 1) & 1]);
+  uint32_t ph[2] = {0, 0};
+  for (int k = N - 1; k >= 1; --k) {
+    const int cur = k & 1;
+    grp_sync(x.g, C);   // buffer cur^1 (read at step k+1) is free
+    if (leader && k - 1 >= 1) {
+      fence_proxy_async();
+      tma_grp_img(SU[cur ^ 1], U + (size_t)(k - 1) * stride + go, C, &bar[cur ^ 1]);
+    }
+    mbar_wait(&bar[cur], ph[cur]);
+    ph[cur] ^= 1;
+    bzero(acc);
+    bmma(acc, A, SU[cur], L);   // X_{k+1} U_k
+    bcopy(A, acc);
+    bstore_img_l2(X + (size_t)(k - 1) * stride + go, A, x.rt, L, l2_evict_first());
+  }
+  if (leader) nprod += (unsigned long long)(N - 1);
+}
+
+__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4) k_blk_suffix_chain(BlkDev D, int N,
+                                                                           const double* __restrict__ U_img,
+                                                                           const double2* __restrict__ V,
+                                                                           double* __restrict__ X_img,
+                                                                           unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];
+  const Lane L = lane_id();
+  const GrpCtx x = grp_of(D, L.w);
+  if (x.rt == 0 && L.lane == 0) {
+    mbar_init(&bars[x.g][0], 1);
+    mbar_init(&bars[x.g][1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const size_t base = (size_t)blockIdx.x * N * 2 * D.packed;
+  unsigned long long nprod = 0;
+  double* sm = smem + D.soff[x.g];
+  switch (x.C) {
+    case 1: blk_suffix_group<1>(D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nprod, L); break;
+    case 2: blk_suffix_group<2>(D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nprod, L); break;
+    default: blk_suffix_group<3>(D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nprod, L); break;
+  }
+  if (ctr && nprod) atomicAdd(ctr, nprod * D.gflops[x.g]);
+}
+
+// --------------------------------------------------------------- gradient slices
+constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
+constexpr int BLK_GRAD_SCR = 6;   // L2 scratch images per group: X, dX, A6, dA6, E, dE
+
+// Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
+// returns the product count and leaves W = L_exp(Omega, G) in A.  SD, SV, SN: group images
+// (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots; scr: the group's L2 scratch.
+template <int C>
+__device__ __forceinline__ int blk_dual_expm(BS<C>& A, BS<C>& acc, const BlkBasis& B, const SliceGrid& G,
+                                             const double* Pk, int b, int k, const GrpCtx& x, double* SD,
+                                             double* SV, double* SN, uint64_t* barN, uint32_t& phN, double* red,
+                                             uint32_t tm, double* scr, int* bad, const Lane& L) {
+  const int g = x.g, rt = x.rt;
+  const size_t IM = 2 * 64 * C * C;
+  double* gX = scr;
+  double* gdX = scr + IM;
+  double* gA6 = scr + 2 * IM;
+  double* gdA6 = scr + 3 * IM;
+  double* gE = scr + 4 * IM;
+  double* gdE = scr + 5 * IM;
+  const uint32_t T0 = tm, T1 = tm + 32, T2 = tm + 64, T3 = tm + 96;   // A2, dA2, A3|Y, dA3|dY
+  const uint64_t keep = l2_evict_last();
+  bbuild_omega(A, B, G, b, k, x.off, rt, L);
+  const double nrm = bnorm1(A, red, g, rt, L);
+  int m, s;
+  choose_scheme(nrm, m, s);
+  if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+  const double sc = ldexp(1.0, -s);
+  bscale(A, sc);
+  bstore_img(SV, A, rt, L);
+  bstore_img_l2(gX, A, rt, L, keep);
+  // G = P_k X_{k+1};  dX = G / 2^s
+  bload_img_l2(A, Pk, rt, L, l2_evict_first());
+  mbar_wait(barN, phN);
+  phN ^= 1;
+  bzero(acc);
+  bmma(acc, A, SN, L);
+  bscale(acc, sc);
+  grp_sync(g, C);                                      // SV (X) complete
+  bstore_img(SD, acc, rt, L);
+  bstore_img_l2(gdX, acc, rt, L, keep);
+  grp_sync(g, C);                                      // SD = dX complete
+  bload_img(A, SV, rt, L);
+  bzero(acc); bmma(acc, A, SV, L);                     // A2 = X X
+  bt_store(T0, acc);
+  bzero(acc); bmma(acc, A, SD, L);                     // X dX
+  bload_img(A, SD, rt, L);
+  bmma(acc, A, SV, L);                                 // + dX X
+  bt_store(T1, acc);
+  int np = 1 + 1 + 2;
+  if (m == 8) {
+    grp_sync(g, C);
+    bzero(acc); baxpy_img_l2(acc, c_t8[0], gX, rt, L, keep); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, rt, L);
+    bzero(acc); baxpy_img_l2(acc, c_t8[0], gdX, rt, L, keep); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, rt, L);
+    grp_sync(g, C);
+    bt_load(A, T0);
+    bzero(acc); bmma(acc, A, SV, L);                   // Y = A2 W
+    bt_store(T2, acc);
+    bzero(acc); bmma(acc, A, SD, L);                   // A2 dW
+    bt_load(A, T1);
+    bmma(acc, A, SV, L);                               // + dA2 W = dY
+    bt_store(T3, acc);
+    grp_sync(g, C);
+    bzero(acc); bt_axpy(acc, 1.0, T2); bt_axpy(acc, c_t8[4], T0); bstore_img(SV, acc, rt, L);
+    bzero(acc); bt_axpy(acc, 1.0, T3); bt_axpy(acc, c_t8[4], T1); bstore_img(SD, acc, rt, L);
+    grp_sync(g, C);
+    bzero(acc);
+    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img_l2(acc, 1.0, gdX, rt, L, keep);
+    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img_l2(A, c_t8[3], gdX, rt, L, keep);   // dL
+    bmma(acc, A, SV, L);
+    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img_l2(A, c_t8[3], gX, rt, L, keep);    // L
+    bmma(acc, A, SD, L);
+    if (s > 0) bstore_img_l2(gdE, acc, rt, L, keep);
+    np += 1 + 2 + 2;
+    if (s > 0) {
+      bzero(acc);
+      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img_l2(acc, 1.0, gX, rt, L, keep);
+      badd_diag(acc, 1.0, rt, L);
+      bmma(acc, A, SV, L);
+      bstore_img_l2(gE, acc, rt, L, keep);
+      ++np;
+    }
+  } else {
+    bt_load(A, T0);
+    bzero(acc); bmma(acc, A, SV, L);                   // A3
+    bt_store(T2, acc);
+    bzero(acc); bmma(acc, A, SD, L);                   // A2 dX
+    bt_load(A, T1);
+    bmma(acc, A, SV, L);                               // + dA2 X = dA3
+    bt_store(T3, acc);
+    grp_sync(g, C);
+    bt_load(A, T2); bstore_img(SV, A, rt, L);
+    bt_load(A, T3); bstore_img(SD, A, rt, L);
+    grp_sync(g, C);
+    bt_load(A, T2);
+    bzero(acc); bmma(acc, A, SV, L);                   // A6
+    bstore_img_l2(gA6, acc, rt, L, keep);
+    bzero(acc); bmma(acc, A, SD, L);                   // A3 dA3
+    bt_load(A, T3);
+    bmma(acc, A, SV, L);                               // + dA3 A3
+    bstore_img_l2(gdA6, acc, rt, L, keep);
+    grp_sync(g, C);
+    bzero(acc);
+    baxpy_img_l2(acc, c_t18[T18_B5][1], gX, rt, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T0);
+    baxpy_img_l2(acc, 1.0, gA6, rt, L, keep);
+    bstore_img(SV, acc, rt, L);
+    bzero(acc);
+    baxpy_img_l2(acc, c_t18[T18_B5][1], gdX, rt, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T1);
+    baxpy_img_l2(acc, 1.0, gdA6, rt, L, keep);
+    bstore_img(SD, acc, rt, L);
+    grp_sync(g, C);
+    bzero(acc);                                        // dA9 = dB4 + dB1 B5 + B1 dB5
+    baxpy_img_l2(acc, c_t18[T18_B4][1], gdX, rt, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T1);
+    bt_axpy(acc, c_t18[T18_B4][3], T3); baxpy_img_l2(acc, c_t18[T18_B4][4], gdA6, rt, L, keep);
+    bzero(A);
+    baxpy_img_l2(A, c_t18[T18_B1][1], gdX, rt, L, keep); bt_axpy(A, c_t18[T18_B1][2], T1);
+    bt_axpy(A, c_t18[T18_B1][3], T3);
+    bmma(acc, A, SV, L);
+    bzero(A);
+    baxpy_img_l2(A, c_t18[T18_B1][1], gX, rt, L, keep); bt_axpy(A, c_t18[T18_B1][2], T0);
+    bt_axpy(A, c_t18[T18_B1][3], T2);
+    bmma(acc, A, SD, L);
+    bstore_img(SN, acc, rt, L);                        // dA9 (SN idle since G)
+    bzero(acc);                                        // A9 = B4 + B1 B5 (A holds B1)
+    badd_diag(acc, c_t18[T18_B4][0], rt, L);
+    baxpy_img_l2(acc, c_t18[T18_B4][1], gX, rt, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T0);
+    bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img_l2(acc, c_t18[T18_B4][4], gA6, rt, L, keep);
+    bmma(acc, A, SV, L);
+    grp_sync(g, C);                                    // reads of SV (B5), SD (dB5) done
+    bstore_img(SV, acc, rt, L);                        // A9
+    grp_sync(g, C);                                    // A9 (SV), dA9 (SN) complete
+    bzero(acc);                                        // dT = dB2 + dL A9 + L dA9
+    baxpy_img_l2(acc, c_t18[T18_B2][1], gdX, rt, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T1);
+    bt_axpy(acc, c_t18[T18_B2][3], T3); baxpy_img_l2(acc, c_t18[T18_B2][4], gdA6, rt, L, keep);
+    bload_img(A, SN, rt, L);                           // dL = dB3 + dA9
+    baxpy_img_l2(A, c_t18[T18_B3][1], gdX, rt, L, keep); bt_axpy(A, c_t18[T18_B3][2], T1);
+    bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img_l2(A, c_t18[T18_B3][4], gdA6, rt, L, keep);
+    bmma(acc, A, SV, L);
+    bload_img(A, SV, rt, L);                           // L = B3 + A9
+    badd_diag(A, c_t18[T18_B3][0], rt, L);
+    baxpy_img_l2(A, c_t18[T18_B3][1], gX, rt, L, keep); bt_axpy(A, c_t18[T18_B3][2], T0);
+    bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img_l2(A, c_t18[T18_B3][4], gA6, rt, L, keep);
+    bmma(acc, A, SN, L);
+    if (s > 0) bstore_img_l2(gdE, acc, rt, L, keep);
+    np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
+    if (s > 0) {                                       // T = B2 + L A9
+      bzero(acc);
+      badd_diag(acc, c_t18[T18_B2][0], rt, L);
+      baxpy_img_l2(acc, c_t18[T18_B2][1], gX, rt, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T0);
+      bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img_l2(acc, c_t18[T18_B2][4], gA6, rt, L, keep);
+      bmma(acc, A, SV, L);
+      bstore_img_l2(gE, acc, rt, L, keep);
+      ++np;
+    }
+  }
+  for (int q = 0; q < s; ++q) {                        // (E, dE) <- (E E, dE E + E dE)
+    grp_sync(g, C);
+    bload_img_l2(A, gE, rt, L, keep);
+    bstore_img(SV, A, rt, L);
+    bload_img_l2(acc, gdE, rt, L, keep);
+    bstore_img(SD, acc, rt, L);
+    grp_sync(g, C);
+    bzero(acc); bmma(acc, A, SD, L);                   // E dE
+    bload_img_l2(A, gdE, rt, L, keep);
+    bmma(acc, A, SV, L);                               // + dE E
+    bstore_img_l2(gdE, acc, rt, L, keep);
+    bload_img_l2(A, gE, rt, L, keep);
+    bzero(acc); bmma(acc, A, SV, L);                   // E E
+    bstore_img_l2(gE, acc, rt, L, keep);
+    np += 3;
+  }
+  if (s > 0) bload_img_l2(A, gdE, rt, L, keep);
+  else bcopy(A, acc);
+  return np;
+}
+
+// weighted traces Re Tr(W_g B_m,g) of the group, per warp partial sums into red_tr[w][m]
+template <int C>
+__device__ __forceinline__ void blk_traces(const BS<C>& W, const BlkDev& D, const BlkBasis& B, int b, const GrpCtx& x,
+                                           double* red_tr, const Lane& L) {
+  constexpr int P = 8 * C;
+  const int K = B.J + B.ncomm;
+  const int r = 8 * x.rt + L.g;
+  const double wr = (double)D.weight[8 * D.wrp0[x.g] + r];
+  for (int mm = 0; mm < K; ++mm) {
+    const double2* Bm = (mm < B.J) ? B.Lc + (size_t)mm * B.packed
+                                   : B.Lcomm + (size_t)b * B.Lcomm_stride + (size_t)(mm - B.J) * B.packed;
+    Bm += x.off;
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      const double2 y = __ldg(Bm + (4 * i + L.t) * P + r);
+      v = fma(W.re[i], y.x, v);
+      v = fma(-W.im[i], y.y, v);
+    }
+    v *= wr;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (L.lane == 0) red_tr[L.w * BLK_TR_MAX + mm] = v;
+  }
+}
+
+// per-group shared memory of the gradient kernel: SD, SV, SN images + norm buffer
+__host__ __device__ constexpr int grad_grp_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
+
+__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4, 1) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B,
+                                                                             SliceGrid G,
+                                                                             const double* __restrict__ P_img,
+                                                                             const double* __restrict__ X_img,
+                                                                             double* __restrict__ grad,
+                                                                             int* __restrict__ status,
+                                                                             double* __restrict__ scratch,
+                                                                             int tmem_cols, unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS];
+  __shared__ double red_tr[(QAL_BLK_MAX_ROWS / 8) * BLK_TR_MAX + BLK_TR_MAX];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int bad_sh;
+  const Lane L = lane_id();
+  const GrpCtx x = grp_of(D, L.w);
+  if (L.w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const bool leader = (x.rt == 0 && L.lane == 0);
+  if (leader) {
+    mbar_init(&bars[x.g], 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x == 0) bad_sh = 0;
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tm = tmem_base_sh + (static_cast<uint32_t>(32 * (L.w & 3)) << 16) + static_cast<uint32_t>((L.w >> 2) * 128);
+  double* sm = smem + D.soff[x.g];
+  const int IM = 2 * 64 * x.C * x.C;
+  double* SD = sm;
+  double* SV = sm + IM;
+  double* SN = sm + 2 * IM;
+  double* red = sm + 3 * IM;
+  double* scr = scratch + ((size_t)blockIdx.x * 2 * D.packed + 2 * x.off) * BLK_GRAD_SCR;
+  const size_t stride = 2 * (size_t)D.packed;
+  const int N = G.count;
+  const int items = batch * N;
+  const int K = B.J + B.ncomm;
+  uint32_t phN = 0;
+  unsigned long long nprod = 0;
+  if (leader && blockIdx.x < items)
+    tma_grp_img(SN, X_img + (size_t)blockIdx.x * stride + 2 * x.off, x.C, &bars[x.g]);
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = item / N, k = item % N;
+    const double* Pk = P_img + (size_t)item * stride + 2 * x.off;
+    BS<3> A3, acc3;
+    int np;
+    switch (x.C) {
+      case 1: {
+        BS<1> A, acc;
+        np = blk_dual_expm<1>(A, acc, B, G, Pk, b, k, x, SD, SV, SN, &bars[x.g], phN, red, tm, scr, &bad_sh, L);
+        blk_traces<1>(A, D, B, b, x, red_tr, L);
+        break;
+      }
+      case 2: {
+        BS<2> A, acc;
+        np = blk_dual_expm<2>(A, acc, B, G, Pk, b, k, x, SD, SV, SN, &bars[x.g], phN, red, tm, scr, &bad_sh, L);
+        blk_traces<2>(A, D, B, b, x, red_tr, L);
+        break;
+      }
+      default:
+        np = blk_dual_expm<3>(A3, acc3, B, G, Pk, b, k, x, SD, SV, SN, &bars[x.g], phN, red, tm, scr, &bad_sh, L);
+        blk_traces<3>(A3, D, B, b, x, red_tr, L);
+        break;
+    }
+    if (leader) nprod += (unsigned long long)np * D.gflops[x.g];
+    __syncthreads();   // every group done with this item: SN free, red_tr complete
+    if (leader && item + (int)gridDim.x < items) {
+      fence_proxy_async();
+      tma_grp_img(SN, X_img + (size_t)(item + gridDim.x) * stride + 2 * x.off, x.C, &bars[x.g]);
+    }
+    if (threadIdx.x < K) {
+      double t = 0.0;
+      for (int w = 0; w < D.nwarps; ++w) t += red_tr[w * BLK_TR_MAX + threadIdx.x];
+      red_tr[(QAL_BLK_MAX_ROWS / 8) * BLK_TR_MAX + threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double* T = red_tr + (QAL_BLK_MAX_ROWS / 8) * BLK_TR_MAX;
+      const int J = B.J;
+      const double inv_d2 = 1.0 / 64.0;
+      if (G.mode == 0) {
+        double* gg = grad + ((size_t)b * N + k) * J;
+        for (int j = 0; j < J; ++j) gg[j] = G.h * T[j] * inv_d2;
+      } else {
+        const double* u = G.u + ((size_t)b * N + k) * 2 * J;
+        double* gg = grad + ((size_t)b * N + k) * 2 * J;
+        for (int j = 0; j < J; ++j) {
+          double g1 = 0.5 * G.h * T[j], g2 = 0.5 * G.h * T[j];
+          if (B.ncomm > 0) {
+            double c1 = -T[J + j], c2 = T[J + j];
+            int p = 2 * J;
+            for (int a = 0; a < J; ++a)
+              for (int c = a + 1; c < J; ++c, ++p) {
+                const double Tp = T[p];
+                if (a == j) { c1 += u[J + c] * Tp; c2 -= u[c] * Tp; }
+                if (c == j) { c1 -= u[J + a] * Tp; c2 += u[a] * Tp; }
+              }
+            g1 -= G.c4 * c1;
+            g2 -= G.c4 * c2;
+          }
+          gg[j] = g1 * inv_d2;
+          gg[J + j] = g2 * inv_d2;
+        }
+      }
+      if (bad_sh && status) { status[b] = QAL_ERR_NONFINITE; }
+      bad_sh = 0;
+    }
+  }
+  if (ctr && leader && nprod) atomicAdd(ctr, nprod);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (L.w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "r"(tmem_cols));
+}
+
 // ------------------------------------------------------------------ launchers
 namespace {
 int grp_smem_doubles(const BlkDev& D, int (*per)(int), int* soff) {
@@ -612,6 +1152,8 @@ int grp_smem_doubles(const BlkDev& D, int (*per)(int), int* soff) {
   return o;
 }
 int fwd_per(int C) { return fwd_grp_doubles(C); }
+int chain_per(int C) { return 2 * 2 * 64 * C * C; }
+int grad_per(int C) { return grad_grp_doubles(C); }
 int pair_per(int C) { return 2 * 64 * C * C; }
 }  // namespace
 
@@ -641,6 +1183,54 @@ cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, c
   prof_pre(ST_BLK_TREE, st);
   k_blk_tree_level<<<batch * half, 32 * D.nwarps, bytes, st>>>(D, cnt, in, out, prof_counter(ST_BLK_TREE));
   prof_post(ST_BLK_TREE, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
+                                    const double2* V, double* X_img, cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  const size_t bytes = (size_t)grp_smem_doubles(D, chain_per, D.soff) * 8;
+  static size_t attr = 0;
+  if (bytes > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_blk_suffix_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    attr = bytes;
+  }
+  prof_pre(ST_BLK_SUFFIX, st);
+  k_blk_suffix_chain<<<batch, 32 * D.nwarps, bytes, st>>>(D, N, U_img, V, X_img, prof_counter(ST_BLK_SUFFIX));
+  prof_post(ST_BLK_SUFFIX, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// persistent: two CTAs per SM (TMEM: 128 columns per warp pair sharing a lane quarter)
+static int blk_grad_grid() { return 2 * num_sms(); }
+
+size_t blk_grad_scratch_bytes(const qal_block_plan& p) {
+  return (size_t)blk_grad_grid() * BLK_GRAD_SCR * 2 * p.packed * 8;
+}
+
+cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
+                                   const double* P_img, const double* X_img, double* grad, int* status,
+                                   double* scratch, cudaStream_t st) {
+  BlkDev D = to_dev(p);
+  const size_t bytes = (size_t)grp_smem_doubles(D, grad_per, D.soff) * 8;
+  static size_t attr = 0;
+  if (bytes > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_blk_grad_slices, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    attr = bytes;
+  }
+  const int quarters_rows = (D.nwarps + 3) / 4;           // warps sharing a lane quarter
+  int cols = 32;
+  while (cols < 128 * quarters_rows) cols *= 2;
+  const int items = batch * G.count;
+  const int grid = items < blk_grad_grid() ? items : blk_grad_grid();
+  prof_pre(ST_BLK_GRAD, st);
+  k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, cols,
+                                                         prof_counter(ST_BLK_GRAD));
+  prof_post(ST_BLK_GRAD, st);
   ++launch_counter();
   return cudaGetLastError();
 }

@@ -53,6 +53,7 @@ struct BlkFwdOut {
   double2* chunk_nat;  // [batch][count/chunk] packed natural, or nullptr
   int chunk;
   int* status;
+  double* P_img;       // gradient path (chunk == count): prefix images P_k = U_{k-1}..U_0, or nullptr
 };
 int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block_plan* out);
 cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
@@ -63,6 +64,12 @@ cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* n
                             cudaStream_t st);
 cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2* packed, double2* nat,
                               cudaStream_t st);
+cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
+                                    const double2* V, double* X_img, cudaStream_t st);
+cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
+                                   const double* P_img, const double* X_img, double* grad, int* status,
+                                   double* scratch, cudaStream_t st);
+size_t blk_grad_scratch_bytes(const qal_block_plan& p);
 cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
                                 cudaStream_t st);
 

@@ -179,3 +179,71 @@ def test_block_norm_regimes(torch_cuda, qal, oracle, T, N):
                                            want_grad=False, want_Lambda=True)
     got = qal.qal_block_unpack(plan, Lp)[0].cpu().numpy()
     assert relfro(got, Lam) <= TOL_PROP
+
+
+# ------------------------------------------------------------------ gradient (a7) on the blocks
+@pytest.mark.parametrize("mirror", [True, False])
+def test_cfg1_block_gradient(torch_cuda, qal, oracle, mirror):
+    torch = torch_cuda
+    p = qi.cfg1()
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p, mirror)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Fr, gr, Lam = oracle.gradient(rL0, rLc, p.u[0], p.T, p.N, p.V)
+    F, g, Lp = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V),
+                                           want_Lambda=True)
+    assert relfro(qal.qal_block_unpack(plan, Lp)[0].cpu().numpy(), Lam) <= TOL_PROP
+    assert abs(F.item() - Fr) / abs(Fr) <= TOL_PROP
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD, relfro(g[0].cpu().numpy(), gr)
+
+
+def test_cfg2_recipe_block_gradient(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    p = qi.cfg2(batch=3, N=32, T=200.0 * 32 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    F, g, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V))
+    for b in range(3):
+        rL0, rLc = oracle.build_liouvillian(p.H0[b], p.Hc, p.C)
+        Fr, gr, _ = oracle.gradient(rL0, rLc, p.u[b], p.T, p.N, p.V)
+        assert abs(F[b].item() - Fr) / abs(Fr) <= TOL_PROP
+        assert relfro(g[b].cpu().numpy(), gr) <= TOL_GRAD
+
+
+def test_nodes_mode_block_gradient(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    p = qi.cfg3()
+    N, T = 64, 300.0
+    u = oracle.sines_nodes(p.sines, p.u_max, N, T)[None]
+    plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Fr, gr, _ = oracle.gradient(rL0, rLc, u[0], T, N, p.V, mode=1)
+    F, g, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, u), T, N, dev(torch, p.V), ctrl_mode=1,
+                                          Lcommp=Lcommp)
+    assert abs(F.item() - Fr) / abs(Fr) <= TOL_PROP
+    assert g.shape == (1, N, 2, 2)
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
+
+
+@pytest.mark.parametrize("T,N", [(100.0, 4), (1000.0, 2), (3.0, 8), (100.0, 64)])
+def test_block_gradient_norm_regimes(torch_cuda, qal, oracle, T, N):
+    torch = torch_cuda
+    p = qi.cfg0(N=N, T=T)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Fr, gr, _ = oracle.gradient(rL0, rLc, p.u[0], T, N, p.V)
+    F, g, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), T, N, dev(torch, p.V))
+    assert abs(F.item() - Fr) <= TOL_PROP * max(abs(Fr), 1e-3)
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
+
+
+def test_block_gradient_matches_dense_path_bitwise_shape(torch_cuda, qal):
+    """Same layout and values (within rounding) as the dense qal_fidelity_grad on a larger batch."""
+    torch = torch_cuda
+    p = qi.cfg2(batch=64, N=128, T=200.0 * 128 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    L0, Lc, _ = qal.qal_build_liouvillian(dev(torch, p.H0), dev(torch, p.Hc), dev(torch, p.C))
+    Fd, gd, _ = qal.qal_fidelity_grad(L0, Lc, dev(torch, p.u), p.T, p.N, dev(torch, p.V))
+    Fb, gb, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V))
+    assert gb.shape == gd.shape
+    assert ((Fb - Fd).abs() / Fd.abs()).max().item() <= 1e-12
+    err = ((gb - gd).reshape(64, -1).norm(dim=1) / gd.reshape(64, -1).norm(dim=1)).max().item()
+    assert err <= 1e-11, err

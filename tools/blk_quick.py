@@ -27,3 +27,14 @@ ms_b, (Fb, _, _) = timeit(lambda: qal.qal_block_fidelity_grad(plan, L0p, Lcp, u,
 err = (Fb - Fd).abs().max().item() / Fd.abs().max().item()
 print(f"dense fwd {ms_d:.1f} ms  {B*N/ms_d/1e3:.3f} M slices/s")
 print(f"block fwd {ms_b:.1f} ms  {B*N/ms_b/1e3:.3f} M slices/s  speedup {ms_d/ms_b:.1f}x  maxrelF {err:.2e}")
+Bg = min(B, 296)
+ug = u[:Bg].contiguous()
+ms_dg, (Fdg, gd, _) = timeit(lambda: qal.qal_fidelity_grad(L0[:Bg].contiguous(), Lc, ug, p.T, N, V), reps=1)
+ms_bg, (Fbg, gb, _) = timeit(lambda: qal.qal_block_fidelity_grad(plan, L0p[:Bg].contiguous(), Lcp, ug, p.T, N, V), reps=1)
+eg = ((gb - gd).reshape(Bg, -1).norm(dim=1) / gd.reshape(Bg, -1).norm(dim=1)).max().item()
+print(f"dense fwd+grad {ms_dg:.1f} ms  {Bg*N/ms_dg/1e3:.3f} M slices/s")
+print(f"block fwd+grad {ms_bg:.1f} ms  {Bg*N/ms_bg/1e3:.3f} M slices/s  speedup {ms_dg/ms_bg:.1f}x  max rel grad err {eg:.2e}")
+qal.qal_profile_begin()
+qal.qal_block_fidelity_grad(plan, L0p[:Bg].contiguous(), Lcp, ug, p.T, N, V)
+torch.cuda.synchronize()
+print({k: v for k, v in qal.qal_profile_end().items() if v[1]})
