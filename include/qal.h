@@ -300,6 +300,7 @@ typedef struct {
     int packed;                         /* complex elements per packed matrix = sum width^2   */
     int n_components;                   /* connected components of the basis sparsity graph  */
     int width[QAL_BLK_MAX_GROUPS];      /* padded width of group g: 8, 16 or 24               */
+    int used[QAL_BLK_MAX_GROUPS];       /* rows of group g that are not padding               */
     int row0[QAL_BLK_MAX_GROUPS];       /* first packed row of group g                        */
     int off[QAL_BLK_MAX_GROUPS];        /* complex offset of group g inside a packed matrix   */
     double flops[QAL_BLK_MAX_GROUPS];   /* algorithmic flops of one product of group g:

@@ -9,19 +9,23 @@
 // product Lambda (Eq. 15) and every prefix / suffix product -- is block diagonal, with
 // blocks 20/15/15/6/6/1/1 for d = 8.  Hermiticity preservation (Lambda[s(R), s(C)] =
 // conj(Lambda[R, C]), s(i + d j) = j + d i, pin P-5) pairs block q with block -q, so with
-// `mirror` only q >= 0 is computed (20, 15, 6, 1): 2.9% of the dense flops.
+// `mirror` only q >= 0 is computed (20, 15, 6, 1): 4.4% of the dense flops.
 //
 // The structure is DETECTED, not assumed: qal_block_plan_build takes the union sparsity
 // pattern of the generator basis and finds its connected components (host), and
 // k_blk_check re-verifies on the device that every off-block entry of every basis matrix
-// of every pulse is exactly zero (status QAL_ERR_STRUCTURE otherwise).
+// of every pulse is exactly zero (QAL_ERR_STRUCTURE otherwise).
 //
-// Layout: components are packed into "super-blocks" (groups) of padded width
-// P = 8C, C in {1..4} column tiles; a packed matrix is the concatenation of the groups'
-// P x P blocks (natural row-major complex).  A CTA holds one warp per 8-row tile of every
-// group (6 warps for d = 8 with mirror): the warps of group g run the dense kernels'
-// strip algorithm (qal_dev.cuh) on a P-wide strip, synchronised by their own named
-// barrier, independently of the other groups.
+// Layout: components are packed (best fit) into "super-blocks" (groups) of padded width
+// P = 8C, C in {1, 2, 3}; a packed matrix is the concatenation of the groups' P x P blocks.
+// Work mapping: a CTA owns one item (pulse chunk / slice) of every group.  A group with
+// C = 3 is run by 3 warps (one 8-row strip each, named barrier); smaller groups are run
+// whole by one warp (R = C strips), several of them on the same warp, so that every warp
+// issues about the same number of DMMAs per product (d = 8 with the mirror: warps 0-2 the
+// 20-block, warp 3 the 15+1 and 6 blocks; 60 / 60 / 60 / 72 DMMAs per product).  With
+// 4-warp CTAs, warp w runs on SM sub-partition w % 4, so the FP64 pipes of all four
+// sub-partitions are loaded evenly.  Products skip the k-steps that only touch padding
+// rows (K trim: the 20-block multiplies with K = 20, not 24).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -34,34 +38,84 @@
 
 namespace qal {
 
+constexpr int BLK_MAX_WARPS = 8;
+constexpr int BLK_MAX_TASKS = 3;
+#ifndef QAL_BLK_MAXNREG
+#define QAL_BLK_MAXNREG 168   // 3 four-warp CTAs per SM (64K registers)
+#endif
+
 // ------------------------------------------------------------------ device plan
+struct BlkTask {
+  signed char g, rt0, R, pad;   // group, first row tile, row tiles owned
+};
 struct BlkDev {
-  int ngroups, nwarps, packed;
+  int ngroups, nwarps, packed, d;
   int C[QAL_BLK_MAX_GROUPS];       // column (= row) tiles of group g
+  int ks[QAL_BLK_MAX_GROUPS];      // k-steps of 4 covering the used rows of group g
   int off[QAL_BLK_MAX_GROUPS];     // complex offset of group g in a packed matrix
-  int wrp0[QAL_BLK_MAX_GROUPS];    // first warp (row tile) of group g
+  int row0[QAL_BLK_MAX_GROUPS];    // first packed row of group g
+  int gwarps[QAL_BLK_MAX_GROUPS];  // warps sharing group g (named barrier size / 32)
   int soff[QAL_BLK_MAX_GROUPS];    // double offset of group g's shared-memory region
-  signed char perm[QAL_BLK_MAX_ROWS];     // packed row -> natural index (-1 pad)
-  unsigned char weight[QAL_BLK_MAX_ROWS]; // 0 pad, 1, 2
-  signed char inv[64];                    // natural index -> packed row (-1 not stored)
-  signed char comp[64];                   // natural index -> component
-  int d;
+  int ntask[BLK_MAX_WARPS];
+  BlkTask task[BLK_MAX_WARPS][BLK_MAX_TASKS];
+  signed char perm[QAL_BLK_MAX_ROWS];      // packed row -> natural index (-1 pad)
+  unsigned char weight[QAL_BLK_MAX_ROWS];  // 0 pad, 1, 2
+  signed char inv[64];                     // natural index -> packed row (-1 not stored)
+  signed char comp[64];                    // natural index -> component
   unsigned long long gflops[QAL_BLK_MAX_GROUPS];   // algorithmic flops of one product of group g
 };
 
-BlkDev to_dev(const qal_block_plan& p) {
-  BlkDev D;
+// warp roles: C = 3 groups -> 3 warps (one strip each); C <= 2 groups -> whole group on one
+// warp, greedily stacked so that no warp exceeds the heaviest single-strip load
+static int blk_cost(int C, int R, int ks) { return C * R * ks; }
+
+bool to_dev(const qal_block_plan& p, BlkDev& D) {
   memset(&D, 0, sizeof(D));
   D.ngroups = p.ngroups;
-  D.nwarps = p.nrows / 8;
   D.packed = p.packed;
   D.d = p.d;
   for (int g = 0; g < p.ngroups; ++g) {
     D.C[g] = p.width[g] / 8;
+    D.ks[g] = (p.used[g] + 3) / 4;
     D.off[g] = p.off[g];
-    D.wrp0[g] = p.row0[g] / 8;
+    D.row0[g] = p.row0[g];
     D.gflops[g] = (unsigned long long)p.flops[g];
   }
+  int w = 0, heavy = 0;
+  for (int g = 0; g < p.ngroups; ++g)
+    if (D.C[g] == 3) {
+      D.gwarps[g] = 3;
+      for (int r = 0; r < 3; ++r) {
+        if (w >= BLK_MAX_WARPS) return false;
+        D.task[w][0] = {(signed char)g, (signed char)r, 1, 0};
+        D.ntask[w++] = 1;
+      }
+      heavy = std::max(heavy, blk_cost(3, 1, D.ks[g]));
+    }
+  std::vector<int> small;
+  for (int g = 0; g < p.ngroups; ++g)
+    if (D.C[g] < 3) small.push_back(g);
+  std::stable_sort(small.begin(), small.end(), [&](int a, int b) {
+    return blk_cost(D.C[a], D.C[a], D.ks[a]) > blk_cost(D.C[b], D.C[b], D.ks[b]);
+  });
+  int load[BLK_MAX_WARPS] = {0};
+  const int first_small = w;
+  for (int g : small) {
+    const int c = blk_cost(D.C[g], D.C[g], D.ks[g]);
+    int best = -1;
+    for (int v = first_small; v < w; ++v)
+      if (D.ntask[v] < BLK_MAX_TASKS && load[v] + c <= std::max(heavy, c) + c / 4 &&
+          (best < 0 || load[v] < load[best]))
+        best = v;
+    if (best < 0) {
+      if (w >= BLK_MAX_WARPS) return false;
+      best = w++;
+    }
+    D.task[best][D.ntask[best]++] = {(signed char)g, 0, (signed char)D.C[g], 0};
+    D.gwarps[g] = 1;
+    load[best] += c;
+  }
+  D.nwarps = w;
   for (int r = 0; r < QAL_BLK_MAX_ROWS; ++r) {
     D.perm[r] = (signed char)(r < p.nrows ? p.perm[r] : -1);
     D.weight[r] = (unsigned char)(r < p.nrows ? p.weight[r] : 0);
@@ -70,154 +124,233 @@ BlkDev to_dev(const qal_block_plan& p) {
     D.inv[i] = (signed char)(i < p.n ? p.inv[i] : -1);
     D.comp[i] = (signed char)(i < p.n ? p.comp[i] : -1);
   }
-  return D;
+  return true;
 }
 
-// group of the calling warp
-struct GrpCtx {
-  int g, C, rt, P, off;   // rt = row tile within the group
+// the calling warp's view of one task
+struct Ctx {
+  int g, rt0, ks, off, row0, nw;
 };
-__device__ __forceinline__ GrpCtx grp_of(const BlkDev& D, int w) {
-  GrpCtx x;
-  x.g = 0;
-#pragma unroll 1
-  for (int g = 1; g < D.ngroups; ++g)
-    if (w >= D.wrp0[g]) x.g = g;
-  x.C = D.C[x.g];
-  x.rt = w - D.wrp0[x.g];
-  x.P = 8 * x.C;
-  x.off = D.off[x.g];
+__device__ __forceinline__ Ctx ctx_of(const BlkDev& D, const BlkTask& t) {
+  Ctx x;
+  x.g = t.g;
+  x.rt0 = t.rt0;
+  x.ks = D.ks[t.g];
+  x.off = D.off[t.g];
+  x.row0 = D.row0[t.g];
+  x.nw = D.gwarps[t.g];
   return x;
 }
-
-__device__ __forceinline__ void grp_sync(int g, int C) {
-  if (C == 1) {
+__device__ __forceinline__ void grp_sync(const Ctx& x) {
+  if (x.nw == 1) {
     __syncwarp();
   } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(32 * C) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(x.g + 1), "r"(32 * x.nw) : "memory");
   }
 }
 
-// ------------------------------------------------------------------ P-wide strips
-// Strip of 8 rows (row tile rt) of a P x P block, A-fragment layout: s[i] = M[8 rt + g][4 i + t].
-template <int C>
-struct BS {
-  double re[2 * C], im[2 * C];
+// the warp roles every kernel instantiates: (C, R, KS) = (3, 1, 5|6), (2, 2, 4), (1, 1, 2)
+// (KS = k-steps of the products; the 20-block runs with K = 20: 5 k-steps)
+#define BLK_DISPATCH(CC, KSV, FN, ...)                    \
+  do {                                                    \
+    if ((CC) == 3) {                                      \
+      if ((KSV) <= 5) FN<3, 1, 5>(__VA_ARGS__);           \
+      else FN<3, 1, 6>(__VA_ARGS__);                      \
+    } else if ((CC) == 2) FN<2, 2, 4>(__VA_ARGS__);       \
+    else FN<1, 1, 2>(__VA_ARGS__);                        \
+  } while (0)
+
+// ------------------------------------------------------------------ P-wide strips, R per warp
+// Strip r (row tile rt0 + r) of a P x P block in the A-fragment layout:
+//   s.re/im[r][i] = M[8 (rt0 + r) + g][4 i + t],  i < 2C.
+template <int C, int R>
+struct BR {
+  double re[R][2 * C], im[R][2 * C];
 };
 
-template <int C>
-__device__ __forceinline__ void bzero(BS<C>& s) {
+template <int C, int R>
+__device__ __forceinline__ void bzero(BR<C, R>& s) {
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) { s.re[i] = 0.0; s.im[i] = 0.0; }
-}
-template <int C>
-__device__ __forceinline__ void bcopy(BS<C>& d, const BS<C>& s) {
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) { d.re[i] = s.re[i]; d.im[i] = s.im[i]; }
+    for (int i = 0; i < 2 * C; ++i) { s.re[r][i] = 0.0; s.im[r][i] = 0.0; }
 }
-template <int C>
-__device__ __forceinline__ void baxpy(BS<C>& acc, double a, const BS<C>& x) {
+template <int C, int R>
+__device__ __forceinline__ void bcopy(BR<C, R>& d, const BR<C, R>& s) {
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) { acc.re[i] = fma(a, x.re[i], acc.re[i]); acc.im[i] = fma(a, x.im[i], acc.im[i]); }
-}
-template <int C>
-__device__ __forceinline__ void bscale(BS<C>& s, double a) {
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) { s.re[i] *= a; s.im[i] *= a; }
+    for (int i = 0; i < 2 * C; ++i) { d.re[r][i] = s.re[r][i]; d.im[r][i] = s.im[r][i]; }
 }
-// diagonal test: row 8 rt + g, column 4 i + t
-template <int C>
-__device__ __forceinline__ void badd_diag(BS<C>& s, double a, int rt, const Lane& L) {
+template <int C, int R>
+__device__ __forceinline__ void baxpy(BR<C, R>& acc, double a, const BR<C, R>& x) {
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i)
-    if (8 * rt + L.g == 4 * i + L.t) s.re[i] += a;
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      acc.re[r][i] = fma(a, x.re[r][i], acc.re[r][i]);
+      acc.im[r][i] = fma(a, x.im[r][i], acc.im[r][i]);
+    }
 }
-template <int C>
-__device__ __forceinline__ void bset_identity(BS<C>& s, int rt, const Lane& L) {
+template <int C, int R>
+__device__ __forceinline__ void bscale(BR<C, R>& s, double a) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) { s.re[r][i] *= a; s.im[r][i] *= a; }
+}
+template <int C, int R>
+__device__ __forceinline__ void badd_diag(BR<C, R>& s, double a, const Ctx& x, const Lane& L) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i)
+      if (8 * (x.rt0 + r) + L.g == 4 * i + L.t) s.re[r][i] += a;
+}
+template <int C, int R>
+__device__ __forceinline__ void bset_identity(BR<C, R>& s, const Ctx& x, const Lane& L) {
   bzero(s);
-  badd_diag(s, 1.0, rt, L);
+  badd_diag(s, 1.0, x, L);
 }
 
 // image of a P x P block: re plane (P*P doubles) then im plane; column c of row r at
 // r*P + phys(c) (the within-tile permutation of qal_dev.cuh) XOR 8 on odd rows when C is
 // even (with C odd the row stride 8C already alternates the bank halves).
 template <int C>
-__device__ __forceinline__ int bpair_off(int rt, const Lane& L, int j) {
-  const int r = 8 * rt + L.g;
+__device__ __forceinline__ int bpair_off(int row, const Lane& L, int j) {
   const int swz = (C % 2 == 0) ? ((L.g & 1) << 3) : 0;
-  return r * (8 * C) + ((8 * j + 2 * L.t) ^ swz);
+  return row * (8 * C) + ((8 * j + 2 * L.t) ^ swz);
 }
-template <int C>
-__device__ __forceinline__ void bload_img(BS<C>& s, const double* __restrict__ img, int rt, const Lane& L) {
+template <int C, int R>
+__device__ __forceinline__ void bload_img(BR<C, R>& s, const double* __restrict__ img, const Ctx& x, const Lane& L) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int o = bpair_off<C>(rt, L, j);
-    const double2 a = *reinterpret_cast<const double2*>(img + o);
-    const double2 b = *reinterpret_cast<const double2*>(img + PL + o);
-    s.re[2 * j] = a.x; s.re[2 * j + 1] = a.y;
-    s.im[2 * j] = b.x; s.im[2 * j + 1] = b.y;
-  }
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
+      const double2 a = *reinterpret_cast<const double2*>(img + o);
+      const double2 b = *reinterpret_cast<const double2*>(img + PL + o);
+      s.re[r][2 * j] = a.x; s.re[r][2 * j + 1] = a.y;
+      s.im[r][2 * j] = b.x; s.im[r][2 * j + 1] = b.y;
+    }
 }
-template <int C>
-__device__ __forceinline__ void bstore_img(double* __restrict__ img, const BS<C>& s, int rt, const Lane& L) {
+template <int C, int R>
+__device__ __forceinline__ void bstore_img(double* __restrict__ img, const BR<C, R>& s, const Ctx& x, const Lane& L) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int o = bpair_off<C>(rt, L, j);
-    *reinterpret_cast<double2*>(img + o) = make_double2(s.re[2 * j], s.re[2 * j + 1]);
-    *reinterpret_cast<double2*>(img + PL + o) = make_double2(s.im[2 * j], s.im[2 * j + 1]);
-  }
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
+      *reinterpret_cast<double2*>(img + o) = make_double2(s.re[r][2 * j], s.re[r][2 * j + 1]);
+      *reinterpret_cast<double2*>(img + PL + o) = make_double2(s.im[r][2 * j], s.im[r][2 * j + 1]);
+    }
 }
-// acc += a * image strip (no temporary strip kept live)
-template <int C>
-__device__ __forceinline__ void baxpy_img(BS<C>& acc, double a, const double* __restrict__ img, int rt,
+// acc += a * image (no temporary strip kept live)
+template <int C, int R>
+__device__ __forceinline__ void baxpy_img(BR<C, R>& acc, double a, const double* __restrict__ img, const Ctx& x,
                                           const Lane& L) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int o = bpair_off<C>(rt, L, j);
-    const double2 x = *reinterpret_cast<const double2*>(img + o);
-    const double2 y = *reinterpret_cast<const double2*>(img + PL + o);
-    acc.re[2 * j] = fma(a, x.x, acc.re[2 * j]); acc.re[2 * j + 1] = fma(a, x.y, acc.re[2 * j + 1]);
-    acc.im[2 * j] = fma(a, y.x, acc.im[2 * j]); acc.im[2 * j + 1] = fma(a, y.y, acc.im[2 * j + 1]);
-  }
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
+      const double2 u = *reinterpret_cast<const double2*>(img + o);
+      const double2 v = *reinterpret_cast<const double2*>(img + PL + o);
+      acc.re[r][2 * j] = fma(a, u.x, acc.re[r][2 * j]); acc.re[r][2 * j + 1] = fma(a, u.y, acc.re[r][2 * j + 1]);
+      acc.im[r][2 * j] = fma(a, v.x, acc.im[r][2 * j]); acc.im[r][2 * j + 1] = fma(a, v.y, acc.im[r][2 * j + 1]);
+    }
 }
-// natural row-major P x P complex block <-> strip
-template <int C>
-__device__ __forceinline__ void bload_nat(BS<C>& s, const double2* __restrict__ M, int rt, const Lane& L) {
+// global image with an L2 policy
+template <int C, int R>
+__device__ __forceinline__ void bload_img_l2(BR<C, R>& s, const double* __restrict__ img, const Ctx& x, const Lane& L,
+                                             uint64_t pol) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
+      asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(s.re[r][2 * j]), "=d"(s.re[r][2 * j + 1])
+                   : "l"(img + o), "l"(pol));
+      asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(s.im[r][2 * j]), "=d"(s.im[r][2 * j + 1])
+                   : "l"(img + PL + o), "l"(pol));
+    }
+}
+template <int C, int R>
+__device__ __forceinline__ void bstore_img_l2(double* __restrict__ img, const BR<C, R>& s, const Ctx& x,
+                                              const Lane& L, uint64_t pol) {
+  constexpr int PL = 64 * C * C;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
+      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + o), "d"(s.re[r][2 * j]),
+                   "d"(s.re[r][2 * j + 1]), "l"(pol)
+                   : "memory");
+      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + PL + o), "d"(s.im[r][2 * j]),
+                   "d"(s.im[r][2 * j + 1]), "l"(pol)
+                   : "memory");
+    }
+}
+template <int C, int R>
+__device__ __forceinline__ void baxpy_img_l2(BR<C, R>& acc, double a, const double* __restrict__ img, const Ctx& x,
+                                             const Lane& L, uint64_t pol) {
+  if (a == 0.0) return;
+  BR<C, R> y;
+  bload_img_l2(y, img, x, L, pol);
+  baxpy(acc, a, y);
+}
+// natural row-major P x P complex block <-> strips
+template <int C, int R>
+__device__ __forceinline__ void bload_nat(BR<C, R>& s, const double2* __restrict__ M, const Ctx& x, const Lane& L) {
   constexpr int P = 8 * C;
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) {
-    const double2 v = __ldg(M + (8 * rt + L.g) * P + 4 * i + L.t);
-    s.re[i] = v.x; s.im[i] = v.y;
-  }
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      const double2 v = __ldg(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t);
+      s.re[r][i] = v.x; s.im[r][i] = v.y;
+    }
 }
-template <int C>
-__device__ __forceinline__ void bstore_nat(double2* __restrict__ M, const BS<C>& s, int rt, const Lane& L) {
+template <int C, int R>
+__device__ __forceinline__ void bstore_nat(double2* __restrict__ M, const BR<C, R>& s, const Ctx& x, const Lane& L) {
   constexpr int P = 8 * C;
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) M[(8 * rt + L.g) * P + 4 * i + L.t] = make_double2(s.re[i], s.im[i]);
-}
-template <int C>
-__device__ __forceinline__ void baxpy_nat(BS<C>& X, double a, const double2* __restrict__ M, int rt, const Lane& L) {
-  constexpr int P = 8 * C;
-  const uint64_t keep = l2_evict_last();
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) {
-    double vx, vy;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(vx), "=d"(vy)
-                 : "l"(M + (8 * rt + L.g) * P + 4 * i + L.t), "l"(keep));
-    X.re[i] = fma(a, vx, X.re[i]);
-    X.im[i] = fma(a, vy, X.im[i]);
-  }
+    for (int i = 0; i < 2 * C; ++i) M[(8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t] = make_double2(s.re[r][i], s.im[r][i]);
+}
+template <int C, int R>
+__device__ __forceinline__ void baxpy_nat(BR<C, R>& X, double a, const double2* __restrict__ M, const Ctx& x,
+                                          const Lane& L) {
+  constexpr int P = 8 * C;
+  const uint64_t keep = l2_evict_last();   // the basis is shared by every CTA
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      double vx, vy;
+      asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(vx), "=d"(vy)
+                   : "l"(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t), "l"(keep));
+      X.re[r][i] = fma(a, vx, X.re[r][i]);
+      X.im[r][i] = fma(a, vy, X.im[r][i]);
+    }
 }
 
-// acc += A * B, A = strip, B = image (FP64 tensor cores, 4 real MMAs per complex 8x8x4 step;
-// the P-wide version of qal_dev.cuh's mma_acc_4m)
-template <int C>
-__device__ __forceinline__ void bmma(BS<C>& acc, const BS<C>& a, const double* __restrict__ Bs, const Lane& L) {
+// acc += A * B on the FP64 tensor cores: A = strips (registers), B = image (shared).
+// 4 real MMAs per complex 8x8x4 step (qal_dev.cuh mma_acc_4m); only the first KS k-steps
+// (rows of B that are not padding); the B fragments of a k-step serve all R strips.
+template <int C, int R, int KS>
+__device__ __forceinline__ void bmma(BR<C, R>& acc, const BR<C, R>& a, const double* __restrict__ Bs, const Ctx& x,
+                                     const Lane& L) {
+  static_assert(KS >= 1 && KS <= 2 * C, "k-steps");
   constexpr int P = 8 * C, PL = P * P;
   const int swz = (C % 2 == 0) ? (L.t & 1) : 0;   // physical tile of logical tile j: j ^ swz
   const uint32_t base = smem_u32(Bs + L.t * P + L.g);
@@ -229,45 +362,53 @@ __device__ __forceinline__ void bmma(BS<C>& acc, const BS<C>& a, const double* _
     bi[0][j] = lds_v(p + 8u * PL);
   }
 #pragma unroll
-  for (int q = 0; q < 2 * C; ++q) {
-    const int cur = q & 1;
-    if (q + 1 < 2 * C) {
+  for (int q = 0; q < KS; ++q) {
+    {
+      const int cur = q & 1;
+      if (q + 1 < KS) {
 #pragma unroll
-      for (int j = 0; j < C; ++j) {
-        const uint32_t p = base + 8u * ((q + 1) * 4 * P + 8 * (j ^ swz));
-        br[cur ^ 1][j] = lds_v(p);
-        bi[cur ^ 1][j] = lds_v(p + 8u * PL);
+        for (int j = 0; j < C; ++j) {
+          const uint32_t p = base + 8u * ((q + 1) * 4 * P + 8 * (j ^ swz));
+          br[cur ^ 1][j] = lds_v(p);
+          bi[cur ^ 1][j] = lds_v(p + 8u * PL);
+        }
       }
-    }
-    const double ar = a.re[q], ai = a.im[q], nai = -a.im[q];
 #pragma unroll
-    for (int j = 0; j < C; ++j) {
-      dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br[cur][j]);
-      dmma(acc.re[2 * j], acc.re[2 * j + 1], nai, bi[cur][j]);
-      dmma(acc.im[2 * j], acc.im[2 * j + 1], ar, bi[cur][j]);
-      dmma(acc.im[2 * j], acc.im[2 * j + 1], ai, br[cur][j]);
+      for (int r = 0; r < R; ++r) {
+        const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
+          dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], nai, bi[cur][j]);
+          dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ar, bi[cur][j]);
+          dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ai, br[cur][j]);
+        }
+      }
     }
   }
   QAL_FENCE();
 }
 
-// ||X||_1 of the group's block (max column sum of |x|), fixed order; red: >= 8 C * 8 C doubles
-// private to the group.  One group barrier; every warp of the group returns the same value.
-template <int C>
-__device__ __forceinline__ double bnorm1(const BS<C>& s, double* red, int g, int rt, const Lane& L) {
+// ||X||_1 of the group's block (max column sum of |x|), fixed order.  red: >= P * P doubles of
+// the group's region (partial column sums per row tile).  One group barrier.
+template <int C, int R>
+__device__ __forceinline__ double bnorm1(const BR<C, R>& s, double* red, const Ctx& x, const Lane& L) {
   constexpr int P = 8 * C;
-  double cs[2 * C];
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) cs[i] = hypot(s.re[i], s.im[i]);
+  for (int r = 0; r < R; ++r) {
+    double cs[2 * C];
 #pragma unroll
-  for (int o = 4; o < 32; o <<= 1)
+    for (int i = 0; i < 2 * C; ++i) cs[i] = hypot(s.re[r][i], s.im[r][i]);
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
-  if (L.g == 0) {
+    for (int o = 4; o < 32; o <<= 1)
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) red[rt * P + 4 * i + L.t] = cs[i];
+      for (int i = 0; i < 2 * C; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
+    if (L.g == 0) {
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) red[(x.rt0 + r) * P + 4 * i + L.t] = cs[i];
+    }
   }
-  grp_sync(g, C);
+  grp_sync(x);
   double m = 0.0;
   if (L.lane < P) {
     double a = 0.0;
@@ -278,218 +419,338 @@ __device__ __forceinline__ double bnorm1(const BS<C>& s, double* red, int g, int
   bool nan = !(m == m);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const double x = __shfl_xor_sync(0xffffffffu, m, o);
-    nan = nan || !(x == x);
-    m = fmax(m, x);
+    const double y = __shfl_xor_sync(0xffffffffu, m, o);
+    nan = nan || !(y == y);
+    m = fmax(m, y);
   }
   nan = __any_sync(0xffffffffu, nan);
   return nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
 }
 
-// Omega_k strip of the group from the packed generator basis (a1-a3, as build_omega)
-template <int C>
-__device__ __forceinline__ void bbuild_omega(BS<C>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
-                                             int off, int rt, const Lane& L) {
+// Omega_k strips of the group from the packed generator basis (a1-a3, as build_omega)
+template <int C, int R>
+__device__ __forceinline__ void bbuild_omega(BR<C, R>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
+                                             const Ctx& x, const Lane& L) {
   const int J = B.J;
   const int nodes = (G.mode == 1) ? 2 : 1;
   const double* u = G.u + ((size_t)b * G.count + k) * nodes * J;
   bzero(X);
-  baxpy_nat(X, G.h, B.L0 + (size_t)b * B.L0_stride + off, rt, L);
+  baxpy_nat(X, G.h, B.L0 + (size_t)b * B.L0_stride + x.off, x, L);
   for (int j = 0; j < J; ++j) {
     const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * J + j);
-    baxpy_nat(X, 0.5 * G.h * (v1 + v2), B.Lc + (size_t)j * B.packed + off, rt, L);
+    baxpy_nat(X, 0.5 * G.h * (v1 + v2), B.Lc + (size_t)j * B.packed + x.off, x, L);
   }
   if (B.ncomm > 0) {
-    const double2* Cb = B.Lcomm + (size_t)b * B.Lcomm_stride + off;
+    const double2* Cb = B.Lcomm + (size_t)b * B.Lcomm_stride + x.off;
     for (int j = 0; j < J; ++j) {
       const double v1 = __ldg(u + j), v2 = __ldg(u + J + j);
-      baxpy_nat(X, -G.c4 * (v2 - v1), Cb + (size_t)j * B.packed, rt, L);
+      baxpy_nat(X, -G.c4 * (v2 - v1), Cb + (size_t)j * B.packed, x, L);
     }
     int p = J;
     for (int a = 0; a < J; ++a)
       for (int c = a + 1; c < J; ++c, ++p) {
         const double coef = -G.c4 * (__ldg(u + a) * __ldg(u + J + c) - __ldg(u + c) * __ldg(u + J + a));
-        baxpy_nat(X, coef, Cb + (size_t)p * B.packed, rt, L);
+        baxpy_nat(X, coef, Cb + (size_t)p * B.packed, x, L);
       }
   }
 }
 
-// U = expm(X 2^s) for the group's block (the T8 / T18 schemes of qal_slice.cuh, powers kept in
-// registers); X's strip in A and its image in SX; SX4 = the group's shared operand image.
-// Result in A.  Returns the products done.
+// ------------------------------------------------------------------ TMEM strips
+// 8C columns per strip (re 4C words, im 4C words); a warp's slot s of strip r starts at column
+// tm + 32 s + 8C r (slot stride 32 columns: R * 8C <= 32 for every role).
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t addr, const uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_st<4>(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_st<8>(uint32_t addr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t addr, uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_ld<4>(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(addr)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(addr)
+               : "memory");
+}
+// one plane of 2C doubles = 4C words: C = 1 -> x4, C = 2 -> x8, C = 3 -> x8 + x4
 template <int C>
-__device__ __forceinline__ int bexpm(BS<C>& A, BS<C>& acc, int m, int s, double* SX, double* SX4, int g, int rt,
-                                     const Lane& L) {
-  BS<C> T0, T1, T2;
+__device__ __forceinline__ void tm_st_plane(uint32_t addr, const double* y) {
+  uint32_t v[4 * C];
+#pragma unroll
+  for (int i = 0; i < 2 * C; ++i) {
+    v[2 * i] = static_cast<uint32_t>(__double2loint(y[i]));
+    v[2 * i + 1] = static_cast<uint32_t>(__double2hiint(y[i]));
+  }
+  if (C == 1) tm_st<4>(addr, v);
+  if (C >= 2) tm_st<8>(addr, v);
+  if (C == 3) tm_st<4>(addr + 8, v + 8);
+}
+template <int C>
+__device__ __forceinline__ void tm_ld_plane(uint32_t addr, uint32_t* v) {
+  if (C == 1) tm_ld<4>(addr, v);
+  if (C >= 2) tm_ld<8>(addr, v);
+  if (C == 3) tm_ld<4>(addr + 8, v + 8);
+}
+template <int C, int R>
+__device__ __forceinline__ void bt_store(uint32_t addr, const BR<C, R>& s) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    tm_st_plane<C>(addr + 8 * C * r, s.re[r]);
+    tm_st_plane<C>(addr + 8 * C * r + 4 * C, s.im[r]);
+  }
+  tmem_wait_st();
+}
+template <int C, int R>
+__device__ __forceinline__ void bt_load(BR<C, R>& s, uint32_t addr) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t v[4 * C], w[4 * C];
+    tm_ld_plane<C>(addr + 8 * C * r, v);
+    tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      s.re[r][i] = __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i]));
+      s.im[r][i] = __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i]));
+    }
+  }
+}
+template <int C, int R>
+__device__ __forceinline__ void bt_axpy(BR<C, R>& acc, double a, uint32_t addr) {
+  if (a == 0.0) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t v[4 * C], w[4 * C];
+    tm_ld_plane<C>(addr + 8 * C * r, v);
+    tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      acc.re[r][i] = fma(a, __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i])), acc.re[r][i]);
+      acc.im[r][i] = fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[r][i]);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t warp_tmem(uint32_t base, const Lane& L) {
+  return base + (static_cast<uint32_t>(32 * (L.w & 3)) << 16) + static_cast<uint32_t>((L.w >> 2) * 128);
+}
+__device__ __forceinline__ void blk_tmem_alloc(uint32_t* slot, int cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void blk_tmem_dealloc(uint32_t base, int cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols));
+}
+
+// ------------------------------------------------------------------ expm (a4) per group
+// U = expm(X 2^s): the T8 / T18 schemes of qal_slice.cuh with the powers in TMEM slots
+// tm + {0, 32, 64}; X's strips in A and its image in SX; SX4 = the group's operand image.
+// Result in A.  Returns the products done.
+template <int C, int R, int KS>
+__device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, double* SX, double* SX4, uint32_t tm,
+                                     const Ctx& x, const Lane& L) {
+  const uint32_t T0 = tm, T1 = tm + 32, T2 = tm + 64;
   int prods;
-  bzero(acc); bmma(acc, A, SX, L);                     // A2 = X X
-  bcopy(T0, acc);
+  bzero(acc); bmma<C, R, KS>(acc, A, SX, x, L);                  // A2 = X X
+  bt_store(T0, acc);
   if (m == 8) {
     bzero(A);                                          // W = c1 X + c2 A2 (shared)
-    baxpy(A, c_t8[1], T0);
-    baxpy_img(A, c_t8[0], SX, rt, L);
-    bstore_img(SX4, A, rt, L);
-    grp_sync(g, C);
-    bzero(acc); bmma(acc, T0, SX4, L);                 // Y = A2 W
-    bcopy(T1, acc);
-    grp_sync(g, C);                                    // reads of SX4 (W) done
-    baxpy(acc, c_t8[4], T0);                           // R = Y + c5 A2 (shared)
-    bstore_img(SX4, acc, rt, L);
-    bcopy(A, T1);                                      // L = Y + c3 A2 + c4 X
-    baxpy(A, c_t8[2], T0);
-    baxpy_img(A, c_t8[3], SX, rt, L);
-    grp_sync(g, C);
+    baxpy(A, c_t8[1], acc);
+    baxpy_img(A, c_t8[0], SX, x, L);
+    bstore_img(SX4, A, x, L);
+    bcopy(A, acc);                                     // A = A2
+    grp_sync(x);
+    bzero(acc); bmma<C, R, KS>(acc, A, SX4, x, L);               // Y = A2 W
+    bt_store(T1, acc);
+    grp_sync(x);                                       // reads of SX4 (W) done
+    baxpy(acc, c_t8[4], A);                            // R = Y + c5 A2 (shared)
+    bstore_img(SX4, acc, x, L);
+    bt_load(A, T1);                                    // L = Y + c3 A2 + c4 X
+    bt_axpy(A, c_t8[2], T0);
+    baxpy_img(A, c_t8[3], SX, x, L);
+    grp_sync(x);
     bzero(acc);                                        // T8 = c6 Y + c7 A2 + X + I + L R
-    baxpy(acc, c_t8[5], T1);
-    baxpy(acc, c_t8[6], T0);
-    baxpy_img(acc, 1.0, SX, rt, L);
-    badd_diag(acc, 1.0, rt, L);
-    bmma(acc, A, SX4, L);
+    bt_axpy(acc, c_t8[5], T1);
+    bt_axpy(acc, c_t8[6], T0);
+    baxpy_img(acc, 1.0, SX, x, L);
+    badd_diag(acc, 1.0, x, L);
+    bmma<C, R, KS>(acc, A, SX4, x, L);
     bcopy(A, acc);
     prods = 3;
   } else {
-    bzero(acc); bmma(acc, T0, SX, L);                  // A3 = A2 X
-    bcopy(T1, acc);
-    bstore_img(SX4, acc, rt, L);
-    grp_sync(g, C);
-    bzero(acc); bmma(acc, T1, SX4, L);                 // A6 = A3 A3
-    bcopy(T2, acc);
-    baxpy_img(acc, c_t18[T18_B5][1], SX, rt, L);       // B5 = e1 X + e2 A2 + A6
-    baxpy(acc, c_t18[T18_B5][2], T0);
-    grp_sync(g, C);                                    // reads of SX4 (A3) done
-    bstore_img(SX4, acc, rt, L);
+    bcopy(A, acc);
+    bzero(acc); bmma<C, R, KS>(acc, A, SX, x, L);                // A3 = A2 X
+    bt_store(T1, acc);
+    bstore_img(SX4, acc, x, L);
+    bcopy(A, acc);
+    grp_sync(x);
+    bzero(acc); bmma<C, R, KS>(acc, A, SX4, x, L);               // A6 = A3 A3
+    bt_store(T2, acc);
+    baxpy_img(acc, c_t18[T18_B5][1], SX, x, L);        // B5 = e1 X + e2 A2 + A6
+    bt_axpy(acc, c_t18[T18_B5][2], T0);
+    grp_sync(x);                                       // reads of SX4 (A3) done
+    bstore_img(SX4, acc, x, L);
     bzero(A);                                          // B1
-    baxpy_img(A, c_t18[T18_B1][1], SX, rt, L);
-    baxpy(A, c_t18[T18_B1][2], T0);
-    baxpy(A, c_t18[T18_B1][3], T1);
+    baxpy_img(A, c_t18[T18_B1][1], SX, x, L);
+    bt_axpy(A, c_t18[T18_B1][2], T0);
+    bt_axpy(A, c_t18[T18_B1][3], T1);
     bzero(acc);                                        // B4
-    badd_diag(acc, c_t18[T18_B4][0], rt, L);
-    baxpy_img(acc, c_t18[T18_B4][1], SX, rt, L);
-    baxpy(acc, c_t18[T18_B4][2], T0);
-    baxpy(acc, c_t18[T18_B4][3], T1);
-    baxpy(acc, c_t18[T18_B4][4], T2);
-    grp_sync(g, C);                                    // B5 image complete
-    bmma(acc, A, SX4, L);                              // A9 = B4 + B1 B5
-    grp_sync(g, C);                                    // reads of SX4 (B5) done
-    bstore_img(SX4, acc, rt, L);
+    badd_diag(acc, c_t18[T18_B4][0], x, L);
+    baxpy_img(acc, c_t18[T18_B4][1], SX, x, L);
+    bt_axpy(acc, c_t18[T18_B4][2], T0);
+    bt_axpy(acc, c_t18[T18_B4][3], T1);
+    bt_axpy(acc, c_t18[T18_B4][4], T2);
+    grp_sync(x);                                       // B5 image complete
+    bmma<C, R, KS>(acc, A, SX4, x, L);                           // A9 = B4 + B1 B5
+    grp_sync(x);                                       // reads of SX4 (B5) done
+    bstore_img(SX4, acc, x, L);
     bcopy(A, acc);                                     // L = B3 + A9
-    badd_diag(A, c_t18[T18_B3][0], rt, L);
-    baxpy_img(A, c_t18[T18_B3][1], SX, rt, L);
-    baxpy(A, c_t18[T18_B3][2], T0);
-    baxpy(A, c_t18[T18_B3][3], T1);
-    baxpy(A, c_t18[T18_B3][4], T2);
+    badd_diag(A, c_t18[T18_B3][0], x, L);
+    baxpy_img(A, c_t18[T18_B3][1], SX, x, L);
+    bt_axpy(A, c_t18[T18_B3][2], T0);
+    bt_axpy(A, c_t18[T18_B3][3], T1);
+    bt_axpy(A, c_t18[T18_B3][4], T2);
     bzero(acc);                                        // T18 = B2 + L A9
-    badd_diag(acc, c_t18[T18_B2][0], rt, L);
-    baxpy_img(acc, c_t18[T18_B2][1], SX, rt, L);
-    baxpy(acc, c_t18[T18_B2][2], T0);
-    baxpy(acc, c_t18[T18_B2][3], T1);
-    baxpy(acc, c_t18[T18_B2][4], T2);
-    grp_sync(g, C);                                    // A9 image complete
-    bmma(acc, A, SX4, L);
+    badd_diag(acc, c_t18[T18_B2][0], x, L);
+    baxpy_img(acc, c_t18[T18_B2][1], SX, x, L);
+    bt_axpy(acc, c_t18[T18_B2][2], T0);
+    bt_axpy(acc, c_t18[T18_B2][3], T1);
+    bt_axpy(acc, c_t18[T18_B2][4], T2);
+    grp_sync(x);                                       // A9 image complete
+    bmma<C, R, KS>(acc, A, SX4, x, L);
     bcopy(A, acc);
     prods = 5;
   }
   for (int q = 0; q < s; ++q) {                        // squarings
-    grp_sync(g, C);
-    bstore_img(SX4, A, rt, L);
-    grp_sync(g, C);
-    bzero(acc); bmma(acc, A, SX4, L);
+    grp_sync(x);
+    bstore_img(SX4, A, x, L);
+    grp_sync(x);
+    bzero(acc); bmma<C, R, KS>(acc, A, SX4, x, L);
     bcopy(A, acc);
     ++prods;
   }
   return prods;
 }
 
-// per-group shared memory of the forward kernel: SX, SX4, SP images + norm buffer
-__host__ __device__ constexpr int fwd_grp_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
+// per-group shared memory: three images + the norm buffer (P*P doubles)
+__host__ __device__ constexpr int grp3_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
 
-template <int C>
-__device__ void blk_fwd_group(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
-                              const GrpCtx& x, double* sm, int* bad, unsigned long long& nprod, const Lane& L) {
+// ------------------------------------------------------------------ forward fold (a1-a5)
+template <int C, int R, int KS>
+__device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
+                             const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long& nflop,
+                             const Lane& L) {
   double* SX = sm;
   double* SX4 = sm + 2 * 64 * C * C;
   double* SP = sm + 4 * 64 * C * C;
   double* red = sm + 6 * 64 * C * C;
   const int nchunk = G.count / O.chunk;
   const int b = item / nchunk, c = item % nchunk;
-  BS<C> A, acc;
+  const bool leader = (x.rt0 == 0 && L.lane == 0);
+  BR<C, R> A, acc;
   for (int kk = 0; kk < O.chunk; ++kk) {
     const int k = c * O.chunk + kk;
-    bbuild_omega(A, B, G, b, k, x.off, x.rt, L);
-    const double nrm = bnorm1(A, red, x.g, x.rt, L);
+    bbuild_omega(A, B, G, b, k, x, L);
+    const double nrm = bnorm1(A, red, x, L);
     int m, s;
     choose_scheme(nrm, m, s);
     if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
     bscale(A, ldexp(1.0, -s));
-    bstore_img(SX, A, x.rt, L);
-    grp_sync(x.g, C);
-    const int np = bexpm(A, acc, m, s, SX, SX4, x.g, x.rt, L);
-    if (x.rt == 0 && L.lane == 0) nprod += np;
+    bstore_img(SX, A, x, L);
+    grp_sync(x);
+    const int np = bexpm<C, R, KS>(A, acc, m, s, SX, SX4, tm, x, L);
+    if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const size_t slot = (size_t)b * G.count + k;
-    if (O.U_img) bstore_img(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x.rt, L);
+    if (O.U_img) bstore_img_l2(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
     if (O.chunk_nat) {
       if (kk == 0) {
         if (O.P_img) {                                // P_0 = I
-          bset_identity(acc, x.rt, L);
-          bstore_img(O.P_img + slot * 2 * D.packed + 2 * x.off, acc, x.rt, L);
+          bset_identity(acc, x, L);
+          bstore_img_l2(O.P_img + slot * 2 * D.packed + 2 * x.off, acc, x, L, l2_evict_first());
         }
-        bstore_img(SP, A, x.rt, L);
+        bstore_img(SP, A, x, L);
       } else {
-        bzero(acc); bmma(acc, A, SP, L);              // P <- U_k P
+        bzero(acc); bmma<C, R, KS>(acc, A, SP, x, L);           // P <- U_k P
         bcopy(A, acc);
-        if (x.rt == 0 && L.lane == 0) ++nprod;
-        grp_sync(x.g, C);
-        bstore_img(SP, A, x.rt, L);
+        if (leader) nflop += D.gflops[x.g];
+        grp_sync(x);
+        bstore_img(SP, A, x, L);
       }
-      if (O.P_img && kk + 1 < O.chunk) bstore_img(O.P_img + (slot + 1) * 2 * D.packed + 2 * x.off, A, x.rt, L);
+      if (O.P_img && kk + 1 < O.chunk)
+        bstore_img_l2(O.P_img + (slot + 1) * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
     }
-    grp_sync(x.g, C);   // SX / SX4 / red free for the next slice
+    grp_sync(x);   // SX / SX4 / red free for the next slice
   }
-  if (O.chunk_nat) bstore_nat(O.chunk_nat + ((size_t)b * nchunk + c) * D.packed + x.off, A, x.rt, L);
+  if (O.chunk_nat) bstore_nat(O.chunk_nat + ((size_t)b * nchunk + c) * D.packed + x.off, A, x, L);
 }
 
-__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4, 1) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
-                                                                           BlkFwdOut O, unsigned long long* ctr) {
+__global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
+                                                                          BlkFwdOut O, int tmem_cols,
+                                                                          unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ int bad_sh;
+  __shared__ uint32_t tmem_base_sh;
   const Lane L = lane_id();
-  const GrpCtx x = grp_of(D, L.w);
-  double* sm = smem + D.soff[x.g];
+  if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   if (threadIdx.x == 0) bad_sh = 0;
+  tmem_fence_before();
   __syncthreads();
-  unsigned long long nprod = 0;
+  tmem_fence_after();
+  const uint32_t tm = warp_tmem(tmem_base_sh, L);
+  unsigned long long nflop = 0;
   const int item = blockIdx.x;
-  switch (x.C) {
-    case 1: blk_fwd_group<1>(D, B, G, O, item, x, sm, &bad_sh, nprod, L); break;
-    case 2: blk_fwd_group<2>(D, B, G, O, item, x, sm, &bad_sh, nprod, L); break;
-    default: blk_fwd_group<3>(D, B, G, O, item, x, sm, &bad_sh, nprod, L); break;
+  for (int t = 0; t < D.ntask[L.w]; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    const Ctx x = ctx_of(D, T);
+    double* sm = smem + D.soff[x.g];
+    BLK_DISPATCH(D.C[x.g], x.ks, blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh, nflop, L);
   }
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+  if (L.w == 0) blk_tmem_dealloc(tmem_base_sh, tmem_cols);
   const int nchunk = G.count / O.chunk;
   if (O.status && threadIdx.x == 0 && bad_sh) O.status[item / nchunk] = QAL_ERR_NONFINITE;
-  // algorithmic flops of the products this group executed (profiling window)
-  if (ctr && L.lane == 0 && x.rt == 0 && nprod) atomicAdd(ctr, nprod * D.gflops[x.g]);
+  if (ctr && nflop) atomicAdd(ctr, nflop);
 }
 
 // ------------------------------------------------------------------ pair products (tree level)
 // out[b][i] = in[b][2i+1] in[b][2i] per group (later factor on the LEFT, Eq. 15); an odd last
 // element is carried.  One CTA per output; packed natural in / out.
-template <int C>
-__device__ void blk_pair_group(const BlkDev& D, const double2* lhs, const double2* rhs, double2* out,
-                               const GrpCtx& x, double* sm, const Lane& L) {
-  BS<C> A, acc;
-  bload_nat(A, rhs + x.off, x.rt, L);        // earlier factor as the B image
-  bstore_img(sm, A, x.rt, L);
-  bload_nat(A, lhs + x.off, x.rt, L);
-  grp_sync(x.g, C);
+template <int C, int R, int KS>
+__device__ void blk_pair_task(const double2* lhs, const double2* rhs, double2* out, const Ctx& x, double* sm,
+                              const Lane& L) {
+  BR<C, R> A, acc;
+  bload_nat(A, rhs + x.off, x, L);           // earlier factor as the B image
+  bstore_img(sm, A, x, L);
+  bload_nat(A, lhs + x.off, x, L);
+  grp_sync(x);
   bzero(acc);
-  bmma(acc, A, sm, L);
-  bstore_nat(out + x.off, acc, x.rt, L);
+  bmma<C, R, KS>(acc, A, sm, x, L);
+  bstore_nat(out + x.off, acc, x, L);
 }
 
-__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4) k_blk_tree_level(BlkDev D, int cnt, const double2* __restrict__ in,
-                                                                         double2* __restrict__ out,
-                                                                         unsigned long long* ctr) {
+__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_tree_level(BlkDev D, int cnt,
+                                                                        const double2* __restrict__ in,
+                                                                        double2* __restrict__ out,
+                                                                        unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   const Lane L = lane_id();
   const int half = (cnt + 1) / 2;
@@ -500,31 +761,43 @@ __global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4) k_blk_tree_level(BlkDev 
     for (int e = threadIdx.x; e < D.packed; e += blockDim.x) dst[e] = src[(size_t)(cnt - 1) * D.packed + e];
     return;
   }
-  const GrpCtx x = grp_of(D, L.w);
-  double* sm = smem + D.soff[x.g];
   const double2* lhs = src + (size_t)(2 * i + 1) * D.packed;
   const double2* rhs = src + (size_t)(2 * i) * D.packed;
-  switch (x.C) {
-    case 1: blk_pair_group<1>(D, lhs, rhs, dst, x, sm, L); break;
-    case 2: blk_pair_group<2>(D, lhs, rhs, dst, x, sm, L); break;
-    default: blk_pair_group<3>(D, lhs, rhs, dst, x, sm, L); break;
+  unsigned long long nflop = 0;
+  for (int t = 0; t < D.ntask[L.w]; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    const Ctx x = ctx_of(D, T);
+    double* sm = smem + D.soff[x.g];
+    BLK_DISPATCH(D.C[x.g], x.ks, blk_pair_task, lhs, rhs, dst, x, sm, L);
+    if (x.rt0 == 0 && L.lane == 0) nflop += D.gflops[x.g];
   }
-  if (ctr && L.lane == 0 && x.rt == 0) atomicAdd(ctr, D.gflops[x.g]);
+  if (ctr && nflop) atomicAdd(ctr, nflop);
 }
 
 // ------------------------------------------------------------------ pack / unpack / check
+__device__ __forceinline__ int group_of_row(const BlkDev& D, int r) {
+  int g = 0;
+  for (int q = 1; q < D.ngroups; ++q)
+    if (r >= D.row0[q]) g = q;
+  return g;
+}
+__device__ __forceinline__ int group_of_off(const BlkDev& D, int idx) {
+  int g = 0;
+  for (int q = 1; q < D.ngroups; ++q)
+    if (idx >= D.off[q]) g = q;
+  return g;
+}
+
 // packed[e][g block (r, c)] = nat[e][perm r][perm c] (0 on padding).
 __global__ void k_blk_pack(BlkDev D, int count, const double2* __restrict__ nat, double2* __restrict__ packed) {
   const int e = blockIdx.y;
   const double2* src = nat + (size_t)e * 4096;
   double2* dst = packed + (size_t)e * D.packed;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < D.packed; idx += gridDim.x * blockDim.x) {
-    int g = 0;
-    for (int q = 1; q < D.ngroups; ++q)
-      if (idx >= D.off[q]) g = q;
+    const int g = group_of_off(D, idx);
     const int P = 8 * D.C[g], loc = idx - D.off[g];
     const int r = loc / P, c = loc % P;
-    const int R = D.perm[8 * D.wrp0[g] + r], Cc = D.perm[8 * D.wrp0[g] + c];
+    const int R = D.perm[D.row0[g] + r], Cc = D.perm[D.row0[g] + c];
     dst[idx] = (R >= 0 && Cc >= 0) ? src[R * 64 + Cc] : make_double2(0.0, 0.0);
   }
 }
@@ -563,11 +836,9 @@ __global__ void k_blk_unpack(BlkDev D, int count, const double2* __restrict__ pa
         cj = true;
       }
       if (r >= 0 && c >= 0) {
-        int g = 0;
-        for (int q = 1; q < D.ngroups; ++q)
-          if (r >= 8 * D.wrp0[q]) g = q;
+        const int g = group_of_row(D, r);
         const int P = 8 * D.C[g];
-        v = src[D.off[g] + (r - 8 * D.wrp0[g]) * P + (c - 8 * D.wrp0[g])];
+        v = src[D.off[g] + (r - D.row0[g]) * P + (c - D.row0[g])];
         if (cj) v.y = -v.y;
       }
     }
@@ -588,17 +859,17 @@ __global__ void __launch_bounds__(256) k_blk_fidelity(BlkDev D, const double2* _
   const double2* M = Lam + (size_t)blockIdx.x * D.packed;
   double acc = 0.0;
   for (int g = 0; g < D.ngroups; ++g) {
-    const int P = 8 * D.C[g], row0 = 8 * D.wrp0[g];
+    const int P = 8 * D.C[g], row0 = D.row0[g];
     for (int e = threadIdx.x; e < P * P; e += blockDim.x) {
       const int r = e / P, c = e % P;
       const int a = D.perm[row0 + r], cc = D.perm[row0 + c];
       if (a < 0 || cc < 0) continue;
       const double w = D.weight[row0 + r];
       const int i = a & 7, j = a >> 3, k = cc & 7, l = cc >> 3;
-      const double2 vjl = Vs[j * 8 + l], vik = Vs[i * 8 + k], x = M[D.off[g] + e];
+      const double2 vjl = Vs[j * 8 + l], vik = Vs[i * 8 + k], y = M[D.off[g] + e];
       const double wr = vjl.x * vik.x + vjl.y * vik.y;
       const double wi = vjl.y * vik.x - vjl.x * vik.y;
-      acc += w * (wr * x.x - wi * x.y);
+      acc += w * (wr * y.x - wi * y.y);
     }
   }
   const double s = block_sum(acc, red, L);
@@ -613,127 +884,6 @@ __global__ void __launch_bounds__(256) k_blk_fidelity(BlkDev D, const double2* _
 // and dF/du = Re Tr(W_k dOmega_k/du)/d^2 sums the blocks with the component weights (a mirrored
 // block gives the same real part as its stored partner).
 
-// TMEM strips: 4C 32-bit columns per plane; warp w uses lane quarter w % 4 and the column range
-// (w / 4) * 128 + slot * 32 (slot < 4).
-template <int N>
-__device__ __forceinline__ void tm_st(uint32_t addr, const uint32_t* v);
-template <>
-__device__ __forceinline__ void tm_st<4>(uint32_t addr, const uint32_t* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v[0]), "r"(v[1]),
-               "r"(v[2]), "r"(v[3])
-               : "memory");
-}
-template <>
-__device__ __forceinline__ void tm_st<8>(uint32_t addr, const uint32_t* v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(v[0]),
-               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
-}
-template <int N>
-__device__ __forceinline__ void tm_ld(uint32_t addr, uint32_t* v);
-template <>
-__device__ __forceinline__ void tm_ld<4>(uint32_t addr, uint32_t* v) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
-               : "r"(addr)
-               : "memory");
-}
-template <>
-__device__ __forceinline__ void tm_ld<8>(uint32_t addr, uint32_t* v) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-               : "r"(addr)
-               : "memory");
-}
-// one plane of 2C doubles = 4C words: C = 1 -> x4, C = 2 -> x8, C = 3 -> x8 + x4
-template <int C>
-__device__ __forceinline__ void tm_st_plane(uint32_t addr, const double* x) {
-  uint32_t v[4 * C];
-#pragma unroll
-  for (int i = 0; i < 2 * C; ++i) {
-    v[2 * i] = static_cast<uint32_t>(__double2loint(x[i]));
-    v[2 * i + 1] = static_cast<uint32_t>(__double2hiint(x[i]));
-  }
-  if (C == 1) tm_st<4>(addr, v);
-  if (C >= 2) tm_st<8>(addr, v);
-  if (C == 3) tm_st<4>(addr + 8, v + 8);
-}
-template <int C>
-__device__ __forceinline__ void tm_ld_plane(uint32_t addr, uint32_t* v) {
-  if (C == 1) tm_ld<4>(addr, v);
-  if (C >= 2) tm_ld<8>(addr, v);
-  if (C == 3) tm_ld<4>(addr + 8, v + 8);
-}
-template <int C>
-__device__ __forceinline__ void bt_store(uint32_t addr, const BS<C>& s) {
-  tm_st_plane<C>(addr, s.re);
-  tm_st_plane<C>(addr + 4 * C, s.im);
-  tmem_wait_st();
-}
-template <int C>
-__device__ __forceinline__ void bt_load(BS<C>& s, uint32_t addr) {
-  uint32_t v[4 * C], w[4 * C];
-  tm_ld_plane<C>(addr, v);
-  tm_ld_plane<C>(addr + 4 * C, w);
-  tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 2 * C; ++i) {
-    s.re[i] = __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i]));
-    s.im[i] = __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i]));
-  }
-}
-template <int C>
-__device__ __forceinline__ void bt_axpy(BS<C>& acc, double a, uint32_t addr) {
-  if (a == 0.0) return;
-  uint32_t v[4 * C], w[4 * C];
-  tm_ld_plane<C>(addr, v);
-  tm_ld_plane<C>(addr + 4 * C, w);
-  tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 2 * C; ++i) {
-    acc.re[i] = fma(a, __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i])), acc.re[i]);
-    acc.im[i] = fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[i]);
-  }
-}
-// global image strip with an L2 policy
-template <int C>
-__device__ __forceinline__ void bload_img_l2(BS<C>& s, const double* __restrict__ img, int rt, const Lane& L,
-                                             uint64_t pol) {
-  constexpr int PL = 64 * C * C;
-#pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int o = bpair_off<C>(rt, L, j);
-    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(s.re[2 * j]), "=d"(s.re[2 * j + 1])
-                 : "l"(img + o), "l"(pol));
-    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(s.im[2 * j]), "=d"(s.im[2 * j + 1])
-                 : "l"(img + PL + o), "l"(pol));
-  }
-}
-template <int C>
-__device__ __forceinline__ void bstore_img_l2(double* __restrict__ img, const BS<C>& s, int rt, const Lane& L,
-                                              uint64_t pol) {
-  constexpr int PL = 64 * C * C;
-#pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int o = bpair_off<C>(rt, L, j);
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + o), "d"(s.re[2 * j]),
-                 "d"(s.re[2 * j + 1]), "l"(pol)
-                 : "memory");
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + PL + o), "d"(s.im[2 * j]),
-                 "d"(s.im[2 * j + 1]), "l"(pol)
-                 : "memory");
-  }
-}
-template <int C>
-__device__ __forceinline__ void baxpy_img_l2(BS<C>& acc, double a, const double* __restrict__ img, int rt,
-                                             const Lane& L, uint64_t pol) {
-  if (a == 0.0) return;
-  BS<C> x;
-  bload_img_l2(x, img, rt, L, pol);
-  baxpy(acc, a, x);
-}
 // one thread: bulk-copy a group image (16 P^2 bytes) global -> shared, arriving on `bar`
 __device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int C, uint64_t* bar) {
   const uint32_t bytes = 16u * 64u * C * C;
@@ -744,37 +894,35 @@ __device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int 
 // --------------------------------------------------------------- suffix chain
 // X_N = S_V^dag on the stored blocks, X_k = X_{k+1} U_k; X_img[b][k-1] = X_k (k = 1..N).
 // One CTA per pulse; the groups run independently; U_k streamed by per-group TMA (double buffer).
-template <int C>
-__device__ void blk_suffix_group(const BlkDev& D, int N, const double* U, const double2* V, double* X,
-                                 const GrpCtx& x, double* sm, uint64_t* bar, unsigned long long& nprod,
-                                 const Lane& L) {
-  constexpr int P = 8 * C;
+template <int C, int R, int KS>
+__device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, double* X, const Ctx& x,
+                                double* sm, uint64_t* bar, unsigned long long& nflop, const Lane& L) {
   double* SU[2] = {sm, sm + 2 * 64 * C * C};
   const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
   const int go = 2 * x.off;
-  const bool leader = (x.rt == 0 && L.lane == 0);
-  const int row0 = 8 * D.wrp0[x.g];
-  BS<C> A, acc;
+  const bool leader = (x.rt0 == 0 && L.lane == 0);
+  BR<C, R> A, acc;
 #pragma unroll
-  for (int i = 0; i < 2 * C; ++i) {
-    const int a = D.perm[row0 + 8 * x.rt + L.g], c = D.perm[row0 + 4 * i + L.t];
-    double re = 0.0, im = 0.0;
-    if (a >= 0 && c >= 0) {
-      const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
-      const double2 vjl = __ldg(V + j * 8 + l), vik = __ldg(V + ii * 8 + kk);
-      re = vjl.x * vik.x + vjl.y * vik.y;
-      im = vjl.y * vik.x - vjl.x * vik.y;
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      const int a = D.perm[x.row0 + 8 * (x.rt0 + r) + L.g], c = D.perm[x.row0 + 4 * i + L.t];
+      double re = 0.0, im = 0.0;
+      if (a >= 0 && c >= 0) {
+        const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
+        const double2 vjl = __ldg(V + j * 8 + l), vik = __ldg(V + ii * 8 + kk);
+        re = vjl.x * vik.x + vjl.y * vik.y;   // S_V^dag[a][c] = V[j][l] conj(V[i][k])
+        im = vjl.y * vik.x - vjl.x * vik.y;
+      }
+      A.re[r][i] = re;
+      A.im[r][i] = im;
     }
-    A.re[i] = re;
-    A.im[i] = im;
-  }
-  (void)P;
-  bstore_img(X + (size_t)(N - 1) * stride + go, A, x.rt, L);
+  bstore_img_l2(X + (size_t)(N - 1) * stride + go, A, x, L, l2_evict_first());
   if (leader && N > 1) tma_grp_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * stride + go, C, &bar[(N - 1) & 1]);
   uint32_t ph[2] = {0, 0};
   for (int k = N - 1; k >= 1; --k) {
     const int cur = k & 1;
-    grp_sync(x.g, C);   // buffer cur^1 (read at step k+1) is free
+    grp_sync(x);   // buffer cur^1 (read at step k+1) is free
     if (leader && k - 1 >= 1) {
       fence_proxy_async();
       tma_grp_img(SU[cur ^ 1], U + (size_t)(k - 1) * stride + go, C, &bar[cur ^ 1]);
@@ -782,37 +930,39 @@ __device__ void blk_suffix_group(const BlkDev& D, int N, const double* U, const 
     mbar_wait(&bar[cur], ph[cur]);
     ph[cur] ^= 1;
     bzero(acc);
-    bmma(acc, A, SU[cur], L);   // X_{k+1} U_k
+    bmma<C, R, KS>(acc, A, SU[cur], x, L);   // X_{k+1} U_k
     bcopy(A, acc);
-    bstore_img_l2(X + (size_t)(k - 1) * stride + go, A, x.rt, L, l2_evict_first());
+    bstore_img_l2(X + (size_t)(k - 1) * stride + go, A, x, L, l2_evict_first());
   }
-  if (leader) nprod += (unsigned long long)(N - 1);
+  if (leader) nflop += (unsigned long long)(N - 1) * D.gflops[x.g];
 }
 
-__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4) k_blk_suffix_chain(BlkDev D, int N,
-                                                                           const double* __restrict__ U_img,
-                                                                           const double2* __restrict__ V,
-                                                                           double* __restrict__ X_img,
-                                                                           unsigned long long* ctr) {
+__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev D, int N,
+                                                                          const double* __restrict__ U_img,
+                                                                          const double2* __restrict__ V,
+                                                                          double* __restrict__ X_img,
+                                                                          unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];
   const Lane L = lane_id();
-  const GrpCtx x = grp_of(D, L.w);
-  if (x.rt == 0 && L.lane == 0) {
-    mbar_init(&bars[x.g][0], 1);
-    mbar_init(&bars[x.g][1], 1);
-    fence_mbar_init();
+  for (int t = 0; t < D.ntask[L.w]; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    if (T.rt0 == 0 && L.lane == 0) {
+      mbar_init(&bars[T.g][0], 1);
+      mbar_init(&bars[T.g][1], 1);
+    }
   }
+  fence_mbar_init();
   __syncthreads();
   const size_t base = (size_t)blockIdx.x * N * 2 * D.packed;
-  unsigned long long nprod = 0;
-  double* sm = smem + D.soff[x.g];
-  switch (x.C) {
-    case 1: blk_suffix_group<1>(D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nprod, L); break;
-    case 2: blk_suffix_group<2>(D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nprod, L); break;
-    default: blk_suffix_group<3>(D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nprod, L); break;
+  unsigned long long nflop = 0;
+  for (int t = 0; t < D.ntask[L.w]; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    const Ctx x = ctx_of(D, T);
+    double* sm = smem + D.soff[x.g];
+    BLK_DISPATCH(D.C[x.g], x.ks, blk_suffix_task, D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nflop, L);
   }
-  if (ctr && nprod) atomicAdd(ctr, nprod * D.gflops[x.g]);
+  if (ctr && nflop) atomicAdd(ctr, nflop);
 }
 
 // --------------------------------------------------------------- gradient slices
@@ -820,14 +970,13 @@ constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
 constexpr int BLK_GRAD_SCR = 6;   // L2 scratch images per group: X, dX, A6, dA6, E, dE
 
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
-// returns the product count and leaves W = L_exp(Omega, G) in A.  SD, SV, SN: group images
+// leaves W = L_exp(Omega, G) in A and returns the product count.  SD, SV, SN: group images
 // (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots; scr: the group's L2 scratch.
-template <int C>
-__device__ __forceinline__ int blk_dual_expm(BS<C>& A, BS<C>& acc, const BlkBasis& B, const SliceGrid& G,
-                                             const double* Pk, int b, int k, const GrpCtx& x, double* SD,
-                                             double* SV, double* SN, uint64_t* barN, uint32_t& phN, double* red,
-                                             uint32_t tm, double* scr, int* bad, const Lane& L) {
-  const int g = x.g, rt = x.rt;
+template <int C, int R, int KS>
+__device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const BlkBasis& B, const SliceGrid& G,
+                                             const double* Pk, int b, int k, const Ctx& x, double* SD, double* SV,
+                                             double* SN, uint64_t* barN, uint32_t& phN, double* red, uint32_t tm,
+                                             double* scr, int* bad, const Lane& L) {
   const size_t IM = 2 * 64 * C * C;
   double* gX = scr;
   double* gdX = scr + IM;
@@ -837,271 +986,269 @@ __device__ __forceinline__ int blk_dual_expm(BS<C>& A, BS<C>& acc, const BlkBasi
   double* gdE = scr + 5 * IM;
   const uint32_t T0 = tm, T1 = tm + 32, T2 = tm + 64, T3 = tm + 96;   // A2, dA2, A3|Y, dA3|dY
   const uint64_t keep = l2_evict_last();
-  bbuild_omega(A, B, G, b, k, x.off, rt, L);
-  const double nrm = bnorm1(A, red, g, rt, L);
+  bbuild_omega(A, B, G, b, k, x, L);
+  const double nrm = bnorm1(A, red, x, L);
   int m, s;
   choose_scheme(nrm, m, s);
   if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
   const double sc = ldexp(1.0, -s);
   bscale(A, sc);
-  bstore_img(SV, A, rt, L);
-  bstore_img_l2(gX, A, rt, L, keep);
+  bstore_img(SV, A, x, L);
+  bstore_img_l2(gX, A, x, L, keep);
   // G = P_k X_{k+1};  dX = G / 2^s
-  bload_img_l2(A, Pk, rt, L, l2_evict_first());
+  bload_img_l2(A, Pk, x, L, l2_evict_first());
   mbar_wait(barN, phN);
   phN ^= 1;
   bzero(acc);
-  bmma(acc, A, SN, L);
+  bmma<C, R, KS>(acc, A, SN, x, L);
   bscale(acc, sc);
-  grp_sync(g, C);                                      // SV (X) complete
-  bstore_img(SD, acc, rt, L);
-  bstore_img_l2(gdX, acc, rt, L, keep);
-  grp_sync(g, C);                                      // SD = dX complete
-  bload_img(A, SV, rt, L);
-  bzero(acc); bmma(acc, A, SV, L);                     // A2 = X X
+  grp_sync(x);                                         // SV (X) complete
+  bstore_img(SD, acc, x, L);
+  bstore_img_l2(gdX, acc, x, L, keep);
+  grp_sync(x);                                         // SD = dX complete
+  bload_img(A, SV, x, L);
+  bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                  // A2 = X X
   bt_store(T0, acc);
-  bzero(acc); bmma(acc, A, SD, L);                     // X dX
-  bload_img(A, SD, rt, L);
-  bmma(acc, A, SV, L);                                 // + dX X
+  bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                  // X dX
+  bload_img(A, SD, x, L);
+  bmma<C, R, KS>(acc, A, SV, x, L);                              // + dX X
   bt_store(T1, acc);
   int np = 1 + 1 + 2;
   if (m == 8) {
-    grp_sync(g, C);
-    bzero(acc); baxpy_img_l2(acc, c_t8[0], gX, rt, L, keep); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, rt, L);
-    bzero(acc); baxpy_img_l2(acc, c_t8[0], gdX, rt, L, keep); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, rt, L);
-    grp_sync(g, C);
+    grp_sync(x);
+    bzero(acc); baxpy_img_l2(acc, c_t8[0], gX, x, L, keep); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, x, L);
+    bzero(acc); baxpy_img_l2(acc, c_t8[0], gdX, x, L, keep); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, x, L);
+    grp_sync(x);
     bt_load(A, T0);
-    bzero(acc); bmma(acc, A, SV, L);                   // Y = A2 W
+    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // Y = A2 W
     bt_store(T2, acc);
-    bzero(acc); bmma(acc, A, SD, L);                   // A2 dW
+    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A2 dW
     bt_load(A, T1);
-    bmma(acc, A, SV, L);                               // + dA2 W = dY
+    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA2 W = dY
     bt_store(T3, acc);
-    grp_sync(g, C);
-    bzero(acc); bt_axpy(acc, 1.0, T2); bt_axpy(acc, c_t8[4], T0); bstore_img(SV, acc, rt, L);
-    bzero(acc); bt_axpy(acc, 1.0, T3); bt_axpy(acc, c_t8[4], T1); bstore_img(SD, acc, rt, L);
-    grp_sync(g, C);
+    grp_sync(x);
+    bzero(acc); bt_axpy(acc, 1.0, T2); bt_axpy(acc, c_t8[4], T0); bstore_img(SV, acc, x, L);
+    bzero(acc); bt_axpy(acc, 1.0, T3); bt_axpy(acc, c_t8[4], T1); bstore_img(SD, acc, x, L);
+    grp_sync(x);
     bzero(acc);
-    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img_l2(acc, 1.0, gdX, rt, L, keep);
-    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img_l2(A, c_t8[3], gdX, rt, L, keep);   // dL
-    bmma(acc, A, SV, L);
-    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img_l2(A, c_t8[3], gX, rt, L, keep);    // L
-    bmma(acc, A, SD, L);
-    if (s > 0) bstore_img_l2(gdE, acc, rt, L, keep);
+    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img_l2(acc, 1.0, gdX, x, L, keep);
+    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img_l2(A, c_t8[3], gdX, x, L, keep);   // dL
+    bmma<C, R, KS>(acc, A, SV, x, L);
+    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img_l2(A, c_t8[3], gX, x, L, keep);    // L
+    bmma<C, R, KS>(acc, A, SD, x, L);
+    if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
     np += 1 + 2 + 2;
     if (s > 0) {
       bzero(acc);
-      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img_l2(acc, 1.0, gX, rt, L, keep);
-      badd_diag(acc, 1.0, rt, L);
-      bmma(acc, A, SV, L);
-      bstore_img_l2(gE, acc, rt, L, keep);
+      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img_l2(acc, 1.0, gX, x, L, keep);
+      badd_diag(acc, 1.0, x, L);
+      bmma<C, R, KS>(acc, A, SV, x, L);
+      bstore_img_l2(gE, acc, x, L, keep);
       ++np;
     }
   } else {
     bt_load(A, T0);
-    bzero(acc); bmma(acc, A, SV, L);                   // A3
+    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // A3
     bt_store(T2, acc);
-    bzero(acc); bmma(acc, A, SD, L);                   // A2 dX
+    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A2 dX
     bt_load(A, T1);
-    bmma(acc, A, SV, L);                               // + dA2 X = dA3
+    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA2 X = dA3
     bt_store(T3, acc);
-    grp_sync(g, C);
-    bt_load(A, T2); bstore_img(SV, A, rt, L);
-    bt_load(A, T3); bstore_img(SD, A, rt, L);
-    grp_sync(g, C);
+    grp_sync(x);
+    bt_load(A, T2); bstore_img(SV, A, x, L);
+    bt_load(A, T3); bstore_img(SD, A, x, L);
+    grp_sync(x);
     bt_load(A, T2);
-    bzero(acc); bmma(acc, A, SV, L);                   // A6
-    bstore_img_l2(gA6, acc, rt, L, keep);
-    bzero(acc); bmma(acc, A, SD, L);                   // A3 dA3
+    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // A6
+    bstore_img_l2(gA6, acc, x, L, keep);
+    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A3 dA3
     bt_load(A, T3);
-    bmma(acc, A, SV, L);                               // + dA3 A3
-    bstore_img_l2(gdA6, acc, rt, L, keep);
-    grp_sync(g, C);
+    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA3 A3
+    bstore_img_l2(gdA6, acc, x, L, keep);
+    grp_sync(x);
     bzero(acc);
-    baxpy_img_l2(acc, c_t18[T18_B5][1], gX, rt, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T0);
-    baxpy_img_l2(acc, 1.0, gA6, rt, L, keep);
-    bstore_img(SV, acc, rt, L);
+    baxpy_img_l2(acc, c_t18[T18_B5][1], gX, x, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T0);
+    baxpy_img_l2(acc, 1.0, gA6, x, L, keep);
+    bstore_img(SV, acc, x, L);
     bzero(acc);
-    baxpy_img_l2(acc, c_t18[T18_B5][1], gdX, rt, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T1);
-    baxpy_img_l2(acc, 1.0, gdA6, rt, L, keep);
-    bstore_img(SD, acc, rt, L);
-    grp_sync(g, C);
+    baxpy_img_l2(acc, c_t18[T18_B5][1], gdX, x, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T1);
+    baxpy_img_l2(acc, 1.0, gdA6, x, L, keep);
+    bstore_img(SD, acc, x, L);
+    grp_sync(x);
     bzero(acc);                                        // dA9 = dB4 + dB1 B5 + B1 dB5
-    baxpy_img_l2(acc, c_t18[T18_B4][1], gdX, rt, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T1);
-    bt_axpy(acc, c_t18[T18_B4][3], T3); baxpy_img_l2(acc, c_t18[T18_B4][4], gdA6, rt, L, keep);
+    baxpy_img_l2(acc, c_t18[T18_B4][1], gdX, x, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T1);
+    bt_axpy(acc, c_t18[T18_B4][3], T3); baxpy_img_l2(acc, c_t18[T18_B4][4], gdA6, x, L, keep);
     bzero(A);
-    baxpy_img_l2(A, c_t18[T18_B1][1], gdX, rt, L, keep); bt_axpy(A, c_t18[T18_B1][2], T1);
+    baxpy_img_l2(A, c_t18[T18_B1][1], gdX, x, L, keep); bt_axpy(A, c_t18[T18_B1][2], T1);
     bt_axpy(A, c_t18[T18_B1][3], T3);
-    bmma(acc, A, SV, L);
+    bmma<C, R, KS>(acc, A, SV, x, L);
     bzero(A);
-    baxpy_img_l2(A, c_t18[T18_B1][1], gX, rt, L, keep); bt_axpy(A, c_t18[T18_B1][2], T0);
+    baxpy_img_l2(A, c_t18[T18_B1][1], gX, x, L, keep); bt_axpy(A, c_t18[T18_B1][2], T0);
     bt_axpy(A, c_t18[T18_B1][3], T2);
-    bmma(acc, A, SD, L);
-    bstore_img(SN, acc, rt, L);                        // dA9 (SN idle since G)
+    bmma<C, R, KS>(acc, A, SD, x, L);
+    bstore_img(SN, acc, x, L);                         // dA9 (SN idle since G)
     bzero(acc);                                        // A9 = B4 + B1 B5 (A holds B1)
-    badd_diag(acc, c_t18[T18_B4][0], rt, L);
-    baxpy_img_l2(acc, c_t18[T18_B4][1], gX, rt, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T0);
-    bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img_l2(acc, c_t18[T18_B4][4], gA6, rt, L, keep);
-    bmma(acc, A, SV, L);
-    grp_sync(g, C);                                    // reads of SV (B5), SD (dB5) done
-    bstore_img(SV, acc, rt, L);                        // A9
-    grp_sync(g, C);                                    // A9 (SV), dA9 (SN) complete
+    badd_diag(acc, c_t18[T18_B4][0], x, L);
+    baxpy_img_l2(acc, c_t18[T18_B4][1], gX, x, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T0);
+    bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img_l2(acc, c_t18[T18_B4][4], gA6, x, L, keep);
+    bmma<C, R, KS>(acc, A, SV, x, L);
+    grp_sync(x);                                       // reads of SV (B5), SD (dB5) done
+    bstore_img(SV, acc, x, L);                         // A9
+    grp_sync(x);                                       // A9 (SV), dA9 (SN) complete
     bzero(acc);                                        // dT = dB2 + dL A9 + L dA9
-    baxpy_img_l2(acc, c_t18[T18_B2][1], gdX, rt, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T1);
-    bt_axpy(acc, c_t18[T18_B2][3], T3); baxpy_img_l2(acc, c_t18[T18_B2][4], gdA6, rt, L, keep);
-    bload_img(A, SN, rt, L);                           // dL = dB3 + dA9
-    baxpy_img_l2(A, c_t18[T18_B3][1], gdX, rt, L, keep); bt_axpy(A, c_t18[T18_B3][2], T1);
-    bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img_l2(A, c_t18[T18_B3][4], gdA6, rt, L, keep);
-    bmma(acc, A, SV, L);
-    bload_img(A, SV, rt, L);                           // L = B3 + A9
-    badd_diag(A, c_t18[T18_B3][0], rt, L);
-    baxpy_img_l2(A, c_t18[T18_B3][1], gX, rt, L, keep); bt_axpy(A, c_t18[T18_B3][2], T0);
-    bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img_l2(A, c_t18[T18_B3][4], gA6, rt, L, keep);
-    bmma(acc, A, SN, L);
-    if (s > 0) bstore_img_l2(gdE, acc, rt, L, keep);
+    baxpy_img_l2(acc, c_t18[T18_B2][1], gdX, x, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T1);
+    bt_axpy(acc, c_t18[T18_B2][3], T3); baxpy_img_l2(acc, c_t18[T18_B2][4], gdA6, x, L, keep);
+    bload_img(A, SN, x, L);                            // dL = dB3 + dA9
+    baxpy_img_l2(A, c_t18[T18_B3][1], gdX, x, L, keep); bt_axpy(A, c_t18[T18_B3][2], T1);
+    bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img_l2(A, c_t18[T18_B3][4], gdA6, x, L, keep);
+    bmma<C, R, KS>(acc, A, SV, x, L);
+    bload_img(A, SV, x, L);                            // L = B3 + A9
+    badd_diag(A, c_t18[T18_B3][0], x, L);
+    baxpy_img_l2(A, c_t18[T18_B3][1], gX, x, L, keep); bt_axpy(A, c_t18[T18_B3][2], T0);
+    bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img_l2(A, c_t18[T18_B3][4], gA6, x, L, keep);
+    bmma<C, R, KS>(acc, A, SN, x, L);
+    if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
     np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
     if (s > 0) {                                       // T = B2 + L A9
       bzero(acc);
-      badd_diag(acc, c_t18[T18_B2][0], rt, L);
-      baxpy_img_l2(acc, c_t18[T18_B2][1], gX, rt, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T0);
-      bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img_l2(acc, c_t18[T18_B2][4], gA6, rt, L, keep);
-      bmma(acc, A, SV, L);
-      bstore_img_l2(gE, acc, rt, L, keep);
+      badd_diag(acc, c_t18[T18_B2][0], x, L);
+      baxpy_img_l2(acc, c_t18[T18_B2][1], gX, x, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T0);
+      bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img_l2(acc, c_t18[T18_B2][4], gA6, x, L, keep);
+      bmma<C, R, KS>(acc, A, SV, x, L);
+      bstore_img_l2(gE, acc, x, L, keep);
       ++np;
     }
   }
   for (int q = 0; q < s; ++q) {                        // (E, dE) <- (E E, dE E + E dE)
-    grp_sync(g, C);
-    bload_img_l2(A, gE, rt, L, keep);
-    bstore_img(SV, A, rt, L);
-    bload_img_l2(acc, gdE, rt, L, keep);
-    bstore_img(SD, acc, rt, L);
-    grp_sync(g, C);
-    bzero(acc); bmma(acc, A, SD, L);                   // E dE
-    bload_img_l2(A, gdE, rt, L, keep);
-    bmma(acc, A, SV, L);                               // + dE E
-    bstore_img_l2(gdE, acc, rt, L, keep);
-    bload_img_l2(A, gE, rt, L, keep);
-    bzero(acc); bmma(acc, A, SV, L);                   // E E
-    bstore_img_l2(gE, acc, rt, L, keep);
+    grp_sync(x);
+    bload_img_l2(A, gE, x, L, keep);
+    bstore_img(SV, A, x, L);
+    bload_img_l2(acc, gdE, x, L, keep);
+    bstore_img(SD, acc, x, L);
+    grp_sync(x);
+    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // E dE
+    bload_img_l2(A, gdE, x, L, keep);
+    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dE E
+    bstore_img_l2(gdE, acc, x, L, keep);
+    bload_img_l2(A, gE, x, L, keep);
+    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // E E
+    bstore_img_l2(gE, acc, x, L, keep);
     np += 3;
   }
-  if (s > 0) bload_img_l2(A, gdE, rt, L, keep);
+  if (s > 0) bload_img_l2(A, gdE, x, L, keep);
   else bcopy(A, acc);
   return np;
 }
 
-// weighted traces Re Tr(W_g B_m,g) of the group, per warp partial sums into red_tr[w][m]
-template <int C>
-__device__ __forceinline__ void blk_traces(const BS<C>& W, const BlkDev& D, const BlkBasis& B, int b, const GrpCtx& x,
-                                           double* red_tr, const Lane& L) {
+// weighted traces Re Tr(W_g B_m,g) over the warp's rows, added to the warp's partial sums
+template <int C, int R>
+__device__ __forceinline__ void blk_traces(const BR<C, R>& W, const BlkDev& D, const BlkBasis& B, int b, const Ctx& x,
+                                           double* tr, bool first, const Lane& L) {
   constexpr int P = 8 * C;
   const int K = B.J + B.ncomm;
-  const int r = 8 * x.rt + L.g;
-  const double wr = (double)D.weight[8 * D.wrp0[x.g] + r];
   for (int mm = 0; mm < K; ++mm) {
     const double2* Bm = (mm < B.J) ? B.Lc + (size_t)mm * B.packed
                                    : B.Lcomm + (size_t)b * B.Lcomm_stride + (size_t)(mm - B.J) * B.packed;
     Bm += x.off;
     double v = 0.0;
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) {
-      const double2 y = __ldg(Bm + (4 * i + L.t) * P + r);
-      v = fma(W.re[i], y.x, v);
-      v = fma(-W.im[i], y.y, v);
+    for (int r = 0; r < R; ++r) {
+      const int row = 8 * (x.rt0 + r) + L.g;
+      double vr = 0.0;
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) {
+        const double2 y = __ldg(Bm + (4 * i + L.t) * P + row);
+        vr = fma(W.re[r][i], y.x, vr);
+        vr = fma(-W.im[r][i], y.y, vr);
+      }
+      v = fma((double)D.weight[x.row0 + row], vr, v);
     }
-    v *= wr;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (L.lane == 0) red_tr[L.w * BLK_TR_MAX + mm] = v;
+    if (L.lane == 0) tr[mm] = first ? v : tr[mm] + v;
   }
 }
 
-// per-group shared memory of the gradient kernel: SD, SV, SN images + norm buffer
-__host__ __device__ constexpr int grad_grp_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
+template <int C, int R, int KS>
+__device__ void blk_grad_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const double* Pk, int b, int k,
+                              const Ctx& x, double* sm, uint64_t* barN, uint32_t& phN, uint32_t tm, double* scr,
+                              int* bad, double* tr, bool first, unsigned long long& nflop, const Lane& L) {
+  const int IM = 2 * 64 * C * C;
+  BR<C, R> A, acc;
+  const int np = blk_dual_expm<C, R, KS>(A, acc, B, G, Pk, b, k, x, sm, sm + IM, sm + 2 * IM, barN, phN, sm + 3 * IM, tm,
+                                     scr, bad, L);
+  if (x.rt0 == 0 && L.lane == 0) nflop += (unsigned long long)np * D.gflops[x.g];
+  blk_traces<C, R>(A, D, B, b, x, tr, first, L);
+}
 
-__global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4, 1) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B,
-                                                                             SliceGrid G,
-                                                                             const double* __restrict__ P_img,
-                                                                             const double* __restrict__ X_img,
-                                                                             double* __restrict__ grad,
-                                                                             int* __restrict__ status,
-                                                                             double* __restrict__ scratch,
-                                                                             int tmem_cols, unsigned long long* ctr) {
+__global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B,
+                                                                            SliceGrid G,
+                                                                            const double* __restrict__ P_img,
+                                                                            const double* __restrict__ X_img,
+                                                                            double* __restrict__ grad,
+                                                                            int* __restrict__ status,
+                                                                            double* __restrict__ scratch,
+                                                                            int tmem_cols, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS];
-  __shared__ double red_tr[(QAL_BLK_MAX_ROWS / 8) * BLK_TR_MAX + BLK_TR_MAX];
+  __shared__ double red_tr[BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int bad_sh;
   const Lane L = lane_id();
-  const GrpCtx x = grp_of(D, L.w);
-  if (L.w == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  const bool leader = (x.rt == 0 && L.lane == 0);
-  if (leader) {
-    mbar_init(&bars[x.g], 1);
-    fence_mbar_init();
-  }
+  if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
+  const int ntask = D.ntask[L.w];
+  for (int t = 0; t < ntask; ++t)
+    if (D.task[L.w][t].rt0 == 0 && L.lane == 0) mbar_init(&bars[D.task[L.w][t].g], 1);
+  fence_mbar_init();
   if (threadIdx.x == 0) bad_sh = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tm = tmem_base_sh + (static_cast<uint32_t>(32 * (L.w & 3)) << 16) + static_cast<uint32_t>((L.w >> 2) * 128);
-  double* sm = smem + D.soff[x.g];
-  const int IM = 2 * 64 * x.C * x.C;
-  double* SD = sm;
-  double* SV = sm + IM;
-  double* SN = sm + 2 * IM;
-  double* red = sm + 3 * IM;
-  double* scr = scratch + ((size_t)blockIdx.x * 2 * D.packed + 2 * x.off) * BLK_GRAD_SCR;
+  const uint32_t tm = warp_tmem(tmem_base_sh, L);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
   const int items = batch * N;
   const int K = B.J + B.ncomm;
-  uint32_t phN = 0;
-  unsigned long long nprod = 0;
-  if (leader && blockIdx.x < items)
-    tma_grp_img(SN, X_img + (size_t)blockIdx.x * stride + 2 * x.off, x.C, &bars[x.g]);
+  uint32_t phN[BLK_MAX_TASKS] = {0, 0, 0};
+  unsigned long long nflop = 0;
+  double* scr_cta = scratch + (size_t)blockIdx.x * stride * BLK_GRAD_SCR;
+  for (int t = 0; t < ntask; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    if (T.rt0 == 0 && L.lane == 0 && blockIdx.x < items) {
+      const int C = D.C[T.g];
+      tma_grp_img(smem + D.soff[T.g] + 2 * 2 * 64 * C * C, X_img + (size_t)blockIdx.x * stride + 2 * D.off[T.g], C,
+                  &bars[T.g]);
+    }
+  }
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
-    const double* Pk = P_img + (size_t)item * stride + 2 * x.off;
-    BS<3> A3, acc3;
-    int np;
-    switch (x.C) {
-      case 1: {
-        BS<1> A, acc;
-        np = blk_dual_expm<1>(A, acc, B, G, Pk, b, k, x, SD, SV, SN, &bars[x.g], phN, red, tm, scr, &bad_sh, L);
-        blk_traces<1>(A, D, B, b, x, red_tr, L);
-        break;
-      }
-      case 2: {
-        BS<2> A, acc;
-        np = blk_dual_expm<2>(A, acc, B, G, Pk, b, k, x, SD, SV, SN, &bars[x.g], phN, red, tm, scr, &bad_sh, L);
-        blk_traces<2>(A, D, B, b, x, red_tr, L);
-        break;
-      }
-      default:
-        np = blk_dual_expm<3>(A3, acc3, B, G, Pk, b, k, x, SD, SV, SN, &bars[x.g], phN, red, tm, scr, &bad_sh, L);
-        blk_traces<3>(A3, D, B, b, x, red_tr, L);
-        break;
+    for (int t = 0; t < ntask; ++t) {
+      const BlkTask T = D.task[L.w][t];
+      const Ctx x = ctx_of(D, T);
+      double* sm = smem + D.soff[x.g];
+      double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
+      const double* Pk = P_img + (size_t)item * stride + 2 * x.off;
+      BLK_DISPATCH(D.C[x.g], x.ks, blk_grad_task, D, B, G, Pk, b, k, x, sm, &bars[x.g], phN[t], tm, scr, &bad_sh,
+                   red_tr + L.w * BLK_TR_MAX, t == 0, nflop, L);
     }
-    if (leader) nprod += (unsigned long long)np * D.gflops[x.g];
-    __syncthreads();   // every group done with this item: SN free, red_tr complete
-    if (leader && item + (int)gridDim.x < items) {
-      fence_proxy_async();
-      tma_grp_img(SN, X_img + (size_t)(item + gridDim.x) * stride + 2 * x.off, x.C, &bars[x.g]);
+    __syncthreads();   // every task done with this item: SN regions free, red_tr complete
+    for (int t = 0; t < ntask; ++t) {
+      const BlkTask T = D.task[L.w][t];
+      if (T.rt0 == 0 && L.lane == 0 && item + (int)gridDim.x < items) {
+        const int C = D.C[T.g];
+        fence_proxy_async();
+        tma_grp_img(smem + D.soff[T.g] + 2 * 2 * 64 * C * C,
+                    X_img + (size_t)(item + gridDim.x) * stride + 2 * D.off[T.g], C, &bars[T.g]);
+      }
     }
     if (threadIdx.x < K) {
-      double t = 0.0;
-      for (int w = 0; w < D.nwarps; ++w) t += red_tr[w * BLK_TR_MAX + threadIdx.x];
-      red_tr[(QAL_BLK_MAX_ROWS / 8) * BLK_TR_MAX + threadIdx.x] = t;
+      double s = 0.0;
+      for (int w = 0; w < D.nwarps; ++w) s += red_tr[w * BLK_TR_MAX + threadIdx.x];
+      red_tr[BLK_MAX_WARPS * BLK_TR_MAX + threadIdx.x] = s;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      const double* T = red_tr + (QAL_BLK_MAX_ROWS / 8) * BLK_TR_MAX;
+      const double* T = red_tr + BLK_MAX_WARPS * BLK_TR_MAX;
       const int J = B.J;
       const double inv_d2 = 1.0 / 64.0;
       if (G.mode == 0) {
@@ -1128,48 +1275,53 @@ __global__ void __launch_bounds__(QAL_BLK_MAX_ROWS * 4, 1) k_blk_grad_slices(Blk
           gg[J + j] = g2 * inv_d2;
         }
       }
-      if (bad_sh && status) { status[b] = QAL_ERR_NONFINITE; }
+      if (bad_sh && status) status[b] = QAL_ERR_NONFINITE;
       bad_sh = 0;
     }
   }
-  if (ctr && leader && nprod) atomicAdd(ctr, nprod);
+  if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  if (L.w == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "r"(tmem_cols));
+  if (L.w == 0) blk_tmem_dealloc(tmem_base_sh, tmem_cols);
 }
 
 // ------------------------------------------------------------------ launchers
 namespace {
-int grp_smem_doubles(const BlkDev& D, int (*per)(int), int* soff) {
+int grp_smem_doubles(BlkDev& D, int (*per)(int)) {
   int o = 0;
   for (int g = 0; g < D.ngroups; ++g) {
-    soff[g] = o;
+    D.soff[g] = o;
     o += per(D.C[g]);
     o = (o + 15) & ~15;   // 128-byte alignment of every region
   }
   return o;
 }
-int fwd_per(int C) { return fwd_grp_doubles(C); }
-int chain_per(int C) { return 2 * 2 * 64 * C * C; }
-int grad_per(int C) { return grad_grp_doubles(C); }
-int pair_per(int C) { return 2 * 64 * C * C; }
+int per3(int C) { return grp3_doubles(C); }
+int per_pair(int C) { return 2 * 64 * C * C; }
+int per_chain(int C) { return 2 * 2 * 64 * C * C; }
+int tmem_cols_for(const BlkDev& D) { return D.nwarps > 4 ? 256 : 128; }
+cudaError_t set_smem(const void* fn, size_t bytes, size_t& attr) {
+  if (bytes > attr) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    attr = bytes;
+  }
+  return cudaSuccess;
+}
 }  // namespace
 
 cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                  const BlkFwdOut& O, cudaStream_t st) {
-  BlkDev D = to_dev(p);
-  const size_t bytes = (size_t)grp_smem_doubles(D, fwd_per, D.soff) * 8;
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
   static size_t attr = 0;
-  if (bytes > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_blk_expm_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    attr = bytes;
-  }
+  cudaError_t e = set_smem((const void*)k_blk_expm_fold, bytes, attr);
+  if (e != cudaSuccess) return e;
   const int items = batch * (G.count / O.chunk);
   prof_pre(ST_BLK_EXPM, st);
-  k_blk_expm_fold<<<items, 32 * D.nwarps, bytes, st>>>(D, B, G, O, prof_counter(ST_BLK_EXPM));
+  k_blk_expm_fold<<<items, 32 * D.nwarps, bytes, st>>>(D, B, G, O, tmem_cols_for(D), prof_counter(ST_BLK_EXPM));
   prof_post(ST_BLK_EXPM, st);
   ++launch_counter();
   return cudaGetLastError();
@@ -1177,8 +1329,9 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
 
 cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, const double2* in, double2* out,
                                   cudaStream_t st) {
-  BlkDev D = to_dev(p);
-  const size_t bytes = (size_t)grp_smem_doubles(D, pair_per, D.soff) * 8;
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per_pair) * 8;
   const int half = (cnt + 1) / 2;
   prof_pre(ST_BLK_TREE, st);
   k_blk_tree_level<<<batch * half, 32 * D.nwarps, bytes, st>>>(D, cnt, in, out, prof_counter(ST_BLK_TREE));
@@ -1189,14 +1342,12 @@ cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, c
 
 cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
                                     const double2* V, double* X_img, cudaStream_t st) {
-  BlkDev D = to_dev(p);
-  const size_t bytes = (size_t)grp_smem_doubles(D, chain_per, D.soff) * 8;
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per_chain) * 8;
   static size_t attr = 0;
-  if (bytes > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_blk_suffix_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    attr = bytes;
-  }
+  cudaError_t e = set_smem((const void*)k_blk_suffix_chain, bytes, attr);
+  if (e != cudaSuccess) return e;
   prof_pre(ST_BLK_SUFFIX, st);
   k_blk_suffix_chain<<<batch, 32 * D.nwarps, bytes, st>>>(D, N, U_img, V, X_img, prof_counter(ST_BLK_SUFFIX));
   prof_post(ST_BLK_SUFFIX, st);
@@ -1204,32 +1355,30 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
   return cudaGetLastError();
 }
 
-// persistent: two CTAs per SM (TMEM: 128 columns per warp pair sharing a lane quarter)
-static int blk_grad_grid() { return 2 * num_sms(); }
+// persistent grid of the gradient kernel: as many CTAs as fit (TMEM: 512 columns per SM)
+static int blk_grad_grid(const BlkDev& D) { return (512 / tmem_cols_for(D)) * num_sms(); }
 
 size_t blk_grad_scratch_bytes(const qal_block_plan& p) {
-  return (size_t)blk_grad_grid() * BLK_GRAD_SCR * 2 * p.packed * 8;
+  BlkDev D;
+  if (!to_dev(p, D)) return 0;
+  return (size_t)blk_grad_grid(D) * BLK_GRAD_SCR * 2 * p.packed * 8;
 }
 
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
                                    double* scratch, cudaStream_t st) {
-  BlkDev D = to_dev(p);
-  const size_t bytes = (size_t)grp_smem_doubles(D, grad_per, D.soff) * 8;
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
   static size_t attr = 0;
-  if (bytes > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_blk_grad_slices, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    attr = bytes;
-  }
-  const int quarters_rows = (D.nwarps + 3) / 4;           // warps sharing a lane quarter
-  int cols = 32;
-  while (cols < 128 * quarters_rows) cols *= 2;
+  cudaError_t e = set_smem((const void*)k_blk_grad_slices, bytes, attr);
+  if (e != cudaSuccess) return e;
   const int items = batch * G.count;
-  const int grid = items < blk_grad_grid() ? items : blk_grad_grid();
+  const int gmax = blk_grad_grid(D);
+  const int grid = items < gmax ? items : gmax;
   prof_pre(ST_BLK_GRAD, st);
-  k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, cols,
-                                                         prof_counter(ST_BLK_GRAD));
+  k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch,
+                                                         tmem_cols_for(D), prof_counter(ST_BLK_GRAD));
   prof_post(ST_BLK_GRAD, st);
   ++launch_counter();
   return cudaGetLastError();
@@ -1237,7 +1386,8 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
 
 cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* nat, double2* packed, int* flag,
                             cudaStream_t st) {
-  BlkDev D = to_dev(p);
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
   dim3 grid(4, count);
   if (flag) {
     k_blk_check<<<grid, 256, 0, st>>>(D, count, nat, flag);
@@ -1250,7 +1400,8 @@ cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* n
 
 cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2* packed, double2* nat,
                               cudaStream_t st) {
-  BlkDev D = to_dev(p);
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
   dim3 grid(4, count);
   k_blk_unpack<<<grid, 256, 0, st>>>(D, count, packed, nat);
   ++launch_counter();
@@ -1259,7 +1410,8 @@ cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2*
 
 cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
                                 cudaStream_t st) {
-  BlkDev D = to_dev(p);
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
   prof_pre(ST_FID, st);
   k_blk_fidelity<<<batch, 256, 0, st>>>(D, Lam, V, F);
   prof_post(ST_FID, st);
@@ -1267,9 +1419,14 @@ cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double
   return cudaGetLastError();
 }
 
+bool block_plan_mappable(const qal_block_plan& p) {
+  BlkDev D;
+  return to_dev(p, D);
+}
+
 // ------------------------------------------------------------------ host: structure detection
 // Components of the union sparsity graph of the given matrices; Hermitian mirror pairing;
-// first-fit-decreasing packing into super-blocks of padded width 8C <= 32.
+// best-fit-decreasing packing into super-blocks of padded width 8C <= 24.
 int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block_plan* out) {
   if (n != 64) return QAL_ERR_UNSUPPORTED;
   const int d = 8;
@@ -1321,10 +1478,14 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
   std::vector<Bin> bins;
   for (int k : keep) {
     const int sz = (int)members[k].size();
-    bool placed = false;
-    for (Bin& bn : bins)
-      if (bn.used + sz <= bn.width) { bn.used += sz; bn.comps.push_back(k); placed = true; break; }
-    if (!placed) bins.push_back({(sz + 7) / 8 * 8, sz, {k}});
+    // best fit: the open super-block with the least room left that still takes the component
+    int best = -1;
+    for (int i = 0; i < (int)bins.size(); ++i)
+      if (bins[i].used + sz <= bins[i].width &&
+          (best < 0 || bins[i].width - bins[i].used < bins[best].width - bins[best].used))
+        best = i;
+    if (best >= 0) { bins[best].used += sz; bins[best].comps.push_back(k); }
+    else bins.push_back({(sz + 7) / 8 * 8, sz, {k}});
   }
   if ((int)bins.size() > QAL_BLK_MAX_GROUPS) return QAL_ERR_UNSUPPORTED;
   qal_block_plan p;
@@ -1339,6 +1500,7 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
   for (int i = 0; i < 64; ++i) { p.inv[i] = -1; p.comp[i] = i < n ? cid[i] : -1; }
   for (int g = 0; g < p.ngroups; ++g) {
     p.width[g] = bins[g].width;
+    p.used[g] = bins[g].used;
     p.row0[g] = row;
     p.off[g] = off;
     int r = row;
@@ -1361,6 +1523,7 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
   if (row > QAL_BLK_MAX_ROWS) return QAL_ERR_UNSUPPORTED;
   p.nrows = row;
   p.packed = off;
+  if (!block_plan_mappable(p)) return QAL_ERR_UNSUPPORTED;   // more than 8 warps per CTA
   *out = p;
   return QAL_OK;
 }

@@ -432,7 +432,8 @@ class BlockPlan(ctypes.Structure):
     """Mirror of qal_block_plan (include/qal.h)."""
     _fields_ = [("n", ctypes.c_int), ("d", ctypes.c_int), ("mirror", ctypes.c_int), ("ngroups", ctypes.c_int),
                 ("nrows", ctypes.c_int), ("packed", ctypes.c_int), ("n_components", ctypes.c_int),
-                ("width", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("row0", ctypes.c_int * QAL_BLK_MAX_GROUPS),
+                ("width", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("used", ctypes.c_int * QAL_BLK_MAX_GROUPS),
+                ("row0", ctypes.c_int * QAL_BLK_MAX_GROUPS),
                 ("off", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("flops", ctypes.c_double * QAL_BLK_MAX_GROUPS),
                 ("perm", ctypes.c_int * QAL_BLK_MAX_ROWS), ("weight", ctypes.c_int * QAL_BLK_MAX_ROWS),
                 ("inv", ctypes.c_int * 64), ("comp", ctypes.c_int * 64)]
