@@ -28,6 +28,8 @@
 // rows (K trim: the 20-block multiplies with K = 20, not 24).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -41,7 +43,7 @@ namespace qal {
 constexpr int BLK_MAX_WARPS = 8;
 constexpr int BLK_MAX_TASKS = 3;
 #ifndef QAL_BLK_MAXNREG
-#define QAL_BLK_MAXNREG 168   // 3 four-warp CTAs per SM (64K registers)
+#define QAL_BLK_MAXNREG 168
 #endif
 
 // ------------------------------------------------------------------ device plan
@@ -58,6 +60,9 @@ struct BlkDev {
   int soff[QAL_BLK_MAX_GROUPS];    // double offset of group g's shared-memory region
   int ntask[BLK_MAX_WARPS];
   BlkTask task[BLK_MAX_WARPS][BLK_MAX_TASKS];
+  int tcol[BLK_MAX_WARPS];          // TMEM column base of warp w (in its lane quarter w % 4)
+  int tstride[BLK_MAX_WARPS];       // TMEM columns per slot of warp w (R * 8C of its widest task)
+  int tmem_cols;                    // columns the CTA allocates (power of two >= 32)
   signed char perm[QAL_BLK_MAX_ROWS];      // packed row -> natural index (-1 pad)
   unsigned char weight[QAL_BLK_MAX_ROWS];  // 0 pad, 1, 2
   signed char inv[64];                     // natural index -> packed row (-1 not stored)
@@ -100,12 +105,17 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
   });
   int load[BLK_MAX_WARPS] = {0};
   const int first_small = w;
+  int cap = heavy;   // stack small groups while a warp stays within 1.25x the heaviest single role
+  for (int g : small) cap = std::max(cap, blk_cost(D.C[g], D.C[g], D.ks[g]));
+  cap += cap / 4;
+#ifndef QAL_BLK_STACK
+  cap = 0;   // measured on B200: one small group per warp beats stacking them (2 vs 3 CTAs/SM)
+#endif
   for (int g : small) {
     const int c = blk_cost(D.C[g], D.C[g], D.ks[g]);
     int best = -1;
     for (int v = first_small; v < w; ++v)
-      if (D.ntask[v] < BLK_MAX_TASKS && load[v] + c <= std::max(heavy, c) + c / 4 &&
-          (best < 0 || load[v] < load[best]))
+      if (D.ntask[v] < BLK_MAX_TASKS && load[v] + c <= cap && (best < 0 || load[v] < load[best]))
         best = v;
     if (best < 0) {
       if (w >= BLK_MAX_WARPS) return false;
@@ -116,6 +126,19 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
     load[best] += c;
   }
   D.nwarps = w;
+  // TMEM: 4 strip slots per warp; warps sharing a lane quarter stack their column ranges
+  int qused[4] = {0, 0, 0, 0};
+  for (int v = 0; v < w; ++v) {
+    int st = 8;
+    for (int t = 0; t < D.ntask[v]; ++t) st = std::max(st, D.task[v][t].R * 8 * D.C[D.task[v][t].g]);
+    D.tstride[v] = st;
+    D.tcol[v] = qused[v & 3];
+    qused[v & 3] += 4 * st;
+  }
+  const int need = std::max(std::max(qused[0], qused[1]), std::max(qused[2], qused[3]));
+  D.tmem_cols = 32;
+  while (D.tmem_cols < need) D.tmem_cols *= 2;
+  if (D.tmem_cols > 512) return false;
   for (int r = 0; r < QAL_BLK_MAX_ROWS; ++r) {
     D.perm[r] = (signed char)(r < p.nrows ? p.perm[r] : -1);
     D.weight[r] = (unsigned char)(r < p.nrows ? p.weight[r] : 0);
@@ -457,7 +480,7 @@ __device__ __forceinline__ void bbuild_omega(BR<C, R>& X, const BlkBasis& B, con
 
 // ------------------------------------------------------------------ TMEM strips
 // 8C columns per strip (re 4C words, im 4C words); a warp's slot s of strip r starts at column
-// tm + 32 s + 8C r (slot stride 32 columns: R * 8C <= 32 for every role).
+// tm + s * tstride + 8C r (tstride = R * 8C of the warp's widest role, host-computed).
 template <int N>
 __device__ __forceinline__ void tm_st(uint32_t addr, const uint32_t* v);
 template <>
@@ -548,8 +571,8 @@ __device__ __forceinline__ void bt_axpy(BR<C, R>& acc, double a, uint32_t addr) 
   }
 }
 
-__device__ __forceinline__ uint32_t warp_tmem(uint32_t base, const Lane& L) {
-  return base + (static_cast<uint32_t>(32 * (L.w & 3)) << 16) + static_cast<uint32_t>((L.w >> 2) * 128);
+__device__ __forceinline__ uint32_t warp_tmem(uint32_t base, const BlkDev& D, const Lane& L) {
+  return base + (static_cast<uint32_t>(32 * (L.w & 3)) << 16) + static_cast<uint32_t>(D.tcol[L.w]);
 }
 __device__ __forceinline__ void blk_tmem_alloc(uint32_t* slot, int cols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols));
@@ -565,8 +588,8 @@ __device__ __forceinline__ void blk_tmem_dealloc(uint32_t base, int cols) {
 // Result in A.  Returns the products done.
 template <int C, int R, int KS>
 __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, double* SX, double* SX4, uint32_t tm,
-                                     const Ctx& x, const Lane& L) {
-  const uint32_t T0 = tm, T1 = tm + 32, T2 = tm + 64;
+                                     uint32_t ts, const Ctx& x, const Lane& L) {
+  const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts;
   int prods;
   bzero(acc); bmma<C, R, KS>(acc, A, SX, x, L);                  // A2 = X X
   bt_store(T0, acc);
@@ -657,6 +680,7 @@ template <int C, int R, int KS>
 __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
                              const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long& nflop,
                              const Lane& L) {
+  const uint32_t ts = D.tstride[L.w];
   double* SX = sm;
   double* SX4 = sm + 2 * 64 * C * C;
   double* SP = sm + 4 * 64 * C * C;
@@ -675,7 +699,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     bscale(A, ldexp(1.0, -s));
     bstore_img(SX, A, x, L);
     grp_sync(x);
-    const int np = bexpm<C, R, KS>(A, acc, m, s, SX, SX4, tm, x, L);
+    const int np = bexpm<C, R, KS>(A, acc, m, s, SX, SX4, tm, ts, x, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const size_t slot = (size_t)b * G.count + k;
     if (O.U_img) bstore_img_l2(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
@@ -713,7 +737,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis 
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tm = warp_tmem(tmem_base_sh, L);
+  const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
   unsigned long long nflop = 0;
   const int item = blockIdx.x;
   for (int t = 0; t < D.ntask[L.w]; ++t) {
@@ -976,7 +1000,7 @@ template <int C, int R, int KS>
 __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const BlkBasis& B, const SliceGrid& G,
                                              const double* Pk, int b, int k, const Ctx& x, double* SD, double* SV,
                                              double* SN, uint64_t* barN, uint32_t& phN, double* red, uint32_t tm,
-                                             double* scr, int* bad, const Lane& L) {
+                                             uint32_t ts, double* scr, int* bad, const Lane& L) {
   const size_t IM = 2 * 64 * C * C;
   double* gX = scr;
   double* gdX = scr + IM;
@@ -984,7 +1008,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
   double* gdA6 = scr + 3 * IM;
   double* gE = scr + 4 * IM;
   double* gdE = scr + 5 * IM;
-  const uint32_t T0 = tm, T1 = tm + 32, T2 = tm + 64, T3 = tm + 96;   // A2, dA2, A3|Y, dA3|dY
+  const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
   const uint64_t keep = l2_evict_last();
   bbuild_omega(A, B, G, b, k, x, L);
   const double nrm = bnorm1(A, red, x, L);
@@ -1175,8 +1199,8 @@ __device__ void blk_grad_task(const BlkDev& D, const BlkBasis& B, const SliceGri
                               int* bad, double* tr, bool first, unsigned long long& nflop, const Lane& L) {
   const int IM = 2 * 64 * C * C;
   BR<C, R> A, acc;
-  const int np = blk_dual_expm<C, R, KS>(A, acc, B, G, Pk, b, k, x, sm, sm + IM, sm + 2 * IM, barN, phN, sm + 3 * IM, tm,
-                                     scr, bad, L);
+  const int np = blk_dual_expm<C, R, KS>(A, acc, B, G, Pk, b, k, x, sm, sm + IM, sm + 2 * IM, barN, phN, sm + 3 * IM,
+                                         tm, D.tstride[L.w], scr, bad, L);
   if (x.rt0 == 0 && L.lane == 0) nflop += (unsigned long long)np * D.gflops[x.g];
   blk_traces<C, R>(A, D, B, b, x, tr, first, L);
 }
@@ -1204,7 +1228,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tm = warp_tmem(tmem_base_sh, L);
+  const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
   const int items = batch * N;
@@ -1300,10 +1324,13 @@ int grp_smem_doubles(BlkDev& D, int (*per)(int)) {
 int per3(int C) { return grp3_doubles(C); }
 int per_pair(int C) { return 2 * 64 * C * C; }
 int per_chain(int C) { return 2 * 2 * 64 * C * C; }
-int tmem_cols_for(const BlkDev& D) { return D.nwarps > 4 ? 256 : 128; }
+int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 cudaError_t set_smem(const void* fn, size_t bytes, size_t& attr) {
   if (bytes > attr) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    // all of the unified L1 / shared capacity as shared memory: several CTAs per SM
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr = bytes;
   }
@@ -1355,8 +1382,25 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
   return cudaGetLastError();
 }
 
-// persistent grid of the gradient kernel: as many CTAs as fit (TMEM: 512 columns per SM)
-static int blk_grad_grid(const BlkDev& D) { return (512 / tmem_cols_for(D)) * num_sms(); }
+// persistent grid of the gradient kernel: exactly the CTAs that are co-resident (registers,
+// shared memory, and TMEM: 512 columns per SM); a CTA beyond that would start only when one
+// finished and double the tail
+static int blk_grad_grid(const BlkDev& D) {
+  BlkDev tmp = D;
+  const size_t bytes = (size_t)grp_smem_doubles(tmp, per3) * 8;
+  cudaFuncAttributes fa;
+  int per_sm = 1;
+  if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess && fa.numRegs > 0) {
+    // registers (64K per SM, per-warp allocation rounded to 256), shared memory (233 KB config,
+    // 1 KB reserved per CTA), named barriers (64 per SM, 16 per CTA), TMEM (512 columns)
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / (regs_warp * D.nwarps);
+    const int by_smem = (int)(233472 / (bytes + fa.sharedSizeBytes + 1024));
+    per_sm = std::min(std::min(by_regs, by_smem), std::min(4, 512 / tmem_cols_for(D)));
+  }
+  if (getenv("QAL_DEBUG")) fprintf(stderr, "blk_grad_grid: nwarps %d smem %zu per_sm %d\n", D.nwarps, bytes, per_sm);
+  return std::max(1, per_sm) * num_sms();
+}
 
 size_t blk_grad_scratch_bytes(const qal_block_plan& p) {
   BlkDev D;

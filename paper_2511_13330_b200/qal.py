@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqal.so")
+LIB_PATH = os.environ.get("QAL_LIB") or os.path.join(_HERE, "libqal.so")   # QAL_LIB: experiment builds only
 
 QAL_OK = 0
 QAL_CTRL_PWC = 0
