@@ -35,11 +35,16 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pulses", type=int, default=4096, help="pulses per GPU (configs[2]: 4096)")
     ap.add_argument("--slices", type=int, default=1024)
-    ap.add_argument("--sub-batch", type=int, default=296)
+    ap.add_argument("--sub-batch", type=int, default=None,
+                    help="pulses per library call (default: dense 296, blocks sized to ~40 GB of workspace)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
     ap.add_argument("--cfg4-slices", type=int, default=8, help="slices per step of the cfg4 sample")
+    ap.add_argument("--structure", default="blocks", choices=["blocks", "dense"],
+                    help="cfg2 path: coherence-block (default, SURVEY 8(f) row 4) or dense 64x64")
+    ap.add_argument("--no-dense-ref", action="store_true",
+                    help="skip the dense-path reference measurement that accompanies the block path")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg3grad", "cfg4", "hubbard3"],
                     help="cfg2: batch fwd+grad (default, weak scaling); cfg3: 2^20-slice horizon, time-sharded")
     return ap.parse_args()
@@ -144,6 +149,56 @@ def load_traffic():
         return {}
 
 
+def roofline_of(stages, prods, steps, peak_tf, units_per_launch):
+    """Roofline of the dominant kernel (largest device time in the profiling window), the per-stage
+    split and the algorithmic flops per step.  Block stages count flops (8 s^3 per block product),
+    dense stages count 64x64 products (qal.FLOP_STAGES, driver.stage_flops)."""
+    from paper_2511_13330_b200 import driver, qal
+    dom = max(stages, key=lambda s: stages[s][0])
+    dom_ms, dom_launch = stages[dom]
+    dom_idx = qal.STAGES.index(dom)
+    dom_flops_per_launch = driver.stage_flops(prods[dom_idx], dom) / max(dom_launch, 1)
+    achieved = dom_flops_per_launch / (dom_ms / max(dom_launch, 1) * 1e-3) / 1e12
+    tr = load_traffic().get(qal.KERNELS[dom])
+    traffic = (tr["dram_bytes_per_unit"] * units_per_launch) if (tr and units_per_launch) else None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": traffic, "kernel": qal.KERNELS[dom],
+                "peak_source": "measured FP64 DMMA.8x8x4 peak (K0 probe, this run, this GPU); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "flops_per_launch": dom_flops_per_launch, "ms_per_launch": dom_ms / max(dom_launch, 1)}
+    step_flops = sum(driver.stage_flops(prods[i], s) for i, s in enumerate(qal.STAGES)) / steps
+    split = {s: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps,
+                 "flops_per_step": driver.stage_flops(prods[i], s) / steps,
+                 "tflops": (driver.stage_flops(prods[i], s) / (v[0] * 1e-3) / 1e12) if v[0] > 0 else None}
+             for i, (s, v) in enumerate(stages.items()) if v[1] > 0}
+    return roofline, split, step_flops
+
+
+def dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, peak_tf, barrier):
+    """The dense 64x64 path on the same pulses (1 warm-up + 1 timed step): slices/s and the roofline of
+    its dominant kernel, reported beside the block path so both numbers come from one run."""
+    eng = driver.PulseBatch(H0, Hc, C, u, V, T, sub_batch=296, structure="dense")
+    eng.step()
+    torch.cuda.synchronize()
+    counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=u.device)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qal.qal_profile_begin(counters)
+    ev0.record()
+    F, g = eng.step()
+    ev1.record()
+    torch.cuda.synchronize()
+    stages = qal.qal_profile_end()
+    ms = ev0.elapsed_time(ev1)
+    roof, split, flops = roofline_of(stages, counters.cpu().tolist(), 1, peak_tf, eng.sub * N)
+    out = {"value": world * B * N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+           "pct_fp64_roofline": flops / (ms * 1e-3) / 1e12 / peak_tf, "roofline": roof,
+           "steps": 1, "warmup": 1, "note": "dense 64x64 superoperators (every SURVEY 8(a) row), same pulses"}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -164,7 +219,8 @@ def run_ours(args):
     prob = qi.cfg2(batch=B, N=N, T=T, first_pulse=rank * B)       # rank owns pulses [rank B, (rank+1) B)
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     H0, Hc, C, u, V = to(prob.H0), to(prob.Hc), to(prob.C), to(prob.u), to(prob.V)
-    eng = driver.PulseBatch(H0, Hc, C, u, V, T, sub_batch=args.sub_batch)
+    sub = args.sub_batch if args.sub_batch else (296 if args.structure == "dense" else None)
+    eng = driver.PulseBatch(H0, Hc, C, u, V, T, sub_batch=sub, structure=args.structure)
 
     sink = torch.zeros(1, dtype=torch.float64, device=dev)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -179,7 +235,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # ---------------- timed region: device-resident inputs
-    counters = torch.zeros(9, dtype=torch.int64, device=dev)
+    counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -232,24 +288,13 @@ def run_ours(args):
                "d2h_bytes_per_step": int(hF.numel() * 8 + hg.numel() * 8)}
 
     # ---------------- roofline of the dominant kernel (largest device time in the window)
-    dom = max(stages, key=lambda s: stages[s][0])
-    dom_ms, dom_launch = stages[dom]
-    dom_idx = qal.STAGES.index(dom)
-    dom_flops_per_launch = driver.stage_flops(prods[dom_idx]) / max(dom_launch, 1)
-    achieved = dom_flops_per_launch / (dom_ms / max(dom_launch, 1) * 1e-3) / 1e12
-    tr = load_traffic().get(qal.KERNELS[dom])
-    units_per_launch = {"grad_slices": eng.sub * N, "expm_fold": eng.sub * N}.get(dom)
-    traffic = (tr["dram_bytes_per_unit"] * units_per_launch) if (tr and units_per_launch) else None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved / peak_tf, "traffic": traffic, "kernel": qal.KERNELS[dom],
-                "peak_source": "measured FP64 DMMA.8x8x4 peak (K0 probe, this run, this GPU); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
-                "flops_per_launch": dom_flops_per_launch, "ms_per_launch": dom_ms / max(dom_launch, 1)}
-    step_flops = sum(driver.stage_flops(p) for p in prods) / args.steps
-    split = {s: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
-                 "products_per_step": prods[i] / args.steps,
-                 "tflops": (driver.stage_flops(prods[i]) / (v[0] * 1e-3) / 1e12) if v[0] > 0 else None}
-             for i, (s, v) in enumerate(stages.items()) if v[1] > 0}
+    roofline, split, step_flops = roofline_of(stages, prods, args.steps, peak_tf, eng.sub * N)
+    structure_ok = eng.structure_ok()
+
+    # ---------------- the dense 64x64 path on the same workload (context for the block path)
+    dense_ref = None
+    if args.structure == "blocks" and not args.no_dense_ref:
+        dense_ref = dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, peak_tf, barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -266,6 +311,10 @@ def run_ours(args):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": "configs[2]: pulses x 1024 PWC slices, T=200 ns, d=8 (64x64 c128 "
                                        "superoperators), forward + fidelity + gradient",
+                           "structure": (f"coherence blocks (detected {eng.plan.n_components} components; "
+                                         f"stored widths {[eng.plan.width[g] for g in range(eng.plan.ngroups)]}, "
+                                         "Hermitian mirror), identical 64x64 results"
+                                         if args.structure == "blocks" else "dense 64x64"),
                            "pulses_per_gpu": B, "slices": N, "sub_batch": eng.sub,
                            "l2": f"inputs larger than L2 (gradient workspace {eng.ws_bytes / 2**30:.1f} GiB)",
                            "parallelism": f"batch-sharded x{world}"},
@@ -273,6 +322,7 @@ def run_ours(args):
                 "pct_fp64_roofline": step_flops / (ms_max / args.steps * 1e-3) / 1e12 / peak_tf,
                 "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "structure_check": "ok" if structure_ok else "FAILED", "dense_path": dense_ref,
                 "gpu": torch.cuda.get_device_name(dev)}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -313,7 +363,7 @@ def run_cfg3grad(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    counters = torch.zeros(9, dtype=torch.int64, device=dev)
+    counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -393,7 +443,7 @@ def run_cfg3(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    counters = torch.zeros(9, dtype=torch.int64, device=dev)
+    counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -485,7 +535,7 @@ def run_cfg4(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    counters = torch.zeros(9, dtype=torch.int64, device=dev)
+    counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:

@@ -35,7 +35,8 @@ class PulseBatch:
     a7 gradient) and leaves F [B] and grad [B][N][J] in preallocated device buffers.
     """
 
-    def __init__(self, H0, Hc, C, u, V, T, *, sub_batch=None, want_grad=True, magnus_order=4, stream=None):
+    def __init__(self, H0, Hc, C, u, V, T, *, sub_batch=None, want_grad=True, magnus_order=4, stream=None,
+                 structure="dense"):
         self.H0, self.Hc, self.C, self.u, self.V = H0, Hc, C, u, V
         self.B, self.N, self.J = u.shape[0], u.shape[1], Hc.shape[0]
         self.d = V.shape[0]
@@ -43,31 +44,60 @@ class PulseBatch:
         self.T = float(T)
         self.order = magnus_order
         self.want_grad = want_grad
+        if structure not in ("dense", "blocks"):
+            raise ValueError(f"structure must be 'dense' or 'blocks', got {structure!r}")
+        self.structure = structure
         dev = u.device
         self.stream = stream
-        self.sub = self.B if sub_batch is None else min(sub_batch, self.B)
         self.L0 = torch.empty((self.B, self.n, self.n), dtype=C128, device=dev)
         self.Lc = torch.empty((self.J, self.n, self.n), dtype=C128, device=dev)
         self.F = torch.empty(self.B, dtype=F64, device=dev)
         self.grad = torch.empty_like(u) if want_grad else None
         self.status = torch.zeros(self.B, dtype=torch.int32, device=dev)
         op = qal.QAL_OP_FIDELITY_GRAD if want_grad else qal.QAL_OP_FIDELITY
-        self.ws_bytes = qal.workspace_bytes(op, self.n, self.sub, self.N, self.J, 0)
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
         self.launches = 0
+        if structure == "dense":
+            self.sub = self.B if sub_batch is None else min(sub_batch, self.B)
+            self.ws_bytes = qal.workspace_bytes(op, self.n, self.sub, self.N, self.J, 0)
+        else:
+            # coherence-block path: the plan is detected once from the generator
+            # basis of pulse 0 (the device structure check re-verifies every pulse on every step)
+            self._build_basis()
+            self.plan = qal.qal_block_plan_build(torch.cat([self.L0[:1], self.Lc]), mirror=True)
+            self.L0p = torch.empty((self.B, self.plan.packed), dtype=C128, device=dev)
+            self.Lcp = torch.empty((self.J, self.plan.packed), dtype=C128, device=dev)
+            self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            if sub_batch is None:
+                # image workspace (3 packed images per slice) within ~40 GB of HBM, in whole waves of
+                # the one-CTA-per-pulse forward and suffix kernels (2 resident CTAs per SM)
+                per = 3 * self.N * self.plan.packed * 16
+                wave = 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+                sub_batch = int(40e9 // per)
+                if sub_batch >= wave:
+                    sub_batch -= sub_batch % wave
+                sub_batch = max(1, min(self.B, sub_batch))
+            self.sub = min(sub_batch, self.B)
+            self.ws_bytes = qal.block_workspace_bytes(self.plan, op, self.sub, self.N)
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
 
     def _s(self):
         s = torch.cuda.current_stream() if self.stream is None else self.stream
         return ctypes.c_void_p(s.cuda_stream)
 
+    def _build_basis(self):
+        lib = qal.load()
+        nc = 0 if self.C is None else self.C.shape[0]
+        rc = lib.qal_build_liouvillian(self.d, self.B, _p(self.H0), self.J, _p(self.Hc), nc, _p(self.C), 0,
+                                       _p(self.L0), _p(self.Lc), None, self._s())
+        qal._check(rc, "qal_build_liouvillian")
+        return lib.qal_last_launch_count()
+
     def step(self):
         lib = qal.load()
         st = self._s()
-        nc = 0 if self.C is None else self.C.shape[0]
-        rc = lib.qal_build_liouvillian(self.d, self.B, _p(self.H0), self.J, _p(self.Hc), nc, _p(self.C), 0,
-                                       _p(self.L0), _p(self.Lc), None, st)
-        qal._check(rc, "qal_build_liouvillian")
-        launches = lib.qal_last_launch_count()
+        launches = self._build_basis()
+        if self.structure == "blocks":
+            return self._step_blocks(lib, st, launches)
         plane = self.n * self.n
         for b0 in range(0, self.B, self.sub):
             nb = min(self.sub, self.B - b0)
@@ -82,6 +112,30 @@ class PulseBatch:
             launches += lib.qal_last_launch_count()
         self.launches = launches
         return self.F, self.grad
+
+    def _step_blocks(self, lib, st, launches):
+        pl = ctypes.byref(self.plan)
+        for src, dst in ((self.L0, self.L0p), (self.Lc, self.Lcp)):
+            qal._check(lib.qal_block_pack(pl, src.shape[0], _p(src), _p(dst), _p(self.flag), st), "qal_block_pack")
+            launches += lib.qal_last_launch_count()
+        P = self.plan.packed
+        for b0 in range(0, self.B, self.sub):
+            nb = min(self.sub, self.B - b0)
+            rc = lib.qal_block_fidelity_grad(
+                pl, nb, self.N, self.T, self.order, qal.QAL_CTRL_PWC, self.J,
+                ctypes.c_void_p(self.u.data_ptr() + b0 * self.N * self.J * 8),
+                ctypes.c_void_p(self.L0p.data_ptr() + b0 * P * 16), P, _p(self.Lcp), None, 0, _p(self.V),
+                ctypes.c_void_p(self.F.data_ptr() + b0 * 8),
+                ctypes.c_void_p(self.grad.data_ptr() + b0 * self.N * self.J * 8) if self.want_grad else None,
+                None, ctypes.c_void_p(self.status.data_ptr() + b0 * 4), _p(self.ws), self.ws_bytes, st)
+            qal._check(rc, "qal_block_fidelity_grad")
+            launches += lib.qal_last_launch_count()
+        self.launches = launches
+        return self.F, self.grad
+
+    def structure_ok(self) -> bool:
+        """False if the device check found an operator coupling two blocks of the plan (synchronises)."""
+        return self.structure == "dense" or int(self.flag.item()) == 0
 
 
 def shard_range(total: int, world: int, rank: int):
@@ -281,7 +335,11 @@ def complex_product_flops(n: int = 64) -> float:
     return 2.0 * n ** 3 * qal.real_mults_per_complex_product()
 
 
-def stage_flops(products: int) -> float:
+def stage_flops(products: int, stage: str = "") -> float:
+    """Algorithmic flops of a profiling-window counter: the dense stages count 64x64 complex
+    products, the coherence-block stages (qal.FLOP_STAGES) count flops directly."""
+    if stage in qal.FLOP_STAGES:
+        return float(products)
     return products * complex_product_flops(64)
 
 

@@ -247,3 +247,24 @@ def test_block_gradient_matches_dense_path_bitwise_shape(torch_cuda, qal):
     assert ((Fb - Fd).abs() / Fd.abs()).max().item() <= 1e-12
     err = ((gb - gd).reshape(64, -1).norm(dim=1) / gd.reshape(64, -1).norm(dim=1)).max().item()
     assert err <= 1e-11, err
+
+
+def test_pulse_batch_block_structure_matches_oracle(torch_cuda, qal, oracle):
+    """The bench engine (driver.PulseBatch, structure='blocks', sub-batched) vs the oracle on sampled
+    pulses of a configs[2]-recipe batch, and vs the dense engine on every pulse."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg2(batch=40, N=64, T=200.0 * 64 / 1024)
+    args = [dev(torch, a) for a in (p.H0, p.Hc, p.C, p.u, p.V)]
+    eb = driver.PulseBatch(*args, p.T, sub_batch=16, structure="blocks")
+    Fb, gb = eb.step()
+    assert eb.structure_ok()
+    ed = driver.PulseBatch(*args, p.T, sub_batch=16, structure="dense")
+    Fd, gd = ed.step()
+    assert ((Fb - Fd).abs() / Fd.abs()).max().item() <= 1e-12
+    assert ((gb - gd).reshape(40, -1).norm(dim=1) / gd.reshape(40, -1).norm(dim=1)).max().item() <= 1e-11
+    for b in (0, 17, 39):
+        rL0, rLc = oracle.build_liouvillian(p.H0[b], p.Hc, p.C)
+        Fr, gr, _ = oracle.gradient(rL0, rLc, p.u[b], p.T, p.N, p.V)
+        assert abs(Fb[b].item() - Fr) / abs(Fr) <= TOL_PROP
+        assert relfro(gb[b].cpu().numpy(), gr) <= TOL_GRAD
