@@ -428,12 +428,24 @@ def run_cfg3(args):
     peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
 
     state = {}
+    plan = None
+    if args.structure == "blocks":
+        L0, Lc, Lcomm = qal.qal_build_liouvillian(H0, Hc, C, want_comm=True)
+        plan = qal.qal_block_plan_build(torch.cat([L0, Lc, Lcomm.reshape(-1, 64, 64)]), mirror=True)
+        state["flag"] = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def step():
         u = qal.qal_sample_controls_sines(prm, prob.u_max, N, T, k0, k1 - k0)
         L0, Lc, Lcomm = qal.qal_build_liouvillian(H0, Hc, C, want_comm=True)
-        Lam = driver.time_shard_propagator(L0, Lc, Lcomm, u.unsqueeze(0), T, N, k0, ctrl_mode=qal.QAL_CTRL_NODES)
-        state["F"] = qal.qal_fidelity(Lam.unsqueeze(0), V)
+        if plan is not None:
+            mats = [qal.qal_block_pack(plan, m, check=True)[0] for m in (L0, Lc, Lcomm)]
+            Lam = driver.time_shard_propagator(*mats, u.unsqueeze(0), T, N, k0, ctrl_mode=qal.QAL_CTRL_NODES,
+                                               plan=plan)
+            state["F"] = qal.qal_block_fidelity(plan, Lam.unsqueeze(0), V)
+        else:
+            Lam = driver.time_shard_propagator(L0, Lc, Lcomm, u.unsqueeze(0), T, N, k0,
+                                               ctrl_mode=qal.QAL_CTRL_NODES)
+            state["F"] = qal.qal_fidelity(Lam.unsqueeze(0), V)
         state["Lam"] = Lam
 
     def barrier():
@@ -464,25 +476,17 @@ def run_cfg3(args):
     ms_max = t.item()
     prods = counters.cpu().tolist()
     value = N * args.steps / (ms_max * 1e-3)
-    dom = "expm_fold"
-    dom_ms, dom_l = stages[dom]
-    ach = driver.stage_flops(prods[qal.STAGES.index(dom)]) / (dom_ms * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
-                "traffic": None, "kernel": "k_expm_fold",
-                "peak_source": "measured FP64 DMMA.8x8x4 peak (K0 probe, this run)",
-                "flops_per_launch": driver.stage_flops(prods[qal.STAGES.index(dom)]) / max(dom_l, 1),
-                "ms_per_launch": dom_ms / max(dom_l, 1)}
-    split = {s: {"ms_per_step": v[0] / args.steps, "products_per_step": prods[i] / args.steps}
-             for i, (s, v) in enumerate(stages.items()) if v[1] > 0}
+    roofline, split, step_flops = roofline_of(stages, prods, args.steps, peak_tf, None)
     if rank == 0:
-        step_flops = sum(driver.stage_flops(p) for p in prods) / args.steps
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": "configs[3]: 1 pulse, N=2^20 Magnus-4 NODES slices over 10 us, "
                                        "time-sharded, all-gather of G partials + ordered combine",
                            "slices": N, "chunk": driver.time_shard_chunk(N), "parallelism": f"time-sharded x{world}",
-                           "l2": "chunk partials 1 GiB > L2"},
+                           "structure": ("coherence blocks (Hermitian mirror), packed partials"
+                                         if plan is not None else "dense 64x64"),
+                           "l2": "chunk partials larger than L2 (dense 1 GiB, blocks 235 MB)"},
                 "pct_fp64_roofline": step_flops / (ms_max / args.steps * 1e-3) / 1e12 / peak_tf,
                 "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split,
                 "F": state["F"].item(), "clocks": clk, "gpu": torch.cuda.get_device_name(dev)}

@@ -268,3 +268,22 @@ def test_pulse_batch_block_structure_matches_oracle(torch_cuda, qal, oracle):
         Fr, gr, _ = oracle.gradient(rL0, rLc, p.u[b], p.T, p.N, p.V)
         assert abs(Fb[b].item() - Fr) / abs(Fr) <= TOL_PROP
         assert relfro(gb[b].cpu().numpy(), gr) <= TOL_GRAD
+
+
+def test_time_shard_propagator_blocks_matches_oracle(torch_cuda, qal, oracle):
+    """configs[3] recipe through driver.time_shard_propagator with a block plan (G = 1 on one GPU):
+    packed chunk fold + tree + ordered combine vs the oracle's sequential fold."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg3()
+    N, T = 512, 400.0
+    u = oracle.sines_nodes(p.sines, p.u_max, N, T)[None]
+    plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
+    Lam_p = driver.time_shard_propagator(L0p, Lcp, Lcommp, dev(torch, u), T, N, 0, ctrl_mode=1, plan=plan)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(rL0, rLc, u[0], T, N, mode=1)
+    got = qal.qal_block_unpack(plan, Lam_p.unsqueeze(0))[0].cpu().numpy()
+    assert relfro(got, Lam) <= TOL_PROP
+    F = qal.qal_block_fidelity(plan, Lam_p.unsqueeze(0), dev(torch, p.V)).item()
+    Fr = oracle.fidelity(Lam, p.V)
+    assert abs(F - Fr) / abs(Fr) <= TOL_PROP
