@@ -991,23 +991,25 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
 
 // --------------------------------------------------------------- gradient slices
 constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
-constexpr int BLK_GRAD_SCR = 6;   // L2 scratch images per group: X, dX, A6, dA6, E, dE
+constexpr int BLK_GRAD_SCR = 2;   // L2 scratch images per group (squarings): E, dE
 
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
 // leaves W = L_exp(Omega, G) in A and returns the product count.  SD, SV, SN: group images
 // (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots; scr: the group's L2 scratch.
 template <int C, int R, int KS>
 __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const BlkBasis& B, const SliceGrid& G,
-                                             const double* Pk, int b, int k, const Ctx& x, double* SD, double* SV,
-                                             double* SN, uint64_t* barN, uint32_t& phN, double* red, uint32_t tm,
-                                             uint32_t ts, double* scr, int* bad, const Lane& L) {
+                                             int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
+                                             uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
+                                             uint32_t tm, uint32_t ts, double* scr, int* bad, const Lane& L) {
   const size_t IM = 2 * 64 * C * C;
-  double* gX = scr;
-  double* gdX = scr + IM;
-  double* gA6 = scr + 2 * IM;
-  double* gdA6 = scr + 3 * IM;
-  double* gE = scr + 4 * IM;
-  double* gdE = scr + 5 * IM;
+  // shared scratch images (own strips only, re-read within the item): X, dX, A6, dA6
+  double* gX = sX;
+  double* gdX = sX + IM;
+  double* gA6 = sX + 2 * IM;
+  double* gdA6 = sX + 3 * IM;
+  // L2 scratch (squarings only): E, dE
+  double* gE = scr;
+  double* gdE = scr + IM;
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
   const uint64_t keep = l2_evict_last();
   bbuild_omega(A, B, G, b, k, x, L);
@@ -1018,17 +1020,18 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
   const double sc = ldexp(1.0, -s);
   bscale(A, sc);
   bstore_img(SV, A, x, L);
-  bstore_img_l2(gX, A, x, L, keep);
-  // G = P_k X_{k+1};  dX = G / 2^s
-  bload_img_l2(A, Pk, x, L, l2_evict_first());
-  mbar_wait(barN, phN);
-  phN ^= 1;
+  bstore_img(gX, A, x, L);
+  // G = P_k X_{k+1} (P_k in SD, X_{k+1} in SN: both TMA-prefetched during the previous item);  dX = G / 2^s
+  mbar_wait(barP, ph);
+  bload_img(A, SD, x, L);
+  mbar_wait(barN, ph);
+  ph ^= 1;
   bzero(acc);
   bmma<C, R, KS>(acc, A, SN, x, L);
   bscale(acc, sc);
-  grp_sync(x);                                         // SV (X) complete
+  grp_sync(x);                                         // SV (X) complete; reads of SD (P_k) done
   bstore_img(SD, acc, x, L);
-  bstore_img_l2(gdX, acc, x, L, keep);
+  bstore_img(gdX, acc, x, L);
   grp_sync(x);                                         // SD = dX complete
   bload_img(A, SV, x, L);
   bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                  // A2 = X X
@@ -1040,8 +1043,8 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
   int np = 1 + 1 + 2;
   if (m == 8) {
     grp_sync(x);
-    bzero(acc); baxpy_img_l2(acc, c_t8[0], gX, x, L, keep); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, x, L);
-    bzero(acc); baxpy_img_l2(acc, c_t8[0], gdX, x, L, keep); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, x, L);
+    bzero(acc); baxpy_img(acc, c_t8[0], gX, x, L); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, x, L);
+    bzero(acc); baxpy_img(acc, c_t8[0], gdX, x, L); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, x, L);
     grp_sync(x);
     bt_load(A, T0);
     bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // Y = A2 W
@@ -1055,16 +1058,16 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     bzero(acc); bt_axpy(acc, 1.0, T3); bt_axpy(acc, c_t8[4], T1); bstore_img(SD, acc, x, L);
     grp_sync(x);
     bzero(acc);
-    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img_l2(acc, 1.0, gdX, x, L, keep);
-    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img_l2(A, c_t8[3], gdX, x, L, keep);   // dL
+    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img(acc, 1.0, gdX, x, L);
+    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img(A, c_t8[3], gdX, x, L);   // dL
     bmma<C, R, KS>(acc, A, SV, x, L);
-    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img_l2(A, c_t8[3], gX, x, L, keep);    // L
+    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img(A, c_t8[3], gX, x, L);    // L
     bmma<C, R, KS>(acc, A, SD, x, L);
     if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
     np += 1 + 2 + 2;
     if (s > 0) {
       bzero(acc);
-      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img_l2(acc, 1.0, gX, x, L, keep);
+      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img(acc, 1.0, gX, x, L);
       badd_diag(acc, 1.0, x, L);
       bmma<C, R, KS>(acc, A, SV, x, L);
       bstore_img_l2(gE, acc, x, L, keep);
@@ -1084,60 +1087,60 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     grp_sync(x);
     bt_load(A, T2);
     bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // A6
-    bstore_img_l2(gA6, acc, x, L, keep);
+    bstore_img(gA6, acc, x, L);
     bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A3 dA3
     bt_load(A, T3);
     bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA3 A3
-    bstore_img_l2(gdA6, acc, x, L, keep);
+    bstore_img(gdA6, acc, x, L);
     grp_sync(x);
     bzero(acc);
-    baxpy_img_l2(acc, c_t18[T18_B5][1], gX, x, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T0);
-    baxpy_img_l2(acc, 1.0, gA6, x, L, keep);
+    baxpy_img(acc, c_t18[T18_B5][1], gX, x, L); bt_axpy(acc, c_t18[T18_B5][2], T0);
+    baxpy_img(acc, 1.0, gA6, x, L);
     bstore_img(SV, acc, x, L);
     bzero(acc);
-    baxpy_img_l2(acc, c_t18[T18_B5][1], gdX, x, L, keep); bt_axpy(acc, c_t18[T18_B5][2], T1);
-    baxpy_img_l2(acc, 1.0, gdA6, x, L, keep);
+    baxpy_img(acc, c_t18[T18_B5][1], gdX, x, L); bt_axpy(acc, c_t18[T18_B5][2], T1);
+    baxpy_img(acc, 1.0, gdA6, x, L);
     bstore_img(SD, acc, x, L);
     grp_sync(x);
     bzero(acc);                                        // dA9 = dB4 + dB1 B5 + B1 dB5
-    baxpy_img_l2(acc, c_t18[T18_B4][1], gdX, x, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T1);
-    bt_axpy(acc, c_t18[T18_B4][3], T3); baxpy_img_l2(acc, c_t18[T18_B4][4], gdA6, x, L, keep);
+    baxpy_img(acc, c_t18[T18_B4][1], gdX, x, L); bt_axpy(acc, c_t18[T18_B4][2], T1);
+    bt_axpy(acc, c_t18[T18_B4][3], T3); baxpy_img(acc, c_t18[T18_B4][4], gdA6, x, L);
     bzero(A);
-    baxpy_img_l2(A, c_t18[T18_B1][1], gdX, x, L, keep); bt_axpy(A, c_t18[T18_B1][2], T1);
+    baxpy_img(A, c_t18[T18_B1][1], gdX, x, L); bt_axpy(A, c_t18[T18_B1][2], T1);
     bt_axpy(A, c_t18[T18_B1][3], T3);
     bmma<C, R, KS>(acc, A, SV, x, L);
     bzero(A);
-    baxpy_img_l2(A, c_t18[T18_B1][1], gX, x, L, keep); bt_axpy(A, c_t18[T18_B1][2], T0);
+    baxpy_img(A, c_t18[T18_B1][1], gX, x, L); bt_axpy(A, c_t18[T18_B1][2], T0);
     bt_axpy(A, c_t18[T18_B1][3], T2);
     bmma<C, R, KS>(acc, A, SD, x, L);
     bstore_img(SN, acc, x, L);                         // dA9 (SN idle since G)
     bzero(acc);                                        // A9 = B4 + B1 B5 (A holds B1)
     badd_diag(acc, c_t18[T18_B4][0], x, L);
-    baxpy_img_l2(acc, c_t18[T18_B4][1], gX, x, L, keep); bt_axpy(acc, c_t18[T18_B4][2], T0);
-    bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img_l2(acc, c_t18[T18_B4][4], gA6, x, L, keep);
+    baxpy_img(acc, c_t18[T18_B4][1], gX, x, L); bt_axpy(acc, c_t18[T18_B4][2], T0);
+    bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img(acc, c_t18[T18_B4][4], gA6, x, L);
     bmma<C, R, KS>(acc, A, SV, x, L);
     grp_sync(x);                                       // reads of SV (B5), SD (dB5) done
     bstore_img(SV, acc, x, L);                         // A9
     grp_sync(x);                                       // A9 (SV), dA9 (SN) complete
     bzero(acc);                                        // dT = dB2 + dL A9 + L dA9
-    baxpy_img_l2(acc, c_t18[T18_B2][1], gdX, x, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T1);
-    bt_axpy(acc, c_t18[T18_B2][3], T3); baxpy_img_l2(acc, c_t18[T18_B2][4], gdA6, x, L, keep);
+    baxpy_img(acc, c_t18[T18_B2][1], gdX, x, L); bt_axpy(acc, c_t18[T18_B2][2], T1);
+    bt_axpy(acc, c_t18[T18_B2][3], T3); baxpy_img(acc, c_t18[T18_B2][4], gdA6, x, L);
     bload_img(A, SN, x, L);                            // dL = dB3 + dA9
-    baxpy_img_l2(A, c_t18[T18_B3][1], gdX, x, L, keep); bt_axpy(A, c_t18[T18_B3][2], T1);
-    bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img_l2(A, c_t18[T18_B3][4], gdA6, x, L, keep);
+    baxpy_img(A, c_t18[T18_B3][1], gdX, x, L); bt_axpy(A, c_t18[T18_B3][2], T1);
+    bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img(A, c_t18[T18_B3][4], gdA6, x, L);
     bmma<C, R, KS>(acc, A, SV, x, L);
     bload_img(A, SV, x, L);                            // L = B3 + A9
     badd_diag(A, c_t18[T18_B3][0], x, L);
-    baxpy_img_l2(A, c_t18[T18_B3][1], gX, x, L, keep); bt_axpy(A, c_t18[T18_B3][2], T0);
-    bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img_l2(A, c_t18[T18_B3][4], gA6, x, L, keep);
+    baxpy_img(A, c_t18[T18_B3][1], gX, x, L); bt_axpy(A, c_t18[T18_B3][2], T0);
+    bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img(A, c_t18[T18_B3][4], gA6, x, L);
     bmma<C, R, KS>(acc, A, SN, x, L);
     if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
     np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
     if (s > 0) {                                       // T = B2 + L A9
       bzero(acc);
       badd_diag(acc, c_t18[T18_B2][0], x, L);
-      baxpy_img_l2(acc, c_t18[T18_B2][1], gX, x, L, keep); bt_axpy(acc, c_t18[T18_B2][2], T0);
-      bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img_l2(acc, c_t18[T18_B2][4], gA6, x, L, keep);
+      baxpy_img(acc, c_t18[T18_B2][1], gX, x, L); bt_axpy(acc, c_t18[T18_B2][2], T0);
+      bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img(acc, c_t18[T18_B2][4], gA6, x, L);
       bmma<C, R, KS>(acc, A, SV, x, L);
       bstore_img_l2(gE, acc, x, L, keep);
       ++np;
@@ -1194,13 +1197,13 @@ __device__ __forceinline__ void blk_traces(const BR<C, R>& W, const BlkDev& D, c
 }
 
 template <int C, int R, int KS>
-__device__ void blk_grad_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const double* Pk, int b, int k,
-                              const Ctx& x, double* sm, uint64_t* barN, uint32_t& phN, uint32_t tm, double* scr,
-                              int* bad, double* tr, bool first, unsigned long long& nflop, const Lane& L) {
+__device__ void blk_grad_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, int b, int k, const Ctx& x,
+                              double* sm, uint64_t* bars, uint32_t& ph, uint32_t tm, double* scr, int* bad, double* tr,
+                              bool first, unsigned long long& nflop, const Lane& L) {
   const int IM = 2 * 64 * C * C;
   BR<C, R> A, acc;
-  const int np = blk_dual_expm<C, R, KS>(A, acc, B, G, Pk, b, k, x, sm, sm + IM, sm + 2 * IM, barN, phN, sm + 3 * IM,
-                                         tm, D.tstride[L.w], scr, bad, L);
+  const int np = blk_dual_expm<C, R, KS>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1], ph,
+                                         sm + 3 * IM, sm + 3 * IM + 64 * C * C, tm, D.tstride[L.w], scr, bad, L);
   if (x.rt0 == 0 && L.lane == 0) nflop += (unsigned long long)np * D.gflops[x.g];
   blk_traces<C, R>(A, D, B, b, x, tr, first, L);
 }
@@ -1214,7 +1217,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
                                                                             double* __restrict__ scratch,
                                                                             int tmem_cols, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS];
+  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];   // [0]: X_{k+1} -> SN, [1]: P_k -> SD
   __shared__ double red_tr[BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int bad_sh;
@@ -1222,7 +1225,10 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   const int ntask = D.ntask[L.w];
   for (int t = 0; t < ntask; ++t)
-    if (D.task[L.w][t].rt0 == 0 && L.lane == 0) mbar_init(&bars[D.task[L.w][t].g], 1);
+    if (D.task[L.w][t].rt0 == 0 && L.lane == 0) {
+      mbar_init(&bars[D.task[L.w][t].g][0], 1);
+      mbar_init(&bars[D.task[L.w][t].g][1], 1);
+    }
   fence_mbar_init();
   if (threadIdx.x == 0) bad_sh = 0;
   tmem_fence_before();
@@ -1236,14 +1242,20 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   uint32_t phN[BLK_MAX_TASKS] = {0, 0, 0};
   unsigned long long nflop = 0;
   double* scr_cta = scratch + (size_t)blockIdx.x * stride * BLK_GRAD_SCR;
-  for (int t = 0; t < ntask; ++t) {
-    const BlkTask T = D.task[L.w][t];
-    if (T.rt0 == 0 && L.lane == 0 && blockIdx.x < items) {
-      const int C = D.C[T.g];
-      tma_grp_img(smem + D.soff[T.g] + 2 * 2 * 64 * C * C, X_img + (size_t)blockIdx.x * stride + 2 * D.off[T.g], C,
-                  &bars[T.g]);
+  // group leaders: bulk-copy the operand images of an item (X_{k+1} -> SN, P_k -> SD)
+  auto prefetch = [&](int it) {
+    for (int t = 0; t < ntask; ++t) {
+      const BlkTask T = D.task[L.w][t];
+      if (T.rt0 == 0 && L.lane == 0 && it < items) {
+        const int C = D.C[T.g];
+        double* base = smem + D.soff[T.g];
+        fence_proxy_async();
+        tma_grp_img(base + 2 * 2 * 64 * C * C, X_img + (size_t)it * stride + 2 * D.off[T.g], C, &bars[T.g][0]);
+        tma_grp_img(base, P_img + (size_t)it * stride + 2 * D.off[T.g], C, &bars[T.g][1]);
+      }
     }
-  }
+  };
+  prefetch(blockIdx.x);
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
     for (int t = 0; t < ntask; ++t) {
@@ -1251,20 +1263,11 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
       const Ctx x = ctx_of(D, T);
       double* sm = smem + D.soff[x.g];
       double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
-      const double* Pk = P_img + (size_t)item * stride + 2 * x.off;
-      BLK_DISPATCH(D.C[x.g], x.ks, blk_grad_task, D, B, G, Pk, b, k, x, sm, &bars[x.g], phN[t], tm, scr, &bad_sh,
+      BLK_DISPATCH(D.C[x.g], x.ks, blk_grad_task, D, B, G, b, k, x, sm, bars[x.g], phN[t], tm, scr, &bad_sh,
                    red_tr + L.w * BLK_TR_MAX, t == 0, nflop, L);
     }
-    __syncthreads();   // every task done with this item: SN regions free, red_tr complete
-    for (int t = 0; t < ntask; ++t) {
-      const BlkTask T = D.task[L.w][t];
-      if (T.rt0 == 0 && L.lane == 0 && item + (int)gridDim.x < items) {
-        const int C = D.C[T.g];
-        fence_proxy_async();
-        tma_grp_img(smem + D.soff[T.g] + 2 * 2 * 64 * C * C,
-                    X_img + (size_t)(item + gridDim.x) * stride + 2 * D.off[T.g], C, &bars[T.g]);
-      }
-    }
+    __syncthreads();   // every task done with this item: SN / SD regions free, red_tr complete
+    prefetch(item + gridDim.x);
     if (threadIdx.x < K) {
       double s = 0.0;
       for (int w = 0; w < D.nwarps; ++w) s += red_tr[w * BLK_TR_MAX + threadIdx.x];
@@ -1322,6 +1325,7 @@ int grp_smem_doubles(BlkDev& D, int (*per)(int)) {
   return o;
 }
 int per3(int C) { return grp3_doubles(C); }
+int per_grad(int C) { return grp3_doubles(C) + 4 * 2 * 64 * C * C; }
 int per_pair(int C) { return 2 * 64 * C * C; }
 int per_chain(int C) { return 2 * 2 * 64 * C * C; }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
@@ -1387,7 +1391,7 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
 // finished and double the tail
 static int blk_grad_grid(const BlkDev& D) {
   BlkDev tmp = D;
-  const size_t bytes = (size_t)grp_smem_doubles(tmp, per3) * 8;
+  const size_t bytes = (size_t)grp_smem_doubles(tmp, per_grad) * 8;
   cudaFuncAttributes fa;
   int per_sm = 1;
   if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess && fa.numRegs > 0) {
@@ -1413,7 +1417,7 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
                                    double* scratch, cudaStream_t st) {
   BlkDev D;
   if (!to_dev(p, D)) return cudaErrorInvalidValue;
-  const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per_grad) * 8;
   static size_t attr = 0;
   cudaError_t e = set_smem((const void*)k_blk_grad_slices, bytes, attr);
   if (e != cudaSuccess) return e;
