@@ -304,12 +304,24 @@ typedef struct {
     int row0[QAL_BLK_MAX_GROUPS];       /* first packed row of group g                        */
     int off[QAL_BLK_MAX_GROUPS];        /* complex offset of group g inside a packed matrix   */
     double flops[QAL_BLK_MAX_GROUPS];   /* algorithmic flops of one product of group g:
-                                           8 sum_{components} s^3 (padding excluded)          */
+                                           8 sum s^3 over complex components, 2 sum s^3 over
+                                           real ones (padding excluded)                       */
     int perm[QAL_BLK_MAX_ROWS];         /* packed row -> natural index, -1 = padding          */
     int weight[QAL_BLK_MAX_ROWS];       /* 0 padding, 1 self-mirror component (or mirror
                                            off), 2 component whose mirror is implied         */
     int inv[64];                        /* natural index -> packed row, -1 = not stored       */
     int comp[64];                       /* natural index -> component id                      */
+    /* Self-mirrored components (s(R) in the component for every R, e.g. coherence order 0) are
+     * stored in the basis of vectorised Hermitian matrices, vec = T x with columns e_R (R = s(R))
+     * and (e_R + e_sR)/sqrt2, i (e_R - e_sR)/sqrt2 (R < s(R)).  T is unitary and every
+     * Hermiticity-preserving map is real there, so these groups run in real arithmetic
+     * (1 real multiplication per product instead of 4).  Packed entries of a real group are
+     * (M'[r][c], 0) with M' = T^dag M T.                                                    */
+    int real[QAL_BLK_MAX_GROUPS];       /* 1: group g holds real-basis components              */
+    int rtype[QAL_BLK_MAX_ROWS];        /* 0 complex row, 1 real diagonal e_R, 2 pair column a,
+                                           3 pair column b (perm = the pair's smaller index)  */
+    int ncode[64];                      /* natural index: 0 complex group, 1 real diagonal,
+                                           2 pair representative R < s(R), 3 pair mirror      */
 } qal_block_plan;
 
 /*

@@ -68,6 +68,9 @@ struct BlkDev {
   signed char inv[64];                     // natural index -> packed row (-1 not stored)
   signed char comp[64];                    // natural index -> component
   unsigned long long gflops[QAL_BLK_MAX_GROUPS];   // algorithmic flops of one product of group g
+  unsigned char real[QAL_BLK_MAX_GROUPS];  // group stored in the real (Hermitian) basis
+  unsigned char rtype[QAL_BLK_MAX_ROWS];   // 0 complex row, 1 real diag, 2 real pair "a", 3 real pair "b"
+  unsigned char ncode[64];                 // natural index: 0 complex, 1 real diag, 2 real pair rep, 3 real mirror
 };
 
 // warp roles: C = 3 groups -> 3 warps (one strip each); C <= 2 groups -> whole group on one
@@ -85,6 +88,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
     D.off[g] = p.off[g];
     D.row0[g] = p.row0[g];
     D.gflops[g] = (unsigned long long)p.flops[g];
+    D.real[g] = (unsigned char)p.real[g];
   }
   int w = 0, heavy = 0;
   for (int g = 0; g < p.ngroups; ++g)
@@ -130,7 +134,10 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
   int qused[4] = {0, 0, 0, 0};
   for (int v = 0; v < w; ++v) {
     int st = 8;
-    for (int t = 0; t < D.ntask[v]; ++t) st = std::max(st, D.task[v][t].R * 8 * D.C[D.task[v][t].g]);
+    for (int t = 0; t < D.ntask[v]; ++t) {
+      const int g = D.task[v][t].g;
+      st = std::max(st, D.task[v][t].R * (D.real[g] ? 4 : 8) * D.C[g]);
+    }
     D.tstride[v] = st;
     D.tcol[v] = qused[v & 3];
     qused[v & 3] += 4 * st;
@@ -142,10 +149,12 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
   for (int r = 0; r < QAL_BLK_MAX_ROWS; ++r) {
     D.perm[r] = (signed char)(r < p.nrows ? p.perm[r] : -1);
     D.weight[r] = (unsigned char)(r < p.nrows ? p.weight[r] : 0);
+    D.rtype[r] = (unsigned char)(r < p.nrows ? p.rtype[r] : 0);
   }
   for (int i = 0; i < 64; ++i) {
     D.inv[i] = (signed char)(i < p.n ? p.inv[i] : -1);
     D.comp[i] = (signed char)(i < p.n ? p.comp[i] : -1);
+    D.ncode[i] = (unsigned char)(i < p.n ? p.ncode[i] : 0);
   }
   return true;
 }
@@ -172,66 +181,76 @@ __device__ __forceinline__ void grp_sync(const Ctx& x) {
   }
 }
 
-// the warp roles every kernel instantiates: (C, R, KS) = (3, 1, 5|6), (2, 2, 4), (1, 1, 2)
+// the warp roles every kernel instantiates: (C, R, KS) = (3, 1, 5|6), (2, 2, 4), (1, 1, 2), each complex or
+// real (RE: a self-mirrored component in the Hermitian basis, 1 real MMA per step instead of 4)
 // (KS = k-steps of the products; the 20-block runs with K = 20: 5 k-steps)
-#define BLK_DISPATCH(CC, KSV, FN, ...)                    \
+#define BLK_DISPATCH(CC, KSV, RV, FN, ...)                \
   do {                                                    \
-    if ((CC) == 3) {                                      \
-      if ((KSV) <= 5) FN<3, 1, 5>(__VA_ARGS__);           \
-      else FN<3, 1, 6>(__VA_ARGS__);                      \
-    } else if ((CC) == 2) FN<2, 2, 4>(__VA_ARGS__);       \
-    else FN<1, 1, 2>(__VA_ARGS__);                        \
+    if ((RV)) {                                           \
+      if ((CC) == 3) {                                    \
+        if ((KSV) <= 5) FN<3, 1, 5, true>(__VA_ARGS__);   \
+        else FN<3, 1, 6, true>(__VA_ARGS__);              \
+      } else if ((CC) == 2) FN<2, 2, 4, true>(__VA_ARGS__); \
+      else FN<1, 1, 2, true>(__VA_ARGS__);                \
+    } else {                                              \
+      if ((CC) == 3) {                                    \
+        if ((KSV) <= 5) FN<3, 1, 5, false>(__VA_ARGS__);  \
+        else FN<3, 1, 6, false>(__VA_ARGS__);             \
+      } else if ((CC) == 2) FN<2, 2, 4, false>(__VA_ARGS__); \
+      else FN<1, 1, 2, false>(__VA_ARGS__);               \
+    }                                                     \
   } while (0)
 
 // ------------------------------------------------------------------ P-wide strips, R per warp
 // Strip r (row tile rt0 + r) of a P x P block in the A-fragment layout:
 //   s.re/im[r][i] = M[8 (rt0 + r) + g][4 i + t],  i < 2C.
-template <int C, int R>
+template <int C, int R, bool RE>
 struct BR {
-  double re[R][2 * C], im[R][2 * C];
+  double re[R][2 * C];
+  double im[R][RE ? 1 : 2 * C];   // RE: a real block (self-mirrored component in the real basis), im unused
 };
 
-template <int C, int R>
-__device__ __forceinline__ void bzero(BR<C, R>& s) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bzero(BR<C, R, RE>& s) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) { s.re[r][i] = 0.0; s.im[r][i] = 0.0; }
+    for (int i = 0; i < 2 * C; ++i) { s.re[r][i] = 0.0; if constexpr (!RE) s.im[r][i] = 0.0; }
 }
-template <int C, int R>
-__device__ __forceinline__ void bcopy(BR<C, R>& d, const BR<C, R>& s) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bcopy(BR<C, R, RE>& d, const BR<C, R, RE>& s) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) { d.re[r][i] = s.re[r][i]; d.im[r][i] = s.im[r][i]; }
+    for (int i = 0; i < 2 * C; ++i) { d.re[r][i] = s.re[r][i]; if constexpr (!RE) d.im[r][i] = s.im[r][i]; }
 }
-template <int C, int R>
-__device__ __forceinline__ void baxpy(BR<C, R>& acc, double a, const BR<C, R>& x) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void baxpy(BR<C, R, RE>& acc, double a, const BR<C, R, RE>& x) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i) {
       acc.re[r][i] = fma(a, x.re[r][i], acc.re[r][i]);
-      acc.im[r][i] = fma(a, x.im[r][i], acc.im[r][i]);
+      if constexpr (!RE) acc.im[r][i] = fma(a, x.im[r][i], acc.im[r][i]);
     }
 }
-template <int C, int R>
-__device__ __forceinline__ void bscale(BR<C, R>& s, double a) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bscale(BR<C, R, RE>& s, double a) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) { s.re[r][i] *= a; s.im[r][i] *= a; }
+    for (int i = 0; i < 2 * C; ++i) { s.re[r][i] *= a; if constexpr (!RE) s.im[r][i] *= a; }
 }
-template <int C, int R>
-__device__ __forceinline__ void badd_diag(BR<C, R>& s, double a, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void badd_diag(BR<C, R, RE>& s, double a, const Ctx& x, const Lane& L) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i)
       if (8 * (x.rt0 + r) + L.g == 4 * i + L.t) s.re[r][i] += a;
 }
-template <int C, int R>
-__device__ __forceinline__ void bset_identity(BR<C, R>& s, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bset_identity(BR<C, R, RE>& s, const Ctx& x, const Lane& L) {
   bzero(s);
   badd_diag(s, 1.0, x, L);
 }
@@ -244,8 +263,8 @@ __device__ __forceinline__ int bpair_off(int row, const Lane& L, int j) {
   const int swz = (C % 2 == 0) ? ((L.g & 1) << 3) : 0;
   return row * (8 * C) + ((8 * j + 2 * L.t) ^ swz);
 }
-template <int C, int R>
-__device__ __forceinline__ void bload_img(BR<C, R>& s, const double* __restrict__ img, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bload_img(BR<C, R, RE>& s, const double* __restrict__ img, const Ctx& x, const Lane& L) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -253,13 +272,15 @@ __device__ __forceinline__ void bload_img(BR<C, R>& s, const double* __restrict_
     for (int j = 0; j < C; ++j) {
       const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
       const double2 a = *reinterpret_cast<const double2*>(img + o);
-      const double2 b = *reinterpret_cast<const double2*>(img + PL + o);
       s.re[r][2 * j] = a.x; s.re[r][2 * j + 1] = a.y;
-      s.im[r][2 * j] = b.x; s.im[r][2 * j + 1] = b.y;
+      if constexpr (!RE) {
+        const double2 b = *reinterpret_cast<const double2*>(img + PL + o);
+        s.im[r][2 * j] = b.x; s.im[r][2 * j + 1] = b.y;
+      }
     }
 }
-template <int C, int R>
-__device__ __forceinline__ void bstore_img(double* __restrict__ img, const BR<C, R>& s, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bstore_img(double* __restrict__ img, const BR<C, R, RE>& s, const Ctx& x, const Lane& L) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -267,12 +288,13 @@ __device__ __forceinline__ void bstore_img(double* __restrict__ img, const BR<C,
     for (int j = 0; j < C; ++j) {
       const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
       *reinterpret_cast<double2*>(img + o) = make_double2(s.re[r][2 * j], s.re[r][2 * j + 1]);
-      *reinterpret_cast<double2*>(img + PL + o) = make_double2(s.im[r][2 * j], s.im[r][2 * j + 1]);
+      if constexpr (!RE)
+        *reinterpret_cast<double2*>(img + PL + o) = make_double2(s.im[r][2 * j], s.im[r][2 * j + 1]);
     }
 }
 // acc += a * image (no temporary strip kept live)
-template <int C, int R>
-__device__ __forceinline__ void baxpy_img(BR<C, R>& acc, double a, const double* __restrict__ img, const Ctx& x,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void baxpy_img(BR<C, R, RE>& acc, double a, const double* __restrict__ img, const Ctx& x,
                                           const Lane& L) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
@@ -281,14 +303,16 @@ __device__ __forceinline__ void baxpy_img(BR<C, R>& acc, double a, const double*
     for (int j = 0; j < C; ++j) {
       const int o = bpair_off<C>(8 * (x.rt0 + r) + L.g, L, j);
       const double2 u = *reinterpret_cast<const double2*>(img + o);
-      const double2 v = *reinterpret_cast<const double2*>(img + PL + o);
       acc.re[r][2 * j] = fma(a, u.x, acc.re[r][2 * j]); acc.re[r][2 * j + 1] = fma(a, u.y, acc.re[r][2 * j + 1]);
-      acc.im[r][2 * j] = fma(a, v.x, acc.im[r][2 * j]); acc.im[r][2 * j + 1] = fma(a, v.y, acc.im[r][2 * j + 1]);
+      if constexpr (!RE) {
+        const double2 v = *reinterpret_cast<const double2*>(img + PL + o);
+        acc.im[r][2 * j] = fma(a, v.x, acc.im[r][2 * j]); acc.im[r][2 * j + 1] = fma(a, v.y, acc.im[r][2 * j + 1]);
+      }
     }
 }
 // global image with an L2 policy
-template <int C, int R>
-__device__ __forceinline__ void bload_img_l2(BR<C, R>& s, const double* __restrict__ img, const Ctx& x, const Lane& L,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bload_img_l2(BR<C, R, RE>& s, const double* __restrict__ img, const Ctx& x, const Lane& L,
                                              uint64_t pol) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
@@ -299,13 +323,14 @@ __device__ __forceinline__ void bload_img_l2(BR<C, R>& s, const double* __restri
       asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                    : "=d"(s.re[r][2 * j]), "=d"(s.re[r][2 * j + 1])
                    : "l"(img + o), "l"(pol));
-      asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                   : "=d"(s.im[r][2 * j]), "=d"(s.im[r][2 * j + 1])
-                   : "l"(img + PL + o), "l"(pol));
+      if constexpr (!RE)
+        asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(s.im[r][2 * j]), "=d"(s.im[r][2 * j + 1])
+                     : "l"(img + PL + o), "l"(pol));
     }
 }
-template <int C, int R>
-__device__ __forceinline__ void bstore_img_l2(double* __restrict__ img, const BR<C, R>& s, const Ctx& x,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bstore_img_l2(double* __restrict__ img, const BR<C, R, RE>& s, const Ctx& x,
                                               const Lane& L, uint64_t pol) {
   constexpr int PL = 64 * C * C;
 #pragma unroll
@@ -316,41 +341,44 @@ __device__ __forceinline__ void bstore_img_l2(double* __restrict__ img, const BR
       asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + o), "d"(s.re[r][2 * j]),
                    "d"(s.re[r][2 * j + 1]), "l"(pol)
                    : "memory");
-      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + PL + o), "d"(s.im[r][2 * j]),
-                   "d"(s.im[r][2 * j + 1]), "l"(pol)
-                   : "memory");
+      if constexpr (!RE)
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(img + PL + o), "d"(s.im[r][2 * j]),
+                     "d"(s.im[r][2 * j + 1]), "l"(pol)
+                     : "memory");
     }
 }
-template <int C, int R>
-__device__ __forceinline__ void baxpy_img_l2(BR<C, R>& acc, double a, const double* __restrict__ img, const Ctx& x,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void baxpy_img_l2(BR<C, R, RE>& acc, double a, const double* __restrict__ img, const Ctx& x,
                                              const Lane& L, uint64_t pol) {
   if (a == 0.0) return;
-  BR<C, R> y;
+  BR<C, R, RE> y;
   bload_img_l2(y, img, x, L, pol);
   baxpy(acc, a, y);
 }
 // natural row-major P x P complex block <-> strips
-template <int C, int R>
-__device__ __forceinline__ void bload_nat(BR<C, R>& s, const double2* __restrict__ M, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bload_nat(BR<C, R, RE>& s, const double2* __restrict__ M, const Ctx& x, const Lane& L) {
   constexpr int P = 8 * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i) {
       const double2 v = __ldg(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t);
-      s.re[r][i] = v.x; s.im[r][i] = v.y;
+      s.re[r][i] = v.x;
+      if constexpr (!RE) s.im[r][i] = v.y;
     }
 }
-template <int C, int R>
-__device__ __forceinline__ void bstore_nat(double2* __restrict__ M, const BR<C, R>& s, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bstore_nat(double2* __restrict__ M, const BR<C, R, RE>& s, const Ctx& x, const Lane& L) {
   constexpr int P = 8 * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) M[(8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t] = make_double2(s.re[r][i], s.im[r][i]);
+    for (int i = 0; i < 2 * C; ++i)
+      M[(8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t] = make_double2(s.re[r][i], RE ? 0.0 : s.im[r][i]);
 }
-template <int C, int R>
-__device__ __forceinline__ void baxpy_nat(BR<C, R>& X, double a, const double2* __restrict__ M, const Ctx& x,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void baxpy_nat(BR<C, R, RE>& X, double a, const double2* __restrict__ M, const Ctx& x,
                                           const Lane& L) {
   constexpr int P = 8 * C;
   const uint64_t keep = l2_evict_last();   // the basis is shared by every CTA
@@ -363,15 +391,15 @@ __device__ __forceinline__ void baxpy_nat(BR<C, R>& X, double a, const double2* 
                    : "=d"(vx), "=d"(vy)
                    : "l"(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t), "l"(keep));
       X.re[r][i] = fma(a, vx, X.re[r][i]);
-      X.im[r][i] = fma(a, vy, X.im[r][i]);
+      if constexpr (!RE) X.im[r][i] = fma(a, vy, X.im[r][i]);
     }
 }
 
 // acc += A * B on the FP64 tensor cores: A = strips (registers), B = image (shared).
 // 4 real MMAs per complex 8x8x4 step (qal_dev.cuh mma_acc_4m); only the first KS k-steps
 // (rows of B that are not padding); the B fragments of a k-step serve all R strips.
-template <int C, int R, int KS>
-__device__ __forceinline__ void bmma(BR<C, R>& acc, const BR<C, R>& a, const double* __restrict__ Bs, const Ctx& x,
+template <int C, int R, int KS, bool RE>
+__device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, const double* __restrict__ Bs, const Ctx& x,
                                      const Lane& L) {
   static_assert(KS >= 1 && KS <= 2 * C, "k-steps");
   constexpr int P = 8 * C, PL = P * P;
@@ -382,7 +410,7 @@ __device__ __forceinline__ void bmma(BR<C, R>& acc, const BR<C, R>& a, const dou
   for (int j = 0; j < C; ++j) {
     const uint32_t p = base + 8u * (8 * (j ^ swz));
     br[0][j] = lds_v(p);
-    bi[0][j] = lds_v(p + 8u * PL);
+    if constexpr (!RE) bi[0][j] = lds_v(p + 8u * PL);
   }
 #pragma unroll
   for (int q = 0; q < KS; ++q) {
@@ -393,18 +421,23 @@ __device__ __forceinline__ void bmma(BR<C, R>& acc, const BR<C, R>& a, const dou
         for (int j = 0; j < C; ++j) {
           const uint32_t p = base + 8u * ((q + 1) * 4 * P + 8 * (j ^ swz));
           br[cur ^ 1][j] = lds_v(p);
-          bi[cur ^ 1][j] = lds_v(p + 8u * PL);
+          if constexpr (!RE) bi[cur ^ 1][j] = lds_v(p + 8u * PL);
         }
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
+        if constexpr (RE) {          // real block: 1 MMA per 8x8x4 step
 #pragma unroll
-        for (int j = 0; j < C; ++j) {
-          dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
-          dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], nai, bi[cur][j]);
-          dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ar, bi[cur][j]);
-          dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ai, br[cur][j]);
+          for (int j = 0; j < C; ++j) dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], a.re[r][q], br[cur][j]);
+        } else {
+          const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
+            dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], nai, bi[cur][j]);
+            dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ar, bi[cur][j]);
+            dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ai, br[cur][j]);
+          }
         }
       }
     }
@@ -414,14 +447,14 @@ __device__ __forceinline__ void bmma(BR<C, R>& acc, const BR<C, R>& a, const dou
 
 // ||X||_1 of the group's block (max column sum of |x|), fixed order.  red: >= P * P doubles of
 // the group's region (partial column sums per row tile).  One group barrier.
-template <int C, int R>
-__device__ __forceinline__ double bnorm1(const BR<C, R>& s, double* red, const Ctx& x, const Lane& L) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ double bnorm1(const BR<C, R, RE>& s, double* red, const Ctx& x, const Lane& L) {
   constexpr int P = 8 * C;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     double cs[2 * C];
 #pragma unroll
-    for (int i = 0; i < 2 * C; ++i) cs[i] = hypot(s.re[r][i], s.im[r][i]);
+    for (int i = 0; i < 2 * C; ++i) cs[i] = RE ? fabs(s.re[r][i]) : hypot(s.re[r][i], s.im[r][i]);
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
 #pragma unroll
@@ -451,8 +484,8 @@ __device__ __forceinline__ double bnorm1(const BR<C, R>& s, double* red, const C
 }
 
 // Omega_k strips of the group from the packed generator basis (a1-a3, as build_omega)
-template <int C, int R>
-__device__ __forceinline__ void bbuild_omega(BR<C, R>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bbuild_omega(BR<C, R, RE>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
                                              const Ctx& x, const Lane& L) {
   const int J = B.J;
   const int nodes = (G.mode == 1) ? 2 : 1;
@@ -530,43 +563,45 @@ __device__ __forceinline__ void tm_ld_plane(uint32_t addr, uint32_t* v) {
   if (C >= 2) tm_ld<8>(addr, v);
   if (C == 3) tm_ld<4>(addr + 8, v + 8);
 }
-template <int C, int R>
-__device__ __forceinline__ void bt_store(uint32_t addr, const BR<C, R>& s) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bt_store(uint32_t addr, const BR<C, R, RE>& s) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    tm_st_plane<C>(addr + 8 * C * r, s.re[r]);
-    tm_st_plane<C>(addr + 8 * C * r + 4 * C, s.im[r]);
+    tm_st_plane<C>(addr + (RE ? 4 : 8) * C * r, s.re[r]);
+    if constexpr (!RE) tm_st_plane<C>(addr + 8 * C * r + 4 * C, s.im[r]);
   }
   tmem_wait_st();
 }
-template <int C, int R>
-__device__ __forceinline__ void bt_load(BR<C, R>& s, uint32_t addr) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bt_load(BR<C, R, RE>& s, uint32_t addr) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t v[4 * C], w[4 * C];
-    tm_ld_plane<C>(addr + 8 * C * r, v);
-    tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
+    tm_ld_plane<C>(addr + (RE ? 4 : 8) * C * r, v);
+    if constexpr (!RE) tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
     tmem_wait_ld();
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i) {
       s.re[r][i] = __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i]));
-      s.im[r][i] = __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i]));
+      if constexpr (!RE) s.im[r][i] = __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i]));
     }
   }
 }
-template <int C, int R>
-__device__ __forceinline__ void bt_axpy(BR<C, R>& acc, double a, uint32_t addr) {
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bt_axpy(BR<C, R, RE>& acc, double a, uint32_t addr) {
   if (a == 0.0) return;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t v[4 * C], w[4 * C];
-    tm_ld_plane<C>(addr + 8 * C * r, v);
-    tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
+    tm_ld_plane<C>(addr + (RE ? 4 : 8) * C * r, v);
+    if constexpr (!RE) tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
     tmem_wait_ld();
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i) {
       acc.re[r][i] = fma(a, __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i])), acc.re[r][i]);
-      acc.im[r][i] = fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[r][i]);
+      if constexpr (!RE)
+        acc.im[r][i] =
+            fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[r][i]);
     }
   }
 }
@@ -586,12 +621,12 @@ __device__ __forceinline__ void blk_tmem_dealloc(uint32_t base, int cols) {
 // U = expm(X 2^s): the T8 / T18 schemes of qal_slice.cuh with the powers in TMEM slots
 // tm + {0, 32, 64}; X's strips in A and its image in SX; SX4 = the group's operand image.
 // Result in A.  Returns the products done.
-template <int C, int R, int KS>
-__device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, double* SX, double* SX4, uint32_t tm,
+template <int C, int R, int KS, bool RE>
+__device__ __forceinline__ int bexpm(BR<C, R, RE>& A, BR<C, R, RE>& acc, int m, int s, double* SX, double* SX4, uint32_t tm,
                                      uint32_t ts, const Ctx& x, const Lane& L) {
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts;
   int prods;
-  bzero(acc); bmma<C, R, KS>(acc, A, SX, x, L);                  // A2 = X X
+  bzero(acc); bmma<C, R, KS, RE>(acc, A, SX, x, L);                  // A2 = X X
   bt_store(T0, acc);
   if (m == 8) {
     bzero(A);                                          // W = c1 X + c2 A2 (shared)
@@ -600,7 +635,7 @@ __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, d
     bstore_img(SX4, A, x, L);
     bcopy(A, acc);                                     // A = A2
     grp_sync(x);
-    bzero(acc); bmma<C, R, KS>(acc, A, SX4, x, L);               // Y = A2 W
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SX4, x, L);               // Y = A2 W
     bt_store(T1, acc);
     grp_sync(x);                                       // reads of SX4 (W) done
     baxpy(acc, c_t8[4], A);                            // R = Y + c5 A2 (shared)
@@ -614,17 +649,17 @@ __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, d
     bt_axpy(acc, c_t8[6], T0);
     baxpy_img(acc, 1.0, SX, x, L);
     badd_diag(acc, 1.0, x, L);
-    bmma<C, R, KS>(acc, A, SX4, x, L);
+    bmma<C, R, KS, RE>(acc, A, SX4, x, L);
     bcopy(A, acc);
     prods = 3;
   } else {
     bcopy(A, acc);
-    bzero(acc); bmma<C, R, KS>(acc, A, SX, x, L);                // A3 = A2 X
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SX, x, L);                // A3 = A2 X
     bt_store(T1, acc);
     bstore_img(SX4, acc, x, L);
     bcopy(A, acc);
     grp_sync(x);
-    bzero(acc); bmma<C, R, KS>(acc, A, SX4, x, L);               // A6 = A3 A3
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SX4, x, L);               // A6 = A3 A3
     bt_store(T2, acc);
     baxpy_img(acc, c_t18[T18_B5][1], SX, x, L);        // B5 = e1 X + e2 A2 + A6
     bt_axpy(acc, c_t18[T18_B5][2], T0);
@@ -641,7 +676,7 @@ __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, d
     bt_axpy(acc, c_t18[T18_B4][3], T1);
     bt_axpy(acc, c_t18[T18_B4][4], T2);
     grp_sync(x);                                       // B5 image complete
-    bmma<C, R, KS>(acc, A, SX4, x, L);                           // A9 = B4 + B1 B5
+    bmma<C, R, KS, RE>(acc, A, SX4, x, L);                           // A9 = B4 + B1 B5
     grp_sync(x);                                       // reads of SX4 (B5) done
     bstore_img(SX4, acc, x, L);
     bcopy(A, acc);                                     // L = B3 + A9
@@ -657,7 +692,7 @@ __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, d
     bt_axpy(acc, c_t18[T18_B2][3], T1);
     bt_axpy(acc, c_t18[T18_B2][4], T2);
     grp_sync(x);                                       // A9 image complete
-    bmma<C, R, KS>(acc, A, SX4, x, L);
+    bmma<C, R, KS, RE>(acc, A, SX4, x, L);
     bcopy(A, acc);
     prods = 5;
   }
@@ -665,7 +700,7 @@ __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, d
     grp_sync(x);
     bstore_img(SX4, A, x, L);
     grp_sync(x);
-    bzero(acc); bmma<C, R, KS>(acc, A, SX4, x, L);
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SX4, x, L);
     bcopy(A, acc);
     ++prods;
   }
@@ -676,7 +711,7 @@ __device__ __forceinline__ int bexpm(BR<C, R>& A, BR<C, R>& acc, int m, int s, d
 __host__ __device__ constexpr int grp3_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
 
 // ------------------------------------------------------------------ forward fold (a1-a5)
-template <int C, int R, int KS>
+template <int C, int R, int KS, bool RE>
 __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
                              const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long& nflop,
                              const Lane& L) {
@@ -688,7 +723,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   const int nchunk = G.count / O.chunk;
   const int b = item / nchunk, c = item % nchunk;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
-  BR<C, R> A, acc;
+  BR<C, R, RE> A, acc;
   for (int kk = 0; kk < O.chunk; ++kk) {
     const int k = c * O.chunk + kk;
     bbuild_omega(A, B, G, b, k, x, L);
@@ -699,7 +734,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     bscale(A, ldexp(1.0, -s));
     bstore_img(SX, A, x, L);
     grp_sync(x);
-    const int np = bexpm<C, R, KS>(A, acc, m, s, SX, SX4, tm, ts, x, L);
+    const int np = bexpm<C, R, KS, RE>(A, acc, m, s, SX, SX4, tm, ts, x, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const size_t slot = (size_t)b * G.count + k;
     if (O.U_img) bstore_img_l2(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
@@ -711,7 +746,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
         }
         bstore_img(SP, A, x, L);
       } else {
-        bzero(acc); bmma<C, R, KS>(acc, A, SP, x, L);           // P <- U_k P
+        bzero(acc); bmma<C, R, KS, RE>(acc, A, SP, x, L);           // P <- U_k P
         bcopy(A, acc);
         if (leader) nflop += D.gflops[x.g];
         grp_sync(x);
@@ -744,7 +779,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis 
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], x.ks, blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh, nflop, L);
+    BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh, nflop, L);
   }
   tmem_fence_before();
   __syncthreads();
@@ -758,16 +793,16 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis 
 // ------------------------------------------------------------------ pair products (tree level)
 // out[b][i] = in[b][2i+1] in[b][2i] per group (later factor on the LEFT, Eq. 15); an odd last
 // element is carried.  One CTA per output; packed natural in / out.
-template <int C, int R, int KS>
+template <int C, int R, int KS, bool RE>
 __device__ void blk_pair_task(const double2* lhs, const double2* rhs, double2* out, const Ctx& x, double* sm,
                               const Lane& L) {
-  BR<C, R> A, acc;
+  BR<C, R, RE> A, acc;
   bload_nat(A, rhs + x.off, x, L);           // earlier factor as the B image
   bstore_img(sm, A, x, L);
   bload_nat(A, lhs + x.off, x, L);
   grp_sync(x);
   bzero(acc);
-  bmma<C, R, KS>(acc, A, sm, x, L);
+  bmma<C, R, KS, RE>(acc, A, sm, x, L);
   bstore_nat(out + x.off, acc, x, L);
 }
 
@@ -792,10 +827,64 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_tree_level(BlkDev D,
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], x.ks, blk_pair_task, lhs, rhs, dst, x, sm, L);
+    BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_pair_task, lhs, rhs, dst, x, sm, L);
     if (x.rt0 == 0 && L.lane == 0) nflop += D.gflops[x.g];
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
+}
+
+// ------------------------------------------------------------------ real (Hermitian) basis of self-mirrored components
+// A self-mirrored component (s(R) in the component for every R) is stored in the basis of vectorised
+// Hermitian matrices, vec = T x: a diagonal index R = s(R) gives column e_R; a pair R < s(R) gives the
+// columns a = (e_R + e_sR)/sqrt2 and b = i (e_R - e_sR)/sqrt2.  T is unitary and every map that
+// preserves Hermiticity (Omega_k, U_k, P_k, X_k, S_V, the basis L0, L_j, commutators) is REAL in it:
+// M' = T^dag M T.  Complex rows (rtype 0) use T = I.
+struct TTerms {
+  int n;
+  int R[2];
+  double tr[2], ti[2];   // T[R[i]][row] = tr + i ti
+};
+__device__ __forceinline__ int mirror_index(int R, int d) { return (R / d) + d * (R % d); }
+__device__ __forceinline__ TTerms row_terms(const BlkDev& D, int grow) {
+  TTerms t;
+  const int R = D.perm[grow];
+  const double h = 0.70710678118654752440;
+  t.R[0] = R;
+  t.tr[0] = 1.0;
+  t.ti[0] = 0.0;
+  t.n = (R < 0) ? 0 : 1;
+  if (R >= 0 && D.rtype[grow] >= 2) {
+    t.n = 2;
+    t.R[1] = mirror_index(R, D.d);
+    if (D.rtype[grow] == 2) { t.tr[0] = h; t.tr[1] = h; t.ti[1] = 0.0; }
+    else { t.tr[0] = 0.0; t.ti[0] = h; t.tr[1] = 0.0; t.ti[1] = -h; }
+  }
+  return t;
+}
+// M'[r][c] = sum conj(T[R][r]) M[R][C] T[C][c] over the natural terms of packed rows r, c (global rows)
+__device__ __forceinline__ double2 to_packed(const BlkDev& D, int gr, int gc, const double2* __restrict__ M) {
+  const TTerms a = row_terms(D, gr), b = row_terms(D, gc);
+  double re = 0.0, im = 0.0;
+  for (int i = 0; i < a.n; ++i)
+    for (int j = 0; j < b.n; ++j) {
+      const double2 m = M[a.R[i] * 64 + b.R[j]];
+      // conj(ta) * m * tb
+      const double xr = a.tr[i] * m.x + a.ti[i] * m.y, xi = a.tr[i] * m.y - a.ti[i] * m.x;
+      re += xr * b.tr[j] - xi * b.ti[j];
+      im += xr * b.ti[j] + xi * b.tr[j];
+    }
+  return make_double2(re, im);
+}
+// rows of natural index R in a real group and T[R][row]: returns the count (0, 1 or 2)
+__device__ __forceinline__ int nat_terms(const BlkDev& D, int R, int* rows, double* tr, double* ti) {
+  const int code = D.ncode[R];
+  const double h = 0.70710678118654752440;
+  if (code == 1) { rows[0] = D.inv[R]; tr[0] = 1.0; ti[0] = 0.0; return 1; }
+  int a = (code == 2) ? D.inv[R] : D.inv[mirror_index(R, D.d)];
+  if (a < 0) return 0;
+  rows[0] = a; tr[0] = h; ti[0] = 0.0;
+  rows[1] = a + 1; tr[1] = 0.0; ti[1] = (code == 2) ? h : -h;
+  return 2;
 }
 
 // ------------------------------------------------------------------ pack / unpack / check
@@ -822,7 +911,12 @@ __global__ void k_blk_pack(BlkDev D, int count, const double2* __restrict__ nat,
     const int P = 8 * D.C[g], loc = idx - D.off[g];
     const int r = loc / P, c = loc % P;
     const int R = D.perm[D.row0[g] + r], Cc = D.perm[D.row0[g] + c];
-    dst[idx] = (R >= 0 && Cc >= 0) ? src[R * 64 + Cc] : make_double2(0.0, 0.0);
+    if (D.real[g]) {
+      const double2 v = (R >= 0 && Cc >= 0) ? to_packed(D, D.row0[g] + r, D.row0[g] + c, src) : make_double2(0.0, 0.0);
+      dst[idx] = make_double2(v.x, 0.0);   // real by Hermiticity preservation (imaginary part is rounding)
+    } else {
+      dst[idx] = (R >= 0 && Cc >= 0) ? src[R * 64 + Cc] : make_double2(0.0, 0.0);
+    }
   }
 }
 
@@ -851,7 +945,23 @@ __global__ void k_blk_unpack(BlkDev D, int count, const double2* __restrict__ pa
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 4096; idx += gridDim.x * blockDim.x) {
     const int R = idx >> 6, Cc = idx & 63;
     double2 v = make_double2(0.0, 0.0);
-    if (D.comp[R] == D.comp[Cc]) {
+    if (D.comp[R] == D.comp[Cc] && D.ncode[R] != 0) {   // real group: M = T M' T^dag
+      int rr[2], cc[2];
+      double ar[2], ai[2], br[2], bi[2];
+      const int na = nat_terms(D, R, rr, ar, ai), nb = nat_terms(D, Cc, cc, br, bi);
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < na; ++i)
+        for (int j = 0; j < nb; ++j) {
+          const int g = group_of_row(D, rr[i]);
+          const int P = 8 * D.C[g];
+          const double m = src[D.off[g] + (rr[i] - D.row0[g]) * P + (cc[j] - D.row0[g])].x;
+          // T[R][r] m conj(T[C][c])
+          const double xr = ar[i] * m, xi = ai[i] * m;
+          re += xr * br[j] + xi * bi[j];
+          im += xi * br[j] - xr * bi[j];
+        }
+      v = make_double2(re, im);
+    } else if (D.comp[R] == D.comp[Cc]) {
       int r = D.inv[R], c = D.inv[Cc];
       bool cj = false;
       if (r < 0) {   // mirrored component: read the stored mirror entry
@@ -888,6 +998,22 @@ __global__ void __launch_bounds__(256) k_blk_fidelity(BlkDev D, const double2* _
       const int r = e / P, c = e % P;
       const int a = D.perm[row0 + r], cc = D.perm[row0 + c];
       if (a < 0 || cc < 0) continue;
+      if (D.real[g]) {
+        const TTerms ta = row_terms(D, row0 + r), tb = row_terms(D, row0 + c);
+        double sre = 0.0;
+        for (int i = 0; i < ta.n; ++i)
+          for (int j = 0; j < tb.n; ++j) {
+            const int A = ta.R[i], Bn = tb.R[j];
+            const int i1 = A & 7, j1 = A >> 3, k1 = Bn & 7, l1 = Bn >> 3;
+            const double2 vj = Vs[j1 * 8 + l1], vi = Vs[i1 * 8 + k1];
+            // S_V[A][B] = conj(V[j][l]) V[i][k]
+            const double sr = vj.x * vi.x + vj.y * vi.y, si = vj.x * vi.y - vj.y * vi.x;
+            const double xr = ta.tr[i] * sr + ta.ti[i] * si, xi = ta.tr[i] * si - ta.ti[i] * sr;
+            sre += xr * tb.tr[j] - xi * tb.ti[j];
+          }
+        acc += sre * M[D.off[g] + e].x;
+        continue;
+      }
       const double w = D.weight[row0 + r];
       const int i = a & 7, j = a >> 3, k = cc & 7, l = cc >> 3;
       const double2 vjl = Vs[j * 8 + l], vik = Vs[i * 8 + k], y = M[D.off[g] + e];
@@ -918,28 +1044,42 @@ __device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int 
 // --------------------------------------------------------------- suffix chain
 // X_N = S_V^dag on the stored blocks, X_k = X_{k+1} U_k; X_img[b][k-1] = X_k (k = 1..N).
 // One CTA per pulse; the groups run independently; U_k streamed by per-group TMA (double buffer).
-template <int C, int R, int KS>
+template <int C, int R, int KS, bool RE>
 __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, double* X, const Ctx& x,
                                 double* sm, uint64_t* bar, unsigned long long& nflop, const Lane& L) {
   double* SU[2] = {sm, sm + 2 * 64 * C * C};
   const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
   const int go = 2 * x.off;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
-  BR<C, R> A, acc;
+  BR<C, R, RE> A, acc;
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i) {
       const int a = D.perm[x.row0 + 8 * (x.rt0 + r) + L.g], c = D.perm[x.row0 + 4 * i + L.t];
       double re = 0.0, im = 0.0;
-      if (a >= 0 && c >= 0) {
+      if constexpr (RE) {
+        // (S_V^dag)' = T^dag S_V^dag T = (S')^T with S' = T^dag S_V T real
+        if (a >= 0 && c >= 0) {
+          const TTerms ta = row_terms(D, x.row0 + 4 * i + L.t), tb = row_terms(D, x.row0 + 8 * (x.rt0 + r) + L.g);
+          for (int p = 0; p < ta.n; ++p)
+            for (int q = 0; q < tb.n; ++q) {
+              const int A = ta.R[p], Bn = tb.R[q];
+              const int i1 = A & 7, j1 = A >> 3, k1 = Bn & 7, l1 = Bn >> 3;
+              const double2 vj = __ldg(V + j1 * 8 + l1), vi = __ldg(V + i1 * 8 + k1);
+              const double sr = vj.x * vi.x + vj.y * vi.y, si = vj.x * vi.y - vj.y * vi.x;
+              const double xr = ta.tr[p] * sr + ta.ti[p] * si, xi = ta.tr[p] * si - ta.ti[p] * sr;
+              re += xr * tb.tr[q] - xi * tb.ti[q];
+            }
+        }
+      } else if (a >= 0 && c >= 0) {
         const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
         const double2 vjl = __ldg(V + j * 8 + l), vik = __ldg(V + ii * 8 + kk);
         re = vjl.x * vik.x + vjl.y * vik.y;   // S_V^dag[a][c] = V[j][l] conj(V[i][k])
         im = vjl.y * vik.x - vjl.x * vik.y;
       }
       A.re[r][i] = re;
-      A.im[r][i] = im;
+      if constexpr (!RE) A.im[r][i] = im;
     }
   bstore_img_l2(X + (size_t)(N - 1) * stride + go, A, x, L, l2_evict_first());
   if (leader && N > 1) tma_grp_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * stride + go, C, &bar[(N - 1) & 1]);
@@ -954,7 +1094,7 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
     mbar_wait(&bar[cur], ph[cur]);
     ph[cur] ^= 1;
     bzero(acc);
-    bmma<C, R, KS>(acc, A, SU[cur], x, L);   // X_{k+1} U_k
+    bmma<C, R, KS, RE>(acc, A, SU[cur], x, L);   // X_{k+1} U_k
     bcopy(A, acc);
     bstore_img_l2(X + (size_t)(k - 1) * stride + go, A, x, L, l2_evict_first());
   }
@@ -984,7 +1124,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], x.ks, blk_suffix_task, D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nflop, L);
+    BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nflop, L);
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
 }
@@ -996,8 +1136,8 @@ constexpr int BLK_GRAD_SCR = 2;   // L2 scratch images per group (squarings): E,
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
 // leaves W = L_exp(Omega, G) in A and returns the product count.  SD, SV, SN: group images
 // (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots; scr: the group's L2 scratch.
-template <int C, int R, int KS>
-__device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const BlkBasis& B, const SliceGrid& G,
+template <int C, int R, int KS, bool RE>
+__device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc, const BlkBasis& B, const SliceGrid& G,
                                              int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
                                              uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
                                              uint32_t tm, uint32_t ts, double* scr, int* bad, const Lane& L) {
@@ -1027,18 +1167,18 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
   mbar_wait(barN, ph);
   ph ^= 1;
   bzero(acc);
-  bmma<C, R, KS>(acc, A, SN, x, L);
+  bmma<C, R, KS, RE>(acc, A, SN, x, L);
   bscale(acc, sc);
   grp_sync(x);                                         // SV (X) complete; reads of SD (P_k) done
   bstore_img(SD, acc, x, L);
   bstore_img(gdX, acc, x, L);
   grp_sync(x);                                         // SD = dX complete
   bload_img(A, SV, x, L);
-  bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                  // A2 = X X
+  bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                  // A2 = X X
   bt_store(T0, acc);
-  bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                  // X dX
+  bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                  // X dX
   bload_img(A, SD, x, L);
-  bmma<C, R, KS>(acc, A, SV, x, L);                              // + dX X
+  bmma<C, R, KS, RE>(acc, A, SV, x, L);                              // + dX X
   bt_store(T1, acc);
   int np = 1 + 1 + 2;
   if (m == 8) {
@@ -1047,11 +1187,11 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     bzero(acc); baxpy_img(acc, c_t8[0], gdX, x, L); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, x, L);
     grp_sync(x);
     bt_load(A, T0);
-    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // Y = A2 W
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // Y = A2 W
     bt_store(T2, acc);
-    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A2 dW
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // A2 dW
     bt_load(A, T1);
-    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA2 W = dY
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dA2 W = dY
     bt_store(T3, acc);
     grp_sync(x);
     bzero(acc); bt_axpy(acc, 1.0, T2); bt_axpy(acc, c_t8[4], T0); bstore_img(SV, acc, x, L);
@@ -1060,37 +1200,37 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     bzero(acc);
     bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img(acc, 1.0, gdX, x, L);
     bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img(A, c_t8[3], gdX, x, L);   // dL
-    bmma<C, R, KS>(acc, A, SV, x, L);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);
     bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img(A, c_t8[3], gX, x, L);    // L
-    bmma<C, R, KS>(acc, A, SD, x, L);
+    bmma<C, R, KS, RE>(acc, A, SD, x, L);
     if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
     np += 1 + 2 + 2;
     if (s > 0) {
       bzero(acc);
       bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img(acc, 1.0, gX, x, L);
       badd_diag(acc, 1.0, x, L);
-      bmma<C, R, KS>(acc, A, SV, x, L);
+      bmma<C, R, KS, RE>(acc, A, SV, x, L);
       bstore_img_l2(gE, acc, x, L, keep);
       ++np;
     }
   } else {
     bt_load(A, T0);
-    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // A3
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // A3
     bt_store(T2, acc);
-    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A2 dX
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // A2 dX
     bt_load(A, T1);
-    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA2 X = dA3
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dA2 X = dA3
     bt_store(T3, acc);
     grp_sync(x);
     bt_load(A, T2); bstore_img(SV, A, x, L);
     bt_load(A, T3); bstore_img(SD, A, x, L);
     grp_sync(x);
     bt_load(A, T2);
-    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // A6
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // A6
     bstore_img(gA6, acc, x, L);
-    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // A3 dA3
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // A3 dA3
     bt_load(A, T3);
-    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dA3 A3
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dA3 A3
     bstore_img(gdA6, acc, x, L);
     grp_sync(x);
     bzero(acc);
@@ -1108,17 +1248,17 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     bzero(A);
     baxpy_img(A, c_t18[T18_B1][1], gdX, x, L); bt_axpy(A, c_t18[T18_B1][2], T1);
     bt_axpy(A, c_t18[T18_B1][3], T3);
-    bmma<C, R, KS>(acc, A, SV, x, L);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);
     bzero(A);
     baxpy_img(A, c_t18[T18_B1][1], gX, x, L); bt_axpy(A, c_t18[T18_B1][2], T0);
     bt_axpy(A, c_t18[T18_B1][3], T2);
-    bmma<C, R, KS>(acc, A, SD, x, L);
+    bmma<C, R, KS, RE>(acc, A, SD, x, L);
     bstore_img(SN, acc, x, L);                         // dA9 (SN idle since G)
     bzero(acc);                                        // A9 = B4 + B1 B5 (A holds B1)
     badd_diag(acc, c_t18[T18_B4][0], x, L);
     baxpy_img(acc, c_t18[T18_B4][1], gX, x, L); bt_axpy(acc, c_t18[T18_B4][2], T0);
     bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img(acc, c_t18[T18_B4][4], gA6, x, L);
-    bmma<C, R, KS>(acc, A, SV, x, L);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);
     grp_sync(x);                                       // reads of SV (B5), SD (dB5) done
     bstore_img(SV, acc, x, L);                         // A9
     grp_sync(x);                                       // A9 (SV), dA9 (SN) complete
@@ -1128,12 +1268,12 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     bload_img(A, SN, x, L);                            // dL = dB3 + dA9
     baxpy_img(A, c_t18[T18_B3][1], gdX, x, L); bt_axpy(A, c_t18[T18_B3][2], T1);
     bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img(A, c_t18[T18_B3][4], gdA6, x, L);
-    bmma<C, R, KS>(acc, A, SV, x, L);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);
     bload_img(A, SV, x, L);                            // L = B3 + A9
     badd_diag(A, c_t18[T18_B3][0], x, L);
     baxpy_img(A, c_t18[T18_B3][1], gX, x, L); bt_axpy(A, c_t18[T18_B3][2], T0);
     bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img(A, c_t18[T18_B3][4], gA6, x, L);
-    bmma<C, R, KS>(acc, A, SN, x, L);
+    bmma<C, R, KS, RE>(acc, A, SN, x, L);
     if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
     np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
     if (s > 0) {                                       // T = B2 + L A9
@@ -1141,7 +1281,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
       badd_diag(acc, c_t18[T18_B2][0], x, L);
       baxpy_img(acc, c_t18[T18_B2][1], gX, x, L); bt_axpy(acc, c_t18[T18_B2][2], T0);
       bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img(acc, c_t18[T18_B2][4], gA6, x, L);
-      bmma<C, R, KS>(acc, A, SV, x, L);
+      bmma<C, R, KS, RE>(acc, A, SV, x, L);
       bstore_img_l2(gE, acc, x, L, keep);
       ++np;
     }
@@ -1153,12 +1293,12 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
     bload_img_l2(acc, gdE, x, L, keep);
     bstore_img(SD, acc, x, L);
     grp_sync(x);
-    bzero(acc); bmma<C, R, KS>(acc, A, SD, x, L);                // E dE
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // E dE
     bload_img_l2(A, gdE, x, L, keep);
-    bmma<C, R, KS>(acc, A, SV, x, L);                            // + dE E
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dE E
     bstore_img_l2(gdE, acc, x, L, keep);
     bload_img_l2(A, gE, x, L, keep);
-    bzero(acc); bmma<C, R, KS>(acc, A, SV, x, L);                // E E
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // E E
     bstore_img_l2(gE, acc, x, L, keep);
     np += 3;
   }
@@ -1168,8 +1308,8 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R>& A, BR<C, R>& acc, const B
 }
 
 // weighted traces Re Tr(W_g B_m,g) over the warp's rows, added to the warp's partial sums
-template <int C, int R>
-__device__ __forceinline__ void blk_traces(const BR<C, R>& W, const BlkDev& D, const BlkBasis& B, int b, const Ctx& x,
+template <int C, int R, bool RE>
+__device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& D, const BlkBasis& B, int b, const Ctx& x,
                                            double* tr, bool first, const Lane& L) {
   constexpr int P = 8 * C;
   const int K = B.J + B.ncomm;
@@ -1186,7 +1326,7 @@ __device__ __forceinline__ void blk_traces(const BR<C, R>& W, const BlkDev& D, c
       for (int i = 0; i < 2 * C; ++i) {
         const double2 y = __ldg(Bm + (4 * i + L.t) * P + row);
         vr = fma(W.re[r][i], y.x, vr);
-        vr = fma(-W.im[r][i], y.y, vr);
+        if constexpr (!RE) vr = fma(-W.im[r][i], y.y, vr);
       }
       v = fma((double)D.weight[x.row0 + row], vr, v);
     }
@@ -1196,16 +1336,16 @@ __device__ __forceinline__ void blk_traces(const BR<C, R>& W, const BlkDev& D, c
   }
 }
 
-template <int C, int R, int KS>
+template <int C, int R, int KS, bool RE>
 __device__ void blk_grad_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, int b, int k, const Ctx& x,
                               double* sm, uint64_t* bars, uint32_t& ph, uint32_t tm, double* scr, int* bad, double* tr,
                               bool first, unsigned long long& nflop, const Lane& L) {
   const int IM = 2 * 64 * C * C;
-  BR<C, R> A, acc;
-  const int np = blk_dual_expm<C, R, KS>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1], ph,
+  BR<C, R, RE> A, acc;
+  const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1], ph,
                                          sm + 3 * IM, sm + 3 * IM + 64 * C * C, tm, D.tstride[L.w], scr, bad, L);
   if (x.rt0 == 0 && L.lane == 0) nflop += (unsigned long long)np * D.gflops[x.g];
-  blk_traces<C, R>(A, D, B, b, x, tr, first, L);
+  blk_traces<C, R, RE>(A, D, B, b, x, tr, first, L);
 }
 
 __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B,
@@ -1263,7 +1403,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
       const Ctx x = ctx_of(D, T);
       double* sm = smem + D.soff[x.g];
       double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
-      BLK_DISPATCH(D.C[x.g], x.ks, blk_grad_task, D, B, G, b, k, x, sm, bars[x.g], phN[t], tm, scr, &bad_sh,
+      BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_grad_task, D, B, G, b, k, x, sm, bars[x.g], phN[t], tm, scr, &bad_sh,
                    red_tr + L.w * BLK_TR_MAX, t == 0, nflop, L);
     }
     __syncthreads();   // every task done with this item: SN / SD regions free, red_tr complete
@@ -1512,8 +1652,9 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
     for (int i : members[k])
       if (cid[(i / d) + d * (i % d)] != mir[k]) return QAL_ERR_STRUCTURE;
   }
-  std::vector<int> keep, weight(ncomp, 1);
+  std::vector<int> keep, weight(ncomp, 1), realc(ncomp, 0);
   for (int k = 0; k < ncomp; ++k) {
+    realc[k] = (mir[k] == k);   // self-mirrored: real in the Hermitian basis
     if (!mirror) { keep.push_back(k); continue; }
     if (mir[k] == k) keep.push_back(k);
     else if (k < mir[k]) { keep.push_back(k); weight[k] = 2; }
@@ -1522,18 +1663,18 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
     if ((int)members[k].size() > 24) return QAL_ERR_UNSUPPORTED;   // super-blocks up to 24 wide
   std::stable_sort(keep.begin(), keep.end(),
                    [&](int a, int b) { return members[a].size() > members[b].size(); });
-  struct Bin { int width, used; std::vector<int> comps; };
+  struct Bin { int width, used, real; std::vector<int> comps; };
   std::vector<Bin> bins;
   for (int k : keep) {
     const int sz = (int)members[k].size();
-    // best fit: the open super-block with the least room left that still takes the component
+    // best fit among open super-blocks of the same arithmetic (real / complex)
     int best = -1;
     for (int i = 0; i < (int)bins.size(); ++i)
-      if (bins[i].used + sz <= bins[i].width &&
+      if (bins[i].real == realc[k] && bins[i].used + sz <= bins[i].width &&
           (best < 0 || bins[i].width - bins[i].used < bins[best].width - bins[best].used))
         best = i;
     if (best >= 0) { bins[best].used += sz; bins[best].comps.push_back(k); }
-    else bins.push_back({(sz + 7) / 8 * 8, sz, {k}});
+    else bins.push_back({(sz + 7) / 8 * 8, sz, realc[k], {k}});
   }
   if ((int)bins.size() > QAL_BLK_MAX_GROUPS) return QAL_ERR_UNSUPPORTED;
   qal_block_plan p;
@@ -1544,25 +1685,33 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
   p.ngroups = (int)bins.size();
   p.n_components = ncomp;
   int row = 0, off = 0;
-  for (int i = 0; i < QAL_BLK_MAX_ROWS; ++i) { p.perm[i] = -1; p.weight[i] = 0; }
-  for (int i = 0; i < 64; ++i) { p.inv[i] = -1; p.comp[i] = i < n ? cid[i] : -1; }
+  for (int i = 0; i < QAL_BLK_MAX_ROWS; ++i) { p.perm[i] = -1; p.weight[i] = 0; p.rtype[i] = 0; }
+  for (int i = 0; i < 64; ++i) { p.inv[i] = -1; p.comp[i] = i < n ? cid[i] : -1; p.ncode[i] = 0; }
   for (int g = 0; g < p.ngroups; ++g) {
     p.width[g] = bins[g].width;
     p.used[g] = bins[g].used;
+    p.real[g] = bins[g].real;
     p.row0[g] = row;
     p.off[g] = off;
     int r = row;
     for (int k : bins[g].comps)
       for (int i : members[k]) {
-        p.perm[r] = i;
-        p.weight[r] = weight[k];
-        p.inv[i] = r;
-        ++r;
+        const int si = (i / d) + d * (i % d);
+        if (!bins[g].real) {
+          p.perm[r] = i; p.weight[r] = weight[k]; p.rtype[r] = 0; p.inv[i] = r; ++r;
+        } else if (si == i) {
+          p.perm[r] = i; p.weight[r] = 1; p.rtype[r] = 1; p.inv[i] = r; p.ncode[i] = 1; ++r;
+        } else if (i < si) {
+          p.perm[r] = i; p.weight[r] = 1; p.rtype[r] = 2; p.inv[i] = r; p.ncode[i] = 2;
+          p.perm[r + 1] = i; p.weight[r + 1] = 1; p.rtype[r + 1] = 3;
+          p.ncode[si] = 3;
+          r += 2;
+        }
       }
     double fl = 0.0;
     for (int k : bins[g].comps) {
       const double sz = (double)members[k].size();
-      fl += 2.0 * QAL_REAL_MMAS_PER_CMMA * sz * sz * sz;   // 8 s^3 per complex product (4M)
+      fl += (bins[g].real ? 2.0 : 2.0 * QAL_REAL_MMAS_PER_CMMA) * sz * sz * sz;
     }
     p.flops[g] = fl;
     row += bins[g].width;

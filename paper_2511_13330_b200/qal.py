@@ -436,7 +436,9 @@ class BlockPlan(ctypes.Structure):
                 ("row0", ctypes.c_int * QAL_BLK_MAX_GROUPS),
                 ("off", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("flops", ctypes.c_double * QAL_BLK_MAX_GROUPS),
                 ("perm", ctypes.c_int * QAL_BLK_MAX_ROWS), ("weight", ctypes.c_int * QAL_BLK_MAX_ROWS),
-                ("inv", ctypes.c_int * 64), ("comp", ctypes.c_int * 64)]
+                ("inv", ctypes.c_int * 64), ("comp", ctypes.c_int * 64),
+                ("real", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("rtype", ctypes.c_int * QAL_BLK_MAX_ROWS),
+                ("ncode", ctypes.c_int * 64)]
 
     def groups(self):
         return [(self.width[g], self.row0[g], self.off[g]) for g in range(self.ngroups)]

@@ -78,7 +78,14 @@ def test_packing_layout_is_consistent(qal, basis):
             row += w
             off += w * w
         assert row == plan.nrows and off == plan.packed
-        stored = [plan.perm[r] for r in range(plan.nrows) if plan.perm[r] >= 0]
+        stored = []
+        for r in range(plan.nrows):
+            R = plan.perm[r]
+            if R < 0 or plan.rtype[r] == 3:
+                continue
+            stored.append(R)
+            if plan.rtype[r] == 2:                     # real pair: a row covers R and its mirror
+                stored.append((R // 8) + 8 * (R % 8))
         assert len(stored) == len(set(stored))
         for R in range(64):
             r = plan.inv[R]
@@ -90,7 +97,8 @@ def test_packing_layout_is_consistent(qal, basis):
 def test_flops_are_the_block_cubes(qal, basis):
     plan = qal.qal_block_plan_build(basis, mirror=True)
     mults = qal.real_mults_per_complex_product()
-    assert plan.flops_per_product() == 2 * mults * (20 ** 3 + 15 ** 3 + 6 ** 3 + 1)
+    # the self-mirrored q = 0 block (20) is real (1 real product), the others complex
+    assert plan.flops_per_product() == 2 * 20 ** 3 + 2 * mults * (15 ** 3 + 6 ** 3 + 1)
     dense = 2 * mults * 64 ** 3
     assert plan.flops_per_product() / dense < 0.05
 
@@ -99,3 +107,39 @@ def test_dense_coupling_gives_one_component_and_is_rejected(qal):
     M = torch.ones((1, 64, 64), dtype=torch.complex128)
     with pytest.raises(qal.QalError):
         qal.qal_block_plan_build(M, mirror=True)     # one 64-wide component > 24: unsupported
+
+
+def hermitian_basis(plan, g):
+    """T (natural x packed rows of group g) from the plan: e_R, (e_R + e_sR)/sqrt2, i(e_R - e_sR)/sqrt2."""
+    w, r0 = plan.width[g], plan.row0[g]
+    T = np.zeros((64, w), dtype=complex)
+    for r in range(w):
+        R = plan.perm[r0 + r]
+        if R < 0:
+            continue
+        sR = (R // 8) + 8 * (R % 8)
+        t = plan.rtype[r0 + r]
+        if t in (0, 1):
+            T[R, r] = 1.0
+        elif t == 2:
+            T[R, r] = T[sR, r] = 2 ** -0.5
+        else:
+            T[R, r], T[sR, r] = 1j * 2 ** -0.5, -1j * 2 ** -0.5
+    return T
+
+
+def test_real_basis_makes_hermiticity_preserving_maps_real(qal, basis, oracle):
+    """A29: in the Hermitian basis of the self-mirrored block, T is an isometry and every
+    Hermiticity-preserving generator (L0, L_j, and a propagator) is real."""
+    plan = qal.qal_block_plan_build(basis, mirror=True)
+    reals = [g for g in range(plan.ngroups) if plan.real[g]]
+    assert len(reals) == 1 and plan.used[reals[0]] == 20
+    g = reals[0]
+    T = hermitian_basis(plan, g)[:, :plan.used[g]]
+    assert np.allclose(T.conj().T @ T, np.eye(plan.used[g]), atol=1e-15)
+    p = qi.cfg0(N=4, T=2.0)
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Lam = oracle.propagate(L0, Lc, p.u[0], p.T, p.N)
+    for M in (L0, Lc[0], Lc[1], Lam):
+        Mp = T.conj().T @ M @ T
+        assert np.max(np.abs(Mp.imag)) <= 1e-14 * max(1.0, np.max(np.abs(Mp)))
