@@ -75,7 +75,6 @@ struct BlkDev {
 
 // warp roles: C = 3 groups -> 3 warps (one strip each); C <= 2 groups -> whole group on one
 // warp, greedily stacked so that no warp exceeds the heaviest single-strip load
-static int blk_cost(int C, int R, int ks) { return C * R * ks; }
 
 bool to_dev(const qal_block_plan& p, BlkDev& D) {
   memset(&D, 0, sizeof(D));
@@ -90,44 +89,44 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
     D.gflops[g] = (unsigned long long)p.flops[g];
     D.real[g] = (unsigned char)p.real[g];
   }
-  int w = 0, heavy = 0;
-  for (int g = 0; g < p.ngroups; ++g)
-    if (D.C[g] == 3) {
-      D.gwarps[g] = 3;
-      for (int r = 0; r < 3; ++r) {
-        if (w >= BLK_MAX_WARPS) return false;
+  // rows per warp of every group: R = 1 (C warps on one block, named barrier) or R = C (one warp owns
+  // the whole block).  Choose the split that minimises the largest per-warp DMMA count per product
+  // (real groups issue 1 MMA per step, complex 4), ties -> fewer warps.  QAL_BLK_SPLIT (bit g = split
+  // group g) overrides, for experiments.
+  auto cost = [&](int g, int R) { return D.C[g] * R * D.ks[g] * (D.real[g] ? 1 : 4); };
+  int best_mask = -1, best_max = 1 << 30, best_w = 1 << 30;
+  const char* env = getenv("QAL_BLK_SPLIT");
+  for (int mask = 0; mask < (1 << p.ngroups); ++mask) {
+    int mx = 0, nw = 0;
+    bool ok = true;
+    for (int g = 0; g < p.ngroups; ++g) {
+      const bool split = (mask >> g) & 1;
+      if (split && D.C[g] == 1) { ok = false; break; }
+      mx = std::max(mx, cost(g, split ? 1 : D.C[g]));
+      nw += split ? D.C[g] : 1;
+    }
+    if (!ok || nw > BLK_MAX_WARPS) continue;
+    if (env) {
+      if (mask == atoi(env)) { best_mask = mask; best_max = mx; best_w = nw; }
+      continue;
+    }
+    if (mx < best_max || (mx == best_max && nw < best_w)) { best_mask = mask; best_max = mx; best_w = nw; }
+  }
+  if (best_mask < 0) return false;
+  int w = 0;
+  for (int g = 0; g < p.ngroups; ++g) {
+    const bool split = (best_mask >> g) & 1;
+    if (split) {
+      D.gwarps[g] = D.C[g];
+      for (int r = 0; r < D.C[g]; ++r) {
         D.task[w][0] = {(signed char)g, (signed char)r, 1, 0};
         D.ntask[w++] = 1;
       }
-      heavy = std::max(heavy, blk_cost(3, 1, D.ks[g]));
+    } else {
+      D.gwarps[g] = 1;
+      D.task[w][0] = {(signed char)g, 0, (signed char)D.C[g], 0};
+      D.ntask[w++] = 1;
     }
-  std::vector<int> small;
-  for (int g = 0; g < p.ngroups; ++g)
-    if (D.C[g] < 3) small.push_back(g);
-  std::stable_sort(small.begin(), small.end(), [&](int a, int b) {
-    return blk_cost(D.C[a], D.C[a], D.ks[a]) > blk_cost(D.C[b], D.C[b], D.ks[b]);
-  });
-  int load[BLK_MAX_WARPS] = {0};
-  const int first_small = w;
-  int cap = heavy;   // stack small groups while a warp stays within 1.25x the heaviest single role
-  for (int g : small) cap = std::max(cap, blk_cost(D.C[g], D.C[g], D.ks[g]));
-  cap += cap / 4;
-#ifndef QAL_BLK_STACK
-  cap = 0;   // measured on B200: one small group per warp beats stacking them (2 vs 3 CTAs/SM)
-#endif
-  for (int g : small) {
-    const int c = blk_cost(D.C[g], D.C[g], D.ks[g]);
-    int best = -1;
-    for (int v = first_small; v < w; ++v)
-      if (D.ntask[v] < BLK_MAX_TASKS && load[v] + c <= cap && (best < 0 || load[v] < load[best]))
-        best = v;
-    if (best < 0) {
-      if (w >= BLK_MAX_WARPS) return false;
-      best = w++;
-    }
-    D.task[best][D.ntask[best]++] = {(signed char)g, 0, (signed char)D.C[g], 0};
-    D.gwarps[g] = 1;
-    load[best] += c;
   }
   D.nwarps = w;
   // TMEM: 4 strip slots per warp; warps sharing a lane quarter stack their column ranges
@@ -181,24 +180,28 @@ __device__ __forceinline__ void grp_sync(const Ctx& x) {
   }
 }
 
-// the warp roles every kernel instantiates: (C, R, KS) = (3, 1, 5|6), (2, 2, 4), (1, 1, 2), each complex or
-// real (RE: a self-mirrored component in the Hermitian basis, 1 real MMA per step instead of 4)
+// the warp roles every kernel instantiates: (C, R) = (3, 1|3), (2, 1|2), (1, 1) with KS = 5|6, 4, 2, each
+// complex or real (RE: a self-mirrored component in the Hermitian basis, 1 real MMA per step instead of 4)
 // (KS = k-steps of the products; the 20-block runs with K = 20: 5 k-steps)
-#define BLK_DISPATCH(CC, KSV, RV, FN, ...)                \
-  do {                                                    \
-    if ((RV)) {                                           \
-      if ((CC) == 3) {                                    \
-        if ((KSV) <= 5) FN<3, 1, 5, true>(__VA_ARGS__);   \
-        else FN<3, 1, 6, true>(__VA_ARGS__);              \
-      } else if ((CC) == 2) FN<2, 2, 4, true>(__VA_ARGS__); \
-      else FN<1, 1, 2, true>(__VA_ARGS__);                \
-    } else {                                              \
-      if ((CC) == 3) {                                    \
-        if ((KSV) <= 5) FN<3, 1, 5, false>(__VA_ARGS__);  \
-        else FN<3, 1, 6, false>(__VA_ARGS__);             \
-      } else if ((CC) == 2) FN<2, 2, 4, false>(__VA_ARGS__); \
-      else FN<1, 1, 2, false>(__VA_ARGS__);               \
-    }                                                     \
+#define BLK_DISPATCH_RE(CC, RR, KSV, RE_, FN, ...)              \
+  do {                                                          \
+    if ((CC) == 3) {                                            \
+      if ((RR) == 1) {                                          \
+        if ((KSV) <= 5) FN<3, 1, 5, RE_>(__VA_ARGS__);          \
+        else FN<3, 1, 6, RE_>(__VA_ARGS__);                     \
+      } else {                                                  \
+        if ((KSV) <= 5) FN<3, 3, 5, RE_>(__VA_ARGS__);          \
+        else FN<3, 3, 6, RE_>(__VA_ARGS__);                     \
+      }                                                         \
+    } else if ((CC) == 2) {                                     \
+      if ((RR) == 1) FN<2, 1, 4, RE_>(__VA_ARGS__);             \
+      else FN<2, 2, 4, RE_>(__VA_ARGS__);                       \
+    } else FN<1, 1, 2, RE_>(__VA_ARGS__);                       \
+  } while (0)
+#define BLK_DISPATCH(CC, RR, KSV, RV, FN, ...)                       \
+  do {                                                               \
+    if ((RV)) BLK_DISPATCH_RE(CC, RR, KSV, true, FN, __VA_ARGS__);   \
+    else BLK_DISPATCH_RE(CC, RR, KSV, false, FN, __VA_ARGS__);       \
   } while (0)
 
 // ------------------------------------------------------------------ P-wide strips, R per warp
@@ -779,7 +782,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis 
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh, nflop, L);
+    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh, nflop, L);
   }
   tmem_fence_before();
   __syncthreads();
@@ -827,7 +830,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_tree_level(BlkDev D,
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_pair_task, lhs, rhs, dst, x, sm, L);
+    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_pair_task, lhs, rhs, dst, x, sm, L);
     if (x.rt0 == 0 && L.lane == 0) nflop += D.gflops[x.g];
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
@@ -1124,7 +1127,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nflop, L);
+    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nflop, L);
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
 }
@@ -1403,7 +1406,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
       const Ctx x = ctx_of(D, T);
       double* sm = smem + D.soff[x.g];
       double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
-      BLK_DISPATCH(D.C[x.g], x.ks, D.real[x.g], blk_grad_task, D, B, G, b, k, x, sm, bars[x.g], phN[t], tm, scr, &bad_sh,
+      BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_task, D, B, G, b, k, x, sm, bars[x.g], phN[t], tm, scr, &bad_sh,
                    red_tr + L.w * BLK_TR_MAX, t == 0, nflop, L);
     }
     __syncthreads();   // every task done with this item: SN / SD regions free, red_tr complete
