@@ -304,8 +304,8 @@ typedef struct {
     int row0[QAL_BLK_MAX_GROUPS];       /* first packed row of group g                        */
     int off[QAL_BLK_MAX_GROUPS];        /* complex offset of group g inside a packed matrix   */
     double flops[QAL_BLK_MAX_GROUPS];   /* algorithmic flops of one product of group g:
-                                           8 sum s^3 over complex components, 2 sum s^3 over
-                                           real ones (padding excluded)                       */
+                                           2 cplx_mults sum s^3 over complex components, 2 sum
+                                           s^3 over real ones (padding excluded)              */
     int perm[QAL_BLK_MAX_ROWS];         /* packed row -> natural index, -1 = padding          */
     int weight[QAL_BLK_MAX_ROWS];       /* 0 padding, 1 self-mirror component (or mirror
                                            off), 2 component whose mirror is implied         */
@@ -322,6 +322,8 @@ typedef struct {
                                            3 pair column b (perm = the pair's smaller index)  */
     int ncode[64];                      /* natural index: 0 complex group, 1 real diagonal,
                                            2 pair representative R < s(R), 3 pair mirror      */
+    int cplx_mults;                     /* real multiplications per complex block product the
+                                           library executes (4, or 3 with the Gauss form)     */
 } qal_block_plan;
 
 /*

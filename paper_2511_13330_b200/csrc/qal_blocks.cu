@@ -41,6 +41,12 @@
 namespace qal {
 
 constexpr int BLK_MAX_WARPS = 8;
+// real MMAs per complex 8x8x4 step of the complex blocks: 4 (default) or 3 (Gauss, -DQAL_BLK_3M)
+#ifdef QAL_BLK_3M
+constexpr int BLK_CPLX_MMAS = 3;
+#else
+constexpr int BLK_CPLX_MMAS = 4;
+#endif
 constexpr int BLK_MAX_TASKS = 3;
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
@@ -93,7 +99,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
   // the whole block).  Choose the split that minimises the largest per-warp DMMA count per product
   // (real groups issue 1 MMA per step, complex 4), ties -> fewer warps.  QAL_BLK_SPLIT (bit g = split
   // group g) overrides, for experiments.
-  auto cost = [&](int g, int R) { return D.C[g] * R * D.ks[g] * (D.real[g] ? 1 : 4); };
+  auto cost = [&](int g, int R) { return D.C[g] * R * D.ks[g] * (D.real[g] ? 1 : BLK_CPLX_MMAS); };
   int best_mask = -1, best_max = 1 << 30, best_w = 1 << 30;
   const char* env = getenv("QAL_BLK_SPLIT");
   for (int mask = 0; mask < (1 << p.ngroups); ++mask) {
@@ -409,6 +415,16 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
   const int swz = (C % 2 == 0) ? (L.t & 1) : 0;   // physical tile of logical tile j: j ^ swz
   const uint32_t base = smem_u32(Bs + L.t * P + L.g);
   double br[2][C], bi[2][C];
+  double g3q[R][RE || BLK_CPLX_MMAS == 4 ? 1 : 2 * C];   // Gauss Q accumulator
+  if constexpr (!RE && BLK_CPLX_MMAS == 3) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) {
+        g3q[r][i] = 0.0;
+        acc.im[r][i] += acc.re[r][i];   // R = acc.re + acc.im
+      }
+  }
 #pragma unroll
   for (int j = 0; j < C; ++j) {
     const uint32_t p = base + 8u * (8 * (j ^ swz));
@@ -432,6 +448,15 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
         if constexpr (RE) {          // real block: 1 MMA per 8x8x4 step
 #pragma unroll
           for (int j = 0; j < C; ++j) dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], a.re[r][q], br[cur][j]);
+        } else if constexpr (BLK_CPLX_MMAS == 3) {   // Gauss: P = Ar Br, Q = Ai Bi, R = (Ar+Ai)(Br+Bi)
+          const double ar = a.re[r][q], ai = a.im[r][q], as = ar + ai;
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            const double bs = br[cur][j] + bi[cur][j];
+            dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
+            dmma(g3q[r][2 * j], g3q[r][2 * j + 1], ai, bi[cur][j]);
+            dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], as, bs);
+          }
         } else {
           const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
 #pragma unroll
@@ -444,6 +469,16 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
         }
       }
     }
+  }
+  if constexpr (!RE && BLK_CPLX_MMAS == 3) {   // Re = P - Q, Im = R - P - Q (P, R carry the old acc)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) {
+        const double pp = acc.re[r][i], qq = g3q[r][i];
+        acc.re[r][i] = pp - qq;
+        acc.im[r][i] -= pp + qq;
+      }
   }
   QAL_FENCE();
 }
@@ -1687,6 +1722,7 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
   p.mirror = mirror ? 1 : 0;
   p.ngroups = (int)bins.size();
   p.n_components = ncomp;
+  p.cplx_mults = BLK_CPLX_MMAS;
   int row = 0, off = 0;
   for (int i = 0; i < QAL_BLK_MAX_ROWS; ++i) { p.perm[i] = -1; p.weight[i] = 0; p.rtype[i] = 0; }
   for (int i = 0; i < 64; ++i) { p.inv[i] = -1; p.comp[i] = i < n ? cid[i] : -1; p.ncode[i] = 0; }
@@ -1714,7 +1750,7 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
     double fl = 0.0;
     for (int k : bins[g].comps) {
       const double sz = (double)members[k].size();
-      fl += (bins[g].real ? 2.0 : 2.0 * QAL_REAL_MMAS_PER_CMMA) * sz * sz * sz;
+      fl += (bins[g].real ? 2.0 : 2.0 * BLK_CPLX_MMAS) * sz * sz * sz;
     }
     p.flops[g] = fl;
     row += bins[g].width;

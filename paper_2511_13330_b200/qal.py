@@ -438,7 +438,7 @@ class BlockPlan(ctypes.Structure):
                 ("perm", ctypes.c_int * QAL_BLK_MAX_ROWS), ("weight", ctypes.c_int * QAL_BLK_MAX_ROWS),
                 ("inv", ctypes.c_int * 64), ("comp", ctypes.c_int * 64),
                 ("real", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("rtype", ctypes.c_int * QAL_BLK_MAX_ROWS),
-                ("ncode", ctypes.c_int * 64)]
+                ("ncode", ctypes.c_int * 64), ("cplx_mults", ctypes.c_int)]
 
     def groups(self):
         return [(self.width[g], self.row0[g], self.off[g]) for g in range(self.ngroups)]
