@@ -130,3 +130,49 @@ def test_segment_seed_algebra_reproduces_the_full_horizon_gradient(oracle, mode)
     assert np.allclose(g_seg, g_full, rtol=0, atol=1e-12 * np.abs(g_full).max())
     F = oracle.fidelity(Lam, p.V)
     assert abs(np.trace(C @ Lam).real - F) <= 1e-15           # the cotangent of the fidelity
+
+
+def _worker_packed(rank, world, port, N, seed, q):
+    """Block path (cfg3 with a plan): every rank all-gathers its PACKED partial (the concatenated
+    super-block matrices, 1-D); the ordered combine acts block by block."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    widths = [24, 16, 8]
+    offs = np.cumsum([0] + [w * w for w in widths])
+    rng = np.random.default_rng(seed)
+    blocks = [(rng.standard_normal((N, w, w)) + 1j * rng.standard_normal((N, w, w))) / np.sqrt(w) for w in widths]
+    lo, hi = driver.shard_range(N, world, rank)
+    Q = np.concatenate([oracle.ordered_product(b[lo:hi]).reshape(-1) for b in blocks])   # packed partial
+    parts = driver.gather_partials(torch.from_numpy(Q))
+    assert parts.shape == (world, offs[-1])
+
+    def blockwise(P):
+        P = P.numpy()
+        return torch.from_numpy(np.concatenate([
+            oracle.ordered_product(P[:, offs[g]:offs[g + 1]].reshape(world, w, w).copy()).reshape(-1)
+            for g, w in enumerate(widths)]))
+
+    Lam = driver.ordered_combine(parts, product=blockwise).numpy()
+    errs = []
+    for g, w in enumerate(widths):
+        ref = oracle.ordered_product(blocks[g])
+        got = Lam[offs[g]:offs[g + 1]].reshape(w, w)
+        errs.append(float(np.linalg.norm(got - ref) / np.linalg.norm(ref)))
+    q.put((rank, max(errs)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_time_sharded_packed_partials_gloo(world):
+    port = free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_packed, args=(r, world, port, 16, 7, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for _, err in res:
+        assert err <= 1e-12
