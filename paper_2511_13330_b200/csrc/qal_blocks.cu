@@ -107,7 +107,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
     bool ok = true;
     for (int g = 0; g < p.ngroups; ++g) {
       const bool split = (mask >> g) & 1;
-      if (split && D.C[g] == 1) { ok = false; break; }
+      if ((split && D.C[g] == 1) || (!split && D.C[g] == 3)) { ok = false; break; }   // roles (3,1) (2,1|2) (1,1)
       mx = std::max(mx, cost(g, split ? 1 : D.C[g]));
       nw += split ? D.C[g] : 1;
     }
@@ -186,19 +186,14 @@ __device__ __forceinline__ void grp_sync(const Ctx& x) {
   }
 }
 
-// the warp roles every kernel instantiates: (C, R) = (3, 1|3), (2, 1|2), (1, 1) with KS = 5|6, 4, 2, each
+// the warp roles every kernel instantiates: (C, R) = (3, 1), (2, 1|2), (1, 1) with KS = 5|6, 4, 2, each
 // complex or real (RE: a self-mirrored component in the Hermitian basis, 1 real MMA per step instead of 4)
 // (KS = k-steps of the products; the 20-block runs with K = 20: 5 k-steps)
 #define BLK_DISPATCH_RE(CC, RR, KSV, RE_, FN, ...)              \
   do {                                                          \
     if ((CC) == 3) {                                            \
-      if ((RR) == 1) {                                          \
-        if ((KSV) <= 5) FN<3, 1, 5, RE_>(__VA_ARGS__);          \
-        else FN<3, 1, 6, RE_>(__VA_ARGS__);                     \
-      } else {                                                  \
-        if ((KSV) <= 5) FN<3, 3, 5, RE_>(__VA_ARGS__);          \
-        else FN<3, 3, 6, RE_>(__VA_ARGS__);                     \
-      }                                                         \
+      if ((KSV) <= 5) FN<3, 1, 5, RE_>(__VA_ARGS__);            \
+      else FN<3, 1, 6, RE_>(__VA_ARGS__);                       \
     } else if ((CC) == 2) {                                     \
       if ((RR) == 1) FN<2, 1, 4, RE_>(__VA_ARGS__);             \
       else FN<2, 2, 4, RE_>(__VA_ARGS__);                       \
@@ -761,10 +756,11 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   const int nchunk = G.count / O.chunk;
   const int b = item / nchunk, c = item % nchunk;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
-  BR<C, R, RE> A, acc;
+  BR<C, R, RE> A, acc, Om;
+  bbuild_omega(Om, B, G, b, c * O.chunk, x, L);
   for (int kk = 0; kk < O.chunk; ++kk) {
     const int k = c * O.chunk + kk;
-    bbuild_omega(A, B, G, b, k, x, L);
+    bcopy(A, Om);
     const double nrm = bnorm1(A, red, x, L);
     int m, s;
     choose_scheme(nrm, m, s);
@@ -774,6 +770,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     grp_sync(x);
     const int np = bexpm<C, R, KS, RE>(A, acc, m, s, SX, SX4, tm, ts, x, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
+    if (kk + 1 < O.chunk) bbuild_omega(Om, B, G, b, k + 1, x, L);   // loads overlap the stores / fold below
     const size_t slot = (size_t)b * G.count + k;
     if (O.U_img) bstore_img_l2(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
     if (O.chunk_nat) {
@@ -1190,7 +1187,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   double* gdE = scr + IM;
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
   const uint64_t keep = l2_evict_last();
-  bbuild_omega(A, B, G, b, k, x, L);
+  // A holds Omega_k on entry (built one item ahead by the caller)
   const double nrm = bnorm1(A, red, x, L);
   int m, s;
   choose_scheme(nrm, m, s);
@@ -1374,78 +1371,45 @@ __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& 
   }
 }
 
+// One warp's role over the whole item sequence (every warp runs the same number of items, so the
+// CTA-wide barriers below match).  Omega of the next item is built right after the dual pass, so its
+// basis loads are in flight during the traces and the CTA barrier.
 template <int C, int R, int KS, bool RE>
-__device__ void blk_grad_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, int b, int k, const Ctx& x,
-                              double* sm, uint64_t* bars, uint32_t& ph, uint32_t tm, double* scr, int* bad, double* tr,
-                              bool first, unsigned long long& nflop, const Lane& L) {
+__device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, const SliceGrid& G,
+                              const double* __restrict__ P_img, const double* __restrict__ X_img,
+                              double* __restrict__ grad, int* __restrict__ status, double* scr_cta, const Ctx& x,
+                              double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr,
+                              unsigned long long& nflop, const Lane& L) {
   const int IM = 2 * 64 * C * C;
-  BR<C, R, RE> A, acc;
-  const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1], ph,
-                                         sm + 3 * IM, sm + 3 * IM + 64 * C * C, tm, D.tstride[L.w], scr, bad, L);
-  if (x.rt0 == 0 && L.lane == 0) nflop += (unsigned long long)np * D.gflops[x.g];
-  blk_traces<C, R, RE>(A, D, B, b, x, tr, first, L);
-}
-
-__global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B,
-                                                                            SliceGrid G,
-                                                                            const double* __restrict__ P_img,
-                                                                            const double* __restrict__ X_img,
-                                                                            double* __restrict__ grad,
-                                                                            int* __restrict__ status,
-                                                                            double* __restrict__ scratch,
-                                                                            int tmem_cols, unsigned long long* ctr) {
-  extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];   // [0]: X_{k+1} -> SN, [1]: P_k -> SD
-  __shared__ double red_tr[BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX];
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ int bad_sh;
-  const Lane L = lane_id();
-  if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
-  const int ntask = D.ntask[L.w];
-  for (int t = 0; t < ntask; ++t)
-    if (D.task[L.w][t].rt0 == 0 && L.lane == 0) {
-      mbar_init(&bars[D.task[L.w][t].g][0], 1);
-      mbar_init(&bars[D.task[L.w][t].g][1], 1);
-    }
-  fence_mbar_init();
-  if (threadIdx.x == 0) bad_sh = 0;
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
   const int items = batch * N;
   const int K = B.J + B.ncomm;
-  uint32_t phN[BLK_MAX_TASKS] = {0, 0, 0};
-  unsigned long long nflop = 0;
-  double* scr_cta = scratch + (size_t)blockIdx.x * stride * BLK_GRAD_SCR;
-  // group leaders: bulk-copy the operand images of an item (X_{k+1} -> SN, P_k -> SD)
-  auto prefetch = [&](int it) {
-    for (int t = 0; t < ntask; ++t) {
-      const BlkTask T = D.task[L.w][t];
-      if (T.rt0 == 0 && L.lane == 0 && it < items) {
-        const int C = D.C[T.g];
-        double* base = smem + D.soff[T.g];
-        fence_proxy_async();
-        tma_grp_img(base + 2 * 2 * 64 * C * C, X_img + (size_t)it * stride + 2 * D.off[T.g], C, &bars[T.g][0]);
-        tma_grp_img(base, P_img + (size_t)it * stride + 2 * D.off[T.g], C, &bars[T.g][1]);
-      }
+  const bool leader = (x.rt0 == 0 && L.lane == 0);
+  double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
+  uint32_t ph = 0;
+  auto prefetch = [&](int it) {   // group leader: bulk-copy X_{k+1} -> SN, P_k -> SD of item `it`
+    if (leader && it < items) {
+      fence_proxy_async();
+      tma_grp_img(sm + 2 * IM, X_img + (size_t)it * stride + 2 * x.off, C, &bars[0]);
+      tma_grp_img(sm, P_img + (size_t)it * stride + 2 * x.off, C, &bars[1]);
     }
   };
+  BR<C, R, RE> A, acc, Om;
   prefetch(blockIdx.x);
+  if ((int)blockIdx.x < items) bbuild_omega(Om, B, G, blockIdx.x / N, blockIdx.x % N, x, L);
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
-    for (int t = 0; t < ntask; ++t) {
-      const BlkTask T = D.task[L.w][t];
-      const Ctx x = ctx_of(D, T);
-      double* sm = smem + D.soff[x.g];
-      double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
-      BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_task, D, B, G, b, k, x, sm, bars[x.g], phN[t], tm, scr, &bad_sh,
-                   red_tr + L.w * BLK_TR_MAX, t == 0, nflop, L);
-    }
-    __syncthreads();   // every task done with this item: SN / SD regions free, red_tr complete
-    prefetch(item + gridDim.x);
+    bcopy(A, Om);
+    const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
+                                               ph, sm + 3 * IM, sm + 3 * IM + 64 * C * C, tm, D.tstride[L.w], scr,
+                                               bad_sh, L);
+    if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
+    const int nx = item + gridDim.x;
+    if (nx < items) bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
+    blk_traces<C, R, RE>(A, D, B, b, x, red_tr + L.w * BLK_TR_MAX, true, L);
+    __syncthreads();   // every warp done with this item: SN / SD free, red_tr complete
+    prefetch(nx);
     if (threadIdx.x < K) {
       double s = 0.0;
       for (int w = 0; w < D.nwarps; ++w) s += red_tr[w * BLK_TR_MAX + threadIdx.x];
@@ -1480,10 +1444,42 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
           gg[J + j] = g2 * inv_d2;
         }
       }
-      if (bad_sh && status) status[b] = QAL_ERR_NONFINITE;
-      bad_sh = 0;
+      if (*bad_sh && status) status[b] = QAL_ERR_NONFINITE;
+      *bad_sh = 0;
     }
   }
+}
+
+__global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B, SliceGrid G,
+                                                               const double* __restrict__ P_img,
+                                                               const double* __restrict__ X_img,
+                                                               double* __restrict__ grad, int* __restrict__ status,
+                                                               double* __restrict__ scratch, int tmem_cols,
+                                                               unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];   // [0]: X_{k+1} -> SN, [1]: P_k -> SD
+  __shared__ double red_tr[BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int bad_sh;
+  const Lane L = lane_id();
+  if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
+  const BlkTask T = D.task[L.w][0];   // one role per warp (to_dev)
+  if (T.rt0 == 0 && L.lane == 0) {
+    mbar_init(&bars[T.g][0], 1);
+    mbar_init(&bars[T.g][1], 1);
+  }
+  fence_mbar_init();
+  if (threadIdx.x == 0) bad_sh = 0;
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
+  unsigned long long nflop = 0;
+  double* scr_cta = scratch + (size_t)blockIdx.x * 2 * (size_t)D.packed * BLK_GRAD_SCR;
+  const Ctx x = ctx_of(D, T);
+  double* sm = smem + D.soff[x.g];
+  BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status, scr_cta,
+               x, sm, bars[x.g], tm, &bad_sh, red_tr, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
