@@ -1166,6 +1166,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
 
 // --------------------------------------------------------------- gradient slices
 constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
+constexpr int BLK_TR_BUF = BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX;   // one parity's trace buffer
 constexpr int BLK_GRAD_SCR = 2;   // L2 scratch images per group (squarings): E, dE
 
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
@@ -1401,23 +1402,27 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
     bcopy(A, Om);
+    const int par = ((item - (int)blockIdx.x) / (int)gridDim.x) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
                                                ph, sm + 3 * IM, sm + 3 * IM + 64 * C * C, tm, D.tstride[L.w], scr,
-                                               bad_sh, L);
+                                               bad_sh + par, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const int nx = item + gridDim.x;
     if (nx < items) bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
-    blk_traces<C, R, RE>(A, D, B, b, x, red_tr + L.w * BLK_TR_MAX, true, L);
-    __syncthreads();   // every warp done with this item: SN / SD free, red_tr complete
+    // per-warp partial traces, double-buffered by item parity so one CTA barrier per item suffices
+    double* rt = red_tr + (size_t)par * BLK_TR_BUF;
+    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * BLK_TR_MAX, true, L);
+    __syncthreads();   // every warp done with this item: SN / SD free, rt complete
     prefetch(nx);
-    if (threadIdx.x < K) {
+    if (L.w != 0) continue;
+    for (int m = L.lane; m < K; m += 32) {   // fixed-order sum over the warps
       double s = 0.0;
-      for (int w = 0; w < D.nwarps; ++w) s += red_tr[w * BLK_TR_MAX + threadIdx.x];
-      red_tr[BLK_MAX_WARPS * BLK_TR_MAX + threadIdx.x] = s;
+      for (int w = 0; w < D.nwarps; ++w) s += rt[w * BLK_TR_MAX + m];
+      rt[BLK_MAX_WARPS * BLK_TR_MAX + m] = s;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double* T = red_tr + BLK_MAX_WARPS * BLK_TR_MAX;
+    __syncwarp();
+    if (L.lane == 0) {
+      const double* T = rt + BLK_MAX_WARPS * BLK_TR_MAX;
       const int J = B.J;
       const double inv_d2 = 1.0 / 64.0;
       if (G.mode == 0) {
@@ -1444,8 +1449,8 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
           gg[J + j] = g2 * inv_d2;
         }
       }
-      if (*bad_sh && status) status[b] = QAL_ERR_NONFINITE;
-      *bad_sh = 0;
+      if (bad_sh[par] && status) status[b] = QAL_ERR_NONFINITE;
+      bad_sh[par] = 0;
     }
   }
 }
@@ -1458,9 +1463,9 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
                                                                unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];   // [0]: X_{k+1} -> SN, [1]: P_k -> SD
-  __shared__ double red_tr[BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX];
+  __shared__ double red_tr[2 * BLK_TR_BUF];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int bad_sh;
+  __shared__ int bad_sh[2];
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   const BlkTask T = D.task[L.w][0];   // one role per warp (to_dev)
@@ -1469,7 +1474,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
     mbar_init(&bars[T.g][1], 1);
   }
   fence_mbar_init();
-  if (threadIdx.x == 0) bad_sh = 0;
+  if (threadIdx.x == 0) { bad_sh[0] = 0; bad_sh[1] = 0; }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -1479,7 +1484,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   const Ctx x = ctx_of(D, T);
   double* sm = smem + D.soff[x.g];
   BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status, scr_cta,
-               x, sm, bars[x.g], tm, &bad_sh, red_tr, nflop, L);
+               x, sm, bars[x.g], tm, bad_sh, red_tr, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
