@@ -741,7 +741,11 @@ __device__ __forceinline__ int bexpm(BR<C, R, RE>& A, BR<C, R, RE>& acc, int m, 
 }
 
 // per-group shared memory: three images + the norm buffer (P*P doubles)
-__host__ __device__ constexpr int grp3_doubles(int C) { return 3 * 2 * 64 * C * C + 64 * C * C; }
+// shared-memory images of a group: complex = re plane + im plane (2 P^2 doubles), real = re plane only;
+// the norm buffer needs C row tiles x P columns (rounded to 128 bytes)
+__host__ __device__ constexpr int img_doubles(int C, bool real) { return (real ? 1 : 2) * 64 * C * C; }
+__host__ __device__ constexpr int red_doubles(int C) { return (8 * C * C + 15) / 16 * 16; }
+__host__ __device__ constexpr int grp3_doubles(int C, bool real) { return 3 * img_doubles(C, real) + red_doubles(C); }
 
 // ------------------------------------------------------------------ forward fold (a1-a5)
 template <int C, int R, int KS, bool RE>
@@ -749,10 +753,11 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
                              const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long& nflop,
                              const Lane& L) {
   const uint32_t ts = D.tstride[L.w];
+  constexpr int IM = img_doubles(C, RE);
   double* SX = sm;
-  double* SX4 = sm + 2 * 64 * C * C;
-  double* SP = sm + 4 * 64 * C * C;
-  double* red = sm + 6 * 64 * C * C;
+  double* SX4 = sm + IM;
+  double* SP = sm + 2 * IM;
+  double* red = sm + 3 * IM;
   const int nchunk = G.count / O.chunk;
   const int b = item / nchunk, c = item % nchunk;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
@@ -1070,8 +1075,8 @@ __global__ void __launch_bounds__(256) k_blk_fidelity(BlkDev D, const double2* _
 // block gives the same real part as its stored partner).
 
 // one thread: bulk-copy a group image (16 P^2 bytes) global -> shared, arriving on `bar`
-__device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int C, uint64_t* bar) {
-  const uint32_t bytes = 16u * 64u * C * C;
+__device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int C, uint64_t* bar, bool real = false) {
+  const uint32_t bytes = (real ? 8u : 16u) * 64u * C * C;   // a real group's image is its re plane
   mbar_expect_tx(bar, bytes);
   bulk_g2s_hint(dst, src, bytes, bar, l2_evict_first());
 }
@@ -1082,7 +1087,7 @@ __device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int 
 template <int C, int R, int KS, bool RE>
 __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, double* X, const Ctx& x,
                                 double* sm, uint64_t* bar, unsigned long long& nflop, const Lane& L) {
-  double* SU[2] = {sm, sm + 2 * 64 * C * C};
+  double* SU[2] = {sm, sm + img_doubles(C, RE)};
   const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
   const int go = 2 * x.off;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
@@ -1117,14 +1122,14 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
       if constexpr (!RE) A.im[r][i] = im;
     }
   bstore_img_l2(X + (size_t)(N - 1) * stride + go, A, x, L, l2_evict_first());
-  if (leader && N > 1) tma_grp_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * stride + go, C, &bar[(N - 1) & 1]);
+  if (leader && N > 1) tma_grp_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * stride + go, C, &bar[(N - 1) & 1], RE);
   uint32_t ph[2] = {0, 0};
   for (int k = N - 1; k >= 1; --k) {
     const int cur = k & 1;
     grp_sync(x);   // buffer cur^1 (read at step k+1) is free
     if (leader && k - 1 >= 1) {
       fence_proxy_async();
-      tma_grp_img(SU[cur ^ 1], U + (size_t)(k - 1) * stride + go, C, &bar[cur ^ 1]);
+      tma_grp_img(SU[cur ^ 1], U + (size_t)(k - 1) * stride + go, C, &bar[cur ^ 1], RE);
     }
     mbar_wait(&bar[cur], ph[cur]);
     ph[cur] ^= 1;
@@ -1177,7 +1182,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
                                              int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
                                              uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
                                              uint32_t tm, uint32_t ts, double* scr, int* bad, const Lane& L) {
-  const size_t IM = 2 * 64 * C * C;
+  constexpr size_t IM = img_doubles(C, RE);
   // shared scratch images (own strips only, re-read within the item): X, dX, A6, dA6
   double* gX = sX;
   double* gdX = sX + IM;
@@ -1381,7 +1386,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
                               double* __restrict__ grad, int* __restrict__ status, double* scr_cta, const Ctx& x,
                               double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr,
                               unsigned long long& nflop, const Lane& L) {
-  const int IM = 2 * 64 * C * C;
+  constexpr int IM = img_doubles(C, RE);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
   const int items = batch * N;
@@ -1392,8 +1397,8 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   auto prefetch = [&](int it) {   // group leader: bulk-copy X_{k+1} -> SN, P_k -> SD of item `it`
     if (leader && it < items) {
       fence_proxy_async();
-      tma_grp_img(sm + 2 * IM, X_img + (size_t)it * stride + 2 * x.off, C, &bars[0]);
-      tma_grp_img(sm, P_img + (size_t)it * stride + 2 * x.off, C, &bars[1]);
+      tma_grp_img(sm + 2 * IM, X_img + (size_t)it * stride + 2 * x.off, C, &bars[0], RE);
+      tma_grp_img(sm, P_img + (size_t)it * stride + 2 * x.off, C, &bars[1], RE);
     }
   };
   BR<C, R, RE> A, acc, Om;
@@ -1404,7 +1409,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     bcopy(A, Om);
     const int par = ((item - (int)blockIdx.x) / (int)gridDim.x) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
-                                               ph, sm + 3 * IM, sm + 3 * IM + 64 * C * C, tm, D.tstride[L.w], scr,
+                                               ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w], scr,
                                                bad_sh + par, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const int nx = item + gridDim.x;
@@ -1494,19 +1499,19 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
 
 // ------------------------------------------------------------------ launchers
 namespace {
-int grp_smem_doubles(BlkDev& D, int (*per)(int)) {
+int grp_smem_doubles(BlkDev& D, int (*per)(int, bool)) {
   int o = 0;
   for (int g = 0; g < D.ngroups; ++g) {
     D.soff[g] = o;
-    o += per(D.C[g]);
+    o += per(D.C[g], D.real[g] != 0);
     o = (o + 15) & ~15;   // 128-byte alignment of every region
   }
   return o;
 }
-int per3(int C) { return grp3_doubles(C); }
-int per_grad(int C) { return grp3_doubles(C) + 4 * 2 * 64 * C * C; }
-int per_pair(int C) { return 2 * 64 * C * C; }
-int per_chain(int C) { return 2 * 2 * 64 * C * C; }
+int per3(int C, bool re) { return grp3_doubles(C, re); }
+int per_grad(int C, bool re) { return grp3_doubles(C, re) + 4 * img_doubles(C, re); }
+int per_pair(int C, bool re) { return img_doubles(C, re); }
+int per_chain(int C, bool re) { return 2 * img_doubles(C, re); }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 cudaError_t set_smem(const void* fn, size_t bytes, size_t& attr) {
   if (bytes > attr) {
