@@ -354,9 +354,19 @@ def run_cfg3grad(args):
     sink = torch.zeros(1, dtype=torch.float64, device=dev)
     peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
 
+    plan = None
+    if args.structure == "blocks":
+        L0, Lc, Lcomm = qal.qal_build_liouvillian(H0, Hc, C, want_comm=True)
+        plan = qal.qal_block_plan_build(torch.cat([L0, Lc, Lcomm.reshape(-1, 64, 64)]), mirror=True)
+
     def step():
         u = qal.qal_sample_controls_sines(prm, prob.u_max, N, T, k0, k1 - k0).unsqueeze(0).contiguous()
         L0, Lc, Lcomm = qal.qal_build_liouvillian(H0, Hc, C, want_comm=True)
+        if plan is not None:
+            mats = [qal.qal_block_pack(plan, m, check=True)[0] for m in (L0, Lc, Lcomm)]
+            return driver.time_sharded_gradient(*mats, u, T, N, k0, ctrl_mode=qal.QAL_CTRL_NODES, plan=plan,
+                                                group_subsegments=8192,
+                                                cotangent=lambda Lm: qal.qal_block_fidelity_cotangent(plan, V))
         return driver.time_sharded_gradient(L0, Lc, Lcomm, u, T, N, k0, ctrl_mode=qal.QAL_CTRL_NODES,
                                             cotangent=lambda Lm: qal.qal_fidelity_cotangent(V))
 
@@ -384,16 +394,18 @@ def run_cfg3grad(args):
     ms = t.item()
     prods = counters.cpu().tolist()
     if rank == 0:
-        flops = sum(driver.stage_flops(x) for x in prods) / args.steps
+        flops = sum(driver.stage_flops(x, st) for x, st in zip(prods, qal.STAGES)) / args.steps
+        roofline, split, _ = roofline_of(stages, prods, args.steps, peak_tf, None)
         line = {"metric": METRIC, "value": N * args.steps / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": "configs[3] gradient (NEXT f2): 2^20 NODES slices, fidelity gradient w.r.t. "
                                        "all 2 x 2 x 2^20 node values, time-sharded; 64-slice sub-segments, log-depth prefix/suffix "
-                                       "scans, one batched VJP"},
+                                       "scans, one batched VJP",
+                           "structure": "coherence blocks (packed)" if plan is not None else "dense 64x64"},
                 "pct_fp64_roofline": flops / (ms / args.steps * 1e-3) / 1e12 / peak_tf,
-                "products_per_slice": sum(prods) / (N * args.steps),
+                "roofline": roofline, "stage_split": split,
                 "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
                 "fp64_peak_tflops": peak_tf, "clocks": clk}
         print(json.dumps(line), flush=True)

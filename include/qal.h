@@ -380,6 +380,33 @@ int qal_block_fidelity_grad(const qal_block_plan *plan, int batch, int n_slices,
                             const qal_c128 *V, double *F, double *grad, qal_c128 *Lambda_packed, int *status,
                             void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * The reverse pass of the block path for a general objective (qal_propagator_forward + _vjp on packed
+ * operands): forward over slices k0 .. k0+count-1 (P_init = I), then
+ * grad = dL/du for dL = Re Tr(C[b] dLambda[b]) with C packed [batch][packed] (pack it with
+ * qal_block_pack, or build it with the block ops).  C must preserve Hermiticity (every cotangent of a
+ * real objective of a Hermiticity-preserving Lambda does: S_V^dag, the Eq. 16-17 loss cotangent, the
+ * time-sharded seeds), because the plan stores one block of each mirror pair and the q = 0 block in the
+ * real basis.  Lambda_packed optional out.  ws >= qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count).
+ */
+int qal_block_propagator_vjp(const qal_block_plan *plan, int batch, int n_slices, double T, int k0, int count,
+                             int magnus_order, int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0p,
+                             long long L0p_stride, const qal_c128 *Lcp, const qal_c128 *Lcommp,
+                             long long Lcommp_stride, const qal_c128 *Cp, double *grad, qal_c128 *Lambda_packed,
+                             int *status, void *ws, size_t ws_bytes, void *stream);
+
+/* qal_ordered_scan on packed matrices (exclusive prefix / suffix products, Hillis-Steele levels).
+ * ws >= 4 * batch * count * plan->packed * 16 bytes. */
+int qal_block_ordered_scan(const qal_block_plan *plan, int batch, int count, const qal_c128 *U,
+                           qal_c128 *prefix_excl, qal_c128 *suffix_excl, void *ws, size_t ws_bytes, void *stream);
+
+/* qal_batched_matmul on packed matrices: C[i] = A[i] B[i], strides plan->packed or 0 (broadcast). */
+int qal_block_batched_matmul(const qal_block_plan *plan, int count, const qal_c128 *A, long long strideA,
+                             const qal_c128 *B, long long strideB, qal_c128 *C, void *stream);
+
+/* qal_fidelity_cotangent in packed form: C = S_V^dag / d^2 on the stored blocks (A8). */
+int qal_block_fidelity_cotangent(const qal_block_plan *plan, const qal_c128 *V, qal_c128 *C, void *stream);
+
 size_t qal_block_workspace_bytes(const qal_block_plan *plan, int op, int batch, int n_slices);
 
 /*

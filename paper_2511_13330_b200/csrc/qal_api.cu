@@ -247,7 +247,8 @@ int run_blk_tree(const qal_block_plan* p, int batch, int count, const double2* U
 
 size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices);
 int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
-                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st);
+                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st,
+                           const double2* Cseed = nullptr);
 
 // chunk of the block forward fold: keep >= ~4 CTAs per SM busy, chunk | n_slices
 int blk_default_chunk(int batch, int n_slices) {
@@ -739,6 +740,7 @@ size_t qal_block_workspace_bytes(const qal_block_plan* plan, int op, int batch, 
       return (size_t)batch * nch * mb + blk_tree_ws_bytes(plan, batch, nch) + (size_t)batch * mb;
     }
     case QAL_OP_FIDELITY_GRAD:
+    case QAL_OP_VJP:
       return blk_grad_ws_bytes(plan, batch, n_slices);
     default: return 0;
   }
@@ -776,6 +778,58 @@ int qal_block_fidelity_grad(const qal_block_plan* plan, int batch, int n_slices,
   }
   return blk_fidelity_grad_impl(plan, batch, c, D2(V), F, grad, D2(Lambda_packed), status, ws, st);
 }
+
+int qal_block_propagator_vjp(const qal_block_plan* plan, int batch, int n_slices, double T, int k0, int count,
+                             int magnus_order, int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0p,
+                             long long L0p_stride, const qal_c128* Lcp, const qal_c128* Lcommp,
+                             long long Lcommp_stride, const qal_c128* Cp, double* grad, qal_c128* Lambda_packed,
+                             int* status, void* ws, size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  BlkCommon c;
+  int rc = check_block_basis(plan, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0p, L0p_stride, Lcp,
+                             Lcommp, Lcommp_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!Cp || !grad) return QAL_ERR_NULL;
+  c.G.count = count;
+  if (!ws || ws_bytes < qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count)) return QAL_ERR_WORKSPACE;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+  return blk_fidelity_grad_impl(plan, batch, c, nullptr, nullptr, grad, D2(Lambda_packed), status, ws, st, D2(Cp));
+}
+
+int qal_block_ordered_scan(const qal_block_plan* plan, int batch, int count, const qal_c128* U,
+                           qal_c128* prefix_excl, qal_c128* suffix_excl, void* ws, size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (batch < 1 || count < 1) return QAL_ERR_EMPTY;
+  if (!U || (!prefix_excl && !suffix_excl)) return QAL_ERR_NULL;
+  if (!ws || ws_bytes < 4 * (size_t)batch * count * blk_mat_bytes(plan)) return QAL_ERR_WORKSPACE;
+  return cuda_rc(launch_blk_scan(*plan, batch, count, D2(U), D2(prefix_excl), D2(suffix_excl),
+                                 reinterpret_cast<double2*>(ws), S(stream)));
+}
+
+int qal_block_batched_matmul(const qal_block_plan* plan, int count, const qal_c128* A, long long strideA,
+                             const qal_c128* B, long long strideB, qal_c128* C, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (!A || !B || !C) return QAL_ERR_NULL;
+  if ((strideA != 0 && strideA != (long long)plan->packed) || (strideB != 0 && strideB != (long long)plan->packed))
+    return QAL_ERR_DIM;
+  return cuda_rc(launch_blk_batched_mm(*plan, count, D2(A), strideA, D2(B), strideB, D2(C), S(stream)));
+}
+
+int qal_block_fidelity_cotangent(const qal_block_plan* plan, const qal_c128* V, qal_c128* C, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (!V || !C) return QAL_ERR_NULL;
+  return cuda_rc(launch_blk_fidelity_cotangent(*plan, D2(V), D2(C), S(stream)));
+}
 }  // extern "C"
 
 namespace {
@@ -785,7 +839,8 @@ size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices) {
 }
 // forward (U_k and prefix P_k images, Lambda) -> fidelity -> suffix chain (X_{k+1}) -> gradient slices
 int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
-                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st) {
+                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st,
+                           const double2* Cseed) {
   const size_t seq = (size_t)batch * c.G.count * 2 * p->packed;   // doubles per image sequence
   double* U = reinterpret_cast<double*>(ws);
   double* P = U + seq;
@@ -795,9 +850,10 @@ int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& 
   double2* lam = Lam ? Lam : lam_tmp;
   BlkFwdOut O{U, lam, c.G.count, status, P};
   if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_blk_suffix_chain(*p, batch, c.G.count, U, V, X, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_blk_grad_slices(*p, batch, c.B, c.G, P, X, grad, status, scratch, st) != cudaSuccess)
+  if (F && launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_blk_suffix_chain(*p, batch, c.G.count, U, V, Cseed, X, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_blk_grad_slices(*p, batch, c.B, c.G, P, X, grad, status, scratch, Cseed ? 1.0 : 1.0 / 64.0, st) !=
+      cudaSuccess)
     return QAL_ERR_CUDA;
   return QAL_OK;
 }

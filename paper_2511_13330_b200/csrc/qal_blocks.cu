@@ -1085,13 +1085,17 @@ __device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int 
 // X_N = S_V^dag on the stored blocks, X_k = X_{k+1} U_k; X_img[b][k-1] = X_k (k = 1..N).
 // One CTA per pulse; the groups run independently; U_k streamed by per-group TMA (double buffer).
 template <int C, int R, int KS, bool RE>
-__device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, double* X, const Ctx& x,
-                                double* sm, uint64_t* bar, unsigned long long& nflop, const Lane& L) {
+__device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, const double2* Cseed,
+                                double* X, const Ctx& x, double* sm, uint64_t* bar, unsigned long long& nflop,
+                                const Lane& L) {
   double* SU[2] = {sm, sm + img_doubles(C, RE)};
   const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
   const int go = 2 * x.off;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   BR<C, R, RE> A, acc;
+  if (Cseed) {   // general cotangent (packed, Hermiticity preserving): dL = Re Tr(C dLambda)
+    bload_nat(A, Cseed + x.off, x, L);
+  } else
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -1144,6 +1148,7 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
 __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev D, int N,
                                                                           const double* __restrict__ U_img,
                                                                           const double2* __restrict__ V,
+                                                                          const double2* __restrict__ Cseed,
                                                                           double* __restrict__ X_img,
                                                                           unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
@@ -1164,7 +1169,8 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
     double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V, X_img + base, x, sm, bars[x.g], nflop, L);
+    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V,
+                 Cseed ? Cseed + (size_t)blockIdx.x * D.packed : nullptr, X_img + base, x, sm, bars[x.g], nflop, L);
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
 }
@@ -1384,7 +1390,7 @@ template <int C, int R, int KS, bool RE>
 __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, const SliceGrid& G,
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
                               double* __restrict__ grad, int* __restrict__ status, double* scr_cta, const Ctx& x,
-                              double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr,
+                              double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr, double gscale,
                               unsigned long long& nflop, const Lane& L) {
   constexpr int IM = img_doubles(C, RE);
   const size_t stride = 2 * (size_t)D.packed;
@@ -1429,7 +1435,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     if (L.lane == 0) {
       const double* T = rt + BLK_MAX_WARPS * BLK_TR_MAX;
       const int J = B.J;
-      const double inv_d2 = 1.0 / 64.0;
+      const double inv_d2 = gscale;   // 1/d^2 for the fidelity, 1 for a general cotangent
       if (G.mode == 0) {
         double* gg = grad + ((size_t)b * N + k) * J;
         for (int j = 0; j < J; ++j) gg[j] = G.h * T[j] * inv_d2;
@@ -1464,8 +1470,8 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
                                                                const double* __restrict__ P_img,
                                                                const double* __restrict__ X_img,
                                                                double* __restrict__ grad, int* __restrict__ status,
-                                                               double* __restrict__ scratch, int tmem_cols,
-                                                               unsigned long long* ctr) {
+                                                               double* __restrict__ scratch, double gscale,
+                                                               int tmem_cols, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];   // [0]: X_{k+1} -> SN, [1]: P_k -> SD
   __shared__ double red_tr[2 * BLK_TR_BUF];
@@ -1489,12 +1495,105 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   const Ctx x = ctx_of(D, T);
   double* sm = smem + D.soff[x.g];
   BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status, scr_cta,
-               x, sm, bars[x.g], tm, bad_sh, red_tr, nflop, L);
+               x, sm, bars[x.g], tm, bad_sh, red_tr, gscale, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   if (L.w == 0) blk_tmem_dealloc(tmem_base_sh, tmem_cols);
+}
+
+// ------------------------------------------------------------------ packed scans / batched products
+// One Hillis-Steele level over per-pulse packed sequences (later factor on the LEFT, Eq. 15):
+// prefix (dir 0): out[s] = in[s] in[s-d]; suffix (dir 1): out[s] = in[s+d] in[s]; else copy.
+__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_scan_level(BlkDev D, int cnt, int dd, int dir,
+                                                                        const double2* __restrict__ in,
+                                                                        double2* __restrict__ out,
+                                                                        unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  const Lane L = lane_id();
+  const int b = blockIdx.x / cnt, s = blockIdx.x % cnt;
+  const double2* src = in + (size_t)b * cnt * D.packed;
+  double2* dst = out + ((size_t)b * cnt + s) * D.packed;
+  const int partner = dir == 0 ? s - dd : s + dd;
+  if (partner < 0 || partner >= cnt) {
+    for (int e = threadIdx.x; e < D.packed; e += blockDim.x) dst[e] = src[(size_t)s * D.packed + e];
+    return;
+  }
+  const int later = dir == 0 ? s : partner, earlier = dir == 0 ? partner : s;
+  const BlkTask T = D.task[L.w][0];
+  const Ctx x = ctx_of(D, T);
+  BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_pair_task, src + (size_t)later * D.packed,
+               src + (size_t)earlier * D.packed, dst, x, smem + D.soff[x.g], L);
+  if (ctr && x.rt0 == 0 && L.lane == 0) atomicAdd(ctr, D.gflops[x.g]);
+}
+
+// packed identity: 1 on the diagonal of every group block (padding rows included, harmlessly)
+__device__ __forceinline__ double2 packed_identity(const BlkDev& D, int e) {
+  const int g = group_of_off(D, e);
+  const int P = 8 * D.C[g], loc = e - D.off[g];
+  return make_double2((loc / P) == (loc % P) ? 1.0 : 0.0, 0.0);
+}
+// exclusive outputs: pre[s] = incl_pre[s-1] (I at s = 0), suf[s] = incl_suf[s+1] (I at s = cnt-1)
+__global__ void k_blk_scan_shift(BlkDev D, int cnt, const double2* __restrict__ ip, const double2* __restrict__ is,
+                                 double2* __restrict__ pre, double2* __restrict__ suf) {
+  const int b = blockIdx.x / cnt, s = blockIdx.x % cnt;
+  double2* p = pre ? pre + ((size_t)b * cnt + s) * D.packed : nullptr;
+  double2* q = suf ? suf + ((size_t)b * cnt + s) * D.packed : nullptr;
+  const double2* ps = s > 0 ? ip + ((size_t)b * cnt + s - 1) * D.packed : nullptr;
+  const double2* qs = s + 1 < cnt ? is + ((size_t)b * cnt + s + 1) * D.packed : nullptr;
+  for (int e = threadIdx.x; e < D.packed; e += blockDim.x) {
+    const double2 id = packed_identity(D, e);
+    if (p) p[e] = ps ? ps[e] : id;
+    if (q) q[e] = qs ? qs[e] : id;
+  }
+}
+
+// C[i] = A[i] B[i] (packed), element strides sa / sb = packed or 0 (broadcast)
+__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_batched_mm(BlkDev D, const double2* __restrict__ A,
+                                                                        long long sa, const double2* __restrict__ B,
+                                                                        long long sb, double2* __restrict__ Cout,
+                                                                        unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  const Lane L = lane_id();
+  const size_t i = blockIdx.x;
+  const BlkTask T = D.task[L.w][0];
+  const Ctx x = ctx_of(D, T);
+  BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_pair_task, A + i * sa, B + i * sb, Cout + i * D.packed, x,
+               smem + D.soff[x.g], L);
+  if (ctr && x.rt0 == 0 && L.lane == 0) atomicAdd(ctr, D.gflops[x.g]);
+}
+
+// fidelity cotangent C = S_V^dag / d^2 (A8) in packed form: complex groups S_V^dag[a][c]; real groups
+// (T^dag S_V^dag T)[r][c] = S'[c][r] with S' = T^dag S_V T real.  dF = Re Tr(C dLambda).
+__global__ void k_blk_fidelity_cotangent(BlkDev D, const double2* __restrict__ V, double2* __restrict__ Cout) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < D.packed; e += gridDim.x * blockDim.x) {
+    const int g = group_of_off(D, e);
+    const int P = 8 * D.C[g], loc = e - D.off[g];
+    const int gr = D.row0[g] + loc / P, gc = D.row0[g] + loc % P;
+    double re = 0.0, im = 0.0;
+    if (D.perm[gr] >= 0 && D.perm[gc] >= 0) {
+      if (D.real[g]) {
+        const TTerms ta = row_terms(D, gc), tb = row_terms(D, gr);
+        for (int p = 0; p < ta.n; ++p)
+          for (int q = 0; q < tb.n; ++q) {
+            const int A = ta.R[p], Bn = tb.R[q];
+            const int i1 = A & 7, j1 = A >> 3, k1 = Bn & 7, l1 = Bn >> 3;
+            const double2 vj = V[j1 * 8 + l1], vi = V[i1 * 8 + k1];
+            const double sr = vj.x * vi.x + vj.y * vi.y, si = vj.x * vi.y - vj.y * vi.x;
+            const double xr = ta.tr[p] * sr + ta.ti[p] * si, xi = ta.tr[p] * si - ta.ti[p] * sr;
+            re += xr * tb.tr[q] - xi * tb.ti[q];
+          }
+      } else {
+        const int a = D.perm[gr], c = D.perm[gc];
+        const int kk = a & 7, l = a >> 3, ii = c & 7, j = c >> 3;
+        const double2 vjl = V[j * 8 + l], vik = V[ii * 8 + kk];
+        re = vjl.x * vik.x + vjl.y * vik.y;   // S_V^dag[a][c] = V[j][l] conj(V[i][k])
+        im = vjl.y * vik.x - vjl.x * vik.y;
+      }
+    }
+    Cout[e] = make_double2(re / 64.0, im / 64.0);
+  }
 }
 
 // ------------------------------------------------------------------ launchers
@@ -1556,7 +1655,7 @@ cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, c
 }
 
 cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
-                                    const double2* V, double* X_img, cudaStream_t st) {
+                                    const double2* V, const double2* Cseed, double* X_img, cudaStream_t st) {
   BlkDev D;
   if (!to_dev(p, D)) return cudaErrorInvalidValue;
   const size_t bytes = (size_t)grp_smem_doubles(D, per_chain) * 8;
@@ -1564,7 +1663,7 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
   cudaError_t e = set_smem((const void*)k_blk_suffix_chain, bytes, attr);
   if (e != cudaSuccess) return e;
   prof_pre(ST_BLK_SUFFIX, st);
-  k_blk_suffix_chain<<<batch, 32 * D.nwarps, bytes, st>>>(D, N, U_img, V, X_img, prof_counter(ST_BLK_SUFFIX));
+  k_blk_suffix_chain<<<batch, 32 * D.nwarps, bytes, st>>>(D, N, U_img, V, Cseed, X_img, prof_counter(ST_BLK_SUFFIX));
   prof_post(ST_BLK_SUFFIX, st);
   ++launch_counter();
   return cudaGetLastError();
@@ -1598,7 +1697,7 @@ size_t blk_grad_scratch_bytes(const qal_block_plan& p) {
 
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
-                                   double* scratch, cudaStream_t st) {
+                                   double* scratch, double gscale, cudaStream_t st) {
   BlkDev D;
   if (!to_dev(p, D)) return cudaErrorInvalidValue;
   const size_t bytes = (size_t)grp_smem_doubles(D, per_grad) * 8;
@@ -1609,9 +1708,57 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
   const int gmax = blk_grad_grid(D);
   const int grid = items < gmax ? items : gmax;
   prof_pre(ST_BLK_GRAD, st);
-  k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch,
+  k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, gscale,
                                                          tmem_cols_for(D), prof_counter(ST_BLK_GRAD));
   prof_post(ST_BLK_GRAD, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_scan(const qal_block_plan& p, int batch, int cnt, const double2* U, double2* pre, double2* suf,
+                            double2* ws, cudaStream_t st) {
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per_pair) * 8;
+  const size_t seq = (size_t)batch * cnt * p.packed;
+  double2* buf[2][2] = {{ws, ws + seq}, {ws + 2 * seq, ws + 3 * seq}};   // [dir][ping-pong]
+  const double2* res[2] = {U, U};
+  for (int dir = 0; dir < 2; ++dir) {
+    if ((dir == 0 && !pre) || (dir == 1 && !suf)) continue;
+    const double2* in = U;
+    int pp = 0;
+    for (int dd = 1; dd < cnt; dd <<= 1) {
+      prof_pre(ST_BLK_TREE, st);
+      k_blk_scan_level<<<batch * cnt, 32 * D.nwarps, bytes, st>>>(D, cnt, dd, dir, in, buf[dir][pp],
+                                                                   prof_counter(ST_BLK_TREE));
+      prof_post(ST_BLK_TREE, st);
+      ++launch_counter();
+      in = buf[dir][pp];
+      pp ^= 1;
+    }
+    res[dir] = in;
+  }
+  k_blk_scan_shift<<<batch * cnt, 128, 0, st>>>(D, cnt, res[0], res[1], pre, suf);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_batched_mm(const qal_block_plan& p, int count, const double2* A, long long sa,
+                                  const double2* B, long long sb, double2* Cout, cudaStream_t st) {
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)grp_smem_doubles(D, per_pair) * 8;
+  prof_pre(ST_BLK_TREE, st);
+  k_blk_batched_mm<<<count, 32 * D.nwarps, bytes, st>>>(D, A, sa, B, sb, Cout, prof_counter(ST_BLK_TREE));
+  prof_post(ST_BLK_TREE, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_fidelity_cotangent(const qal_block_plan& p, const double2* V, double2* Cout, cudaStream_t st) {
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  k_blk_fidelity_cotangent<<<4, 256, 0, st>>>(D, V, Cout);
   ++launch_counter();
   return cudaGetLastError();
 }

@@ -65,10 +65,15 @@ cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* n
 cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2* packed, double2* nat,
                               cudaStream_t st);
 cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
-                                    const double2* V, double* X_img, cudaStream_t st);
+                                    const double2* V, const double2* Cseed, double* X_img, cudaStream_t st);
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
-                                   double* scratch, cudaStream_t st);
+                                   double* scratch, double gscale, cudaStream_t st);
+cudaError_t launch_blk_scan(const qal_block_plan& p, int batch, int cnt, const double2* U, double2* pre, double2* suf,
+                            double2* ws, cudaStream_t st);
+cudaError_t launch_blk_batched_mm(const qal_block_plan& p, int count, const double2* A, long long sa,
+                                  const double2* B, long long sb, double2* Cout, cudaStream_t st);
+cudaError_t launch_blk_fidelity_cotangent(const qal_block_plan& p, const double2* V, double2* Cout, cudaStream_t st);
 size_t blk_grad_scratch_bytes(const qal_block_plan& p);
 cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
                                 cudaStream_t st);

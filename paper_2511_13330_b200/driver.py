@@ -260,7 +260,7 @@ def segment_seeds(Qs, C, product):
 
 
 def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, cotangent, magnus_order=4,
-                          sub=64, group_subsegments=2048, group=None, stream=None):
+                          sub=64, group_subsegments=2048, group=None, stream=None, plan=None):
     """NEXT f2 -- gradient of an objective over a long horizon, time-sharded over the ranks, with
     log-depth parallelism inside each rank.  Rank r owns slices [k0, k0 + count) of ONE pulse
     (u_local [1][count][...]):
@@ -272,11 +272,17 @@ def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode,
       4. sub-segment seeds pre_s C_r suf_s (segment_seeds, batched);
       5. the VJP of all sub-segments as one batch of short "pulses" (qal_propagator_forward / _vjp),
          in groups so the stored images fit HBM.
+    With a block plan (coherence-block path) the basis is packed, every matrix above is packed, the
+    cotangent must return a packed Hermiticity-preserving C, and step 5 is qal_block_propagator_vjp.
     Returns (Lambda, grad of the local slices)."""
     count = u_local.shape[1]
     if count % sub:
         raise ValueError("sub must divide the rank's slice count")
     S = count // sub
+    if plan is not None:
+        return _time_sharded_gradient_blocks(plan, L0, Lc, Lcomm, u_local, T, n_slices, k0, ctrl_mode=ctrl_mode,
+                                             cotangent=cotangent, magnus_order=magnus_order, sub=sub,
+                                             group_subsegments=group_subsegments, group=group, stream=stream)
     _, parts = qal.qal_magnus_expm_slices(L0, Lc, u_local, T, n_slices, k0=k0, count=count,
                                           magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcomm=Lcomm, chunk=sub,
                                           stream=stream)
@@ -304,6 +310,37 @@ def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode,
         sess.forward()
         grad[g0:g1] = sess.vjp(seeds[g0:g1].contiguous())
         del sess
+    return Lam, grad.reshape(u_local.shape)
+
+
+def _time_sharded_gradient_blocks(plan, L0p, Lcp, Lcommp, u_local, T, n_slices, k0, *, ctrl_mode, cotangent,
+                                  magnus_order, sub, group_subsegments, group, stream):
+    count = u_local.shape[1]
+    S = count // sub
+    bmm = lambda A, B: qal.qal_block_batched_matmul(plan, A, B, stream=stream)  # noqa: E731
+    parts = qal.qal_block_expm_slices(plan, L0p, Lcp, u_local, T, n_slices, k0=k0, count=count,
+                                      magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcommp=Lcommp, chunk=sub,
+                                      stream=stream)                                   # [1][S][packed]
+    pre, suf = qal.qal_block_ordered_scan(plan, parts, stream=stream)
+    Q_rank = bmm(parts[0, S - 1], pre[0, S - 1])[0]
+    ranks = gather_partials(Q_rank, group)                                             # [G][packed]
+    rank = _rank(group)
+    Lam = ordered_combine(ranks, stream=stream, plan=plan)
+    C = cotangent(Lam)
+    if rank > 0:
+        C = bmm(ordered_combine(ranks[:rank], stream=stream, plan=plan), C)[0]
+    if rank + 1 < ranks.shape[0]:
+        C = bmm(C, ordered_combine(ranks[rank + 1:], stream=stream, plan=plan))[0]
+    seeds = bmm(pre[0], bmm(C, suf[0]))                                                # pre_s C_r suf_s
+    del pre, suf, parts
+    us = u_local[0].reshape((S, sub) + tuple(u_local.shape[2:]))
+    grad = torch.empty_like(us)
+    for g0 in range(0, S, group_subsegments):
+        g1 = min(S, g0 + group_subsegments)
+        g, _ = qal.qal_block_propagator_vjp(plan, L0p, Lcp, us[g0:g1].contiguous(), T, n_slices,
+                                           seeds[g0:g1].contiguous(), magnus_order=magnus_order,
+                                           ctrl_mode=ctrl_mode, Lcommp=Lcommp, stream=stream)
+        grad[g0:g1] = g
     return Lam, grad.reshape(u_local.shape)
 
 

@@ -106,6 +106,19 @@ _EXPORTS = {
                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                                 ctypes.c_void_p]),
     "qal_block_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "qal_block_propagator_vjp": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                 ctypes.c_void_p]),
+    "qal_block_ordered_scan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                               ctypes.c_void_p]),
+    "qal_block_batched_matmul": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
+                                                 ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_block_fidelity_cotangent": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                     ctypes.c_void_p]),
     "qal_profile_begin": (ctypes.c_int, [ctypes.c_void_p]),
     "qal_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -556,3 +569,65 @@ def qal_block_fidelity_grad(plan: BlockPlan, L0p, Lcp, u, T, n_slices, V, *, mag
                                         _ptr(g), _ptr(Lam), _ptr(status), _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "qal_block_fidelity_grad")
     return F, g, Lam
+
+
+def qal_block_propagator_vjp(plan: BlockPlan, L0p, Lcp, u, T, n_slices, Cp, *, k0=0, count=None, magnus_order=4,
+                             ctrl_mode=QAL_CTRL_PWC, Lcommp=None, want_Lambda=False, status=None, ws=None,
+                             stream=None):
+    """dL/du for dL = Re Tr(C dLambda) over slices k0..k0+count-1 (packed, Hermiticity-preserving C [B][packed]);
+    returns (grad (layout of u), packed Lambda or None)."""
+    c128 = torch.complex128
+    L0p = _dev(L0p, c128, "L0p")
+    Lcp = _dev(Lcp, c128, "Lcp")
+    u = _dev(u, torch.float64, "u")
+    Cp = _dev(Cp, c128, "Cp")
+    B, J = u.shape[0], Lcp.shape[0]
+    count = u.shape[1] if count is None else count
+    g = torch.empty_like(u)
+    Lam = torch.empty((B, plan.packed), dtype=c128, device=u.device) if want_Lambda else None
+    wsb = block_workspace_bytes(plan, QAL_OP_VJP, B, count)
+    if ws is None or ws.numel() < wsb:
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=u.device)
+    L0s = 0 if L0p.shape[0] == 1 else plan.packed
+    Lcs = 0
+    if Lcommp is not None:
+        Lcommp = _dev(Lcommp, c128, "Lcommp")
+        Lcs = 0 if Lcommp.shape[0] == 1 else n_comm(J) * plan.packed
+    rc = load().qal_block_propagator_vjp(ctypes.byref(plan), B, n_slices, float(T), k0, count, magnus_order,
+                                         ctrl_mode, J, _ptr(u), _ptr(L0p), L0s, _ptr(Lcp), _ptr(Lcommp), Lcs,
+                                         _ptr(Cp), _ptr(g), _ptr(Lam), _ptr(status), _ptr(ws), ws.numel(),
+                                         _stream(stream))
+    _check(rc, "qal_block_propagator_vjp")
+    return g, Lam
+
+
+def qal_block_ordered_scan(plan: BlockPlan, U, want_prefix=True, want_suffix=True, stream=None):
+    U = _dev(U, torch.complex128, "U")
+    B, cnt = U.shape[0], U.shape[1]
+    pre = torch.empty_like(U) if want_prefix else None
+    suf = torch.empty_like(U) if want_suffix else None
+    ws = torch.empty(4 * B * cnt * plan.packed * 16, dtype=torch.uint8, device=U.device)
+    _check(load().qal_block_ordered_scan(ctypes.byref(plan), B, cnt, _ptr(U), _ptr(pre), _ptr(suf), _ptr(ws),
+                                         ws.numel(), _stream(stream)), "qal_block_ordered_scan")
+    return pre, suf
+
+
+def qal_block_batched_matmul(plan: BlockPlan, A, B, stream=None):
+    """C[i] = A[i] B[i] on packed matrices [count][packed]; a [packed] (or [1][packed]) operand broadcasts."""
+    A = _dev(A, torch.complex128, "A").reshape(-1, plan.packed)
+    B = _dev(B, torch.complex128, "B").reshape(-1, plan.packed)
+    count = max(A.shape[0], B.shape[0])
+    C = torch.empty((count, plan.packed), dtype=torch.complex128, device=A.device)
+    sa = 0 if A.shape[0] == 1 else plan.packed
+    sb = 0 if B.shape[0] == 1 else plan.packed
+    _check(load().qal_block_batched_matmul(ctypes.byref(plan), count, _ptr(A), sa, _ptr(B), sb, _ptr(C),
+                                           _stream(stream)), "qal_block_batched_matmul")
+    return C
+
+
+def qal_block_fidelity_cotangent(plan: BlockPlan, V, stream=None):
+    V = _dev(V, torch.complex128, "V")
+    C = torch.empty(plan.packed, dtype=torch.complex128, device=V.device)
+    _check(load().qal_block_fidelity_cotangent(ctypes.byref(plan), _ptr(V), _ptr(C), _stream(stream)),
+           "qal_block_fidelity_cotangent")
+    return C

@@ -287,3 +287,67 @@ def test_time_shard_propagator_blocks_matches_oracle(torch_cuda, qal, oracle):
     F = qal.qal_block_fidelity(plan, Lam_p.unsqueeze(0), dev(torch, p.V)).item()
     Fr = oracle.fidelity(Lam, p.V)
     assert abs(F - Fr) / abs(Fr) <= TOL_PROP
+
+
+# ------------------------------------------------------------------ general cotangent (f1/f2 on the blocks)
+def test_block_vjp_with_fidelity_cotangent_equals_fidelity_gradient(torch_cuda, qal):
+    torch = torch_cuda
+    p = qi.cfg2(batch=5, N=48, T=200.0 * 48 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    V = dev(torch, p.V)
+    _, gF, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, V)
+    C = qal.qal_block_fidelity_cotangent(plan, V).unsqueeze(0).repeat(5, 1).contiguous()
+    gC, _ = qal.qal_block_propagator_vjp(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, C)
+    err = ((gC - gF).reshape(5, -1).norm(dim=1) / gF.reshape(5, -1).norm(dim=1)).max().item()
+    assert err <= 1e-13, err
+
+
+def test_block_vjp_general_cotangent_matches_oracle(torch_cuda, qal, oracle):
+    """A Hermiticity-preserving cotangent (C = Lambda_target^dag, the superoperator of a CPTP map)
+    packed with qal_block_pack vs the oracle's per-direction vjp (O7 with a general seed)."""
+    torch = torch_cuda
+    p = qi.cfg0(N=32, T=100.0 * 32 / 256)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    q = qi.cfg0(N=8, T=37.0)
+    Lt = oracle.propagate(rL0, rLc, q.u[0], q.T, q.N)            # a CPTP superoperator: HP
+    Cn = Lt.conj().T.copy()
+    gr, _ = oracle.vjp(rL0, rLc, p.u[0], p.T, p.N, Cn)
+    Cp, flag = qal.qal_block_pack(plan, dev(torch, Cn[None]))
+    assert flag.item() == 0
+    g, _ = qal.qal_block_propagator_vjp(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, Cp)
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
+
+
+def test_block_scan_and_batched_matmul(torch_cuda, qal, oracle):
+    torch = torch_cuda
+    p = qi.cfg0(N=11, T=100.0 * 11 / 256)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    Us = qal.qal_block_expm_slices(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, chunk=1)        # [1][11][packed]
+    pre, suf = qal.qal_block_ordered_scan(plan, Us)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    _, Un = oracle.propagate(rL0, rLc, p.u[0], p.T, p.N, store=True)
+    for s in (0, 4, 10):
+        ref_pre = oracle.ordered_product(Un[:s]) if s > 0 else np.eye(64)
+        ref_suf = oracle.ordered_product(Un[s + 1:]) if s + 1 < 11 else np.eye(64)
+        assert relfro(qal.qal_block_unpack(plan, pre[0, s:s + 1])[0].cpu().numpy(), ref_pre) <= 1e-12
+        assert relfro(qal.qal_block_unpack(plan, suf[0, s:s + 1])[0].cpu().numpy(), ref_suf) <= 1e-12
+    AB = qal.qal_block_batched_matmul(plan, Us[0, 3:4], Us[0, 2:3])
+    assert relfro(qal.qal_block_unpack(plan, AB)[0].cpu().numpy(), Un[3] @ Un[2]) <= 1e-13
+
+
+def test_time_sharded_gradient_blocks_matches_oracle(torch_cuda, qal, oracle):
+    """NEXT f2 on the block path (G = 1): segmented, scanned, one batched block VJP."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg3()
+    N, T = 256, 150.0
+    u = oracle.sines_nodes(p.sines, p.u_max, N, T)[None]
+    plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
+    V = dev(torch, p.V)
+    Lam, g = driver.time_sharded_gradient(L0p, Lcp, Lcommp, dev(torch, u), T, N, 0, ctrl_mode=1, sub=32, plan=plan,
+                                          cotangent=lambda Lm: qal.qal_block_fidelity_cotangent(plan, V))
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Fr, gr, Lr = oracle.gradient(rL0, rLc, u[0], T, N, p.V, mode=1)
+    assert relfro(qal.qal_block_unpack(plan, Lam.unsqueeze(0))[0].cpu().numpy(), Lr) <= TOL_PROP
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
