@@ -214,21 +214,48 @@ def time_shard_propagator(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode,
 
 
 def calibrate(H0, Hc, C, u0, T, Pproj, G, *, iters=200, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8,
-              magnus_order=4, stream=None):
+              magnus_order=4, stream=None, structure="dense"):
     """NEXT f1 -- the paper's calibration loop: Adam over the PWC coefficient matrix
     u [B][M][J] minimising the Eq. 16-17 loss 1/4 ||P^dag Lambda P - G||_F^2, every step on the
     device: forward (qal_propagator_forward) -> loss + cotangent (qal_logical_loss) -> gradient
     (qal_propagator_vjp, one adjoint Frechet derivative per slice; the paper's autodiff hit a
     memory wall here) -> qal_adam_step.  Returns dict(u, loss_history [iters, B],
-    best_u, best_loss); no host synchronisation inside the loop."""
+    best_u, best_loss); no host synchronisation inside the loop.
+
+    structure="blocks": the coherence-block path.  The Eq. 16-17 cotangent
+    C = 1/2 P (Pi - G)^dag P^dag preserves Hermiticity when G is real (Pi = P^dag Lambda P is real for a
+    Hermiticity-preserving Lambda and the Hermitian DFS projectors), so it packs exactly; the forward of
+    each step is recomputed inside qal_block_propagator_vjp (the block path has no split forward/vjp)."""
     u = u0.clone().contiguous()
     L0, Lc, _ = qal.qal_build_liouvillian(H0, Hc, C, stream=stream)
-    sess = qal.GradientSession(L0, Lc, u, T, u.shape[1], magnus_order=magnus_order, stream=stream)
     m = torch.zeros_like(u)
     v = torch.zeros_like(u)
     hist = torch.empty((iters, u.shape[0]), dtype=F64, device=u.device)
     best = torch.full((u.shape[0],), float("inf"), dtype=F64, device=u.device)
     best_u = u.clone()
+    N = u.shape[1]
+    if structure == "blocks":
+        if G.is_complex() and bool((G.imag != 0).any()):
+            raise ValueError("the block path needs a real logical target G (Hermiticity-preserving cotangent)")
+        plan = qal.qal_block_plan_build(torch.cat([L0, Lc]), mirror=True)
+        L0p, _ = qal.qal_block_pack(plan, L0, check=False, stream=stream)
+        Lcp, _ = qal.qal_block_pack(plan, Lc, check=False, stream=stream)
+        ch = N
+        for t in range(1, iters + 1):
+            parts = qal.qal_block_expm_slices(plan, L0p, Lcp, u, T, N, chunk=ch, magnus_order=magnus_order,
+                                              stream=stream)
+            Lam = qal.qal_block_unpack(plan, parts[:, 0], stream=stream)
+            loss, cot = qal.qal_logical_loss(Lam, Pproj, G, stream=stream)
+            hist[t - 1] = loss
+            better = loss < best
+            best = torch.where(better, loss, best)
+            best_u[better] = u[better]
+            cotp, _ = qal.qal_block_pack(plan, cot, check=False, stream=stream)
+            g, _ = qal.qal_block_propagator_vjp(plan, L0p, Lcp, u, T, N, cotp, magnus_order=magnus_order,
+                                                stream=stream)
+            qal.qal_adam_step(u, g, m, v, t, lr, beta1, beta2, eps, stream=stream)
+        return {"u": u, "loss_history": hist, "best_u": best_u, "best_loss": best}
+    sess = qal.GradientSession(L0, Lc, u, T, N, magnus_order=magnus_order, stream=stream)
     for t in range(1, iters + 1):
         Lam = sess.forward()
         loss, cot = qal.qal_logical_loss(Lam, Pproj, G, stream=stream)

@@ -112,3 +112,26 @@ def test_calibration_loop_recovers_a_reachable_target(torch_cuda, qal):
     assert np.all(np.isfinite(hist)) and np.all(hist >= 0)
     assert np.all(np.diff(np.minimum.accumulate(hist)) <= 0)   # best-so-far non-increasing
     assert out["best_loss"][0].item() <= hist[0] * 1e-3
+
+
+def test_calibration_loop_on_the_block_path_matches_dense(torch_cuda, qal):
+    """NEXT f1 on the coherence-block path: the same Adam trajectory as the dense path (the loss and
+    its gradient are identical up to rounding), and the loss falls by orders of magnitude."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg0(N=16, T=60.0)
+    P = to(torch, qi.projection_matrix())
+    H0, Hc, C = to(torch, p.H0), to(torch, p.Hc), to(torch, p.C)
+    ustar = to(torch, p.u)
+    L0, Lc, _ = qal.qal_build_liouvillian(H0, Hc, C)
+    Lam_star = qal.GradientSession(L0, Lc, ustar, p.T, p.N).forward()
+    G = (P.conj().T @ Lam_star[0] @ P).contiguous()
+    assert float(G.imag.abs().max()) <= 1e-12                  # real for an HP map and Hermitian projectors
+    G = G.real.to(torch.complex128).contiguous()
+    rng = np.random.default_rng(0)
+    u0 = ustar + to(torch, 0.05 * rng.standard_normal(p.u.shape))
+    d = driver.calibrate(H0, Hc, C, u0, p.T, P, G, iters=60, lr=5e-3)
+    b = driver.calibrate(H0, Hc, C, u0, p.T, P, G, iters=60, lr=5e-3, structure="blocks")
+    hd, hb = d["loss_history"][:, 0].cpu().numpy(), b["loss_history"][:, 0].cpu().numpy()
+    assert np.max(np.abs(hd - hb) / np.maximum(hd, 1e-300)) <= 1e-8
+    assert hb[-1] <= hb[0] * 1e-1
