@@ -409,6 +409,49 @@ int qal_block_fidelity_cotangent(const qal_block_plan *plan, const qal_c128 *V, 
 
 size_t qal_block_workspace_bytes(const qal_block_plan *plan, int op, int batch, int n_slices);
 
+/* ===================================================================================
+ * Coherence blocks on the n = 4096 path (d = 64: configs[4] six spins, the 3-dot Hubbard model):
+ * the same structure as above with blocks far wider than 24 (six spins: 924, 792, 495, 220, 66, 12, 1
+ * with the mirror), each stored as a grid of 64 x 64 tile images and multiplied by a block-diagonal
+ * tiled DMMA GEMM.  One pulse per call, PWC controls, like the dense n = 4096 path.
+ * =================================================================================== */
+#define QAL_BB_MAX_BLOCKS 48
+#define QAL_BB_MAX_ROWS 8192
+
+typedef struct {
+    int n, d, mirror, nb, n_components;
+    int size[QAL_BB_MAX_BLOCKS];        /* used rows of block b (components packed best-fit)  */
+    int nt[QAL_BB_MAX_BLOCKS];          /* 64 x 64 tiles per dimension of block b             */
+    int row0[QAL_BB_MAX_BLOCKS];        /* first packed row of block b (64-aligned)           */
+    int weight[QAL_BB_MAX_BLOCKS];      /* reserved (1); mirrored blocks are filled at unpack */
+    double flops[QAL_BB_MAX_BLOCKS];    /* algorithmic flops of one product of block b        */
+    double flops_per_product;           /* sum over the blocks                                */
+    int nrows, ntiles;                  /* packed rows (64 x sum nt), output tiles (sum nt^2) */
+    long long total_doubles;            /* doubles of one tiled-block matrix                 */
+    int perm[QAL_BB_MAX_ROWS];          /* packed row -> natural index, -1 = padding          */
+    int inv[4096];                      /* natural index -> packed row, -1 = mirrored         */
+    int comp[4096];                     /* natural index -> component                         */
+} qal_bigblock_plan;
+
+/* Structure detection for n = 4096: the union non-zero pattern of the DEVICE matrices
+ * mats[nmat][4096][4096] is computed on the device, its connected components and Hermitian mirror
+ * pairing on the host (synchronises `stream`).  QAL_ERR_UNSUPPORTED beyond 48 stored blocks. */
+int qal_bigblock_plan_build(int nmat, const qal_c128 *mats, int mirror, qal_bigblock_plan *plan, void *stream);
+
+size_t qal_bigblock_workspace_bytes(const qal_bigblock_plan *plan);
+
+/*
+ * qal_magnus_expm_slices for n = 4096 on the coherence blocks: slices 0 .. count-1 of one pulse
+ * (PWC u [count][n_ctrl], L0 [4096][4096], Lc [n_ctrl][4096][4096], natural layout), chunk folds
+ * written to chunk_prod [count/chunk][4096][4096] (natural, mirror-filled, zero between blocks).
+ * If `flag` (device int, caller-zeroed) is given, every basis entry coupling two blocks is checked
+ * (QAL_ERR_STRUCTURE).  ws >= qal_bigblock_workspace_bytes(plan).
+ */
+int qal_bigblock_expm_slices(const qal_bigblock_plan *plan, int n_slices, double T, int count, int n_ctrl,
+                             const double *u, const qal_c128 *L0, const qal_c128 *Lc, int chunk,
+                             qal_c128 *chunk_prod, int *status, int *flag, void *ws, size_t ws_bytes,
+                             void *stream);
+
 /*
  * Stage profiling (bench.py's roofline and the expm-vs-product split, the Fig. 2
  * analog of P:167-171).  Between qal_profile_begin and qal_profile_end every kernel
@@ -425,7 +468,7 @@ enum { QAL_ST_LIOUV = 0, QAL_ST_COMM = 1, QAL_ST_EXPM = 2, QAL_ST_TREE = 3, QAL_
        /* coherence-block path: these counters accumulate ALGORITHMIC FLOPs (8 s^3 per complex
         * product of an s x s block, padding excluded), not product counts */
        QAL_ST_BLK_EXPM = 9, QAL_ST_BLK_TREE = 10, QAL_ST_BLK_PREFIX = 11, QAL_ST_BLK_SUFFIX = 12,
-       QAL_ST_BLK_GRAD = 13, QAL_NSTAGE = 14 };
+       QAL_ST_BLK_GRAD = 13, QAL_ST_BLK_GEMM = 14, QAL_NSTAGE = 15 };
 int qal_profile_begin(unsigned long long *dev_counters);
 int qal_profile_end(double *ms, int *launches);
 

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libqal.so")
-SOURCES = ["qal_api.cu", "qal_magnus.cu", "qal_product.cu", "qal_grad.cu", "qal_dense.cu", "qal_blocks.cu"]
+SOURCES = ["qal_api.cu", "qal_magnus.cu", "qal_product.cu", "qal_grad.cu", "qal_dense.cu", "qal_blocks.cu", "qal_bigblocks.cu"]
 HEADERS = ["qal_dev.cuh", "qal_slice.cuh", "qal_internal.h", "../../include/qal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [*os.environ.get("QAL_NVCC_EXTRA", "").split(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

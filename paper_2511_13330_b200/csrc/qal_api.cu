@@ -830,6 +830,36 @@ int qal_block_fidelity_cotangent(const qal_block_plan* plan, const qal_c128* V, 
   if (!V || !C) return QAL_ERR_NULL;
   return cuda_rc(launch_blk_fidelity_cotangent(*plan, D2(V), D2(C), S(stream)));
 }
+
+int qal_bigblock_plan_build(int nmat, const qal_c128* mats, int mirror, qal_bigblock_plan* plan, void* stream) {
+  launch_counter() = 0;
+  if (!mats || !plan) return QAL_ERR_NULL;
+  if (nmat < 1) return QAL_ERR_EMPTY;
+  return build_bigblock_plan(nmat, D2(mats), mirror, plan, S(stream));
+}
+
+size_t qal_bigblock_workspace_bytes(const qal_bigblock_plan* plan) {
+  if (!plan || plan->n != 4096 || plan->nb < 1) return 0;
+  return bb_ws_bytes(*plan);
+}
+
+int qal_bigblock_expm_slices(const qal_bigblock_plan* plan, int n_slices, double T, int count, int n_ctrl,
+                             const double* u, const qal_c128* L0, const qal_c128* Lc, int chunk,
+                             qal_c128* chunk_prod, int* status, int* flag, void* ws, size_t ws_bytes,
+                             void* stream) {
+  launch_counter() = 0;
+  if (!plan || !u || !L0 || !Lc || !chunk_prod) return QAL_ERR_NULL;
+  if (plan->n != 4096 || plan->nb < 1 || plan->nb > QAL_BB_MAX_BLOCKS) return QAL_ERR_UNSUPPORTED;
+  if (n_slices < 1 || count < 1) return QAL_ERR_EMPTY;
+  if (count > n_slices || chunk < 1 || count % chunk) return QAL_ERR_DIM;
+  if (n_ctrl < 1 || n_ctrl > QAL_MAX_CTRL) return QAL_ERR_UNSUPPORTED;
+  if (!is_fin(T) || T <= 0.0) return QAL_ERR_NONFINITE;
+  if (!ws || ws_bytes < bb_ws_bytes(*plan)) return QAL_ERR_WORKSPACE;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess) return QAL_ERR_CUDA;
+  return cuda_rc(launch_bb_expm_fold(*plan, D2(L0), D2(Lc), n_ctrl, u, count, T / n_slices, chunk, D2(chunk_prod),
+                                     status, flag, reinterpret_cast<double*>(ws), st));
+}
 }  // extern "C"
 
 namespace {

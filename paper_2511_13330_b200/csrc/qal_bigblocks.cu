@@ -1,0 +1,623 @@
+// qal_bigblocks.cu -- the coherence-block structure on the n = 4096 path (d = 64: two exchange-only
+// qubits, six spins; BASELINE configs[4]; the 3-dot Hubbard model, NEXT f3).
+//
+// As for d = 8 (qal_blocks.cu), every operator conserves total S_z, so the Liouvillian of
+// Eq. 8 and everything built from it by Eqs. 13-15 is block diagonal by coherence order; for six
+// spins the blocks q = 0..6 have 924, 792, 495, 220, 66, 12, 1 rows, and Hermiticity preservation ties q
+// to -q (pin P-5), so with the mirror 2.1% of the dense product flops remain.  These blocks are far larger
+// than the d = 8 ones: each is stored as its own grid of 64 x 64 TILE IMAGES (the K7 layout of
+// qal_dense.cu) and every product is a block-diagonal tiled GEMM -- one persistent launch over the output
+// tiles of all blocks, each tile the DMMA.8x8x4 K loop of k_dense_gemm with TMA-streamed A / B tiles.
+// The expm scheme (Paterson-Stockmeyer m = 16, s squarings) is chosen per block on the device.
+//
+// The structure is detected on the device (union of the non-zero patterns of the basis matrices,
+// k_bb_nzmask) and the components found on the host; k_bb_check re-verifies every call that no basis
+// entry couples two blocks.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/qal.h"
+#include "qal_dev.cuh"
+#include "qal_internal.h"
+
+namespace qal {
+
+constexpr int BBN = 4096;   // superoperator dimension of this path
+constexpr int BBW = BBN / 64;   // 64-bit words per row of the non-zero mask
+
+// device view of a big-block plan (tables in device memory)
+struct BBDev {
+  int nb, ntiles, nrows;
+  int nt[QAL_BB_MAX_BLOCKS];           // tiles per dimension of block b
+  int tstart[QAL_BB_MAX_BLOCKS + 1];   // prefix of nt^2 (output tiles)
+  int row0[QAL_BB_MAX_BLOCKS];         // first packed row (64-aligned)
+  long long toff[QAL_BB_MAX_BLOCKS];   // double offset of block b's tiles in a tiled-block matrix
+  long long total;                     // doubles per tiled-block matrix
+  const int* perm;                     // [nrows] packed row -> natural index (-1 padding)
+  const int* inv;                      // [4096] natural -> packed row (-1: mirrored / not stored)
+  const int* comp;                     // [4096] natural -> component
+};
+
+struct BBPlanRec {   // per block, written on the device
+  int m, s, bad, pad;
+  double nrm;
+};
+
+__device__ __forceinline__ int bb_block_of_tile(const BBDev& D, int t) {
+  int b = 0;
+  for (int q = 1; q < D.nb; ++q)
+    if (t >= D.tstart[q]) b = q;
+  return b;
+}
+// flat double index e of a tiled-block matrix -> block, tile (I, J), logical (r, c) within the tile, plane
+struct BBPos {
+  int b, I, J, r, c, plane;
+};
+__device__ __forceinline__ BBPos bb_decode(const BBDev& D, size_t e) {
+  BBPos p;
+  const int t = (int)(e / IMG);
+  const int within = (int)(e % IMG);
+  p.b = bb_block_of_tile(D, t);
+  const int tl = t - D.tstart[p.b];
+  p.I = tl / D.nt[p.b];
+  p.J = tl % D.nt[p.b];
+  p.plane = within >= PLANE;
+  const int w = within - p.plane * PLANE;
+  p.r = w >> 6;
+  const int pc = (w & 63) ^ ((p.r & 1) << 3);
+  const int q = pc & 7;
+  p.c = (pc & ~7) | (4 * (q & 1) + (q >> 1));
+  return p;
+}
+__device__ __forceinline__ double* bb_tile(const BBDev& D, double* M, int b, int I, int J) {
+  return M + D.toff[b] + ((size_t)I * D.nt[b] + J) * IMG;
+}
+__device__ __forceinline__ const double* bb_tile(const BBDev& D, const double* M, int b, int I, int J) {
+  return M + D.toff[b] + ((size_t)I * D.nt[b] + J) * IMG;
+}
+
+// ------------------------------------------------------------------ structure detection
+// mask[r][w] bit c: some matrix has a non-zero at (r, 64 w + c)
+__global__ void __launch_bounds__(64) k_bb_nzmask(int nmat, const double2* __restrict__ mats,
+                                                  unsigned long long* __restrict__ mask) {
+  const int r = blockIdx.x, w = threadIdx.x;
+  unsigned long long bits = 0;
+  for (int m = 0; m < nmat; ++m) {
+    const double2* row = mats + ((size_t)m * BBN + r) * BBN + 64 * w;
+    for (int c = 0; c < 64; ++c) {
+      const double2 v = __ldg(row + c);
+      if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << c;
+    }
+  }
+  mask[(size_t)r * BBW + w] = bits;
+}
+
+// every entry coupling two components must be exactly zero
+__global__ void __launch_bounds__(256) k_bb_check(BBDev D, const double2* __restrict__ M, int* __restrict__ flag) {
+  int bad = 0;
+  const size_t n2 = (size_t)BBN * BBN;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+    const int R = (int)(e >> 12), C = (int)(e & 4095);
+    if (D.comp[R] != D.comp[C]) {
+      const double2 v = M[e];
+      if (v.x != 0.0 || v.y != 0.0) bad = 1;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = QAL_ERR_STRUCTURE;
+}
+
+// ------------------------------------------------------------------ elementwise
+// X = h (L0 + sum_j u_j L_j) gathered into the tiled blocks (a3, PWC)
+__global__ void __launch_bounds__(NT) k_bb_omega(BBDev D, const double2* __restrict__ L0,
+                                                 const double2* __restrict__ Lc, int J, const double* __restrict__ u,
+                                                 double h, double* __restrict__ X) {
+  __shared__ double cf[MAXJ + 1];
+  if (threadIdx.x <= J) cf[threadIdx.x] = threadIdx.x == 0 ? h : h * u[threadIdx.x - 1];
+  __syncthreads();
+  const size_t n2 = (size_t)BBN * BBN;
+  const size_t half = (size_t)D.ntiles * PLANE;   // complex entries
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < half; e += (size_t)gridDim.x * NT) {
+    const int t = (int)(e / PLANE), w = (int)(e % PLANE);
+    const int b = bb_block_of_tile(D, t);
+    const int tl = t - D.tstart[b];
+    const int I = tl / D.nt[b], Jt = tl % D.nt[b];
+    const int r = w >> 6, c = w & 63;
+    const int R = D.perm[D.row0[b] + 64 * I + r], Cc = D.perm[D.row0[b] + 64 * Jt + c];
+    double re = 0.0, im = 0.0;
+    if (R >= 0 && Cc >= 0) {
+      const size_t idx = (size_t)R * BBN + Cc;
+      const double2 x0 = __ldg(L0 + idx);
+      re = cf[0] * x0.x;
+      im = cf[0] * x0.y;
+      for (int j = 0; j < J; ++j) {
+        const double2 x = __ldg(Lc + (size_t)j * n2 + idx);
+        re = fma(cf[j + 1], x.x, re);
+        im = fma(cf[j + 1], x.y, im);
+      }
+    }
+    double* T = X + D.toff[b] + (size_t)tl * IMG;
+    const int o = img_off(r, c);
+    T[o] = re;
+    T[PLANE + o] = im;
+  }
+}
+
+// part[t][c] = sum over the 64 rows of tile t of |X[r][c]|
+__global__ void __launch_bounds__(64) k_bb_colsum(BBDev D, const double* __restrict__ X, double* __restrict__ part) {
+  const int t = blockIdx.x, c = threadIdx.x;
+  const int b = bb_block_of_tile(D, t);
+  const double* T = X + D.toff[b] + (size_t)(t - D.tstart[b]) * IMG;
+  double s = 0.0;
+  for (int r = 0; r < 64; ++r) {
+    const int o = img_off(r, c);
+    s += hypot(T[o], T[PLANE + o]);
+  }
+  part[(size_t)t * 64 + c] = s;
+}
+
+// per block: ||X_b||_1 = max_c sum_I part[(I, c / 64)][c % 64]; m = 16, s from theta_16 (A15)
+__global__ void __launch_bounds__(1024) k_bb_plan(BBDev D, const double* __restrict__ part, BBPlanRec* plan,
+                                                  int smax, int* status) {
+  __shared__ double red[32];
+  const int b = blockIdx.x, nt = D.nt[b];
+  double m = 0.0;
+  bool nan = false;
+  for (int c = threadIdx.x; c < 64 * nt; c += 1024) {
+    double s = 0.0;
+    for (int I = 0; I < nt; ++I) s += part[(size_t)(D.tstart[b] + I * nt + c / 64) * 64 + (c % 64)];
+    if (!(s == s)) nan = true;
+    m = fmax(m, s);
+  }
+  if (nan) m = __longlong_as_double(0x7ff8000000000000LL);
+  for (int off = 16; off > 0; off >>= 1) {
+    const double o = __shfl_xor_sync(0xffffffffu, m, off);
+    m = (o != o || o > m) ? o : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = red[0];
+    for (int w = 1; w < 32; ++w) v = (red[w] != red[w] || red[w] > v) ? red[w] : v;
+    int mm, s;
+    choose_ms(v, mm, s);
+    const int bad = !(v <= 1e300) || s > smax;
+    if (bad) s = 0;
+    plan[b].m = 16;
+    plan[b].s = s;
+    plan[b].bad = bad;
+    plan[b].nrm = v;
+    if (bad && status) *status = QAL_ERR_NONFINITE;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_bb_scale(BBDev D, double* X, const BBPlanRec* plan) {
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < (size_t)D.total; e += (size_t)gridDim.x * NT) {
+    const int b = bb_block_of_tile(D, (int)(e / IMG));
+    const int s = plan[b].s;
+    if (s) X[e] *= ldexp(1.0, -s);
+  }
+}
+
+// out = cid I + sum_q coef[q] src[q]
+struct BBCombo {
+  const double* src[5];
+  double coef[5];
+  int nsrc;
+  double cid;
+  double* out;
+};
+__global__ void __launch_bounds__(NT) k_bb_combo(BBDev D, BBCombo g) {
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < (size_t)D.total; e += (size_t)gridDim.x * NT) {
+    double v = 0.0;
+    for (int q = 0; q < g.nsrc; ++q) v = fma(g.coef[q], g.src[q][e], v);
+    if (g.cid != 0.0) {
+      const BBPos p = bb_decode(D, e);
+      if (!p.plane && p.I == p.J && p.r == p.c) v += g.cid;
+    }
+    g.out[e] = v;
+  }
+}
+
+// dst = per block (s odd ? b : a)
+__global__ void __launch_bounds__(NT) k_bb_copy_sel(BBDev D, double* dst, const double* a, const double* bsrc,
+                                                    const BBPlanRec* plan) {
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < (size_t)D.total; e += (size_t)gridDim.x * NT) {
+    const int b = bb_block_of_tile(D, (int)(e / IMG));
+    dst[e] = (plan[b].s & 1) ? bsrc[e] : a[e];
+  }
+}
+
+// natural from the tiled blocks: stored component -> value, mirrored component -> conj of the stored
+// mirror entry (Lambda[s(R), s(C)] = conj(Lambda[R, C]), s(i + d j) = j + d i), else 0
+__global__ void __launch_bounds__(NT) k_bb_unpack(BBDev D, const double* __restrict__ X, double2* __restrict__ M) {
+  const size_t n2 = (size_t)BBN * BBN;
+  for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < n2; e += (size_t)gridDim.x * NT) {
+    const int R = (int)(e >> 12), C = (int)(e & 4095);
+    double2 v = make_double2(0.0, 0.0);
+    if (D.comp[R] == D.comp[C]) {
+      int r = D.inv[R], c = D.inv[C];
+      bool cj = false;
+      if (r < 0) {
+        r = D.inv[(R >> 6) + 64 * (R & 63)];
+        c = D.inv[(C >> 6) + 64 * (C & 63)];
+        cj = true;
+      }
+      if (r >= 0 && c >= 0) {
+        int b = 0;
+        for (int q = 1; q < D.nb; ++q)
+          if (r >= D.row0[q]) b = q;
+        const int lr = r - D.row0[b], lc = c - D.row0[b];
+        const double* T = bb_tile(D, X, b, lr >> 6, lc >> 6);
+        const int o = img_off(lr & 63, lc & 63);
+        v = make_double2(T[o], cj ? -T[PLANE + o] : T[PLANE + o]);
+      }
+    }
+    M[e] = v;
+  }
+}
+
+// ------------------------------------------------------------------ block-diagonal tiled GEMM
+// C = A B block by block (C_b = A_b B_b), accumulator initialised to cid I + sum coef[q] src[q];
+// slot >= 0: a squaring, active for block b only when slot < plan[b].s; A_alt is used for blocks with
+// odd plan[b].s (the result of their squarings).
+struct BBGemm {
+  const double* A;
+  const double* A_alt;
+  const double* B;
+  double* C;
+  const double* src[3];
+  double coef[3];
+  double cid;
+  int nsrc;
+  int slot;
+  const BBPlanRec* plan;
+  unsigned long long* ctr;   // profiling: algorithmic flops of the executed block products
+  unsigned long long bflops[QAL_BB_MAX_BLOCKS];
+};
+
+__device__ __forceinline__ bool bb_active(const BBDev& D, const BBGemm& g, int b) {
+  return g.slot < 0 || g.slot < g.plan[b].s;
+}
+// next active output tile >= t (or D.ntiles)
+__device__ __forceinline__ int bb_next_tile(const BBDev& D, const BBGemm& g, int t, int stride) {
+  while (t < D.ntiles && !bb_active(D, g, bb_block_of_tile(D, t))) t += stride;
+  return t;
+}
+
+__global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
+  extern __shared__ __align__(128) double smem[];
+  double* SA = smem;
+  double* SB[2] = {smem + IMG, smem + 2 * IMG};
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * IMG);
+  const Lane L = lane_id();
+  if (g.ctr && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int b = 0; b < D.nb; ++b)
+      if (bb_active(D, g, b)) atomicAdd(g.ctr, g.bflops[b]);
+  int t = bb_next_tile(D, g, blockIdx.x, gridDim.x);
+  if (t >= D.ntiles) return;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto Aof = [&](int b) { return (g.A_alt && (g.plan[b].s & 1)) ? g.A_alt : g.A; };
+  int b = bb_block_of_tile(D, t);
+  int tl = t - D.tstart[b];
+  int I = tl / D.nt[b], J = tl % D.nt[b];
+  if (threadIdx.x == 0) {
+    tma_load_img(SA, bb_tile(D, Aof(b), b, I, 0), &bar[0]);
+    tma_load_img(SB[0], bb_tile(D, g.B, b, 0, J), &bar[1]);
+  }
+  uint32_t phA = 0, phB[2] = {0, 0};
+  int step = 0;
+  Strip a, acc;
+  while (t < D.ntiles) {
+    b = bb_block_of_tile(D, t);
+    tl = t - D.tstart[b];
+    const int nt = D.nt[b];
+    I = tl / nt;
+    J = tl % nt;
+    zero(acc);
+    for (int q = 0; q < g.nsrc; ++q) {
+      Strip x;
+      load_img(x, bb_tile(D, g.src[q], b, I, J), L);
+      const double c = g.coef[q];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) { acc.re[i] = fma(c, x.re[i], acc.re[i]); acc.im[i] = fma(c, x.im[i], acc.im[i]); }
+    }
+    if (I == J && g.cid != 0.0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (is_diag(L, i)) acc.re[i] += g.cid;
+    }
+    const int tnext = bb_next_tile(D, g, t + gridDim.x, gridDim.x);
+    for (int K = 0; K < nt; ++K, ++step) {
+      const int cur = step & 1;
+      mbar_wait(&bar[0], phA);
+      phA ^= 1;
+      mbar_wait(&bar[1 + cur], phB[cur]);
+      phB[cur] ^= 1;
+      load_img(a, SA, L);
+      __syncthreads();   // SA drained by every warp; SB[cur^1] no longer read
+      if (threadIdx.x == 0) {
+        int tn = t, Kn = K + 1, bn = b, In = I, Jn = J;
+        if (Kn == nt) {
+          tn = tnext;
+          Kn = 0;
+          if (tn < D.ntiles) {
+            bn = bb_block_of_tile(D, tn);
+            const int tln = tn - D.tstart[bn];
+            In = tln / D.nt[bn];
+            Jn = tln % D.nt[bn];
+          }
+        }
+        if (tn < D.ntiles) {
+          fence_proxy_async();
+          tma_load_img(SA, bb_tile(D, Aof(bn), bn, In, Kn), &bar[0]);
+          tma_load_img(SB[cur ^ 1], bb_tile(D, g.B, bn, Kn, Jn), &bar[1 + (cur ^ 1)]);
+        }
+      }
+      mma_acc(acc, a, SB[cur], L);
+    }
+    store_img(bb_tile(D, g.C, b, I, J), acc, L);
+    t = tnext;
+  }
+}
+
+// ------------------------------------------------------------------ host
+namespace {
+constexpr int BB_GEMM_SMEM = 3 * IMG * 8 + 64;
+int bb_grid_ew() { return 4 * num_sms(); }
+}  // namespace
+
+size_t bb_ws_bytes(const qal_bigblock_plan& p) {
+  // 8 tiled-block matrices + column partials + per-block plan records + device tables
+  return 8 * (size_t)p.total_doubles * 8 + (size_t)p.ntiles * 64 * 8 + 64 * sizeof(BBPlanRec) +
+         (size_t)(p.nrows + 2 * BBN) * sizeof(int) + 1024;
+}
+
+// device view; copies the index tables into `tab` (device, inside the workspace) on `st`
+static cudaError_t bb_dev(const qal_bigblock_plan& p, int* tab, BBDev& D, cudaStream_t st) {
+  memset(&D, 0, sizeof(D));
+  D.nb = p.nb;
+  D.ntiles = p.ntiles;
+  D.nrows = p.nrows;
+  D.total = p.total_doubles;
+  int ts = 0;
+  for (int b = 0; b < p.nb; ++b) {
+    D.nt[b] = p.nt[b];
+    D.row0[b] = p.row0[b];
+    D.toff[b] = (long long)ts * IMG;
+    D.tstart[b] = ts;
+    ts += p.nt[b] * p.nt[b];
+  }
+  D.tstart[p.nb] = ts;
+  std::vector<int> h(p.nrows + 2 * BBN);
+  for (int r = 0; r < p.nrows; ++r) h[r] = p.perm[r];
+  for (int i = 0; i < BBN; ++i) { h[p.nrows + i] = p.inv[i]; h[p.nrows + BBN + i] = p.comp[i]; }
+  // pageable source: the runtime stages it before returning, so `h` may die with this frame
+  const cudaError_t e = cudaMemcpyAsync(tab, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+  D.perm = tab;
+  D.inv = tab + p.nrows;
+  D.comp = tab + p.nrows + BBN;
+  return e;
+}
+
+int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_plan* out, cudaStream_t st) {
+  // non-zero pattern on the device (2 MB), components on the host
+  unsigned long long* dmask = nullptr;
+  if (cudaMallocAsync(&dmask, (size_t)BBN * BBW * 8, st) != cudaSuccess) return QAL_ERR_CUDA;
+  k_bb_nzmask<<<BBN, BBW, 0, st>>>(nmat, mats, dmask);
+  std::vector<unsigned long long> mask((size_t)BBN * BBW);
+  cudaError_t e = cudaMemcpyAsync(mask.data(), dmask, mask.size() * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(dmask, st);
+  if (e != cudaSuccess) return QAL_ERR_CUDA;
+  std::vector<int> par(BBN);
+  for (int i = 0; i < BBN; ++i) par[i] = i;
+  auto find = [&](int a) {
+    while (par[a] != a) a = par[a] = par[par[a]];
+    return a;
+  };
+  for (int r = 0; r < BBN; ++r)
+    for (int w = 0; w < BBW; ++w) {
+      unsigned long long bits = mask[(size_t)r * BBW + w];
+      while (bits) {
+        const int c = 64 * w + __builtin_ctzll(bits);
+        bits &= bits - 1;
+        const int a = find(r), b = find(c);
+        if (a != b) par[std::max(a, b)] = std::min(a, b);
+      }
+    }
+  std::vector<int> cid(BBN), root(BBN, -1);
+  int ncomp = 0;
+  for (int i = 0; i < BBN; ++i) {
+    const int r = find(i);
+    if (root[r] < 0) root[r] = ncomp++;
+    cid[i] = root[r];
+  }
+  std::vector<std::vector<int>> members(ncomp);
+  for (int i = 0; i < BBN; ++i) members[cid[i]].push_back(i);
+  std::vector<int> mir(ncomp);
+  for (int k = 0; k < ncomp; ++k) {
+    const int i0 = members[k][0];
+    mir[k] = cid[(i0 >> 6) + 64 * (i0 & 63)];
+    for (int i : members[k])
+      if (cid[(i >> 6) + 64 * (i & 63)] != mir[k]) return QAL_ERR_STRUCTURE;
+  }
+  std::vector<int> keep;
+  for (int k = 0; k < ncomp; ++k)
+    if (!mirror || k <= mir[k]) keep.push_back(k);
+  std::stable_sort(keep.begin(), keep.end(), [&](int a, int b) { return members[a].size() > members[b].size(); });
+  // best-fit-decreasing packing of the components into blocks of 64-multiple width (components that
+  // share a block are multiplied densely together -- their cross terms are zero)
+  struct Bin { int width, used; std::vector<int> comps; };
+  std::vector<Bin> bins;
+  for (int k : keep) {
+    const int sz = (int)members[k].size();
+    int best = -1;
+    for (int i = 0; i < (int)bins.size(); ++i)
+      if (bins[i].used + sz <= bins[i].width &&
+          (best < 0 || bins[i].width - bins[i].used < bins[best].width - bins[best].used))
+        best = i;
+    if (best >= 0) { bins[best].used += sz; bins[best].comps.push_back(k); }
+    else bins.push_back({(sz + 63) / 64 * 64, sz, {k}});
+  }
+  if ((int)bins.size() > QAL_BB_MAX_BLOCKS) return QAL_ERR_UNSUPPORTED;
+  qal_bigblock_plan p;
+  memset(&p, 0, sizeof(p));
+  p.n = BBN;
+  p.d = 64;
+  p.mirror = mirror ? 1 : 0;
+  p.nb = (int)bins.size();
+  p.n_components = ncomp;
+  for (int i = 0; i < QAL_BB_MAX_ROWS; ++i) p.perm[i] = -1;
+  for (int i = 0; i < BBN; ++i) { p.inv[i] = -1; p.comp[i] = cid[i]; }
+  int row = 0, tiles = 0;
+  double flops = 0.0;
+  for (int b = 0; b < p.nb; ++b) {
+    p.size[b] = bins[b].used;
+    p.nt[b] = bins[b].width / 64;
+    p.row0[b] = row;
+    p.weight[b] = 1;
+    if (row + bins[b].width > QAL_BB_MAX_ROWS) return QAL_ERR_UNSUPPORTED;
+    int r = row;
+    double fl = 0.0;
+    for (int k : bins[b].comps) {
+      for (int i : members[k]) {
+        p.perm[r] = i;
+        p.inv[i] = r;
+        ++r;
+      }
+      const double sz = (double)members[k].size();
+      fl += 2.0 * QAL_REAL_MMAS_PER_CMMA * sz * sz * sz;
+    }
+    p.flops[b] = fl;
+    flops += fl;
+    row += bins[b].width;
+    tiles += p.nt[b] * p.nt[b];
+  }
+  p.nrows = row;
+  p.ntiles = tiles;
+  p.total_doubles = (long long)tiles * IMG;
+  p.flops_per_product = flops;
+  *out = p;
+  return QAL_OK;
+}
+
+static cudaError_t bb_gemm(const BBDev& D, const BBGemm& g0, const qal_bigblock_plan& p, cudaStream_t st) {
+  BBGemm g = g0;
+  g.ctr = prof_counter(ST_BLK_GEMM);
+  for (int b = 0; b < p.nb; ++b) g.bflops[b] = (unsigned long long)p.flops[b];
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_bb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, BB_GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  prof_pre(ST_BLK_GEMM, st);
+  k_bb_gemm<<<num_sms(), NT, BB_GEMM_SMEM, st>>>(D, g);
+  prof_post(ST_BLK_GEMM, st);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// Propagator of `count` PWC slices of one pulse on the tiled blocks: chunk folds -> chunk_nat (natural,
+// mirror-filled).  The Paterson-Stockmeyer / squaring schedule of launch_dense_expm_fold, per block.
+cudaError_t launch_bb_expm_fold(const qal_bigblock_plan& p, const double2* L0, const double2* Lc, int J,
+                                const double* u, int count, double h, int chunk, double2* chunk_nat, int* status,
+                                int* flag, double* ws, cudaStream_t st) {
+  const size_t M = (size_t)p.total_doubles;
+  double* X = ws;
+  double* X2 = X + M;
+  double* X3 = X2 + M;
+  double* X4 = X3 + M;
+  double* T0 = X4 + M;
+  double* T1 = T0 + M;
+  double* P[2] = {T1 + M, T1 + 2 * M};
+  double* part = T1 + 3 * M;
+  BBPlanRec* plan = reinterpret_cast<BBPlanRec*>(part + (size_t)p.ntiles * 64);
+  int* tab = reinterpret_cast<int*>(plan + 64);
+  BBDev D;
+  cudaError_t e = bb_dev(p, tab, D, st);
+  if (e != cudaSuccess) return e;
+  if (flag) {   // structure check of the basis of this call
+    k_bb_check<<<bb_grid_ew(), 256, 0, st>>>(D, L0, flag);
+    for (int j = 0; j < J; ++j) k_bb_check<<<bb_grid_ew(), 256, 0, st>>>(D, Lc + (size_t)j * BBN * BBN, flag);
+    launch_counter() += 1 + J;
+  }
+  constexpr int SMAX = 8;
+  static const double ifac[17] = {1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333,
+                                  0.001388888888888889, 0.0001984126984126984, 2.48015873015873e-05,
+                                  2.7557319223985893e-06, 2.755731922398589e-07, 2.505210838544172e-08,
+                                  2.08767569878681e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,
+                                  7.647163731819816e-13, 4.779477332387385e-14};
+  int pc = 0;
+  for (int k = 0; k < count && e == cudaSuccess; ++k) {
+    k_bb_omega<<<bb_grid_ew(), NT, 0, st>>>(D, L0, Lc, J, u + (size_t)k * J, h, X);
+    k_bb_colsum<<<p.ntiles, 64, 0, st>>>(D, X, part);
+    k_bb_plan<<<p.nb, 1024, 0, st>>>(D, part, plan, SMAX, status);
+    k_bb_scale<<<bb_grid_ew(), NT, 0, st>>>(D, X, plan);
+    launch_counter() += 4;
+    BBGemm g{};
+    g.slot = -1;
+    g.plan = plan;
+    g.A = X; g.B = X; g.C = X2;
+    if ((e = bb_gemm(D, g, p, st)) != cudaSuccess) break;
+    g.A = X2; g.C = X3;
+    if ((e = bb_gemm(D, g, p, st)) != cudaSuccess) break;
+    g.A = X3; g.C = X4;
+    if ((e = bb_gemm(D, g, p, st)) != cudaSuccess) break;
+    BBCombo cb{};
+    cb.src[0] = X; cb.src[1] = X2; cb.src[2] = X3; cb.src[3] = X4;
+    cb.coef[0] = ifac[13]; cb.coef[1] = ifac[14]; cb.coef[2] = ifac[15]; cb.coef[3] = ifac[16];
+    cb.nsrc = 4;
+    cb.cid = ifac[12];
+    cb.out = T0;
+    k_bb_combo<<<bb_grid_ew(), NT, 0, st>>>(D, cb);
+    ++launch_counter();
+    double* Hin = T0;
+    double* Hout = T1;
+    for (int blk = 2; blk >= 0 && e == cudaSuccess; --blk) {   // H <- B_blk + H X^4
+      BBGemm h2{};
+      h2.A = Hin; h2.B = X4; h2.C = Hout; h2.slot = -1; h2.plan = plan;
+      h2.src[0] = X; h2.src[1] = X2; h2.src[2] = X3;
+      h2.coef[0] = ifac[4 * blk + 1]; h2.coef[1] = ifac[4 * blk + 2]; h2.coef[2] = ifac[4 * blk + 3];
+      h2.nsrc = 3;
+      h2.cid = ifac[4 * blk];
+      e = bb_gemm(D, h2, p, st);
+      double* tmp = Hin; Hin = Hout; Hout = tmp;
+    }
+    if (e != cudaSuccess) break;
+    double* E[2] = {Hin, Hout};
+    for (int q = 0; q < SMAX && e == cudaSuccess; ++q) {   // squarings, per block only while q < s_b
+      BBGemm sq{};
+      sq.A = E[q & 1]; sq.B = E[q & 1]; sq.C = E[(q + 1) & 1]; sq.slot = q; sq.plan = plan;
+      e = bb_gemm(D, sq, p, st);
+    }
+    if (e != cudaSuccess) break;
+    if (chunk_nat) {
+      if (k % chunk == 0) {
+        k_bb_copy_sel<<<bb_grid_ew(), NT, 0, st>>>(D, P[pc], E[0], E[1], plan);
+        ++launch_counter();
+      } else {
+        BBGemm f{};
+        f.A = E[0]; f.A_alt = E[1]; f.B = P[pc]; f.C = P[pc ^ 1]; f.slot = -1; f.plan = plan;
+        if ((e = bb_gemm(D, f, p, st)) != cudaSuccess) break;
+        pc ^= 1;
+      }
+      if (k % chunk == chunk - 1) {
+        k_bb_unpack<<<bb_grid_ew(), NT, 0, st>>>(D, P[pc], chunk_nat + (size_t)(k / chunk) * BBN * BBN);
+        ++launch_counter();
+      }
+    }
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace qal

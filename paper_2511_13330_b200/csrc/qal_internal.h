@@ -78,12 +78,19 @@ size_t blk_grad_scratch_bytes(const qal_block_plan& p);
 cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
                                 cudaStream_t st);
 
+// coherence blocks on the n = 4096 path (qal_bigblocks.cu)
+int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_plan* out, cudaStream_t st);
+size_t bb_ws_bytes(const qal_bigblock_plan& p);
+cudaError_t launch_bb_expm_fold(const qal_bigblock_plan& p, const double2* L0, const double2* Lc, int J,
+                                const double* u, int count, double h, int chunk, double2* chunk_nat, int* status,
+                                int* flag, double* ws, cudaStream_t st);
+
 int num_sms();
 int& launch_counter();
 
 // profiling window (qal_profile_begin/end): stage ids as in qal.h
 enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, ST_DENSE_GEMM,
-       ST_BLK_EXPM, ST_BLK_TREE, ST_BLK_PREFIX, ST_BLK_SUFFIX, ST_BLK_GRAD, NSTAGE };
+       ST_BLK_EXPM, ST_BLK_TREE, ST_BLK_PREFIX, ST_BLK_SUFFIX, ST_BLK_GRAD, ST_BLK_GEMM, NSTAGE };
 unsigned long long* prof_counter(int stage);   // device counter slot or nullptr
 void prof_pre(int stage, cudaStream_t st);      // record start event (no-op when off)
 void prof_post(int stage, cudaStream_t st);     // record end event

@@ -26,14 +26,14 @@ QAL_OP_VJP = 5
 QAL_MAX_CTRL = 8
 STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
           "grad_slices", "dense_gemm", "blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain",
-          "blk_grad_slices"]
+          "blk_grad_slices", "blk_gemm"]
 # stages whose device counter holds algorithmic FLOPs (coherence-block path), not product counts
-FLOP_STAGES = {"blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain", "blk_grad_slices"}
+FLOP_STAGES = {"blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain", "blk_grad_slices", "blk_gemm"}
 KERNELS = {"liouvillian": "k_liouvillian", "commutators": "k_commutators", "expm_fold": "k_expm_fold",
            "tree": "k_tree_level", "fidelity": "k_fidelity", "prefix_chain": "k_prefix_chain",
            "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices", "dense_gemm": "k_dense_gemm",
            "blk_expm_fold": "k_blk_expm_fold", "blk_tree": "k_blk_tree_level", "blk_prefix_chain": "k_blk_prefix_chain",
-           "blk_suffix_chain": "k_blk_suffix_chain", "blk_grad_slices": "k_blk_grad_slices"}
+           "blk_suffix_chain": "k_blk_suffix_chain", "blk_grad_slices": "k_blk_grad_slices", "blk_gemm": "k_bb_gemm"}
 
 _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
@@ -119,6 +119,13 @@ _EXPORTS = {
                                                  ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]),
     "qal_block_fidelity_cotangent": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                      ctypes.c_void_p]),
+    "qal_bigblock_plan_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                                ctypes.c_void_p]),
+    "qal_bigblock_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p]),
+    "qal_bigblock_expm_slices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "qal_profile_begin": (ctypes.c_int, [ctypes.c_void_p]),
     "qal_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "qal_fp64_peak_probe": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -631,3 +638,53 @@ def qal_block_fidelity_cotangent(plan: BlockPlan, V, stream=None):
     _check(load().qal_block_fidelity_cotangent(ctypes.byref(plan), _ptr(V), _ptr(C), _stream(stream)),
            "qal_block_fidelity_cotangent")
     return C
+
+
+# --------------------------------------------------------------------------- coherence blocks, n = 4096
+QAL_BB_MAX_BLOCKS = 48
+QAL_BB_MAX_ROWS = 8192
+
+
+class BigBlockPlan(ctypes.Structure):
+    """Mirror of qal_bigblock_plan (include/qal.h)."""
+    _fields_ = [("n", ctypes.c_int), ("d", ctypes.c_int), ("mirror", ctypes.c_int), ("nb", ctypes.c_int),
+                ("n_components", ctypes.c_int), ("size", ctypes.c_int * QAL_BB_MAX_BLOCKS),
+                ("nt", ctypes.c_int * QAL_BB_MAX_BLOCKS), ("row0", ctypes.c_int * QAL_BB_MAX_BLOCKS),
+                ("weight", ctypes.c_int * QAL_BB_MAX_BLOCKS), ("flops", ctypes.c_double * QAL_BB_MAX_BLOCKS),
+                ("flops_per_product", ctypes.c_double), ("nrows", ctypes.c_int), ("ntiles", ctypes.c_int),
+                ("total_doubles", ctypes.c_longlong), ("perm", ctypes.c_int * QAL_BB_MAX_ROWS),
+                ("inv", ctypes.c_int * 4096), ("comp", ctypes.c_int * 4096)]
+
+    def sizes(self):
+        return [self.size[b] for b in range(self.nb)]
+
+
+def qal_bigblock_plan_build(mats, mirror=True, stream=None) -> BigBlockPlan:
+    """Structure of n = 4096 operators (device tensor [m][4096][4096]; pattern computed on the device)."""
+    mats = _dev(mats, torch.complex128, "mats")
+    plan = BigBlockPlan()
+    rc = load().qal_bigblock_plan_build(mats.shape[0], _ptr(mats), 1 if mirror else 0, ctypes.byref(plan),
+                                        _stream(stream))
+    _check(rc, "qal_bigblock_plan_build")
+    return plan
+
+
+def qal_bigblock_expm_slices(plan: BigBlockPlan, L0, Lc, u, T, n_slices, *, count=None, chunk=None, status=None,
+                             check=True, ws=None, stream=None):
+    """Chunk products [count/chunk][4096][4096] (natural) of one pulse's PWC slices (u [count][J])."""
+    c128 = torch.complex128
+    L0 = _dev(L0, c128, "L0")
+    Lc = _dev(Lc, c128, "Lc")
+    u = _dev(u, torch.float64, "u")
+    count = u.shape[0] if count is None else count
+    chunk = count if chunk is None else chunk
+    out = torch.empty((count // chunk, 4096, 4096), dtype=c128, device=u.device)
+    wsb = load().qal_bigblock_workspace_bytes(ctypes.byref(plan))
+    if ws is None or ws.numel() < wsb:
+        ws = torch.empty(wsb, dtype=torch.uint8, device=u.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=u.device) if check else None
+    rc = load().qal_bigblock_expm_slices(ctypes.byref(plan), n_slices, float(T), count, Lc.shape[0], _ptr(u),
+                                         _ptr(L0), _ptr(Lc), chunk, _ptr(out), _ptr(status), _ptr(flag), _ptr(ws),
+                                         ws.numel(), _stream(stream))
+    _check(rc, "qal_bigblock_expm_slices")
+    return out, flag
