@@ -13,6 +13,7 @@ Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -40,7 +41,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
-    ap.add_argument("--cfg4-slices", type=int, default=8, help="slices per step of the cfg4 sample")
+    ap.add_argument("--cfg4-slices", type=int, default=None,
+                    help="slices per step of the cfg4 / hubbard3 sample (default: dense 8, blocks 64)")
     ap.add_argument("--structure", default="blocks", choices=["blocks", "dense"],
                     help="cfg2 path: coherence-block (default, SURVEY 8(f) row 4) or dense 64x64")
     ap.add_argument("--no-dense-ref", action="store_true",
@@ -525,7 +527,7 @@ def run_cfg4(args):
     dev = torch.device("cuda", local)
     _build.build()
     qal.load()
-    S = args.cfg4_slices
+    S = args.cfg4_slices or (64 if args.structure == "blocks" else 8)
     prob = qi.hubbard3() if args.config == "hubbard3" else qi.cfg4()
     pulse = rank % prob.u.shape[0]
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
@@ -541,11 +543,23 @@ def run_cfg4(args):
     lib = qal.load()
     st = lambda: qal._stream(None)  # noqa: E731
 
+    plan = None
+    if args.structure == "blocks":
+        plan = qal.qal_bigblock_plan_build(torch.cat([L0[:1], Lc]), mirror=True)
+        ws = torch.empty(lib.qal_bigblock_workspace_bytes(ctypes.byref(plan)), dtype=torch.uint8, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
     def step():
-        rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, prob.J, qal._ptr(u), qal._ptr(L0), 0,
-                                        qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
-                                        ws.numel(), st())
-        qal._check(rc, "qal_magnus_expm_slices")
+        if plan is not None:
+            rc = lib.qal_bigblock_expm_slices(ctypes.byref(plan), prob.N, prob.T, S, prob.J, qal._ptr(u[0]),
+                                              qal._ptr(L0), qal._ptr(Lc), S, qal._ptr(P), None, qal._ptr(flag),
+                                              qal._ptr(ws), ws.numel(), st())
+            qal._check(rc, "qal_bigblock_expm_slices")
+        else:
+            rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, prob.J, qal._ptr(u), qal._ptr(L0), 0,
+                                            qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
+                                            ws.numel(), st())
+            qal._check(rc, "qal_magnus_expm_slices")
         qal._check(lib.qal_fidelity(64, 1, qal._ptr(P), qal._ptr(V), qal._ptr(F), st()), "qal_fidelity")
 
     for _ in range(args.warmup):
@@ -570,11 +584,13 @@ def run_cfg4(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = t.item()
-    g_ms, g_l = stages["dense_gemm"]
-    flops_per_product = driver.complex_product_flops(n)
-    nprod = counters.cpu().tolist()[qal.STAGES.index("dense_gemm")]   # executed 4096^2 products
+    gstage = "blk_gemm" if plan is not None else "dense_gemm"
+    g_ms, g_l = stages[gstage]
+    gcount = counters.cpu().tolist()[qal.STAGES.index(gstage)]
+    gflops = driver.stage_flops(gcount, gstage) if plan is not None else gcount * driver.complex_product_flops(n)
+    nprod = gcount if plan is None else gflops / plan.flops_per_product   # 4096^2 (block) products executed
     if rank == 0:
-        ach = nprod * flops_per_product / (g_ms * 1e-3) / 1e12
+        ach = gflops / (g_ms * 1e-3) / 1e12
         line = {"metric": METRIC, "value": world * S * args.steps / (ms_max * 1e-3), "unit": UNIT,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -582,8 +598,11 @@ def run_cfg4(args):
                 "config": {"workload": f"{prob.name} sample: pulse {pulse}, first {S} of {prob.N} PWC slices, d=64 "
                                        f"(4096x4096 c128), expm + fold + fidelity", "slices_per_step": S},
                 "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
-                             "frac": ach / peak_tf, "traffic": None, "kernel": "k_dense_gemm",
+                             "frac": ach / peak_tf, "traffic": None,
+                             "kernel": "k_bb_gemm" if plan is not None else "k_dense_gemm",
                              "ms_per_launch": g_ms / max(g_l, 1)},
+                "structure": (f"coherence blocks {plan.sizes()} (mirror), {plan.flops_per_product / (8.0 * n ** 3):.4f}"
+                              " of the dense flops" if plan is not None else "dense 4096x4096"),
                 "fp64_peak_tflops": peak_tf, "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()
                                                                    if v[1]},
                 "products_per_slice": nprod / (S * args.steps),
