@@ -69,6 +69,8 @@ struct BlkDev {
   int tcol[BLK_MAX_WARPS];          // TMEM column base of warp w (in its lane quarter w % 4)
   int tstride[BLK_MAX_WARPS];       // TMEM columns per slot of warp w (R * 8C of its widest task)
   int tmem_cols;                    // columns the CTA allocates (power of two >= 32)
+  int tcache_off;                   // gradient kernel: double offset of the trace-basis cache (-1: none)
+  int tcache_w[BLK_MAX_WARPS];      // double2 offset of warp w's cache slice
   signed char perm[QAL_BLK_MAX_ROWS];      // packed row -> natural index (-1 pad)
   unsigned char weight[QAL_BLK_MAX_ROWS];  // 0 pad, 1, 2
   signed char inv[64];                     // natural index -> packed row (-1 not stored)
@@ -1178,6 +1180,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
 // --------------------------------------------------------------- gradient slices
 constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
 constexpr int BLK_TR_BUF = BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX;   // one parity's trace buffer
+constexpr int BLK_TRC_MAXJ = 2;   // PWC trace-basis cache in shared memory up to this many controls
 constexpr int BLK_GRAD_SCR = 2;   // L2 scratch images per group (squarings): E, dE
 
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
@@ -1357,9 +1360,26 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
 // weighted traces Re Tr(W_g B_m,g) over the warp's rows, added to the warp's partial sums
 template <int C, int R, bool RE>
 __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& D, const BlkBasis& B, int b, const Ctx& x,
-                                           double* tr, bool first, const Lane& L) {
+                                           double* tr, bool first, const double2* cache, const Lane& L) {
   constexpr int P = 8 * C;
   const int K = B.J + B.ncomm;
+  if (cache) {   // PWC: the warp's weighted basis values B_m[c][row], staged once in shared memory
+    for (int mm = 0; mm < K; ++mm) {
+      double v = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int i = 0; i < 2 * C; ++i) {
+          const double2 y = cache[((mm * R + r) * 2 * C + i) * 32 + L.lane];
+          v = fma(W.re[r][i], y.x, v);
+          if constexpr (!RE) v = fma(-W.im[r][i], y.y, v);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (L.lane == 0) tr[mm] = first ? v : tr[mm] + v;
+    }
+    return;
+  }
   for (int mm = 0; mm < K; ++mm) {
     const double2* Bm = (mm < B.J) ? B.Lc + (size_t)mm * B.packed
                                    : B.Lcomm + (size_t)b * B.Lcomm_stride + (size_t)(mm - B.J) * B.packed;
@@ -1391,7 +1411,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
                               double* __restrict__ grad, int* __restrict__ status, double* scr_cta, const Ctx& x,
                               double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr, double gscale,
-                              unsigned long long& nflop, const Lane& L) {
+                              double2* cache, unsigned long long& nflop, const Lane& L) {
   constexpr int IM = img_doubles(C, RE);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
@@ -1410,6 +1430,19 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   BR<C, R, RE> A, acc, Om;
   prefetch(blockIdx.x);
   if ((int)blockIdx.x < items) bbuild_omega(Om, B, G, blockIdx.x / N, blockIdx.x % N, x, L);
+  if (cache) {   // PWC trace basis: the warp's own entries B_m[c][row] x row weight, once per launch
+    for (int mm = 0; mm < B.J; ++mm)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int i = 0; i < 2 * C; ++i) {
+          const int row = 8 * (x.rt0 + r) + L.g;
+          const double w = (double)D.weight[x.row0 + row];
+          const double2 y = __ldg(B.Lc + (size_t)mm * B.packed + x.off + (4 * i + L.t) * (8 * C) + row);
+          cache[((mm * R + r) * 2 * C + i) * 32 + L.lane] = make_double2(w * y.x, w * y.y);
+        }
+    __syncwarp();
+  }
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / N, k = item % N;
     bcopy(A, Om);
@@ -1422,7 +1455,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     if (nx < items) bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
     // per-warp partial traces, double-buffered by item parity so one CTA barrier per item suffices
     double* rt = red_tr + (size_t)par * BLK_TR_BUF;
-    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * BLK_TR_MAX, true, L);
+    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * BLK_TR_MAX, true, cache, L);
     __syncthreads();   // every warp done with this item: SN / SD free, rt complete
     prefetch(nx);
     if (L.w != 0) continue;
@@ -1494,8 +1527,11 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   double* scr_cta = scratch + (size_t)blockIdx.x * 2 * (size_t)D.packed * BLK_GRAD_SCR;
   const Ctx x = ctx_of(D, T);
   double* sm = smem + D.soff[x.g];
+  double2* cache = (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ && D.tcache_off >= 0)
+                       ? reinterpret_cast<double2*>(smem + D.tcache_off) + (size_t)D.tcache_w[L.w]
+                       : nullptr;
   BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status, scr_cta,
-               x, sm, bars[x.g], tm, bad_sh, red_tr, gscale, nflop, L);
+               x, sm, bars[x.g], tm, bad_sh, red_tr, gscale, cache, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
@@ -1695,17 +1731,42 @@ size_t blk_grad_scratch_bytes(const qal_block_plan& p) {
   return (size_t)blk_grad_grid(D) * BLK_GRAD_SCR * 2 * p.packed * 8;
 }
 
+// the PWC trace-basis cache: per warp J x R x 2C x 32 double2, after the group regions
+static int grad_cache_layout(BlkDev& D, int J, int base_doubles) {
+  int o = 0;
+  for (int w = 0; w < D.nwarps; ++w) {
+    const BlkTask& T = D.task[w][0];
+    D.tcache_w[w] = o;
+    o += J * T.R * 2 * D.C[T.g] * 32;
+  }
+  D.tcache_off = (base_doubles + 15) & ~15;
+  return D.tcache_off + 2 * o;   // doubles
+}
+
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
                                    double* scratch, double gscale, cudaStream_t st) {
   BlkDev D;
   if (!to_dev(p, D)) return cudaErrorInvalidValue;
-  const size_t bytes = (size_t)grp_smem_doubles(D, per_grad) * 8;
+  const int base = grp_smem_doubles(D, per_grad);
+  const int gmax = blk_grad_grid(D);   // the scratch was sized for this grid
+  size_t bytes = (size_t)base * 8;
+  D.tcache_off = -1;
+  if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
+    BlkDev trial = D;
+    const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
+    cudaFuncAttributes fa;
+    // keep the cache only if it does not cost a CTA per SM
+    if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess &&
+        (int)(233472 / (with + fa.sharedSizeBytes + 1024)) * num_sms() >= gmax) {
+      D = trial;
+      bytes = with;
+    }
+  }
   static size_t attr = 0;
   cudaError_t e = set_smem((const void*)k_blk_grad_slices, bytes, attr);
   if (e != cudaSuccess) return e;
   const int items = batch * G.count;
-  const int gmax = blk_grad_grid(D);
   const int grid = items < gmax ? items : gmax;
   prof_pre(ST_BLK_GRAD, st);
   k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, gscale,
