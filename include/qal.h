@@ -431,6 +431,10 @@ typedef struct {
     int perm[QAL_BB_MAX_ROWS];          /* packed row -> natural index, -1 = padding          */
     int inv[4096];                      /* natural index -> packed row, -1 = mirrored         */
     int comp[4096];                     /* natural index -> component                         */
+    int real[QAL_BB_MAX_BLOCKS];        /* block b holds self-mirrored components in the real
+                                           Hermitian basis (as qal_block_plan.real)           */
+    int rtype[QAL_BB_MAX_ROWS];         /* as qal_block_plan.rtype                            */
+    int ncode[4096];                    /* as qal_block_plan.ncode                            */
 } qal_bigblock_plan;
 
 /* Structure detection for n = 4096: the union non-zero pattern of the DEVICE matrices

@@ -38,6 +38,9 @@ struct BBDev {
   const int* perm;                     // [nrows] packed row -> natural index (-1 padding)
   const int* inv;                      // [4096] natural -> packed row (-1: mirrored / not stored)
   const int* comp;                     // [4096] natural -> component
+  const int* rtype;                    // [nrows] 0 complex, 1 real diagonal, 2 pair a, 3 pair b
+  const int* ncode;                    // [4096] 0 complex, 1 real diagonal, 2 pair rep, 3 pair mirror
+  int real[QAL_BB_MAX_BLOCKS];         // block b in the real Hermitian basis (qal_blocks.cu A29)
 };
 
 struct BBPlanRec {   // per block, written on the device
@@ -108,6 +111,20 @@ __global__ void __launch_bounds__(256) k_bb_check(BBDev D, const double2* __rest
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = QAL_ERR_STRUCTURE;
 }
 
+// T[natural][packed row] of a real block row (the Hermitian basis of qal_blocks.cu, A29)
+__device__ __forceinline__ int bb_row_terms(const BBDev& D, int grow, int* R, double* tr, double* ti) {
+  const int r0 = D.perm[grow];
+  const double h = 0.70710678118654752440;
+  if (r0 < 0) return 0;
+  const int t = D.rtype[grow];
+  R[0] = r0;
+  if (t <= 1) { tr[0] = 1.0; ti[0] = 0.0; return 1; }
+  R[1] = (r0 >> 6) + 64 * (r0 & 63);
+  if (t == 2) { tr[0] = h; ti[0] = 0.0; tr[1] = h; ti[1] = 0.0; }
+  else { tr[0] = 0.0; ti[0] = h; tr[1] = 0.0; ti[1] = -h; }
+  return 2;
+}
+
 // ------------------------------------------------------------------ elementwise
 // X = h (L0 + sum_j u_j L_j) gathered into the tiled blocks (a3, PWC)
 __global__ void __launch_bounds__(NT) k_bb_omega(BBDev D, const double2* __restrict__ L0,
@@ -126,7 +143,26 @@ __global__ void __launch_bounds__(NT) k_bb_omega(BBDev D, const double2* __restr
     const int r = w >> 6, c = w & 63;
     const int R = D.perm[D.row0[b] + 64 * I + r], Cc = D.perm[D.row0[b] + 64 * Jt + c];
     double re = 0.0, im = 0.0;
-    if (R >= 0 && Cc >= 0) {
+    if (R >= 0 && Cc >= 0 && D.real[b]) {
+      // M'[r][c] = Re sum conj(T[Ri][r]) M[Ri][Cj] T[Cj][c] for M = h (L0 + sum_j u_j L_j)
+      int Ra[2], Cb[2];
+      double ar[2], ai[2], br[2], bi[2];
+      const int na = bb_row_terms(D, D.row0[b] + 64 * I + r, Ra, ar, ai);
+      const int nb = bb_row_terms(D, D.row0[b] + 64 * Jt + c, Cb, br, bi);
+      for (int i1 = 0; i1 < na; ++i1)
+        for (int j1 = 0; j1 < nb; ++j1) {
+          const size_t idx = (size_t)Ra[i1] * BBN + Cb[j1];
+          const double2 x0 = __ldg(L0 + idx);
+          double mr = cf[0] * x0.x, mi = cf[0] * x0.y;
+          for (int j = 0; j < J; ++j) {
+            const double2 x = __ldg(Lc + (size_t)j * n2 + idx);
+            mr = fma(cf[j + 1], x.x, mr);
+            mi = fma(cf[j + 1], x.y, mi);
+          }
+          const double xr = ar[i1] * mr + ai[i1] * mi, xi = ar[i1] * mi - ai[i1] * mr;   // conj(ta) m
+          re += xr * br[j1] - xi * bi[j1];                                              // ... tb
+        }
+    } else if (R >= 0 && Cc >= 0) {
       const size_t idx = (size_t)R * BBN + Cc;
       const double2 x0 = __ldg(L0 + idx);
       re = cf[0] * x0.x;
@@ -229,6 +265,18 @@ __global__ void __launch_bounds__(NT) k_bb_copy_sel(BBDev D, double* dst, const 
   }
 }
 
+// rows of natural index R in a real block and T[R][row]
+__device__ __forceinline__ int bb_nat_terms(const BBDev& D, int R, int* rows, double* tr, double* ti) {
+  const int code = D.ncode[R];
+  const double h = 0.70710678118654752440;
+  if (code == 1) { rows[0] = D.inv[R]; tr[0] = 1.0; ti[0] = 0.0; return 1; }
+  const int a = (code == 2) ? D.inv[R] : D.inv[(R >> 6) + 64 * (R & 63)];
+  if (a < 0) return 0;
+  rows[0] = a; tr[0] = h; ti[0] = 0.0;
+  rows[1] = a + 1; tr[1] = 0.0; ti[1] = (code == 2) ? h : -h;
+  return 2;
+}
+
 // natural from the tiled blocks: stored component -> value, mirrored component -> conj of the stored
 // mirror entry (Lambda[s(R), s(C)] = conj(Lambda[R, C]), s(i + d j) = j + d i), else 0
 __global__ void __launch_bounds__(NT) k_bb_unpack(BBDev D, const double* __restrict__ X, double2* __restrict__ M) {
@@ -236,7 +284,24 @@ __global__ void __launch_bounds__(NT) k_bb_unpack(BBDev D, const double* __restr
   for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < n2; e += (size_t)gridDim.x * NT) {
     const int R = (int)(e >> 12), C = (int)(e & 4095);
     double2 v = make_double2(0.0, 0.0);
-    if (D.comp[R] == D.comp[C]) {
+    if (D.comp[R] == D.comp[C] && D.ncode[R] != 0) {   // real block: M = T M' T^dag
+      int rr[2], cc[2];
+      double ar[2], ai[2], br[2], bi[2];
+      const int na = bb_nat_terms(D, R, rr, ar, ai), nb = bb_nat_terms(D, C, cc, br, bi);
+      double re = 0.0, im = 0.0;
+      for (int i1 = 0; i1 < na; ++i1)
+        for (int j1 = 0; j1 < nb; ++j1) {
+          int b = 0;
+          for (int q = 1; q < D.nb; ++q)
+            if (rr[i1] >= D.row0[q]) b = q;
+          const int lr = rr[i1] - D.row0[b], lc = cc[j1] - D.row0[b];
+          const double m = bb_tile(D, X, b, lr >> 6, lc >> 6)[img_off(lr & 63, lc & 63)];
+          const double xr = ar[i1] * m, xi = ai[i1] * m;
+          re += xr * br[j1] + xi * bi[j1];
+          im += xi * br[j1] - xr * bi[j1];
+        }
+      v = make_double2(re, im);
+    } else if (D.comp[R] == D.comp[C]) {
       int r = D.inv[R], c = D.inv[C];
       bool cj = false;
       if (r < 0) {
@@ -262,6 +327,36 @@ __global__ void __launch_bounds__(NT) k_bb_unpack(BBDev D, const double* __restr
 // C = A B block by block (C_b = A_b B_b), accumulator initialised to cid I + sum coef[q] src[q];
 // slot >= 0: a squaring, active for block b only when slot < plan[b].s; A_alt is used for blocks with
 // odd plan[b].s (the result of their squarings).
+// acc.re += a.re * B.re (a real block: 1 DMMA per 8x8x4 step)
+__device__ __forceinline__ void mma_acc_re(Strip& acc, const Strip& a, const double* __restrict__ Bs,
+                                           const Lane& L) {
+  const int todd = L.t & 1;
+  const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);
+  const uint32_t bO = smem_u32(Bs + L.t * 64 + L.g - 8 * todd);
+  double br[2][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) br[0][j] = lds_v(((j & 1) ? bO : bE) + 8u * (8 * j));
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int cur = q & 1;
+    if (q + 1 < 16) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) br[cur ^ 1][j] = lds_v(((j & 1) ? bO : bE) + 8u * ((q + 1) * 256 + 8 * j));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma(acc.re[2 * j], acc.re[2 * j + 1], a.re[q], br[cur][j]);
+  }
+  QAL_FENCE();
+}
+__device__ __forceinline__ void load_img_re(Strip& s, const double* __restrict__ img, const Lane& L) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double2 a = *reinterpret_cast<const double2*>(img + pair_off(L, j));
+    s.re[2 * j] = a.x; s.re[2 * j + 1] = a.y;
+    s.im[2 * j] = 0.0; s.im[2 * j + 1] = 0.0;
+  }
+}
+
 struct BBGemm {
   const double* A;
   const double* A_alt;
@@ -297,6 +392,13 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
       if (bb_active(D, g, b)) atomicAdd(g.ctr, g.bflops[b]);
   int t = bb_next_tile(D, g, blockIdx.x, gridDim.x);
   if (t >= D.ntiles) return;
+  // a real block's tiles carry only their re plane (the im plane is zero and never read)
+  auto tma_tile = [&](double* dst, const double* src, uint64_t* br, bool real) {
+    if (!real) { tma_load_img(dst, src, br); return; }
+    mbar_expect_tx(br, PLANE * 8);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) bulk_g2s(dst + q * (PLANE / 2), src + q * (PLANE / 2), PLANE * 4, br);
+  };
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -309,8 +411,8 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
   int tl = t - D.tstart[b];
   int I = tl / D.nt[b], J = tl % D.nt[b];
   if (threadIdx.x == 0) {
-    tma_load_img(SA, bb_tile(D, Aof(b), b, I, 0), &bar[0]);
-    tma_load_img(SB[0], bb_tile(D, g.B, b, 0, J), &bar[1]);
+    tma_tile(SA, bb_tile(D, Aof(b), b, I, 0), &bar[0], D.real[b]);
+    tma_tile(SB[0], bb_tile(D, g.B, b, 0, J), &bar[1], D.real[b]);
   }
   uint32_t phA = 0, phB[2] = {0, 0};
   int step = 0;
@@ -341,7 +443,8 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
       phA ^= 1;
       mbar_wait(&bar[1 + cur], phB[cur]);
       phB[cur] ^= 1;
-      load_img(a, SA, L);
+      if (D.real[b]) load_img_re(a, SA, L);
+      else load_img(a, SA, L);
       __syncthreads();   // SA drained by every warp; SB[cur^1] no longer read
       if (threadIdx.x == 0) {
         int tn = t, Kn = K + 1, bn = b, In = I, Jn = J;
@@ -357,11 +460,16 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
         }
         if (tn < D.ntiles) {
           fence_proxy_async();
-          tma_load_img(SA, bb_tile(D, Aof(bn), bn, In, Kn), &bar[0]);
-          tma_load_img(SB[cur ^ 1], bb_tile(D, g.B, bn, Kn, Jn), &bar[1 + (cur ^ 1)]);
+          tma_tile(SA, bb_tile(D, Aof(bn), bn, In, Kn), &bar[0], D.real[bn]);
+          tma_tile(SB[cur ^ 1], bb_tile(D, g.B, bn, Kn, Jn), &bar[1 + (cur ^ 1)], D.real[bn]);
         }
       }
-      mma_acc(acc, a, SB[cur], L);
+      if (D.real[b]) mma_acc_re(acc, a, SB[cur], L);
+      else mma_acc(acc, a, SB[cur], L);
+    }
+    if (D.real[b]) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc.im[i] = 0.0;   // keep the unused plane zero
     }
     store_img(bb_tile(D, g.C, b, I, J), acc, L);
     t = tnext;
@@ -377,7 +485,7 @@ int bb_grid_ew() { return 4 * num_sms(); }
 size_t bb_ws_bytes(const qal_bigblock_plan& p) {
   // 8 tiled-block matrices + column partials + per-block plan records + device tables
   return 8 * (size_t)p.total_doubles * 8 + (size_t)p.ntiles * 64 * 8 + 64 * sizeof(BBPlanRec) +
-         (size_t)(p.nrows + 2 * BBN) * sizeof(int) + 1024;
+         (size_t)(2 * p.nrows + 3 * BBN) * sizeof(int) + 1024;
 }
 
 // device view; copies the index tables into `tab` (device, inside the workspace) on `st`
@@ -396,14 +504,21 @@ static cudaError_t bb_dev(const qal_bigblock_plan& p, int* tab, BBDev& D, cudaSt
     ts += p.nt[b] * p.nt[b];
   }
   D.tstart[p.nb] = ts;
-  std::vector<int> h(p.nrows + 2 * BBN);
-  for (int r = 0; r < p.nrows; ++r) h[r] = p.perm[r];
-  for (int i = 0; i < BBN; ++i) { h[p.nrows + i] = p.inv[i]; h[p.nrows + BBN + i] = p.comp[i]; }
+  std::vector<int> h(2 * p.nrows + 3 * BBN);
+  for (int r = 0; r < p.nrows; ++r) { h[r] = p.perm[r]; h[p.nrows + 3 * BBN + r] = p.rtype[r]; }
+  for (int i = 0; i < BBN; ++i) {
+    h[p.nrows + i] = p.inv[i];
+    h[p.nrows + BBN + i] = p.comp[i];
+    h[p.nrows + 2 * BBN + i] = p.ncode[i];
+  }
+  for (int b = 0; b < p.nb; ++b) D.real[b] = p.real[b];
   // pageable source: the runtime stages it before returning, so `h` may die with this frame
   const cudaError_t e = cudaMemcpyAsync(tab, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, st);
   D.perm = tab;
   D.inv = tab + p.nrows;
   D.comp = tab + p.nrows + BBN;
+  D.ncode = tab + p.nrows + 2 * BBN;
+  D.rtype = tab + p.nrows + 3 * BBN;
   return e;
 }
 
@@ -455,17 +570,18 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
   std::stable_sort(keep.begin(), keep.end(), [&](int a, int b) { return members[a].size() > members[b].size(); });
   // best-fit-decreasing packing of the components into blocks of 64-multiple width (components that
   // share a block are multiplied densely together -- their cross terms are zero)
-  struct Bin { int width, used; std::vector<int> comps; };
+  struct Bin { int width, used, real; std::vector<int> comps; };
   std::vector<Bin> bins;
   for (int k : keep) {
     const int sz = (int)members[k].size();
+    const int rl = (mir[k] == k);   // self-mirrored: real in the Hermitian basis
     int best = -1;
     for (int i = 0; i < (int)bins.size(); ++i)
-      if (bins[i].used + sz <= bins[i].width &&
+      if (bins[i].real == rl && bins[i].used + sz <= bins[i].width &&
           (best < 0 || bins[i].width - bins[i].used < bins[best].width - bins[best].used))
         best = i;
     if (best >= 0) { bins[best].used += sz; bins[best].comps.push_back(k); }
-    else bins.push_back({(sz + 63) / 64 * 64, sz, {k}});
+    else bins.push_back({(sz + 63) / 64 * 64, sz, rl, {k}});
   }
   if ((int)bins.size() > QAL_BB_MAX_BLOCKS) return QAL_ERR_UNSUPPORTED;
   qal_bigblock_plan p;
@@ -475,8 +591,8 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
   p.mirror = mirror ? 1 : 0;
   p.nb = (int)bins.size();
   p.n_components = ncomp;
-  for (int i = 0; i < QAL_BB_MAX_ROWS; ++i) p.perm[i] = -1;
-  for (int i = 0; i < BBN; ++i) { p.inv[i] = -1; p.comp[i] = cid[i]; }
+  for (int i = 0; i < QAL_BB_MAX_ROWS; ++i) { p.perm[i] = -1; p.rtype[i] = 0; }
+  for (int i = 0; i < BBN; ++i) { p.inv[i] = -1; p.comp[i] = cid[i]; p.ncode[i] = 0; }
   int row = 0, tiles = 0;
   double flops = 0.0;
   for (int b = 0; b < p.nb; ++b) {
@@ -485,16 +601,25 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
     p.row0[b] = row;
     p.weight[b] = 1;
     if (row + bins[b].width > QAL_BB_MAX_ROWS) return QAL_ERR_UNSUPPORTED;
+    p.real[b] = bins[b].real;
     int r = row;
     double fl = 0.0;
     for (int k : bins[b].comps) {
       for (int i : members[k]) {
-        p.perm[r] = i;
-        p.inv[i] = r;
-        ++r;
+        const int si = (i >> 6) + 64 * (i & 63);
+        if (!bins[b].real) {
+          p.perm[r] = i; p.inv[i] = r; ++r;
+        } else if (si == i) {
+          p.perm[r] = i; p.rtype[r] = 1; p.inv[i] = r; p.ncode[i] = 1; ++r;
+        } else if (i < si) {
+          p.perm[r] = i; p.rtype[r] = 2; p.inv[i] = r; p.ncode[i] = 2;
+          p.perm[r + 1] = i; p.rtype[r + 1] = 3;
+          p.ncode[si] = 3;
+          r += 2;
+        }
       }
       const double sz = (double)members[k].size();
-      fl += 2.0 * QAL_REAL_MMAS_PER_CMMA * sz * sz * sz;
+      fl += (bins[b].real ? 2.0 : 2.0 * QAL_REAL_MMAS_PER_CMMA) * sz * sz * sz;
     }
     p.flops[b] = fl;
     flops += fl;

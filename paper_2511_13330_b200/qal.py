@@ -653,7 +653,9 @@ class BigBlockPlan(ctypes.Structure):
                 ("weight", ctypes.c_int * QAL_BB_MAX_BLOCKS), ("flops", ctypes.c_double * QAL_BB_MAX_BLOCKS),
                 ("flops_per_product", ctypes.c_double), ("nrows", ctypes.c_int), ("ntiles", ctypes.c_int),
                 ("total_doubles", ctypes.c_longlong), ("perm", ctypes.c_int * QAL_BB_MAX_ROWS),
-                ("inv", ctypes.c_int * 4096), ("comp", ctypes.c_int * 4096)]
+                ("inv", ctypes.c_int * 4096), ("comp", ctypes.c_int * 4096),
+                ("real", ctypes.c_int * QAL_BB_MAX_BLOCKS), ("rtype", ctypes.c_int * QAL_BB_MAX_ROWS),
+                ("ncode", ctypes.c_int * 4096)]
 
     def sizes(self):
         return [self.size[b] for b in range(self.nb)]
