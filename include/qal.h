@@ -179,6 +179,8 @@ int qal_batched_matmul(int n, int count, const qal_c128 *A, long long strideA, c
  * (the superoperator of rho -> V rho V^dag under column stacking).  S_V is never
  * formed: S_V[i+dj, k+dl] = conj(V[j][l]) V[i][k].  Fixed-order reduction.
  *   Lambda [batch][n][n], V [d][d], F [batch] (f64).
+ * d = 64 with batch <= 64 reduces over 512 row slabs per pulse through a static device scratch:
+ * such calls must not run concurrently on two streams.
  */
 int qal_fidelity(int d, int batch, const qal_c128 *Lambda, const qal_c128 *V, double *F,
                  void *stream);
@@ -438,8 +440,9 @@ typedef struct {
 } qal_bigblock_plan;
 
 /* Structure detection for n = 4096: the union non-zero pattern of the DEVICE matrices
- * mats[nmat][4096][4096] is computed on the device, its connected components and Hermitian mirror
- * pairing on the host (synchronises `stream`).  QAL_ERR_UNSUPPORTED beyond 48 stored blocks. */
+ * mats[nmat][4096][4096] is computed on the device (a 2 MB temporary, allocated and freed
+ * stream-ordered: a setup call), its connected components and Hermitian mirror pairing on the host
+ * (synchronises `stream`).  QAL_ERR_UNSUPPORTED beyond 48 stored blocks. */
 int qal_bigblock_plan_build(int nmat, const qal_c128 *mats, int mirror, qal_bigblock_plan *plan, void *stream);
 
 size_t qal_bigblock_workspace_bytes(const qal_bigblock_plan *plan);

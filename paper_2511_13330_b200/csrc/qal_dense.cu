@@ -515,11 +515,50 @@ cudaError_t launch_dense_liouvillian(int batch, const double2* H0, int J, const 
   return cudaGetLastError();
 }
 
+// static scratch of the n = 4096 fidelity: calls that run concurrently on different streams must not
+// both use it (the library's n = 4096 path is one pulse per call on one stream)
+__device__ double g_fid_part[64 * 512];
+
+// fidelity over 512 row slabs of 8 rows per pulse (HBM-bound: 268 MB per pulse), then a fixed-order sum
+__global__ void __launch_bounds__(NT) k_dense_fid_slab(const double2* __restrict__ Lam, const double2* __restrict__ V,
+                                                       double* __restrict__ part) {
+  __shared__ double red[16];
+  const Lane L = lane_id();
+  const int slab = blockIdx.x, b = blockIdx.y;
+  const double2* M = Lam + (size_t)b * 4096 * 4096 + (size_t)slab * 8 * 4096;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < 8 * 4096; e += NT) {
+    const int a = slab * 8 + (e >> 12), c = e & 4095;
+    const int i = a & 63, j = a >> 6, k = c & 63, l = c >> 6;
+    const double2 vjl = __ldg(V + j * 64 + l), vik = __ldg(V + i * 64 + k);
+    const double2 x = __ldg(M + e);
+    const double wr = vjl.x * vik.x + vjl.y * vik.y, wi = vjl.y * vik.x - vjl.x * vik.y;
+    acc += wr * x.x - wi * x.y;
+  }
+  const double s = block_sum(acc, red, L);
+  if (threadIdx.x == 0) part[(size_t)b * 512 + slab] = s;
+}
+__global__ void __launch_bounds__(32) k_dense_fid_sum(const double* __restrict__ part, double* __restrict__ F) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int q = 0; q < 512; ++q) s += part[(size_t)blockIdx.x * 512 + q];
+  F[blockIdx.x] = s / 4096.0;
+}
+
 cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st) {
   prof_pre(ST_FID, st);
-  k_dense_fid_1cta<<<batch, 1024, 0, st>>>(Lam, V, F);
+  if (batch <= 64) {
+    double* part = nullptr;   // 512 partials per pulse in the module's static scratch (no allocation)
+    cudaError_t e = cudaGetSymbolAddress(reinterpret_cast<void**>(&part), g_fid_part);
+    if (e != cudaSuccess) return e;
+    k_dense_fid_slab<<<dim3(512, batch), NT, 0, st>>>(Lam, V, part);
+    k_dense_fid_sum<<<batch, 32, 0, st>>>(part, F);
+    launch_counter() += 2;
+  } else {
+    k_dense_fid_1cta<<<batch, 1024, 0, st>>>(Lam, V, F);
+    ++launch_counter();
+  }
   prof_post(ST_FID, st);
-  ++launch_counter();
   return cudaGetLastError();
 }
 
