@@ -446,6 +446,7 @@ def qal_fp64_peak_probe(kind: int, blocks: int, iters: int, sink, stream=None) -
 QAL_BLK_MAX_GROUPS = 16
 QAL_BLK_MAX_ROWS = 96
 QAL_ERR_STRUCTURE = -8
+QAL_ERR_NONFINITE = -4
 
 
 class BlockPlan(ctypes.Structure):

@@ -351,3 +351,44 @@ def test_time_sharded_gradient_blocks_matches_oracle(torch_cuda, qal, oracle):
     Fr, gr, Lr = oracle.gradient(rL0, rLc, u[0], T, N, p.V, mode=1)
     assert relfro(qal.qal_block_unpack(plan, Lam.unsqueeze(0))[0].cpu().numpy(), Lr) <= TOL_PROP
     assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
+
+
+# ------------------------------------------------------------------ status flags, determinism, structure check
+def test_block_status_flags_nonfinite_input(torch_cuda, qal):
+    torch = torch_cuda
+    p = qi.cfg0(N=8)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    u = np.concatenate([p.u, p.u], axis=0)
+    u[1, 3, 0] = np.nan
+    V = dev(torch, p.V)
+    for want_grad in (False, True):
+        status = torch.full((2,), 7, dtype=torch.int32, device="cuda")
+        qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, u), p.T, p.N, V, want_grad=want_grad, status=status)
+        assert status.cpu().tolist() == [0, qal.QAL_ERR_NONFINITE]
+
+
+def test_block_path_bit_identical_runs(torch_cuda, qal):
+    torch = torch_cuda
+    p = qi.cfg2(batch=7, N=64, T=200.0 * 64 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    outs = [qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V), want_Lambda=True)
+            for _ in range(2)]
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+
+
+def test_pulse_batch_reports_a_broken_structure(torch_cuda, qal):
+    """A transverse drift term (sigma_x on spin 1) breaks total S_z: the per-call device check of the
+    bench engine reports it (the plan was detected from the symmetric basis)."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg2(batch=3, N=8, T=2.0)
+    args = [dev(torch, a) for a in (p.H0, p.Hc, p.C, p.u, p.V)]
+    eng = driver.PulseBatch(*args, p.T, structure="blocks")
+    eng.step()
+    assert eng.structure_ok()
+    sx = np.kron(np.array([[0, 1], [1, 0]], dtype=complex), np.eye(4))
+    eng.H0[2] += dev(torch, 0.01 * sx)
+    eng.H0 = eng.H0.contiguous()
+    eng.step()
+    assert not eng.structure_ok()
