@@ -130,3 +130,75 @@ def test_product_path_has_no_oracle_or_cpu_fallback():
                 text = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", text, re.M), f
                 assert "qalref" not in text and "libqalref" not in text, f
+
+
+# ------------------------------------------------------------------ coherence-block entry points
+@pytest.fixture(scope="module")
+def plan(lib):
+    """A real plan from the configs[0] basis (host call: no device work)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2511_13330_b200 import inputs as qi, qal
+    oracle.build()
+    p = qi.cfg0(N=4, T=1.0)
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    return qal.qal_block_plan_build(torch.from_numpy(np.concatenate([L0[None], Lc])), mirror=True)
+
+
+def test_block_plan_rejects_bad_input(lib):
+    from paper_2511_13330_b200 import qal
+    pl = qal.BlockPlan()
+    buf = (ctypes.c_double * (2 * 16 * 16))()
+    assert lib.qal_block_plan_build(16, 1, buf, 1, ctypes.byref(pl)) == -5       # n = 64 only
+    assert lib.qal_block_plan_build(64, 0, buf, 1, ctypes.byref(pl)) == -3
+    assert lib.qal_block_plan_build(64, 1, None, 1, ctypes.byref(pl)) == -1
+    nan = (ctypes.c_double * (2 * 64 * 64))()
+    nan[0] = float("nan")
+    assert lib.qal_block_plan_build(64, 1, nan, 1, ctypes.byref(pl)) == -4
+
+
+def test_block_calls_validate_before_launch(lib, plan):
+    p = ctypes.c_void_p(1)
+    bp = ctypes.byref(plan)
+    P = plan.packed
+    # expm slices: empty batch, bad order, chunk not dividing, missing output, bad stride
+    assert lib.qal_block_expm_slices(bp, 0, 8, 1.0, 0, 8, 4, 0, 2, p, p, 0, p, None, 0, 1, p, None, None) == -3
+    assert lib.qal_block_expm_slices(bp, 1, 8, 1.0, 0, 8, 3, 0, 2, p, p, 0, p, None, 0, 1, p, None, None) == -5
+    assert lib.qal_block_expm_slices(bp, 1, 8, 1.0, 0, 8, 4, 0, 2, p, p, 0, p, None, 0, 3, p, None, None) == -2
+    assert lib.qal_block_expm_slices(bp, 1, 8, 1.0, 0, 8, 4, 0, 2, p, p, 0, p, None, 0, 1, None, None, None) == -1
+    assert lib.qal_block_expm_slices(bp, 1, 8, 1.0, 0, 8, 4, 0, 2, p, p, P + 1, p, None, 0, 1, p, None, None) == -2
+    # fidelity-gradient: workspace, V
+    args = [bp, 1, 16, 1.0, 4, 0, 2, p, p, 0, p, None, 0, p, p, p, None, None, None, 0, None]
+    assert lib.qal_block_fidelity_grad(*args) == -6
+    a2 = list(args)
+    a2[13] = None
+    assert lib.qal_block_fidelity_grad(*a2) == -1
+    # a corrupted plan is refused
+    bad = type(plan).from_buffer_copy(plan)
+    bad.width[0] = 40
+    assert lib.qal_block_pack(ctypes.byref(bad), 1, p, p, None, None) == -2
+    assert lib.qal_block_pack(bp, 0, p, p, None, None) == -3
+    assert lib.qal_block_ordered_product(bp, 1, 5, p, p, None, 0, None) == -6
+    assert lib.qal_block_batched_matmul(bp, 2, p, 7, p, 0, p, None) == -2
+    assert lib.qal_block_fidelity_cotangent(bp, None, p, None) == -1
+
+
+def test_block_workspace_sizes(lib, plan):
+    bp = ctypes.byref(plan)
+    M = plan.packed * 16
+    assert lib.qal_block_workspace_bytes(bp, 1, 1, 2) == 0
+    assert lib.qal_block_workspace_bytes(bp, 1, 2, 7) == 2 * (4 + 2) * M
+    assert lib.qal_block_workspace_bytes(bp, 3, 3, 16) >= 3 * 3 * 16 * M
+    assert lib.qal_block_workspace_bytes(bp, 5, 3, 16) == lib.qal_block_workspace_bytes(bp, 3, 3, 16)
+
+
+def test_bigblock_calls_validate(lib):
+    from paper_2511_13330_b200 import qal
+    p = ctypes.c_void_p(1)
+    pl = qal.BigBlockPlan()
+    assert lib.qal_bigblock_plan_build(0, p, 1, ctypes.byref(pl), None) == -3
+    assert lib.qal_bigblock_plan_build(1, None, 1, ctypes.byref(pl), None) == -1
+    assert lib.qal_bigblock_workspace_bytes(ctypes.byref(pl)) == 0               # empty plan
+    assert lib.qal_bigblock_expm_slices(ctypes.byref(pl), 8, 1.0, 8, 2, p, p, p, 8, p, None, None, p, 1, None) == -5
