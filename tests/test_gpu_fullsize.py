@@ -120,3 +120,73 @@ def oracle_range(oracle, L0, Lc, u_rows, T, N, k0, count):
     full = np.zeros((k0 + count,) + u_rows.shape[1:])
     full[k0:] = u_rows
     return oracle.propagate(L0, Lc, full, T, N, mode=1, k0=k0, k1=k0 + count)
+
+
+# ---- coherence-block path (bench.py's default structure) at the same full sizes -----------------------
+
+@pytest.fixture(scope="module")
+def cfg2_full_blocks(torch_cuda, qal):
+    """configs[2] at full size through driver.PulseBatch(structure="blocks") with bench.py's automatic
+    sub-batch -- the exact launch configuration of the headline bench line."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p = qi.cfg2()
+    eng = driver.PulseBatch(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C), to(torch, p.u), to(torch, p.V),
+                            p.T, structure="blocks")
+    F, g = eng.step()
+    torch.cuda.synchronize()
+    ok = eng.structure_ok()
+    out = (p, F.cpu().numpy(), g.cpu().numpy(), eng.status.cpu().numpy(), ok, eng.sub)
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.parametrize("which", ["first", "last_of_sub", "first_of_next", "middle", "last"])
+def test_cfg2_blocks_full_size_sampled_pulses(cfg2_full_blocks, oracle, which):
+    p, F, g, status, ok, sub = cfg2_full_blocks
+    assert ok
+    pulse = {"first": 0, "last_of_sub": sub - 1, "first_of_next": sub, "middle": 2047, "last": 4095}[which]
+    assert status[pulse] == 0
+    L0, Lc = oracle.build_liouvillian(p.H0[pulse], p.Hc, p.C)
+    Fr, gr, _ = oracle.gradient(L0, Lc, p.u[pulse], p.T, p.N, p.V)
+    assert abs(F[pulse] - Fr) / abs(Fr) <= 1e-10
+    assert relfro(g[pulse], gr) <= 1e-8
+
+
+def test_cfg2_blocks_full_size_properties_and_dense_agreement(cfg2_full_blocks, cfg2_full):
+    """Every one of the 4096 pulses: finite, F in (0, 1), and the same F / gradient as the dense path
+    (two independent kernel families; the block path drops only exact zeros, A26)."""
+    _, F, g, status, ok, _ = cfg2_full_blocks
+    _, Fd, gd, _ = cfg2_full
+    assert ok and np.all(status == 0)
+    assert np.all(np.isfinite(F)) and np.all(np.isfinite(g))
+    assert np.all((F > 0.0) & (F < 1.0))
+    assert np.max(np.abs(F - Fd) / np.abs(Fd)) <= 1e-11
+    rel = np.linalg.norm((g - gd).reshape(len(g), -1), axis=1) / np.linalg.norm(gd.reshape(len(gd), -1), axis=1)
+    assert np.max(rel) <= 1e-9
+
+
+def test_cfg3_blocks_full_horizon_bit_identity_and_dense_agreement(cfg3_full, qal, torch_cuda):
+    """N = 2^20 on the packed block path (bench.py --config cfg3): the time-sharded product is
+    bit-identical across G = 1, 2, 4, 8 (A16) and its unpacked Lambda equals the dense one."""
+    torch = torch_cuda
+    from paper_2511_13330_b200 import driver
+    p, L0, Lc, Lcomm, u = cfg3_full
+    plan = qal.qal_block_plan_build(torch.cat([L0, Lc, Lcomm.reshape(-1, 64, 64)]), mirror=True)
+    L0p, Lcp, Lcommp = (qal.qal_block_pack(plan, m, check=True)[0] for m in (L0, Lc, Lcomm))
+    N = p.N
+    lam = {}
+    for G in (1, 2, 4, 8):
+        parts = []
+        for r in range(G):
+            k0, k1 = driver.shard_range(N, G, r)
+            parts.append(driver.local_partial(L0p, Lcp, Lcommp, u[k0:k1].unsqueeze(0).contiguous(), p.T, N, k0,
+                                              ctrl_mode=1, plan=plan))
+        lam[G] = driver.ordered_combine(torch.stack(parts), plan=plan)
+    for G in (2, 4, 8):
+        assert torch.equal(lam[G], lam[1]), G
+    Lam_b = qal.qal_block_unpack(plan, lam[1].unsqueeze(0))[0].cpu().numpy()
+    Lam_d = driver.ordered_combine(torch.stack([driver.local_partial(L0, Lc, Lcomm, u.unsqueeze(0).contiguous(),
+                                                                     p.T, N, 0, ctrl_mode=1)])).cpu().numpy()
+    assert relfro(Lam_b, Lam_d) <= 1e-10
