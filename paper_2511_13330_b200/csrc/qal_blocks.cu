@@ -47,6 +47,16 @@ constexpr int BLK_CPLX_MMAS = 3;
 #else
 constexpr int BLK_CPLX_MMAS = 4;
 #endif
+// issue order of the 4 real MMAs of a complex step: two passes over the tiles (default) or the
+// accumulator pairs back to back (-DQAL_BLK_INTERLEAVE=0)
+#ifndef QAL_BLK_INTERLEAVE
+#define QAL_BLK_INTERLEAVE 1
+#endif
+constexpr bool BLK_INTERLEAVE = QAL_BLK_INTERLEAVE != 0;
+// gradient squarings: E, dE in shared memory (default) or in the L2 scratch (-DQAL_BLK_SQ_SMEM=0)
+#ifndef QAL_BLK_SQ_SMEM
+#define QAL_BLK_SQ_SMEM 1
+#endif
 constexpr int BLK_MAX_TASKS = 3;
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
@@ -453,6 +463,21 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
             dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
             dmma(g3q[r][2 * j], g3q[r][2 * j + 1], ai, bi[cur][j]);
             dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], as, bs);
+          }
+        } else if constexpr (BLK_INTERLEAVE) {
+          // two passes over the output tiles: the 2C accumulators of a pass are independent, so
+          // the second MMA into an accumulator issues 2C MMAs after the first (mma.sync is
+          // volatile asm: ptxas keeps program order, it will not interleave the chains itself)
+          const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
+            dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ar, bi[cur][j]);
+          }
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], nai, bi[cur][j]);
+            dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ai, br[cur][j]);
           }
         } else {
           const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
@@ -1197,9 +1222,20 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   double* gdX = sX + IM;
   double* gA6 = sX + 2 * IM;
   double* gdA6 = sX + 3 * IM;
+#if QAL_BLK_SQ_SMEM
+  // squarings: E, dE reuse the A6 / dA6 slots (dead once the polynomial is formed; own strips,
+  // so a lane re-reads only what it wrote)
+  double* gE = gA6;
+  double* gdE = gdA6;
+#define SQ_LD(s_, img_) bload_img(s_, img_, x, L)
+#define SQ_ST(img_, s_) bstore_img(img_, s_, x, L)
+#else
   // L2 scratch (squarings only): E, dE
   double* gE = scr;
   double* gdE = scr + IM;
+#define SQ_LD(s_, img_) bload_img_l2(s_, img_, x, L, keep)
+#define SQ_ST(img_, s_) bstore_img_l2(img_, s_, x, L, keep)
+#endif
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
   const uint64_t keep = l2_evict_last();
   // A holds Omega_k on entry (built one item ahead by the caller)
@@ -1253,14 +1289,14 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
     bmma<C, R, KS, RE>(acc, A, SV, x, L);
     bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img(A, c_t8[3], gX, x, L);    // L
     bmma<C, R, KS, RE>(acc, A, SD, x, L);
-    if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
+    if (s > 0) SQ_ST(gdE, acc);
     np += 1 + 2 + 2;
     if (s > 0) {
       bzero(acc);
       bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img(acc, 1.0, gX, x, L);
       badd_diag(acc, 1.0, x, L);
       bmma<C, R, KS, RE>(acc, A, SV, x, L);
-      bstore_img_l2(gE, acc, x, L, keep);
+      SQ_ST(gE, acc);
       ++np;
     }
   } else {
@@ -1324,7 +1360,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
     baxpy_img(A, c_t18[T18_B3][1], gX, x, L); bt_axpy(A, c_t18[T18_B3][2], T0);
     bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img(A, c_t18[T18_B3][4], gA6, x, L);
     bmma<C, R, KS, RE>(acc, A, SN, x, L);
-    if (s > 0) bstore_img_l2(gdE, acc, x, L, keep);
+    if (s > 0) SQ_ST(gdE, acc);
     np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
     if (s > 0) {                                       // T = B2 + L A9
       bzero(acc);
@@ -1332,29 +1368,31 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
       baxpy_img(acc, c_t18[T18_B2][1], gX, x, L); bt_axpy(acc, c_t18[T18_B2][2], T0);
       bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img(acc, c_t18[T18_B2][4], gA6, x, L);
       bmma<C, R, KS, RE>(acc, A, SV, x, L);
-      bstore_img_l2(gE, acc, x, L, keep);
+      SQ_ST(gE, acc);
       ++np;
     }
   }
   for (int q = 0; q < s; ++q) {                        // (E, dE) <- (E E, dE E + E dE)
     grp_sync(x);
-    bload_img_l2(A, gE, x, L, keep);
+    SQ_LD(A, gE);
     bstore_img(SV, A, x, L);
-    bload_img_l2(acc, gdE, x, L, keep);
+    SQ_LD(acc, gdE);
     bstore_img(SD, acc, x, L);
     grp_sync(x);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // E dE
-    bload_img_l2(A, gdE, x, L, keep);
+    SQ_LD(A, gdE);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dE E
-    bstore_img_l2(gdE, acc, x, L, keep);
-    bload_img_l2(A, gE, x, L, keep);
+    SQ_ST(gdE, acc);
+    SQ_LD(A, gE);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // E E
-    bstore_img_l2(gE, acc, x, L, keep);
+    SQ_ST(gE, acc);
     np += 3;
   }
-  if (s > 0) bload_img_l2(A, gdE, x, L, keep);
+  if (s > 0) SQ_LD(A, gdE);
   else bcopy(A, acc);
   return np;
+#undef SQ_LD
+#undef SQ_ST
 }
 
 // weighted traces Re Tr(W_g B_m,g) over the warp's rows, added to the warp's partial sums
