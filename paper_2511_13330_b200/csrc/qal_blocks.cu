@@ -40,7 +40,9 @@
 
 namespace qal {
 
-constexpr int BLK_MAX_WARPS = 8;
+constexpr int BLK_MAX_WARPS = 12;
+constexpr int BLK_FUSED_WARPS = 8;   // one item per CTA, all groups (every kernel but fwd / grad sets)
+constexpr int BLK_MAX_SLOTS = 4;   // independent item streams per CTA (group-specialised launches)
 // real MMAs per complex 8x8x4 step of the complex blocks: 4 (default) or 3 (Gauss, -DQAL_BLK_3M)
 #ifdef QAL_BLK_3M
 constexpr int BLK_CPLX_MMAS = 3;
@@ -53,10 +55,6 @@ constexpr int BLK_CPLX_MMAS = 4;
 #define QAL_BLK_INTERLEAVE 1
 #endif
 constexpr bool BLK_INTERLEAVE = QAL_BLK_INTERLEAVE != 0;
-// gradient squarings: E, dE in shared memory (default) or in the L2 scratch (-DQAL_BLK_SQ_SMEM=0)
-#ifndef QAL_BLK_SQ_SMEM
-#define QAL_BLK_SQ_SMEM 1
-#endif
 constexpr int BLK_MAX_TASKS = 3;
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
@@ -64,10 +62,16 @@ constexpr int BLK_MAX_TASKS = 3;
 
 // ------------------------------------------------------------------ device plan
 struct BlkTask {
-  signed char g, rt0, R, pad;   // group, first row tile, row tiles owned
+  signed char g, rt0, R, slot;   // group, first row tile, row tiles owned, item slot of the CTA
+  signed char bar, pad[3];       // named barrier of the (slot, group) pair
 };
 struct BlkDev {
   int ngroups, nwarps, packed, d;
+  unsigned gmask;                  // groups of this launch
+  int nslot;                       // item slots per CTA (1: one item, all groups of the set)
+  int swarps;                      // warps per slot
+  int sstride;                     // shared-memory doubles per slot
+  signed char sbar[BLK_MAX_SLOTS]; // per-slot barrier: 0 = __syncthreads, -1 = __syncwarp, else named
   int C[QAL_BLK_MAX_GROUPS];       // column (= row) tiles of group g
   int ks[QAL_BLK_MAX_GROUPS];      // k-steps of 4 covering the used rows of group g
   int off[QAL_BLK_MAX_GROUPS];     // complex offset of group g in a packed matrix
@@ -94,7 +98,9 @@ struct BlkDev {
 // warp roles: C = 3 groups -> 3 warps (one strip each); C <= 2 groups -> whole group on one
 // warp, greedily stacked so that no warp exceeds the heaviest single-strip load
 
-bool to_dev(const qal_block_plan& p, BlkDev& D) {
+// gmask: the groups this launch runs (bit g); nslot: independent item streams per CTA, each with its
+// own warps, barriers and shared-memory regions (one set of groups = one launch, see blk_sets).
+bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot = 1) {
   memset(&D, 0, sizeof(D));
   D.ngroups = p.ngroups;
   D.packed = p.packed;
@@ -114,16 +120,18 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
   auto cost = [&](int g, int R) { return D.C[g] * R * D.ks[g] * (D.real[g] ? 1 : BLK_CPLX_MMAS); };
   int best_mask = -1, best_max = 1 << 30, best_w = 1 << 30;
   const char* env = getenv("QAL_BLK_SPLIT");
+  if (env && !*env) env = nullptr;
   for (int mask = 0; mask < (1 << p.ngroups); ++mask) {
     int mx = 0, nw = 0;
     bool ok = true;
     for (int g = 0; g < p.ngroups; ++g) {
+      if (!((gmask >> g) & 1)) continue;
       const bool split = (mask >> g) & 1;
       if ((split && D.C[g] == 1) || (!split && D.C[g] == 3)) { ok = false; break; }   // roles (3,1) (2,1|2) (1,1)
       mx = std::max(mx, cost(g, split ? 1 : D.C[g]));
       nw += split ? D.C[g] : 1;
     }
-    if (!ok || nw > BLK_MAX_WARPS) continue;
+    if (!ok || nw * nslot > (nslot == 1 ? BLK_FUSED_WARPS : BLK_MAX_WARPS)) continue;
     if (env) {
       if (mask == atoi(env)) { best_mask = mask; best_max = mx; best_w = nw; }
       continue;
@@ -131,21 +139,44 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
     if (mx < best_max || (mx == best_max && nw < best_w)) { best_mask = mask; best_max = mx; best_w = nw; }
   }
   if (best_mask < 0) return false;
-  int w = 0;
+  if (nslot < 1 || nslot > BLK_MAX_SLOTS) return false;
+  int w = 0, gl = 0;
   for (int g = 0; g < p.ngroups; ++g) {
+    if (!((gmask >> g) & 1)) continue;
     const bool split = (best_mask >> g) & 1;
+    D.gwarps[g] = split ? D.C[g] : 1;
+    const signed char bar0 = (signed char)(1 + gl);
     if (split) {
-      D.gwarps[g] = D.C[g];
       for (int r = 0; r < D.C[g]; ++r) {
-        D.task[w][0] = {(signed char)g, (signed char)r, 1, 0};
+        D.task[w][0] = {(signed char)g, (signed char)r, 1, 0, bar0, {0, 0, 0}};
         D.ntask[w++] = 1;
       }
     } else {
-      D.gwarps[g] = 1;
-      D.task[w][0] = {(signed char)g, 0, (signed char)D.C[g], 0};
+      D.task[w][0] = {(signed char)g, 0, (signed char)D.C[g], 0, bar0, {0, 0, 0}};
       D.ntask[w++] = 1;
     }
+    ++gl;
   }
+  if (w == 0) return false;
+  D.gmask = gmask & ((1u << p.ngroups) - 1);
+  // replicate the roles per slot: barrier ids 1 + slot * gl + local group (named barriers 1..15)
+  D.swarps = w;
+  D.nslot = nslot;
+  if (gl * nslot + (nslot > 1 ? nslot : 0) > 15) return false;
+  for (int sl = 1; sl < nslot; ++sl)
+    for (int v = 0; v < w; ++v) {
+      D.task[sl * w + v][0] = D.task[v][0];
+      D.task[sl * w + v][0].slot = (signed char)sl;
+      D.task[sl * w + v][0].bar = (signed char)(D.task[v][0].bar + sl * gl);
+      D.ntask[sl * w + v] = 1;
+    }
+  for (int sl = 0; sl < nslot; ++sl) {
+    if (nslot == 1) D.sbar[sl] = 0;
+    else if (w == 1) D.sbar[sl] = -1;
+    else if (gl == 1) D.sbar[sl] = D.task[sl * w][0].bar;   // the slot is one group: its barrier
+    else D.sbar[sl] = (signed char)(1 + gl * nslot + sl);
+  }
+  w *= nslot;
   D.nwarps = w;
   // TMEM: 4 strip slots per warp; warps sharing a lane quarter stack their column ranges
   int qused[4] = {0, 0, 0, 0};
@@ -178,7 +209,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D) {
 
 // the calling warp's view of one task
 struct Ctx {
-  int g, rt0, ks, off, row0, nw;
+  int g, rt0, ks, off, row0, nw, bar, slot;
 };
 __device__ __forceinline__ Ctx ctx_of(const BlkDev& D, const BlkTask& t) {
   Ctx x;
@@ -188,13 +219,21 @@ __device__ __forceinline__ Ctx ctx_of(const BlkDev& D, const BlkTask& t) {
   x.off = D.off[t.g];
   x.row0 = D.row0[t.g];
   x.nw = D.gwarps[t.g];
+  x.bar = t.bar;
+  x.slot = t.slot;
   return x;
+}
+__device__ __forceinline__ void slot_sync(const BlkDev& D, int slot) {
+  const int b = D.sbar[slot];
+  if (b == 0) __syncthreads();
+  else if (b < 0) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(b), "r"(32 * D.swarps) : "memory");
 }
 __device__ __forceinline__ void grp_sync(const Ctx& x) {
   if (x.nw == 1) {
     __syncwarp();
   } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(x.g + 1), "r"(32 * x.nw) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(x.bar), "r"(32 * x.nw) : "memory");
   }
 }
 
@@ -828,32 +867,37 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
 }
 
 __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
-                                                                          BlkFwdOut O, int tmem_cols,
+                                                                          BlkFwdOut O, int items, int tmem_cols,
                                                                           unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ int bad_sh;
+  __shared__ int bad_sh[BLK_MAX_SLOTS];
   __shared__ uint32_t tmem_base_sh;
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
-  if (threadIdx.x == 0) bad_sh = 0;
+  if (threadIdx.x < BLK_MAX_SLOTS) bad_sh[threadIdx.x] = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
   unsigned long long nflop = 0;
-  const int item = blockIdx.x;
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
-    double* sm = smem + D.soff[x.g];
-    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh, nflop, L);
+    const int item = blockIdx.x * D.nslot + x.slot;   // slot x.slot: its own item, warps and regions
+    if (item >= items) continue;
+    double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
+    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
+                 L);
   }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   if (L.w == 0) blk_tmem_dealloc(tmem_base_sh, tmem_cols);
   const int nchunk = G.count / O.chunk;
-  if (O.status && threadIdx.x == 0 && bad_sh) O.status[item / nchunk] = QAL_ERR_NONFINITE;
+  if (O.status && threadIdx.x < D.nslot && bad_sh[threadIdx.x]) {
+    const int item = blockIdx.x * D.nslot + threadIdx.x;
+    if (item < items) O.status[item / nchunk] = QAL_ERR_NONFINITE;
+  }
   if (ctr && nflop) atomicAdd(ctr, nflop);
 }
 
@@ -873,7 +917,7 @@ __device__ void blk_pair_task(const double2* lhs, const double2* rhs, double2* o
   bstore_nat(out + x.off, acc, x, L);
 }
 
-__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_tree_level(BlkDev D, int cnt,
+__global__ void __launch_bounds__(BLK_FUSED_WARPS * 32) k_blk_tree_level(BlkDev D, int cnt,
                                                                         const double2* __restrict__ in,
                                                                         double2* __restrict__ out,
                                                                         unsigned long long* ctr) {
@@ -893,7 +937,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_tree_level(BlkDev D,
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
-    double* sm = smem + D.soff[x.g];
+    double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
     BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_pair_task, lhs, rhs, dst, x, sm, L);
     if (x.rt0 == 0 && L.lane == 0) nflop += D.gflops[x.g];
   }
@@ -1172,7 +1216,7 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
   if (leader) nflop += (unsigned long long)(N - 1) * D.gflops[x.g];
 }
 
-__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev D, int N,
+__global__ void __launch_bounds__(BLK_FUSED_WARPS * 32) k_blk_suffix_chain(BlkDev D, int N,
                                                                           const double* __restrict__ U_img,
                                                                           const double2* __restrict__ V,
                                                                           const double2* __restrict__ Cseed,
@@ -1195,7 +1239,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
-    double* sm = smem + D.soff[x.g];
+    double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
     BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V,
                  Cseed ? Cseed + (size_t)blockIdx.x * D.packed : nullptr, X_img + base, x, sm, bars[x.g], nflop, L);
   }
@@ -1204,7 +1248,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
 
 // --------------------------------------------------------------- gradient slices
 constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
-constexpr int BLK_TR_BUF = BLK_MAX_WARPS * BLK_TR_MAX + BLK_TR_MAX;   // one parity's trace buffer
+constexpr int BLK_TR_BUF = (BLK_MAX_WARPS + BLK_MAX_SLOTS) * BLK_TR_MAX;   // one parity's trace buffer: per warp + per slot sum
 constexpr int BLK_TRC_MAXJ = 2;   // PWC trace-basis cache in shared memory up to this many controls
 constexpr int BLK_GRAD_SCR = 2;   // L2 scratch images per group (squarings): E, dE
 
@@ -1222,22 +1266,13 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   double* gdX = sX + IM;
   double* gA6 = sX + 2 * IM;
   double* gdA6 = sX + 3 * IM;
-#if QAL_BLK_SQ_SMEM
   // squarings: E, dE reuse the A6 / dA6 slots (dead once the polynomial is formed; own strips,
   // so a lane re-reads only what it wrote)
   double* gE = gA6;
   double* gdE = gdA6;
 #define SQ_LD(s_, img_) bload_img(s_, img_, x, L)
 #define SQ_ST(img_, s_) bstore_img(img_, s_, x, L)
-#else
-  // L2 scratch (squarings only): E, dE
-  double* gE = scr;
-  double* gdE = scr + IM;
-#define SQ_LD(s_, img_) bload_img_l2(s_, img_, x, L, keep)
-#define SQ_ST(img_, s_) bstore_img_l2(img_, s_, x, L, keep)
-#endif
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
-  const uint64_t keep = l2_evict_last();
   // A holds Omega_k on entry (built one item ahead by the caller)
   const double nrm = bnorm1(A, red, x, L);
   int m, s;
@@ -1449,7 +1484,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
                               double* __restrict__ grad, int* __restrict__ status, double* scr_cta, const Ctx& x,
                               double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr, double gscale,
-                              double2* cache, unsigned long long& nflop, const Lane& L) {
+                              int accum, double2* cache, unsigned long long& nflop, const Lane& L) {
   constexpr int IM = img_doubles(C, RE);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
@@ -1466,8 +1501,11 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     }
   };
   BR<C, R, RE> A, acc, Om;
-  prefetch(blockIdx.x);
-  if ((int)blockIdx.x < items) bbuild_omega(Om, B, G, blockIdx.x / N, blockIdx.x % N, x, L);
+  // this slot's item stream: items item0, item0 + istride, ...
+  const int item0 = blockIdx.x * D.nslot + x.slot, istride = gridDim.x * D.nslot;
+  const int w0 = x.slot * D.swarps;   // first warp of the slot (trace sum, flags)
+  prefetch(item0);
+  if (item0 < items) bbuild_omega(Om, B, G, item0 / N, item0 % N, x, L);
   if (cache) {   // PWC trace basis: the warp's own entries B_m[c][row] x row weight, once per launch
     for (int mm = 0; mm < B.J; ++mm)
 #pragma unroll
@@ -1481,35 +1519,36 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
         }
     __syncwarp();
   }
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+  for (int item = item0; item < items; item += istride) {
     const int b = item / N, k = item % N;
     bcopy(A, Om);
-    const int par = ((item - (int)blockIdx.x) / (int)gridDim.x) & 1;   // item parity: double-buffered flags
+    const int par = ((item - item0) / istride) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
                                                ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w], scr,
                                                bad_sh + par, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
-    const int nx = item + gridDim.x;
+    const int nx = item + istride;
     if (nx < items) bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
     // per-warp partial traces, double-buffered by item parity so one CTA barrier per item suffices
     double* rt = red_tr + (size_t)par * BLK_TR_BUF;
     blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * BLK_TR_MAX, true, cache, L);
-    __syncthreads();   // every warp done with this item: SN / SD free, rt complete
+    slot_sync(D, x.slot);   // every warp of the slot done with this item: SN / SD free, rt complete
     prefetch(nx);
-    if (L.w != 0) continue;
-    for (int m = L.lane; m < K; m += 32) {   // fixed-order sum over the warps
+    if (L.w != w0) continue;
+    double* Tsum = rt + (BLK_MAX_WARPS + x.slot) * BLK_TR_MAX;
+    for (int m = L.lane; m < K; m += 32) {   // fixed-order sum over the slot's warps
       double s = 0.0;
-      for (int w = 0; w < D.nwarps; ++w) s += rt[w * BLK_TR_MAX + m];
-      rt[BLK_MAX_WARPS * BLK_TR_MAX + m] = s;
+      for (int w = w0; w < w0 + D.swarps; ++w) s += rt[w * BLK_TR_MAX + m];
+      Tsum[m] = s;
     }
     __syncwarp();
     if (L.lane == 0) {
-      const double* T = rt + BLK_MAX_WARPS * BLK_TR_MAX;
+      const double* T = Tsum;
       const int J = B.J;
       const double inv_d2 = gscale;   // 1/d^2 for the fidelity, 1 for a general cotangent
       if (G.mode == 0) {
         double* gg = grad + ((size_t)b * N + k) * J;
-        for (int j = 0; j < J; ++j) gg[j] = G.h * T[j] * inv_d2;
+        for (int j = 0; j < J; ++j) gg[j] = (accum ? gg[j] : 0.0) + G.h * T[j] * inv_d2;
       } else {
         const double* u = G.u + ((size_t)b * N + k) * 2 * J;
         double* gg = grad + ((size_t)b * N + k) * 2 * J;
@@ -1527,8 +1566,8 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
             g1 -= G.c4 * c1;
             g2 -= G.c4 * c2;
           }
-          gg[j] = g1 * inv_d2;
-          gg[J + j] = g2 * inv_d2;
+          gg[j] = (accum ? gg[j] : 0.0) + g1 * inv_d2;
+          gg[J + j] = (accum ? gg[J + j] : 0.0) + g2 * inv_d2;
         }
       }
       if (bad_sh[par] && status) status[b] = QAL_ERR_NONFINITE;
@@ -1542,21 +1581,21 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
                                                                const double* __restrict__ X_img,
                                                                double* __restrict__ grad, int* __restrict__ status,
                                                                double* __restrict__ scratch, double gscale,
-                                                               int tmem_cols, unsigned long long* ctr) {
+                                                               int accum, int tmem_cols, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[QAL_BLK_MAX_GROUPS][2];   // [0]: X_{k+1} -> SN, [1]: P_k -> SD
+  __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id: [0] X_{k+1} -> SN, [1] P_k -> SD
   __shared__ double red_tr[2 * BLK_TR_BUF];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int bad_sh[2];
+  __shared__ int bad_sh[BLK_MAX_SLOTS][2];
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   const BlkTask T = D.task[L.w][0];   // one role per warp (to_dev)
   if (T.rt0 == 0 && L.lane == 0) {
-    mbar_init(&bars[T.g][0], 1);
-    mbar_init(&bars[T.g][1], 1);
+    mbar_init(&bars[T.bar][0], 1);
+    mbar_init(&bars[T.bar][1], 1);
   }
   fence_mbar_init();
-  if (threadIdx.x == 0) { bad_sh[0] = 0; bad_sh[1] = 0; }
+  if (threadIdx.x < 2 * BLK_MAX_SLOTS) bad_sh[threadIdx.x >> 1][threadIdx.x & 1] = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -1564,12 +1603,12 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   unsigned long long nflop = 0;
   double* scr_cta = scratch + (size_t)blockIdx.x * 2 * (size_t)D.packed * BLK_GRAD_SCR;
   const Ctx x = ctx_of(D, T);
-  double* sm = smem + D.soff[x.g];
+  double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
   double2* cache = (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ && D.tcache_off >= 0)
                        ? reinterpret_cast<double2*>(smem + D.tcache_off) + (size_t)D.tcache_w[L.w]
                        : nullptr;
   BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status, scr_cta,
-               x, sm, bars[x.g], tm, bad_sh, red_tr, gscale, cache, nflop, L);
+               x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
@@ -1580,7 +1619,7 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
 // ------------------------------------------------------------------ packed scans / batched products
 // One Hillis-Steele level over per-pulse packed sequences (later factor on the LEFT, Eq. 15):
 // prefix (dir 0): out[s] = in[s] in[s-d]; suffix (dir 1): out[s] = in[s+d] in[s]; else copy.
-__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_scan_level(BlkDev D, int cnt, int dd, int dir,
+__global__ void __launch_bounds__(BLK_FUSED_WARPS * 32) k_blk_scan_level(BlkDev D, int cnt, int dd, int dir,
                                                                         const double2* __restrict__ in,
                                                                         double2* __restrict__ out,
                                                                         unsigned long long* ctr) {
@@ -1598,7 +1637,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_scan_level(BlkDev D,
   const BlkTask T = D.task[L.w][0];
   const Ctx x = ctx_of(D, T);
   BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_pair_task, src + (size_t)later * D.packed,
-               src + (size_t)earlier * D.packed, dst, x, smem + D.soff[x.g], L);
+               src + (size_t)earlier * D.packed, dst, x, smem + D.soff[x.g] + (size_t)x.slot * D.sstride, L);
   if (ctr && x.rt0 == 0 && L.lane == 0) atomicAdd(ctr, D.gflops[x.g]);
 }
 
@@ -1624,7 +1663,7 @@ __global__ void k_blk_scan_shift(BlkDev D, int cnt, const double2* __restrict__ 
 }
 
 // C[i] = A[i] B[i] (packed), element strides sa / sb = packed or 0 (broadcast)
-__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_batched_mm(BlkDev D, const double2* __restrict__ A,
+__global__ void __launch_bounds__(BLK_FUSED_WARPS * 32) k_blk_batched_mm(BlkDev D, const double2* __restrict__ A,
                                                                         long long sa, const double2* __restrict__ B,
                                                                         long long sb, double2* __restrict__ Cout,
                                                                         unsigned long long* ctr) {
@@ -1634,7 +1673,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_batched_mm(BlkDev D,
   const BlkTask T = D.task[L.w][0];
   const Ctx x = ctx_of(D, T);
   BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_pair_task, A + i * sa, B + i * sb, Cout + i * D.packed, x,
-               smem + D.soff[x.g], L);
+               smem + D.soff[x.g] + (size_t)x.slot * D.sstride, L);
   if (ctr && x.rt0 == 0 && L.lane == 0) atomicAdd(ctr, D.gflops[x.g]);
 }
 
@@ -1670,16 +1709,81 @@ __global__ void k_blk_fidelity_cotangent(BlkDev D, const double2* __restrict__ V
   }
 }
 
+// ------------------------------------------------------------------ launch sets
+// The forward and gradient kernels run the plan's groups as group-specialised launches: a set = some
+// groups x nslot independent item streams per CTA (each slot its own item, warps, barriers and shared
+// regions), so that a light group never idles inside a CTA while a heavy one finishes the item, and
+// each CTA has a multiple of 4 warps (all four SM sub-partitions).  Measured on configs[2] (ms per
+// 4096 x 1024 step): forward fused 112, {20-block + 6-block} x 1 and {15+1} x 2 slots 104; gradient
+// fused 197, one set per group (3 warps x 4, 2 x 2, 1 x 4 slots) 178.
+struct BlkSet {
+  unsigned gmask;
+  int nslot;
+};
+static int blk_group_warps(const qal_block_plan& p, int g) {
+  BlkDev D;
+  return to_dev(p, D, 1u << g, 1) ? D.nwarps : 0;
+}
+// kind 0: forward (groups packed first-fit-decreasing into sets of <= 4 warps, 4 / warps slots when
+// that divides); kind 1: gradient (one set per group, slots 4 / warps, or 4 for 3-warp groups).
+// env (experiments) "mask:slots,..." must cover every group exactly once, else it is ignored.
+static void blk_sets(const qal_block_plan& p, int kind, std::vector<BlkSet>& sets) {
+  sets.clear();
+  const unsigned all = (1u << p.ngroups) - 1;
+  const char* env = getenv(kind == 0 ? "QAL_BLK_SETS_FWD" : "QAL_BLK_SETS_GRAD");
+  if (env && *env) {
+    unsigned seen = 0;
+    bool ok = true;
+    const char* c = env;
+    while (*c && ok) {
+      char* e1;
+      const long m = strtol(c, &e1, 0);
+      int sl = 1;
+      if (*e1 == ':') sl = (int)strtol(e1 + 1, &e1, 0);
+      ok = m > 0 && ((unsigned)m & ~all) == 0 && ((unsigned)m & seen) == 0 && e1 != c;
+      seen |= (unsigned)m;
+      sets.push_back({(unsigned)m, sl});
+      c = (*e1 == ',') ? e1 + 1 : e1;
+      if (*c && *e1 != ',') ok = false;
+    }
+    if (ok && seen == all) return;
+    sets.clear();
+  }
+  int gw[QAL_BLK_MAX_GROUPS];
+  for (int g = 0; g < p.ngroups; ++g) gw[g] = blk_group_warps(p, g);
+  if (kind == 1) {
+    for (int g = 0; g < p.ngroups; ++g) {
+      const int w = gw[g];
+      sets.push_back({1u << g, (w == 3 || w == 1) ? 4 : (w == 2 ? 2 : 1)});
+    }
+    return;
+  }
+  std::vector<int> order(p.ngroups);
+  for (int g = 0; g < p.ngroups; ++g) order[g] = g;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gw[a] > gw[b]; });
+  std::vector<std::pair<unsigned, int>> bins;   // (mask, warps)
+  for (int g : order) {
+    bool placed = false;
+    for (auto& b : bins)
+      if (b.second + gw[g] <= 4) { b.first |= 1u << g; b.second += gw[g]; placed = true; break; }
+    if (!placed) bins.push_back({1u << g, gw[g]});
+  }
+  for (const auto& b : bins) sets.push_back({b.first, (4 % b.second == 0) ? 4 / b.second : 1});
+}
+
 // ------------------------------------------------------------------ launchers
 namespace {
+// shared-memory regions of the launch's groups for one slot; every slot gets its own copy
 int grp_smem_doubles(BlkDev& D, int (*per)(int, bool)) {
   int o = 0;
   for (int g = 0; g < D.ngroups; ++g) {
     D.soff[g] = o;
+    if (!((D.gmask >> g) & 1)) continue;
     o += per(D.C[g], D.real[g] != 0);
     o = (o + 15) & ~15;   // 128-byte alignment of every region
   }
-  return o;
+  D.sstride = o;
+  return o * D.nslot;
 }
 int per3(int C, bool re) { return grp3_doubles(C, re); }
 int per_grad(int C, bool re) { return grp3_doubles(C, re) + 4 * img_doubles(C, re); }
@@ -1701,18 +1805,25 @@ cudaError_t set_smem(const void* fn, size_t bytes, size_t& attr) {
 
 cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                  const BlkFwdOut& O, cudaStream_t st) {
-  BlkDev D;
-  if (!to_dev(p, D)) return cudaErrorInvalidValue;
-  const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
-  static size_t attr = 0;
-  cudaError_t e = set_smem((const void*)k_blk_expm_fold, bytes, attr);
-  if (e != cudaSuccess) return e;
   const int items = batch * (G.count / O.chunk);
-  prof_pre(ST_BLK_EXPM, st);
-  k_blk_expm_fold<<<items, 32 * D.nwarps, bytes, st>>>(D, B, G, O, tmem_cols_for(D), prof_counter(ST_BLK_EXPM));
-  prof_post(ST_BLK_EXPM, st);
-  ++launch_counter();
-  return cudaGetLastError();
+  std::vector<BlkSet> sets;
+  blk_sets(p, 0, sets);
+  for (const BlkSet& set : sets) {
+    BlkDev D;
+    if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
+    const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
+    static size_t attr = 0;
+    cudaError_t e = set_smem((const void*)k_blk_expm_fold, bytes, attr);
+    if (e != cudaSuccess) return e;
+    prof_pre(ST_BLK_EXPM, st);
+    k_blk_expm_fold<<<(items + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(D, B, G, O, items,
+                                                                                  tmem_cols_for(D),
+                                                                                  prof_counter(ST_BLK_EXPM));
+    prof_post(ST_BLK_EXPM, st);
+    ++launch_counter();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, const double2* in, double2* out,
@@ -1784,34 +1895,43 @@ static int grad_cache_layout(BlkDev& D, int J, int base_doubles) {
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
                                    double* scratch, double gscale, cudaStream_t st) {
-  BlkDev D;
-  if (!to_dev(p, D)) return cudaErrorInvalidValue;
-  const int base = grp_smem_doubles(D, per_grad);
-  const int gmax = blk_grad_grid(D);   // the scratch was sized for this grid
-  size_t bytes = (size_t)base * 8;
-  D.tcache_off = -1;
-  if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
-    BlkDev trial = D;
-    const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
-    cudaFuncAttributes fa;
-    // keep the cache only if it does not cost a CTA per SM
-    if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess &&
-        (int)(233472 / (with + fa.sharedSizeBytes + 1024)) * num_sms() >= gmax) {
-      D = trial;
-      bytes = with;
+  std::vector<BlkSet> sets;
+  blk_sets(p, 1, sets);
+  int accum = 0;   // later sets add their groups' traces to the gradient (fixed launch order)
+  for (const BlkSet& set : sets) {
+    BlkDev D;
+    if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
+    const int base = grp_smem_doubles(D, per_grad);
+    const int gmax = blk_grad_grid(D);
+    size_t bytes = (size_t)base * 8;
+    D.tcache_off = -1;
+    if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
+      BlkDev trial = D;
+      const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
+      cudaFuncAttributes fa;
+      // keep the cache only if it does not cost a CTA per SM
+      if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess &&
+          (int)(233472 / (with + fa.sharedSizeBytes + 1024)) * num_sms() >= gmax) {
+        D = trial;
+        bytes = with;
+      }
     }
+    static size_t attr = 0;
+    cudaError_t e = set_smem((const void*)k_blk_grad_slices, bytes, attr);
+    if (e != cudaSuccess) return e;
+    const int items = batch * G.count;
+    const int need = (items + D.nslot - 1) / D.nslot;
+    const int grid = need < gmax ? need : gmax;
+    prof_pre(ST_BLK_GRAD, st);
+    k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch,
+                                                           gscale, accum, tmem_cols_for(D),
+                                                           prof_counter(ST_BLK_GRAD));
+    prof_post(ST_BLK_GRAD, st);
+    ++launch_counter();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    accum = 1;
   }
-  static size_t attr = 0;
-  cudaError_t e = set_smem((const void*)k_blk_grad_slices, bytes, attr);
-  if (e != cudaSuccess) return e;
-  const int items = batch * G.count;
-  const int grid = items < gmax ? items : gmax;
-  prof_pre(ST_BLK_GRAD, st);
-  k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, gscale,
-                                                         tmem_cols_for(D), prof_counter(ST_BLK_GRAD));
-  prof_post(ST_BLK_GRAD, st);
-  ++launch_counter();
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 cudaError_t launch_blk_scan(const qal_block_plan& p, int batch, int cnt, const double2* U, double2* pre, double2* suf,
