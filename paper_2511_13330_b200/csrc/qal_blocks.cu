@@ -59,6 +59,18 @@ constexpr int BLK_MAX_TASKS = 3;
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
 #endif
+// register caps of the role-specialised forward / gradient kernels (by the role's column tiles C)
+#ifndef QAL_BLK_MAXNREG_C1
+#define QAL_BLK_MAXNREG_C1 168
+#endif
+#ifndef QAL_BLK_MAXNREG_C2
+#define QAL_BLK_MAXNREG_C2 168
+#endif
+#ifndef QAL_BLK_MAXNREG_C3
+#define QAL_BLK_MAXNREG_C3 168
+#endif
+#define BLK_ROLE_MAXNREG(FC) \
+  ((FC) == 1 ? QAL_BLK_MAXNREG_C1 : (FC) == 2 ? QAL_BLK_MAXNREG_C2 : (FC) == 3 ? QAL_BLK_MAXNREG_C3 : QAL_BLK_MAXNREG)
 
 // ------------------------------------------------------------------ device plan
 struct BlkTask {
@@ -866,7 +878,8 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   if (O.chunk_nat) bstore_nat(O.chunk_nat + ((size_t)b * nchunk + c) * D.packed + x.off, A, x, L);
 }
 
-__global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
+template <int FC, int FR, int FKS, int FRE>   // as k_blk_grad_slices: FC == 0 any roles
+__global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
                                                                           BlkFwdOut O, int items, int tmem_cols,
                                                                           unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
@@ -886,8 +899,11 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_expm_fold(BlkDev D, BlkBasis 
     const int item = blockIdx.x * D.nslot + x.slot;   // slot x.slot: its own item, warps and regions
     if (item >= items) continue;
     double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
-    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
-                 L);
+    if constexpr (FC == 0)
+      BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
+                   nflop, L);
+    else
+      blk_fwd_task<FC, FR, FKS, FRE != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop, L);
   }
   tmem_fence_before();
   __syncthreads();
@@ -1578,7 +1594,10 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   }
 }
 
-__global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B, SliceGrid G,
+// FC == 0: any mix of roles (runtime dispatch); else every warp runs role <FC, FR, FKS, FRE> and the
+// kernel is compiled for that role alone (its own register count: a light role gets more warps per SM)
+template <int FC, int FR, int FKS, int FRE>
+__global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B, SliceGrid G,
                                                                const double* __restrict__ P_img,
                                                                const double* __restrict__ X_img,
                                                                double* __restrict__ grad, int* __restrict__ status,
@@ -1609,8 +1628,12 @@ __global__ void __maxnreg__(QAL_BLK_MAXNREG) k_blk_grad_slices(BlkDev D, int bat
   double2* cache = (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ && D.tcache_off >= 0)
                        ? reinterpret_cast<double2*>(smem + D.tcache_off) + (size_t)D.tcache_w[L.w]
                        : nullptr;
-  BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status, scr_cta,
-               x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
+  if constexpr (FC == 0)
+    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status,
+                 scr_cta, x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
+  else
+    blk_grad_loop<FC, FR, FKS, FRE != 0>(D, batch, B, G, P_img, X_img, grad, status, scr_cta, x, sm, bars[x.bar], tm,
+                                          bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
@@ -1714,10 +1737,10 @@ __global__ void k_blk_fidelity_cotangent(BlkDev D, const double2* __restrict__ V
 // ------------------------------------------------------------------ launch sets
 // The forward and gradient kernels run the plan's groups as group-specialised launches: a set = some
 // groups x nslot independent item streams per CTA (each slot its own item, warps, barriers and shared
-// regions), so that a light group never idles inside a CTA while a heavy one finishes the item, and
-// each CTA has a multiple of 4 warps (all four SM sub-partitions).  Measured on configs[2] (ms per
-// 4096 x 1024 step): forward fused 112, {20-block + 6-block} x 1 and {15+1} x 2 slots 104; gradient
-// fused 197, one set per group (3 warps x 4, 2 x 2, 1 x 4 slots) 178.
+// regions), so that a light group never idles inside a CTA while a heavy one finishes the item, every
+// CTA has a multiple of 4 warps (all four SM sub-partitions), and a one-role launch runs the kernel
+// compiled for that role alone (below).  Measured on configs[2] (ms per 4096 x 1024 step): forward
+// 112 fused -> 96 per group; gradient 197 fused -> 176 per group; the suffix chain stays fused (17.5).
 struct BlkSet {
   unsigned gmask;
   int nslot;
@@ -1726,10 +1749,9 @@ static int blk_group_warps(const qal_block_plan& p, int g) {
   BlkDev D;
   return to_dev(p, D, 1u << g, 1) ? D.nwarps : 0;
 }
-// kind 0: forward (groups packed first-fit-decreasing into sets of <= 4 warps, 4 / warps slots when
-// that divides); kind 1 gradient (one set per group, slots 4 / warps, or 4 for 3-warp groups); kind 2
-// suffix chain (one CTA per pulse, all groups).
-// env (experiments) "mask:slots,..." must cover every group exactly once, else it is ignored.
+// kind 0 forward, 1 gradient: one set per group, slots 4 / warps (4 for 3-warp groups); kind 2 suffix
+// chain: one CTA per pulse, all groups.  env (experiments) QAL_BLK_SETS_FWD / _GRAD / _CHAIN =
+// "mask:slots,..." must cover every group exactly once, else it is ignored.
 static void blk_sets(const qal_block_plan& p, int kind, std::vector<BlkSet>& sets) {
   sets.clear();
   const unsigned all = (1u << p.ngroups) - 1;
@@ -1752,30 +1774,74 @@ static void blk_sets(const qal_block_plan& p, int kind, std::vector<BlkSet>& set
     if (ok && seen == all) return;
     sets.clear();
   }
-  if (kind == 2) {   // suffix chain: all groups in one CTA per pulse (measured best: 17.7 ms vs 20.1 split)
+  if (kind == 2) {
     sets.push_back({all, 1});
     return;
   }
-  int gw[QAL_BLK_MAX_GROUPS];
-  for (int g = 0; g < p.ngroups; ++g) gw[g] = blk_group_warps(p, g);
-  if (kind == 1) {   // gradient
-    for (int g = 0; g < p.ngroups; ++g) {
-      const int w = gw[g];
-      sets.push_back({1u << g, (w == 3 || w == 1) ? 4 : (w == 2 ? 2 : 1)});
+  for (int g = 0; g < p.ngroups; ++g) {
+    const int w = blk_group_warps(p, g);
+    sets.push_back({1u << g, (w == 3 || w == 1) ? 4 : (w == 2 ? 2 : 1)});
+  }
+}
+
+// ------------------------------------------------------------------ role-specialised kernels
+// The d = 8 roles (mirror plan): the real 20-block on 3 warps (3, 1, 5, real), the 15+1 block on 2
+// warps (2, 1, 4), the 6-block on one warp (1, 1, 2).  A launch whose warps all run one of them uses
+// the kernel compiled for it alone; anything else the dispatching kernel.  QAL_BLK_SPEC=0: always the
+// dispatching kernel (experiments).
+static int blk_role(const BlkDev& D) {
+  const char* env = getenv("QAL_BLK_SPEC");
+  if (env && env[0] == '0') return 0;
+  int key = -1;
+  for (int w = 0; w < D.nwarps; ++w) {
+    if (D.ntask[w] != 1) return 0;
+    const BlkTask& t = D.task[w][0];
+    const int C = D.C[t.g], ks = D.ks[t.g];
+    const int KS = C == 3 ? (ks <= 5 ? 5 : 6) : (C == 2 ? 4 : 2);
+    const int k = ((C * 4 + t.R) * 8 + KS) * 2 + (D.real[t.g] ? 1 : 0);
+    if (key >= 0 && k != key) return 0;
+    key = k;
+  }
+  if (key == ((3 * 4 + 1) * 8 + 5) * 2 + 1) return 1;
+  if (key == ((2 * 4 + 1) * 8 + 4) * 2 + 0) return 2;
+  if (key == ((1 * 4 + 1) * 8 + 2) * 2 + 0) return 3;
+  return 0;
+}
+using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, const double*, double*, int*, double*,
+                            double, int, int, unsigned long long*);
+using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*);
+static GradKernel grad_kernel(const BlkDev& D) {
+  switch (blk_role(D)) {
+    case 1: return k_blk_grad_slices<3, 1, 5, 1>;
+    case 2: return k_blk_grad_slices<2, 1, 4, 0>;
+    case 3: return k_blk_grad_slices<1, 1, 2, 0>;
+    default: return k_blk_grad_slices<0, 0, 0, 0>;
+  }
+}
+static FwdKernel fwd_kernel(const BlkDev& D) {
+  switch (blk_role(D)) {
+    case 1: return k_blk_expm_fold<3, 1, 5, 1>;
+    case 2: return k_blk_expm_fold<2, 1, 4, 0>;
+    case 3: return k_blk_expm_fold<1, 1, 2, 0>;
+    default: return k_blk_expm_fold<0, 0, 0, 0>;
+  }
+}
+// dynamic shared-memory opt-in per kernel function (several kernels share one launcher)
+static cudaError_t set_smem_fn(const void* fn, size_t bytes) {
+  static std::vector<std::pair<const void*, size_t>> done;
+  for (auto& d : done)
+    if (d.first == fn) {
+      if (bytes <= d.second) return cudaSuccess;
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e == cudaSuccess) d.second = bytes;
+      return e;
     }
-    return;
-  }
-  std::vector<int> order(p.ngroups);
-  for (int g = 0; g < p.ngroups; ++g) order[g] = g;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gw[a] > gw[b]; });
-  std::vector<std::pair<unsigned, int>> bins;   // (mask, warps)
-  for (int g : order) {
-    bool placed = false;
-    for (auto& b : bins)
-      if (b.second + gw[g] <= 4) { b.first |= 1u << g; b.second += gw[g]; placed = true; break; }
-    if (!placed) bins.push_back({1u << g, gw[g]});
-  }
-  for (const auto& b : bins) sets.push_back({b.first, (4 % b.second == 0) ? 4 / b.second : 1});
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  done.push_back({fn, bytes});
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------------------ launchers
@@ -1819,13 +1885,12 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
     BlkDev D;
     if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
     const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
-    static size_t attr = 0;
-    cudaError_t e = set_smem((const void*)k_blk_expm_fold, bytes, attr);
+    const FwdKernel fn = fwd_kernel(D);
+    cudaError_t e = set_smem_fn((const void*)fn, bytes);
     if (e != cudaSuccess) return e;
     prof_pre(ST_BLK_EXPM, st);
-    k_blk_expm_fold<<<(items + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(D, B, G, O, items,
-                                                                                  tmem_cols_for(D),
-                                                                                  prof_counter(ST_BLK_EXPM));
+    fn<<<(items + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(D, B, G, O, items, tmem_cols_for(D),
+                                                                     prof_counter(ST_BLK_EXPM));
     prof_post(ST_BLK_EXPM, st);
     ++launch_counter();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1870,18 +1935,19 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
 // persistent grid of the gradient kernel: exactly the CTAs that are co-resident (registers,
 // shared memory, and TMEM: 512 columns per SM); a CTA beyond that would start only when one
 // finished and double the tail
-static int blk_grad_grid(const BlkDev& D) {
+static int blk_grad_grid(const BlkDev& D, GradKernel fn = nullptr) {
   BlkDev tmp = D;
   const size_t bytes = (size_t)grp_smem_doubles(tmp, per_grad) * 8;
+  if (!fn) fn = grad_kernel(D);
   cudaFuncAttributes fa;
   int per_sm = 1;
-  if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess && fa.numRegs > 0) {
+  if (cudaFuncGetAttributes(&fa, (const void*)fn) == cudaSuccess && fa.numRegs > 0) {
     // registers (64K per SM, per-warp allocation rounded to 256), shared memory (233 KB config,
     // 1 KB reserved per CTA), named barriers (64 per SM, 16 per CTA), TMEM (512 columns)
     const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
     const int by_regs = 65536 / (regs_warp * D.nwarps);
     const int by_smem = (int)(233472 / (bytes + fa.sharedSizeBytes + 1024));
-    per_sm = std::min(std::min(by_regs, by_smem), std::min(4, 512 / tmem_cols_for(D)));
+    per_sm = std::min(std::min(by_regs, by_smem), std::min(8, 512 / tmem_cols_for(D)));
   }
   if (getenv("QAL_DEBUG")) fprintf(stderr, "blk_grad_grid: nwarps %d smem %zu per_sm %d\n", D.nwarps, bytes, per_sm);
   return std::max(1, per_sm) * num_sms();
@@ -1915,7 +1981,8 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
     BlkDev D;
     if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
     const int base = grp_smem_doubles(D, per_grad);
-    const int gmax = blk_grad_grid(D);
+    const GradKernel fn = grad_kernel(D);
+    const int gmax = blk_grad_grid(D, fn);
     size_t bytes = (size_t)base * 8;
     D.tcache_off = -1;
     if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
@@ -1923,22 +1990,20 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
       const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
       cudaFuncAttributes fa;
       // keep the cache only if it does not cost a CTA per SM
-      if (cudaFuncGetAttributes(&fa, k_blk_grad_slices) == cudaSuccess &&
+      if (cudaFuncGetAttributes(&fa, (const void*)fn) == cudaSuccess &&
           (int)(233472 / (with + fa.sharedSizeBytes + 1024)) * num_sms() >= gmax) {
         D = trial;
         bytes = with;
       }
     }
-    static size_t attr = 0;
-    cudaError_t e = set_smem((const void*)k_blk_grad_slices, bytes, attr);
+    cudaError_t e = set_smem_fn((const void*)fn, bytes);
     if (e != cudaSuccess) return e;
     const int items = batch * G.count;
     const int need = (items + D.nslot - 1) / D.nslot;
     const int grid = need < gmax ? need : gmax;
     prof_pre(ST_BLK_GRAD, st);
-    k_blk_grad_slices<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch,
-                                                           gscale, accum, tmem_cols_for(D),
-                                                           prof_counter(ST_BLK_GRAD));
+    fn<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, gscale, accum,
+                                           tmem_cols_for(D), prof_counter(ST_BLK_GRAD));
     prof_post(ST_BLK_GRAD, st);
     ++launch_counter();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
