@@ -55,6 +55,10 @@ constexpr int BLK_CPLX_MMAS = 4;
 #define QAL_BLK_INTERLEAVE 1
 #endif
 constexpr bool BLK_INTERLEAVE = QAL_BLK_INTERLEAVE != 0;
+#ifndef QAL_BLK_SPLIT_ACC
+#define QAL_BLK_SPLIT_ACC 0
+#endif
+constexpr bool BLK_SPLIT_ACC = QAL_BLK_SPLIT_ACC != 0;
 constexpr int BLK_MAX_TASKS = 3;
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
@@ -474,6 +478,19 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
   const uint32_t base = smem_u32(Bs + L.t * P + L.g);
   double br[2][C], bi[2][C];
   double g3q[R][RE || BLK_CPLX_MMAS == 4 ? 1 : 2 * C];   // Gauss Q accumulator
+  // BLK_SPLIT_ACC: a second accumulator set halves the dependent DMMA chain of every output tile
+  // (real: odd k-steps; complex: the -Ai Bi / Ai Br terms), summed once at the end
+  constexpr bool SPL = BLK_SPLIT_ACC && (RE || BLK_CPLX_MMAS == 4);
+  double s2r[R][SPL ? 2 * C : 1], s2i[R][SPL && !RE ? 2 * C : 1];
+  if constexpr (SPL) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) {
+        s2r[r][i] = 0.0;
+        if constexpr (!RE) s2i[r][i] = 0.0;
+      }
+  }
   if constexpr (!RE && BLK_CPLX_MMAS == 3) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -503,7 +520,13 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if constexpr (RE) {          // real block: 1 MMA per 8x8x4 step
+        if constexpr (RE && SPL) {   // real block, odd k-steps into the second set
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            if (q & 1) dmma(s2r[r][2 * j], s2r[r][2 * j + 1], a.re[r][q], br[cur][j]);
+            else dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], a.re[r][q], br[cur][j]);
+          }
+        } else if constexpr (RE) {          // real block: 1 MMA per 8x8x4 step
 #pragma unroll
           for (int j = 0; j < C; ++j) dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], a.re[r][q], br[cur][j]);
         } else if constexpr (BLK_CPLX_MMAS == 3) {   // Gauss: P = Ar Br, Q = Ai Bi, R = (Ar+Ai)(Br+Bi)
@@ -514,6 +537,15 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
             dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
             dmma(g3q[r][2 * j], g3q[r][2 * j + 1], ai, bi[cur][j]);
             dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], as, bs);
+          }
+        } else if constexpr (SPL) {
+          const double ar = a.re[r][q], ai = a.im[r][q], nai = -a.im[r][q];
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            dmma(acc.re[r][2 * j], acc.re[r][2 * j + 1], ar, br[cur][j]);
+            dmma(acc.im[r][2 * j], acc.im[r][2 * j + 1], ar, bi[cur][j]);
+            dmma(s2r[r][2 * j], s2r[r][2 * j + 1], nai, bi[cur][j]);
+            dmma(s2i[r][2 * j], s2i[r][2 * j + 1], ai, br[cur][j]);
           }
         } else if constexpr (BLK_INTERLEAVE) {
           // two passes over the output tiles: the 2C accumulators of a pass are independent, so
@@ -542,6 +574,15 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
         }
       }
     }
+  }
+  if constexpr (SPL) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) {
+        acc.re[r][i] += s2r[r][i];
+        if constexpr (!RE) acc.im[r][i] += s2i[r][i];
+      }
   }
   if constexpr (!RE && BLK_CPLX_MMAS == 3) {   // Re = P - Q, Im = R - P - Q (P, R carry the old acc)
 #pragma unroll
@@ -1882,8 +1923,11 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
   std::vector<BlkSet> sets;
   blk_sets(p, 0, sets);
   for (const BlkSet& set : sets) {
+    // fewer slots when the items would not fill two CTAs per SM (small batches, one chunk per pulse)
+    int ns = set.nslot;
+    while (ns > 1 && (items + ns - 1) / ns < 2 * num_sms()) ns >>= 1;
     BlkDev D;
-    if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
+    if (!to_dev(p, D, set.gmask, ns)) return cudaErrorInvalidValue;
     const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
     const FwdKernel fn = fwd_kernel(D);
     cudaError_t e = set_smem_fn((const void*)fn, bytes);
