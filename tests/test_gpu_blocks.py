@@ -392,3 +392,32 @@ def test_pulse_batch_reports_a_broken_structure(torch_cuda, qal):
     eng.H0 = eng.H0.contiguous()
     eng.step()
     assert not eng.structure_ok()
+
+
+@pytest.mark.parametrize("mirror", [True, False])
+def test_launch_sets_fused_vs_group_specialised(torch_cuda, qal, monkeypatch, mirror):
+    """The forward / gradient kernels run one launch per group (slots, role-compiled kernels) by
+    default; one fused CTA per item ("all groups : 1 slot") must give the identical forward (the same
+    arithmetic per group) and the same gradient up to the order of the per-group trace sums.  A set
+    list that does not cover every group exactly once is ignored (default sets)."""
+    torch = torch_cuda
+    p = qi.cfg2(batch=40, N=96, T=200.0 * 96 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p, mirror)
+    u, V = dev(torch, p.u), dev(torch, p.V)
+    allg = (1 << plan.ngroups) - 1
+
+    def run(fwd, grad):
+        monkeypatch.setenv("QAL_BLK_SETS_FWD", fwd)
+        monkeypatch.setenv("QAL_BLK_SETS_GRAD", grad)
+        F, g, Lam = qal.qal_block_fidelity_grad(plan, L0p, Lcp, u, p.T, p.N, V, want_Lambda=True)
+        torch.cuda.synchronize()
+        return F.cpu().numpy(), g.cpu().numpy(), Lam.cpu().numpy()
+
+    Fd, gd, Ld = run("", "")
+    Ff, gf, Lf = run(f"{allg}:1", f"{allg}:1")
+    assert np.array_equal(Ld, Lf) and np.array_equal(Fd, Ff)
+    rel = np.linalg.norm((gd - gf).reshape(len(gd), -1), axis=1) / np.linalg.norm(gf.reshape(len(gf), -1), axis=1)
+    assert np.max(rel) <= 1e-13
+    # two slots per set, and an invalid list (group 0 twice) falling back to the default
+    F2, g2, L2 = run(",".join(f"{1 << k}:2" for k in range(plan.ngroups)), f"1:1,1:1,{allg}:1")
+    assert np.array_equal(L2, Ld) and np.array_equal(g2, gd)
