@@ -47,6 +47,14 @@ struct BBPlanRec {   // per block, written on the device
   int m, s, bad, pad;
   double nrm;
 };
+constexpr int BB_PLAN_STRIDE = 64;   // plan records per slice of a batch (>= QAL_BB_MAX_BLOCKS)
+// slices per batch (every launch covers the tiles of a whole batch): as many as ~4 GB of batch
+// workspace holds, at most 64 (configs[4]: 16; the Hubbard blocks: 64)
+inline int bb_sb(const qal_bigblock_plan& p) {
+  const size_t per = 6 * (size_t)p.total_doubles * 8;
+  const size_t n = ((size_t)4 << 30) / std::max<size_t>(per, 1);
+  return (int)std::min<size_t>(64, std::max<size_t>(1, n));
+}
 
 __device__ __forceinline__ int bb_block_of_tile(const BBDev& D, int t) {
   int b = 0;
@@ -127,9 +135,12 @@ __device__ __forceinline__ int bb_row_terms(const BBDev& D, int grow, int* R, do
 
 // ------------------------------------------------------------------ elementwise
 // X = h (L0 + sum_j u_j L_j) gathered into the tiled blocks (a3, PWC)
+// batched over slices: blockIdx.y = slice i of the batch (u row i, X + i * total)
 __global__ void __launch_bounds__(NT) k_bb_omega(BBDev D, const double2* __restrict__ L0,
                                                  const double2* __restrict__ Lc, int J, const double* __restrict__ u,
                                                  double h, double* __restrict__ X) {
+  u += (size_t)blockIdx.y * J;
+  X += (size_t)blockIdx.y * D.total;
   __shared__ double cf[MAXJ + 1];
   if (threadIdx.x <= J) cf[threadIdx.x] = threadIdx.x == 0 ? h : h * u[threadIdx.x - 1];
   __syncthreads();
@@ -182,6 +193,8 @@ __global__ void __launch_bounds__(NT) k_bb_omega(BBDev D, const double2* __restr
 
 // part[t][c] = sum over the 64 rows of tile t of |X[r][c]|
 __global__ void __launch_bounds__(64) k_bb_colsum(BBDev D, const double* __restrict__ X, double* __restrict__ part) {
+  X += (size_t)blockIdx.y * D.total;
+  part += (size_t)blockIdx.y * D.ntiles * 64;
   const int t = blockIdx.x, c = threadIdx.x;
   const int b = bb_block_of_tile(D, t);
   const double* T = X + D.toff[b] + (size_t)(t - D.tstart[b]) * IMG;
@@ -196,6 +209,8 @@ __global__ void __launch_bounds__(64) k_bb_colsum(BBDev D, const double* __restr
 // per block: ||X_b||_1 = max_c sum_I part[(I, c / 64)][c % 64]; m = 16, s from theta_16 (A15)
 __global__ void __launch_bounds__(1024) k_bb_plan(BBDev D, const double* __restrict__ part, BBPlanRec* plan,
                                                   int smax, int* status) {
+  part += (size_t)blockIdx.y * D.ntiles * 64;
+  plan += (size_t)blockIdx.y * BB_PLAN_STRIDE;
   __shared__ double red[32];
   const int b = blockIdx.x, nt = D.nt[b];
   double m = 0.0;
@@ -229,6 +244,8 @@ __global__ void __launch_bounds__(1024) k_bb_plan(BBDev D, const double* __restr
 }
 
 __global__ void __launch_bounds__(NT) k_bb_scale(BBDev D, double* X, const BBPlanRec* plan) {
+  X += (size_t)blockIdx.y * D.total;
+  plan += (size_t)blockIdx.y * BB_PLAN_STRIDE;
   for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < (size_t)D.total; e += (size_t)gridDim.x * NT) {
     const int b = bb_block_of_tile(D, (int)(e / IMG));
     const int s = plan[b].s;
@@ -245,9 +262,11 @@ struct BBCombo {
   double* out;
 };
 __global__ void __launch_bounds__(NT) k_bb_combo(BBDev D, BBCombo g) {
+  const size_t sl = (size_t)blockIdx.y * D.total;   // slice of the batch
+  g.out += sl;
   for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < (size_t)D.total; e += (size_t)gridDim.x * NT) {
     double v = 0.0;
-    for (int q = 0; q < g.nsrc; ++q) v = fma(g.coef[q], g.src[q][e], v);
+    for (int q = 0; q < g.nsrc; ++q) v = fma(g.coef[q], g.src[q][sl + e], v);
     if (g.cid != 0.0) {
       const BBPos p = bb_decode(D, e);
       if (!p.plane && p.I == p.J && p.r == p.c) v += g.cid;
@@ -259,6 +278,11 @@ __global__ void __launch_bounds__(NT) k_bb_combo(BBDev D, BBCombo g) {
 // dst = per block (s odd ? b : a)
 __global__ void __launch_bounds__(NT) k_bb_copy_sel(BBDev D, double* dst, const double* a, const double* bsrc,
                                                     const BBPlanRec* plan) {
+  const size_t sl = (size_t)blockIdx.y * D.total;
+  dst += sl;
+  a += sl;
+  bsrc += sl;
+  plan += (size_t)blockIdx.y * BB_PLAN_STRIDE;
   for (size_t e = (size_t)blockIdx.x * NT + threadIdx.x; e < (size_t)D.total; e += (size_t)gridDim.x * NT) {
     const int b = bb_block_of_tile(D, (int)(e / IMG));
     dst[e] = (plan[b].s & 1) ? bsrc[e] : a[e];
@@ -357,6 +381,8 @@ __device__ __forceinline__ void load_img_re(Strip& s, const double* __restrict__
   }
 }
 
+// C_i = A_i B_i for i < nbatch (A_i = A + i sA, ...; the accumulator is initialised to
+// cid I + sum coef[q] src[q]_i, src_i = src + i sSrc); plan_i = plan + i pstride.
 struct BBGemm {
   const double* A;
   const double* A_alt;
@@ -367,18 +393,39 @@ struct BBGemm {
   double cid;
   int nsrc;
   int slot;
+  int nbatch;
+  long long sA, sB, sC, sSrc;   // doubles between batch members
+  int pstride;                  // plan records between batch members
   const BBPlanRec* plan;
   unsigned long long* ctr;   // profiling: algorithmic flops of the executed block products
   unsigned long long bflops[QAL_BB_MAX_BLOCKS];
 };
 
-__device__ __forceinline__ bool bb_active(const BBDev& D, const BBGemm& g, int b) {
-  return g.slot < 0 || g.slot < g.plan[b].s;
+__device__ __forceinline__ bool bb_active(const BBDev& D, const BBGemm& g, int i, int b) {
+  return g.slot < 0 || g.slot < g.plan[(size_t)i * g.pstride + b].s;
 }
-// next active output tile >= t (or D.ntiles)
-__device__ __forceinline__ int bb_next_tile(const BBDev& D, const BBGemm& g, int t, int stride) {
-  while (t < D.ntiles && !bb_active(D, g, bb_block_of_tile(D, t))) t += stride;
-  return t;
+// virtual tile v = i * ntiles + t: batch member i, output tile t
+struct BBVT {
+  int i, b, I, J;
+};
+__device__ __forceinline__ BBVT bb_vt(const BBDev& D, int v) {
+  BBVT r;
+  r.i = v / D.ntiles;
+  const int t = v - r.i * D.ntiles;
+  r.b = bb_block_of_tile(D, t);
+  const int tl = t - D.tstart[r.b];
+  r.I = tl / D.nt[r.b];
+  r.J = tl % D.nt[r.b];
+  return r;
+}
+// next active virtual tile >= v (or nv)
+__device__ __forceinline__ int bb_next_vt(const BBDev& D, const BBGemm& g, int v, int stride, int nv) {
+  while (v < nv) {
+    const int i = v / D.ntiles;
+    if (bb_active(D, g, i, bb_block_of_tile(D, v - i * D.ntiles))) break;
+    v += stride;
+  }
+  return v;
 }
 
 __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
@@ -387,11 +434,13 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
   double* SB[2] = {smem + IMG, smem + 2 * IMG};
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * IMG);
   const Lane L = lane_id();
+  const int nv = g.nbatch * D.ntiles;
   if (g.ctr && blockIdx.x == 0 && threadIdx.x == 0)
-    for (int b = 0; b < D.nb; ++b)
-      if (bb_active(D, g, b)) atomicAdd(g.ctr, g.bflops[b]);
-  int t = bb_next_tile(D, g, blockIdx.x, gridDim.x);
-  if (t >= D.ntiles) return;
+    for (int i = 0; i < g.nbatch; ++i)
+      for (int b = 0; b < D.nb; ++b)
+        if (bb_active(D, g, i, b)) atomicAdd(g.ctr, g.bflops[b]);
+  int v = bb_next_vt(D, g, blockIdx.x, gridDim.x, nv);
+  if (v >= nv) return;
   // a real block's tiles carry only their re plane (the im plane is zero and never read)
   auto tma_tile = [&](double* dst, const double* src, uint64_t* br, bool real) {
     if (!real) { tma_load_img(dst, src, br); return; }
@@ -406,73 +455,69 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
     fence_mbar_init();
   }
   __syncthreads();
-  auto Aof = [&](int b) { return (g.A_alt && (g.plan[b].s & 1)) ? g.A_alt : g.A; };
-  int b = bb_block_of_tile(D, t);
-  int tl = t - D.tstart[b];
-  int I = tl / D.nt[b], J = tl % D.nt[b];
+  auto Aof = [&](const BBVT& x) {
+    const double* a = (g.A_alt && (g.plan[(size_t)x.i * g.pstride + x.b].s & 1)) ? g.A_alt : g.A;
+    return a + x.i * g.sA;
+  };
+  auto Bof = [&](const BBVT& x) { return g.B + x.i * g.sB; };
+  BBVT x = bb_vt(D, v);
   if (threadIdx.x == 0) {
-    tma_tile(SA, bb_tile(D, Aof(b), b, I, 0), &bar[0], D.real[b]);
-    tma_tile(SB[0], bb_tile(D, g.B, b, 0, J), &bar[1], D.real[b]);
+    tma_tile(SA, bb_tile(D, Aof(x), x.b, x.I, 0), &bar[0], D.real[x.b]);
+    tma_tile(SB[0], bb_tile(D, Bof(x), x.b, 0, x.J), &bar[1], D.real[x.b]);
   }
   uint32_t phA = 0, phB[2] = {0, 0};
   int step = 0;
   Strip a, acc;
-  while (t < D.ntiles) {
-    b = bb_block_of_tile(D, t);
-    tl = t - D.tstart[b];
-    const int nt = D.nt[b];
-    I = tl / nt;
-    J = tl % nt;
+  while (v < nv) {
+    x = bb_vt(D, v);
+    const int nt = D.nt[x.b];
     zero(acc);
     for (int q = 0; q < g.nsrc; ++q) {
-      Strip x;
-      load_img(x, bb_tile(D, g.src[q], b, I, J), L);
+      Strip y;
+      load_img(y, bb_tile(D, g.src[q] + x.i * g.sSrc, x.b, x.I, x.J), L);
       const double c = g.coef[q];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) { acc.re[i] = fma(c, x.re[i], acc.re[i]); acc.im[i] = fma(c, x.im[i], acc.im[i]); }
+      for (int i = 0; i < 16; ++i) { acc.re[i] = fma(c, y.re[i], acc.re[i]); acc.im[i] = fma(c, y.im[i], acc.im[i]); }
     }
-    if (I == J && g.cid != 0.0) {
+    if (x.I == x.J && g.cid != 0.0) {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         if (is_diag(L, i)) acc.re[i] += g.cid;
     }
-    const int tnext = bb_next_tile(D, g, t + gridDim.x, gridDim.x);
+    const int vnext = bb_next_vt(D, g, v + gridDim.x, gridDim.x, nv);
     for (int K = 0; K < nt; ++K, ++step) {
       const int cur = step & 1;
       mbar_wait(&bar[0], phA);
       phA ^= 1;
       mbar_wait(&bar[1 + cur], phB[cur]);
       phB[cur] ^= 1;
-      if (D.real[b]) load_img_re(a, SA, L);
+      if (D.real[x.b]) load_img_re(a, SA, L);
       else load_img(a, SA, L);
       __syncthreads();   // SA drained by every warp; SB[cur^1] no longer read
       if (threadIdx.x == 0) {
-        int tn = t, Kn = K + 1, bn = b, In = I, Jn = J;
+        BBVT xn = x;
+        int Kn = K + 1;
+        bool more = true;
         if (Kn == nt) {
-          tn = tnext;
           Kn = 0;
-          if (tn < D.ntiles) {
-            bn = bb_block_of_tile(D, tn);
-            const int tln = tn - D.tstart[bn];
-            In = tln / D.nt[bn];
-            Jn = tln % D.nt[bn];
-          }
+          more = vnext < nv;
+          if (more) xn = bb_vt(D, vnext);
         }
-        if (tn < D.ntiles) {
+        if (more) {
           fence_proxy_async();
-          tma_tile(SA, bb_tile(D, Aof(bn), bn, In, Kn), &bar[0], D.real[bn]);
-          tma_tile(SB[cur ^ 1], bb_tile(D, g.B, bn, Kn, Jn), &bar[1 + (cur ^ 1)], D.real[bn]);
+          tma_tile(SA, bb_tile(D, Aof(xn), xn.b, xn.I, Kn), &bar[0], D.real[xn.b]);
+          tma_tile(SB[cur ^ 1], bb_tile(D, Bof(xn), xn.b, Kn, xn.J), &bar[1 + (cur ^ 1)], D.real[xn.b]);
         }
       }
-      if (D.real[b]) mma_acc_re(acc, a, SB[cur], L);
+      if (D.real[x.b]) mma_acc_re(acc, a, SB[cur], L);
       else mma_acc(acc, a, SB[cur], L);
     }
-    if (D.real[b]) {
+    if (D.real[x.b]) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc.im[i] = 0.0;   // keep the unused plane zero
     }
-    store_img(bb_tile(D, g.C, b, I, J), acc, L);
-    t = tnext;
+    store_img(bb_tile(D, g.C + x.i * g.sC, x.b, x.I, x.J), acc, L);
+    v = vnext;
   }
 }
 
@@ -483,8 +528,10 @@ int bb_grid_ew() { return 4 * num_sms(); }
 }  // namespace
 
 size_t bb_ws_bytes(const qal_bigblock_plan& p) {
-  // 8 tiled-block matrices + column partials + per-block plan records + device tables
-  return 8 * (size_t)p.total_doubles * 8 + (size_t)p.ntiles * 64 * 8 + 64 * sizeof(BBPlanRec) +
+  // 6 batches of SB tiled-block matrices (X, X2, X3, X4, T0, T1) + the running products P[2] +
+  // column partials and plan records per slice of a batch + device tables
+  const size_t SB = bb_sb(p);
+  return (6 * SB + 2) * (size_t)p.total_doubles * 8 + SB * p.ntiles * 64 * 8 + SB * BB_PLAN_STRIDE * sizeof(BBPlanRec) +
          (size_t)(2 * p.nrows + 3 * BBN) * sizeof(int) + 1024;
 }
 
@@ -636,6 +683,7 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
 
 static cudaError_t bb_gemm(const BBDev& D, const BBGemm& g0, const qal_bigblock_plan& p, cudaStream_t st) {
   BBGemm g = g0;
+  if (g.nbatch < 1) g.nbatch = 1;
   g.ctr = prof_counter(ST_BLK_GEMM);
   for (int b = 0; b < p.nb; ++b) g.bflops[b] = (unsigned long long)p.flops[b];
   static bool attr = false;
@@ -652,21 +700,26 @@ static cudaError_t bb_gemm(const BBDev& D, const BBGemm& g0, const qal_bigblock_
 }
 
 // Propagator of `count` PWC slices of one pulse on the tiled blocks: chunk folds -> chunk_nat (natural,
-// mirror-filled).  The Paterson-Stockmeyer / squaring schedule of launch_dense_expm_fold, per block.
+// mirror-filled).  Slices go in batches of up to bb_sb(p) (never across a chunk boundary): every launch
+// covers the tiles of the whole batch (the per-slice Paterson-Stockmeyer / squaring schedule of
+// launch_dense_expm_fold, per slice and block), the batch's U_k are multiplied by a balanced tree
+// (later slice on the left, Eq. 15) and folded into the chunk's running product.
 cudaError_t launch_bb_expm_fold(const qal_bigblock_plan& p, const double2* L0, const double2* Lc, int J,
                                 const double* u, int count, double h, int chunk, double2* chunk_nat, int* status,
                                 int* flag, double* ws, cudaStream_t st) {
   const size_t M = (size_t)p.total_doubles;
+  const int SB = bb_sb(p);
+  const size_t MB = (size_t)SB * M;
   double* X = ws;
-  double* X2 = X + M;
-  double* X3 = X2 + M;
-  double* X4 = X3 + M;
-  double* T0 = X4 + M;
-  double* T1 = T0 + M;
-  double* P[2] = {T1 + M, T1 + 2 * M};
-  double* part = T1 + 3 * M;
-  BBPlanRec* plan = reinterpret_cast<BBPlanRec*>(part + (size_t)p.ntiles * 64);
-  int* tab = reinterpret_cast<int*>(plan + 64);
+  double* X2 = X + MB;
+  double* X3 = X2 + MB;
+  double* X4 = X3 + MB;
+  double* T0 = X4 + MB;
+  double* T1 = T0 + MB;
+  double* P[2] = {T1 + MB, T1 + MB + M};
+  double* part = P[1] + M;
+  BBPlanRec* plan = reinterpret_cast<BBPlanRec*>(part + (size_t)SB * p.ntiles * 64);
+  int* tab = reinterpret_cast<int*>(plan + (size_t)SB * BB_PLAN_STRIDE);
   BBDev D;
   cudaError_t e = bb_dev(p, tab, D, st);
   if (e != cudaSuccess) return e;
@@ -681,64 +734,96 @@ cudaError_t launch_bb_expm_fold(const qal_bigblock_plan& p, const double2* L0, c
                                   2.7557319223985893e-06, 2.755731922398589e-07, 2.505210838544172e-08,
                                   2.08767569878681e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,
                                   7.647163731819816e-13, 4.779477332387385e-14};
+  // a batch GEMM over S slices with the per-slice plans
+  auto batch = [&](BBGemm g, int S) {
+    g.nbatch = S;
+    g.sA = g.sB = g.sC = g.sSrc = (long long)M;
+    g.pstride = BB_PLAN_STRIDE;
+    g.plan = plan;
+    return bb_gemm(D, g, p, st);
+  };
   int pc = 0;
-  for (int k = 0; k < count && e == cudaSuccess; ++k) {
-    k_bb_omega<<<bb_grid_ew(), NT, 0, st>>>(D, L0, Lc, J, u + (size_t)k * J, h, X);
-    k_bb_colsum<<<p.ntiles, 64, 0, st>>>(D, X, part);
-    k_bb_plan<<<p.nb, 1024, 0, st>>>(D, part, plan, SMAX, status);
-    k_bb_scale<<<bb_grid_ew(), NT, 0, st>>>(D, X, plan);
+  for (int k = 0; k < count && e == cudaSuccess;) {
+    const int S = std::min(SB, std::min(chunk - k % chunk, count - k));
+    const dim3 gew((unsigned)std::max(1, bb_grid_ew() / S), (unsigned)S);
+    k_bb_omega<<<gew, NT, 0, st>>>(D, L0, Lc, J, u + (size_t)k * J, h, X);
+    k_bb_colsum<<<dim3(p.ntiles, S), 64, 0, st>>>(D, X, part);
+    k_bb_plan<<<dim3(p.nb, S), 1024, 0, st>>>(D, part, plan, SMAX, status);
+    k_bb_scale<<<gew, NT, 0, st>>>(D, X, plan);
     launch_counter() += 4;
     BBGemm g{};
     g.slot = -1;
-    g.plan = plan;
     g.A = X; g.B = X; g.C = X2;
-    if ((e = bb_gemm(D, g, p, st)) != cudaSuccess) break;
+    if ((e = batch(g, S)) != cudaSuccess) break;
     g.A = X2; g.C = X3;
-    if ((e = bb_gemm(D, g, p, st)) != cudaSuccess) break;
+    if ((e = batch(g, S)) != cudaSuccess) break;
     g.A = X3; g.C = X4;
-    if ((e = bb_gemm(D, g, p, st)) != cudaSuccess) break;
+    if ((e = batch(g, S)) != cudaSuccess) break;
     BBCombo cb{};
     cb.src[0] = X; cb.src[1] = X2; cb.src[2] = X3; cb.src[3] = X4;
     cb.coef[0] = ifac[13]; cb.coef[1] = ifac[14]; cb.coef[2] = ifac[15]; cb.coef[3] = ifac[16];
     cb.nsrc = 4;
     cb.cid = ifac[12];
     cb.out = T0;
-    k_bb_combo<<<bb_grid_ew(), NT, 0, st>>>(D, cb);
+    k_bb_combo<<<gew, NT, 0, st>>>(D, cb);
     ++launch_counter();
     double* Hin = T0;
     double* Hout = T1;
     for (int blk = 2; blk >= 0 && e == cudaSuccess; --blk) {   // H <- B_blk + H X^4
       BBGemm h2{};
-      h2.A = Hin; h2.B = X4; h2.C = Hout; h2.slot = -1; h2.plan = plan;
+      h2.A = Hin; h2.B = X4; h2.C = Hout; h2.slot = -1;
       h2.src[0] = X; h2.src[1] = X2; h2.src[2] = X3;
       h2.coef[0] = ifac[4 * blk + 1]; h2.coef[1] = ifac[4 * blk + 2]; h2.coef[2] = ifac[4 * blk + 3];
       h2.nsrc = 3;
       h2.cid = ifac[4 * blk];
-      e = bb_gemm(D, h2, p, st);
+      e = batch(h2, S);
       double* tmp = Hin; Hin = Hout; Hout = tmp;
     }
     if (e != cudaSuccess) break;
     double* E[2] = {Hin, Hout};
-    for (int q = 0; q < SMAX && e == cudaSuccess; ++q) {   // squarings, per block only while q < s_b
+    for (int q = 0; q < SMAX && e == cudaSuccess; ++q) {   // squarings, per slice and block only while q < s
       BBGemm sq{};
-      sq.A = E[q & 1]; sq.B = E[q & 1]; sq.C = E[(q + 1) & 1]; sq.slot = q; sq.plan = plan;
-      e = bb_gemm(D, sq, p, st);
+      sq.A = E[q & 1]; sq.B = E[q & 1]; sq.C = E[(q + 1) & 1]; sq.slot = q;
+      e = batch(sq, S);
     }
     if (e != cudaSuccess) break;
-    if (chunk_nat) {
-      if (k % chunk == 0) {
-        k_bb_copy_sel<<<bb_grid_ew(), NT, 0, st>>>(D, P[pc], E[0], E[1], plan);
-        ++launch_counter();
-      } else {
-        BBGemm f{};
-        f.A = E[0]; f.A_alt = E[1]; f.B = P[pc]; f.C = P[pc ^ 1]; f.slot = -1; f.plan = plan;
-        if ((e = bb_gemm(D, f, p, st)) != cudaSuccess) break;
-        pc ^= 1;
+    // U_k of the batch, contiguous in X (free since the Horner step)
+    k_bb_copy_sel<<<gew, NT, 0, st>>>(D, X, E[0], E[1], plan);
+    ++launch_counter();
+    // balanced tree over the batch: level (2i+1, 2i) -> i, an odd last member carried
+    double* in = X;
+    double* outb[2] = {X2, X3};
+    int cnt = S, ob = 0;
+    while (cnt > 1 && e == cudaSuccess) {
+      const int half = cnt / 2;
+      BBGemm t{};
+      t.slot = -1; t.plan = plan; t.pstride = 0;
+      t.A = in + M; t.B = in; t.C = outb[ob];
+      t.nbatch = half;
+      t.sA = t.sB = 2 * (long long)M; t.sC = (long long)M;
+      if ((e = bb_gemm(D, t, p, st)) != cudaSuccess) break;
+      if (cnt & 1) {
+        e = cudaMemcpyAsync(outb[ob] + (size_t)half * M, in + (size_t)(cnt - 1) * M, M * 8, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) break;
       }
-      if (k % chunk == chunk - 1) {
-        k_bb_unpack<<<bb_grid_ew(), NT, 0, st>>>(D, P[pc], chunk_nat + (size_t)(k / chunk) * BBN * BBN);
-        ++launch_counter();
-      }
+      in = outb[ob];
+      ob ^= 1;
+      cnt = half + (cnt & 1);
+    }
+    if (e != cudaSuccess) break;
+    if (k % chunk == 0) {   // first batch of a chunk: P = Q
+      e = cudaMemcpyAsync(P[pc], in, M * 8, cudaMemcpyDeviceToDevice, st);
+    } else {                 // P <- Q P
+      BBGemm f{};
+      f.A = in; f.B = P[pc]; f.C = P[pc ^ 1]; f.slot = -1; f.plan = plan; f.pstride = 0; f.nbatch = 1;
+      e = bb_gemm(D, f, p, st);
+      pc ^= 1;
+    }
+    if (e != cudaSuccess) break;
+    k += S;
+    if (k % chunk == 0) {
+      k_bb_unpack<<<bb_grid_ew(), NT, 0, st>>>(D, P[pc], chunk_nat + (size_t)(k / chunk - 1) * BBN * BBN);
+      ++launch_counter();
     }
     e = cudaGetLastError();
   }
