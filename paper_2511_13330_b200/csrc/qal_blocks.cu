@@ -55,6 +55,10 @@ constexpr int BLK_CPLX_MMAS = 4;
 #define QAL_BLK_INTERLEAVE 1
 #endif
 constexpr bool BLK_INTERLEAVE = QAL_BLK_INTERLEAVE != 0;
+#ifndef QAL_BLK_SWZ4
+#define QAL_BLK_SWZ4 1
+#endif
+constexpr bool BLK_SWZ4 = QAL_BLK_SWZ4 != 0;   // XOR-4 image swizzle (bpair_off)
 #ifndef QAL_BLK_SPLIT_ACC
 #define QAL_BLK_SPLIT_ACC 0
 #endif
@@ -328,10 +332,13 @@ __device__ __forceinline__ void bset_identity(BR<C, R, RE>& s, const Ctx& x, con
 
 // image of a P x P block: re plane (P*P doubles) then im plane; column c of row r at
 // r*P + phys(c) (the within-tile permutation of qal_dev.cuh) XOR 8 on odd rows when C is
-// even (with C odd the row stride 8C already alternates the bank halves).
+// even (with C odd the row stride 8C already alternates the bank halves), XOR 4 on rows with
+// bit 1 set: the B-fragment loads of a k-step (rows 4q + t, 8 consecutive columns per t) then hit
+// 16 distinct 8-byte bank pairs per half-warp for every C (without it rows t and t + 2 collide:
+// ncu counted 35% of the gradient kernel's shared wavefronts as bank conflicts).
 template <int C>
 __device__ __forceinline__ int bpair_off(int row, const Lane& L, int j) {
-  const int swz = (C % 2 == 0) ? ((L.g & 1) << 3) : 0;
+  const int swz = ((C % 2 == 0) ? ((L.g & 1) << 3) : 0) ^ (BLK_SWZ4 ? (((L.g >> 1) & 1) << 2) : 0);
   return row * (8 * C) + ((8 * j + 2 * L.t) ^ swz);
 }
 template <int C, int R, bool RE>
@@ -475,7 +482,7 @@ __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, c
   static_assert(KS >= 1 && KS <= 2 * C, "k-steps");
   constexpr int P = 8 * C, PL = P * P;
   const int swz = (C % 2 == 0) ? (L.t & 1) : 0;   // physical tile of logical tile j: j ^ swz
-  const uint32_t base = smem_u32(Bs + L.t * P + L.g);
+  const uint32_t base = smem_u32(Bs + L.t * P + (L.g ^ (BLK_SWZ4 ? (((L.t >> 1) & 1) << 2) : 0)));
   double br[2][C], bi[2][C];
   double g3q[R][RE || BLK_CPLX_MMAS == 4 ? 1 : 2 * C];   // Gauss Q accumulator
   // BLK_SPLIT_ACC: a second accumulator set halves the dependent DMMA chain of every output tile
