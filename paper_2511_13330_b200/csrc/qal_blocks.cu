@@ -1316,16 +1316,15 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
 constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
 constexpr int BLK_TR_BUF = (BLK_MAX_WARPS + BLK_MAX_SLOTS) * BLK_TR_MAX;   // one parity's trace buffer: per warp + per slot sum
 constexpr int BLK_TRC_MAXJ = 2;   // PWC trace-basis cache in shared memory up to this many controls
-constexpr int BLK_GRAD_SCR = 2;   // L2 scratch images per group (squarings): E, dE
 
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
 // leaves W = L_exp(Omega, G) in A and returns the product count.  SD, SV, SN: group images
-// (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots; scr: the group's L2 scratch.
+// (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots.
 template <int C, int R, int KS, bool RE>
 __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc, const BlkBasis& B, const SliceGrid& G,
                                              int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
                                              uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
-                                             uint32_t tm, uint32_t ts, double* scr, int* bad, const Lane& L) {
+                                             uint32_t tm, uint32_t ts, int* bad, const Lane& L) {
   constexpr size_t IM = img_doubles(C, RE);
   // shared scratch images (own strips only, re-read within the item): X, dX, A6, dA6
   double* gX = sX;
@@ -1548,7 +1547,7 @@ __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& 
 template <int C, int R, int KS, bool RE>
 __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, const SliceGrid& G,
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
-                              double* __restrict__ grad, int* __restrict__ status, double* scr_cta, const Ctx& x,
+                              double* __restrict__ grad, int* __restrict__ status, const Ctx& x,
                               double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr, double gscale,
                               int accum, double2* cache, unsigned long long& nflop, const Lane& L) {
   constexpr int IM = img_doubles(C, RE);
@@ -1557,7 +1556,6 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const int items = batch * N;
   const int K = B.J + B.ncomm;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
-  double* scr = scr_cta + 2 * (size_t)x.off * BLK_GRAD_SCR;
   uint32_t ph = 0;
   auto prefetch = [&](int it) {   // group leader: bulk-copy X_{k+1} -> SN, P_k -> SD of item `it`
     if (leader && it < items) {
@@ -1590,7 +1588,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     bcopy(A, Om);
     const int par = ((item - item0) / istride) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
-                                               ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w], scr,
+                                               ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
                                                bad_sh + par, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const int nx = item + istride;
@@ -1649,7 +1647,7 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
                                                                const double* __restrict__ P_img,
                                                                const double* __restrict__ X_img,
                                                                double* __restrict__ grad, int* __restrict__ status,
-                                                               double* __restrict__ scratch, double gscale,
+                                                               double gscale,
                                                                int accum, int tmem_cols, unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id: [0] X_{k+1} -> SN, [1] P_k -> SD
@@ -1670,7 +1668,6 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
   tmem_fence_after();
   const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
   unsigned long long nflop = 0;
-  double* scr_cta = scratch + (size_t)blockIdx.x * 2 * (size_t)D.packed * BLK_GRAD_SCR;
   const Ctx x = ctx_of(D, T);
   double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
   double2* cache = (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ && D.tcache_off >= 0)
@@ -1678,9 +1675,9 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
                        : nullptr;
   if constexpr (FC == 0)
     BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status,
-                 scr_cta, x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
+                 x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
   else
-    blk_grad_loop<FC, FR, FKS, FRE != 0>(D, batch, B, G, P_img, X_img, grad, status, scr_cta, x, sm, bars[x.bar], tm,
+    blk_grad_loop<FC, FR, FKS, FRE != 0>(D, batch, B, G, P_img, X_img, grad, status, x, sm, bars[x.bar], tm,
                                           bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
@@ -1855,8 +1852,8 @@ static int blk_role(const BlkDev& D) {
   if (key == ((1 * 4 + 1) * 8 + 2) * 2 + 0) return 3;
   return 0;
 }
-using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, const double*, double*, int*, double*,
-                            double, int, int, unsigned long long*);
+using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, const double*, double*, int*, double,
+                            int, int, unsigned long long*);
 using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*);
 static GradKernel grad_kernel(const BlkDev& D) {
   switch (blk_role(D)) {
@@ -2004,11 +2001,7 @@ static int blk_grad_grid(const BlkDev& D, GradKernel fn = nullptr) {
   return std::max(1, per_sm) * num_sms();
 }
 
-size_t blk_grad_scratch_bytes(const qal_block_plan& p) {
-  BlkDev D;
-  if (!to_dev(p, D)) return 0;
-  return (size_t)blk_grad_grid(D) * BLK_GRAD_SCR * 2 * p.packed * 8;
-}
+size_t blk_grad_scratch_bytes(const qal_block_plan&) { return 0; }   // the squarings stay in shared memory
 
 // the PWC trace-basis cache: per warp J x R x 2C x 32 double2, after the group regions
 static int grad_cache_layout(BlkDev& D, int J, int base_doubles) {
@@ -2053,7 +2046,7 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
     const int need = (items + D.nslot - 1) / D.nslot;
     const int grid = need < gmax ? need : gmax;
     prof_pre(ST_BLK_GRAD, st);
-    fn<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, scratch, gscale, accum,
+    fn<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, gscale, accum,
                                            tmem_cols_for(D), prof_counter(ST_BLK_GRAD));
     prof_post(ST_BLK_GRAD, st);
     ++launch_counter();
