@@ -41,13 +41,18 @@ struct BBDev {
   const int* rtype;                    // [nrows] 0 complex, 1 real diagonal, 2 pair a, 3 pair b
   const int* ncode;                    // [4096] 0 complex, 1 real diagonal, 2 pair rep, 3 pair mirror
   int real[QAL_BB_MAX_BLOCKS];         // block b in the real Hermitian basis (qal_blocks.cu A29)
+  int used[QAL_BB_MAX_BLOCKS];         // stored rows of block b (the rest of its 64-multiple is padding)
 };
 
 struct BBPlanRec {   // per block, written on the device
   int m, s, bad, pad;
   double nrm;
 };
-constexpr int BB_PLAN_STRIDE = 64;   // plan records per slice of a batch (>= QAL_BB_MAX_BLOCKS)
+constexpr int BB_PLAN_STRIDE = 64;
+#ifndef QAL_BB_TRIM
+#define QAL_BB_TRIM 1
+#endif
+constexpr bool BB_TRIM = QAL_BB_TRIM != 0;   // skip the padding k-steps / column tiles / row strips   // plan records per slice of a batch (>= QAL_BB_MAX_BLOCKS)
 // slices per batch (every launch covers the tiles of a whole batch): as many as ~4 GB of batch
 // workspace holds, at most 64 (configs[4]: 16; the Hubbard blocks: 64)
 inline int bb_sb(const qal_bigblock_plan& p) {
@@ -372,6 +377,68 @@ __device__ __forceinline__ void mma_acc_re(Strip& acc, const Strip& a, const dou
   }
   QAL_FENCE();
 }
+// The same products restricted to the first qmax k-steps and the first jmax output column tiles (the
+// rest of the tile is block padding: zero rows of B / columns nobody reads).  Exact for the stored
+// entries: the padding rows and columns of every block matrix are decoupled from the stored ones.
+__device__ __forceinline__ void mma_acc_trim(Strip& acc, const Strip& a, const double* __restrict__ Bs, const Lane& L,
+                                             int qmax, int jmax) {
+  const int todd = L.t & 1;
+  const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);
+  const uint32_t bO = smem_u32(Bs + L.t * 64 + L.g - 8 * todd);
+  double br[2][8], bi[2][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t p = ((j & 1) ? bO : bE) + 8u * (8 * j);
+    br[0][j] = lds_v(p);
+    bi[0][j] = lds_v(p + 8u * PLANE);
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (q >= qmax) break;
+    const int cur = q & 1;
+    if (q + 1 < qmax) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t p = ((j & 1) ? bO : bE) + 8u * ((q + 1) * 256 + 8 * j);
+        br[cur ^ 1][j] = lds_v(p);
+        bi[cur ^ 1][j] = lds_v(p + 8u * PLANE);
+      }
+    }
+    const double ar = a.re[q], ai = a.im[q], nai = -a.im[q];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < jmax) {
+        dmma(acc.re[2 * j], acc.re[2 * j + 1], ar, br[cur][j]);
+        dmma(acc.re[2 * j], acc.re[2 * j + 1], nai, bi[cur][j]);
+        dmma(acc.im[2 * j], acc.im[2 * j + 1], ar, bi[cur][j]);
+        dmma(acc.im[2 * j], acc.im[2 * j + 1], ai, br[cur][j]);
+      }
+    }
+  }
+  QAL_FENCE();
+}
+__device__ __forceinline__ void mma_acc_re_trim(Strip& acc, const Strip& a, const double* __restrict__ Bs,
+                                                const Lane& L, int qmax, int jmax) {
+  const int todd = L.t & 1;
+  const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);
+  const uint32_t bO = smem_u32(Bs + L.t * 64 + L.g - 8 * todd);
+  double br[2][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) br[0][j] = lds_v(((j & 1) ? bO : bE) + 8u * (8 * j));
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (q >= qmax) break;
+    const int cur = q & 1;
+    if (q + 1 < qmax) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) br[cur ^ 1][j] = lds_v(((j & 1) ? bO : bE) + 8u * ((q + 1) * 256 + 8 * j));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < jmax) dmma(acc.re[2 * j], acc.re[2 * j + 1], a.re[q], br[cur][j]);
+  }
+  QAL_FENCE();
+}
 __device__ __forceinline__ void load_img_re(Strip& s, const double* __restrict__ img, const Lane& L) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -509,8 +576,19 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
           tma_tile(SB[cur ^ 1], bb_tile(D, Bof(xn), xn.b, Kn, xn.J), &bar[1 + (cur ^ 1)], D.real[xn.b]);
         }
       }
-      if (D.real[x.b]) mma_acc_re(acc, a, SB[cur], L);
-      else mma_acc(acc, a, SB[cur], L);
+      // padding: k-steps past the block's stored rows (last K tile), output column tiles past them
+      // (last column tile), and whole strips of padding rows (last row tile) are skipped
+      const int ub = D.used[x.b];
+      const int qmax = BB_TRIM ? std::min(16, (ub - 64 * K + 3) >> 2) : 16;
+      const int jmax = BB_TRIM ? std::min(8, (ub - 64 * x.J + 7) >> 3) : 8;
+      const bool rows = !BB_TRIM || 64 * x.I + 8 * L.w < ub;
+      if (rows && qmax == 16 && jmax == 8) {
+        if (D.real[x.b]) mma_acc_re(acc, a, SB[cur], L);
+        else mma_acc(acc, a, SB[cur], L);
+      } else if (rows) {
+        if (D.real[x.b]) mma_acc_re_trim(acc, a, SB[cur], L, qmax, jmax);
+        else mma_acc_trim(acc, a, SB[cur], L, qmax, jmax);
+      }
     }
     if (D.real[x.b]) {
 #pragma unroll
@@ -559,6 +637,7 @@ static cudaError_t bb_dev(const qal_bigblock_plan& p, int* tab, BBDev& D, cudaSt
     h[p.nrows + 2 * BBN + i] = p.ncode[i];
   }
   for (int b = 0; b < p.nb; ++b) D.real[b] = p.real[b];
+  for (int b = 0; b < p.nb; ++b) D.used[b] = p.size[b];
   // pageable source: the runtime stages it before returning, so `h` may die with this frame
   const cudaError_t e = cudaMemcpyAsync(tab, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, st);
   D.perm = tab;
