@@ -26,7 +26,9 @@
  *   vjp                 pinned (equals gradient for C = S_V^dag/d^2; central FD of Re Tr(C Lambda))
  *   logical_loss        pinned (Pi = I for Lambda = I, logical swap, FD of the loss vs cotangent)
  *   adam_step           pinned (closed forms: first step lr sign(g); constant gradient)
- *   sines_eval          parity unpinned vs the paper (A11: the paper gives no values)
+ *   sines_eval          pinned by the mathematics of A11 (the paper prints no values): one-term
+ *                       extremes u_max/2 (1 +- 1/sqrt 2) and period, unit RMS, Cauchy-Schwarz
+ *                       clipping, Gauss-Legendre nodes vs numpy leggauss (tests/test_oracle_pins.py)
  */
 #include <complex.h>
 #include <math.h>
@@ -451,7 +453,7 @@ static int gradient_core(int d, int N, double T, int order, int mode, int J, con
 /* configs[3] control function (A11):                                               */
 /*   s_j(t) = sum_m a_m sin(2 pi f_m t + phi_m) / sqrt(sum_m a_m^2 / 2)               */
 /*   u_j(t) = clip(u_max/2 (1 + 0.5 s_j(t)), 0, u_max)                                */
-/* prm[j][m][3] = (a, f, phi).  parity unpinned vs the paper (no values printed).     */
+/* prm[j][m][3] = (a, f, phi).  The paper prints no values; pinned by A11's mathematics. */
 /* ------------------------------------------------------------------ */
 void qalref_sines_eval(int J, int nterm, const double *prm, double umax, double t, double *out)
 {

@@ -400,6 +400,78 @@ def test_sines_controls_clip_and_nodes(oracle):
     assert np.allclose(nodes[k, 1], oracle.sines_eval(prm, qi.U_MAX, k * h + (0.5 + math.sqrt(3) / 6) * h))
 
 
+def test_sines_single_term_extremes_and_period(oracle):
+    """A11 pins from the mathematics of the normalised sum, not its formula: with one term the
+    normalisation a / sqrt(a^2 / 2) makes s = sqrt(2) sin(.), so u never clips, has period 1/f, and
+    reaches exactly u_max/2 (1 +- 1/sqrt(2)) where the sine peaks."""
+    a, f, phi = 0.37, 0.0125, 0.9
+    prm = np.array([[[a, f, phi]]])
+    umax = qi.U_MAX
+    t_peak = (0.25 - phi / (2 * math.pi)) / f            # 2 pi f t + phi = pi / 2
+    t_trough = t_peak + 0.5 / f
+    assert abs(oracle.sines_eval(prm, umax, t_peak)[0] - umax / 2 * (1 + 2 ** -0.5)) <= 1e-15 * umax
+    assert abs(oracle.sines_eval(prm, umax, t_trough)[0] - umax / 2 * (1 - 2 ** -0.5)) <= 1e-15 * umax
+    ts = np.linspace(0.0, 1.0 / f, 777)
+    v = np.array([oracle.sines_eval(prm, umax, t)[0] for t in ts])
+    v2 = np.array([oracle.sines_eval(prm, umax, t + 3.0 / f)[0] for t in ts])
+    assert np.max(np.abs(v - v2)) <= 1e-13 * umax
+    assert umax / 2 * (1 - 2 ** -0.5) - 1e-15 <= v.min() and v.max() <= umax / 2 * (1 + 2 ** -0.5) + 1e-15
+    # a second control channel is independent of the first
+    prm2 = np.array([[[a, f, phi]], [[1.0, 0.0, math.pi / 2]]])   # f = 0: s = sqrt(2), constant
+    out = oracle.sines_eval(prm2, umax, 123.0)
+    assert abs(out[1] - umax / 2 * (1 + 2 ** -0.5)) <= 1e-15 * umax
+
+
+def test_sines_unit_rms_and_clipping(oracle):
+    """The normalisation gives s unit RMS for incommensurate frequencies (mean sin^2 = 1/2, cross
+    terms average out): two equal-amplitude terms never clip (|s| <= 2) and mean(s^2) -> 1; amplitudes
+    pushing s beyond +-2 clip to exactly 0 and u_max."""
+    umax = qi.U_MAX
+    prm = np.array([[[0.5, 0.0101, 0.3], [0.5, 0.0163, 1.7]]])
+    ts = np.linspace(0.0, 40000.0, 200001)
+    u = np.array([oracle.sines_eval(prm, umax, t)[0] for t in ts])
+    s = 4.0 * u / umax - 2.0                               # invert u = u_max/2 (1 + s/2) (no clipping)
+    assert np.all((u > 0.0) & (u < umax))
+    assert abs(np.mean(s * s) - 1.0) < 5e-3 and abs(np.mean(s)) < 5e-3
+    # two equal terms: s = sin + sin, |s| <= 2 (Cauchy-Schwarz bound sqrt(2 n) with n = 2)
+    assert np.max(np.abs(s)) <= 2.0 + 1e-12
+    # a constant (f = 0) term at phase pi/2 plus a sinusoid: s = 1 + sin(.), reaching the bound 2
+    prm_c = np.array([[[1.0, 0.0, math.pi / 2], [1.0, 0.02, 0.0]]])   # s = sin(.) + 1 over sqrt(1)
+    t_hi = 0.25 / 0.02                                      # s = 2 (edge), u = u_max exactly
+    t_lo = 0.75 / 0.02                                      # s = 0, u = u_max / 2
+    assert abs(oracle.sines_eval(prm_c, umax, t_hi)[0] - umax) <= 1e-15 * umax
+    assert abs(oracle.sines_eval(prm_c, umax, t_lo)[0] - umax / 2) <= 1e-15 * umax
+    # Cauchy-Schwarz: |s| <= sqrt(2 n); three equal constant terms give s = 3 / sqrt(3/2) = sqrt(6) > 2
+    prm_x = np.array([[[1.0, 0.0, math.pi / 2]] * 3])
+    assert oracle.sines_eval(prm_x, umax, 5.0)[0] == umax
+    prm_y = np.array([[[1.0, 0.0, -math.pi / 2]] * 3])
+    assert oracle.sines_eval(prm_y, umax, 5.0)[0] == 0.0
+
+
+def test_sines_nodes_are_gauss_legendre(oracle):
+    """Node sampling pinned to numpy's Gauss-Legendre rule (leggauss(2) mapped onto each slice), and
+    the 2-point rule's exactness for cubics: integrating the sampled slice values reproduces the
+    exact integral of u over [0, T] up to the rule's O(h^4) error."""
+    prm = qi.sine_params(3, 2)
+    umax = qi.U_MAX
+    N, T = 40, 200.0
+    h = T / N
+    xi, wts = np.polynomial.legendre.leggauss(2)
+    nodes = oracle.sines_nodes(prm, umax, N, T)
+    for k in (0, 17, N - 1):
+        for a in range(2):
+            t = k * h + h * (1.0 + xi[a]) / 2.0
+            assert np.array_equal(nodes[k, a], oracle.sines_eval(prm, umax, t)) or \
+                np.max(np.abs(nodes[k, a] - oracle.sines_eval(prm, umax, t))) <= 1e-15 * umax
+    # composite 2-point Gauss vs a fine composite Simpson integral of the same function
+    gauss = (h / 2.0) * np.einsum("a,kaj->j", wts, nodes)
+    tf = np.linspace(0.0, T, 20001)
+    uf = np.array([oracle.sines_eval(prm, umax, t) for t in tf])
+    from scipy.integrate import simpson
+    ref = simpson(uf, x=tf, axis=0)
+    assert np.max(np.abs(gauss - ref)) <= 1e-3 * T * umax   # clipped kinks make u only C^0
+
+
 # ---------------------------------------------------------------- helpers used by the d = 64 checks
 def test_matmul_rows_is_the_matrix_product(oracle):
     rng = np.random.default_rng(11)
