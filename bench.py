@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
+    ap.add_argument("--cpu-sample-pulses", type=int, default=3,
+                    help="pulses in the cpu_baseline sample of our arm (~5 s of oracle work each)")
     ap.add_argument("--cfg4-slices", type=int, default=None,
                     help="slices per step of the cfg4 / hubbard3 sample (default: dense 8, blocks 64)")
     ap.add_argument("--structure", default="blocks", choices=["blocks", "dense"],
@@ -101,18 +103,19 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
-def oracle_sample(prob, n_sample):
+def oracle_sample(prob, n_sample, pulses=1):
     """The oracle as it stands (O1-O7: forward + per-direction gradient) on the first n_sample
-    slices of pulse 0 with the workload's slice width; returns (slices/s, seconds, threads)."""
+    slices of pulses 0..pulses-1 (each with its own drift) with the workload's slice width; returns
+    (slices/s, seconds, threads)."""
     import oracle
-    L0, Lc = oracle.build_liouvillian(prob.H0[0], prob.Hc, prob.C)
     h = prob.T / prob.N
-    u = prob.u[0, :n_sample]
     t0 = time.perf_counter()
-    oracle.gradient(L0, Lc, u, h * n_sample, n_sample, prob.V)
+    for p in range(pulses):
+        L0, Lc = oracle.build_liouvillian(prob.H0[p], prob.Hc, prob.C)
+        oracle.gradient(L0, Lc, prob.u[p, :n_sample], h * n_sample, n_sample, prob.V)
     dt = time.perf_counter() - t0
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return n_sample / dt, dt, threads
+    return pulses * n_sample / dt, dt, threads
 
 
 def run_reference(args):
@@ -302,10 +305,11 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
-        v, dt, threads = oracle_sample(prob, args.cpu_sample_slices)
+        npl = max(1, min(args.cpu_sample_pulses, prob.u.shape[0]))
+        v, dt, threads = oracle_sample(prob, args.cpu_sample_slices, npl)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"oracle forward + gradient on slices 0..{args.cpu_sample_slices - 1} of pulse 0 "
-                         f"of this workload ({dt:.1f} s), OpenMP over gradient directions"}
+               "sample": f"oracle forward + gradient on slices 0..{args.cpu_sample_slices - 1} of pulses "
+                         f"0..{npl - 1} of this workload ({dt:.1f} s), OpenMP over gradient directions"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
