@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/qal.h"
@@ -1871,8 +1872,11 @@ static FwdKernel fwd_kernel(const BlkDev& D) {
     default: return k_blk_expm_fold<0, 0, 0, 0>;
   }
 }
-// dynamic shared-memory opt-in per kernel function (several kernels share one launcher)
+// dynamic shared-memory opt-in per kernel function (several kernels share one launcher; callers on
+// several host threads are serialised here)
 static cudaError_t set_smem_fn(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   static std::vector<std::pair<const void*, size_t>> done;
   for (auto& d : done)
     if (d.first == fn) {

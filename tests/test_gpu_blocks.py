@@ -421,3 +421,23 @@ def test_launch_sets_fused_vs_group_specialised(torch_cuda, qal, monkeypatch, mi
     # two slots per set, and an invalid list (group 0 twice) falling back to the default
     F2, g2, L2 = run(",".join(f"{1 << k}:2" for k in range(plan.ngroups)), f"1:1,1:1,{allg}:1")
     assert np.array_equal(L2, Ld) and np.array_equal(g2, gd)
+
+
+@pytest.mark.parametrize("batch,N", [(1, 1), (3, 5), (5, 2), (7, 3)])
+def test_block_gradient_degenerate_and_ragged_sizes(torch_cuda, qal, oracle, batch, N):
+    """Item counts below and not divisible by the slots per CTA (group-specialised launches leave
+    slots empty), a single slice, and pulse counts that are not multiples of anything, vs the oracle."""
+    torch = torch_cuda
+    p = qi.cfg2(batch=batch, N=N, T=200.0 * N / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, qi.cfg2(batch=1, N=2), True)
+    L0 = qal.qal_build_liouvillian(dev(torch, p.H0), dev(torch, p.Hc), dev(torch, p.C))[0]
+    L0p, f0 = qal.qal_block_pack(plan, L0)
+    assert f0.item() == 0
+    F, g, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V))
+    torch.cuda.synchronize()
+    F, g = F.cpu().numpy(), g.cpu().numpy()
+    for b in range(batch):
+        rL0, rLc = oracle.build_liouvillian(p.H0[b], p.Hc, p.C)
+        Fr, gr, _ = oracle.gradient(rL0, rLc, p.u[b], p.T, p.N, p.V)
+        assert abs(F[b] - Fr) / abs(Fr) <= TOL_PROP
+        assert relfro(g[b], gr) <= TOL_GRAD
