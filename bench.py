@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--pulses", type=int, default=4096, help="pulses per GPU (configs[2]: 4096)")
     ap.add_argument("--slices", type=int, default=1024)
     ap.add_argument("--sub-batch", type=int, default=None,
-                    help="pulses per library call (default: dense 296, blocks sized to ~40 GB of workspace)")
+                    help="pulses per library call (default: dense 296, blocks sized to ~80 GB of workspace)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=1024)
