@@ -60,6 +60,11 @@ constexpr bool BLK_INTERLEAVE = QAL_BLK_INTERLEAVE != 0;
 #define QAL_BLK_SWZ4 1
 #endif
 constexpr bool BLK_SWZ4 = QAL_BLK_SWZ4 != 0;   // XOR-4 image swizzle (bpair_off)
+#ifndef QAL_BLK_TMEM_SCR
+#define QAL_BLK_TMEM_SCR 0
+#endif
+constexpr bool BLK_TMEM_SCR = QAL_BLK_TMEM_SCR != 0;   // gradient scratch strips in TMEM slots 4..7
+constexpr int BLK_TSLOTS = BLK_TMEM_SCR ? 8 : 4;       // TMEM strip slots per warp
 #ifndef QAL_BLK_SPLIT_ACC
 #define QAL_BLK_SPLIT_ACC 0
 #endif
@@ -209,7 +214,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
     }
     D.tstride[v] = st;
     D.tcol[v] = qused[v & 3];
-    qused[v & 3] += 4 * st;
+    qused[v & 3] += BLK_TSLOTS * st;
   }
   const int need = std::max(std::max(qused[0], qused[1]), std::max(qused[2], qused[3]));
   D.tmem_cols = 32;
@@ -1332,12 +1337,26 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   double* gdX = sX + IM;
   double* gA6 = sX + 2 * IM;
   double* gdA6 = sX + 3 * IM;
-  // squarings: E, dE reuse the A6 / dA6 slots (dead once the polynomial is formed; own strips,
-  // so a lane re-reads only what it wrote)
-  double* gE = gA6;
-  double* gdE = gdA6;
-#define SQ_LD(s_, img_) bload_img(s_, img_, x, L)
-#define SQ_ST(img_, s_) bstore_img(img_, s_, x, L)
+  // warp-private scratch strips X, dX, A6, dA6 (E, dE of the squarings reuse A6, dA6): shared-memory
+  // images (own strips only) or, with BLK_TMEM_SCR, TMEM slots 4..7 of the warp (the real group's
+  // gradient is nearer its shared-memory wavefront limit than its DMMA pipe)
+  double* const gS[4] = {gX, gdX, gA6, gdA6};
+  (void)gS;
+#define SCR_ST(i_, s_)                                         \
+  do {                                                         \
+    if constexpr (BLK_TMEM_SCR) bt_store(tm + (4 + (i_)) * ts, s_); \
+    else bstore_img(gS[i_], s_, x, L);                         \
+  } while (0)
+#define SCR_LD(s_, i_)                                         \
+  do {                                                         \
+    if constexpr (BLK_TMEM_SCR) bt_load(s_, tm + (4 + (i_)) * ts); \
+    else bload_img(s_, gS[i_], x, L);                          \
+  } while (0)
+#define SCR_AXPY(d_, a_, i_)                                   \
+  do {                                                         \
+    if constexpr (BLK_TMEM_SCR) bt_axpy(d_, a_, tm + (4 + (i_)) * ts); \
+    else baxpy_img(d_, a_, gS[i_], x, L);                      \
+  } while (0)
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
   // A holds Omega_k on entry (built one item ahead by the caller)
   const double nrm = bnorm1(A, red, x, L);
@@ -1347,7 +1366,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   const double sc = ldexp(1.0, -s);
   bscale(A, sc);
   bstore_img(SV, A, x, L);
-  bstore_img(gX, A, x, L);
+  SCR_ST(0, A);
   // G = P_k X_{k+1} (P_k in SD, X_{k+1} in SN: both TMA-prefetched during the previous item);  dX = G / 2^s
   mbar_wait(barP, ph);
   bload_img(A, SD, x, L);
@@ -1358,7 +1377,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   bscale(acc, sc);
   grp_sync(x);                                         // SV (X) complete; reads of SD (P_k) done
   bstore_img(SD, acc, x, L);
-  bstore_img(gdX, acc, x, L);
+  SCR_ST(1, acc);
   grp_sync(x);                                         // SD = dX complete
   bload_img(A, SV, x, L);
   bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                  // A2 = X X
@@ -1370,8 +1389,8 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   int np = 1 + 1 + 2;
   if (m == 8) {
     grp_sync(x);
-    bzero(acc); baxpy_img(acc, c_t8[0], gX, x, L); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, x, L);
-    bzero(acc); baxpy_img(acc, c_t8[0], gdX, x, L); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, x, L);
+    bzero(acc); SCR_AXPY(acc, c_t8[0], 0); bt_axpy(acc, c_t8[1], T0); bstore_img(SV, acc, x, L);
+    bzero(acc); SCR_AXPY(acc, c_t8[0], 1); bt_axpy(acc, c_t8[1], T1); bstore_img(SD, acc, x, L);
     grp_sync(x);
     bt_load(A, T0);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // Y = A2 W
@@ -1385,19 +1404,19 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
     bzero(acc); bt_axpy(acc, 1.0, T3); bt_axpy(acc, c_t8[4], T1); bstore_img(SD, acc, x, L);
     grp_sync(x);
     bzero(acc);
-    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); baxpy_img(acc, 1.0, gdX, x, L);
-    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); baxpy_img(A, c_t8[3], gdX, x, L);   // dL
+    bt_axpy(acc, c_t8[5], T3); bt_axpy(acc, c_t8[6], T1); SCR_AXPY(acc, 1.0, 1);
+    bzero(A); bt_axpy(A, 1.0, T3); bt_axpy(A, c_t8[2], T1); SCR_AXPY(A, c_t8[3], 1);   // dL
     bmma<C, R, KS, RE>(acc, A, SV, x, L);
-    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); baxpy_img(A, c_t8[3], gX, x, L);    // L
+    bzero(A); bt_axpy(A, 1.0, T2); bt_axpy(A, c_t8[2], T0); SCR_AXPY(A, c_t8[3], 0);    // L
     bmma<C, R, KS, RE>(acc, A, SD, x, L);
-    if (s > 0) SQ_ST(gdE, acc);
+    if (s > 0) SCR_ST(3, acc);
     np += 1 + 2 + 2;
     if (s > 0) {
       bzero(acc);
-      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); baxpy_img(acc, 1.0, gX, x, L);
+      bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); SCR_AXPY(acc, 1.0, 0);
       badd_diag(acc, 1.0, x, L);
       bmma<C, R, KS, RE>(acc, A, SV, x, L);
-      SQ_ST(gE, acc);
+      SCR_ST(2, acc);
       ++np;
     }
   } else {
@@ -1414,86 +1433,87 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
     grp_sync(x);
     bt_load(A, T2);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // A6
-    bstore_img(gA6, acc, x, L);
+    SCR_ST(2, acc);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // A3 dA3
     bt_load(A, T3);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dA3 A3
-    bstore_img(gdA6, acc, x, L);
+    SCR_ST(3, acc);
     grp_sync(x);
     bzero(acc);
-    baxpy_img(acc, c_t18[T18_B5][1], gX, x, L); bt_axpy(acc, c_t18[T18_B5][2], T0);
-    baxpy_img(acc, 1.0, gA6, x, L);
+    SCR_AXPY(acc, c_t18[T18_B5][1], 0); bt_axpy(acc, c_t18[T18_B5][2], T0);
+    SCR_AXPY(acc, 1.0, 2);
     bstore_img(SV, acc, x, L);
     bzero(acc);
-    baxpy_img(acc, c_t18[T18_B5][1], gdX, x, L); bt_axpy(acc, c_t18[T18_B5][2], T1);
-    baxpy_img(acc, 1.0, gdA6, x, L);
+    SCR_AXPY(acc, c_t18[T18_B5][1], 1); bt_axpy(acc, c_t18[T18_B5][2], T1);
+    SCR_AXPY(acc, 1.0, 3);
     bstore_img(SD, acc, x, L);
     grp_sync(x);
     bzero(acc);                                        // dA9 = dB4 + dB1 B5 + B1 dB5
-    baxpy_img(acc, c_t18[T18_B4][1], gdX, x, L); bt_axpy(acc, c_t18[T18_B4][2], T1);
-    bt_axpy(acc, c_t18[T18_B4][3], T3); baxpy_img(acc, c_t18[T18_B4][4], gdA6, x, L);
+    SCR_AXPY(acc, c_t18[T18_B4][1], 1); bt_axpy(acc, c_t18[T18_B4][2], T1);
+    bt_axpy(acc, c_t18[T18_B4][3], T3); SCR_AXPY(acc, c_t18[T18_B4][4], 3);
     bzero(A);
-    baxpy_img(A, c_t18[T18_B1][1], gdX, x, L); bt_axpy(A, c_t18[T18_B1][2], T1);
+    SCR_AXPY(A, c_t18[T18_B1][1], 1); bt_axpy(A, c_t18[T18_B1][2], T1);
     bt_axpy(A, c_t18[T18_B1][3], T3);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);
     bzero(A);
-    baxpy_img(A, c_t18[T18_B1][1], gX, x, L); bt_axpy(A, c_t18[T18_B1][2], T0);
+    SCR_AXPY(A, c_t18[T18_B1][1], 0); bt_axpy(A, c_t18[T18_B1][2], T0);
     bt_axpy(A, c_t18[T18_B1][3], T2);
     bmma<C, R, KS, RE>(acc, A, SD, x, L);
     bstore_img(SN, acc, x, L);                         // dA9 (SN idle since G)
     bzero(acc);                                        // A9 = B4 + B1 B5 (A holds B1)
     badd_diag(acc, c_t18[T18_B4][0], x, L);
-    baxpy_img(acc, c_t18[T18_B4][1], gX, x, L); bt_axpy(acc, c_t18[T18_B4][2], T0);
-    bt_axpy(acc, c_t18[T18_B4][3], T2); baxpy_img(acc, c_t18[T18_B4][4], gA6, x, L);
+    SCR_AXPY(acc, c_t18[T18_B4][1], 0); bt_axpy(acc, c_t18[T18_B4][2], T0);
+    bt_axpy(acc, c_t18[T18_B4][3], T2); SCR_AXPY(acc, c_t18[T18_B4][4], 2);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);
     grp_sync(x);                                       // reads of SV (B5), SD (dB5) done
     bstore_img(SV, acc, x, L);                         // A9
     grp_sync(x);                                       // A9 (SV), dA9 (SN) complete
     bzero(acc);                                        // dT = dB2 + dL A9 + L dA9
-    baxpy_img(acc, c_t18[T18_B2][1], gdX, x, L); bt_axpy(acc, c_t18[T18_B2][2], T1);
-    bt_axpy(acc, c_t18[T18_B2][3], T3); baxpy_img(acc, c_t18[T18_B2][4], gdA6, x, L);
+    SCR_AXPY(acc, c_t18[T18_B2][1], 1); bt_axpy(acc, c_t18[T18_B2][2], T1);
+    bt_axpy(acc, c_t18[T18_B2][3], T3); SCR_AXPY(acc, c_t18[T18_B2][4], 3);
     bload_img(A, SN, x, L);                            // dL = dB3 + dA9
-    baxpy_img(A, c_t18[T18_B3][1], gdX, x, L); bt_axpy(A, c_t18[T18_B3][2], T1);
-    bt_axpy(A, c_t18[T18_B3][3], T3); baxpy_img(A, c_t18[T18_B3][4], gdA6, x, L);
+    SCR_AXPY(A, c_t18[T18_B3][1], 1); bt_axpy(A, c_t18[T18_B3][2], T1);
+    bt_axpy(A, c_t18[T18_B3][3], T3); SCR_AXPY(A, c_t18[T18_B3][4], 3);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);
     bload_img(A, SV, x, L);                            // L = B3 + A9
     badd_diag(A, c_t18[T18_B3][0], x, L);
-    baxpy_img(A, c_t18[T18_B3][1], gX, x, L); bt_axpy(A, c_t18[T18_B3][2], T0);
-    bt_axpy(A, c_t18[T18_B3][3], T2); baxpy_img(A, c_t18[T18_B3][4], gA6, x, L);
+    SCR_AXPY(A, c_t18[T18_B3][1], 0); bt_axpy(A, c_t18[T18_B3][2], T0);
+    bt_axpy(A, c_t18[T18_B3][3], T2); SCR_AXPY(A, c_t18[T18_B3][4], 2);
     bmma<C, R, KS, RE>(acc, A, SN, x, L);
-    if (s > 0) SQ_ST(gdE, acc);
+    if (s > 0) SCR_ST(3, acc);
     np += 1 + 2 + 1 + 2 + 2 + 1 + 2;
     if (s > 0) {                                       // T = B2 + L A9
       bzero(acc);
       badd_diag(acc, c_t18[T18_B2][0], x, L);
-      baxpy_img(acc, c_t18[T18_B2][1], gX, x, L); bt_axpy(acc, c_t18[T18_B2][2], T0);
-      bt_axpy(acc, c_t18[T18_B2][3], T2); baxpy_img(acc, c_t18[T18_B2][4], gA6, x, L);
+      SCR_AXPY(acc, c_t18[T18_B2][1], 0); bt_axpy(acc, c_t18[T18_B2][2], T0);
+      bt_axpy(acc, c_t18[T18_B2][3], T2); SCR_AXPY(acc, c_t18[T18_B2][4], 2);
       bmma<C, R, KS, RE>(acc, A, SV, x, L);
-      SQ_ST(gE, acc);
+      SCR_ST(2, acc);
       ++np;
     }
   }
   for (int q = 0; q < s; ++q) {                        // (E, dE) <- (E E, dE E + E dE)
     grp_sync(x);
-    SQ_LD(A, gE);
+    SCR_LD(A, 2);
     bstore_img(SV, A, x, L);
-    SQ_LD(acc, gdE);
+    SCR_LD(acc, 3);
     bstore_img(SD, acc, x, L);
     grp_sync(x);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // E dE
-    SQ_LD(A, gdE);
+    SCR_LD(A, 3);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dE E
-    SQ_ST(gdE, acc);
-    SQ_LD(A, gE);
+    SCR_ST(3, acc);
+    SCR_LD(A, 2);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // E E
-    SQ_ST(gE, acc);
+    SCR_ST(2, acc);
     np += 3;
   }
-  if (s > 0) SQ_LD(A, gdE);
+  if (s > 0) SCR_LD(A, 3);
   else bcopy(A, acc);
   return np;
-#undef SQ_LD
-#undef SQ_ST
+#undef SCR_ST
+#undef SCR_LD
+#undef SCR_AXPY
 }
 
 // weighted traces Re Tr(W_g B_m,g) over the warp's rows, added to the warp's partial sums
