@@ -445,6 +445,11 @@ typedef struct {
  * (synchronises `stream`).  QAL_ERR_UNSUPPORTED beyond 48 stored blocks. */
 int qal_bigblock_plan_build(int nmat, const qal_c128 *mats, int mirror, qal_bigblock_plan *plan, void *stream);
 
+/*
+ * Device workspace of qal_bigblock_expm_slices: six tiled-block matrices per slice of a batch (slices
+ * are processed in batches of up to 64, as many as ~4 GB holds for the plan's tile count), the two
+ * running chunk products, per-slice norm partials and plan records, and the index tables.
+ */
 size_t qal_bigblock_workspace_bytes(const qal_bigblock_plan *plan);
 
 /*
@@ -452,7 +457,10 @@ size_t qal_bigblock_workspace_bytes(const qal_bigblock_plan *plan);
  * (PWC u [count][n_ctrl], L0 [4096][4096], Lc [n_ctrl][4096][4096], natural layout), chunk folds
  * written to chunk_prod [count/chunk][4096][4096] (natural, mirror-filled, zero between blocks).
  * If `flag` (device int, caller-zeroed) is given, every basis entry coupling two blocks is checked
- * (QAL_ERR_STRUCTURE).  ws >= qal_bigblock_workspace_bytes(plan).
+ * (QAL_ERR_STRUCTURE).  ws >= qal_bigblock_workspace_bytes(plan).  Slices are exponentiated in
+ * batches that never cross a chunk boundary; each batch's U_k are multiplied by a balanced tree (later
+ * slice on the left, Eq. 15) and folded into the chunk product, so the rounding order
+ * differs from a slice-by-slice fold (same product, within the BJ tolerance).
  */
 int qal_bigblock_expm_slices(const qal_bigblock_plan *plan, int n_slices, double T, int count, int n_ctrl,
                              const double *u, const qal_c128 *L0, const qal_c128 *Lc, int chunk,
