@@ -1286,6 +1286,7 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
   if (leader) nflop += (unsigned long long)(N - 1) * D.gflops[x.g];
 }
 
+template <int FC, int FR, int FKS, int FRE>   // as k_blk_grad_slices: FC == 0 any roles
 __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev D, int batch, int N,
                                                                         const double* __restrict__ U_img,
                                                                         const double2* __restrict__ V,
@@ -1312,8 +1313,12 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
     if (b >= batch) continue;
     const size_t base = (size_t)b * N * 2 * D.packed;
     double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
-    BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V,
-                 Cseed ? Cseed + (size_t)b * D.packed : nullptr, X_img + base, x, sm, bars[x.bar], nflop, L);
+    const double2* cs = Cseed ? Cseed + (size_t)b * D.packed : nullptr;
+    if constexpr (FC == 0)
+      BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V, cs, X_img + base, x, sm,
+                   bars[x.bar], nflop, L);
+    else
+      blk_suffix_task<FC, FR, FKS, FRE != 0>(D, N, U_img + base, V, cs, X_img + base, x, sm, bars[x.bar], nflop, L);
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
 }
@@ -1806,7 +1811,8 @@ __global__ void k_blk_fidelity_cotangent(BlkDev D, const double2* __restrict__ V
 // regions), so that a light group never idles inside a CTA while a heavy one finishes the item, every
 // CTA has a multiple of 4 warps (all four SM sub-partitions), and a one-role launch runs the kernel
 // compiled for that role alone (below).  Measured on configs[2] (ms per 4096 x 1024 step): forward
-// 112 fused -> 96 per group; gradient 197 fused -> 176 per group; the suffix chain stays fused (17.5).
+// 112 fused -> 96 per group; gradient 197 fused -> 176 per group; suffix chain 17.3 fused -> 15.6 per
+// group (role kernels).
 struct BlkSet {
   unsigned gmask;
   int nslot;
@@ -1816,7 +1822,7 @@ static int blk_group_warps(const qal_block_plan& p, int g) {
   return to_dev(p, D, 1u << g, 1) ? D.nwarps : 0;
 }
 // kind 0 forward, 1 gradient: one set per group, slots 4 / warps (4 for 3-warp groups); kind 2 suffix
-// chain: one CTA per pulse, all groups.  env (experiments) QAL_BLK_SETS_FWD / _GRAD / _CHAIN =
+// chain: one set per group, 4 pulses per CTA.  env (experiments) QAL_BLK_SETS_FWD / _GRAD / _CHAIN =
 // "mask:slots,..." must cover every group exactly once, else it is ignored.
 static void blk_sets(const qal_block_plan& p, int kind, std::vector<BlkSet>& sets) {
   sets.clear();
@@ -1840,8 +1846,8 @@ static void blk_sets(const qal_block_plan& p, int kind, std::vector<BlkSet>& set
     if (ok && seen == all) return;
     sets.clear();
   }
-  if (kind == 2) {
-    sets.push_back({all, 1});
+  if (kind == 2) {   // suffix chain: one launch per group, 4 pulses per CTA (role kernels: 56 registers)
+    for (int g = 0; g < p.ngroups; ++g) sets.push_back({1u << g, 4});
     return;
   }
   for (int g = 0; g < p.ngroups; ++g) {
@@ -1882,6 +1888,16 @@ static GradKernel grad_kernel(const BlkDev& D) {
     case 2: return k_blk_grad_slices<2, 1, 4, 0>;
     case 3: return k_blk_grad_slices<1, 1, 2, 0>;
     default: return k_blk_grad_slices<0, 0, 0, 0>;
+  }
+}
+using ChainKernel = void (*)(BlkDev, int, int, const double*, const double2*, const double2*, double*,
+                             unsigned long long*);
+static ChainKernel chain_kernel(const BlkDev& D) {
+  switch (blk_role(D)) {
+    case 1: return k_blk_suffix_chain<3, 1, 5, 1>;
+    case 2: return k_blk_suffix_chain<2, 1, 4, 0>;
+    case 3: return k_blk_suffix_chain<1, 1, 2, 0>;
+    default: return k_blk_suffix_chain<0, 0, 0, 0>;
   }
 }
 static FwdKernel fwd_kernel(const BlkDev& D) {
@@ -1991,11 +2007,11 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
     BlkDev D;
     if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
     const size_t bytes = (size_t)grp_smem_doubles(D, per_chain) * 8;
-    static size_t attr = 0;
-    cudaError_t e = set_smem((const void*)k_blk_suffix_chain, bytes, attr);
+    const ChainKernel fn = chain_kernel(D);
+    cudaError_t e = set_smem_fn((const void*)fn, bytes);
     if (e != cudaSuccess) return e;
     prof_pre(ST_BLK_SUFFIX, st);
-    k_blk_suffix_chain<<<(batch + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(
+    fn<<<(batch + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(
         D, batch, N, U_img, V, Cseed, X_img, prof_counter(ST_BLK_SUFFIX));
     prof_post(ST_BLK_SUFFIX, st);
     ++launch_counter();
