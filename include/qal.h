@@ -283,7 +283,7 @@ int qal_fp64_peak_probe(int kind, int blocks, int iters, double *flops, double *
  * order q = m_a - m_b (d = 8: blocks 20/15/15/6/6/1/1).  Hermiticity preservation
  * (Lambda[s(R), s(C)] = conj(Lambda[R, C]), s(i + d j) = j + d i) pairs q with -q.
  * The path computes exactly the same Omega_k, U_k, Lambda, F and dF/du as the dense path,
- * restricted to the blocks (2.9% of the dense flops with the mirror).
+ * restricted to the blocks (2.13% of the dense flops with the mirror and the real q = 0 block).
  *
  * A PACKED matrix is the concatenation of the plan's super-block matrices (groups g of
  * padded width width[g] = 8, 16 or 24; each row-major complex128, entries on padding

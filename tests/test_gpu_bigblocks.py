@@ -110,3 +110,46 @@ def test_hubbard_structure_and_slice(torch_cuda, qal):
     assert flag.item() == 0
     _, D = qal.qal_magnus_expm_slices(L0, Lc, u.unsqueeze(0), p.T, p.N, chunk=p.N)
     assert relfro(P[0].cpu().numpy(), D[0, 0].cpu().numpy()) <= 1e-11
+
+
+# ---- direct oracle checks of the n = 4096 block path (no dense GPU path in between) ------------------
+
+def test_bigblock_dissipative_slices_vs_oracle_rk4_on_rho(torch_cuda, qal, oracle):
+    """configs[4] pulse 0, two dissipative slices on the coherence-block path, applied to random density
+    matrices vs the oracle's RK4 of Eq. 6 on rho (256 sub-steps per slice, RK4 error ~1e-13):
+    the packed blocks, the Hermitian mirror and the real basis of the q = 0 block all enter Lambda."""
+    torch = torch_cuda
+    N = 2
+    p = qi.cfg4(batch=1, N=N, T=100.0 * N / 512)
+    L0, Lc, _ = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C))
+    plan = qal.qal_bigblock_plan_build(torch.cat([L0, Lc]), mirror=True)
+    P, flag = qal.qal_bigblock_expm_slices(plan, L0, Lc, to(torch, p.u[0]), p.T, p.N)
+    assert flag.item() == 0
+    Lam = P[0]
+    rng = np.random.default_rng(19)
+    for _ in range(2):
+        a = rng.standard_normal((64, 64)) + 1j * rng.standard_normal((64, 64))
+        rho0 = a @ a.conj().T
+        rho0 /= np.trace(rho0)
+        ref = oracle.evolve_rho(p.H0[0], p.Hc, p.C, p.u[0], p.T, p.N, 256, rho0)
+        v = to(torch, rho0.reshape(-1, order="F").copy())
+        got = (Lam @ v).cpu().numpy().reshape(64, 64, order="F")
+        assert relfro(got, ref) <= 1e-10
+
+
+def test_bigblock_hubbard_dissipative_slice_vs_oracle_rk4_on_rho(torch_cuda, qal, oracle):
+    """NEXT f3 on the block path: one 3-dot Hubbard slice (||Omega||_1 ~ 25: per-block squarings) applied
+    to a logical-subspace density matrix vs the oracle's RK4 of Eq. 6 with 8192 sub-steps."""
+    torch = torch_cuda
+    p = qi.hubbard3(N=1, T=100.0 / 512)
+    L0, Lc, _ = qal.qal_build_liouvillian(to(torch, p.H0), to(torch, p.Hc), to(torch, p.C))
+    plan = qal.qal_bigblock_plan_build(torch.cat([L0, Lc]), mirror=True)
+    P, flag = qal.qal_bigblock_expm_slices(plan, L0, Lc, to(torch, p.u[0]), p.T, p.N)
+    assert flag.item() == 0
+    phis = qi.hubbard_logical_states()
+    rho0 = 0.7 * np.outer(phis[0], phis[0].conj()) + 0.3 * np.outer(phis[1], phis[1].conj())
+    rho0 += 0.2 * (np.outer(phis[0], phis[1].conj()) + np.outer(phis[1], phis[0].conj()))
+    ref = oracle.evolve_rho(p.H0[0], p.Hc, p.C, p.u[0], p.T, 1, 8192, rho0)
+    v = to(torch, rho0.reshape(-1, order="F").copy())
+    got = (P[0] @ v).cpu().numpy().reshape(64, 64, order="F")
+    assert relfro(got, ref) <= 1e-10

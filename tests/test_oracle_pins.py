@@ -327,6 +327,23 @@ def test_p7_pwc_matches_rk4(oracle):
     assert e2 < 1e-8 and 14 < e1 / e2 < 18
 
 
+def test_rk4_sinusoid_mode_matches_solve_ivp_and_is_order_4(oracle):
+    """O8 with continuous controls (cmode 2): the RK4 of Eq. 9 evaluating u(t) at every stage agrees
+    with an independent DOP853 integration of Eq. 6 (matrix form, tight tolerances), and halving its
+    step divides the error by ~16."""
+    p, C, prm = _smooth_case()
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, C)
+    T = 12.0
+    rho0 = rand_rho(np.random.default_rng(5), 8)
+    ref = _ivp_reference(p, C, prm, T, rho0, oracle)
+    errs = []
+    for sub in (32, 64):
+        Lam = oracle.rk4(L0, Lc, T, 8, sub, prm=prm, umax=qi.U_MAX)
+        errs.append(np.abs(unvec(Lam @ vec(rho0), 8) - ref).max())
+    assert errs[1] <= 3e-8, errs
+    assert 13.0 < errs[0] / errs[1] < 19.0, errs
+
+
 # ---------------------------------------------------------------- P-10 fidelity
 def test_p10_fidelity(oracle):
     V = qi.haar_unitary(8, 0)
@@ -535,6 +552,13 @@ def test_logical_loss_identity_swap_and_cotangent(oracle):
     Lsw = np.kron(W.conj(), W)
     loss, _ = oracle.logical_loss(Lsw, P, qi.LOGICAL_GATES["X"])
     assert loss < 1e-28
+    # normalisation (A22: 1/4 ||Pi - G||_F^2, "mean" over the 4 entries of the 2x2 matrices): Lambda = I
+    # gives Pi = P^dag P = I_2 exactly, so against G = X the residual is [[1, -1], [-1, 1]] with
+    # ||.||_F^2 = 4 -> loss = 1; against G = 0, ||I_2||_F^2 = 2 -> loss = 1/2
+    loss, _ = oracle.logical_loss(np.eye(64, dtype=np.complex128), P, qi.LOGICAL_GATES["X"])
+    assert abs(loss - 1.0) <= 1e-14
+    loss, _ = oracle.logical_loss(np.eye(64, dtype=np.complex128), P, np.zeros((2, 2), np.complex128))
+    assert abs(loss - 0.5) <= 1e-14
     # cotangent: d loss along E equals Re Tr(C E) (central difference)
     rng = np.random.default_rng(3)
     Lam = rand_c(rng, 64, 64) / 8.0
