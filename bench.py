@@ -544,6 +544,7 @@ def run_cfg4(args):
     ws = torch.empty(qal.workspace_bytes(qal.QAL_OP_EXPM_SLICES, n, 1, S), dtype=torch.uint8, device=dev)
     P = torch.empty((1, 1, n, n), dtype=torch.complex128, device=dev)
     F = torch.empty(1, dtype=torch.float64, device=dev)
+    fws = torch.empty(qal.workspace_bytes(qal.QAL_OP_FIDELITY_REDUCE, n, 1, 1), dtype=torch.uint8, device=dev)
     lib = qal.load()
     st = lambda: qal._stream(None)  # noqa: E731
 
@@ -564,7 +565,8 @@ def run_cfg4(args):
                                             qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
                                             ws.numel(), st())
             qal._check(rc, "qal_magnus_expm_slices")
-        qal._check(lib.qal_fidelity(64, 1, qal._ptr(P), qal._ptr(V), qal._ptr(F), st()), "qal_fidelity")
+        qal._check(lib.qal_fidelity_ws(64, 1, qal._ptr(P), qal._ptr(V), qal._ptr(F), qal._ptr(fws), fws.numel(), st()),
+                   "qal_fidelity_ws")
 
     for _ in range(args.warmup):
         step()

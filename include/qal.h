@@ -68,11 +68,12 @@ enum {                   /* op codes for qal_workspace_bytes */
     QAL_OP_FIDELITY = 2,      /* qal_fidelity_grad with grad == NULL */
     QAL_OP_FIDELITY_GRAD = 3, /* qal_fidelity_grad with grad != NULL */
     QAL_OP_EXPM_SLICES = 4,   /* qal_magnus_expm_slices (non-zero only for n = 4096) */
-    QAL_OP_VJP = 5            /* qal_propagator_forward + qal_propagator_vjp (n_slices = count) */
+    QAL_OP_VJP = 5,           /* qal_propagator_forward + qal_propagator_vjp (n_slices = count) */
+    QAL_OP_FIDELITY_REDUCE = 6 /* qal_fidelity_ws (n = 4096: 512 partial sums per pulse; n = 64: 0) */
 };
 
 #define QAL_MAX_CTRL 8
-#define QAL_ABI_VERSION 1
+#define QAL_ABI_VERSION 2
 
 int qal_abi_version(void);
 
@@ -179,11 +180,17 @@ int qal_batched_matmul(int n, int count, const qal_c128 *A, long long strideA, c
  * (the superoperator of rho -> V rho V^dag under column stacking).  S_V is never
  * formed: S_V[i+dj, k+dl] = conj(V[j][l]) V[i][k].  Fixed-order reduction.
  *   Lambda [batch][n][n], V [d][d], F [batch] (f64).
- * d = 64 with batch <= 64 reduces over 512 row slabs per pulse through a static device scratch:
- * such calls must not run concurrently on two streams.
+ * d = 64: one CTA per pulse reads the 268 MB matrix (no workspace; use qal_fidelity_ws for the
+ * bandwidth-bound form).  The library holds no device state, so calls on any streams are independent.
  */
 int qal_fidelity(int d, int batch, const qal_c128 *Lambda, const qal_c128 *V, double *F,
                  void *stream);
+
+/* qal_fidelity with a caller workspace: d = 64 reduces each pulse over 512 row slabs (512 CTAs per
+ * pulse, HBM bound) into ws, then sums the 512 partials in a fixed order.
+ * ws >= qal_workspace_bytes(QAL_OP_FIDELITY_REDUCE, n, batch, 1, 0, 0) (0 for d = 8). */
+int qal_fidelity_ws(int d, int batch, const qal_c128 *Lambda, const qal_c128 *V, double *F, void *ws,
+                    size_t ws_bytes, void *stream);
 
 /*
  * Control table of configs[3] (a1, NODES mode; A11): the smooth random controls
@@ -326,7 +333,17 @@ typedef struct {
                                            2 pair representative R < s(R), 3 pair mirror      */
     int cplx_mults;                     /* real multiplications per complex block product the
                                            library executes (4, or 3 with the Gauss form)     */
+    int launch_sets;                    /* launch layout of the forward, suffix-chain and
+                                           gradient kernels (caller option, set after
+                                           qal_block_plan_build; QAL_BLK_SETS_*): results are
+                                           identical (gradient: up to the trace-sum order)     */
 } qal_block_plan;
+
+enum {
+    QAL_BLK_SETS_DEFAULT = 0,  /* one launch per group, several items per CTA (role-compiled kernels) */
+    QAL_BLK_SETS_FUSED = 1,    /* one launch, every group of one item per CTA                         */
+    QAL_BLK_SETS_PAIRS = 2     /* one launch per group, two items per CTA                             */
+};
 
 /*
  * Structure detection (host only, no device work): the connected components of the union
@@ -345,6 +362,18 @@ int qal_block_plan_build(int n, int nmat, const qal_c128 *mats, int mirror, qal_
  */
 int qal_block_pack(const qal_block_plan *plan, int count, const qal_c128 *nat, qal_c128 *packed, int *flag,
                    void *stream);
+
+/*
+ * The device structure check of qal_block_pack reported per pulse, for a caller that runs it after the
+ * block calls of a step (those reset `status` on entry): every entry of nat[e] ([count][n][n], device)
+ * coupling two components of the plan must be exactly zero (A26; Eq. 8 conserves the coherence order
+ * only if every operator of Eq. 6 conserves S_z).  A failing matrix e sets status[e] = QAL_ERR_STRUCTURE
+ * (broadcast = 0: one matrix per pulse, nstatus == count, e.g. L0_b), or every status[0 .. nstatus)
+ * (broadcast = 1: a basis matrix shared by all pulses, e.g. L_j).  Entries of passing matrices are left
+ * as they are.  The F / gradient of a flagged pulse are not meaningful.
+ */
+int qal_block_check(const qal_block_plan *plan, int count, const qal_c128 *nat, int broadcast, int *status,
+                    int nstatus, void *stream);
 
 /* packed -> natural [count][n][n]; blocks of mirrored components are filled from their stored
  * partner by Lambda[s(R), s(C)] = conj(Lambda[R, C]); entries between components are 0. */
@@ -440,10 +469,13 @@ typedef struct {
 } qal_bigblock_plan;
 
 /* Structure detection for n = 4096: the union non-zero pattern of the DEVICE matrices
- * mats[nmat][4096][4096] is computed on the device (a 2 MB temporary, allocated and freed
- * stream-ordered: a setup call), its connected components and Hermitian mirror pairing on the host
- * (synchronises `stream`).  QAL_ERR_UNSUPPORTED beyond 48 stored blocks. */
-int qal_bigblock_plan_build(int nmat, const qal_c128 *mats, int mirror, qal_bigblock_plan *plan, void *stream);
+ * mats[nmat][4096][4096] is computed on the device into the caller's workspace (a 2 MB bitmask,
+ * ws_bytes >= qal_bigblock_plan_workspace_bytes()), its connected components and Hermitian mirror
+ * pairing on the host (a setup call: synchronises `stream`).  The library allocates nothing.
+ * QAL_ERR_UNSUPPORTED beyond 48 stored blocks. */
+size_t qal_bigblock_plan_workspace_bytes(void);
+int qal_bigblock_plan_build(int nmat, const qal_c128 *mats, int mirror, qal_bigblock_plan *plan, void *ws,
+                            size_t ws_bytes, void *stream);
 
 /*
  * Device workspace of qal_bigblock_expm_slices: six tiled-block matrices per slice of a batch (slices

@@ -15,8 +15,23 @@ FLAGS = [*os.environ.get("QAL_NVCC_EXTRA", "").split(), "-gencode", "arch=comput
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
+STAMP = os.path.join(HERE, "build", "flags.txt")
+
+
+def _flags_text() -> str:
+    """Everything that decides what libqal.so contains besides the sources: compiler and flag list
+    (including QAL_NVCC_EXTRA experiment flags)."""
+    return "\n".join([NVCC, *FLAGS, *SOURCES]) + "\n"
+
+
 def _stale() -> bool:
     if not os.path.exists(OUT):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read() != _flags_text():   # built with other flags (e.g. an experiment build)
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(OUT)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
@@ -49,6 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = OUT + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-o", tmp, *objs, "-lcudart"])
     os.replace(tmp, OUT)
+    with open(STAMP, "w") as f:
+        f.write(_flags_text())
     return OUT
 
 

@@ -2,6 +2,7 @@
 // validation, then kernel launches on the caller's stream.  No allocation.
 #include <cmath>
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "../../include/qal.h"
@@ -21,6 +22,36 @@ int num_sms() {
     cached[dev] = v > 0 ? v : 1;
   }
   return cached[dev];
+}
+
+// dynamic shared-memory opt-in (and the all-shared carveout) of a kernel, once per (device, kernel):
+// the attribute is per device, so a process driving several GPUs sets it on each; callers on several
+// host threads are serialised here.  Raising the size later re-applies the attribute.
+cudaError_t ensure_smem(const void* fn, size_t bytes) {
+  struct Rec {
+    int dev;
+    const void* fn;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Rec> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (Rec& r : done)
+    if (r.dev == dev && r.fn == fn) {
+      if (bytes <= r.bytes) return cudaSuccess;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e == cudaSuccess) r.bytes = bytes;
+      return e;
+    }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  done.push_back({dev, fn, bytes});
+  return cudaSuccess;
 }
 
 int& launch_counter() {
@@ -168,6 +199,7 @@ int check_plan(const qal_block_plan* p) {
   if (!p) return QAL_ERR_NULL;
   if (p->n != 64 || p->d != 8 || p->ngroups < 1 || p->ngroups > QAL_BLK_MAX_GROUPS) return QAL_ERR_UNSUPPORTED;
   if (p->nrows < 8 || p->nrows > QAL_BLK_MAX_ROWS || p->nrows % 8) return QAL_ERR_DIM;
+  if (p->launch_sets < QAL_BLK_SETS_DEFAULT || p->launch_sets > QAL_BLK_SETS_PAIRS) return QAL_ERR_UNSUPPORTED;
   int row = 0, off = 0;
   for (int g = 0; g < p->ngroups; ++g) {
     const int w = p->width[g];
@@ -363,7 +395,8 @@ size_t qal_workspace_bytes(int op, int n, int batch, int n_slices, int n_ctrl, i
     switch (op) {
       case QAL_OP_EXPM_SLICES: return dense_expm_ws_bytes();
       case QAL_OP_ORDERED_PRODUCT: return dense_tree_ws_bytes(batch, n_slices);
-      case QAL_OP_FIDELITY: return dense_expm_ws_bytes() + (size_t)batch * BIG_BYTES;
+      case QAL_OP_FIDELITY: return dense_expm_ws_bytes() + (size_t)batch * (BIG_BYTES + DENSE_FID_PART_BYTES);
+      case QAL_OP_FIDELITY_REDUCE: return (size_t)batch * DENSE_FID_PART_BYTES;
       default: return 0;
     }
   }
@@ -489,8 +522,19 @@ int qal_fidelity(int d, int batch, const qal_c128* Lambda, const qal_c128* V, do
   if (d != 8 && d != 64) return QAL_ERR_UNSUPPORTED;
   if (batch < 1) return QAL_ERR_EMPTY;
   if (!Lambda || !V || !F) return QAL_ERR_NULL;
-  if (d == 64) return cuda_rc(launch_dense_fidelity(batch, D2(Lambda), D2(V), F, S(stream)));
+  if (d == 64) return cuda_rc(launch_dense_fidelity(batch, D2(Lambda), D2(V), F, nullptr, S(stream)));
   return cuda_rc(launch_fidelity(batch, D2(Lambda), D2(V), F, S(stream)));
+}
+
+int qal_fidelity_ws(int d, int batch, const qal_c128* Lambda, const qal_c128* V, double* F, void* ws,
+                    size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  if (d != 8 && d != 64) return QAL_ERR_UNSUPPORTED;
+  if (batch < 1) return QAL_ERR_EMPTY;
+  if (!Lambda || !V || !F) return QAL_ERR_NULL;
+  if (d == 8) return cuda_rc(launch_fidelity(batch, D2(Lambda), D2(V), F, S(stream)));
+  if (!ws || ws_bytes < qal_workspace_bytes(QAL_OP_FIDELITY_REDUCE, 4096, batch, 1, 0, 0)) return QAL_ERR_WORKSPACE;
+  return cuda_rc(launch_dense_fidelity(batch, D2(Lambda), D2(V), F, reinterpret_cast<double*>(ws), S(stream)));
 }
 
 int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order, int ctrl_mode, int n_ctrl,
@@ -517,7 +561,9 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
                                  st) != cudaSuccess)
         return QAL_ERR_CUDA;
     }
-    return cuda_rc(launch_dense_fidelity(batch, lam, D2(V), F, st));
+    double* part = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + dense_expm_ws_bytes() +
+                                             (size_t)batch * BIG_BYTES);
+    return cuda_rc(launch_dense_fidelity(batch, lam, D2(V), F, part, st));
   }
   const size_t need = qal_workspace_bytes(grad ? QAL_OP_FIDELITY_GRAD : QAL_OP_FIDELITY, 64, batch, n_slices,
                                           n_ctrl, ctrl_mode);
@@ -678,6 +724,17 @@ int qal_block_pack(const qal_block_plan* plan, int count, const qal_c128* nat, q
   return cuda_rc(launch_blk_pack(*plan, count, D2(nat), D2(packed), flag, S(stream)));
 }
 
+int qal_block_check(const qal_block_plan* plan, int count, const qal_c128* nat, int broadcast, int* status,
+                    int nstatus, void* stream) {
+  launch_counter() = 0;
+  int rc = check_plan(plan);
+  if (rc != QAL_OK) return rc;
+  if (count < 1 || nstatus < 1) return QAL_ERR_EMPTY;
+  if (!nat || !status) return QAL_ERR_NULL;
+  if (!broadcast && nstatus != count) return QAL_ERR_DIM;
+  return cuda_rc(launch_blk_check_status(*plan, count, D2(nat), broadcast ? 1 : 0, status, nstatus, S(stream)));
+}
+
 int qal_block_unpack(const qal_block_plan* plan, int count, const qal_c128* packed, qal_c128* nat, void* stream) {
   launch_counter() = 0;
   int rc = check_plan(plan);
@@ -831,11 +888,15 @@ int qal_block_fidelity_cotangent(const qal_block_plan* plan, const qal_c128* V, 
   return cuda_rc(launch_blk_fidelity_cotangent(*plan, D2(V), D2(C), S(stream)));
 }
 
-int qal_bigblock_plan_build(int nmat, const qal_c128* mats, int mirror, qal_bigblock_plan* plan, void* stream) {
+size_t qal_bigblock_plan_workspace_bytes(void) { return bb_plan_ws_bytes(); }
+
+int qal_bigblock_plan_build(int nmat, const qal_c128* mats, int mirror, qal_bigblock_plan* plan, void* ws,
+                            size_t ws_bytes, void* stream) {
   launch_counter() = 0;
   if (!mats || !plan) return QAL_ERR_NULL;
   if (nmat < 1) return QAL_ERR_EMPTY;
-  return build_bigblock_plan(nmat, D2(mats), mirror, plan, S(stream));
+  if (!ws || ws_bytes < bb_plan_ws_bytes()) return QAL_ERR_WORKSPACE;
+  return build_bigblock_plan(nmat, D2(mats), mirror, plan, ws, S(stream));
 }
 
 size_t qal_bigblock_workspace_bytes(const qal_bigblock_plan* plan) {

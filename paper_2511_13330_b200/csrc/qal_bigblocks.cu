@@ -648,15 +648,17 @@ static cudaError_t bb_dev(const qal_bigblock_plan& p, int* tab, BBDev& D, cudaSt
   return e;
 }
 
-int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_plan* out, cudaStream_t st) {
-  // non-zero pattern on the device (2 MB), components on the host
-  unsigned long long* dmask = nullptr;
-  if (cudaMallocAsync(&dmask, (size_t)BBN * BBW * 8, st) != cudaSuccess) return QAL_ERR_CUDA;
+size_t bb_plan_ws_bytes() { return (size_t)BBN * BBW * 8; }
+
+int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_plan* out, void* ws, cudaStream_t st) {
+  // non-zero pattern on the device (2 MB bitmask in the caller's workspace), components on the host
+  unsigned long long* dmask = reinterpret_cast<unsigned long long*>(ws);
   k_bb_nzmask<<<BBN, BBW, 0, st>>>(nmat, mats, dmask);
+  ++launch_counter();
   std::vector<unsigned long long> mask((size_t)BBN * BBW);
-  cudaError_t e = cudaMemcpyAsync(mask.data(), dmask, mask.size() * 8, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mask.data(), dmask, mask.size() * 8, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFreeAsync(dmask, st);
   if (e != cudaSuccess) return QAL_ERR_CUDA;
   std::vector<int> par(BBN);
   for (int i = 0; i < BBN; ++i) par[i] = i;
@@ -765,11 +767,9 @@ static cudaError_t bb_gemm(const BBDev& D, const BBGemm& g0, const qal_bigblock_
   if (g.nbatch < 1) g.nbatch = 1;
   g.ctr = prof_counter(ST_BLK_GEMM);
   for (int b = 0; b < p.nb; ++b) g.bflops[b] = (unsigned long long)p.flops[b];
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_bb_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, BB_GEMM_SMEM);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_bb_gemm, BB_GEMM_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   prof_pre(ST_BLK_GEMM, st);
   k_bb_gemm<<<num_sms(), NT, BB_GEMM_SMEM, st>>>(D, g);

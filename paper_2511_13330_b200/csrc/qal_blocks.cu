@@ -141,12 +141,10 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
   }
   // rows per warp of every group: R = 1 (C warps on one block, named barrier) or R = C (one warp owns
   // the whole block).  Choose the split that minimises the largest per-warp DMMA count per product
-  // (real groups issue 1 MMA per step, complex 4), ties -> fewer warps.  QAL_BLK_SPLIT (bit g = split
-  // group g) overrides, for experiments.
+  // (real groups issue 1 MMA per step, complex 4), ties -> fewer warps.  -DQAL_BLK_SPLIT_MASK=m (bit g =
+  // split group g) overrides, for experiment builds only (no run-time knobs in the library).
   auto cost = [&](int g, int R) { return D.C[g] * R * D.ks[g] * (D.real[g] ? 1 : BLK_CPLX_MMAS); };
   int best_mask = -1, best_max = 1 << 30, best_w = 1 << 30;
-  const char* env = getenv("QAL_BLK_SPLIT");
-  if (env && !*env) env = nullptr;
   for (int mask = 0; mask < (1 << p.ngroups); ++mask) {
     int mx = 0, nw = 0;
     bool ok = true;
@@ -158,10 +156,10 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
       nw += split ? D.C[g] : 1;
     }
     if (!ok || nw * nslot > (nslot == 1 ? BLK_FUSED_WARPS : BLK_MAX_WARPS)) continue;
-    if (env) {
-      if (mask == atoi(env)) { best_mask = mask; best_max = mx; best_w = nw; }
-      continue;
-    }
+#ifdef QAL_BLK_SPLIT_MASK
+    if (mask == QAL_BLK_SPLIT_MASK) { best_mask = mask; best_max = mx; best_w = nw; }
+    continue;
+#endif
     if (mx < best_max || (mx == best_max && nw < best_w)) { best_mask = mask; best_max = mx; best_w = nw; }
   }
   if (best_mask < 0) return false;
@@ -1116,6 +1114,29 @@ __global__ void k_blk_check(BlkDev D, int count, const double2* __restrict__ nat
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = QAL_ERR_STRUCTURE;
 }
 
+// the same check, reported per pulse: matrix e couples two components -> status[e] = QAL_ERR_STRUCTURE
+// (broadcast = 0: one matrix per pulse, e.g. L0_b), or every status[0 .. nstatus) (broadcast = 1: a
+// basis matrix shared by all pulses, e.g. L_j).  Only ever writes QAL_ERR_STRUCTURE (idempotent).
+__global__ void k_blk_check_status(BlkDev D, int count, const double2* __restrict__ nat, int broadcast,
+                                   int* __restrict__ status, int nstatus) {
+  const int e = blockIdx.y;
+  const double2* src = nat + (size_t)e * 4096;
+  int bad = 0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 4096; idx += gridDim.x * blockDim.x) {
+    const int R = idx >> 6, Cc = idx & 63;
+    if (D.comp[R] != D.comp[Cc]) {
+      const double2 v = src[idx];
+      if (v.x != 0.0 || v.y != 0.0) bad = 1;
+    }
+  }
+  if (!__syncthreads_or(bad)) return;
+  if (!broadcast) {
+    if (threadIdx.x == 0) status[e] = QAL_ERR_STRUCTURE;
+  } else {
+    for (int i = threadIdx.x; i < nstatus; i += blockDim.x) status[i] = QAL_ERR_STRUCTURE;
+  }
+}
+
 // natural from packed: stored component -> value; mirrored component -> conj of the stored
 // mirror entry (Lambda[s(R), s(C)] = conj(Lambda[R, C]), s(i + d j) = j + d i); else 0.
 __global__ void k_blk_unpack(BlkDev D, int count, const double2* __restrict__ packed, double2* __restrict__ nat) {
@@ -1821,49 +1842,39 @@ static int blk_group_warps(const qal_block_plan& p, int g) {
   BlkDev D;
   return to_dev(p, D, 1u << g, 1) ? D.nwarps : 0;
 }
-// kind 0 forward, 1 gradient: one set per group, slots 4 / warps (4 for 3-warp groups); kind 2 suffix
-// chain: one set per group, 4 pulses per CTA.  env (experiments) QAL_BLK_SETS_FWD / _GRAD / _CHAIN =
-// "mask:slots,..." must cover every group exactly once, else it is ignored.
+// kind 0 forward, 1 gradient, 2 suffix chain.  plan.launch_sets (an explicit option of the caller-owned
+// plan, no run-time environment knobs): QAL_BLK_SETS_DEFAULT -- one set per group, slots 4 / warps for the
+// forward and gradient (4 for 3-warp groups), 4 pulses per CTA for the suffix chain;
+// QAL_BLK_SETS_FUSED -- one set of every group, one item per CTA; QAL_BLK_SETS_PAIRS -- one set per
+// group with 2 slots (a cross-check of the slot machinery).  Validated by check_plan (qal_api.cu).
 static void blk_sets(const qal_block_plan& p, int kind, std::vector<BlkSet>& sets) {
   sets.clear();
   const unsigned all = (1u << p.ngroups) - 1;
-  const char* env = getenv(kind == 0 ? "QAL_BLK_SETS_FWD" : kind == 1 ? "QAL_BLK_SETS_GRAD" : "QAL_BLK_SETS_CHAIN");
-  if (env && *env) {
-    unsigned seen = 0;
-    bool ok = true;
-    const char* c = env;
-    while (*c && ok) {
-      char* e1;
-      const long m = strtol(c, &e1, 0);
-      int sl = 1;
-      if (*e1 == ':') sl = (int)strtol(e1 + 1, &e1, 0);
-      ok = m > 0 && ((unsigned)m & ~all) == 0 && ((unsigned)m & seen) == 0 && e1 != c;
-      seen |= (unsigned)m;
-      sets.push_back({(unsigned)m, sl});
-      c = (*e1 == ',') ? e1 + 1 : e1;
-      if (*c && *e1 != ',') ok = false;
-    }
-    if (ok && seen == all) return;
-    sets.clear();
-  }
-  if (kind == 2) {   // suffix chain: one launch per group, 4 pulses per CTA (role kernels: 56 registers)
-    for (int g = 0; g < p.ngroups; ++g) sets.push_back({1u << g, 4});
+  if (p.launch_sets == QAL_BLK_SETS_FUSED) {
+    sets.push_back({all, 1});
     return;
   }
   for (int g = 0; g < p.ngroups; ++g) {
-    const int w = blk_group_warps(p, g);
-    sets.push_back({1u << g, (w == 3 || w == 1) ? 4 : (w == 2 ? 2 : 1)});
+    int sl;
+    if (p.launch_sets == QAL_BLK_SETS_PAIRS) sl = 2;
+    else if (kind == 2) sl = 4;   // suffix chain: one launch per group, 4 pulses per CTA (role kernels: 56 registers)
+    else {
+      const int w = blk_group_warps(p, g);
+      sl = (w == 3 || w == 1) ? 4 : (w == 2 ? 2 : 1);
+    }
+    sets.push_back({1u << g, sl});
   }
 }
 
 // ------------------------------------------------------------------ role-specialised kernels
 // The d = 8 roles (mirror plan): the real 20-block on 3 warps (3, 1, 5, real), the 15+1 block on 2
 // warps (2, 1, 4), the 6-block on one warp (1, 1, 2).  A launch whose warps all run one of them uses
-// the kernel compiled for it alone; anything else the dispatching kernel.  QAL_BLK_SPEC=0: always the
-// dispatching kernel (experiments).
+// the kernel compiled for it alone; anything else the dispatching kernel (-DQAL_BLK_NO_SPEC: always the
+// dispatching kernel, experiment builds only).
 static int blk_role(const BlkDev& D) {
-  const char* env = getenv("QAL_BLK_SPEC");
-  if (env && env[0] == '0') return 0;
+#ifdef QAL_BLK_NO_SPEC
+  return 0;
+#endif
   int key = -1;
   for (int w = 0; w < D.nwarps; ++w) {
     if (D.ntask[w] != 1) return 0;
@@ -1908,26 +1919,7 @@ static FwdKernel fwd_kernel(const BlkDev& D) {
     default: return k_blk_expm_fold<0, 0, 0, 0>;
   }
 }
-// dynamic shared-memory opt-in per kernel function (several kernels share one launcher; callers on
-// several host threads are serialised here)
-static cudaError_t set_smem_fn(const void* fn, size_t bytes) {
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  static std::vector<std::pair<const void*, size_t>> done;
-  for (auto& d : done)
-    if (d.first == fn) {
-      if (bytes <= d.second) return cudaSuccess;
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (e == cudaSuccess) d.second = bytes;
-      return e;
-    }
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return e;
-  done.push_back({fn, bytes});
-  return cudaSuccess;
-}
+static cudaError_t set_smem_fn(const void* fn, size_t bytes) { return ensure_smem(fn, bytes); }
 
 // ------------------------------------------------------------------ launchers
 namespace {
@@ -1948,17 +1940,6 @@ int per_grad(int C, bool re) { return grp3_doubles(C, re) + 4 * img_doubles(C, r
 int per_pair(int C, bool re) { return img_doubles(C, re); }
 int per_chain(int C, bool re) { return 2 * img_doubles(C, re); }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
-cudaError_t set_smem(const void* fn, size_t bytes, size_t& attr) {
-  if (bytes > attr) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    // all of the unified L1 / shared capacity as shared memory: several CTAs per SM
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    attr = bytes;
-  }
-  return cudaSuccess;
-}
 }  // namespace
 
 cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
@@ -2037,7 +2018,6 @@ static int blk_grad_grid(const BlkDev& D, GradKernel fn = nullptr) {
     const int by_smem = (int)(233472 / (bytes + fa.sharedSizeBytes + 1024));
     per_sm = std::min(std::min(by_regs, by_smem), std::min(8, 512 / tmem_cols_for(D)));
   }
-  if (getenv("QAL_DEBUG")) fprintf(stderr, "blk_grad_grid: nwarps %d smem %zu per_sm %d\n", D.nwarps, bytes, per_sm);
   return std::max(1, per_sm) * num_sms();
 }
 
@@ -2154,6 +2134,15 @@ cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* n
     ++launch_counter();
   }
   k_blk_pack<<<grid, 256, 0, st>>>(D, count, nat, packed);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_check_status(const qal_block_plan& p, int count, const double2* nat, int broadcast, int* status,
+                                   int nstatus, cudaStream_t st) {
+  BlkDev D;
+  if (!to_dev(p, D)) return cudaErrorInvalidValue;
+  k_blk_check_status<<<dim3(4, count), 256, 0, st>>>(D, count, nat, broadcast, status, nstatus);
   ++launch_counter();
   return cudaGetLastError();
 }

@@ -372,11 +372,9 @@ size_t dense_expm_ws_bytes() { return 8 * DIMG * 8 + (size_t)NTD * 4096 * 8 + 25
 static cudaError_t gemm(const GemmArgs& g0, cudaStream_t st) {
   GemmArgs g = g0;
   g.ctr = prof_counter(ST_DENSE_GEMM);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_dense_gemm, GEMM_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   prof_pre(ST_DENSE_GEMM, st);
   k_dense_gemm<<<num_sms(), NT, GEMM_SMEM, st>>>(g);
@@ -498,11 +496,9 @@ cudaError_t launch_dense_tree_pair(const double2* Alater, const double2* Bearlie
 
 cudaError_t launch_dense_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops,
                                      const double2* C, double2* L0, double2* Lc, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_liouv, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_dense_liouv, 4096 * 16);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   prof_pre(ST_LIOUV, st);
   k_dense_liouv<<<dim3(64, 1, batch), NT, 4096 * 16, st>>>(H0, Hc, ncops, C, L0, Lc, 0);
@@ -514,10 +510,6 @@ cudaError_t launch_dense_liouvillian(int batch, const double2* H0, int J, const 
   ++launch_counter();
   return cudaGetLastError();
 }
-
-// static scratch of the n = 4096 fidelity: calls that run concurrently on different streams must not
-// both use it (the library's n = 4096 path is one pulse per call on one stream)
-__device__ double g_fid_part[64 * 512];
 
 // fidelity over 512 row slabs of 8 rows per pulse (HBM-bound: 268 MB per pulse), then a fixed-order sum
 __global__ void __launch_bounds__(NT) k_dense_fid_slab(const double2* __restrict__ Lam, const double2* __restrict__ V,
@@ -545,12 +537,13 @@ __global__ void __launch_bounds__(32) k_dense_fid_sum(const double* __restrict__
   F[blockIdx.x] = s / 4096.0;
 }
 
-cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st) {
+// part: caller workspace of 512 doubles per pulse (the slab partials) or nullptr: then one CTA per
+// pulse reads the whole matrix (no scratch, slower).  The library keeps no state of its own, so calls on
+// different streams are independent.
+cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, double* part,
+                                  cudaStream_t st) {
   prof_pre(ST_FID, st);
-  if (batch <= 64) {
-    double* part = nullptr;   // 512 partials per pulse in the module's static scratch (no allocation)
-    cudaError_t e = cudaGetSymbolAddress(reinterpret_cast<void**>(&part), g_fid_part);
-    if (e != cudaSuccess) return e;
+  if (part) {
     k_dense_fid_slab<<<dim3(512, batch), NT, 0, st>>>(Lam, V, part);
     k_dense_fid_sum<<<batch, 32, 0, st>>>(part, F);
     launch_counter() += 2;

@@ -420,11 +420,9 @@ size_t grad_scratch_bytes() { return (size_t)num_sms() * GRAD_SCRATCH_STRIPS * M
 
 cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P_img, double2* Lam,
                                 const double2* P_init, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_prefix_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, CHAIN_SMEM_BYTES);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_prefix_chain, CHAIN_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   prof_pre(ST_PREFIX, st);
   k_prefix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, P_img, Lam, P_init, prof_counter(ST_PREFIX));
@@ -435,11 +433,9 @@ cudaError_t launch_prefix_chain(int batch, int N, const double* U_img, double* P
 
 cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const double2* V, const double2* Cseed,
                                 double* X_img, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_suffix_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, CHAIN_SMEM_BYTES);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_suffix_chain, CHAIN_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   prof_pre(ST_SUFFIX, st);
   k_suffix_chain<<<batch, NT, CHAIN_SMEM_BYTES, st>>>(N, U_img, V, Cseed, X_img, prof_counter(ST_SUFFIX));
@@ -451,11 +447,9 @@ cudaError_t launch_suffix_chain(int batch, int N, const double* U_img, const dou
 cudaError_t launch_grad_slices(int batch, const Basis& B, const SliceGrid& G, const double* P_img,
                                const double* X_img, double* grad, int* status, double* scratch, double gscale,
                                cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_grad_slices, cudaFuncAttributeMaxDynamicSharedMemorySize, GRAD_SMEM_BYTES);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_grad_slices, GRAD_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int items = batch * G.count;
   const int grid = items < num_sms() ? items : num_sms();

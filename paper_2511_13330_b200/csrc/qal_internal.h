@@ -62,6 +62,8 @@ cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, c
                                   cudaStream_t st);
 cudaError_t launch_blk_pack(const qal_block_plan& p, int count, const double2* nat, double2* packed, int* flag,
                             cudaStream_t st);
+cudaError_t launch_blk_check_status(const qal_block_plan& p, int count, const double2* nat, int broadcast, int* status,
+                                   int nstatus, cudaStream_t st);
 cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2* packed, double2* nat,
                               cudaStream_t st);
 cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
@@ -79,7 +81,8 @@ cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double
                                 cudaStream_t st);
 
 // coherence blocks on the n = 4096 path (qal_bigblocks.cu)
-int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_plan* out, cudaStream_t st);
+size_t bb_plan_ws_bytes();
+int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_plan* out, void* ws, cudaStream_t st);
 size_t bb_ws_bytes(const qal_bigblock_plan& p);
 cudaError_t launch_bb_expm_fold(const qal_bigblock_plan& p, const double2* L0, const double2* Lc, int J,
                                 const double* u, int count, double h, int chunk, double2* chunk_nat, int* status,
@@ -87,6 +90,8 @@ cudaError_t launch_bb_expm_fold(const qal_bigblock_plan& p, const double2* L0, c
 
 int num_sms();
 int& launch_counter();
+// per-(device, kernel) dynamic shared-memory opt-in (qal_api.cu)
+cudaError_t ensure_smem(const void* fn, size_t bytes);
 
 // profiling window (qal_profile_begin/end): stage ids as in qal.h
 enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, ST_DENSE_GEMM,
@@ -133,7 +138,9 @@ cudaError_t launch_dense_tree_pair(const double2* Alater, const double2* Bearlie
                                    cudaStream_t st);
 cudaError_t launch_dense_liouvillian(int batch, const double2* H0, int J, const double2* Hc, int ncops,
                                      const double2* C, double2* L0, double2* Lc, cudaStream_t st);
-cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, cudaStream_t st);
+cudaError_t launch_dense_fidelity(int batch, const double2* Lam, const double2* V, double* F, double* part,
+                                  cudaStream_t st);
+constexpr size_t DENSE_FID_PART_BYTES = 512 * sizeof(double);   // per pulse (n = 4096 slab partials)
 cudaError_t launch_fp64_probe(int kind, int blocks, int iters, double* sink, cudaStream_t st);
 
 }  // namespace qal

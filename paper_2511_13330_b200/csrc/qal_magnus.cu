@@ -177,11 +177,9 @@ __global__ void __launch_bounds__(NT, 1) k_expm_fold(int batch, Basis B, SliceGr
 }
 
 cudaError_t launch_expm_fold(int batch, const Basis& B, const SliceGrid& G, const FwdOut& O, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_expm_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM_BYTES);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_expm_fold, FWD_SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int items = batch * (G.count / O.chunk);
   const int grid = items < num_sms() ? items : num_sms();

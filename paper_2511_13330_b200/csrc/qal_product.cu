@@ -31,11 +31,9 @@ __global__ void __launch_bounds__(NT, 2) k_tree_level(int batch, int cnt, const 
 }
 
 cudaError_t launch_tree_level(int batch, int cnt, const double2* in, double2* out, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_tree_level, cudaFuncAttributeMaxDynamicSharedMemorySize, IMG * 8);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_tree_level, IMG * 8);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int half = (cnt + 1) / 2;
   prof_pre(ST_TREE, st);
@@ -90,11 +88,9 @@ __global__ void __launch_bounds__(NT) k_scan_shift(int cnt, const double2* __res
 
 cudaError_t launch_scan(int batch, int cnt, const double2* U, double2* pre, double2* suf, double2* ws,
                         cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan_level, cudaFuncAttributeMaxDynamicSharedMemorySize, IMG * 8);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_scan_level, IMG * 8);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const size_t seq = (size_t)batch * cnt * PLANE;
   double2* buf[2][2] = {{ws, ws + seq}, {ws + 2 * seq, ws + 3 * seq}};   // [dir][ping-pong]
@@ -137,11 +133,9 @@ __global__ void __launch_bounds__(NT, 2) k_batched_mm(const double2* __restrict_
 
 cudaError_t launch_batched_mm(int count, const double2* A, long long sa, const double2* B, long long sb, double2* C,
                               cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_batched_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, IMG * 8);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_batched_mm, IMG * 8);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   prof_pre(ST_TREE, st);
   k_batched_mm<<<count, NT, IMG * 8, st>>>(A, sa, B, sb, C, prof_counter(ST_TREE));
@@ -300,11 +294,9 @@ __global__ void __launch_bounds__(NT, 1) k_commutators(int J, const double2* __r
 
 cudaError_t launch_commutators(int batch, int J, const double2* L0, const double2* Lc, double2* Lcomm,
                                cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_commutators, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * IMG * 8);
+  {
+    const cudaError_t e = ensure_smem((const void*)k_commutators, 2 * IMG * 8);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int ncomm = J + J * (J - 1) / 2;
   prof_pre(ST_COMM, st);

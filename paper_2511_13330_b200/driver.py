@@ -61,12 +61,12 @@ class PulseBatch:
             self.ws_bytes = qal.workspace_bytes(op, self.n, self.sub, self.N, self.J, 0)
         else:
             # coherence-block path: the plan is detected once from the generator
-            # basis of pulse 0 (the device structure check re-verifies every pulse on every step)
+            # basis of pulse 0; every step re-verifies every pulse on the device and reports a pulse whose
+            # L0_b (or the shared L_j) couples two blocks as QAL_ERR_STRUCTURE in status[b]
             self._build_basis()
             self.plan = qal.qal_block_plan_build(torch.cat([self.L0[:1], self.Lc]), mirror=True)
             self.L0p = torch.empty((self.B, self.plan.packed), dtype=C128, device=dev)
             self.Lcp = torch.empty((self.J, self.plan.packed), dtype=C128, device=dev)
-            self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
             if sub_batch is None:
                 # image workspace (3 packed images per slice) within ~80 GB of HBM (at most 45% of the
                 # device, so a dense reference run fits beside it), in whole waves of the one-item-per-
@@ -120,7 +120,7 @@ class PulseBatch:
     def _step_blocks(self, lib, st, launches):
         pl = ctypes.byref(self.plan)
         for src, dst in ((self.L0, self.L0p), (self.Lc, self.Lcp)):
-            qal._check(lib.qal_block_pack(pl, src.shape[0], _p(src), _p(dst), _p(self.flag), st), "qal_block_pack")
+            qal._check(lib.qal_block_pack(pl, src.shape[0], _p(src), _p(dst), None, st), "qal_block_pack")
             launches += lib.qal_last_launch_count()
         P = self.plan.packed
         for b0 in range(0, self.B, self.sub):
@@ -134,12 +134,20 @@ class PulseBatch:
                 None, ctypes.c_void_p(self.status.data_ptr() + b0 * 4), _p(self.ws), self.ws_bytes, st)
             qal._check(rc, "qal_block_fidelity_grad")
             launches += lib.qal_last_launch_count()
+        # the structure check of this step's operators, per pulse (after the calls above, which reset
+        # their status slices on entry): L0_b -> status[b]; a shared L_j -> every pulse
+        qal._check(lib.qal_block_check(pl, self.B, _p(self.L0), 0, _p(self.status), self.B, st), "qal_block_check")
+        if self.J > 0:
+            qal._check(lib.qal_block_check(pl, self.J, _p(self.Lc), 1, _p(self.status), self.B, st),
+                       "qal_block_check")
+        launches += 1 + (self.J > 0)
         self.launches = launches
         return self.F, self.grad
 
     def structure_ok(self) -> bool:
-        """False if the device check found an operator coupling two blocks of the plan (synchronises)."""
-        return self.structure == "dense" or int(self.flag.item()) == 0
+        """False if the last step's device check found an operator coupling two blocks of the plan
+        (those pulses carry QAL_ERR_STRUCTURE in `status`; synchronises)."""
+        return self.structure == "dense" or not bool((self.status == qal.QAL_ERR_STRUCTURE).any())
 
 
 def shard_range(total: int, world: int, rank: int):

@@ -23,6 +23,8 @@ QAL_OP_FIDELITY = 2
 QAL_OP_FIDELITY_GRAD = 3
 QAL_OP_EXPM_SLICES = 4
 QAL_OP_VJP = 5
+QAL_OP_FIDELITY_REDUCE = 6
+QAL_BLK_SETS_DEFAULT, QAL_BLK_SETS_FUSED, QAL_BLK_SETS_PAIRS = 0, 1, 2
 QAL_MAX_CTRL = 8
 STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
           "grad_slices", "dense_gemm", "blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain",
@@ -55,6 +57,8 @@ _EXPORTS = {
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "qal_fidelity": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_void_p, ctypes.c_void_p]),
+    "qal_fidelity_ws": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "qal_fidelity_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
@@ -89,6 +93,8 @@ _EXPORTS = {
                                        ctypes.c_void_p, ctypes.c_void_p]),
     "qal_block_unpack": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p]),
+    "qal_block_check": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "qal_block_expm_slices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
@@ -119,8 +125,9 @@ _EXPORTS = {
                                                  ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]),
     "qal_block_fidelity_cotangent": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                      ctypes.c_void_p]),
+    "qal_bigblock_plan_workspace_bytes": (ctypes.c_size_t, []),
     "qal_bigblock_plan_build": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
-                                                ctypes.c_void_p]),
+                                                ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "qal_bigblock_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p]),
     "qal_bigblock_expm_slices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                                  ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -294,12 +301,18 @@ def qal_batched_matmul(A, B, stream=None):
     return out
 
 
-def qal_fidelity(Lam, V, stream=None):
-    """A8: F[b] = Re Tr(S_V^dag Lambda_b) / d^2."""
+def qal_fidelity(Lam, V, ws=None, stream=None):
+    """A8: F[b] = Re Tr(S_V^dag Lambda_b) / d^2.  With `ws` (a device byte tensor of at least
+    qal_workspace_bytes(QAL_OP_FIDELITY_REDUCE, n, B)) the d = 64 reduction runs over 512 row slabs
+    per pulse (qal_fidelity_ws); without it one CTA per pulse (qal_fidelity)."""
     Lam = _dev(Lam, torch.complex128, "Lambda")
     V = _dev(V, torch.complex128, "V")
     F = torch.empty(Lam.shape[0], dtype=torch.float64, device=Lam.device)
-    rc = load().qal_fidelity(V.shape[0], Lam.shape[0], _ptr(Lam), _ptr(V), _ptr(F), _stream(stream))
+    if ws is None:
+        rc = load().qal_fidelity(V.shape[0], Lam.shape[0], _ptr(Lam), _ptr(V), _ptr(F), _stream(stream))
+    else:
+        rc = load().qal_fidelity_ws(V.shape[0], Lam.shape[0], _ptr(Lam), _ptr(V), _ptr(F), _ptr(ws), ws.numel(),
+                                    _stream(stream))
     _check(rc, "qal_fidelity")
     return F
 
@@ -459,7 +472,7 @@ class BlockPlan(ctypes.Structure):
                 ("perm", ctypes.c_int * QAL_BLK_MAX_ROWS), ("weight", ctypes.c_int * QAL_BLK_MAX_ROWS),
                 ("inv", ctypes.c_int * 64), ("comp", ctypes.c_int * 64),
                 ("real", ctypes.c_int * QAL_BLK_MAX_GROUPS), ("rtype", ctypes.c_int * QAL_BLK_MAX_ROWS),
-                ("ncode", ctypes.c_int * 64), ("cplx_mults", ctypes.c_int)]
+                ("ncode", ctypes.c_int * 64), ("cplx_mults", ctypes.c_int), ("launch_sets", ctypes.c_int)]
 
     def groups(self):
         return [(self.width[g], self.row0[g], self.off[g]) for g in range(self.ngroups)]
@@ -490,6 +503,16 @@ def qal_block_pack(plan: BlockPlan, nat, check=True, stream=None):
     _check(load().qal_block_pack(ctypes.byref(plan), cnt, _ptr(nat), _ptr(out), _ptr(flag), _stream(stream)),
            "qal_block_pack")
     return out, flag
+
+
+def qal_block_check(plan: BlockPlan, nat, status, broadcast=False, stream=None):
+    """Per-pulse structure check (after the step's block calls): status[e] = QAL_ERR_STRUCTURE for every
+    matrix nat[e] coupling two blocks (broadcast: every status entry if any matrix fails)."""
+    nat = _dev(nat, torch.complex128, "nat")
+    cnt = nat.reshape(-1, plan.n, plan.n).shape[0]
+    _check(load().qal_block_check(ctypes.byref(plan), cnt, _ptr(nat), 1 if broadcast else 0, _ptr(status),
+                                  status.numel(), _stream(stream)), "qal_block_check")
+    return status
 
 
 def qal_block_unpack(plan: BlockPlan, packed, stream=None):
@@ -666,8 +689,9 @@ def qal_bigblock_plan_build(mats, mirror=True, stream=None) -> BigBlockPlan:
     """Structure of n = 4096 operators (device tensor [m][4096][4096]; pattern computed on the device)."""
     mats = _dev(mats, torch.complex128, "mats")
     plan = BigBlockPlan()
+    ws = torch.empty(load().qal_bigblock_plan_workspace_bytes(), dtype=torch.uint8, device=mats.device)
     rc = load().qal_bigblock_plan_build(mats.shape[0], _ptr(mats), 1 if mirror else 0, ctypes.byref(plan),
-                                        _stream(stream))
+                                        _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "qal_bigblock_plan_build")
     return plan
 

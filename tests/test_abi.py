@@ -42,7 +42,7 @@ def test_binding_covers_every_symbol():
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.qal_abi_version() == 1
+    assert lib.qal_abi_version() == 2
     assert lib.qal_status_string(0) == b"ok"
     assert b"NULL" in lib.qal_status_string(-1)
     assert lib.qal_status_string(-99) == b"unknown status"
@@ -102,6 +102,9 @@ def test_fidelity_grad_validation(lib):
     a3[13] = None
     assert lib.qal_fidelity_grad(*a3) == -1            # V missing
     assert lib.qal_fidelity(8, 0, p, p, p, None) == -3
+    assert lib.qal_fidelity_ws(64, 1, p, p, p, None, 0, None) == -6          # d = 64 needs the slab workspace
+    assert lib.qal_fidelity_ws(64, 1, p, None, p, p, 1 << 20, None) == -1
+    assert lib.qal_fidelity_ws(16, 1, p, p, p, None, 0, None) == -5
     assert lib.qal_build_liouvillian(2, 1, p, 1, p, 0, None, 0, p, p, None, None) == -5
     assert lib.qal_build_liouvillian(8, 1, p, 0, None, 0, None, 1, p, None, p, None) == -2
 
@@ -113,12 +116,28 @@ def test_workspace_sizes(lib):
     g = lib.qal_workspace_bytes(3, 64, 3, 16, 2, 0)
     assert g >= 3 * 3 * 16 * MB + 3 * MB
     assert lib.qal_workspace_bytes(3, 32, 3, 16, 2, 0) == 0
+    # qal_fidelity_ws: 512 partial sums per pulse at n = 4096, nothing at n = 64 (no library-held scratch)
+    assert lib.qal_workspace_bytes(6, 4096, 3, 1, 0, 0) == 3 * 512 * 8
+    assert lib.qal_workspace_bytes(6, 64, 3, 1, 0, 0) == 0
 
 
 def test_default_chunk_divides_and_is_power_of_two(lib):
     for b, n in [(1, 256), (4096, 1024), (1, 1 << 20), (3, 96), (1, 7)]:
         c = lib.qal_default_chunk(b, n)
         assert c >= 1 and n % c == 0 and (c & (c - 1)) == 0 and c <= 64
+
+
+def test_library_has_no_runtime_knobs_or_device_globals():
+    """reentrant, no global mutable state, the library never allocates in the hot-path calls:
+    no getenv, no __device__ scratch arrays, no cudaMalloc in the CUDA sources."""
+    csrc = os.path.join(ROOT, "paper_2511_13330_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        if not f.endswith((".cu", ".cuh", ".h")):
+            continue
+        text = re.sub(r"//.*", "", open(os.path.join(csrc, f)).read())
+        assert "getenv" not in text, f
+        assert not re.search(r"cudaMalloc", text), f
+        assert not re.search(r"^\s*__device__\s+(?!__forceinline__|inline|static\s+__forceinline__)[\w:<>]+\s+\w+\s*\[", text, re.M), f
 
 
 def test_product_path_has_no_oracle_or_cpu_fallback():
@@ -183,6 +202,14 @@ def test_block_calls_validate_before_launch(lib, plan):
     assert lib.qal_block_ordered_product(bp, 1, 5, p, p, None, 0, None) == -6
     assert lib.qal_block_batched_matmul(bp, 2, p, 7, p, 0, p, None) == -2
     assert lib.qal_block_fidelity_cotangent(bp, None, p, None) == -1
+    # per-pulse structure check: empty, NULL status, per-matrix mode needs one status per matrix
+    assert lib.qal_block_check(bp, 0, p, 0, p, 1, None) == -3
+    assert lib.qal_block_check(bp, 2, p, 0, None, 2, None) == -1
+    assert lib.qal_block_check(bp, 2, p, 0, p, 3, None) == -2
+    # the launch-layout option of the plan is validated (no run-time environment knobs)
+    bad = type(plan).from_buffer_copy(plan)
+    bad.launch_sets = 7
+    assert lib.qal_block_pack(ctypes.byref(bad), 1, p, p, None, None) == -5
 
 
 def test_block_workspace_sizes(lib, plan):
@@ -198,7 +225,11 @@ def test_bigblock_calls_validate(lib):
     from paper_2511_13330_b200 import qal
     p = ctypes.c_void_p(1)
     pl = qal.BigBlockPlan()
-    assert lib.qal_bigblock_plan_build(0, p, 1, ctypes.byref(pl), None) == -3
-    assert lib.qal_bigblock_plan_build(1, None, 1, ctypes.byref(pl), None) == -1
+    wsb = lib.qal_bigblock_plan_workspace_bytes()
+    assert wsb == 4096 * 64 * 8                                                   # the 2 MB bitmask
+    assert lib.qal_bigblock_plan_build(0, p, 1, ctypes.byref(pl), p, wsb, None) == -3
+    assert lib.qal_bigblock_plan_build(1, None, 1, ctypes.byref(pl), p, wsb, None) == -1
+    assert lib.qal_bigblock_plan_build(1, p, 1, ctypes.byref(pl), None, 0, None) == -6   # caller workspace
+    assert lib.qal_bigblock_plan_build(1, p, 1, ctypes.byref(pl), p, wsb - 1, None) == -6
     assert lib.qal_bigblock_workspace_bytes(ctypes.byref(pl)) == 0               # empty plan
     assert lib.qal_bigblock_expm_slices(ctypes.byref(pl), 8, 1.0, 8, 2, p, p, p, 8, p, None, None, p, 1, None) == -5

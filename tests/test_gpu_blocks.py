@@ -378,49 +378,72 @@ def test_block_path_bit_identical_runs(torch_cuda, qal):
 
 
 def test_pulse_batch_reports_a_broken_structure(torch_cuda, qal):
-    """A transverse drift term (sigma_x on spin 1) breaks total S_z: the per-call device check of the
-    bench engine reports it (the plan was detected from the symmetric basis)."""
+    """A transverse drift term (sigma_x on spin 1) breaks total S_z: the per-step device check of the
+    bench engine reports it as QAL_ERR_STRUCTURE (-8) in status[b] of exactly that pulse (the plan was
+    detected from the symmetric basis of pulse 0), and a clean step clears it again."""
     torch = torch_cuda
     from paper_2511_13330_b200 import driver
     p = qi.cfg2(batch=3, N=8, T=2.0)
     args = [dev(torch, a) for a in (p.H0, p.Hc, p.C, p.u, p.V)]
     eng = driver.PulseBatch(*args, p.T, structure="blocks")
     eng.step()
-    assert eng.structure_ok()
+    assert eng.structure_ok() and eng.status.cpu().tolist() == [0, 0, 0]
+    H0_clean = eng.H0.clone()
     sx = np.kron(np.array([[0, 1], [1, 0]], dtype=complex), np.eye(4))
     eng.H0[2] += dev(torch, 0.01 * sx)
     eng.H0 = eng.H0.contiguous()
     eng.step()
     assert not eng.structure_ok()
+    assert eng.status.cpu().tolist() == [0, 0, qal.QAL_ERR_STRUCTURE]
+    eng.H0 = H0_clean
+    eng.step()
+    assert eng.structure_ok() and eng.status.cpu().tolist() == [0, 0, 0]
+
+
+def test_block_check_broadcasts_a_broken_shared_basis(torch_cuda, qal):
+    """A shared control operator that breaks the structure flags every pulse (broadcast mode)."""
+    torch = torch_cuda
+    p = qi.cfg2(batch=4, N=4, T=1.0)
+    plan, _, _, _ = packed_basis(torch, qal, p, True)
+    Hc = p.Hc.copy()
+    Hc[1] = Hc[1] + 0.3 * np.kron(np.array([[0, 1], [1, 0]], dtype=complex), np.eye(4))
+    _, Lc, _ = qal.qal_build_liouvillian(dev(torch, p.H0[:1]), dev(torch, Hc), dev(torch, p.C))
+    status = torch.zeros(4, dtype=torch.int32, device="cuda")
+    qal.qal_block_check(plan, Lc[:1], status, broadcast=True)
+    assert status.cpu().tolist() == [0, 0, 0, 0]               # L_1 alone still conserves S_z
+    qal.qal_block_check(plan, Lc, status, broadcast=True)
+    assert status.cpu().tolist() == [qal.QAL_ERR_STRUCTURE] * 4
 
 
 @pytest.mark.parametrize("mirror", [True, False])
-def test_launch_sets_fused_vs_group_specialised(torch_cuda, qal, monkeypatch, mirror):
-    """The forward / gradient kernels run one launch per group (slots, role-compiled kernels) by
-    default; one fused CTA per item ("all groups : 1 slot") must give the identical forward (the same
-    arithmetic per group) and the same gradient up to the order of the per-group trace sums.  A set
-    list that does not cover every group exactly once is ignored (default sets)."""
+def test_launch_sets_fused_vs_group_specialised(torch_cuda, qal, mirror):
+    """The forward / suffix-chain / gradient kernels run one launch per group (slots, role-compiled
+    kernels) by default; the plan's launch_sets option selects one fused CTA per item (every group) or
+    two items per CTA.  The forward and the suffix chain are identical (the same arithmetic per group),
+    the gradient equal up to the order of the per-group trace sums.  An invalid option is refused
+    before any launch."""
     torch = torch_cuda
     p = qi.cfg2(batch=40, N=96, T=200.0 * 96 / 1024)
     plan, L0p, Lcp, _ = packed_basis(torch, qal, p, mirror)
     u, V = dev(torch, p.u), dev(torch, p.V)
-    allg = (1 << plan.ngroups) - 1
 
-    def run(fwd, grad):
-        monkeypatch.setenv("QAL_BLK_SETS_FWD", fwd)
-        monkeypatch.setenv("QAL_BLK_SETS_GRAD", grad)
+    def run(sets):
+        plan.launch_sets = sets
         F, g, Lam = qal.qal_block_fidelity_grad(plan, L0p, Lcp, u, p.T, p.N, V, want_Lambda=True)
         torch.cuda.synchronize()
         return F.cpu().numpy(), g.cpu().numpy(), Lam.cpu().numpy()
 
-    Fd, gd, Ld = run("", "")
-    Ff, gf, Lf = run(f"{allg}:1", f"{allg}:1")
+    Fd, gd, Ld = run(qal.QAL_BLK_SETS_DEFAULT)
+    Ff, gf, Lf = run(qal.QAL_BLK_SETS_FUSED)
+    F2, g2, L2 = run(qal.QAL_BLK_SETS_PAIRS)
     assert np.array_equal(Ld, Lf) and np.array_equal(Fd, Ff)
+    assert np.array_equal(L2, Ld) and np.array_equal(g2, gd)
     rel = np.linalg.norm((gd - gf).reshape(len(gd), -1), axis=1) / np.linalg.norm(gf.reshape(len(gf), -1), axis=1)
     assert np.max(rel) <= 1e-13
-    # two slots per set, and an invalid list (group 0 twice) falling back to the default
-    F2, g2, L2 = run(",".join(f"{1 << k}:2" for k in range(plan.ngroups)), f"1:1,1:1,{allg}:1")
-    assert np.array_equal(L2, Ld) and np.array_equal(g2, gd)
+    plan.launch_sets = 5
+    with pytest.raises(RuntimeError):
+        qal.qal_block_fidelity_grad(plan, L0p, Lcp, u, p.T, p.N, V)
+    plan.launch_sets = qal.QAL_BLK_SETS_DEFAULT
 
 
 @pytest.mark.parametrize("batch,N", [(1, 1), (3, 5), (5, 2), (7, 3)])

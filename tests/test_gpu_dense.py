@@ -114,6 +114,39 @@ def test_dense_fidelity_matches_oracle(dissipative_short, qal, oracle, torch_cud
     assert abs(F - Fr) <= 1e-12 * abs(Fr) + 1e-17
 
 
+def test_dense_fidelity_concurrent_streams_are_bit_identical(torch_cuda, qal):
+    """SURVEY 8(b) reentrancy: the n = 4096 fidelity keeps no library-held scratch, so two calls on two
+    streams at once (each with its own workspace for the slab reduction, and the no-workspace form)
+    return exactly the serial results."""
+    torch = torch_cuda
+    V = to(torch, qi.haar_unitary(64, 5))
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    lams = [torch.complex(torch.randn(2, 4096, 4096, dtype=torch.float64, device="cuda", generator=gen),
+                          torch.randn(2, 4096, 4096, dtype=torch.float64, device="cuda", generator=gen))
+            for _ in range(2)]
+    wsb = qal.workspace_bytes(qal.QAL_OP_FIDELITY_REDUCE, 4096, 2, 1)
+    assert wsb == 2 * 512 * 8
+    ws = [torch.empty(wsb, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    serial = [qal.qal_fidelity(L, V, ws=w) for L, w in zip(lams, ws)]
+    serial1 = [qal.qal_fidelity(L, V) for L in lams]
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            a = qal.qal_fidelity(lams[0], V, ws=ws[0], stream=s1)
+            a1 = qal.qal_fidelity(lams[0], V, stream=s1)
+        with torch.cuda.stream(s2):
+            b = qal.qal_fidelity(lams[1], V, ws=ws[1], stream=s2)
+            b1 = qal.qal_fidelity(lams[1], V, stream=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(a, serial[0]) and torch.equal(b, serial[1])
+        assert torch.equal(a1, serial1[0]) and torch.equal(b1, serial1[1])
+    # the two reductions (512 slabs + fixed-order sum vs one CTA) agree to rounding
+    for x, y in zip(serial, serial1):
+        assert torch.allclose(x, y, rtol=1e-12, atol=1e-12)
+
+
 def check_cptp_invariants(Lam, tol):
     d = 64
     vecI = np.eye(d).reshape(-1, order="F")
