@@ -2,13 +2,17 @@
 """bench.py -- Magnus slices/s of the Qalibrate hot path on B200 (BASELINE.json metric).
 
 Default workload (one "step" = every SURVEY 8(a) row once over one batch):
-  configs[2]: 4096 pulses x 1024 PWC slices (T = 200 ns, d = 8, n = 64, complex128) per GPU,
-  quasistatic Zeeman offsets per pulse; a2 Liouvillian build, a3-a5 Magnus-4 expm + ordered
-  product, a6 fidelity, a7 gradient w.r.t. all 2 x 1024 controls of every pulse.
-  value = slices/s summed over all ranks (weak scaling: every rank owns 4096 distinct pulses).
+  configs[2]: 4096 pulses x 1024 PWC slices (T = 200 ns, d = 8, n = 64, complex128), quasistatic
+  Zeeman offsets per pulse; a2 Liouvillian build, a3-a5 Magnus-4 expm + ordered product, a6 fidelity,
+  a7 gradient w.r.t. all 2 x 1024 controls of every pulse.  As BASELINE configs[2] says, the fixed
+  4096-pulse batch is sharded by pulse over the N GPUs (4096/N per rank, strong scaling) and every
+  step ends with the all-gather of F[4096] and grad[4096][1024][2] (NCCL) inside the
+  timed region.  value = 4096 x 1024 slices per step / the max over ranks of the step time.
+  (--weak: 4096 pulses PER GPU, no gather -- an extra measurement, not the headline.)
 
-Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-        (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config ...]
+  N > 1 without a torchrun environment: bench.py starts the N ranks itself
+  (python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ...).
 """
 from __future__ import annotations
 
@@ -34,7 +38,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pulses", type=int, default=4096, help="pulses per GPU (configs[2]: 4096)")
+    ap.add_argument("--pulses", type=int, default=4096,
+                    help="configs[2] batch: pulses of the whole job, split over the ranks (--weak: per rank)")
+    ap.add_argument("--weak", action="store_true", help="weak scaling: --pulses per rank, no result gather")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)   # launch-path test (gloo, CPU)
     ap.add_argument("--slices", type=int, default=1024)
     ap.add_argument("--sub-batch", type=int, default=None,
                     help="pulses per library call (default: dense 296, blocks sized to ~80 GB of workspace)")
@@ -50,7 +57,9 @@ def parse():
     ap.add_argument("--no-dense-ref", action="store_true",
                     help="skip the dense-path reference measurement that accompanies the block path")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg3grad", "cfg4", "hubbard3"],
-                    help="cfg2: batch fwd+grad (default, weak scaling); cfg3: 2^20-slice horizon, time-sharded")
+                    help="cfg2: batch fwd+grad (default, pulse-sharded); cfg3: 2^20-slice horizon, time-sharded")
+    ap.add_argument("--cfg4-full", action="store_true",
+                    help="configs[4] at full size: all 32 pulses x 512 slices per step, split over the ranks")
     return ap.parse_args()
 
 
@@ -59,6 +68,48 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without a torchrun environment: start the N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and return their exit status (rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+class Dist:
+    """The process group of the run (NCCL on GPUs, gloo for the CPU launch-path test), barriers and the
+    max-over-ranks step time."""
+
+    def __init__(self, backend):
+        import torch.distributed as dist
+        self.dist = dist
+        self.world, self.rank, self.local = dist_env()
+        if self.world > 1:
+            dist.init_process_group(backend, init_method="env://")
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x, device):
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.item()
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -103,19 +154,51 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
-def oracle_sample(prob, n_sample, pulses=1):
+def oracle_sample(prob, n_sample, pulses=1, threads=None):
     """The oracle as it stands (O1-O7: forward + per-direction gradient) on the first n_sample
-    slices of pulses 0..pulses-1 (each with its own drift) with the workload's slice width; returns
-    (slices/s, seconds, threads)."""
+    slices of pulses 0..pulses-1 (each with its own drift) with the workload's slice width, on
+    `threads` OpenMP threads (default: every host core -- torchrun's OMP_NUM_THREADS=1 does not
+    apply to this leg); returns (slices/s, seconds, threads)."""
     import oracle
+    threads = threads or os.cpu_count() or 1
+    oracle.set_threads(threads)
     h = prob.T / prob.N
     t0 = time.perf_counter()
     for p in range(pulses):
         L0, Lc = oracle.build_liouvillian(prob.H0[p], prob.Hc, prob.C)
         oracle.gradient(L0, Lc, prob.u[p, :n_sample], h * n_sample, n_sample, prob.V)
     dt = time.perf_counter() - t0
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return pulses * n_sample / dt, dt, threads
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(args, prob):
+    """The oracle as it stands on the host cores of this box: all cores (OpenMP over the gradient
+    directions) on a few pulses, and one thread (the sequential definition) on a shorter sample."""
+    import oracle
+    oracle.build()
+    npl = max(1, min(args.cpu_sample_pulses, prob.u.shape[0]))
+    v, dt, threads = oracle_sample(prob, args.cpu_sample_slices, npl)
+    out = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "sample": f"oracle forward + gradient on slices 0..{args.cpu_sample_slices - 1} of pulses 0..{npl - 1} "
+                     f"of this workload ({dt:.1f} s), OpenMP over gradient directions",
+           "cpu_model": cpu_model(), "host_cores": os.cpu_count()}
+    ns1 = max(1, args.cpu_sample_slices // 8)
+    v1, dt1, _ = oracle_sample(prob, ns1, 1, threads=1)
+    out["single_thread"] = {"value": v1, "unit": UNIT, "cores": 1,
+                            "sample": f"oracle forward + gradient on slices 0..{ns1 - 1} of pulse 0 ({dt1:.1f} s), "
+                                      "one thread (the sequential definition)"}
+    return out
 
 
 def run_reference(args):
@@ -133,10 +216,10 @@ def run_reference(args):
             vals.append((v, dt))
     value = statistics.median(v for v, _ in vals)
     sample = (f"oracle (O1-O7, sequential C, OpenMP over gradient directions) on slices 0..{args.cpu_sample_slices - 1}"
-              f" of pulse 0 of configs[2] (h = 200/1024 ns), forward + gradient, per step")
+              f" of pulse 0 of configs[2] (h = 200/1024 ns), forward + gradient, per step; host CPU {cpu_model()}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(d for _, d in vals),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "configs[2] bounded sample (oracle)", "slices_per_step": args.cpu_sample_slices},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -204,135 +287,205 @@ def dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, p
     return out
 
 
+class StubBatch:
+    """Launch-path test only (--stub, gloo on CPU): the PulseBatch interface with a trivial step whose
+    result identifies the global pulse, F[b] = first + b, grad[b][k][j] = (first + b) + k / N."""
+
+    def __init__(self, B, N, J, first):
+        import torch
+        self.B, self.N, self.J, self.first = B, N, J, first
+        self.F = torch.empty(B, dtype=torch.float64)
+        self.grad = torch.empty((B, N, J), dtype=torch.float64)
+        self.launches = 0
+        self.sub = B
+
+    def step(self):
+        import torch
+        idx = torch.arange(self.first, self.first + self.B, dtype=torch.float64)
+        self.F.copy_(idx)
+        self.grad.copy_(idx[:, None, None] + torch.arange(self.N, dtype=torch.float64)[None, :, None] / self.N)
+        return self.F, self.grad
+
+
 def run_ours(args):
+    """configs[2]: the fixed batch sharded by pulse over the ranks (strong scaling), one step = the whole
+    hot path on the rank's pulses + the C2 all-gather of F and grad."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
-    from paper_2511_13330_b200 import _build, driver, inputs as qi, qal
-
-    world, rank, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    _build.build()
-    qal.load()
-
-    B, N = args.pulses, args.slices
+    stub = args.stub
+    D = Dist("gloo" if stub else "nccl")
+    world, rank, local = D.world, D.rank, D.local
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}")
+    from paper_2511_13330_b200 import driver
+    B_total, N = args.pulses, args.slices
     T = 200.0 * N / 1024
-    prob = qi.cfg2(batch=B, N=N, T=T, first_pulse=rank * B)       # rank owns pulses [rank B, (rank+1) B)
-    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-    H0, Hc, C, u, V = to(prob.H0), to(prob.Hc), to(prob.C), to(prob.u), to(prob.V)
-    sub = args.sub_batch if args.sub_batch else (296 if args.structure == "dense" else None)
-    eng = driver.PulseBatch(H0, Hc, C, u, V, T, sub_batch=sub, structure=args.structure)
+    if args.weak:
+        B, first = B_total, rank * B_total                          # every rank its own 4096 pulses
+    else:
+        first, hi = driver.shard_range(B_total, world, rank)       # rank owns pulses [first, hi)
+        B = hi - first
+    if stub:
+        dev = torch.device("cpu")
+        eng = StubBatch(B, N, 2, first)
+        peak_tf = None
+    else:
+        from paper_2511_13330_b200 import _build, inputs as qi, qal
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        _build.build()
+        qal.load()
+        prob = qi.cfg2(batch=B, N=N, T=T, first_pulse=first)      # the global pulses [first, first + B)
+        to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        H0, Hc, C, u, V = to(prob.H0), to(prob.Hc), to(prob.C), to(prob.u), to(prob.V)
+        sub = args.sub_batch if args.sub_batch else (296 if args.structure == "dense" else None)
+        eng = driver.PulseBatch(H0, Hc, C, u, V, T, sub_batch=sub, structure=args.structure)
+        sink = torch.zeros(1, dtype=torch.float64, device=dev)
+        peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
+    gather = not args.weak
 
-    sink = torch.zeros(1, dtype=torch.float64, device=dev)
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak_tf = driver.fp64_peak(sink, blocks=2 * nsm)
+    def step():
+        F, g = eng.step()
+        if gather:
+            F, g = driver.gather_results(F, g)                   # C2: whole batch on every rank
+        return F, g
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    def sync():
+        if not stub:
+            torch.cuda.synchronize()
+
+    class Timer:
+        def __init__(self):
+            if stub:
+                self.t0 = self.t1 = 0.0
+            else:
+                self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def start(self):
+            if stub:
+                self.t0 = time.perf_counter()
+            else:
+                self.e0.record()
+
+        def stop(self):
+            if stub:
+                self.t1 = time.perf_counter()
+            else:
+                self.e1.record()
+
+        def ms(self):
+            return (self.t1 - self.t0) * 1e3 if stub else self.e0.elapsed_time(self.e1)
 
     for _ in range(args.warmup):
-        eng.step()
-    torch.cuda.synchronize()
+        Fg, gg = step()
+    sync()
 
-    # ---------------- timed region: device-resident inputs
-    counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
-    clocks = ClockSampler(local)
-    clocks.start()
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    qal.qal_profile_begin(counters)
-    ev0.record()
+    # ---------------- timed region: device-resident inputs; every step ends with the result gather
+    counters = None
+    clocks = None
+    if not stub:
+        from paper_2511_13330_b200 import qal
+        counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
+        clocks = ClockSampler(local)
+        clocks.start()
+    D.barrier()
+    sync()
+    tm = Timer()
+    if not stub:
+        qal.qal_profile_begin(counters)
+    tm.start()
     launches = 0
     for _ in range(args.steps):
-        eng.step()
+        Fg, gg = step()
         launches += eng.launches
-    ev1.record()
-    torch.cuda.synchronize()
-    stages = qal.qal_profile_end()
-    barrier()
-    clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = t.item()
-    prods = counters.cpu().tolist()
-
-    slices_total = world * B * N * args.steps
+    tm.stop()
+    sync()
+    stages = qal.qal_profile_end() if not stub else None
+    D.barrier()
+    clk = clocks.stop() if clocks else None
+    ms_max = D.max(tm.ms(), dev)
+    slices_total = (world * B if args.weak else B_total) * N * args.steps
     value = slices_total / (ms_max * 1e-3)
+    gathered_ok = None
+    if gather:
+        Fh = Fg.cpu()
+        gathered_ok = bool(Fg.shape[0] == B_total and gg.shape[0] == B_total)
+        if stub:
+            gathered_ok = gathered_ok and bool(torch.equal(Fh, torch.arange(B_total, dtype=torch.float64)))
+    if stub:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                              "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                              "scaling": "weak" if args.weak else "strong", "pulses_per_rank": B,
+                              "gathered_ok": gathered_ok, "stub": True}), flush=True)
+        D.close()
+        return 0
 
     # ---------------- e2e: host (pinned) inputs -> device -> host results, copies inside the timed region
     e2e = None
     if not args.no_e2e:
         hu = torch.from_numpy(prob.u).pin_memory()
         hH0 = torch.from_numpy(prob.H0).pin_memory()
-        hF = torch.empty(B, dtype=torch.float64).pin_memory()
-        hg = torch.empty_like(hu).pin_memory()
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record()
+        nres = B_total if gather else B
+        hF = torch.empty(nres, dtype=torch.float64).pin_memory()
+        hg = torch.empty((nres,) + tuple(prob.u.shape[1:]), dtype=torch.float64).pin_memory()
+        D.barrier()
+        sync()
+        tm.start()
         for _ in range(args.steps):
             eng.u.copy_(hu, non_blocking=True)
             eng.H0.copy_(hH0, non_blocking=True)
-            eng.step()
-            hF.copy_(eng.F, non_blocking=True)
-            hg.copy_(eng.grad, non_blocking=True)
-        ev1.record()
-        torch.cuda.synchronize()
-        t2 = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": slices_total / (t2.item() * 1e-3), "unit": UNIT,
+            F2, g2 = step()
+            hF.copy_(F2, non_blocking=True)
+            hg.copy_(g2, non_blocking=True)
+        tm.stop()
+        sync()
+        t2 = D.max(tm.ms(), dev)
+        e2e = {"value": slices_total / (t2 * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(hu.numel() * 8 + hH0.numel() * 16),
                "d2h_bytes_per_step": int(hF.numel() * 8 + hg.numel() * 8)}
 
     # ---------------- roofline of the dominant kernel (largest device time in the window)
+    prods = counters.cpu().tolist()
     roofline, split, step_flops = roofline_of(stages, prods, args.steps, peak_tf, eng.sub * N)
     structure_ok = eng.structure_ok()
+    status_ok = bool((eng.status == 0).all().item())
 
     # ---------------- the dense 64x64 path on the same workload (context for the block path)
     dense_ref = None
     if args.structure == "blocks" and not args.no_dense_ref:
-        dense_ref = dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, peak_tf, barrier)
+        dense_ref = dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, peak_tf, D.barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle
-        oracle.build()
-        npl = max(1, min(args.cpu_sample_pulses, prob.u.shape[0]))
-        v, dt, threads = oracle_sample(prob, args.cpu_sample_slices, npl)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"oracle forward + gradient on slices 0..{args.cpu_sample_slices - 1} of pulses "
-                         f"0..{npl - 1} of this workload ({dt:.1f} s), OpenMP over gradient directions"}
+        cpu = cpu_baseline(args, prob)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "configs[2]: pulses x 1024 PWC slices, T=200 ns, d=8 (64x64 c128 "
-                                       "superoperators), forward + fidelity + gradient",
+                "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"configs[2]: {B_total if not args.weak else world * B} pulses x {N} PWC "
+                                       f"slices, T={T:g} ns, d=8 (64x64 c128 superoperators), forward + fidelity "
+                                       "+ gradient" + ("" if args.weak else ", all-gather of F and grad per step"),
                            "structure": (f"coherence blocks (detected {eng.plan.n_components} components; "
                                          f"stored widths {[eng.plan.width[g] for g in range(eng.plan.ngroups)]}, "
                                          "Hermitian mirror), identical 64x64 results"
                                          if args.structure == "blocks" else "dense 64x64"),
                            "pulses_per_gpu": B, "slices": N, "sub_batch": eng.sub,
                            "l2": f"inputs larger than L2 (gradient workspace {eng.ws_bytes / 2**30:.1f} GiB)",
-                           "parallelism": f"batch-sharded x{world}"},
-                "pulses_per_s": world * B * args.steps / (ms_max * 1e-3),
+                           "parallelism": f"batch-sharded x{world}" + (" (weak)" if args.weak else "")},
+                "pulses_per_s": slices_total / N / (ms_max * 1e-3),
                 "pct_fp64_roofline": step_flops / (ms_max / args.steps * 1e-3) / 1e12 / peak_tf,
                 "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-                "structure_check": "ok" if structure_ok else "FAILED", "dense_path": dense_ref,
-                "gpu": torch.cuda.get_device_name(dev)}
+                "structure_check": "ok" if structure_ok else "FAILED", "status_ok": status_ok,
+                "result_gather": ("all_gather_into_tensor (NCCL) of F and grad, every step" if world > 1 and gather
+                                  else ("single rank: results already whole" if gather else "none (weak)")),
+                "dense_path": dense_ref, "gpu": torch.cuda.get_device_name(dev)}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    D.close()
     return 0
 
 
@@ -515,35 +668,37 @@ def run_cfg3(args):
 
 
 def run_cfg4(args):
-    """configs[4]: d = 64 (n = 4096) dense tiled DMMA path, PWC; pulses sharded over ranks (weak:
-    one pulse per rank per step).  A step is a bounded sample of one pulse: the first
-    --cfg4-slices slices (expm + fold, chunk = all of them) + the fidelity."""
+    """configs[4]: d = 64 (n = 4096), PWC, 32 pulses sharded by pulse over the ranks (rank r owns pulses
+    [r 32/G, (r+1) 32/G)); a step = for every owned pulse the expm + fold of its first S slices and the
+    fidelity, then the all-gather of F[32] (SURVEY 8(e) C2).  --cfg4-full: S = 512, the whole config;
+    otherwise S = --cfg4-slices (a bounded sample of every pulse, F of the truncated pulse)."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     from paper_2511_13330_b200 import _build, driver, inputs as qi, qal
 
-    world, rank, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+    D = Dist("nccl")
+    world, rank, local = D.world, D.rank, D.local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     _build.build()
     qal.load()
-    S = args.cfg4_slices or (64 if args.structure == "blocks" else 8)
     prob = qi.hubbard3() if args.config == "hubbard3" else qi.cfg4()
-    pulse = rank % prob.u.shape[0]
+    P_total = prob.u.shape[0]
+    S = prob.N if args.cfg4_full else (args.cfg4_slices or (64 if args.structure == "blocks" else 8))
+    if args.structure == "dense" and not args.cfg4_full:
+        P_total = min(P_total, max(world, 4))                   # dense sample: a few pulses only
+    p0, p1 = driver.shard_range(P_total, world, rank)
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
     L0, Lc, _ = qal.qal_build_liouvillian(to(prob.H0), to(prob.Hc), to(prob.C))
-    u = to(prob.u[pulse:pulse + 1, :S])
+    u_all = to(prob.u[p0:p1, :S])
     V = to(prob.V)
     sink = torch.zeros(1, dtype=torch.float64, device=dev)
     peak_tf = driver.fp64_peak(sink, blocks=2 * torch.cuda.get_device_properties(dev).multi_processor_count)
     n = 4096
     ws = torch.empty(qal.workspace_bytes(qal.QAL_OP_EXPM_SLICES, n, 1, S), dtype=torch.uint8, device=dev)
     P = torch.empty((1, 1, n, n), dtype=torch.complex128, device=dev)
-    F = torch.empty(1, dtype=torch.float64, device=dev)
+    F = torch.empty(p1 - p0, dtype=torch.float64, device=dev)
     fws = torch.empty(qal.workspace_bytes(qal.QAL_OP_FIDELITY_REDUCE, n, 1, 1), dtype=torch.uint8, device=dev)
     lib = qal.load()
     st = lambda: qal._stream(None)  # noqa: E731
@@ -555,18 +710,21 @@ def run_cfg4(args):
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def step():
-        if plan is not None:
-            rc = lib.qal_bigblock_expm_slices(ctypes.byref(plan), prob.N, prob.T, S, prob.J, qal._ptr(u[0]),
-                                              qal._ptr(L0), qal._ptr(Lc), S, qal._ptr(P), None, qal._ptr(flag),
-                                              qal._ptr(ws), ws.numel(), st())
-            qal._check(rc, "qal_bigblock_expm_slices")
-        else:
-            rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, prob.J, qal._ptr(u), qal._ptr(L0), 0,
-                                            qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
-                                            ws.numel(), st())
-            qal._check(rc, "qal_magnus_expm_slices")
-        qal._check(lib.qal_fidelity_ws(64, 1, qal._ptr(P), qal._ptr(V), qal._ptr(F), qal._ptr(fws), fws.numel(), st()),
-                   "qal_fidelity_ws")
+        for i in range(p1 - p0):
+            u = u_all[i]
+            if plan is not None:
+                rc = lib.qal_bigblock_expm_slices(ctypes.byref(plan), prob.N, prob.T, S, prob.J, qal._ptr(u),
+                                                  qal._ptr(L0), qal._ptr(Lc), S, qal._ptr(P), None, qal._ptr(flag),
+                                                  qal._ptr(ws), ws.numel(), st())
+                qal._check(rc, "qal_bigblock_expm_slices")
+            else:
+                rc = lib.qal_magnus_expm_slices(n, 1, prob.N, prob.T, 0, S, 4, 0, prob.J, qal._ptr(u), qal._ptr(L0),
+                                                0, qal._ptr(Lc), None, 0, None, S, qal._ptr(P), None, qal._ptr(ws),
+                                                ws.numel(), st())
+                qal._check(rc, "qal_magnus_expm_slices")
+            qal._check(lib.qal_fidelity_ws(64, 1, qal._ptr(P), qal._ptr(V), ctypes.c_void_p(F.data_ptr() + 8 * i),
+                                           qal._ptr(fws), fws.numel(), st()), "qal_fidelity_ws")
+        return driver.gather_results(F)[0]                      # F[32] on every rank
 
     for _ in range(args.warmup):
         step()
@@ -574,22 +732,18 @@ def run_cfg4(args):
     counters = torch.zeros(len(qal.STAGES), dtype=torch.int64, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
-    if world > 1:
-        dist.barrier()
+    D.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     qal.qal_profile_begin(counters)
     ev0.record()
     for _ in range(args.steps):
-        step()
+        Fall = step()
     ev1.record()
     torch.cuda.synchronize()
     stages = qal.qal_profile_end()
     clk = clocks.stop()
-    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = t.item()
+    ms_max = D.max(ev0.elapsed_time(ev1), dev)
     gstage = "blk_gemm" if plan is not None else "dense_gemm"
     g_ms, g_l = stages[gstage]
     gcount = counters.cpu().tolist()[qal.STAGES.index(gstage)]
@@ -597,12 +751,15 @@ def run_cfg4(args):
     nprod = gcount if plan is None else gflops / plan.flops_per_product   # 4096^2 (block) products executed
     if rank == 0:
         ach = gflops / (g_ms * 1e-3) / 1e12
-        line = {"metric": METRIC, "value": world * S * args.steps / (ms_max * 1e-3), "unit": UNIT,
+        full = S == prob.N and P_total == prob.u.shape[0]
+        line = {"metric": METRIC, "value": P_total * S * args.steps / (ms_max * 1e-3), "unit": UNIT,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"{prob.name} sample: pulse {pulse}, first {S} of {prob.N} PWC slices, d=64 "
-                                       f"(4096x4096 c128), expm + fold + fidelity", "slices_per_step": S},
+                "config": {"workload": (f"{prob.name}{' (full size)' if full else ' sample'}: {P_total} pulses x "
+                                        f"first {S} of {prob.N} PWC slices, d=64 (4096x4096 c128), expm + fold + "
+                                        "fidelity, pulses sharded over the ranks, all-gather of F"),
+                           "slices_per_step": P_total * S, "pulses": P_total, "pulses_per_gpu": p1 - p0},
                 "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
                              "frac": ach / peak_tf, "traffic": None,
                              "kernel": "k_bb_gemm" if plan is not None else "k_dense_gemm",
@@ -611,20 +768,24 @@ def run_cfg4(args):
                               " of the dense flops" if plan is not None else "dense 4096x4096"),
                 "fp64_peak_tflops": peak_tf, "stage_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()
                                                                    if v[1]},
-                "products_per_slice": nprod / (S * args.steps),
-                "F_sample": F.item(), "clocks": clk, "gpu": torch.cuda.get_device_name(dev)}
+                "products_per_slice": nprod / (P_total // world * S * args.steps),
+                "F": Fall.cpu().tolist(), "clocks": clk, "gpu": torch.cuda.get_device_name(dev)}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    D.close()
     return 0
 
 
 def main():
     args = parse()
-    if args.config in ("cfg4", "hubbard3") and args.impl != "reference":
-        return run_cfg4(args)
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args)            # the oracle on the host cores; rank 0 only under torchrun
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)              # one process per GPU, started here
+    world = dist_env()[0]
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}")
+    if args.config in ("cfg4", "hubbard3"):
+        return run_cfg4(args)
     if args.config == "cfg3":
         return run_cfg3(args)
     if args.config == "cfg3grad":

@@ -38,6 +38,11 @@ def lib():
     return _lib
 
 
+def set_threads(n: int):
+    """OpenMP threads of the oracle's parallel loops (libgomp, linked into libqalref.so)."""
+    lib().omp_set_num_threads(int(n))
+
+
 def _c(a, dtype):
     a = np.ascontiguousarray(a, dtype=dtype)
     return a, a.ctypes.data_as(ctypes.c_void_p)

@@ -186,6 +186,25 @@ def gather_partials(Q, group=None):
     return out
 
 
+def gather_results(F, grad=None, group=None):
+    """configs[2] / configs[4] result exchange: every rank's F [B_r] (and grad
+    [B_r][N][J]) -> the whole batch [G B_r] (...) in rank order, i.e. in global pulse order when rank r
+    owns pulses [r B_r, (r+1) B_r) -- all_gather_into_tensor (NCCL over NVLink on GPUs, gloo on CPU).
+    With no process group (one rank) the local tensors are returned as they are."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return F, grad
+    world = dist.get_world_size(group)
+    Fa = torch.empty((world * F.shape[0],), dtype=F.dtype, device=F.device)
+    dist.all_gather_into_tensor(Fa, F.contiguous(), group=group)
+    ga = None
+    if grad is not None:
+        ga = torch.empty((world * grad.shape[0],) + tuple(grad.shape[1:]), dtype=grad.dtype, device=grad.device)
+        dist.all_gather_into_tensor(ga.reshape(-1), grad.contiguous().reshape(-1), group=group)
+    return Fa, ga
+
+
 def ordered_combine(parts, product=None, stream=None, plan=None):
     """Lambda = Q_{G-1} ... Q_0 (Eq. 15, later rank on the LEFT) from the gathered partials [G][n][n]
     (or [G][packed] with a block plan), with the same balanced-tree shape as qal_ordered_product.
@@ -298,6 +317,21 @@ def segment_seeds(Qs, C, product):
     return seeds
 
 
+def rank_seed(ranks, C, rank, combine, matmul):
+    """Cotangent of rank `rank`'s own partial Q_r in a time-sharded objective (NEXT f2): with
+    Lambda = Q_{G-1} ... Q_0 (later rank on the LEFT, Eq. 15) and dL = Re Tr(C dLambda),
+        dL = Re Tr(C A_r dQ_r B_r) = Re Tr((B_r C A_r) dQ_r),
+    B_r = Q_{r-1} ... Q_0 (earlier ranks), A_r = Q_{G-1} ... Q_{r+1} (later ranks); so the seed is
+    B_r C A_r.  ranks: the gathered partials [G][...]; combine(parts) = their ordered product;
+    matmul(X, Y) = X Y (dense or packed).  Identity factors are skipped (rank 0 / rank G-1)."""
+    G = ranks.shape[0]
+    if rank > 0:                     # earlier ranks sit right of the local prefix: C <- B_r C
+        C = matmul(combine(ranks[:rank]), C)
+    if rank + 1 < G:                 # later ranks sit left of the local suffix: C <- C A_r
+        C = matmul(C, combine(ranks[rank + 1:]))
+    return C
+
+
 def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode, cotangent, magnus_order=4,
                           sub=64, group_subsegments=2048, group=None, stream=None, plan=None):
     """NEXT f2 -- gradient of an objective over a long horizon, time-sharded over the ranks, with
@@ -330,13 +364,8 @@ def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode,
     ranks = gather_partials(Q_rank, group)                                        # [G][n][n]
     rank = _rank(group)
     Lam = ordered_combine(ranks, stream=stream)
-    C = cotangent(Lam)
-    if rank > 0:                     # earlier ranks sit right of the local prefix: C <- B_r C
-        C = qal.qal_batched_matmul(ordered_combine(ranks[:rank], stream=stream).unsqueeze(0), C.unsqueeze(0),
-                                   stream=stream)[0]
-    if rank + 1 < ranks.shape[0]:    # later ranks sit left of the local suffix: C <- C A_r
-        C = qal.qal_batched_matmul(C.unsqueeze(0), ordered_combine(ranks[rank + 1:], stream=stream).unsqueeze(0),
-                                   stream=stream)[0]
+    C = rank_seed(ranks, cotangent(Lam), rank, lambda P: ordered_combine(P, stream=stream),
+                  lambda X, Y: qal.qal_batched_matmul(X.unsqueeze(0), Y.unsqueeze(0), stream=stream)[0])
     tmp = qal.qal_batched_matmul(C.unsqueeze(0), suf[0], stream=stream)          # C_r suf_s
     seeds = qal.qal_batched_matmul(pre[0], tmp, stream=stream)                    # pre_s C_r suf_s
     del tmp, pre, suf, parts
@@ -365,11 +394,8 @@ def _time_sharded_gradient_blocks(plan, L0p, Lcp, Lcommp, u_local, T, n_slices, 
     ranks = gather_partials(Q_rank, group)                                             # [G][packed]
     rank = _rank(group)
     Lam = ordered_combine(ranks, stream=stream, plan=plan)
-    C = cotangent(Lam)
-    if rank > 0:
-        C = bmm(ordered_combine(ranks[:rank], stream=stream, plan=plan), C)[0]
-    if rank + 1 < ranks.shape[0]:
-        C = bmm(C, ordered_combine(ranks[rank + 1:], stream=stream, plan=plan))[0]
+    C = rank_seed(ranks, cotangent(Lam), rank, lambda P: ordered_combine(P, stream=stream, plan=plan),
+                  lambda X, Y: bmm(X, Y)[0])
     seeds = bmm(pre[0], bmm(C, suf[0]))                                                # pre_s C_r suf_s
     del pre, suf, parts
     us = u_local[0].reshape((S, sub) + tuple(u_local.shape[2:]))
@@ -429,5 +455,5 @@ def stage_flops(products: int, stage: str = "") -> float:
 
 
 __all__ = ["PulseBatch", "shard_range", "time_shard_chunk", "time_shard_propagator", "ordered_combine",
-           "gather_partials", "local_partial", "calibrate", "segment_seeds", "time_sharded_gradient", "fp64_peak",
+           "gather_partials", "gather_results", "rank_seed", "local_partial", "calibrate", "segment_seeds", "time_sharded_gradient", "fp64_peak",
            "MATMUL_FLOPS_64", "complex_product_flops", "stage_flops", "math"]

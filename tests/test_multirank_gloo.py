@@ -176,3 +176,138 @@ def test_time_sharded_packed_partials_gloo(world):
         p.join(timeout=60)
     for _, err in res:
         assert err <= 1e-12
+
+
+# ---- result gather (cfg2 / cfg4) and the time-sharded gradient's rank seeds (NEXT f2) ----
+
+def _run_world(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    B_total, N, J = 12, 5, 2
+    lo, hi = driver.shard_range(B_total, world, rank)
+    F = torch.arange(lo, hi, dtype=torch.float64) * 0.5
+    g = torch.arange(lo * N * J, hi * N * J, dtype=torch.float64).reshape(hi - lo, N, J)
+    Fa, ga = driver.gather_results(F, g)
+    ok = (torch.equal(Fa, torch.arange(B_total, dtype=torch.float64) * 0.5)
+          and torch.equal(ga, torch.arange(B_total * N * J, dtype=torch.float64).reshape(B_total, N, J)))
+    Fo, go = driver.gather_results(F)                    # F only (configs[4])
+    ok = ok and go is None and torch.equal(Fo, Fa)
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+def test_result_gather_puts_every_rank_shard_in_global_pulse_order():
+    assert _run_world(_gather_worker, 2) == [(0, True), (1, True)]
+
+
+def _seed_worker(rank, world, port, q):
+    """rank_seed with the oracle as the product: Re Tr(seed_r E) must equal the directional derivative of
+    L(Q_r) = Re Tr(C Q_{G-1} ... Q_0) along E (central difference, exact up to rounding: L is linear)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    oracle.build()
+    n = 12
+    rng = np.random.default_rng(100 + rank)
+    Q = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)
+    ranks = driver.gather_partials(torch.from_numpy(Q))              # [G][n][n], rank order
+    crng = np.random.default_rng(7)                                   # the same C on every rank
+    C = crng.standard_normal((n, n)) + 1j * crng.standard_normal((n, n))
+    combine = lambda P: torch.from_numpy(oracle.ordered_product(np.ascontiguousarray(P.numpy())))  # noqa: E731
+    mm = lambda X, Y: torch.from_numpy(oracle.matmul(X.numpy(), Y.numpy()))                          # noqa: E731
+    seed = driver.rank_seed(ranks, torch.from_numpy(C), rank, combine, mm).numpy()
+    E = np.random.default_rng(200 + rank).standard_normal((n, n)) + 0j
+
+    def loss(Qr):
+        parts = ranks.numpy().copy()
+        parts[rank] = Qr
+        return np.trace(C @ oracle.ordered_product(parts)).real
+    eps = 1e-3
+    fd = (loss(Q + eps * E) - loss(Q - eps * E)) / (2 * eps)
+    an = np.trace(seed @ E).real
+    # and a wrong order (seed C B_r A_r) must not pass
+    q.put((rank, abs(fd - an) <= 1e-10 * max(1.0, abs(fd)), float(abs(fd))))
+    dist.destroy_process_group()
+
+
+def test_rank_seed_of_the_time_sharded_gradient_gloo():
+    res = _run_world(_seed_worker, 2)
+    assert [r[:2] for r in res] == [(0, True), (1, True)], res
+    assert all(r[2] > 1e-3 for r in res)          # non-trivial derivative
+
+
+def _seed_worker_vjp(rank, world, port, q):
+    """The seeds drive the per-rank VJP: with the oracle's per-direction vjp on each rank's slices and
+    C_r = rank_seed(...), the gathered gradient equals the oracle's whole-horizon vjp (the rank > 0 branches
+    of driver.time_sharded_gradient, with the oracle as the product)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2511_13330_b200 import inputs as qi
+    oracle.build()
+    p = qi.cfg0(N=8, T=100.0 * 8 / 256)
+    L0, Lc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    lo, hi = driver.shard_range(p.N, world, rank)
+    # this rank's partial Q_r = U_{hi-1} .. U_lo (oracle.propagate indexes u by absolute slice)
+    Q = oracle.propagate(L0, Lc, p.u[0], p.T, p.N, k0=lo, k1=hi)
+    ranks = driver.gather_partials(torch.from_numpy(Q))
+    crng = np.random.default_rng(9)
+    C = (crng.standard_normal((64, 64)) + 1j * crng.standard_normal((64, 64))) / 64
+    combine = lambda P: torch.from_numpy(oracle.ordered_product(np.ascontiguousarray(P.numpy())))  # noqa: E731
+    mm = lambda X, Y: torch.from_numpy(oracle.matmul(X.numpy(), Y.numpy()))                          # noqa: E731
+    Cr = driver.rank_seed(ranks, torch.from_numpy(C), rank, combine, mm).numpy()
+    # the rank's VJP on its own slices: a problem whose horizon is [lo, hi)
+    h = p.T / p.N
+    g_loc, _ = oracle.vjp(L0, Lc, p.u[0, lo:hi], h * (hi - lo), hi - lo, Cr)
+    g_all = torch.empty((p.N, p.u.shape[2]), dtype=torch.float64)
+    dist.all_gather_into_tensor(g_all.reshape(-1), torch.from_numpy(np.ascontiguousarray(g_loc)).reshape(-1))
+    g_ref, _ = oracle.vjp(L0, Lc, p.u[0], p.T, p.N, C)
+    err = float(np.linalg.norm(g_all.numpy() - g_ref) / np.linalg.norm(g_ref))
+    q.put((rank, err))
+    dist.destroy_process_group()
+
+
+def test_time_sharded_vjp_with_rank_seeds_matches_the_whole_horizon_gloo():
+    res = _run_world(_seed_worker_vjp, 2)
+    for rank, err in res:
+        assert err <= 1e-12, (rank, err)
+
+
+def _bench_stub(*extra):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--stub", "--steps", "2",
+                          "--warmup", "3", "--pulses", "64", "--slices", "8", *extra], capture_output=True, text=True,
+                         timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout          # rank 0 alone prints one JSON line
+    return json.loads(lines[0])
+
+
+def test_bench_spawns_its_ranks_and_gathers_the_split_batch():
+    """bench.py --gpus 2 with no torchrun environment starts 2 ranks itself (torch.distributed.run,
+    127.0.0.1), splits the 64-pulse batch 32/32, gathers F and grad every step (gloo here, NCCL on GPUs)
+    in global pulse order, and reports the max-over-ranks time once."""
+    line = _bench_stub()
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["pulses_per_rank"] == 32
+    assert line["gathered_ok"] is True and line["value"] > 0
+    weak = _bench_stub("--weak")
+    assert weak["scaling"] == "weak" and weak["pulses_per_rank"] == 64 and weak["gathered_ok"] is None
