@@ -780,6 +780,42 @@ __device__ __forceinline__ void blk_tmem_dealloc(uint32_t base, int cols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols));
 }
 
+// ------------------------------------------------------------------ Taylor T12 in 4 products (block path)
+// A2 = A^2, A3 = A2 A, B4 = b1 A + b2 A2 + b3 A3, A6 = B3 + B4^2, T12 = B1 + (B2 + A6) A6 with
+// B_i = x0 I + x1 A + x2 A2 + x3 A3 (columns below).  Coefficients solved in 50-digit arithmetic by
+// tools/derive_taylor12.py: the scheme equals sum_{k<=12} A^k/k! exactly as a polynomial and evaluates
+// random matrices of 1-norm theta12 to 2.75e-16 of the extended-precision Taylor sum (A15).
+constexpr double THETA_T12 = 0.3269045734215958;
+enum { T12_B1 = 0, T12_B2, T12_B3, T12_B4 };
+__constant__ double c_t12[4][4] = {
+    {1.0, -9.082905024086696, 1.5128269936229322, -0.19580740868765686},      // B1
+    {5.041452512043348, -2.6906761270300597, 0.08737480281237756, -0.0025088693217934794},  // B2
+    {0.0, 2.0, 0.05572498750413882, 0.012905662592475982},                   // B3
+    {0.0, 0.13181061013830184, 0.02027855540589259, 0.006759518468630863}};  // B4
+
+// scheme m in {8, 12, 18} and squarings s for a group's ||X||_1 = nrm: the cheapest in products of the
+// forward AND its dual (the gradient pass re-evaluates the same scheme as value + derivative):
+//   forward m + s products (T8: 3, T12: 4, T18: 5), dual 8 / 11 / 14 at s = 0, else 9 / 12 / 15 + 3 s
+// (plus the G product, common to all).  Ties -> the higher degree.  Same rule in both passes.
+__device__ __forceinline__ int blk_scheme_cost(int m, int s) {
+  const int f = (m == 8 ? 3 : m == 12 ? 4 : 5) + s;
+  const int d = (m == 8 ? 8 : m == 12 ? 11 : 14) + (s > 0 ? 1 + 3 * s : 0);
+  return f + d;
+}
+__device__ __forceinline__ void choose_scheme_blk(double nrm, int& m, int& s) {
+  if (!(nrm <= 1e300)) { m = 18; s = 0; return; }
+  const int ms[3] = {18, 12, 8};
+  const double th[3] = {THETA_T18, THETA_T12, THETA_T8};
+  int best = 1 << 30;
+  for (int i = 0; i < 3; ++i) {
+    int si = 0;
+    double a = nrm;
+    while (a > th[i] && si < 1100) { a *= 0.5; ++si; }
+    const int cst = blk_scheme_cost(ms[i], si);
+    if (cst < best) { best = cst; m = ms[i]; s = si; }
+  }
+}
+
 // ------------------------------------------------------------------ expm (a4) per group
 // U = expm(X 2^s): the T8 / T18 schemes of qal_slice.cuh with the powers in TMEM slots
 // tm + {0, 32, 64}; X's strips in A and its image in SX; SX4 = the group's operand image.
@@ -815,6 +851,36 @@ __device__ __forceinline__ int bexpm(BR<C, R, RE>& A, BR<C, R, RE>& acc, int m, 
     bmma<C, R, KS, RE>(acc, A, SX4, x, L);
     bcopy(A, acc);
     prods = 3;
+  } else if (m == 12) {
+    bcopy(A, acc);                                     // A = A2
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SX, x, L);                // A3 = A2 X
+    bt_store(T1, acc);
+    bscale(acc, c_t12[T12_B4][3]);                     // B4 = b1 X + b2 A2 + b3 A3
+    baxpy(acc, c_t12[T12_B4][2], A);
+    baxpy_img(acc, c_t12[T12_B4][1], SX, x, L);
+    bstore_img(SX4, acc, x, L);
+    bcopy(A, acc);
+    grp_sync(x);                                       // B4 image complete
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SX4, x, L);               // B4 B4
+    baxpy_img(acc, c_t12[T12_B3][1], SX, x, L);        // A6 = B3 + B4^2 (B3 has no I term)
+    bt_axpy(acc, c_t12[T12_B3][2], T0);
+    bt_axpy(acc, c_t12[T12_B3][3], T1);
+    grp_sync(x);                                       // reads of SX4 (B4) done
+    bstore_img(SX4, acc, x, L);
+    bcopy(A, acc);                                     // L = B2 + A6
+    badd_diag(A, c_t12[T12_B2][0], x, L);
+    baxpy_img(A, c_t12[T12_B2][1], SX, x, L);
+    bt_axpy(A, c_t12[T12_B2][2], T0);
+    bt_axpy(A, c_t12[T12_B2][3], T1);
+    bzero(acc);                                        // T12 = B1 + L A6
+    badd_diag(acc, c_t12[T12_B1][0], x, L);
+    baxpy_img(acc, c_t12[T12_B1][1], SX, x, L);
+    bt_axpy(acc, c_t12[T12_B1][2], T0);
+    bt_axpy(acc, c_t12[T12_B1][3], T1);
+    grp_sync(x);                                       // A6 image complete
+    bmma<C, R, KS, RE>(acc, A, SX4, x, L);
+    bcopy(A, acc);
+    prods = 4;
   } else {
     bcopy(A, acc);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SX, x, L);                // A3 = A2 X
@@ -898,7 +964,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     bcopy(A, Om);
     const double nrm = bnorm1(A, red, x, L);
     int m, s;
-    choose_scheme(nrm, m, s);
+    choose_scheme_blk(nrm, m, s);
     if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
     bscale(A, ldexp(1.0, -s));
     bstore_img(SX, A, x, L);
@@ -1387,7 +1453,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   // A holds Omega_k on entry (built one item ahead by the caller)
   const double nrm = bnorm1(A, red, x, L);
   int m, s;
-  choose_scheme(nrm, m, s);
+  choose_scheme_blk(nrm, m, s);
   if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
   const double sc = ldexp(1.0, -s);
   bscale(A, sc);
@@ -1441,6 +1507,55 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
       bzero(acc);
       bt_axpy(acc, c_t8[5], T2); bt_axpy(acc, c_t8[6], T0); SCR_AXPY(acc, 1.0, 0);
       badd_diag(acc, 1.0, x, L);
+      bmma<C, R, KS, RE>(acc, A, SV, x, L);
+      SCR_ST(2, acc);
+      ++np;
+    }
+  } else if (m == 12) {
+    // T12 = B1 + (B2 + A6) A6, A6 = B3 + B4^2, B4 = b1 X + b2 A2 + b3 A3, as value + derivative
+    bt_load(A, T0);
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // A3 = A2 X
+    bt_store(T2, acc);
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // A2 dX
+    bt_load(A, T1);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dA2 X = dA3
+    bt_store(T3, acc);
+    grp_sync(x);                                       // reads of SV (X), SD (dX) done
+    bzero(acc);                                        // B4 -> SV
+    SCR_AXPY(acc, c_t12[T12_B4][1], 0); bt_axpy(acc, c_t12[T12_B4][2], T0); bt_axpy(acc, c_t12[T12_B4][3], T2);
+    bstore_img(SV, acc, x, L);
+    bzero(acc);                                        // dB4 -> SD
+    SCR_AXPY(acc, c_t12[T12_B4][1], 1); bt_axpy(acc, c_t12[T12_B4][2], T1); bt_axpy(acc, c_t12[T12_B4][3], T3);
+    bstore_img(SD, acc, x, L);
+    grp_sync(x);                                       // B4, dB4 images complete
+    bload_img(A, SV, x, L);
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // B4 B4
+    SCR_AXPY(acc, c_t12[T12_B3][1], 0); bt_axpy(acc, c_t12[T12_B3][2], T0); bt_axpy(acc, c_t12[T12_B3][3], T2);
+    SCR_ST(2, acc);                                    // A6
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // B4 dB4
+    bload_img(A, SD, x, L);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dB4 B4
+    SCR_AXPY(acc, c_t12[T12_B3][1], 1); bt_axpy(acc, c_t12[T12_B3][2], T1); bt_axpy(acc, c_t12[T12_B3][3], T3);
+    SCR_ST(3, acc);                                    // dA6
+    grp_sync(x);                                       // reads of SV (B4), SD (dB4) done
+    SCR_LD(A, 2); bstore_img(SV, A, x, L);             // A6 image
+    SCR_LD(acc, 3); bstore_img(SD, acc, x, L);         // dA6 image
+    grp_sync(x);
+    bzero(acc);                                        // dT = dB1 + dL A6 + L dA6
+    SCR_AXPY(acc, c_t12[T12_B1][1], 1); bt_axpy(acc, c_t12[T12_B1][2], T1); bt_axpy(acc, c_t12[T12_B1][3], T3);
+    SCR_LD(A, 3);                                      // dL = dB2 + dA6
+    SCR_AXPY(A, c_t12[T12_B2][1], 1); bt_axpy(A, c_t12[T12_B2][2], T1); bt_axpy(A, c_t12[T12_B2][3], T3);
+    bmma<C, R, KS, RE>(acc, A, SV, x, L);
+    SCR_LD(A, 2);                                      // L = B2 + A6
+    badd_diag(A, c_t12[T12_B2][0], x, L);
+    SCR_AXPY(A, c_t12[T12_B2][1], 0); bt_axpy(A, c_t12[T12_B2][2], T0); bt_axpy(A, c_t12[T12_B2][3], T2);
+    bmma<C, R, KS, RE>(acc, A, SD, x, L);
+    if (s > 0) SCR_ST(3, acc);
+    np += 1 + 2 + 1 + 2 + 2;
+    if (s > 0) {                                       // T = B1 + L A6
+      bzero(acc);
+      badd_diag(acc, c_t12[T12_B1][0], x, L);
+      SCR_AXPY(acc, c_t12[T12_B1][1], 0); bt_axpy(acc, c_t12[T12_B1][2], T0); bt_axpy(acc, c_t12[T12_B1][3], T2);
       bmma<C, R, KS, RE>(acc, A, SV, x, L);
       SCR_ST(2, acc);
       ++np;
@@ -1942,29 +2057,102 @@ int per_chain(int C, bool re) { return 2 * img_doubles(C, re); }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 }  // namespace
 
+// Concurrent group launches: the forward and suffix-chain kernels run one launch per group, each a
+// single wave of independent per-pulse chains; launched one after the other they leave the GPU part
+// idle when the batch is small (configs[2] at 4096/8 = 512 pulses per GPU: 3.5 chains per SM per
+// group).  The sets are therefore forked onto per-device side streams after an event on the caller's
+// stream and joined back with events, so every group's CTAs share the SMs; the call stays stream-ordered
+// on the caller's stream.  The side streams / events are created once per device (setup, like the
+// shared-memory opt-in) and the record/wait sequence is enqueued under a mutex, so concurrent callers
+// cannot interleave their fork / join events.
+namespace {
+struct SideStreams {
+  int dev = -1;
+  cudaStream_t s[QAL_BLK_MAX_GROUPS] = {};
+  cudaEvent_t fork = nullptr, join[QAL_BLK_MAX_GROUPS] = {};
+};
+std::mutex g_side_mu;
+std::vector<SideStreams*>& side_table() {
+  static std::vector<SideStreams*> t;
+  return t;
+}
+// caller holds g_side_mu
+cudaError_t side_streams(SideStreams** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  for (SideStreams* x : side_table())
+    if (x->dev == dev) {
+      *out = x;
+      return cudaSuccess;
+    }
+  SideStreams* x = new SideStreams;
+  x->dev = dev;
+  for (int i = 0; i < QAL_BLK_MAX_GROUPS && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&x->s[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->join[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->fork, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;
+  side_table().push_back(x);
+  *out = x;
+  return cudaSuccess;
+}
+// run launch(i, stream) for i < n: i = 0 on `st`, the others on side streams, all after the work already
+// on `st` and before anything enqueued on `st` afterwards
+template <class F>
+cudaError_t fork_join(cudaStream_t st, int n, F&& launch) {
+  if (n <= 1) return n == 1 ? launch(0, st) : cudaSuccess;
+  std::lock_guard<std::mutex> lock(g_side_mu);
+  SideStreams* x = nullptr;
+  cudaError_t e = side_streams(&x);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaEventRecord(x->fork, st)) != cudaSuccess) return e;
+  for (int i = 1; i < n; ++i)
+    if ((e = cudaStreamWaitEvent(x->s[i - 1], x->fork, 0)) != cudaSuccess) return e;
+  cudaError_t first = cudaSuccess;
+  for (int i = 0; i < n; ++i) {
+    e = launch(i, i == 0 ? st : x->s[i - 1]);
+    if (e != cudaSuccess && first == cudaSuccess) first = e;
+  }
+  for (int i = 1; i < n; ++i) {
+    if ((e = cudaEventRecord(x->join[i - 1], x->s[i - 1])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, x->join[i - 1], 0)) != cudaSuccess) return e;
+  }
+  return first;
+}
+}  // namespace
+
 cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                  const BlkFwdOut& O, cudaStream_t st) {
   const int items = batch * (G.count / O.chunk);
   std::vector<BlkSet> sets;
   blk_sets(p, 0, sets);
+  struct L { BlkDev D; FwdKernel fn; size_t bytes; };
+  std::vector<L> ls;
   for (const BlkSet& set : sets) {
     // fewer slots when the items would not fill two CTAs per SM (small batches, one chunk per pulse)
     int ns = set.nslot;
     while (ns > 1 && (items + ns - 1) / ns < 2 * num_sms()) ns >>= 1;
-    BlkDev D;
-    if (!to_dev(p, D, set.gmask, ns)) return cudaErrorInvalidValue;
-    const size_t bytes = (size_t)grp_smem_doubles(D, per3) * 8;
-    const FwdKernel fn = fwd_kernel(D);
-    cudaError_t e = set_smem_fn((const void*)fn, bytes);
+    L l;
+    if (!to_dev(p, l.D, set.gmask, ns)) return cudaErrorInvalidValue;
+    l.bytes = (size_t)grp_smem_doubles(l.D, per3) * 8;
+    l.fn = fwd_kernel(l.D);
+    cudaError_t e = set_smem_fn((const void*)l.fn, l.bytes);
     if (e != cudaSuccess) return e;
-    prof_pre(ST_BLK_EXPM, st);
-    fn<<<(items + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(D, B, G, O, items, tmem_cols_for(D),
-                                                                     prof_counter(ST_BLK_EXPM));
-    prof_post(ST_BLK_EXPM, st);
-    ++launch_counter();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ls.push_back(l);
   }
-  return cudaSuccess;
+  prof_pre(ST_BLK_EXPM, st);
+  const cudaError_t e = fork_join(st, (int)ls.size(), [&](int i, cudaStream_t s) {
+    const L& l = ls[i];
+    l.fn<<<(items + l.D.nslot - 1) / l.D.nslot, 32 * l.D.nwarps, l.bytes, s>>>(l.D, B, G, O, items,
+                                                                              tmem_cols_for(l.D),
+                                                                              prof_counter(ST_BLK_EXPM));
+    ++launch_counter();
+    return cudaGetLastError();
+  });
+  prof_post(ST_BLK_EXPM, st);
+  return e;
 }
 
 cudaError_t launch_blk_tree_level(const qal_block_plan& p, int batch, int cnt, const double2* in, double2* out,
@@ -1984,21 +2172,29 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
                                     const double2* V, const double2* Cseed, double* X_img, cudaStream_t st) {
   std::vector<BlkSet> sets;
   blk_sets(p, 2, sets);
+  struct L { BlkDev D; ChainKernel fn; size_t bytes; };
+  std::vector<L> ls;
   for (const BlkSet& set : sets) {
-    BlkDev D;
-    if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
-    const size_t bytes = (size_t)grp_smem_doubles(D, per_chain) * 8;
-    const ChainKernel fn = chain_kernel(D);
-    cudaError_t e = set_smem_fn((const void*)fn, bytes);
+    int ns = set.nslot;   // fewer pulses per CTA when the batch would not fill two CTAs per SM
+    while (ns > 1 && (batch + ns - 1) / ns < 2 * num_sms()) ns >>= 1;
+    L l;
+    if (!to_dev(p, l.D, set.gmask, ns)) return cudaErrorInvalidValue;
+    l.bytes = (size_t)grp_smem_doubles(l.D, per_chain) * 8;
+    l.fn = chain_kernel(l.D);
+    cudaError_t e = set_smem_fn((const void*)l.fn, l.bytes);
     if (e != cudaSuccess) return e;
-    prof_pre(ST_BLK_SUFFIX, st);
-    fn<<<(batch + D.nslot - 1) / D.nslot, 32 * D.nwarps, bytes, st>>>(
-        D, batch, N, U_img, V, Cseed, X_img, prof_counter(ST_BLK_SUFFIX));
-    prof_post(ST_BLK_SUFFIX, st);
-    ++launch_counter();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ls.push_back(l);
   }
-  return cudaSuccess;
+  prof_pre(ST_BLK_SUFFIX, st);
+  const cudaError_t e = fork_join(st, (int)ls.size(), [&](int i, cudaStream_t s) {
+    const L& l = ls[i];
+    l.fn<<<(batch + l.D.nslot - 1) / l.D.nslot, 32 * l.D.nwarps, l.bytes, s>>>(l.D, batch, N, U_img, V, Cseed, X_img,
+                                                                              prof_counter(ST_BLK_SUFFIX));
+    ++launch_counter();
+    return cudaGetLastError();
+  });
+  prof_post(ST_BLK_SUFFIX, st);
+  return e;
 }
 
 // persistent grid of the gradient kernel: exactly the CTAs that are co-resident (registers,
@@ -2228,11 +2424,16 @@ int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block
   std::vector<Bin> bins;
   for (int k : keep) {
     const int sz = (int)members[k].size();
-    // best fit among open super-blocks of the same arithmetic (real / complex)
+    // among open super-blocks of the same arithmetic (real / complex) that fit: the narrowest, then the
+    // best fit.  A component sharing a block makes every product of the block pay for its 1-norm (the
+    // (m, s) choice is per block), so a small component goes to the cheapest block: for d = 8 the 1 x 1
+    // q = 3 block (||Omega||_1 ~ 0.39 on configs[2]) joins the 6-block (~0.36), not the 15-block
+    // (~0.27), which then runs T12 without squarings.
     int best = -1;
     for (int i = 0; i < (int)bins.size(); ++i)
       if (bins[i].real == realc[k] && bins[i].used + sz <= bins[i].width &&
-          (best < 0 || bins[i].width - bins[i].used < bins[best].width - bins[best].used))
+          (best < 0 || bins[i].width < bins[best].width ||
+           (bins[i].width == bins[best].width && bins[i].width - bins[i].used < bins[best].width - bins[best].used)))
         best = i;
     if (best >= 0) { bins[best].used += sz; bins[best].comps.push_back(k); }
     else bins.push_back({(sz + 7) / 8 * 8, sz, realc[k], {k}});

@@ -94,6 +94,15 @@ def test_packing_layout_is_consistent(qal, basis):
             assert sorted(stored) == list(range(64))
 
 
+def test_small_components_join_the_narrowest_block(qal, basis):
+    """Packing rule (DESIGN 5c): the 1 x 1 q = 3 component joins the 6-block (width 8), not the 15-block,
+    so the 15-block's (m, s) choice does not pay for the q = 3 norm.  d = 8 with the mirror:
+    {20} real in 24, {15} in 16, {6, 1} in 8."""
+    plan = qal.qal_block_plan_build(basis, mirror=True)
+    got = sorted((plan.width[g], plan.used[g], plan.real[g]) for g in range(plan.ngroups))
+    assert got == [(8, 7, 0), (16, 15, 0), (24, 20, 1)]
+
+
 def test_flops_are_the_block_cubes(qal, basis):
     plan = qal.qal_block_plan_build(basis, mirror=True)
     mults = plan.cplx_mults
