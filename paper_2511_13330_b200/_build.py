@@ -38,17 +38,28 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def build_variant(name: str, extra: list) -> str:
+    """Experiment build with extra nvcc flags into variants/libqal_<name>.so (never the in-tree
+    libqal.so); load it with QAL_LIB=<path>."""
+    out = os.path.join(HERE, "variants", f"libqal_{name}.so")
+    objdir = os.path.join(HERE, "variants", f"build_{name}")
+    return _compile(out, objdir, [*extra, *FLAGS], stamp=None)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
-    objdir = os.path.join(HERE, "build")
+    return _compile(OUT, os.path.join(HERE, "build"), FLAGS, stamp=STAMP, verbose=verbose)
+
+
+def _compile(out_path: str, objdir: str, flags: list, stamp=None, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     logs = []
     for src, p in procs:
@@ -61,13 +72,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    tmp = OUT + ".tmp"
+    tmp = out_path + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-o", tmp, *objs, "-lcudart"])
-    os.replace(tmp, OUT)
-    with open(STAMP, "w") as f:
-        f.write(_flags_text())
-    return OUT
+    os.replace(tmp, out_path)
+    if stamp:
+        with open(stamp, "w") as f:
+            f.write(_flags_text())
+    return out_path
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":   # _build.py --variant NAME FLAG...
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        build(force="--force" in sys.argv, verbose=True)

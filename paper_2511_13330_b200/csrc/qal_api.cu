@@ -926,7 +926,7 @@ int qal_bigblock_expm_slices(const qal_bigblock_plan* plan, int n_slices, double
 namespace {
 size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices) {
   const size_t img = (size_t)p->packed * 16;
-  return 3 * (size_t)batch * n_slices * img + (size_t)batch * img + blk_grad_scratch_bytes(*p);
+  return 3 * (size_t)batch * n_slices * img + (size_t)batch * img + blk_grad_scratch_bytes(*p, batch, n_slices);
 }
 // forward (U_k and prefix P_k images, Lambda) -> fidelity -> suffix chain (X_{k+1}) -> gradient slices
 int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
@@ -937,13 +937,13 @@ int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& 
   double* P = U + seq;
   double* X = P + seq;
   double2* lam_tmp = reinterpret_cast<double2*>(X + seq);
-  double* scratch = reinterpret_cast<double*>(lam_tmp + (size_t)batch * p->packed);
+  unsigned short* scheme = reinterpret_cast<unsigned short*>(lam_tmp + (size_t)batch * p->packed);
   double2* lam = Lam ? Lam : lam_tmp;
-  BlkFwdOut O{U, lam, c.G.count, status, P};
+  BlkFwdOut O{U, lam, c.G.count, status, P, scheme};
   if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
   if (F && launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
   if (launch_blk_suffix_chain(*p, batch, c.G.count, U, V, Cseed, X, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_blk_grad_slices(*p, batch, c.B, c.G, P, X, grad, status, scratch, Cseed ? 1.0 : 1.0 / 64.0, st) !=
+  if (launch_blk_grad_slices(*p, batch, c.B, c.G, P, X, grad, status, scheme, Cseed ? 1.0 : 1.0 / 64.0, st) !=
       cudaSuccess)
     return QAL_ERR_CUDA;
   return QAL_OK;

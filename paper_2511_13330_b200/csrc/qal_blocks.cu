@@ -41,9 +41,10 @@
 
 namespace qal {
 
-constexpr int BLK_MAX_WARPS = 12;
+constexpr int BLK_MAX_WARPS = 16;
 constexpr int BLK_FUSED_WARPS = 8;   // one item per CTA, all groups (every kernel but fwd / grad sets)
-constexpr int BLK_MAX_SLOTS = 4;   // independent item streams per CTA (group-specialised launches)
+constexpr int BLK_MAX_SLOTS = 5;   // independent item streams per CTA (group-specialised launches)
+constexpr int BLK_CHAIN_WARPS = 12;   // launch bound of the suffix-chain kernel (4 pulses x 3 warps)
 // real MMAs per complex 8x8x4 step of the complex blocks: 4 (default) or 3 (Gauss, -DQAL_BLK_3M)
 #ifdef QAL_BLK_3M
 constexpr int BLK_CPLX_MMAS = 3;
@@ -110,6 +111,9 @@ struct BlkDev {
   int tstride[BLK_MAX_WARPS];       // TMEM columns per slot of warp w (R * 8C of its widest task)
   int tmem_cols;                    // columns the CTA allocates (power of two >= 32)
   int tcache_off;                   // gradient kernel: double offset of the trace-basis cache (-1: none)
+  int tr_off;                       // gradient kernel: double offset of the trace buffers (2 parities)
+  int tr_k;                         // trace entries per warp / slot (J + ncomm)
+  int tr_buf;                       // doubles per parity: (nwarps + nslot) * tr_k
   int tcache_w[BLK_MAX_WARPS];      // double2 offset of warp w's cache slice
   signed char perm[QAL_BLK_MAX_ROWS];      // packed row -> natural index (-1 pad)
   unsigned char weight[QAL_BLK_MAX_ROWS];  // 0 pad, 1, 2
@@ -816,6 +820,19 @@ __device__ __forceinline__ void choose_scheme_blk(double nrm, int& m, int& s) {
   }
 }
 
+// the forward's (m, s) per (pulse, slice, group), kept for the gradient pass (which then needs no norm):
+// code = s << 2 | (0: T8, 1: T12, 2: T18); 0xFFFF = non-finite norm
+__device__ __forceinline__ unsigned short scheme_code(double nrm, int m, int s) {
+  if (!(nrm <= 1e300)) return 0xFFFFu;
+  return (unsigned short)((s << 2) | (m == 8 ? 0 : m == 12 ? 1 : 2));
+}
+__device__ __forceinline__ bool scheme_decode(unsigned short c, int& m, int& s) {
+  if (c == 0xFFFFu) { m = 18; s = 0; return false; }
+  m = (c & 3) == 0 ? 8 : (c & 3) == 1 ? 12 : 18;
+  s = c >> 2;
+  return true;
+}
+
 // ------------------------------------------------------------------ expm (a4) per group
 // U = expm(X 2^s): the T8 / T18 schemes of qal_slice.cuh with the powers in TMEM slots
 // tm + {0, 32, 64}; X's strips in A and its image in SX; SX4 = the group's operand image.
@@ -966,6 +983,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     int m, s;
     choose_scheme_blk(nrm, m, s);
     if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+    if (O.scheme && leader) O.scheme[((size_t)b * G.count + k) * D.ngroups + x.g] = scheme_code(nrm, m, s);
     bscale(A, ldexp(1.0, -s));
     bstore_img(SX, A, x, L);
     grp_sync(x);
@@ -1374,7 +1392,7 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
 }
 
 template <int FC, int FR, int FKS, int FRE>   // as k_blk_grad_slices: FC == 0 any roles
-__global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev D, int batch, int N,
+__global__ void __launch_bounds__(BLK_CHAIN_WARPS * 32) k_blk_suffix_chain(BlkDev D, int batch, int N,
                                                                         const double* __restrict__ U_img,
                                                                         const double2* __restrict__ V,
                                                                         const double2* __restrict__ Cseed,
@@ -1411,8 +1429,7 @@ __global__ void __launch_bounds__(BLK_MAX_WARPS * 32) k_blk_suffix_chain(BlkDev 
 }
 
 // --------------------------------------------------------------- gradient slices
-constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;
-constexpr int BLK_TR_BUF = (BLK_MAX_WARPS + BLK_MAX_SLOTS) * BLK_TR_MAX;   // one parity's trace buffer: per warp + per slot sum
+constexpr int BLK_TR_MAX = MAXJ + MAXJ + MAXJ * (MAXJ - 1) / 2;   // trace entries per item at most (J + ncomm)
 constexpr int BLK_TRC_MAXJ = 2;   // PWC trace-basis cache in shared memory up to this many controls
 
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
@@ -1422,7 +1439,8 @@ template <int C, int R, int KS, bool RE>
 __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc, const BlkBasis& B, const SliceGrid& G,
                                              int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
                                              uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
-                                             uint32_t tm, uint32_t ts, int* bad, const Lane& L) {
+                                             uint32_t tm, uint32_t ts, int* bad, const unsigned short* scheme,
+                                             int ngroups, const Lane& L) {
   constexpr size_t IM = img_doubles(C, RE);
   // shared scratch images (own strips only, re-read within the item): X, dX, A6, dA6
   double* gX = sX;
@@ -1450,11 +1468,16 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
     else baxpy_img(d_, a_, gS[i_], x, L);                      \
   } while (0)
   const uint32_t T0 = tm, T1 = tm + ts, T2 = tm + 2 * ts, T3 = tm + 3 * ts;   // A2, dA2, A3|Y, dA3|dY
-  // A holds Omega_k on entry (built one item ahead by the caller)
-  const double nrm = bnorm1(A, red, x, L);
+  // A holds Omega_k on entry (built one item ahead by the caller).  (m, s): the forward pass's choice for
+  // this (pulse, slice, group) when it was kept (no norm, no group barrier here), else the same rule
   int m, s;
-  choose_scheme_blk(nrm, m, s);
-  if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+  if (scheme) {
+    if (!scheme_decode(scheme[((size_t)b * G.count + k) * ngroups + x.g], m, s) && L.lane == 0) *bad = 1;
+  } else {
+    const double nrm = bnorm1(A, red, x, L);
+    choose_scheme_blk(nrm, m, s);
+    if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+  }
   const double sc = ldexp(1.0, -s);
   bscale(A, sc);
   bstore_img(SV, A, x, L);
@@ -1711,7 +1734,8 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
                               double* __restrict__ grad, int* __restrict__ status, const Ctx& x,
                               double* sm, uint64_t* bars, uint32_t tm, int* bad_sh, double* red_tr, double gscale,
-                              int accum, double2* cache, unsigned long long& nflop, const Lane& L) {
+                              int accum, double2* cache, const unsigned short* scheme, unsigned long long& nflop,
+                              const Lane& L) {
   constexpr int IM = img_doubles(C, RE);
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
@@ -1751,20 +1775,20 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     const int par = ((item - item0) / istride) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
                                                ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
-                                               bad_sh + par, L);
+                                               bad_sh + par, scheme, D.ngroups, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const int nx = item + istride;
     if (nx < items) bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
     // per-warp partial traces, double-buffered by item parity so one CTA barrier per item suffices
-    double* rt = red_tr + (size_t)par * BLK_TR_BUF;
-    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * BLK_TR_MAX, true, cache, L);
+    double* rt = red_tr + (size_t)par * D.tr_buf;
+    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
     slot_sync(D, x.slot);   // every warp of the slot done with this item: SN / SD free, rt complete
     prefetch(nx);
     if (L.w != w0) continue;
-    double* Tsum = rt + (BLK_MAX_WARPS + x.slot) * BLK_TR_MAX;
+    double* Tsum = rt + (D.nwarps + x.slot) * D.tr_k;
     for (int m = L.lane; m < K; m += 32) {   // fixed-order sum over the slot's warps
       double s = 0.0;
-      for (int w = w0; w < w0 + D.swarps; ++w) s += rt[w * BLK_TR_MAX + m];
+      for (int w = w0; w < w0 + D.swarps; ++w) s += rt[w * D.tr_k + m];
       Tsum[m] = s;
     }
     __syncwarp();
@@ -1810,10 +1834,12 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
                                                                const double* __restrict__ X_img,
                                                                double* __restrict__ grad, int* __restrict__ status,
                                                                double gscale,
-                                                               int accum, int tmem_cols, unsigned long long* ctr) {
+                                                               int accum, int tmem_cols,
+                                                               const unsigned short* __restrict__ scheme,
+                                                               unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id: [0] X_{k+1} -> SN, [1] P_k -> SD
-  __shared__ double red_tr[2 * BLK_TR_BUF];
+  double* red_tr = smem + D.tr_off;   // per-warp partial traces + per-slot sums, two item parities
   __shared__ uint32_t tmem_base_sh;
   __shared__ int bad_sh[BLK_MAX_SLOTS][2];
   const Lane L = lane_id();
@@ -1837,10 +1863,10 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
                        : nullptr;
   if constexpr (FC == 0)
     BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status,
-                 x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
+                 x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, scheme, nflop, L);
   else
     blk_grad_loop<FC, FR, FKS, FRE != 0>(D, batch, B, G, P_img, X_img, grad, status, x, sm, bars[x.bar], tm,
-                                          bad_sh[x.slot], red_tr, gscale, accum, cache, nflop, L);
+                                          bad_sh[x.slot], red_tr, gscale, accum, cache, scheme, nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
@@ -2006,7 +2032,7 @@ static int blk_role(const BlkDev& D) {
   return 0;
 }
 using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, const double*, double*, int*, double,
-                            int, int, unsigned long long*);
+                            int, int, const unsigned short*, unsigned long long*);
 using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*);
 static GradKernel grad_kernel(const BlkDev& D) {
   switch (blk_role(D)) {
@@ -2056,6 +2082,29 @@ int per_pair(int C, bool re) { return img_doubles(C, re); }
 int per_chain(int C, bool re) { return 2 * img_doubles(C, re); }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 }  // namespace
+
+// CTAs of kernel fn that are co-resident on one SM with `nwarps` warps, `bytes` of dynamic shared memory
+// and `tcols` TMEM columns: registers (64K per SM, per-warp allocation rounded to 256), shared memory
+// (233 KB configuration, 1 KB reserved per CTA), 64 warps, TMEM (512 columns)
+static int ctas_per_sm(const void* fn, int nwarps, size_t bytes, int tcols) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess || fa.numRegs <= 0) return 1;
+  const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+  const int by_regs = 65536 / (regs_warp * nwarps);
+  const int by_smem = (int)(233472 / (bytes + fa.sharedSizeBytes + 1024));
+  const int by_tmem = 512 / std::max(tcols, 32);
+  return std::max(0, std::min(std::min(by_regs, by_smem), std::min(64 / nwarps, std::min(by_tmem, 32))));
+}
+// co-resident warps per SM of per_sm CTAs of nwarps warps, or 0 if their warps load the four SM
+// sub-partitions (warp w of a CTA runs on sub-partition w % 4, each with its own FP64 pipe) unevenly by
+// more than one warp: 3-warp CTAs would leave a sub-partition without work.
+static int balanced_warps(int per_sm, int nwarps) {
+  int cnt[4] = {0, 0, 0, 0};
+  for (int w = 0; w < nwarps; ++w) cnt[w & 3] += per_sm;
+  const int mx = std::max(std::max(cnt[0], cnt[1]), std::max(cnt[2], cnt[3]));
+  const int mn = std::min(std::min(cnt[0], cnt[1]), std::min(cnt[2], cnt[3]));
+  return (mx - mn > 1) ? 0 : per_sm * nwarps;
+}
 
 // Concurrent group launches: the forward and suffix-chain kernels run one launch per group, each a
 // single wave of independent per-pulse chains; launched one after the other they leave the GPU part
@@ -2131,13 +2180,27 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
   struct L { BlkDev D; FwdKernel fn; size_t bytes; };
   std::vector<L> ls;
   for (const BlkSet& set : sets) {
-    // fewer slots when the items would not fill two CTAs per SM (small batches, one chunk per pulse)
-    int ns = set.nslot;
-    while (ns > 1 && (items + ns - 1) / ns < 2 * num_sms()) ns >>= 1;
+    // item slots per CTA: the count that keeps the most items in flight (co-resident CTAs x slots, at most
+    // the items), ties -> fewer slots (smaller CTAs spread a small batch over more SMs); the non-default
+    // layouts keep theirs
     L l;
-    if (!to_dev(p, l.D, set.gmask, ns)) return cudaErrorInvalidValue;
-    l.bytes = (size_t)grp_smem_doubles(l.D, per3) * 8;
-    l.fn = fwd_kernel(l.D);
+    bool have = false;
+    long long best = -1;
+    for (int pass = 0; pass < 2 && !have; ++pass)   // balanced sub-partitions first, else any
+      for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns) {
+        if (p.launch_sets != QAL_BLK_SETS_DEFAULT && ns != set.nslot) continue;
+        L t;
+        if (!to_dev(p, t.D, set.gmask, ns)) continue;
+        t.bytes = (size_t)grp_smem_doubles(t.D, per3) * 8;
+        t.fn = fwd_kernel(t.D);
+        const int per_sm = ctas_per_sm((const void*)t.fn, t.D.nwarps, t.bytes, tmem_cols_for(t.D));
+        if (per_sm < 1 || (pass == 0 && p.launch_sets == QAL_BLK_SETS_DEFAULT && !balanced_warps(per_sm, t.D.nwarps)))
+          continue;
+        const long long slots = (long long)per_sm * num_sms() * ns;
+        const long long used = std::min<long long>(slots, items);
+        if (!have || used > best) { l = t; best = used; have = true; }
+      }
+    if (!have) return cudaErrorInvalidValue;
     cudaError_t e = set_smem_fn((const void*)l.fn, l.bytes);
     if (e != cudaSuccess) return e;
     ls.push_back(l);
@@ -2197,27 +2260,10 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
   return e;
 }
 
-// persistent grid of the gradient kernel: exactly the CTAs that are co-resident (registers,
-// shared memory, and TMEM: 512 columns per SM); a CTA beyond that would start only when one
-// finished and double the tail
-static int blk_grad_grid(const BlkDev& D, GradKernel fn = nullptr) {
-  BlkDev tmp = D;
-  const size_t bytes = (size_t)grp_smem_doubles(tmp, per_grad) * 8;
-  if (!fn) fn = grad_kernel(D);
-  cudaFuncAttributes fa;
-  int per_sm = 1;
-  if (cudaFuncGetAttributes(&fa, (const void*)fn) == cudaSuccess && fa.numRegs > 0) {
-    // registers (64K per SM, per-warp allocation rounded to 256), shared memory (233 KB config,
-    // 1 KB reserved per CTA), named barriers (64 per SM, 16 per CTA), TMEM (512 columns)
-    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
-    const int by_regs = 65536 / (regs_warp * D.nwarps);
-    const int by_smem = (int)(233472 / (bytes + fa.sharedSizeBytes + 1024));
-    per_sm = std::min(std::min(by_regs, by_smem), std::min(8, 512 / tmem_cols_for(D)));
-  }
-  return std::max(1, per_sm) * num_sms();
+// the forward's scheme codes, one per (pulse, slice, group), read by the gradient pass
+size_t blk_grad_scratch_bytes(const qal_block_plan& p, int batch, int n_slices) {
+  return ((size_t)batch * n_slices * p.ngroups * sizeof(unsigned short) + 255) & ~(size_t)255;
 }
-
-size_t blk_grad_scratch_bytes(const qal_block_plan&) { return 0; }   // the squarings stay in shared memory
 
 // the PWC trace-basis cache: per warp J x R x 2C x 32 double2, after the group regions
 static int grad_cache_layout(BlkDev& D, int J, int base_doubles) {
@@ -2231,39 +2277,71 @@ static int grad_cache_layout(BlkDev& D, int J, int base_doubles) {
   return D.tcache_off + 2 * o;   // doubles
 }
 
+// the gradient kernel's launch for one set with `ns` item slots per CTA: group regions, the per-warp /
+// per-slot trace buffers (two item parities, sized by the call's J + ncomm) and, for PWC, the trace-basis
+// cache when it does not cost a CTA per SM.  Returns false if the set cannot be mapped.
+struct GradLaunch {
+  BlkDev D;
+  GradKernel fn;
+  size_t bytes;
+  int per_sm;
+};
+static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g) {
+  if (!to_dev(p, g.D, gmask, ns)) return false;
+  int base = grp_smem_doubles(g.D, per_grad);
+  g.D.tr_k = std::max(1, B.J + B.ncomm);
+  g.D.tr_buf = (g.D.nwarps + g.D.nslot) * g.D.tr_k;
+  g.D.tr_off = (base + 15) & ~15;
+  base = g.D.tr_off + 2 * g.D.tr_buf;
+  g.D.tcache_off = -1;
+  g.fn = grad_kernel(g.D);
+  g.bytes = (size_t)base * 8;
+  g.per_sm = ctas_per_sm((const void*)g.fn, g.D.nwarps, g.bytes, tmem_cols_for(g.D));
+  if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
+    BlkDev trial = g.D;
+    const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
+    if (ctas_per_sm((const void*)g.fn, g.D.nwarps, with, tmem_cols_for(g.D)) >= g.per_sm) {
+      g.D = trial;
+      g.bytes = with;
+    }
+  }
+  return g.per_sm > 0;
+}
+
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
-                                   double* scratch, double gscale, cudaStream_t st) {
+                                   const unsigned short* scheme, double gscale, cudaStream_t st) {
   std::vector<BlkSet> sets;
   blk_sets(p, 1, sets);
   int accum = 0;   // later sets add their groups' traces to the gradient (fixed launch order)
   for (const BlkSet& set : sets) {
-    BlkDev D;
-    if (!to_dev(p, D, set.gmask, set.nslot)) return cudaErrorInvalidValue;
-    const int base = grp_smem_doubles(D, per_grad);
-    const GradKernel fn = grad_kernel(D);
-    const int gmax = blk_grad_grid(D, fn);
-    size_t bytes = (size_t)base * 8;
-    D.tcache_off = -1;
-    if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
-      BlkDev trial = D;
-      const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
-      cudaFuncAttributes fa;
-      // keep the cache only if it does not cost a CTA per SM
-      if (cudaFuncGetAttributes(&fa, (const void*)fn) == cudaSuccess &&
-          (int)(233472 / (with + fa.sharedSizeBytes + 1024)) * num_sms() >= gmax) {
-        D = trial;
-        bytes = with;
-      }
+    // item slots per CTA: the default layout takes the count with the most co-resident warps per SM
+    // (registers, shared memory, TMEM; ties -> fewer slots); the other layouts keep theirs
+    GradLaunch g;
+    bool have = false;
+    if (p.launch_sets == QAL_BLK_SETS_DEFAULT) {
+      int best = 0;
+      for (int pass = 0; pass < 2 && !have; ++pass)   // balanced sub-partitions first, else any
+        for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns) {
+          GradLaunch t;
+          if (!grad_layout(p, set.gmask, ns, B, t)) continue;
+          const int wt = pass == 0 ? balanced_warps(t.per_sm, t.D.nwarps) : t.per_sm * t.D.nwarps;
+          if (wt > best) { g = t; best = wt; }
+        }
+      have = best > 0;
+    } else {
+      have = grad_layout(p, set.gmask, set.nslot, B, g);
     }
-    cudaError_t e = set_smem_fn((const void*)fn, bytes);
+    if (!have) return cudaErrorInvalidValue;
+    cudaError_t e = set_smem_fn((const void*)g.fn, g.bytes);
     if (e != cudaSuccess) return e;
     const int items = batch * G.count;
-    const int need = (items + D.nslot - 1) / D.nslot;
+    const int need = (items + g.D.nslot - 1) / g.D.nslot;
+    const int gmax = g.per_sm * num_sms();   // persistent: exactly the co-resident CTAs
     const int grid = need < gmax ? need : gmax;
     prof_pre(ST_BLK_GRAD, st);
-    fn<<<grid, 32 * D.nwarps, bytes, st>>>(D, batch, B, G, P_img, X_img, grad, status, gscale, accum,
-                                           tmem_cols_for(D), prof_counter(ST_BLK_GRAD));
+    g.fn<<<grid, 32 * g.D.nwarps, g.bytes, st>>>(g.D, batch, B, G, P_img, X_img, grad, status, gscale, accum,
+                                                 tmem_cols_for(g.D), scheme, prof_counter(ST_BLK_GRAD));
     prof_post(ST_BLK_GRAD, st);
     ++launch_counter();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -54,6 +54,7 @@ struct BlkFwdOut {
   int chunk;
   int* status;
   double* P_img;       // gradient path (chunk == count): prefix images P_k = U_{k-1}..U_0, or nullptr
+  unsigned short* scheme = nullptr;   // gradient path: (m, s) code per [batch][count][group], or nullptr
 };
 int build_block_plan(int n, int nmat, const double2* mats, int mirror, qal_block_plan* out);
 cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
@@ -70,13 +71,13 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
                                     const double2* V, const double2* Cseed, double* X_img, cudaStream_t st);
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
-                                   double* scratch, double gscale, cudaStream_t st);
+                                   const unsigned short* scheme, double gscale, cudaStream_t st);
 cudaError_t launch_blk_scan(const qal_block_plan& p, int batch, int cnt, const double2* U, double2* pre, double2* suf,
                             double2* ws, cudaStream_t st);
 cudaError_t launch_blk_batched_mm(const qal_block_plan& p, int count, const double2* A, long long sa,
                                   const double2* B, long long sb, double2* Cout, cudaStream_t st);
 cudaError_t launch_blk_fidelity_cotangent(const qal_block_plan& p, const double2* V, double2* Cout, cudaStream_t st);
-size_t blk_grad_scratch_bytes(const qal_block_plan& p);
+size_t blk_grad_scratch_bytes(const qal_block_plan& p, int batch, int n_slices);
 cudaError_t launch_blk_fidelity(const qal_block_plan& p, int batch, const double2* Lam, const double2* V, double* F,
                                 cudaStream_t st);
 
