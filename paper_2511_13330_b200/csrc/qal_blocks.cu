@@ -87,6 +87,12 @@ constexpr int BLK_MAX_TASKS = 3;
 #define BLK_ROLE_MAXNREG(FC) \
   ((FC) == 1 ? QAL_BLK_MAXNREG_C1 : (FC) == 2 ? QAL_BLK_MAXNREG_C2 : (FC) == 3 ? QAL_BLK_MAXNREG_C3 : QAL_BLK_MAXNREG)
 
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+
 // ------------------------------------------------------------------ device plan
 struct BlkTask {
   signed char g, rt0, R, slot;   // group, first row tile, row tiles owned, item slot of the CTA
@@ -351,6 +357,7 @@ __device__ __forceinline__ int bpair_off(int row, const Lane& L, int j) {
 }
 template <int C, int R, bool RE>
 __device__ __forceinline__ void bload_img(BR<C, R, RE>& s, const double* __restrict__ img, const Ctx& x, const Lane& L) {
+  QAL_JITTER();
   constexpr int PL = 64 * C * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -367,6 +374,7 @@ __device__ __forceinline__ void bload_img(BR<C, R, RE>& s, const double* __restr
 }
 template <int C, int R, bool RE>
 __device__ __forceinline__ void bstore_img(double* __restrict__ img, const BR<C, R, RE>& s, const Ctx& x, const Lane& L) {
+  QAL_JITTER();
   constexpr int PL = 64 * C * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -382,6 +390,7 @@ __device__ __forceinline__ void bstore_img(double* __restrict__ img, const BR<C,
 template <int C, int R, bool RE>
 __device__ __forceinline__ void baxpy_img(BR<C, R, RE>& acc, double a, const double* __restrict__ img, const Ctx& x,
                                           const Lane& L) {
+  QAL_JITTER();
   constexpr int PL = 64 * C * C;
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -487,6 +496,7 @@ __device__ __forceinline__ void baxpy_nat(BR<C, R, RE>& X, double a, const doubl
 template <int C, int R, int KS, bool RE>
 __device__ __forceinline__ void bmma(BR<C, R, RE>& acc, const BR<C, R, RE>& a, const double* __restrict__ Bs, const Ctx& x,
                                      const Lane& L) {
+  QAL_JITTER();
   static_assert(KS >= 1 && KS <= 2 * C, "k-steps");
   constexpr int P = 8 * C, PL = P * P;
   const int swz = (C % 2 == 0) ? (L.t & 1) : 0;   // physical tile of logical tile j: j ^ swz
@@ -732,6 +742,7 @@ __device__ __forceinline__ void tm_ld_plane(uint32_t addr, uint32_t* v) {
 }
 template <int C, int R, bool RE>
 __device__ __forceinline__ void bt_store(uint32_t addr, const BR<C, R, RE>& s) {
+  QAL_JITTER();
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     tm_st_plane<C>(addr + (RE ? 4 : 8) * C * r, s.re[r]);
@@ -741,6 +752,7 @@ __device__ __forceinline__ void bt_store(uint32_t addr, const BR<C, R, RE>& s) {
 }
 template <int C, int R, bool RE>
 __device__ __forceinline__ void bt_load(BR<C, R, RE>& s, uint32_t addr) {
+  QAL_JITTER();
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t v[4 * C], w[4 * C];
@@ -1035,6 +1047,7 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
     const int item = blockIdx.x * D.nslot + x.slot;   // slot x.slot: its own item, warps and regions
     if (item >= items) continue;
     double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
+    QAL_DCHECK(D.soff[x.g] < D.sstride && (size_t)(x.slot + 1) * D.sstride * 8 <= dyn_smem_bytes());
     if constexpr (FC == 0)
       BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
                    nflop, L);
@@ -1418,6 +1431,7 @@ __global__ void __launch_bounds__(BLK_CHAIN_WARPS * 32) k_blk_suffix_chain(BlkDe
     if (b >= batch) continue;
     const size_t base = (size_t)b * N * 2 * D.packed;
     double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
+    QAL_DCHECK(D.soff[x.g] < D.sstride && (size_t)(x.slot + 1) * D.sstride * 8 <= dyn_smem_bytes());
     const double2* cs = Cseed ? Cseed + (size_t)b * D.packed : nullptr;
     if constexpr (FC == 0)
       BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_suffix_task, D, N, U_img + base, V, cs, X_img + base, x, sm,
@@ -1771,6 +1785,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   }
   for (int item = item0; item < items; item += istride) {
     const int b = item / N, k = item % N;
+    QAL_DCHECK(b < batch && k < N);
     bcopy(A, Om);
     const int par = ((item - item0) / istride) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
@@ -1858,6 +1873,8 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
   unsigned long long nflop = 0;
   const Ctx x = ctx_of(D, T);
   double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
+  QAL_DCHECK(D.soff[x.g] < D.sstride && (size_t)(x.slot + 1) * D.sstride * 8 <= dyn_smem_bytes());
+  QAL_DCHECK((size_t)(D.tr_off + 2 * D.tr_buf) * 8 <= dyn_smem_bytes());
   double2* cache = (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ && D.tcache_off >= 0)
                        ? reinterpret_cast<double2*>(smem + D.tcache_off) + (size_t)D.tcache_w[L.w]
                        : nullptr;

@@ -19,6 +19,7 @@
 //     Taylor evaluation) are parked in Tensor Memory with tcgen05.st / tcgen05.ld:
 //     TMEM is 256 KB/SM of otherwise idle on-chip storage on this FP64 path.
 #pragma once
+#include <cassert>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -50,6 +51,30 @@ struct Strip {
 // into the current DMMA loop (they would need another 64 live registers).
 #define QAL_FENCE() asm volatile("" ::: "memory")
 
+// Race stress (experiment build -DQAL_RACE_JITTER, tools/stress_check.py): a pseudo-random per-warp delay
+// of 0-2 us in front of every shared-memory image access, product and TMEM access changes the interleaving
+// of the warps that share images.  Every reduction in the library has a fixed order, so a build with the
+// jitter must reproduce the default build bit for bit; a missing barrier would show as a difference.
+// (compute-sanitizer is not available on this pool.)  Bounds mode (-DQAL_CHECKED): device asserts on the
+// shared-memory regions and item indices of the block kernels.
+#ifdef QAL_RACE_JITTER
+__device__ __forceinline__ void qal_jitter() {
+  const unsigned long long t = clock64();
+  unsigned h = static_cast<unsigned>(t ^ (t >> 13)) * 2654435761u;
+  h ^= (threadIdx.x >> 5) * 40503u + blockIdx.x * 9973u;
+  h *= 2246822519u;
+  if ((h >> 29) == 0) __nanosleep((h >> 8) & 2047);
+}
+#define QAL_JITTER() qal_jitter()
+#else
+#define QAL_JITTER() ((void)0)
+#endif
+#ifdef QAL_CHECKED
+#define QAL_DCHECK(c) assert(c)
+#else
+#define QAL_DCHECK(c) ((void)0)
+#endif
+
 // ---------------------------------------------------------------- layout
 __device__ __forceinline__ int phys_col(int r, int c) {
   return ((c & ~7) | ((c & 3) << 1) | ((c >> 2) & 1)) ^ ((r & 1) << 3);
@@ -73,6 +98,7 @@ __device__ __forceinline__ void copy(Strip& d, const Strip& s) {
 
 // strip <-> image (shared or global; generic pointers, 16-byte accesses)
 __device__ __forceinline__ void load_img(Strip& s, const double* __restrict__ img, const Lane& L) {
+  QAL_JITTER();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int o = pair_off(L, j);
@@ -83,6 +109,7 @@ __device__ __forceinline__ void load_img(Strip& s, const double* __restrict__ im
   }
 }
 __device__ __forceinline__ void store_img(double* __restrict__ img, const Strip& s, const Lane& L) {
+  QAL_JITTER();
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int o = pair_off(L, j);
@@ -198,6 +225,7 @@ __device__ __forceinline__ double lds_v(uint32_t a) {
 }
 __device__ __forceinline__ void mma_acc_4m(Strip& acc, const Strip& a, const double* __restrict__ Bs,
                                            const Lane& L) {
+  QAL_JITTER();
   const int todd = L.t & 1;
   // row 4q+t of B; physical tile of output tile j is j ^ (t & 1)
   const uint32_t bE = smem_u32(Bs + L.t * 64 + L.g + 8 * todd);  // even j: tile j + todd
@@ -380,6 +408,7 @@ __device__ __forceinline__ void tmem_load_half(uint32_t addr, double (&x)[16]) {
   for (int i = 0; i < 16; ++i) x[i] = __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i]));
 }
 __device__ __forceinline__ void tmem_store(uint32_t addr, const Strip& s) {
+  QAL_JITTER();
   tmem_store_half(addr, s.re);
   tmem_store_half(addr + 32, s.im);
   tmem_wait_st();
@@ -387,6 +416,7 @@ __device__ __forceinline__ void tmem_store(uint32_t addr, const Strip& s) {
 
 // acc += a * M  where M is a strip parked in TMEM (both halves in flight, one wait)
 __device__ __forceinline__ void tmem_axpy(Strip& acc, double a, uint32_t addr) {
+  QAL_JITTER();
   uint32_t v[32], w[32];
   tmem_ld32(addr, v);
   tmem_ld32(addr + 32, w);
@@ -424,6 +454,7 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  QAL_JITTER();
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
           smem_u32(bar)),
