@@ -240,12 +240,14 @@ def load_traffic():
 def roofline_of(stages, prods, steps, peak_tf, units_per_launch):
     """Roofline of the dominant kernel (largest device time in the profiling window), the per-stage
     split and the algorithmic flops per step.  Block stages count flops (8 s^3 per block product),
-    dense stages count 64x64 products (qal.FLOP_STAGES, driver.stage_flops)."""
+    dense stages count 64x64 products (qal.FLOP_STAGES, driver.stage_flops).  The fused block forward
+    counts its fold products apart (blk_prefix_chain, no launches of its own): they belong to its time."""
     from paper_2511_13330_b200 import driver, qal
+    fl = {s: driver.stage_flops(prods[i], s) for i, s in enumerate(qal.STAGES)}
+    fl["blk_expm_fold"] += fl["blk_prefix_chain"] if stages["blk_prefix_chain"][1] == 0 else 0.0
     dom = max(stages, key=lambda s: stages[s][0])
     dom_ms, dom_launch = stages[dom]
-    dom_idx = qal.STAGES.index(dom)
-    dom_flops_per_launch = driver.stage_flops(prods[dom_idx], dom) / max(dom_launch, 1)
+    dom_flops_per_launch = fl[dom] / max(dom_launch, 1)
     achieved = dom_flops_per_launch / (dom_ms / max(dom_launch, 1) * 1e-3) / 1e12
     tr = load_traffic().get(qal.KERNELS[dom])
     traffic = (tr["dram_bytes_per_unit"] * units_per_launch) if (tr and units_per_launch) else None
@@ -256,10 +258,27 @@ def roofline_of(stages, prods, steps, peak_tf, units_per_launch):
                 "flops_per_launch": dom_flops_per_launch, "ms_per_launch": dom_ms / max(dom_launch, 1)}
     step_flops = sum(driver.stage_flops(prods[i], s) for i, s in enumerate(qal.STAGES)) / steps
     split = {s: {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps,
-                 "flops_per_step": driver.stage_flops(prods[i], s) / steps,
-                 "tflops": (driver.stage_flops(prods[i], s) / (v[0] * 1e-3) / 1e12) if v[0] > 0 else None}
-             for i, (s, v) in enumerate(stages.items()) if v[1] > 0}
+                 "flops_per_step": fl[s] / steps,
+                 "tflops": (fl[s] / (v[0] * 1e-3) / 1e12) if v[0] > 0 else None}
+             for s, v in stages.items() if v[1] > 0}
     return roofline, split, step_flops
+
+
+def fig2_split(qal, stages, prods, steps):
+    """The Fig. 2 analog (matrix exponentials vs the ordered multiplication): algorithmic
+    flops per step of the slice expansions (Eq. 14) and of the products (Eq. 15: the prefix fold, counted
+    apart inside the fused forward kernel, and the suffix chain), with the fused kernel's time apportioned
+    by its two flop counts (same kernel, same efficiency)."""
+    ix = qal.STAGES.index
+    f_exp, f_fold = prods[ix("blk_expm_fold")], prods[ix("blk_prefix_chain")]
+    f_suf = prods[ix("blk_suffix_chain")]
+    t_fwd = stages["blk_expm_fold"][0]
+    t_exp = t_fwd * f_exp / max(f_exp + f_fold, 1)
+    t_mul = t_fwd - t_exp + stages["blk_suffix_chain"][0]
+    return {"expansion": {"flops_per_step": f_exp / steps, "ms_per_step": t_exp / steps},
+            "multiplication": {"flops_per_step": (f_fold + f_suf) / steps, "ms_per_step": t_mul / steps},
+            "note": "forward fold time apportioned by flops inside the fused expm + fold kernel; the gradient "
+                    "stage (dual expansion + products) is reported apart in stage_split"}
 
 
 def dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, peak_tf, barrier):
@@ -449,6 +468,7 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel (largest device time in the window)
     prods = counters.cpu().tolist()
     roofline, split, step_flops = roofline_of(stages, prods, args.steps, peak_tf, eng.sub * N)
+    fig2 = fig2_split(qal, stages, prods, args.steps) if args.structure == "blocks" else None
     structure_ok = eng.structure_ok()
     status_ok = bool((eng.status == 0).all().item())
 
@@ -478,7 +498,7 @@ def run_ours(args):
                            "parallelism": f"batch-sharded x{world}" + (" (weak)" if args.weak else "")},
                 "pulses_per_s": slices_total / N / (ms_max * 1e-3),
                 "pct_fp64_roofline": step_flops / (ms_max / args.steps * 1e-3) / 1e12 / peak_tf,
-                "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split,
+                "fp64_peak_tflops": peak_tf, "roofline": roofline, "stage_split": split, "fig2_split": fig2,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
                 "structure_check": "ok" if structure_ok else "FAILED", "status_ok": status_ok,
                 "result_gather": ("all_gather_into_tensor (NCCL) of F and grad, every step" if world > 1 and gather

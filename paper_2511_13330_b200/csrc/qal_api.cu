@@ -5,6 +5,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: no-op unless a profiler injects itself
+
 #include "../../include/qal.h"
 #include "qal_dev.cuh"
 #include "qal_internal.h"
@@ -91,14 +93,20 @@ unsigned long long* prof_counter(int stage) {
   ProfState& P = prof();
   return (P.on && P.ctr) ? P.ctr + stage : nullptr;
 }
+// NVTX range names of the stages (host-side ranges around every stage launch; nsys / ncu --nvtx)
+static const char* const kStageNames[NSTAGE] = {
+    "qal:liouvillian", "qal:commutators", "qal:expm_fold", "qal:tree", "qal:fidelity", "qal:prefix_chain",
+    "qal:suffix_chain", "qal:grad_slices", "qal:dense_gemm", "qal:blk_expm_fold", "qal:blk_tree",
+    "qal:blk_prefix", "qal:blk_suffix_chain", "qal:blk_grad_slices", "qal:blk_gemm"};
 void prof_pre(int stage, cudaStream_t st) {
-  (void)stage;
+  nvtxRangePushA(stage >= 0 && stage < NSTAGE ? kStageNames[stage] : "qal");
   ProfState& P = prof();
   if (!P.on) return;
   P.pending = prof_event();
   cudaEventRecord(P.pending, st);
 }
 void prof_post(int stage, cudaStream_t st) {
+  nvtxRangePop();
   ProfState& P = prof();
   if (!P.on || !P.pending) return;
   cudaEvent_t e1 = prof_event();

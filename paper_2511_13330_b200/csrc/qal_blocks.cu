@@ -975,7 +975,7 @@ __host__ __device__ constexpr int grp3_doubles(int C, bool real) { return 3 * im
 // ------------------------------------------------------------------ forward fold (a1-a5)
 template <int C, int R, int KS, bool RE>
 __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
-                             const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long& nflop,
+                             const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long* nflop,
                              const Lane& L) {
   const uint32_t ts = D.tstride[L.w];
   constexpr int IM = img_doubles(C, RE);
@@ -1000,7 +1000,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     bstore_img(SX, A, x, L);
     grp_sync(x);
     const int np = bexpm<C, R, KS, RE>(A, acc, m, s, SX, SX4, tm, ts, x, L);
-    if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
+    if (leader) nflop[0] += (unsigned long long)np * D.gflops[x.g];   // expansion (Eq. 14)
     if (kk + 1 < O.chunk) bbuild_omega(Om, B, G, b, k + 1, x, L);   // loads overlap the stores / fold below
     const size_t slot = (size_t)b * G.count + k;
     if (O.U_img) bstore_img_l2(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
@@ -1014,7 +1014,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
       } else {
         bzero(acc); bmma<C, R, KS, RE>(acc, A, SP, x, L);           // P <- U_k P
         bcopy(A, acc);
-        if (leader) nflop += D.gflops[x.g];
+        if (leader) nflop[1] += D.gflops[x.g];                      // ordered product (Eq. 15)
         grp_sync(x);
         bstore_img(SP, A, x, L);
       }
@@ -1029,7 +1029,8 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
 template <int FC, int FR, int FKS, int FRE>   // as k_blk_grad_slices: FC == 0 any roles
 __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
                                                                           BlkFwdOut O, int items, int tmem_cols,
-                                                                          unsigned long long* ctr) {
+                                                                          unsigned long long* ctr,
+                                                                          unsigned long long* ctr_fold) {
   extern __shared__ __align__(128) double smem[];
   __shared__ int bad_sh[BLK_MAX_SLOTS];
   __shared__ uint32_t tmem_base_sh;
@@ -1040,7 +1041,7 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
   __syncthreads();
   tmem_fence_after();
   const uint32_t tm = warp_tmem(tmem_base_sh, D, L);
-  unsigned long long nflop = 0;
+  unsigned long long nflop[2] = {0, 0};   // expansion, fold (the Fig. 2 split of P:167-171)
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
@@ -1063,7 +1064,8 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
     const int item = blockIdx.x * D.nslot + threadIdx.x;
     if (item < items) O.status[item / nchunk] = QAL_ERR_NONFINITE;
   }
-  if (ctr && nflop) atomicAdd(ctr, nflop);
+  if (ctr && nflop[0]) atomicAdd(ctr, nflop[0]);
+  if (ctr_fold && nflop[1]) atomicAdd(ctr_fold, nflop[1]);
 }
 
 // ------------------------------------------------------------------ pair products (tree level)
@@ -2050,7 +2052,8 @@ static int blk_role(const BlkDev& D) {
 }
 using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, const double*, double*, int*, double,
                             int, int, const unsigned short*, unsigned long long*);
-using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*);
+using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*,
+                           unsigned long long*);
 static GradKernel grad_kernel(const BlkDev& D) {
   switch (blk_role(D)) {
     case 1: return k_blk_grad_slices<3, 1, 5, 1>;
@@ -2227,7 +2230,8 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
     const L& l = ls[i];
     l.fn<<<(items + l.D.nslot - 1) / l.D.nslot, 32 * l.D.nwarps, l.bytes, s>>>(l.D, B, G, O, items,
                                                                               tmem_cols_for(l.D),
-                                                                              prof_counter(ST_BLK_EXPM));
+                                                                              prof_counter(ST_BLK_EXPM),
+                                                                              prof_counter(ST_BLK_PREFIX));
     ++launch_counter();
     return cudaGetLastError();
   });
