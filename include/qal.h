@@ -426,6 +426,26 @@ int qal_block_propagator_vjp(const qal_block_plan *plan, int batch, int n_slices
                              long long Lcommp_stride, const qal_c128 *Cp, double *grad, qal_c128 *Lambda_packed,
                              int *status, void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * qal_block_propagator_vjp in two calls (the counterpart of qal_propagator_forward / _vjp): the forward
+ * writes Lambda_packed [batch][packed] (required) and keeps every U_k, prefix P_k and the (m, s) choice of
+ * every slice in `ws`; the backward then runs only the reverse pass (suffix chain seeded with Cp, one
+ * adjoint Frechet derivative per slice) on that stored forward.  Both calls take the same arguments and
+ * the same ws (>= qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count)); the cotangent may be
+ * computed from Lambda in between (the time-sharded gradient of NEXT f2 does).  The forward resets
+ * `status`, the backward only adds flags.
+ */
+int qal_block_propagator_forward(const qal_block_plan *plan, int batch, int n_slices, double T, int k0, int count,
+                                 int magnus_order, int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0p,
+                                 long long L0p_stride, const qal_c128 *Lcp, const qal_c128 *Lcommp,
+                                 long long Lcommp_stride, qal_c128 *Lambda_packed, int *status, void *ws,
+                                 size_t ws_bytes, void *stream);
+int qal_block_propagator_backward(const qal_block_plan *plan, int batch, int n_slices, double T, int k0, int count,
+                                  int magnus_order, int ctrl_mode, int n_ctrl, const double *u, const qal_c128 *L0p,
+                                  long long L0p_stride, const qal_c128 *Lcp, const qal_c128 *Lcommp,
+                                  long long Lcommp_stride, const qal_c128 *Cp, double *grad, int *status, void *ws,
+                                  size_t ws_bytes, void *stream);
+
 /* qal_ordered_scan on packed matrices (exclusive prefix / suffix products, Hillis-Steele levels).
  * ws >= 4 * batch * count * plan->packed * 16 bytes. */
 int qal_block_ordered_scan(const qal_block_plan *plan, int batch, int count, const qal_c128 *U,

@@ -289,6 +289,10 @@ size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices);
 int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
                            double* grad, double2* Lam, int* status, void* ws, cudaStream_t st,
                            const double2* Cseed = nullptr);
+int blk_forward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, double2* Lam, int* status, void* ws,
+                     cudaStream_t st);
+int blk_backward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* grad,
+                      int* status, void* ws, cudaStream_t st, const double2* Cseed);
 
 // chunk of the block forward fold: keep >= ~4 CTAs per SM busy, chunk | n_slices
 int blk_default_chunk(int batch, int n_slices) {
@@ -864,6 +868,44 @@ int qal_block_propagator_vjp(const qal_block_plan* plan, int batch, int n_slices
   return blk_fidelity_grad_impl(plan, batch, c, nullptr, nullptr, grad, D2(Lambda_packed), status, ws, st, D2(Cp));
 }
 
+int qal_block_propagator_forward(const qal_block_plan* plan, int batch, int n_slices, double T, int k0, int count,
+                                 int magnus_order, int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0p,
+                                 long long L0p_stride, const qal_c128* Lcp, const qal_c128* Lcommp,
+                                 long long Lcommp_stride, qal_c128* Lambda_packed, int* status, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  BlkCommon c;
+  int rc = check_block_basis(plan, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0p, L0p_stride, Lcp,
+                             Lcommp, Lcommp_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!Lambda_packed) return QAL_ERR_NULL;
+  c.G.count = count;
+  if (!ws || ws_bytes < qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count)) return QAL_ERR_WORKSPACE;
+  cudaStream_t st = S(stream);
+  if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
+  return blk_forward_impl(plan, batch, c, D2(Lambda_packed), status, ws, st);
+}
+
+int qal_block_propagator_backward(const qal_block_plan* plan, int batch, int n_slices, double T, int k0, int count,
+                                  int magnus_order, int ctrl_mode, int n_ctrl, const double* u, const qal_c128* L0p,
+                                  long long L0p_stride, const qal_c128* Lcp, const qal_c128* Lcommp,
+                                  long long Lcommp_stride, const qal_c128* Cp, double* grad, int* status, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  launch_counter() = 0;
+  BlkCommon c;
+  int rc = check_block_basis(plan, batch, n_slices, T, magnus_order, ctrl_mode, n_ctrl, u, L0p, L0p_stride, Lcp,
+                             Lcommp, Lcommp_stride, c);
+  if (rc != QAL_OK) return rc;
+  if (count < 1) return QAL_ERR_EMPTY;
+  if (k0 < 0 || (long long)k0 + count > n_slices) return QAL_ERR_DIM;
+  if (!Cp || !grad) return QAL_ERR_NULL;
+  c.G.count = count;
+  if (!ws || ws_bytes < qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count)) return QAL_ERR_WORKSPACE;
+  return blk_backward_impl(plan, batch, c, nullptr, grad, status, ws, S(stream), D2(Cp));
+}
+
 int qal_block_ordered_scan(const qal_block_plan* plan, int batch, int count, const qal_c128* U,
                            qal_c128* prefix_excl, qal_c128* suffix_excl, void* ws, size_t ws_bytes, void* stream) {
   launch_counter() = 0;
@@ -936,24 +978,48 @@ size_t blk_grad_ws_bytes(const qal_block_plan* p, int batch, int n_slices) {
   const size_t img = (size_t)p->packed * 16;
   return 3 * (size_t)batch * n_slices * img + (size_t)batch * img + blk_grad_scratch_bytes(*p, batch, n_slices);
 }
-// forward (U_k and prefix P_k images, Lambda) -> fidelity -> suffix chain (X_{k+1}) -> gradient slices
-int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
-                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st,
-                           const double2* Cseed) {
-  const size_t seq = (size_t)batch * c.G.count * 2 * p->packed;   // doubles per image sequence
-  double* U = reinterpret_cast<double*>(ws);
-  double* P = U + seq;
-  double* X = P + seq;
-  double2* lam_tmp = reinterpret_cast<double2*>(X + seq);
-  unsigned short* scheme = reinterpret_cast<unsigned short*>(lam_tmp + (size_t)batch * p->packed);
-  double2* lam = Lam ? Lam : lam_tmp;
-  BlkFwdOut O{U, lam, c.G.count, status, P, scheme};
-  if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (F && launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_blk_suffix_chain(*p, batch, c.G.count, U, V, Cseed, X, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_blk_grad_slices(*p, batch, c.B, c.G, P, X, grad, status, scheme, Cseed ? 1.0 : 1.0 / 64.0, st) !=
+// workspace layout of the block gradient path: U_k, P_k, X_{k+1} image sequences, Lambda, scheme codes
+struct BlkGradWs {
+  double *U, *P, *X;
+  double2* lam_tmp;
+  unsigned short* scheme;
+};
+BlkGradWs blk_grad_ws(const qal_block_plan* p, int batch, int count, void* ws) {
+  const size_t seq = (size_t)batch * count * 2 * p->packed;   // doubles per image sequence
+  BlkGradWs w;
+  w.U = reinterpret_cast<double*>(ws);
+  w.P = w.U + seq;
+  w.X = w.P + seq;
+  w.lam_tmp = reinterpret_cast<double2*>(w.X + seq);
+  w.scheme = reinterpret_cast<unsigned short*>(w.lam_tmp + (size_t)batch * p->packed);
+  return w;
+}
+// forward (U_k and prefix P_k images, scheme codes, Lambda) of the gradient path
+int blk_forward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, double2* Lam, int* status, void* ws,
+                     cudaStream_t st) {
+  const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
+  BlkFwdOut O{w.U, Lam ? Lam : w.lam_tmp, c.G.count, status, w.P, w.scheme};
+  return cuda_rc(launch_blk_expm_fold(*p, batch, c.B, c.G, O, st));
+}
+// reverse pass on a stored forward: suffix chain (X_{k+1}, seeded by S_V^dag or Cseed) -> gradient slices
+int blk_backward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* grad,
+                      int* status, void* ws, cudaStream_t st, const double2* Cseed) {
+  const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
+  if (launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, Cseed, w.X, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (launch_blk_grad_slices(*p, batch, c.B, c.G, w.P, w.X, grad, status, w.scheme, Cseed ? 1.0 : 1.0 / 64.0, st) !=
       cudaSuccess)
     return QAL_ERR_CUDA;
   return QAL_OK;
+}
+// forward -> fidelity -> suffix chain -> gradient slices
+int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* F,
+                           double* grad, double2* Lam, int* status, void* ws, cudaStream_t st,
+                           const double2* Cseed) {
+  const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
+  double2* lam = Lam ? Lam : w.lam_tmp;
+  int rc = blk_forward_impl(p, batch, c, lam, status, ws, st);
+  if (rc != QAL_OK) return rc;
+  if (F && launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
+  return blk_backward_impl(p, batch, c, V, grad, status, ws, st, Cseed);
 }
 }  // namespace

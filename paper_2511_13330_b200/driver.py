@@ -383,12 +383,18 @@ def time_sharded_gradient(L0, Lc, Lcomm, u_local, T, n_slices, k0, *, ctrl_mode,
 
 def _time_sharded_gradient_blocks(plan, L0p, Lcp, Lcommp, u_local, T, n_slices, k0, *, ctrl_mode, cotangent,
                                   magnus_order, sub, group_subsegments, group, stream):
+    """Block path of time_sharded_gradient: ONE forward over all sub-segments (qal_block_propagator_forward:
+    its per-sub-segment Lambda are the partials Q_s, and it keeps every U_k, P_k and (m, s) choice), then
+    the scans / all-gather / seeds, then only the reverse pass on the stored forward
+    (qal_block_propagator_backward) -- no slice is exponentiated twice.  The stored forward takes
+    3 packed images per slice (45 GB for 2^20 slices at G = 1); group_subsegments is not used here."""
     count = u_local.shape[1]
     S = count // sub
     bmm = lambda A, B: qal.qal_block_batched_matmul(plan, A, B, stream=stream)  # noqa: E731
-    parts = qal.qal_block_expm_slices(plan, L0p, Lcp, u_local, T, n_slices, k0=k0, count=count,
-                                      magnus_order=magnus_order, ctrl_mode=ctrl_mode, Lcommp=Lcommp, chunk=sub,
-                                      stream=stream)                                   # [1][S][packed]
+    us = u_local[0].reshape((S, sub) + tuple(u_local.shape[2:])).contiguous()
+    sess = qal.BlockGradientSession(plan, L0p, Lcp, us, T, n_slices, magnus_order=magnus_order,
+                                    ctrl_mode=ctrl_mode, Lcommp=Lcommp, stream=stream)
+    parts = sess.forward().unsqueeze(0)                                               # [1][S][packed]
     pre, suf = qal.qal_block_ordered_scan(plan, parts, stream=stream)
     Q_rank = bmm(parts[0, S - 1], pre[0, S - 1])[0]
     ranks = gather_partials(Q_rank, group)                                             # [G][packed]
@@ -398,14 +404,8 @@ def _time_sharded_gradient_blocks(plan, L0p, Lcp, Lcommp, u_local, T, n_slices, 
                   lambda X, Y: bmm(X, Y)[0])
     seeds = bmm(pre[0], bmm(C, suf[0]))                                                # pre_s C_r suf_s
     del pre, suf, parts
-    us = u_local[0].reshape((S, sub) + tuple(u_local.shape[2:]))
-    grad = torch.empty_like(us)
-    for g0 in range(0, S, group_subsegments):
-        g1 = min(S, g0 + group_subsegments)
-        g, _ = qal.qal_block_propagator_vjp(plan, L0p, Lcp, us[g0:g1].contiguous(), T, n_slices,
-                                           seeds[g0:g1].contiguous(), magnus_order=magnus_order,
-                                           ctrl_mode=ctrl_mode, Lcommp=Lcommp, stream=stream)
-        grad[g0:g1] = g
+    grad = sess.vjp(seeds)
+    del sess
     return Lam, grad.reshape(u_local.shape)
 
 

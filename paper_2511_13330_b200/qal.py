@@ -112,6 +112,19 @@ _EXPORTS = {
                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                                 ctypes.c_void_p]),
     "qal_block_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "qal_block_propagator_forward": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                                     ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                                     ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "qal_block_propagator_backward": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                                      ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                                      ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                                      ctypes.c_void_p]),
     "qal_block_propagator_vjp": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
@@ -630,6 +643,51 @@ def qal_block_propagator_vjp(plan: BlockPlan, L0p, Lcp, u, T, n_slices, Cp, *, k
                                          _stream(stream))
     _check(rc, "qal_block_propagator_vjp")
     return g, Lam
+
+
+class BlockGradientSession:
+    """qal_block_propagator_forward / _backward around one workspace: forward() stores the U_k, P_k and
+    scheme codes of slices k0..k0+count-1 and returns the packed Lambda [B][packed]; vjp(Cp) runs only the
+    reverse pass for the packed cotangent Cp [B][packed] (the GradientSession of the block path)."""
+
+    def __init__(self, plan: BlockPlan, L0p, Lcp, u, T, n_slices, *, k0=0, count=None, magnus_order=4,
+                 ctrl_mode=QAL_CTRL_PWC, Lcommp=None, status=None, stream=None):
+        c128 = torch.complex128
+        self.plan = plan
+        self.L0p = _dev(L0p, c128, "L0p")
+        self.Lcp = _dev(Lcp, c128, "Lcp")
+        self.u = _dev(u, torch.float64, "u")
+        self.B, self.J = self.u.shape[0], self.Lcp.shape[0]
+        self.count = self.u.shape[1] if count is None else count
+        self.args = (float(T), k0, self.count, magnus_order, ctrl_mode)
+        self.n_slices = n_slices
+        self.L0s = 0 if self.L0p.shape[0] == 1 else plan.packed
+        self.Lcommp = None if Lcommp is None else _dev(Lcommp, c128, "Lcommp")
+        self.Lcs = 0 if self.Lcommp is None or self.Lcommp.shape[0] == 1 else n_comm(self.J) * plan.packed
+        self.status = status
+        self.stream = stream
+        wsb = block_workspace_bytes(plan, QAL_OP_VJP, self.B, self.count)
+        self.ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=self.u.device)
+
+    def _common(self):
+        T, k0, count, order, mode = self.args
+        return (ctypes.byref(self.plan), self.B, self.n_slices, T, k0, count, order, mode, self.J, _ptr(self.u),
+                _ptr(self.L0p), self.L0s, _ptr(self.Lcp), _ptr(self.Lcommp), self.Lcs)
+
+    def forward(self):
+        Lam = torch.empty((self.B, self.plan.packed), dtype=torch.complex128, device=self.u.device)
+        rc = load().qal_block_propagator_forward(*self._common(), _ptr(Lam), _ptr(self.status), _ptr(self.ws),
+                                                 self.ws.numel(), _stream(self.stream))
+        _check(rc, "qal_block_propagator_forward")
+        return Lam
+
+    def vjp(self, Cp):
+        Cp = _dev(Cp, torch.complex128, "Cp")
+        g = torch.empty_like(self.u)
+        rc = load().qal_block_propagator_backward(*self._common(), _ptr(Cp), _ptr(g), _ptr(self.status),
+                                                  _ptr(self.ws), self.ws.numel(), _stream(self.stream))
+        _check(rc, "qal_block_propagator_backward")
+        return g
 
 
 def qal_block_ordered_scan(plan: BlockPlan, U, want_prefix=True, want_suffix=True, stream=None):

@@ -319,6 +319,31 @@ def test_block_vjp_general_cotangent_matches_oracle(torch_cuda, qal, oracle):
     assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
 
 
+def test_block_forward_backward_session_equals_one_call_vjp_and_oracle(torch_cuda, qal, oracle):
+    """qal_block_propagator_forward + _backward (the stored forward of the time-sharded gradient) give
+    bit for bit the Lambda and gradient of the one-call qal_block_propagator_vjp, and the oracle's
+    per-direction vjp; the cotangent is built from the forward's Lambda in between (NODES mode with the
+    commutator basis, so the stored (m, s) codes and the commutator traces are exercised)."""
+    torch = torch_cuda
+    p = qi.cfg3(N=96, T=40.0)
+    plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
+    u = qal.qal_sample_controls_sines(dev(torch, p.sines), p.u_max, p.N, p.T).reshape(3, 32, 2, 2).contiguous()
+    sess = qal.BlockGradientSession(plan, L0p, Lcp, u, p.T, p.N, ctrl_mode=1, Lcommp=Lcommp)
+    Lam = sess.forward()
+    C = qal.qal_block_fidelity_cotangent(plan, dev(torch, p.V)).unsqueeze(0).repeat(3, 1).contiguous()
+    C = qal.qal_block_batched_matmul(plan, C, Lam)      # a cotangent that depends on the forward's Lambda
+    g = sess.vjp(C)
+    g1, L1 = qal.qal_block_propagator_vjp(plan, L0p, Lcp, u, p.T, p.N, C, ctrl_mode=1, Lcommp=Lcommp,
+                                          want_Lambda=True)
+    assert torch.equal(Lam, L1) and torch.equal(g, g1)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Cn = qal.qal_block_unpack(plan, C)
+    un = u.cpu().numpy()
+    for b in range(3):
+        gr, _ = oracle.vjp(rL0, rLc, un[b], p.T * 32 / p.N, 32, Cn[b].cpu().numpy(), mode=1)
+        assert relfro(g[b].cpu().numpy(), gr) <= TOL_GRAD
+
+
 def test_block_scan_and_batched_matmul(torch_cuda, qal, oracle):
     torch = torch_cuda
     p = qi.cfg0(N=11, T=100.0 * 11 / 256)
