@@ -244,7 +244,10 @@ def roofline_of(stages, prods, steps, peak_tf, units_per_launch):
     counts its fold products apart (blk_prefix_chain, no launches of its own): they belong to its time."""
     from paper_2511_13330_b200 import driver, qal
     fl = {s: driver.stage_flops(prods[i], s) for i, s in enumerate(qal.STAGES)}
-    fl["blk_expm_fold"] += fl["blk_prefix_chain"] if stages["blk_prefix_chain"][1] == 0 else 0.0
+    if stages["blk_prefix_chain"][1] == 0:          # fused forward: its fold flops belong to its own time
+        fl["blk_expm_fold"] += fl["blk_prefix_chain"]
+    elif stages["blk_suffix_chain"][1] == 0:        # prefix and suffix chains timed as one concurrent launch
+        fl["blk_prefix_chain"] += fl["blk_suffix_chain"]
     dom = max(stages, key=lambda s: stages[s][0])
     dom_ms, dom_launch = stages[dom]
     dom_flops_per_launch = fl[dom] / max(dom_launch, 1)
@@ -266,19 +269,23 @@ def roofline_of(stages, prods, steps, peak_tf, units_per_launch):
 
 def fig2_split(qal, stages, prods, steps):
     """The Fig. 2 analog (matrix exponentials vs the ordered multiplication): algorithmic
-    flops per step of the slice expansions (Eq. 14) and of the products (Eq. 15: the prefix fold, counted
-    apart inside the fused forward kernel, and the suffix chain), with the fused kernel's time apportioned
-    by its two flop counts (same kernel, same efficiency)."""
+    flops and device time per step of the slice expansions (Eq. 14: the persistent expm kernel) and of the
+    products (Eq. 15: the prefix fold and the suffix chain, two concurrent chains timed as one launch).
+    (Paths with the fused chunk forward apportion that kernel's time by its two flop counts.)"""
     ix = qal.STAGES.index
     f_exp, f_fold = prods[ix("blk_expm_fold")], prods[ix("blk_prefix_chain")]
     f_suf = prods[ix("blk_suffix_chain")]
     t_fwd = stages["blk_expm_fold"][0]
-    t_exp = t_fwd * f_exp / max(f_exp + f_fold, 1)
-    t_mul = t_fwd - t_exp + stages["blk_suffix_chain"][0]
+    if stages["blk_prefix_chain"][1] > 0:
+        t_exp, t_mul = t_fwd, stages["blk_prefix_chain"][0] + stages["blk_suffix_chain"][0]
+        note = "expansions: the persistent expm kernel; products: the prefix and suffix chains (concurrent)"
+    else:
+        t_exp = t_fwd * f_exp / max(f_exp + f_fold, 1)
+        t_mul = t_fwd - t_exp + stages["blk_suffix_chain"][0]
+        note = "fused expm + fold kernel: its time apportioned by flops"
     return {"expansion": {"flops_per_step": f_exp / steps, "ms_per_step": t_exp / steps},
             "multiplication": {"flops_per_step": (f_fold + f_suf) / steps, "ms_per_step": t_mul / steps},
-            "note": "forward fold time apportioned by flops inside the fused expm + fold kernel; the gradient "
-                    "stage (dual expansion + products) is reported apart in stage_split"}
+            "note": note + "; the gradient stage (dual expansion + products) is reported apart in stage_split"}
 
 
 def dense_reference(args, driver, qal, torch, H0, Hc, C, u, V, T, B, N, world, peak_tf, barrier):

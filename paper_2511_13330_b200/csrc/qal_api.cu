@@ -290,9 +290,9 @@ int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& 
                            double* grad, double2* Lam, int* status, void* ws, cudaStream_t st,
                            const double2* Cseed = nullptr);
 int blk_forward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, double2* Lam, int* status, void* ws,
-                     cudaStream_t st);
+                     cudaStream_t st, bool with_suffix, const double2* V);
 int blk_backward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* grad,
-                      int* status, void* ws, cudaStream_t st, const double2* Cseed);
+                      int* status, void* ws, cudaStream_t st, const double2* Cseed, bool suffix_done);
 
 // chunk of the block forward fold: keep >= ~4 CTAs per SM busy, chunk | n_slices
 int blk_default_chunk(int batch, int n_slices) {
@@ -885,7 +885,7 @@ int qal_block_propagator_forward(const qal_block_plan* plan, int batch, int n_sl
   if (!ws || ws_bytes < qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count)) return QAL_ERR_WORKSPACE;
   cudaStream_t st = S(stream);
   if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
-  return blk_forward_impl(plan, batch, c, D2(Lambda_packed), status, ws, st);
+  return blk_forward_impl(plan, batch, c, D2(Lambda_packed), status, ws, st, false, nullptr);
 }
 
 int qal_block_propagator_backward(const qal_block_plan* plan, int batch, int n_slices, double T, int k0, int count,
@@ -903,7 +903,7 @@ int qal_block_propagator_backward(const qal_block_plan* plan, int batch, int n_s
   if (!Cp || !grad) return QAL_ERR_NULL;
   c.G.count = count;
   if (!ws || ws_bytes < qal_block_workspace_bytes(plan, QAL_OP_VJP, batch, count)) return QAL_ERR_WORKSPACE;
-  return blk_backward_impl(plan, batch, c, nullptr, grad, status, ws, S(stream), D2(Cp));
+  return blk_backward_impl(plan, batch, c, nullptr, grad, status, ws, S(stream), D2(Cp), false);
 }
 
 int qal_block_ordered_scan(const qal_block_plan* plan, int batch, int count, const qal_c128* U,
@@ -994,18 +994,35 @@ BlkGradWs blk_grad_ws(const qal_block_plan* p, int batch, int count, void* ws) {
   w.scheme = reinterpret_cast<unsigned short*>(w.lam_tmp + (size_t)batch * p->packed);
   return w;
 }
-// forward (U_k and prefix P_k images, scheme codes, Lambda) of the gradient path
+// forward of the gradient path, two layouts with the same results (U_k images, prefix P_k images, (m, s)
+// codes, Lambda):
+//  * fused (large batches): one CTA slot per pulse folds its slices in order -- expm + prefix product per
+//    slice in one kernel; 19.4 KB of images written per slice.
+//  * split (small batches, e.g. the 512 pulses per GPU of configs[2] at G = 8, where one chain per pulse
+//    leaves the fused kernel latency-bound in a single wave): the persistent expm kernel exponentiates every
+//    slice independently (full occupancy), then the prefix chain folds the stored U_k -- concurrently with
+//    the suffix chain when its seed is known (the fidelity gradient).  Costs one more read of the U_k
+//    images per chain (the chains run at ~85% of the HBM bandwidth).
+bool blk_split_forward(int batch) { return batch < 8 * num_sms(); }
 int blk_forward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, double2* Lam, int* status, void* ws,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool with_suffix, const double2* V) {
   const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
-  BlkFwdOut O{w.U, Lam ? Lam : w.lam_tmp, c.G.count, status, w.P, w.scheme};
-  return cuda_rc(launch_blk_expm_fold(*p, batch, c.B, c.G, O, st));
+  double2* lam = Lam ? Lam : w.lam_tmp;
+  if (!blk_split_forward(batch)) {
+    BlkFwdOut O{w.U, lam, c.G.count, status, w.P, w.scheme};
+    if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+    return with_suffix ? cuda_rc(launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, nullptr, w.X, st)) : QAL_OK;
+  }
+  BlkFwdOut O{w.U, nullptr, 1, status, nullptr, w.scheme};
+  if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+  return cuda_rc(launch_blk_chains(*p, batch, c.G.count, w.U, w.P, lam, V, nullptr, with_suffix ? w.X : nullptr, st));
 }
 // reverse pass on a stored forward: suffix chain (X_{k+1}, seeded by S_V^dag or Cseed) -> gradient slices
 int blk_backward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* grad,
-                      int* status, void* ws, cudaStream_t st, const double2* Cseed) {
+                      int* status, void* ws, cudaStream_t st, const double2* Cseed, bool suffix_done) {
   const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
-  if (launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, Cseed, w.X, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (!suffix_done && launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, Cseed, w.X, st) != cudaSuccess)
+    return QAL_ERR_CUDA;
   if (launch_blk_grad_slices(*p, batch, c.B, c.G, w.P, w.X, grad, status, w.scheme, Cseed ? 1.0 : 1.0 / 64.0, st) !=
       cudaSuccess)
     return QAL_ERR_CUDA;
@@ -1017,9 +1034,10 @@ int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& 
                            const double2* Cseed) {
   const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
   double2* lam = Lam ? Lam : w.lam_tmp;
-  int rc = blk_forward_impl(p, batch, c, lam, status, ws, st);
+  const bool fid = Cseed == nullptr;   // the seed S_V^dag is known up front: suffix chain beside the prefix
+  int rc = blk_forward_impl(p, batch, c, lam, status, ws, st, fid, V);
   if (rc != QAL_OK) return rc;
   if (F && launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
-  return blk_backward_impl(p, batch, c, V, grad, status, ws, st, Cseed);
+  return blk_backward_impl(p, batch, c, V, grad, status, ws, st, Cseed, fid);
 }
 }  // namespace

@@ -994,7 +994,10 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     const double nrm = bnorm1(A, red, x, L);
     int m, s;
     choose_scheme_blk(nrm, m, s);
-    if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+    if (!(nrm <= 1e300) && L.lane == 0) {
+      *bad = 1;
+      if (O.status) O.status[b] = QAL_ERR_NONFINITE;   // (idempotent write; persistent items)
+    }
     if (O.scheme && leader) O.scheme[((size_t)b * G.count + k) * D.ngroups + x.g] = scheme_code(nrm, m, s);
     bscale(A, ldexp(1.0, -s));
     bstore_img(SX, A, x, L);
@@ -1045,25 +1048,23 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
     const Ctx x = ctx_of(D, T);
-    const int item = blockIdx.x * D.nslot + x.slot;   // slot x.slot: its own item, warps and regions
-    if (item >= items) continue;
     double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
     QAL_DCHECK(D.soff[x.g] < D.sstride && (size_t)(x.slot + 1) * D.sstride * 8 <= dyn_smem_bytes());
-    if constexpr (FC == 0)
-      BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
-                   nflop, L);
-    else
-      blk_fwd_task<FC, FR, FKS, FRE != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop, L);
+    // persistent: slot x.slot (its own warps and regions) runs items item0, item0 + stride, ...; every
+    // warp of the slot follows the same sequence, so the group barriers match
+    for (int item = blockIdx.x * D.nslot + x.slot; item < items; item += gridDim.x * D.nslot) {
+      if constexpr (FC == 0)
+        BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
+                     nflop, L);
+      else
+        blk_fwd_task<FC, FR, FKS, FRE != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop, L);
+      grp_sync(x);   // the slot's regions are reused by its next item
+    }
   }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   if (L.w == 0) blk_tmem_dealloc(tmem_base_sh, tmem_cols);
-  const int nchunk = G.count / O.chunk;
-  if (O.status && threadIdx.x < D.nslot && bad_sh[threadIdx.x]) {
-    const int item = blockIdx.x * D.nslot + threadIdx.x;
-    if (item < items) O.status[item / nchunk] = QAL_ERR_NONFINITE;
-  }
   if (ctr && nflop[0]) atomicAdd(ctr, nflop[0]);
   if (ctr_fold && nflop[1]) atomicAdd(ctr_fold, nflop[1]);
 }
@@ -1440,6 +1441,88 @@ __global__ void __launch_bounds__(BLK_CHAIN_WARPS * 32) k_blk_suffix_chain(BlkDe
                    bars[x.bar], nflop, L);
     else
       blk_suffix_task<FC, FR, FKS, FRE != 0>(D, N, U_img + base, V, cs, X_img + base, x, sm, bars[x.bar], nflop, L);
+  }
+  if (ctr && nflop) atomicAdd(ctr, nflop);
+}
+
+// --------------------------------------------------------------- prefix chain
+// The gradient path's forward fold as a chain of its own (the slices' exponentials come from the
+// persistent expm kernel, chunk = 1): P_0 = I, P_{k+1} = U_k P_k (later slice on the LEFT, Eq. 15),
+// P_img[b][k] = P_k (k = 0..N-1), and Lambda = U_{N-1} P_{N-1} -> lam[b] (packed natural).  U_k streamed
+// by per-group TMA (double buffer) like the suffix chain; the running product is the right-hand operand,
+// so it lives in a ping-pong pair of shared images (one group barrier per step).
+template <int C, int R, int KS, bool RE>
+__device__ void blk_prefix_task(const BlkDev& D, int N, const double* U, double* P, double2* lam, const Ctx& x,
+                                double* sm, uint64_t* bar, unsigned long long& nflop, const Lane& L) {
+  constexpr int IM = img_doubles(C, RE);
+  double* SU[2] = {sm, sm + IM};
+  double* SP[2] = {sm + 2 * IM, sm + 3 * IM};
+  const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
+  const int go = 2 * x.off;
+  const bool leader = (x.rt0 == 0 && L.lane == 0);
+  BR<C, R, RE> A, acc;
+  bset_identity(acc, x, L);                                          // P_0 = I
+  bstore_img_l2(P + go, acc, x, L, l2_evict_first());
+  if (leader) tma_grp_img(SU[0], U + go, C, &bar[0], RE);
+  uint32_t ph[2] = {0, 0};
+  for (int k = 0; k < N; ++k) {
+    const int cur = k & 1;
+    grp_sync(x);   // SP[cur] holds P_k (all rows); SU[cur ^ 1], SP[cur ^ 1] were last read at step k - 1
+    if (leader && k + 1 < N) {
+      fence_proxy_async();
+      tma_grp_img(SU[cur ^ 1], U + (size_t)(k + 1) * stride + go, C, &bar[cur ^ 1], RE);
+    }
+    mbar_wait(&bar[cur], ph[cur]);
+    ph[cur] ^= 1;
+    bload_img(A, SU[cur], x, L);                                     // own rows of U_k
+    if (k == 0) {
+      bcopy(acc, A);                                                 // P_1 = U_0
+    } else {
+      bzero(acc);
+      bmma<C, R, KS, RE>(acc, A, SP[cur], x, L);                     // P_{k+1} = U_k P_k
+    }
+    if (k + 1 < N) {
+      bstore_img_l2(P + (size_t)(k + 1) * stride + go, acc, x, L, l2_evict_first());
+      bstore_img(SP[cur ^ 1], acc, x, L);
+    }
+  }
+  bstore_nat(lam + x.off, acc, x, L);                                // Lambda = U_{N-1} P_{N-1}
+  if (leader) nflop += (unsigned long long)(N - 1) * D.gflops[x.g];
+}
+
+template <int FC, int FR, int FKS, int FRE>   // as k_blk_grad_slices: FC == 0 any roles
+__global__ void __launch_bounds__(BLK_CHAIN_WARPS * 32) k_blk_prefix_chain(BlkDev D, int batch, int N,
+                                                                        const double* __restrict__ U_img,
+                                                                        double* __restrict__ P_img,
+                                                                        double2* __restrict__ lam,
+                                                                        unsigned long long* ctr) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id
+  const Lane L = lane_id();
+  for (int t = 0; t < D.ntask[L.w]; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    if (T.rt0 == 0 && L.lane == 0) {
+      mbar_init(&bars[T.bar][0], 1);
+      mbar_init(&bars[T.bar][1], 1);
+    }
+  }
+  fence_mbar_init();
+  __syncthreads();
+  unsigned long long nflop = 0;
+  for (int t = 0; t < D.ntask[L.w]; ++t) {
+    const BlkTask T = D.task[L.w][t];
+    const Ctx x = ctx_of(D, T);
+    const int b = blockIdx.x * D.nslot + x.slot;   // the slot's pulse
+    if (b >= batch) continue;
+    const size_t base = (size_t)b * N * 2 * D.packed;
+    double* sm = smem + D.soff[x.g] + (size_t)x.slot * D.sstride;
+    QAL_DCHECK(D.soff[x.g] < D.sstride && (size_t)(x.slot + 1) * D.sstride * 8 <= dyn_smem_bytes());
+    if constexpr (FC == 0)
+      BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_prefix_task, D, N, U_img + base, P_img + base,
+                   lam + (size_t)b * D.packed, x, sm, bars[x.bar], nflop, L);
+    else
+      blk_prefix_task<FC, FR, FKS, FRE != 0>(D, N, U_img + base, P_img + base, lam + (size_t)b * D.packed, x, sm,
+                                             bars[x.bar], nflop, L);
   }
   if (ctr && nflop) atomicAdd(ctr, nflop);
 }
@@ -2072,6 +2155,15 @@ static ChainKernel chain_kernel(const BlkDev& D) {
     default: return k_blk_suffix_chain<0, 0, 0, 0>;
   }
 }
+using PrefixKernel = void (*)(BlkDev, int, int, const double*, double*, double2*, unsigned long long*);
+static PrefixKernel prefix_kernel(const BlkDev& D) {
+  switch (blk_role(D)) {
+    case 1: return k_blk_prefix_chain<3, 1, 5, 1>;
+    case 2: return k_blk_prefix_chain<2, 1, 4, 0>;
+    case 3: return k_blk_prefix_chain<1, 1, 2, 0>;
+    default: return k_blk_prefix_chain<0, 0, 0, 0>;
+  }
+}
 static FwdKernel fwd_kernel(const BlkDev& D) {
   switch (blk_role(D)) {
     case 1: return k_blk_expm_fold<3, 1, 5, 1>;
@@ -2100,6 +2192,7 @@ int per3(int C, bool re) { return grp3_doubles(C, re); }
 int per_grad(int C, bool re) { return grp3_doubles(C, re) + 4 * img_doubles(C, re); }
 int per_pair(int C, bool re) { return img_doubles(C, re); }
 int per_chain(int C, bool re) { return 2 * img_doubles(C, re); }
+int per_prefix(int C, bool re) { return 4 * img_doubles(C, re); }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 }  // namespace
 
@@ -2197,7 +2290,7 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
   const int items = batch * (G.count / O.chunk);
   std::vector<BlkSet> sets;
   blk_sets(p, 0, sets);
-  struct L { BlkDev D; FwdKernel fn; size_t bytes; };
+  struct L { BlkDev D; FwdKernel fn; size_t bytes; int per_sm; };
   std::vector<L> ls;
   for (const BlkSet& set : sets) {
     // item slots per CTA: the count that keeps the most items in flight (co-resident CTAs x slots, at most
@@ -2218,6 +2311,7 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
           continue;
         const long long slots = (long long)per_sm * num_sms() * ns;
         const long long used = std::min<long long>(slots, items);
+        t.per_sm = per_sm;
         if (!have || used > best) { l = t; best = used; have = true; }
       }
     if (!have) return cudaErrorInvalidValue;
@@ -2228,10 +2322,11 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
   prof_pre(ST_BLK_EXPM, st);
   const cudaError_t e = fork_join(st, (int)ls.size(), [&](int i, cudaStream_t s) {
     const L& l = ls[i];
-    l.fn<<<(items + l.D.nslot - 1) / l.D.nslot, 32 * l.D.nwarps, l.bytes, s>>>(l.D, B, G, O, items,
-                                                                              tmem_cols_for(l.D),
-                                                                              prof_counter(ST_BLK_EXPM),
-                                                                              prof_counter(ST_BLK_PREFIX));
+    // persistent grid: at most the co-resident CTAs (one chunk per item, or one slice per item with chunk 1)
+    const int need = (items + l.D.nslot - 1) / l.D.nslot;
+    const int grid = std::min(need, l.per_sm * num_sms());
+    l.fn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, B, G, O, items, tmem_cols_for(l.D), prof_counter(ST_BLK_EXPM),
+                                                prof_counter(ST_BLK_PREFIX));
     ++launch_counter();
     return cudaGetLastError();
   });
@@ -2278,6 +2373,48 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
     return cudaGetLastError();
   });
   prof_post(ST_BLK_SUFFIX, st);
+  return e;
+}
+
+// The gradient path's two chains on the stored U_k images, concurrently (fork / join over their group
+// launches): the prefix fold P_{k+1} = U_k P_k (P_img, Lambda) and the suffix X_k = X_{k+1} U_k (X_img,
+// seeded with S_V^dag or Cseed).  Either may be skipped (P_img == nullptr / X_img == nullptr).
+cudaError_t launch_blk_chains(const qal_block_plan& p, int batch, int N, const double* U_img, double* P_img,
+                              double2* lam, const double2* V, const double2* Cseed, double* X_img, cudaStream_t st) {
+  std::vector<BlkSet> sets;
+  blk_sets(p, 2, sets);
+  struct L { BlkDev D; PrefixKernel pfn; ChainKernel cfn; size_t bytes; bool prefix; };
+  std::vector<L> ls;
+  for (int pre = 1; pre >= 0; --pre) {
+    if ((pre && !P_img) || (!pre && !X_img)) continue;
+    for (const BlkSet& set : sets) {
+      int ns = set.nslot;   // fewer pulses per CTA when the batch would not fill two CTAs per SM
+      while (ns > 1 && (batch + ns - 1) / ns < 2 * num_sms()) ns >>= 1;
+      L l;
+      l.prefix = pre != 0;
+      if (!to_dev(p, l.D, set.gmask, ns)) return cudaErrorInvalidValue;
+      l.bytes = (size_t)grp_smem_doubles(l.D, pre ? per_prefix : per_chain) * 8;
+      l.pfn = pre ? prefix_kernel(l.D) : nullptr;
+      l.cfn = pre ? nullptr : chain_kernel(l.D);
+      cudaError_t e = set_smem_fn(pre ? (const void*)l.pfn : (const void*)l.cfn, l.bytes);
+      if (e != cudaSuccess) return e;
+      ls.push_back(l);
+    }
+  }
+  const int stage = P_img ? ST_BLK_PREFIX : ST_BLK_SUFFIX;   // one timing record for the concurrent chains
+  prof_pre(stage, st);
+  const cudaError_t e = fork_join(st, (int)ls.size(), [&](int i, cudaStream_t s) {
+    const L& l = ls[i];
+    const int grid = (batch + l.D.nslot - 1) / l.D.nslot;
+    if (l.prefix)
+      l.pfn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, batch, N, U_img, P_img, lam, prof_counter(ST_BLK_PREFIX));
+    else
+      l.cfn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, batch, N, U_img, V, Cseed, X_img,
+                                                  prof_counter(ST_BLK_SUFFIX));
+    ++launch_counter();
+    return cudaGetLastError();
+  });
+  prof_post(stage, st);
   return e;
 }
 

@@ -69,6 +69,8 @@ cudaError_t launch_blk_unpack(const qal_block_plan& p, int count, const double2*
                               cudaStream_t st);
 cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, const double* U_img,
                                     const double2* V, const double2* Cseed, double* X_img, cudaStream_t st);
+cudaError_t launch_blk_chains(const qal_block_plan& p, int batch, int N, const double* U_img, double* P_img,
+                              double2* lam, const double2* V, const double2* Cseed, double* X_img, cudaStream_t st);
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,
                                    const double* P_img, const double* X_img, double* grad, int* status,
                                    const unsigned short* scheme, double gscale, cudaStream_t st);

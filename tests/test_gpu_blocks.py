@@ -319,6 +319,24 @@ def test_block_vjp_general_cotangent_matches_oracle(torch_cuda, qal, oracle):
     assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
 
 
+def test_fused_and_split_forward_layouts_are_bit_identical(torch_cuda, qal):
+    """The gradient path's forward runs fused (one slot per pulse: expm + prefix fold per slice) for large
+    batches and split (persistent expm over all slices, then the prefix chain beside the suffix chain)
+    for batches below 8 x SMs: the same arithmetic, so 1200 pulses in one call (fused) equal the same
+    pulses in two calls of 600 (split) bit for bit."""
+    torch = torch_cuda
+    B = 1200
+    assert B >= 8 * torch.cuda.get_device_properties(0).multi_processor_count
+    p = qi.cfg2(batch=B, N=6, T=200.0 * 6 / 1024)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    u, V = dev(torch, p.u), dev(torch, p.V)
+    F1, g1, L1 = qal.qal_block_fidelity_grad(plan, L0p, Lcp, u, p.T, p.N, V, want_Lambda=True)
+    parts = [qal.qal_block_fidelity_grad(plan, L0p[i:i + 600].contiguous(), Lcp, u[i:i + 600].contiguous(), p.T, p.N,
+                                         V, want_Lambda=True) for i in (0, 600)]
+    F2, g2, L2 = (torch.cat([a[k] for a in parts]) for k in range(3))
+    assert torch.equal(L1, L2) and torch.equal(F1, F2) and torch.equal(g1, g2)
+
+
 def test_block_forward_backward_session_equals_one_call_vjp_and_oracle(torch_cuda, qal, oracle):
     """qal_block_propagator_forward + _backward (the stored forward of the time-sharded gradient) give
     bit for bit the Lambda and gradient of the one-call qal_block_propagator_vjp, and the oracle's
