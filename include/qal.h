@@ -85,6 +85,8 @@ int qal_abi_version(void);
  */
 int qal_real_mults_per_complex_product(void);
 const char *qal_status_string(int code);
+/* the CUDA runtime's message for the error behind this host thread's last QAL_ERR_CUDA */
+const char *qal_last_cuda_error(void);
 
 /*
  * Eq. 8 from Eq. 6: the Liouvillian superoperator is linear

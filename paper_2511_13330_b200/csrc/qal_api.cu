@@ -122,7 +122,18 @@ using namespace qal;
 namespace {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-inline int cuda_rc(cudaError_t e) { return e == cudaSuccess ? QAL_OK : QAL_ERR_CUDA; }
+thread_local cudaError_t g_last_cuda_error = cudaSuccess;   // per host thread, for qal_last_cuda_error
+inline int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return QAL_OK;
+  g_last_cuda_error = e;
+  return QAL_ERR_CUDA;
+}
+// a failing runtime call or launcher: record its error and return QAL_ERR_CUDA
+#define QAL_TRY(expr)                                  \
+  do {                                                 \
+    const cudaError_t qal_e_ = (expr);                 \
+    if (qal_e_ != cudaSuccess) return cuda_rc(qal_e_); \
+  } while (0)
 inline const double2* D2(const qal_c128* p) { return reinterpret_cast<const double2*>(p); }
 inline double2* D2(qal_c128* p) { return reinterpret_cast<double2*>(p); }
 inline int ncomm_of(int J) { return J + J * (J - 1) / 2; }
@@ -187,7 +198,7 @@ int run_tree(int batch, int count, const double2* U, double2* out, void* ws, cud
     const int half = (cnt + 1) / 2;
     double2* dst = (half == 1) ? out : ((lvl & 1) ? bufB : bufA);
     cudaError_t e = launch_tree_level(batch, cnt, in, dst, st);
-    if (e != cudaSuccess) return QAL_ERR_CUDA;
+    QAL_TRY(e);
     in = dst;
     cnt = half;
     ++lvl;
@@ -277,7 +288,7 @@ int run_blk_tree(const qal_block_plan* p, int batch, int count, const double2* U
   while (cnt > 1) {
     const int half = (cnt + 1) / 2;
     double2* dst = (half == 1) ? out : ((lvl & 1) ? bufB : bufA);
-    if (launch_blk_tree_level(*p, batch, cnt, in, dst, st) != cudaSuccess) return QAL_ERR_CUDA;
+    QAL_TRY(launch_blk_tree_level(*p, batch, cnt, in, dst, st));
     in = dst;
     cnt = half;
     ++lvl;
@@ -352,17 +363,16 @@ int forward_impl(int batch, const Common& c, const double2* P_init, double2* Lam
                  cudaStream_t st) {
   GradWs g = grad_ws(ws, batch, c.G.count);
   FwdOut O{nullptr, g.U, nullptr, 1, status};
-  if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_prefix_chain(batch, c.G.count, g.U, g.P, Lam, P_init, st) != cudaSuccess) return QAL_ERR_CUDA;
+  QAL_TRY(launch_expm_fold(batch, c.B, c.G, O, st));
+  QAL_TRY(launch_prefix_chain(batch, c.G.count, g.U, g.P, Lam, P_init, st));
   return QAL_OK;
 }
 
 int vjp_impl(int batch, const Common& c, const double2* V, const double2* C, double gscale, double* grad, int* status,
              void* ws, cudaStream_t st) {
   GradWs g = grad_ws(ws, batch, c.G.count);
-  if (launch_suffix_chain(batch, c.G.count, g.U, V, C, g.X, st) != cudaSuccess) return QAL_ERR_CUDA;
-  if (launch_grad_slices(batch, c.B, c.G, g.P, g.X, grad, status, g.scratch, gscale, st) != cudaSuccess)
-    return QAL_ERR_CUDA;
+  QAL_TRY(launch_suffix_chain(batch, c.G.count, g.U, V, C, g.X, st));
+  QAL_TRY(launch_grad_slices(batch, c.B, c.G, g.P, g.X, grad, status, g.scratch, gscale, st));
   return QAL_OK;
 }
 
@@ -371,6 +381,12 @@ int vjp_impl(int batch, const Common& c, const double2* V, const double2* C, dou
 extern "C" {
 
 int qal_abi_version(void) { return QAL_ABI_VERSION; }
+
+const char* qal_last_cuda_error(void) {
+  // the CUDA error behind the last QAL_ERR_CUDA of this host thread (or the runtime's pending one)
+  const cudaError_t e = g_last_cuda_error != cudaSuccess ? g_last_cuda_error : cudaPeekAtLastError();
+  return cudaGetErrorString(e);
+}
 
 int qal_real_mults_per_complex_product(void) { return qal::QAL_REAL_MMAS_PER_CMMA; }
 
@@ -444,7 +460,7 @@ int qal_build_liouvillian(int d, int batch, const qal_c128* H0, int n_ctrl, cons
                                             S(stream)));
   }
   cudaError_t e = launch_liouvillian(batch, D2(H0), n_ctrl, D2(Hc), n_cops, D2(C), D2(L0), D2(Lc), S(stream));
-  if (e != cudaSuccess) return QAL_ERR_CUDA;
+  QAL_TRY(e);
   if (want_comm) e = launch_commutators(batch, n_ctrl, D2(L0), D2(Lc), D2(Lcomm), S(stream));
   return cuda_rc(e);
 }
@@ -473,7 +489,7 @@ int qal_magnus_expm_slices(int n, int batch, int n_slices, double T, int k0, int
           chunk_prod ? chunk : count, chunk_prod ? D2(chunk_prod) + (size_t)b * (count / chunk) * BIG : nullptr,
           U_out ? D2(U_out) + (size_t)b * count * BIG : nullptr, status ? status + b : nullptr,
           reinterpret_cast<double*>(ws), nullptr, S(stream));
-      if (e != cudaSuccess) return QAL_ERR_CUDA;
+      QAL_TRY(e);
     }
     return QAL_OK;
   }
@@ -567,11 +583,10 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
     cudaStream_t st = S(stream);
     if (status && cudaMemsetAsync(status, 0, sizeof(int) * batch, st) != cudaSuccess) return QAL_ERR_CUDA;
     for (int b = 0; b < batch; ++b) {
-      if (launch_dense_expm_fold(D2(L0) + (size_t)b * L0_batch_stride, D2(Lc), n_ctrl,
+      QAL_TRY(launch_dense_expm_fold(D2(L0) + (size_t)b * L0_batch_stride, D2(Lc), n_ctrl,
                                  u + (size_t)b * n_slices * n_ctrl, n_slices, c.G.h, n_slices, lam + (size_t)b * BIG,
                                  nullptr, status ? status + b : nullptr, reinterpret_cast<double*>(ws), nullptr,
-                                 st) != cudaSuccess)
-        return QAL_ERR_CUDA;
+                                 st));
     }
     double* part = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + dense_expm_ws_bytes() +
                                              (size_t)batch * BIG_BYTES);
@@ -592,7 +607,7 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
     w += (size_t)batch * MAT_BYTES;
     double2* lam = Lambda ? D2(Lambda) : lam_tmp;
     FwdOut O{nullptr, nullptr, parts, ch, status};
-    if (launch_expm_fold(batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+    QAL_TRY(launch_expm_fold(batch, c.B, c.G, O, st));
     rc = run_tree(batch, nch, parts, lam, w, st);
     if (rc != QAL_OK) return rc;
     return cuda_rc(launch_fidelity(batch, lam, D2(V), F, st));
@@ -600,7 +615,7 @@ int qal_fidelity_grad(int d, int batch, int n_slices, double T, int magnus_order
   // gradient path: forward (U_k images, prefix P_k) -> fidelity -> VJP with C = S_V^dag (in-kernel from V)
   double2* lam = Lambda ? D2(Lambda) : reinterpret_cast<double2*>(w + 3 * (size_t)batch * n_slices * MAT_BYTES);
   if ((rc = forward_impl(batch, c, nullptr, lam, status, ws, st)) != QAL_OK) return rc;
-  if (launch_fidelity(batch, lam, D2(V), F, st) != cudaSuccess) return QAL_ERR_CUDA;
+  QAL_TRY(launch_fidelity(batch, lam, D2(V), F, st));
   return vjp_impl(batch, c, D2(V), nullptr, 1.0 / 64.0, grad, status, ws, st);
 }
 
@@ -841,7 +856,7 @@ int qal_block_fidelity_grad(const qal_block_plan* plan, int batch, int n_slices,
     w += (size_t)batch * mb;
     double2* lam = Lambda_packed ? D2(Lambda_packed) : lam_tmp;
     BlkFwdOut O{nullptr, parts, ch, status, nullptr};
-    if (launch_blk_expm_fold(*plan, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+    QAL_TRY(launch_blk_expm_fold(*plan, batch, c.B, c.G, O, st));
     if ((rc = run_blk_tree(plan, batch, nch, parts, lam, w, st)) != QAL_OK) return rc;
     return cuda_rc(launch_blk_fidelity(*plan, batch, lam, D2(V), F, st));
   }
@@ -1010,22 +1025,19 @@ int blk_forward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, dou
   double2* lam = Lam ? Lam : w.lam_tmp;
   if (!blk_split_forward(batch)) {
     BlkFwdOut O{w.U, lam, c.G.count, status, w.P, w.scheme};
-    if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+    QAL_TRY(launch_blk_expm_fold(*p, batch, c.B, c.G, O, st));
     return with_suffix ? cuda_rc(launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, nullptr, w.X, st)) : QAL_OK;
   }
   BlkFwdOut O{w.U, nullptr, 1, status, nullptr, w.scheme};
-  if (launch_blk_expm_fold(*p, batch, c.B, c.G, O, st) != cudaSuccess) return QAL_ERR_CUDA;
+  QAL_TRY(launch_blk_expm_fold(*p, batch, c.B, c.G, O, st));
   return cuda_rc(launch_blk_chains(*p, batch, c.G.count, w.U, w.P, lam, V, nullptr, with_suffix ? w.X : nullptr, st));
 }
 // reverse pass on a stored forward: suffix chain (X_{k+1}, seeded by S_V^dag or Cseed) -> gradient slices
 int blk_backward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, const double2* V, double* grad,
                       int* status, void* ws, cudaStream_t st, const double2* Cseed, bool suffix_done) {
   const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
-  if (!suffix_done && launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, Cseed, w.X, st) != cudaSuccess)
-    return QAL_ERR_CUDA;
-  if (launch_blk_grad_slices(*p, batch, c.B, c.G, w.P, w.X, grad, status, w.scheme, Cseed ? 1.0 : 1.0 / 64.0, st) !=
-      cudaSuccess)
-    return QAL_ERR_CUDA;
+  if (!suffix_done) QAL_TRY(launch_blk_suffix_chain(*p, batch, c.G.count, w.U, V, Cseed, w.X, st));
+  QAL_TRY(launch_blk_grad_slices(*p, batch, c.B, c.G, w.P, w.X, grad, status, w.scheme, Cseed ? 1.0 : 1.0 / 64.0, st));
   return QAL_OK;
 }
 // forward -> fidelity -> suffix chain -> gradient slices
@@ -1037,7 +1049,7 @@ int blk_fidelity_grad_impl(const qal_block_plan* p, int batch, const BlkCommon& 
   const bool fid = Cseed == nullptr;   // the seed S_V^dag is known up front: suffix chain beside the prefix
   int rc = blk_forward_impl(p, batch, c, lam, status, ws, st, fid, V);
   if (rc != QAL_OK) return rc;
-  if (F && launch_blk_fidelity(*p, batch, lam, V, F, st) != cudaSuccess) return QAL_ERR_CUDA;
+  if (F) QAL_TRY(launch_blk_fidelity(*p, batch, lam, V, F, st));
   return blk_backward_impl(p, batch, c, V, grad, status, ws, st, Cseed, fid);
 }
 }  // namespace

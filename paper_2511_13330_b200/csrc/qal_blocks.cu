@@ -472,23 +472,6 @@ __device__ __forceinline__ void bstore_nat(double2* __restrict__ M, const BR<C, 
     for (int i = 0; i < 2 * C; ++i)
       M[(8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t] = make_double2(s.re[r][i], RE ? 0.0 : s.im[r][i]);
 }
-template <int C, int R, bool RE>
-__device__ __forceinline__ void baxpy_nat(BR<C, R, RE>& X, double a, const double2* __restrict__ M, const Ctx& x,
-                                          const Lane& L) {
-  constexpr int P = 8 * C;
-  const uint64_t keep = l2_evict_last();   // the basis is shared by every CTA
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int i = 0; i < 2 * C; ++i) {
-      double vx, vy;
-      asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                   : "=d"(vx), "=d"(vy)
-                   : "l"(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t), "l"(keep));
-      X.re[r][i] = fma(a, vx, X.re[r][i]);
-      if constexpr (!RE) X.im[r][i] = fma(a, vy, X.im[r][i]);
-    }
-}
 
 // acc += A * B on the FP64 tensor cores: A = strips (registers), B = image (shared).
 // 4 real MMAs per complex 8x8x4 step (qal_dev.cuh mma_acc_4m); only the first KS k-steps
@@ -660,7 +643,27 @@ __device__ __forceinline__ double bnorm1(const BR<C, R, RE>& s, double* red, con
   return nan ? __longlong_as_double(0x7ff8000000000000LL) : m;
 }
 
-// Omega_k strips of the group from the packed generator basis (a1-a3, as build_omega)
+template <int C, int R, bool RE>
+__device__ __forceinline__ void baxpy_nat(BR<C, R, RE>& X, double a, const double2* __restrict__ M, const Ctx& x,
+                                          const Lane& L) {
+  constexpr int P = 8 * C;
+  const uint64_t keep = l2_evict_last();   // the basis is shared by every CTA
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      double vx, vy;
+      asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(vx), "=d"(vy)
+                   : "l"(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t), "l"(keep));
+      X.re[r][i] = fma(a, vx, X.re[r][i]);
+      if constexpr (!RE) X.im[r][i] = fma(a, vy, X.im[r][i]);
+    }
+}
+
+// Omega_k strips of the group from the packed generator basis (a1-a3, as build_omega).  (Measured: issuing
+// the loads of three basis matrices before their FMAs gave nothing -- 18.2M vs 18.5M slices/s on
+// configs[2] -- the L2 latency of the basis is hidden by the other warps of the SM.)
 template <int C, int R, bool RE>
 __device__ __forceinline__ void bbuild_omega(BR<C, R, RE>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
                                              const Ctx& x, const Lane& L) {
@@ -1539,7 +1542,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
                                              int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
                                              uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
                                              uint32_t tm, uint32_t ts, int* bad, const unsigned short* scheme,
-                                             int ngroups, const Lane& L) {
+                                             unsigned short code, const Lane& L) {
   constexpr size_t IM = img_doubles(C, RE);
   // shared scratch images (own strips only, re-read within the item): X, dX, A6, dA6
   double* gX = sX;
@@ -1571,7 +1574,7 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   // this (pulse, slice, group) when it was kept (no norm, no group barrier here), else the same rule
   int m, s;
   if (scheme) {
-    if (!scheme_decode(scheme[((size_t)b * G.count + k) * ngroups + x.g], m, s) && L.lane == 0) *bad = 1;
+    if (!scheme_decode(code, m, s) && L.lane == 0) *bad = 1;
   } else {
     const double nrm = bnorm1(A, red, x, L);
     choose_scheme_blk(nrm, m, s);
@@ -1854,7 +1857,16 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const int item0 = blockIdx.x * D.nslot + x.slot, istride = gridDim.x * D.nslot;
   const int w0 = x.slot * D.swarps;   // first warp of the slot (trace sum, flags)
   prefetch(item0);
-  if (item0 < items) bbuild_omega(Om, B, G, item0 / N, item0 % N, x, L);
+  // the forward's (m, s) code of an item, loaded with its Omega one item ahead (an L2 round trip that the
+  // dual pass of the current item hides)
+  auto code_of = [&](int it) -> unsigned short {
+    return scheme ? __ldg(scheme + ((size_t)(it / N) * N + it % N) * D.ngroups + x.g) : (unsigned short)0;
+  };
+  unsigned short code = 0;
+  if (item0 < items) {
+    bbuild_omega(Om, B, G, item0 / N, item0 % N, x, L);
+    code = code_of(item0);
+  }
   if (cache) {   // PWC trace basis: the warp's own entries B_m[c][row] x row weight, once per launch
     for (int mm = 0; mm < B.J; ++mm)
 #pragma unroll
@@ -1875,10 +1887,13 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     const int par = ((item - item0) / istride) & 1;   // item parity: double-buffered flags
     const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
                                                ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
-                                               bad_sh + par, scheme, D.ngroups, L);
+                                               bad_sh + par, scheme, code, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
     const int nx = item + istride;
-    if (nx < items) bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
+    if (nx < items) {
+      bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
+      code = code_of(nx);
+    }
     // per-warp partial traces, double-buffered by item parity so one CTA barrier per item suffices
     double* rt = red_tr + (size_t)par * D.tr_buf;
     blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
@@ -2202,8 +2217,12 @@ int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 static int ctas_per_sm(const void* fn, int nwarps, size_t bytes, int tcols) {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess || fa.numRegs <= 0) return 1;
+  // the register file is split over the four sub-partitions (16K registers each) and warp w of a CTA
+  // lives on sub-partition w % 4: the fullest sub-partition decides (a 15-warp CTA puts 4 warps on three
+  // of them, so it needs <= 128 registers per thread -- "too many resources" otherwise)
   const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
-  const int by_regs = 65536 / (regs_warp * nwarps);
+  const int warps_q0 = (nwarps + 3) / 4;   // warps of one CTA on sub-partition 0 (the fullest)
+  const int by_regs = 16384 / (regs_warp * warps_q0);
   const int by_smem = (int)(233472 / (bytes + fa.sharedSizeBytes + 1024));
   const int by_tmem = 512 / std::max(tcols, 32);
   return std::max(0, std::min(std::min(by_regs, by_smem), std::min(64 / nwarps, std::min(by_tmem, 32))));

@@ -41,6 +41,7 @@ _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
     "qal_real_mults_per_complex_product": (ctypes.c_int, []),
     "qal_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "qal_last_cuda_error": (ctypes.c_char_p, []),
     "qal_last_launch_count": (ctypes.c_int, []),
     "qal_default_chunk": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "qal_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int] * 6),
@@ -176,7 +177,10 @@ def load(path: str = LIB_PATH):
 
 def _check(rc: int, what: str):
     if rc != QAL_OK:
-        raise QalError(f"{what}: {load().qal_status_string(rc).decode()} ({rc})")
+        msg = f"{what}: {load().qal_status_string(rc).decode()} ({rc})"
+        if rc == -7:
+            msg += f": {load().qal_last_cuda_error().decode()}"
+        raise QalError(msg)
 
 
 def _ptr(t):
