@@ -1348,7 +1348,8 @@ __device__ __forceinline__ void tma_grp_img(double* dst, const double* src, int 
 
 // --------------------------------------------------------------- suffix chain
 // X_N = S_V^dag on the stored blocks, X_k = X_{k+1} U_k; X_img[b][k-1] = X_k (k = 1..N).
-// One CTA per pulse; the groups run independently; U_k streamed by per-group TMA (double buffer).
+// One CTA slot per pulse (several pulses per CTA, one launch per group, the groups' launches concurrent);
+// U_k streamed by per-group TMA (double buffer).  The running product X_{k+1} stays in registers (own rows).
 template <int C, int R, int KS, bool RE>
 __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, const double2* Cseed,
                                 double* X, const Ctx& x, double* sm, uint64_t* bar, unsigned long long& nflop,
@@ -2145,6 +2146,9 @@ static int blk_role(const BlkDev& D) {
   }
   if (key == ((3 * 4 + 1) * 8 + 5) * 2 + 1) return 1;
   if (key == ((2 * 4 + 1) * 8 + 4) * 2 + 0) return 2;
+#ifdef QAL_BLK_ROLE_2_2
+  if (key == ((2 * 4 + 2) * 8 + 4) * 2 + 0) return 4;   // experiment: the 16-wide group whole on one warp
+#endif
   if (key == ((1 * 4 + 1) * 8 + 2) * 2 + 0) return 3;
   return 0;
 }
@@ -2157,6 +2161,9 @@ static GradKernel grad_kernel(const BlkDev& D) {
     case 1: return k_blk_grad_slices<3, 1, 5, 1>;
     case 2: return k_blk_grad_slices<2, 1, 4, 0>;
     case 3: return k_blk_grad_slices<1, 1, 2, 0>;
+#ifdef QAL_BLK_ROLE_2_2
+    case 4: return k_blk_grad_slices<2, 2, 4, 0>;
+#endif
     default: return k_blk_grad_slices<0, 0, 0, 0>;
   }
 }
@@ -2167,6 +2174,9 @@ static ChainKernel chain_kernel(const BlkDev& D) {
     case 1: return k_blk_suffix_chain<3, 1, 5, 1>;
     case 2: return k_blk_suffix_chain<2, 1, 4, 0>;
     case 3: return k_blk_suffix_chain<1, 1, 2, 0>;
+#ifdef QAL_BLK_ROLE_2_2
+    case 4: return k_blk_suffix_chain<2, 2, 4, 0>;
+#endif
     default: return k_blk_suffix_chain<0, 0, 0, 0>;
   }
 }
@@ -2176,6 +2186,9 @@ static PrefixKernel prefix_kernel(const BlkDev& D) {
     case 1: return k_blk_prefix_chain<3, 1, 5, 1>;
     case 2: return k_blk_prefix_chain<2, 1, 4, 0>;
     case 3: return k_blk_prefix_chain<1, 1, 2, 0>;
+#ifdef QAL_BLK_ROLE_2_2
+    case 4: return k_blk_prefix_chain<2, 2, 4, 0>;
+#endif
     default: return k_blk_prefix_chain<0, 0, 0, 0>;
   }
 }
@@ -2184,6 +2197,9 @@ static FwdKernel fwd_kernel(const BlkDev& D) {
     case 1: return k_blk_expm_fold<3, 1, 5, 1>;
     case 2: return k_blk_expm_fold<2, 1, 4, 0>;
     case 3: return k_blk_expm_fold<1, 1, 2, 0>;
+#ifdef QAL_BLK_ROLE_2_2
+    case 4: return k_blk_expm_fold<2, 2, 4, 0>;
+#endif
     default: return k_blk_expm_fold<0, 0, 0, 0>;
   }
 }

@@ -69,10 +69,11 @@ class PulseBatch:
             self.Lcp = torch.empty((self.J, self.plan.packed), dtype=C128, device=dev)
             if sub_batch is None:
                 # image workspace (3 packed images per slice) within ~80 GB of HBM (at most 45% of the
-                # device, so a dense reference run fits beside it), in whole waves of the one-item-per-
-                # pulse forward and suffix kernels (2 resident CTAs per SM).  Larger sub-batches keep
-                # more pulse chains in flight in the forward: configs[2] 888 -> 1776 pulses per launch
-                # took the forward from 88.6 to 79.3 ms per step
+                # device, so a dense reference run fits beside it), rounded to whole multiples of
+                # 2 x SMs pulses.  Larger sub-batches keep more pulse chains in flight in the fused
+                # forward (one CTA slot per pulse): configs[2] 888 -> 1776 pulses per launch took the
+                # forward from 88.6 to 79.3 ms per step (round 1).  Batches below 8 x SMs pulses run the
+                # split forward instead (qal_api.cu blk_split_forward)
                 props = torch.cuda.get_device_properties(dev)
                 per = 3 * self.N * self.plan.packed * 16
                 wave = 2 * props.multi_processor_count

@@ -43,6 +43,7 @@ def test_binding_covers_every_symbol():
 
 def test_abi_version_and_status_strings(lib):
     assert lib.qal_abi_version() == 2
+    assert isinstance(lib.qal_last_cuda_error(), bytes)
     assert lib.qal_status_string(0) == b"ok"
     assert b"NULL" in lib.qal_status_string(-1)
     assert lib.qal_status_string(-99) == b"unknown status"
@@ -202,6 +203,20 @@ def test_block_calls_validate_before_launch(lib, plan):
     assert lib.qal_block_ordered_product(bp, 1, 5, p, p, None, 0, None) == -6
     assert lib.qal_block_batched_matmul(bp, 2, p, 7, p, 0, p, None) == -2
     assert lib.qal_block_fidelity_cotangent(bp, None, p, None) == -1
+    # stored forward / reverse pass of the block path: workspace, output, slice range
+    fw = [bp, 1, 16, 1.0, 0, 16, 4, 0, 2, p, p, 0, p, None, 0, p, None, None, 0, None]
+    assert lib.qal_block_propagator_forward(*fw) == -6                       # no workspace
+    f2 = list(fw)
+    f2[15] = None
+    assert lib.qal_block_propagator_forward(*f2) == -1                       # Lambda required
+    f3 = list(fw)
+    f3[4], f3[5] = 8, 16
+    assert lib.qal_block_propagator_forward(*f3) == -2                       # range past the grid
+    bw = [bp, 1, 16, 1.0, 0, 16, 4, 0, 2, p, p, 0, p, None, 0, p, p, None, None, 0, None]
+    assert lib.qal_block_propagator_backward(*bw) == -6
+    b2 = list(bw)
+    b2[15] = None
+    assert lib.qal_block_propagator_backward(*b2) == -1                      # cotangent required
     # per-pulse structure check: empty, NULL status, per-matrix mode needs one status per matrix
     assert lib.qal_block_check(bp, 0, p, 0, p, 1, None) == -3
     assert lib.qal_block_check(bp, 2, p, 0, None, 2, None) == -1

@@ -11,9 +11,9 @@ M = {
     "time_ms": "gpu__time_duration.sum",
     "dmma_pipe_pct": "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
     "dmma_inst_pct": "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
-    "issue_active_pct": "sm__issue_active.avg.pct_of_peak_sustained_active",
+    "issue_active_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
     "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
-    "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_active",
+    "smem_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
     "dram_read_bytes": "dram__bytes_read.sum",
     "dram_write_bytes": "dram__bytes_write.sum",
     "registers": "launch__registers_per_thread",
