@@ -136,7 +136,10 @@ struct BlkDev {
 
 // gmask: the groups this launch runs (bit g); nslot: independent item streams per CTA, each with its
 // own warps, barriers and shared-memory regions (one set of groups = one launch, see blk_sets).
-bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot = 1) {
+// whole_c2: run 16-wide groups whole on one warp (role (2, 2)) instead of one warp per 8-row strip -- the
+// forward's choice (no group barriers in its per-pulse chain; measured 70.4 -> 67.7 ms per configs[2] step),
+// while the gradient keeps the split (138 vs 169 ms)
+bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot = 1, bool whole_c2 = false) {
   memset(&D, 0, sizeof(D));
   D.ngroups = p.ngroups;
   D.packed = p.packed;
@@ -162,6 +165,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
       if (!((gmask >> g) & 1)) continue;
       const bool split = (mask >> g) & 1;
       if ((split && D.C[g] == 1) || (!split && D.C[g] == 3)) { ok = false; break; }   // roles (3,1) (2,1|2) (1,1)
+      if (whole_c2 && split && D.C[g] == 2) { ok = false; break; }
       mx = std::max(mx, cost(g, split ? 1 : D.C[g]));
       nw += split ? D.C[g] : 1;
     }
@@ -2146,9 +2150,7 @@ static int blk_role(const BlkDev& D) {
   }
   if (key == ((3 * 4 + 1) * 8 + 5) * 2 + 1) return 1;
   if (key == ((2 * 4 + 1) * 8 + 4) * 2 + 0) return 2;
-#ifdef QAL_BLK_ROLE_2_2
-  if (key == ((2 * 4 + 2) * 8 + 4) * 2 + 0) return 4;   // experiment: the 16-wide group whole on one warp
-#endif
+  if (key == ((2 * 4 + 2) * 8 + 4) * 2 + 0) return 4;   // the 16-wide group whole on one warp (forward)
   if (key == ((1 * 4 + 1) * 8 + 2) * 2 + 0) return 3;
   return 0;
 }
@@ -2197,9 +2199,7 @@ static FwdKernel fwd_kernel(const BlkDev& D) {
     case 1: return k_blk_expm_fold<3, 1, 5, 1>;
     case 2: return k_blk_expm_fold<2, 1, 4, 0>;
     case 3: return k_blk_expm_fold<1, 1, 2, 0>;
-#ifdef QAL_BLK_ROLE_2_2
     case 4: return k_blk_expm_fold<2, 2, 4, 0>;
-#endif
     default: return k_blk_expm_fold<0, 0, 0, 0>;
   }
 }
@@ -2338,7 +2338,8 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
       for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns) {
         if (p.launch_sets != QAL_BLK_SETS_DEFAULT && ns != set.nslot) continue;
         L t;
-        if (!to_dev(p, t.D, set.gmask, ns)) continue;
+        if (!to_dev(p, t.D, set.gmask, ns, p.launch_sets == QAL_BLK_SETS_DEFAULT) && !to_dev(p, t.D, set.gmask, ns))
+          continue;
         t.bytes = (size_t)grp_smem_doubles(t.D, per3) * 8;
         t.fn = fwd_kernel(t.D);
         const int per_sm = ctas_per_sm((const void*)t.fn, t.D.nwarps, t.bytes, tmem_cols_for(t.D));
