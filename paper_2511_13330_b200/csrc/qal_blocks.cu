@@ -1597,10 +1597,9 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   bzero(acc);
   bmma<C, R, KS, RE>(acc, A, SN, x, L);
   bscale(acc, sc);
-  grp_sync(x);                                         // SV (X) complete; reads of SD (P_k) done
-  bstore_img(SD, acc, x, L);
+  bstore_img(SD, acc, x, L);                           // dX over P_k: each warp read only its own rows of P_k
   SCR_ST(1, acc);
-  grp_sync(x);                                         // SD = dX complete
+  grp_sync(x);                                         // SV = X and SD = dX complete
   bload_img(A, SV, x, L);
   bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                  // A2 = X X
   bt_store(T0, acc);
@@ -1642,7 +1641,10 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
       ++np;
     }
   } else if (m == 12) {
-    // T12 = B1 + (B2 + A6) A6, A6 = B3 + B4^2, B4 = b1 X + b2 A2 + b3 A3, as value + derivative
+    // T12 = B1 + (B2 + A6) A6, A6 = B3 + B4^2, B4 = b1 X + b2 A2 + b3 A3, as value + derivative.  Two
+    // group barriers: B4 goes to SN (idle since G) and dB4 to the A6 scratch image used whole, so A6 / dA6
+    // can be written into SV / SD right after their products (every warp's reads of X / dX are behind the
+    // first barrier)
     bt_load(A, T0);
     bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // A3 = A2 X
     bt_store(T2, acc);
@@ -1650,33 +1652,29 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
     bt_load(A, T1);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dA2 X = dA3
     bt_store(T3, acc);
-    grp_sync(x);                                       // reads of SV (X), SD (dX) done
-    bzero(acc);                                        // B4 -> SV
+    bzero(acc);                                        // B4 -> SN
     SCR_AXPY(acc, c_t12[T12_B4][1], 0); bt_axpy(acc, c_t12[T12_B4][2], T0); bt_axpy(acc, c_t12[T12_B4][3], T2);
-    bstore_img(SV, acc, x, L);
-    bzero(acc);                                        // dB4 -> SD
+    bstore_img(SN, acc, x, L);
+    bzero(acc);                                        // dB4 -> gA6 (as a whole image)
     SCR_AXPY(acc, c_t12[T12_B4][1], 1); bt_axpy(acc, c_t12[T12_B4][2], T1); bt_axpy(acc, c_t12[T12_B4][3], T3);
-    bstore_img(SD, acc, x, L);
-    grp_sync(x);                                       // B4, dB4 images complete
-    bload_img(A, SV, x, L);
-    bzero(acc); bmma<C, R, KS, RE>(acc, A, SV, x, L);                // B4 B4
+    bstore_img(gA6, acc, x, L);
+    grp_sync(x);                                       // B4, dB4 complete; reads of SV (X), SD (dX) done
+    bload_img(A, SN, x, L);
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, SN, x, L);                // B4 B4
     SCR_AXPY(acc, c_t12[T12_B3][1], 0); bt_axpy(acc, c_t12[T12_B3][2], T0); bt_axpy(acc, c_t12[T12_B3][3], T2);
-    SCR_ST(2, acc);                                    // A6
-    bzero(acc); bmma<C, R, KS, RE>(acc, A, SD, x, L);                // B4 dB4
-    bload_img(A, SD, x, L);
-    bmma<C, R, KS, RE>(acc, A, SV, x, L);                            // + dB4 B4
+    bstore_img(SV, acc, x, L);                         // A6
+    bzero(acc); bmma<C, R, KS, RE>(acc, A, gA6, x, L);               // B4 dB4
+    bload_img(A, gA6, x, L);
+    bmma<C, R, KS, RE>(acc, A, SN, x, L);                            // + dB4 B4
     SCR_AXPY(acc, c_t12[T12_B3][1], 1); bt_axpy(acc, c_t12[T12_B3][2], T1); bt_axpy(acc, c_t12[T12_B3][3], T3);
-    SCR_ST(3, acc);                                    // dA6
-    grp_sync(x);                                       // reads of SV (B4), SD (dB4) done
-    SCR_LD(A, 2); bstore_img(SV, A, x, L);             // A6 image
-    SCR_LD(acc, 3); bstore_img(SD, acc, x, L);         // dA6 image
-    grp_sync(x);
+    bstore_img(SD, acc, x, L);                         // dA6
+    grp_sync(x);                                       // A6 (SV), dA6 (SD) complete
     bzero(acc);                                        // dT = dB1 + dL A6 + L dA6
     SCR_AXPY(acc, c_t12[T12_B1][1], 1); bt_axpy(acc, c_t12[T12_B1][2], T1); bt_axpy(acc, c_t12[T12_B1][3], T3);
-    SCR_LD(A, 3);                                      // dL = dB2 + dA6
+    bload_img(A, SD, x, L);                            // dL = dB2 + dA6
     SCR_AXPY(A, c_t12[T12_B2][1], 1); bt_axpy(A, c_t12[T12_B2][2], T1); bt_axpy(A, c_t12[T12_B2][3], T3);
     bmma<C, R, KS, RE>(acc, A, SV, x, L);
-    SCR_LD(A, 2);                                      // L = B2 + A6
+    bload_img(A, SV, x, L);                            // L = B2 + A6
     badd_diag(A, c_t12[T12_B2][0], x, L);
     SCR_AXPY(A, c_t12[T12_B2][1], 0); bt_axpy(A, c_t12[T12_B2][2], T0); bt_axpy(A, c_t12[T12_B2][3], T2);
     bmma<C, R, KS, RE>(acc, A, SD, x, L);
