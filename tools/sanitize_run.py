@@ -62,6 +62,14 @@ def main():
         keep(f'blk{sets}_F', Fb); keep(f'blk{sets}_g', gb); keep(f'blk{sets}_Lam', Lp)
     plan.launch_sets = qal.QAL_BLK_SETS_DEFAULT
     keep('blk_unpack', qal.qal_block_unpack(plan, Lp))
+    # the fused forward layout of the gradient path (>= 8 x SMs pulses) and s > 0 squarings (long slices)
+    pb = qi.cfg2(batch=1200, N=4, T=200.0 * 4 / 1024)
+    L0b = qal.qal_build_liouvillian(d(pb.H0), d(pb.Hc), d(pb.C))[0]
+    L0bp, _ = qal.qal_block_pack(plan, L0b)
+    Fz, gz, _ = qal.qal_block_fidelity_grad(plan, L0bp, Lcp, d(pb.u), pb.T, pb.N, V)
+    keep('blk_fused_F', Fz); keep('blk_fused_g', gz)
+    Fs, gs, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, u, 40.0 * p.T, p.N, V)
+    keep('blk_long_F', Fs); keep('blk_long_g', gs)
     bparts = qal.qal_block_expm_slices(plan, L0p, Lcp, u, p.T, p.N, chunk=4)
     keep('blk_parts', bparts); keep('blk_prod', qal.qal_block_ordered_product(plan, bparts))
     bpre, bsuf = qal.qal_block_ordered_scan(plan, bparts)
