@@ -139,7 +139,10 @@ struct BlkDev {
 // whole_c2: run 16-wide groups whole on one warp (role (2, 2)) instead of one warp per 8-row strip -- the
 // forward's choice (no group barriers in its per-pulse chain; measured 70.4 -> 67.7 ms per configs[2] step),
 // while the gradient keeps the split (138 vs 169 ms)
-bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot = 1, bool whole_c2 = false) {
+// whole_c3: the real 24-wide group whole on one warp too (role (3, 3), forward only).
+// tslots: TMEM strip slots per warp (the forward needs 3, the gradient 4).
+bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot = 1, bool whole_c2 = false,
+            bool whole_c3 = false, int tslots = BLK_TSLOTS) {
   memset(&D, 0, sizeof(D));
   D.ngroups = p.ngroups;
   D.packed = p.packed;
@@ -164,8 +167,9 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
     for (int g = 0; g < p.ngroups; ++g) {
       if (!((gmask >> g) & 1)) continue;
       const bool split = (mask >> g) & 1;
-      if ((split && D.C[g] == 1) || (!split && D.C[g] == 3)) { ok = false; break; }   // roles (3,1) (2,1|2) (1,1)
+      if ((split && D.C[g] == 1) || (!split && D.C[g] == 3 && !whole_c3)) { ok = false; break; }   // roles (3,1|3) (2,1|2) (1,1)
       if (whole_c2 && split && D.C[g] == 2) { ok = false; break; }
+      if (whole_c3 && split && D.C[g] == 3) { ok = false; break; }
       mx = std::max(mx, cost(g, split ? 1 : D.C[g]));
       nw += split ? D.C[g] : 1;
     }
@@ -226,7 +230,7 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
     }
     D.tstride[v] = st;
     D.tcol[v] = qused[v & 3];
-    qused[v & 3] += BLK_TSLOTS * st;
+    qused[v & 3] += tslots * st;
   }
   const int need = std::max(std::max(qused[0], qused[1]), std::max(qused[2], qused[3]));
   D.tmem_cols = 32;
@@ -2149,6 +2153,7 @@ static int blk_role(const BlkDev& D) {
   if (key == ((3 * 4 + 1) * 8 + 5) * 2 + 1) return 1;
   if (key == ((2 * 4 + 1) * 8 + 4) * 2 + 0) return 2;
   if (key == ((2 * 4 + 2) * 8 + 4) * 2 + 0) return 4;   // the 16-wide group whole on one warp (forward)
+  if (key == ((3 * 4 + 3) * 8 + 5) * 2 + 1) return 5;   // the real 24-wide group whole on one warp (forward)
   if (key == ((1 * 4 + 1) * 8 + 2) * 2 + 0) return 3;
   return 0;
 }
@@ -2198,6 +2203,7 @@ static FwdKernel fwd_kernel(const BlkDev& D) {
     case 2: return k_blk_expm_fold<2, 1, 4, 0>;
     case 3: return k_blk_expm_fold<1, 1, 2, 0>;
     case 4: return k_blk_expm_fold<2, 2, 4, 0>;
+    case 5: return k_blk_expm_fold<3, 3, 5, 1>;
     default: return k_blk_expm_fold<0, 0, 0, 0>;
   }
 }
@@ -2336,7 +2342,13 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
       for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns) {
         if (p.launch_sets != QAL_BLK_SETS_DEFAULT && ns != set.nslot) continue;
         L t;
-        if (!to_dev(p, t.D, set.gmask, ns, p.launch_sets == QAL_BLK_SETS_DEFAULT) && !to_dev(p, t.D, set.gmask, ns))
+        // whole groups on one warp (no group barriers in the per-pulse chain: measured 70.4 -> 67.7 ms
+        // (16-wide) and 67.9 -> 62.3 ms (real 24-wide) per configs[2] step), when a role kernel exists for
+        // the layout (the dispatching kernel runs the 24-wide group only split)
+        const bool whole = p.launch_sets == QAL_BLK_SETS_DEFAULT;
+        if (!(whole && to_dev(p, t.D, set.gmask, ns, true, true, 3) && blk_role(t.D) != 0) &&
+            !(whole && to_dev(p, t.D, set.gmask, ns, true, false, 3) && blk_role(t.D) != 0) &&
+            !to_dev(p, t.D, set.gmask, ns, false, false, 3))
           continue;
         t.bytes = (size_t)grp_smem_doubles(t.D, per3) * 8;
         t.fn = fwd_kernel(t.D);
