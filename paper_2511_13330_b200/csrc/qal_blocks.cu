@@ -1836,8 +1836,13 @@ __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& 
 }
 
 // One warp's role over the whole item sequence (every warp runs the same number of items, so the
-// CTA-wide barriers below match).  Omega of the next item is built right after the dual pass, so its
-// basis loads are in flight during the traces and the CTA barrier.
+// CTA-wide barriers below match).  Per item: the dual pass, the slot barrier (every warp done with the
+// item's shared images), then at once the TMA of the next item's P_k / X_{k+1} (its latency overlaps
+// the rest of this item: the next Omega, the traces and the previous item's trace sum), the fixed-order
+// sum of the PREVIOUS item's per-warp traces (complete at this barrier) and its gradient entries, the
+// next item's Omega (basis loads in flight during the traces) and this item's per-warp traces.  The
+// trace buffers are double-buffered by item parity and the non-finite flags kept four deep, so one slot
+// barrier per item suffices.
 template <int C, int R, int KS, bool RE>
 __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, const SliceGrid& G,
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
@@ -1850,6 +1855,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const int N = G.count;
   const int items = batch * N;
   const int K = B.J + B.ncomm;
+  const int nodes = (G.mode == 1) ? 2 : 1;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   uint32_t ph = 0;
   auto prefetch = [&](int it) {   // group leader: bulk-copy X_{k+1} -> SN, P_k -> SD of item `it`
@@ -1859,11 +1865,17 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
       tma_grp_img(sm, P_img + (size_t)it * stride + 2 * x.off, C, &bars[1], RE);
     }
   };
+  // the control values of item `it` into L1 ahead of its Omega build (one line per warp)
+  auto prefetch_u = [&](int it) {
+    if (L.lane == 0 && it < items)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(G.u + (size_t)it * nodes * B.J));
+  };
   BR<C, R, RE> A, acc, Om;
   // this slot's item stream: items item0, item0 + istride, ...
   const int item0 = blockIdx.x * D.nslot + x.slot, istride = gridDim.x * D.nslot;
   const int w0 = x.slot * D.swarps;   // first warp of the slot (trace sum, flags)
   prefetch(item0);
+  prefetch_u(item0 + istride);
   // the forward's (m, s) code of an item, loaded with its Omega one item ahead (an L2 round trip that the
   // dual pass of the current item hides)
   auto code_of = [&](int it) -> unsigned short {
@@ -1887,28 +1899,12 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
         }
     __syncwarp();
   }
-  for (int item = item0; item < items; item += istride) {
-    const int b = item / N, k = item % N;
-    QAL_DCHECK(b < batch && k < N);
-    bcopy(A, Om);
-    const int par = ((item - item0) / istride) & 1;   // item parity: double-buffered flags
-    const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
-                                               ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
-                                               bad_sh + par, scheme, code, L);
-    if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
-    const int nx = item + istride;
-    if (nx < items) {
-      bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
-      code = code_of(nx);
-    }
-    // per-warp partial traces, double-buffered by item parity so one CTA barrier per item suffices
-    double* rt = red_tr + (size_t)par * D.tr_buf;
-    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
-    slot_sync(D, x.slot);   // every warp of the slot done with this item: SN / SD free, rt complete
-    prefetch(nx);
-    if (L.w != w0) continue;
-    double* Tsum = rt + (D.nwarps + x.slot) * D.tr_k;
-    for (int m = L.lane; m < K; m += 32) {   // fixed-order sum over the slot's warps
+  // warp w0: fixed-order sum over the slot's warps of item `it`'s partial traces (parity buffer rt, flag
+  // slot fl) and its gradient entries
+  auto finish = [&](int it, const double* rt, int fl) {
+    const int b = it / N, k = it % N;
+    double* Tsum = const_cast<double*>(rt) + (D.nwarps + x.slot) * D.tr_k;
+    for (int m = L.lane; m < K; m += 32) {
       double s = 0.0;
       for (int w = w0; w < w0 + D.swarps; ++w) s += rt[w * D.tr_k + m];
       Tsum[m] = s;
@@ -1942,10 +1938,35 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
           gg[J + j] = (accum ? gg[J + j] : 0.0) + g2 * inv_d2;
         }
       }
-      if (bad_sh[par] && status) status[b] = QAL_ERR_NONFINITE;
-      bad_sh[par] = 0;
+      if (bad_sh[fl] && status) status[b] = QAL_ERR_NONFINITE;
+      bad_sh[fl] = 0;
     }
+  };
+  int idx = 0;
+  for (int item = item0; item < items; item += istride, ++idx) {
+    const int b = item / N, k = item % N;
+    QAL_DCHECK(b < batch && k < N);
+    bcopy(A, Om);
+    const int par = idx & 1;   // item parity: double-buffered traces
+    const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
+                                               ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
+                                               bad_sh + (idx & 3), scheme, code, L);
+    if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
+    const int nx = item + istride;
+    slot_sync(D, x.slot);   // every warp of the slot done with this item's images; previous traces complete
+    prefetch(nx);
+    prefetch_u(nx + istride);
+    if (L.w == w0 && idx > 0) finish(item - istride, red_tr + (size_t)(par ^ 1) * D.tr_buf, (idx - 1) & 3);
+    if (nx < items) {
+      bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
+      code = code_of(nx);
+    }
+    double* rt = red_tr + (size_t)par * D.tr_buf;
+    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
   }
+  slot_sync(D, x.slot);   // the last item's traces complete
+  if (L.w == w0 && idx > 0)
+    finish(item0 + (idx - 1) * istride, red_tr + (size_t)((idx - 1) & 1) * D.tr_buf, (idx - 1) & 3);
 }
 
 // FC == 0: any mix of roles (runtime dispatch); else every warp runs role <FC, FR, FKS, FRE> and the
@@ -1963,7 +1984,7 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
   __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id: [0] X_{k+1} -> SN, [1] P_k -> SD
   double* red_tr = smem + D.tr_off;   // per-warp partial traces + per-slot sums, two item parities
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int bad_sh[BLK_MAX_SLOTS][2];
+  __shared__ int bad_sh[BLK_MAX_SLOTS][4];
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   const BlkTask T = D.task[L.w][0];   // one role per warp (to_dev)
@@ -1972,7 +1993,7 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
     mbar_init(&bars[T.bar][1], 1);
   }
   fence_mbar_init();
-  if (threadIdx.x < 2 * BLK_MAX_SLOTS) bad_sh[threadIdx.x >> 1][threadIdx.x & 1] = 0;
+  if (threadIdx.x < 4 * BLK_MAX_SLOTS) bad_sh[threadIdx.x >> 2][threadIdx.x & 3] = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
