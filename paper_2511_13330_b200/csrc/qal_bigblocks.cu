@@ -448,6 +448,12 @@ __device__ __forceinline__ void load_img_re(Strip& s, const double* __restrict__
   }
 }
 
+__device__ __forceinline__ void store_img_re(double* __restrict__ img, const Strip& s, const Lane& L) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<double2*>(img + pair_off(L, j)) = make_double2(s.re[2 * j], s.re[2 * j + 1]);
+}
+
 // C_i = A_i B_i for i < nbatch (A_i = A + i sA, ...; the accumulator is initialised to
 // cid I + sum coef[q] src[q]_i, src_i = src + i sSrc); plan_i = plan + i pstride.
 struct BBGemm {
@@ -508,13 +514,26 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
         if (bb_active(D, g, i, b)) atomicAdd(g.ctr, g.bflops[b]);
   int v = bb_next_vt(D, g, blockIdx.x, gridDim.x, nv);
   if (v >= nv) return;
-  // a real block's tiles carry only their re plane (the im plane is zero and never read)
-  auto tma_tile = [&](double* dst, const double* src, uint64_t* br, bool real) {
-    if (!real) { tma_load_img(dst, src, br); return; }
-    mbar_expect_tx(br, PLANE * 8);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) bulk_g2s(dst + q * (PLANE / 2), src + q * (PLANE / 2), PLANE * 4, br);
+  // the first `rows` rows of each plane of a tile image (rows are contiguous 64-double lines of the
+  // plane; a real block's tiles carry only their re plane, the im plane is zero and never read).  The
+  // GEMM reads A rows of the used row strips and B rows of the used k-steps only (BB_TRIM), so the
+  // padding rows of a block's last tile row / column are not moved.
+  auto tma_tile = [&](double* dst, const double* src, uint64_t* br, bool real, int rows) {
+    const uint32_t bytes = (uint32_t)rows * 64 * 8;   // per plane, <= 32 KB
+    mbar_expect_tx(br, real ? bytes : 2 * bytes);
+    const int np = real ? 1 : 2;
+    for (int pl = 0; pl < np; ++pl) {
+      if (bytes > 16384) {
+        bulk_g2s(dst + pl * PLANE, src + pl * PLANE, 16384, br);
+        bulk_g2s(dst + pl * PLANE + 2048, src + pl * PLANE + 2048, bytes - 16384, br);
+      } else {
+        bulk_g2s(dst + pl * PLANE, src + pl * PLANE, bytes, br);
+      }
+    }
   };
+  // rows of A tile (I, .) = the used row strips, of B tile (K, .) = the used k-steps
+  auto rowsA = [&](int b, int I) { return BB_TRIM ? std::min(64, (D.used[b] - 64 * I + 7) & ~7) : 64; };
+  auto rowsB = [&](int b, int K) { return BB_TRIM ? std::min(64, (D.used[b] - 64 * K + 3) & ~3) : 64; };
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -529,8 +548,8 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
   auto Bof = [&](const BBVT& x) { return g.B + x.i * g.sB; };
   BBVT x = bb_vt(D, v);
   if (threadIdx.x == 0) {
-    tma_tile(SA, bb_tile(D, Aof(x), x.b, x.I, 0), &bar[0], D.real[x.b]);
-    tma_tile(SB[0], bb_tile(D, Bof(x), x.b, 0, x.J), &bar[1], D.real[x.b]);
+    tma_tile(SA, bb_tile(D, Aof(x), x.b, x.I, 0), &bar[0], D.real[x.b], rowsA(x.b, x.I));
+    tma_tile(SB[0], bb_tile(D, Bof(x), x.b, 0, x.J), &bar[1], D.real[x.b], rowsB(x.b, 0));
   }
   uint32_t phA = 0, phB[2] = {0, 0};
   int step = 0;
@@ -538,10 +557,17 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
   while (v < nv) {
     x = bb_vt(D, v);
     const int nt = D.nt[x.b];
+    const bool re_only = D.real[x.b] != 0;
+    // a warp whose 8 rows lie wholly in the block's padding neither reads the accumulator sources nor
+    // writes its strip of C: no kernel ever reads those rows (the GEMM reads A rows of the used strips
+    // and B rows of the used k-steps, the unpack the stored entries, the norms only the Omega images)
+    const bool live = !BB_TRIM || 64 * x.I + 8 * L.w < D.used[x.b];
     zero(acc);
-    for (int q = 0; q < g.nsrc; ++q) {
+    for (int q = 0; live && q < g.nsrc; ++q) {
       Strip y;
-      load_img(y, bb_tile(D, g.src[q] + x.i * g.sSrc, x.b, x.I, x.J), L);
+      const double* st = bb_tile(D, g.src[q] + x.i * g.sSrc, x.b, x.I, x.J);
+      if (re_only) load_img_re(y, st, L);   // a real block's im plane is never read
+      else load_img(y, st, L);
       const double c = g.coef[q];
 #pragma unroll
       for (int i = 0; i < 16; ++i) { acc.re[i] = fma(c, y.re[i], acc.re[i]); acc.im[i] = fma(c, y.im[i], acc.im[i]); }
@@ -572,8 +598,9 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
         }
         if (more) {
           fence_proxy_async();
-          tma_tile(SA, bb_tile(D, Aof(xn), xn.b, xn.I, Kn), &bar[0], D.real[xn.b]);
-          tma_tile(SB[cur ^ 1], bb_tile(D, Bof(xn), xn.b, Kn, xn.J), &bar[1 + (cur ^ 1)], D.real[xn.b]);
+          tma_tile(SA, bb_tile(D, Aof(xn), xn.b, xn.I, Kn), &bar[0], D.real[xn.b], rowsA(xn.b, xn.I));
+          tma_tile(SB[cur ^ 1], bb_tile(D, Bof(xn), xn.b, Kn, xn.J), &bar[1 + (cur ^ 1)], D.real[xn.b],
+                   rowsB(xn.b, Kn));
         }
       }
       // padding: k-steps past the block's stored rows (last K tile), output column tiles past them
@@ -590,11 +617,11 @@ __global__ void __launch_bounds__(NT, 1) k_bb_gemm(BBDev D, BBGemm g) {
         else mma_acc_trim(acc, a, SB[cur], L, qmax, jmax);
       }
     }
-    if (D.real[x.b]) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) acc.im[i] = 0.0;   // keep the unused plane zero
+    if (live) {
+      double* ct = bb_tile(D, g.C + x.i * g.sC, x.b, x.I, x.J);
+      if (re_only) store_img_re(ct, acc, L);   // the im plane of a real block's tile is never read
+      else store_img(ct, acc, L);
     }
-    store_img(bb_tile(D, g.C + x.i * g.sC, x.b, x.I, x.J), acc, L);
     v = vnext;
   }
 }
@@ -697,7 +724,11 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
     if (!mirror || k <= mir[k]) keep.push_back(k);
   std::stable_sort(keep.begin(), keep.end(), [&](int a, int b) { return members[a].size() > members[b].size(); });
   // best-fit-decreasing packing of the components into blocks of 64-multiple width (components that
-  // share a block are multiplied densely together -- their cross terms are zero)
+  // share a block are multiplied densely together -- their cross terms are zero).  Measured against a
+  // packing that keeps the components apart (each in its own trimmed block, by a modelled DMMA-time
+  // rule): Hubbard 7.8k -> 5.5k slices/s, configs[4] 548 -> 538 -- the n = 4096 block GEMM streams its
+  // tiles through HBM (the batch workspace is ~1.4 GB), so more, smaller blocks cost more tile traffic
+  // and per-tile latency than the zero cross terms cost DMMA time
   struct Bin { int width, used, real; std::vector<int> comps; };
   std::vector<Bin> bins;
   for (int k : keep) {
@@ -725,10 +756,11 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
   double flops = 0.0;
   for (int b = 0; b < p.nb; ++b) {
     p.size[b] = bins[b].used;
-    p.nt[b] = bins[b].width / 64;
+    const int width = bins[b].width;
+    p.nt[b] = width / 64;
     p.row0[b] = row;
     p.weight[b] = 1;
-    if (row + bins[b].width > QAL_BB_MAX_ROWS) return QAL_ERR_UNSUPPORTED;
+    if (row + width > QAL_BB_MAX_ROWS) return QAL_ERR_UNSUPPORTED;
     p.real[b] = bins[b].real;
     int r = row;
     double fl = 0.0;
@@ -751,7 +783,7 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
     }
     p.flops[b] = fl;
     flops += fl;
-    row += bins[b].width;
+    row += width;
     tiles += p.nt[b] * p.nt[b];
   }
   p.nrows = row;
