@@ -345,7 +345,8 @@ def test_block_forward_backward_session_equals_one_call_vjp_and_oracle(torch_cud
     torch = torch_cuda
     p = qi.cfg3(N=96, T=40.0)
     plan, L0p, Lcp, Lcommp = packed_basis(torch, qal, p, want_comm=True)
-    u = qal.qal_sample_controls_sines(dev(torch, p.sines), p.u_max, p.N, p.T).reshape(3, 32, 2, 2).contiguous()
+    un = oracle.sines_nodes(p.sines, p.u_max, p.N, p.T).reshape(3, 32, 2, 2)   # host controls, both sides
+    u = dev(torch, un)
     sess = qal.BlockGradientSession(plan, L0p, Lcp, u, p.T, p.N, ctrl_mode=1, Lcommp=Lcommp)
     Lam = sess.forward()
     C = qal.qal_block_fidelity_cotangent(plan, dev(torch, p.V)).unsqueeze(0).repeat(3, 1).contiguous()
@@ -354,11 +355,12 @@ def test_block_forward_backward_session_equals_one_call_vjp_and_oracle(torch_cud
     g1, L1 = qal.qal_block_propagator_vjp(plan, L0p, Lcp, u, p.T, p.N, C, ctrl_mode=1, Lcommp=Lcommp,
                                           want_Lambda=True)
     assert torch.equal(Lam, L1) and torch.equal(g, g1)
+    # the oracle's reference: its own Lambda and cotangent (no GPU value enters the oracle)
     rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
-    Cn = qal.qal_block_unpack(plan, C)
-    un = u.cpu().numpy()
+    Cf = oracle.fidelity_cotangent(p.V)
     for b in range(3):
-        gr, _ = oracle.vjp(rL0, rLc, un[b], p.T * 32 / p.N, 32, Cn[b].cpu().numpy(), mode=1)
+        Lr = oracle.propagate(rL0, rLc, un[b], p.T * 32 / p.N, 32, mode=1)
+        gr, _ = oracle.vjp(rL0, rLc, un[b], p.T * 32 / p.N, 32, oracle.matmul(Cf, Lr), mode=1)
         assert relfro(g[b].cpu().numpy(), gr) <= TOL_GRAD
 
 
