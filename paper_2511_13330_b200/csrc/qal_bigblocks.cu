@@ -55,10 +55,13 @@ constexpr int BB_PLAN_STRIDE = 64;
 constexpr bool BB_TRIM = QAL_BB_TRIM != 0;   // skip the padding k-steps / column tiles / row strips   // plan records per slice of a batch (>= QAL_BB_MAX_BLOCKS)
 // slices per batch (every launch covers the tiles of a whole batch): as many as ~4 GB of batch
 // workspace holds, at most 64 (configs[4]: 16; the Hubbard blocks: 64)
+#ifndef QAL_BB_SB_MAX
+#define QAL_BB_SB_MAX 64
+#endif
 inline int bb_sb(const qal_bigblock_plan& p) {
   const size_t per = 6 * (size_t)p.total_doubles * 8;
   const size_t n = ((size_t)4 << 30) / std::max<size_t>(per, 1);
-  return (int)std::min<size_t>(64, std::max<size_t>(1, n));
+  return (int)std::min<size_t>(QAL_BB_SB_MAX, std::max<size_t>(1, n));
 }
 
 __device__ __forceinline__ int bb_block_of_tile(const BBDev& D, int t) {
@@ -726,9 +729,9 @@ int build_bigblock_plan(int nmat, const double2* mats, int mirror, qal_bigblock_
   // best-fit-decreasing packing of the components into blocks of 64-multiple width (components that
   // share a block are multiplied densely together -- their cross terms are zero).  Measured against a
   // packing that keeps the components apart (each in its own trimmed block, by a modelled DMMA-time
-  // rule): Hubbard 7.8k -> 5.5k slices/s, configs[4] 548 -> 538 -- the n = 4096 block GEMM streams its
-  // tiles through HBM (the batch workspace is ~1.4 GB), so more, smaller blocks cost more tile traffic
-  // and per-tile latency than the zero cross terms cost DMMA time
+  // rule): Hubbard 7.8k -> 5.5k slices/s, configs[4] 548 -> 538 -- more, shorter (tile, K) steps whose TMA
+  // wait and per-tile source loads are no longer hidden behind a full tile's DMMAs cost more than the zero
+  // cross terms of the packed tiles (DESIGN 5d)
   struct Bin { int width, used, real; std::vector<int> comps; };
   std::vector<Bin> bins;
   for (int k : keep) {
