@@ -45,6 +45,7 @@ constexpr int BLK_MAX_WARPS = 16;
 constexpr int BLK_FUSED_WARPS = 8;   // one item per CTA, all groups (every kernel but fwd / grad sets)
 constexpr int BLK_MAX_SLOTS = 5;   // independent item streams per CTA (group-specialised launches)
 constexpr int BLK_CHAIN_WARPS = 12;   // launch bound of the suffix-chain kernel (4 pulses x 3 warps)
+constexpr int BLK_CHAIN_STAGES = 4;   // deepest U_k ring of the chain kernels
 // real MMAs per complex 8x8x4 step of the complex blocks: 4 (default) or 3 (Gauss, -DQAL_BLK_3M)
 #ifdef QAL_BLK_3M
 constexpr int BLK_CPLX_MMAS = 3;
@@ -104,6 +105,7 @@ struct BlkDev {
   int nslot;                       // item slots per CTA (1: one item, all groups of the set)
   int swarps;                      // warps per slot
   int sstride;                     // shared-memory doubles per slot
+  int cstages;                     // chain kernels: U_k ring depth (TMA stages in flight, 2..BLK_CHAIN_STAGES)
   signed char sbar[BLK_MAX_SLOTS]; // per-slot barrier: 0 = __syncthreads, -1 = __syncwarp, else named
   int C[QAL_BLK_MAX_GROUPS];       // column (= row) tiles of group g
   int ks[QAL_BLK_MAX_GROUPS];      // k-steps of 4 covering the used rows of group g
@@ -1362,7 +1364,8 @@ template <int C, int R, int KS, bool RE>
 __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const double2* V, const double2* Cseed,
                                 double* X, const Ctx& x, double* sm, uint64_t* bar, unsigned long long& nflop,
                                 const Lane& L) {
-  double* SU[2] = {sm, sm + img_doubles(C, RE)};
+  constexpr int IM = img_doubles(C, RE);
+  const int NS = D.cstages;   // U_k ring: stage i holds the image of step k with (N - 1 - k) % NS == i
   const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
   const int go = 2 * x.off;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
@@ -1400,21 +1403,22 @@ __device__ void blk_suffix_task(const BlkDev& D, int N, const double* U, const d
       if constexpr (!RE) A.im[r][i] = im;
     }
   bstore_img_l2(X + (size_t)(N - 1) * stride + go, A, x, L, l2_evict_first());
-  if (leader && N > 1) tma_grp_img(SU[(N - 1) & 1], U + (size_t)(N - 1) * stride + go, C, &bar[(N - 1) & 1], RE);
-  uint32_t ph[2] = {0, 0};
-  for (int k = N - 1; k >= 1; --k) {
-    const int cur = k & 1;
-    grp_sync(x);   // buffer cur^1 (read at step k+1) is free
-    if (leader && k - 1 >= 1) {
-      fence_proxy_async();
-      tma_grp_img(SU[cur ^ 1], U + (size_t)(k - 1) * stride + go, C, &bar[cur ^ 1], RE);
-    }
-    mbar_wait(&bar[cur], ph[cur]);
-    ph[cur] ^= 1;
+  if (leader)
+    for (int i = 0; i < NS && N - 1 - i >= 1; ++i)
+      tma_grp_img(sm + i * IM, U + (size_t)(N - 1 - i) * stride + go, C, &bar[i], RE);
+  uint32_t ph = 0;   // bit i: parity of stage i
+  for (int k = N - 1, st = 0; k >= 1; --k, st = (st + 1 == NS) ? 0 : st + 1) {
+    mbar_wait(&bar[st], (ph >> st) & 1);
+    ph ^= 1u << st;
     bzero(acc);
-    bmma<C, R, KS, RE>(acc, A, SU[cur], x, L);   // X_{k+1} U_k
+    bmma<C, R, KS, RE>(acc, A, sm + st * IM, x, L);   // X_{k+1} U_k
     bcopy(A, acc);
     bstore_img_l2(X + (size_t)(k - 1) * stride + go, A, x, L, l2_evict_first());
+    grp_sync(x);   // every warp done with stage st: refill it with the image NS steps ahead
+    if (leader && k - NS >= 1) {
+      fence_proxy_async();
+      tma_grp_img(sm + st * IM, U + (size_t)(k - NS) * stride + go, C, &bar[st], RE);
+    }
   }
   if (leader) nflop += (unsigned long long)(N - 1) * D.gflops[x.g];
 }
@@ -1427,14 +1431,12 @@ __global__ void __launch_bounds__(BLK_CHAIN_WARPS * 32) k_blk_suffix_chain(BlkDe
                                                                         double* __restrict__ X_img,
                                                                         unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id
+  __shared__ __align__(8) uint64_t bars[16][BLK_CHAIN_STAGES];   // per (slot, group) barrier id: the U_k ring
   const Lane L = lane_id();
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
-    if (T.rt0 == 0 && L.lane == 0) {
-      mbar_init(&bars[T.bar][0], 1);
-      mbar_init(&bars[T.bar][1], 1);
-    }
+    if (T.rt0 == 0 && L.lane == 0)
+      for (int i = 0; i < D.cstages; ++i) mbar_init(&bars[T.bar][i], 1);
   }
   fence_mbar_init();
   __syncthreads();
@@ -1467,26 +1469,22 @@ template <int C, int R, int KS, bool RE>
 __device__ void blk_prefix_task(const BlkDev& D, int N, const double* U, double* P, double2* lam, const Ctx& x,
                                 double* sm, uint64_t* bar, unsigned long long& nflop, const Lane& L) {
   constexpr int IM = img_doubles(C, RE);
-  double* SU[2] = {sm, sm + IM};
-  double* SP[2] = {sm + 2 * IM, sm + 3 * IM};
+  const int NS = D.cstages;   // U_k ring: stage k % NS; then the ping-pong pair of P images
+  double* SP[2] = {sm + NS * IM, sm + (NS + 1) * IM};
   const size_t stride = 2 * (size_t)D.packed;   // doubles per packed image
   const int go = 2 * x.off;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   BR<C, R, RE> A, acc;
   bset_identity(acc, x, L);                                          // P_0 = I
   bstore_img_l2(P + go, acc, x, L, l2_evict_first());
-  if (leader) tma_grp_img(SU[0], U + go, C, &bar[0], RE);
-  uint32_t ph[2] = {0, 0};
-  for (int k = 0; k < N; ++k) {
+  if (leader)
+    for (int i = 0; i < NS && i < N; ++i) tma_grp_img(sm + i * IM, U + (size_t)i * stride + go, C, &bar[i], RE);
+  uint32_t ph = 0;   // bit i: parity of stage i
+  for (int k = 0, st = 0; k < N; ++k, st = (st + 1 == NS) ? 0 : st + 1) {
     const int cur = k & 1;
-    grp_sync(x);   // SP[cur] holds P_k (all rows); SU[cur ^ 1], SP[cur ^ 1] were last read at step k - 1
-    if (leader && k + 1 < N) {
-      fence_proxy_async();
-      tma_grp_img(SU[cur ^ 1], U + (size_t)(k + 1) * stride + go, C, &bar[cur ^ 1], RE);
-    }
-    mbar_wait(&bar[cur], ph[cur]);
-    ph[cur] ^= 1;
-    bload_img(A, SU[cur], x, L);                                     // own rows of U_k
+    mbar_wait(&bar[st], (ph >> st) & 1);
+    ph ^= 1u << st;
+    bload_img(A, sm + st * IM, x, L);                                // own rows of U_k
     if (k == 0) {
       bcopy(acc, A);                                                 // P_1 = U_0
     } else {
@@ -1496,6 +1494,11 @@ __device__ void blk_prefix_task(const BlkDev& D, int N, const double* U, double*
     if (k + 1 < N) {
       bstore_img_l2(P + (size_t)(k + 1) * stride + go, acc, x, L, l2_evict_first());
       bstore_img(SP[cur ^ 1], acc, x, L);
+    }
+    grp_sync(x);   // SP[cur ^ 1] holds P_{k+1} (all rows); every warp done with SP[cur] and stage st
+    if (leader && k + NS < N) {
+      fence_proxy_async();
+      tma_grp_img(sm + st * IM, U + (size_t)(k + NS) * stride + go, C, &bar[st], RE);
     }
   }
   bstore_nat(lam + x.off, acc, x, L);                                // Lambda = U_{N-1} P_{N-1}
@@ -1509,14 +1512,12 @@ __global__ void __launch_bounds__(BLK_CHAIN_WARPS * 32) k_blk_prefix_chain(BlkDe
                                                                         double2* __restrict__ lam,
                                                                         unsigned long long* ctr) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[16][2];   // per (slot, group) barrier id
+  __shared__ __align__(8) uint64_t bars[16][BLK_CHAIN_STAGES];   // per (slot, group) barrier id: the U_k ring
   const Lane L = lane_id();
   for (int t = 0; t < D.ntask[L.w]; ++t) {
     const BlkTask T = D.task[L.w][t];
-    if (T.rt0 == 0 && L.lane == 0) {
-      mbar_init(&bars[T.bar][0], 1);
-      mbar_init(&bars[T.bar][1], 1);
-    }
+    if (T.rt0 == 0 && L.lane == 0)
+      for (int i = 0; i < D.cstages; ++i) mbar_init(&bars[T.bar][i], 1);
   }
   fence_mbar_init();
   __syncthreads();
@@ -2247,8 +2248,17 @@ int grp_smem_doubles(BlkDev& D, int (*per)(int, bool)) {
 int per3(int C, bool re) { return grp3_doubles(C, re); }
 int per_grad(int C, bool re) { return grp3_doubles(C, re) + 4 * img_doubles(C, re); }
 int per_pair(int C, bool re) { return img_doubles(C, re); }
-int per_chain(int C, bool re) { return 2 * img_doubles(C, re); }
-int per_prefix(int C, bool re) { return 4 * img_doubles(C, re); }
+template <int NS>
+int per_chain(int C, bool re) { return NS * img_doubles(C, re); }         // the U_k ring
+template <int NS>
+int per_prefix(int C, bool re) { return (NS + 2) * img_doubles(C, re); }  // the U_k ring + the P pair
+using PerFn = int (*)(int, bool);
+PerFn per_chain_fn(int ns) { return ns >= 4 ? per_chain<4> : ns == 3 ? per_chain<3> : per_chain<2>; }
+PerFn per_prefix_fn(int ns) { return ns >= 4 ? per_prefix<4> : ns == 3 ? per_prefix<3> : per_prefix<2>; }
+// U_k ring depth of the chain kernels: deep when the batch is small (few pulse chains per SM, each one
+// latency-bound on its next image), double-buffered when many chains share the SM (their shared memory
+// then decides how many groups' CTAs run side by side)
+int chain_stages(int batch) { return batch < 8 * num_sms() ? BLK_CHAIN_STAGES : 2; }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 }  // namespace
 
@@ -2425,7 +2435,8 @@ cudaError_t launch_blk_suffix_chain(const qal_block_plan& p, int batch, int N, c
     while (ns > 1 && (batch + ns - 1) / ns < 2 * num_sms()) ns >>= 1;
     L l;
     if (!to_dev(p, l.D, set.gmask, ns)) return cudaErrorInvalidValue;
-    l.bytes = (size_t)grp_smem_doubles(l.D, per_chain) * 8;
+    l.D.cstages = chain_stages(batch);
+    l.bytes = (size_t)grp_smem_doubles(l.D, per_chain_fn(l.D.cstages)) * 8;
     l.fn = chain_kernel(l.D);
     cudaError_t e = set_smem_fn((const void*)l.fn, l.bytes);
     if (e != cudaSuccess) return e;
@@ -2460,7 +2471,8 @@ cudaError_t launch_blk_chains(const qal_block_plan& p, int batch, int N, const d
       L l;
       l.prefix = pre != 0;
       if (!to_dev(p, l.D, set.gmask, ns)) return cudaErrorInvalidValue;
-      l.bytes = (size_t)grp_smem_doubles(l.D, pre ? per_prefix : per_chain) * 8;
+      l.D.cstages = chain_stages(batch);
+      l.bytes = (size_t)grp_smem_doubles(l.D, pre ? per_prefix_fn(l.D.cstages) : per_chain_fn(l.D.cstages)) * 8;
       l.pfn = pre ? prefix_kernel(l.D) : nullptr;
       l.cfn = pre ? nullptr : chain_kernel(l.D);
       cudaError_t e = set_smem_fn(pre ? (const void*)l.pfn : (const void*)l.cfn, l.bytes);
