@@ -45,7 +45,10 @@ constexpr int BLK_MAX_WARPS = 16;
 constexpr int BLK_FUSED_WARPS = 8;   // one item per CTA, all groups (every kernel but fwd / grad sets)
 constexpr int BLK_MAX_SLOTS = 5;   // independent item streams per CTA (group-specialised launches)
 constexpr int BLK_CHAIN_WARPS = 12;   // launch bound of the suffix-chain kernel (4 pulses x 3 warps)
-constexpr int BLK_CHAIN_STAGES = 4;   // deepest U_k ring of the chain kernels
+#ifndef QAL_CHAIN_STAGES
+#define QAL_CHAIN_STAGES 4
+#endif
+constexpr int BLK_CHAIN_STAGES = QAL_CHAIN_STAGES;   // deepest U_k ring of the chain kernels (<= 8)
 // real MMAs per complex 8x8x4 step of the complex blocks: 4 (default) or 3 (Gauss, -DQAL_BLK_3M)
 #ifdef QAL_BLK_3M
 constexpr int BLK_CPLX_MMAS = 3;
@@ -2253,12 +2256,31 @@ int per_chain(int C, bool re) { return NS * img_doubles(C, re); }         // the
 template <int NS>
 int per_prefix(int C, bool re) { return (NS + 2) * img_doubles(C, re); }  // the U_k ring + the P pair
 using PerFn = int (*)(int, bool);
-PerFn per_chain_fn(int ns) { return ns >= 4 ? per_chain<4> : ns == 3 ? per_chain<3> : per_chain<2>; }
-PerFn per_prefix_fn(int ns) { return ns >= 4 ? per_prefix<4> : ns == 3 ? per_prefix<3> : per_prefix<2>; }
+PerFn per_chain_fn(int ns) {
+  switch (ns) {
+    case 8: return per_chain<8>;
+    case 6: return per_chain<6>;
+    case 4: return per_chain<4>;
+    case 3: return per_chain<3>;
+    default: return per_chain<2>;
+  }
+}
+PerFn per_prefix_fn(int ns) {
+  switch (ns) {
+    case 8: return per_prefix<8>;
+    case 6: return per_prefix<6>;
+    case 4: return per_prefix<4>;
+    case 3: return per_prefix<3>;
+    default: return per_prefix<2>;
+  }
+}
 // U_k ring depth of the chain kernels: deep when the batch is small (few pulse chains per SM, each one
 // latency-bound on its next image), double-buffered when many chains share the SM (their shared memory
 // then decides how many groups' CTAs run side by side)
-int chain_stages(int batch) { return batch < 8 * num_sms() ? BLK_CHAIN_STAGES : 2; }
+#ifndef QAL_CHAIN_STAGES_LARGE
+#define QAL_CHAIN_STAGES_LARGE 2
+#endif
+int chain_stages(int batch) { return batch < 8 * num_sms() ? BLK_CHAIN_STAGES : QAL_CHAIN_STAGES_LARGE; }
 int tmem_cols_for(const BlkDev& D) { return D.tmem_cols; }
 }  // namespace
 
