@@ -1018,7 +1018,10 @@ BlkGradWs blk_grad_ws(const qal_block_plan* p, int batch, int count, void* ws) {
 //    slice independently (full occupancy), then the prefix chain folds the stored U_k -- concurrently with
 //    the suffix chain when its seed is known (the fidelity gradient).  Costs one more read of the U_k
 //    images per chain (the chains run at ~85% of the HBM bandwidth).
-bool blk_split_forward(int batch) { return batch < 8 * num_sms(); }
+#ifndef QAL_BLK_SPLIT_BELOW
+#define QAL_BLK_SPLIT_BELOW 8   // split forward below this many pulses per SM
+#endif
+bool blk_split_forward(int batch) { return batch < QAL_BLK_SPLIT_BELOW * num_sms(); }
 int blk_forward_impl(const qal_block_plan* p, int batch, const BlkCommon& c, double2* Lam, int* status, void* ws,
                      cudaStream_t st, bool with_suffix, const double2* V) {
   const BlkGradWs w = blk_grad_ws(p, batch, c.G.count, ws);
