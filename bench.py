@@ -240,14 +240,14 @@ def load_traffic():
 def roofline_of(stages, prods, steps, peak_tf, units_per_launch):
     """Roofline of the dominant kernel (largest device time in the profiling window), the per-stage
     split and the algorithmic flops per step.  Block stages count flops (8 s^3 per block product),
-    dense stages count 64x64 products (qal.FLOP_STAGES, driver.stage_flops).  The fused block forward
-    counts its fold products apart (blk_prefix_chain, no launches of its own): they belong to its time."""
+    dense stages count 64x64 products (qal.FLOP_STAGES, driver.stage_flops).  Every stage's flops are
+    those of the launches its time covers: the fused block forward counts its fold products apart
+    (blk_fold, no launches of its own; they belong to blk_expm_fold's time), and the split forward's
+    concurrent prefix + suffix chains are one timing record (blk_prefix_chain) with both chains' flops."""
     from paper_2511_13330_b200 import driver, qal
     fl = {s: driver.stage_flops(prods[i], s) for i, s in enumerate(qal.STAGES)}
-    if stages["blk_prefix_chain"][1] == 0:          # fused forward: its fold flops belong to its own time
-        fl["blk_expm_fold"] += fl["blk_prefix_chain"]
-    elif stages["blk_suffix_chain"][1] == 0:        # prefix and suffix chains timed as one concurrent launch
-        fl["blk_prefix_chain"] += fl["blk_suffix_chain"]
+    fl["blk_expm_fold"] += fl.pop("blk_fold")
+    stages = {s: v for s, v in stages.items() if s != "blk_fold"}
     dom = max(stages, key=lambda s: stages[s][0])
     dom_ms, dom_launch = stages[dom]
     dom_flops_per_launch = fl[dom] / max(dom_launch, 1)
@@ -273,18 +273,17 @@ def fig2_split(qal, stages, prods, steps):
     products (Eq. 15: the prefix fold and the suffix chain, two concurrent chains timed as one launch).
     (Paths with the fused chunk forward apportion that kernel's time by its two flop counts.)"""
     ix = qal.STAGES.index
-    f_exp, f_fold = prods[ix("blk_expm_fold")], prods[ix("blk_prefix_chain")]
-    f_suf = prods[ix("blk_suffix_chain")]
+    f_exp, f_fold = prods[ix("blk_expm_fold")], prods[ix("blk_fold")]
+    f_chains = prods[ix("blk_prefix_chain")] + prods[ix("blk_suffix_chain")]
     t_fwd = stages["blk_expm_fold"][0]
-    if stages["blk_prefix_chain"][1] > 0:
-        t_exp, t_mul = t_fwd, stages["blk_prefix_chain"][0] + stages["blk_suffix_chain"][0]
-        note = "expansions: the persistent expm kernel; products: the prefix and suffix chains (concurrent)"
-    else:
-        t_exp = t_fwd * f_exp / max(f_exp + f_fold, 1)
-        t_mul = t_fwd - t_exp + stages["blk_suffix_chain"][0]
-        note = "fused expm + fold kernel: its time apportioned by flops"
+    # the fused kernel's time apportioned by its two flop counts (expansions vs the fold products), the
+    # chain kernels (split prefix + suffix, per-group suffix) wholly products
+    t_exp = t_fwd * f_exp / max(f_exp + f_fold, 1)
+    t_mul = t_fwd - t_exp + stages["blk_prefix_chain"][0] + stages["blk_suffix_chain"][0]
+    note = ("expansions: the expm work of the forward kernels; products: the fused fold (time apportioned by "
+            "flops), the prefix and suffix chains")
     return {"expansion": {"flops_per_step": f_exp / steps, "ms_per_step": t_exp / steps},
-            "multiplication": {"flops_per_step": (f_fold + f_suf) / steps, "ms_per_step": t_mul / steps},
+            "multiplication": {"flops_per_step": (f_fold + f_chains) / steps, "ms_per_step": t_mul / steps},
             "note": note + "; the gradient stage (dual expansion + products) is reported apart in stage_split"}
 
 
@@ -456,21 +455,30 @@ def run_ours(args):
         nres = B_total if gather else B
         hF = torch.empty(nres, dtype=torch.float64).pin_memory()
         hg = torch.empty((nres,) + tuple(prob.u.shape[1:]), dtype=torch.float64).pin_memory()
+        pipelined = world == 1 or not gather
         D.barrier()
         sync()
         tm.start()
         for _ in range(args.steps):
-            eng.u.copy_(hu, non_blocking=True)
-            eng.H0.copy_(hH0, non_blocking=True)
-            F2, g2 = step()
-            hF.copy_(F2, non_blocking=True)
-            hg.copy_(g2, non_blocking=True)
+            if pipelined:   # the public end-to-end call: copies on two streams, overlapped with the compute
+                eng.step_host(hH0, hu, hF, hg)
+            else:           # ranks > 1: the gathered results are copied out after the exchange
+                eng.u.copy_(hu, non_blocking=True)
+                eng.H0.copy_(hH0, non_blocking=True)
+                F2, g2 = step()
+                hF.copy_(F2, non_blocking=True)
+                hg.copy_(g2, non_blocking=True)
+        if pipelined:
+            eng.host_fence()   # the timed region ends after the last step's results are in host memory
         tm.stop()
         sync()
         t2 = D.max(tm.ms(), dev)
         e2e = {"value": slices_total / (t2 * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(hu.numel() * 8 + hH0.numel() * 16),
-               "d2h_bytes_per_step": int(hF.numel() * 8 + hg.numel() * 8)}
+               "d2h_bytes_per_step": int(hF.numel() * 8 + hg.numel() * 8),
+               "copies": ("PulseBatch.step_host: per-sub-batch H2D / D2H on two copy streams overlapped with the "
+                          "compute (step s + 1's inputs stream in under step s)" if pipelined else
+                          "serial H2D before / D2H after each step")}
 
     # ---------------- roofline of the dominant kernel (largest device time in the window)
     prods = counters.cpu().tolist()

@@ -537,7 +537,11 @@ enum { QAL_ST_LIOUV = 0, QAL_ST_COMM = 1, QAL_ST_EXPM = 2, QAL_ST_TREE = 3, QAL_
        /* coherence-block path: these counters accumulate ALGORITHMIC FLOPs (8 s^3 per complex
         * product of an s x s block, padding excluded), not product counts */
        QAL_ST_BLK_EXPM = 9, QAL_ST_BLK_TREE = 10, QAL_ST_BLK_PREFIX = 11, QAL_ST_BLK_SUFFIX = 12,
-       QAL_ST_BLK_GRAD = 13, QAL_ST_BLK_GEMM = 14, QAL_NSTAGE = 15 };
+       QAL_ST_BLK_GRAD = 13, QAL_ST_BLK_GEMM = 14,
+       /* the fold products inside the fused block forward (k_blk_expm_fold): flops only, no
+        * launches of their own (their time is inside QAL_ST_BLK_EXPM); QAL_ST_BLK_PREFIX counts
+        * the separate prefix-chain kernel alone */
+       QAL_ST_BLK_FOLD = 15, QAL_NSTAGE = 16 };
 int qal_profile_begin(unsigned long long *dev_counters);
 int qal_profile_end(double *ms, int *launches);
 

@@ -97,7 +97,7 @@ unsigned long long* prof_counter(int stage) {
 static const char* const kStageNames[NSTAGE] = {
     "qal:liouvillian", "qal:commutators", "qal:expm_fold", "qal:tree", "qal:fidelity", "qal:prefix_chain",
     "qal:suffix_chain", "qal:grad_slices", "qal:dense_gemm", "qal:blk_expm_fold", "qal:blk_tree",
-    "qal:blk_prefix", "qal:blk_suffix_chain", "qal:blk_grad_slices", "qal:blk_gemm"};
+    "qal:blk_prefix", "qal:blk_suffix_chain", "qal:blk_grad_slices", "qal:blk_gemm", "qal:blk_fold"};
 void prof_pre(int stage, cudaStream_t st) {
   nvtxRangePushA(stage >= 0 && stage < NSTAGE ? kStageNames[stage] : "qal");
   ProfState& P = prof();

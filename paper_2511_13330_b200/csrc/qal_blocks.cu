@@ -126,6 +126,8 @@ struct BlkDev {
   int tr_k;                         // trace entries per warp / slot (J + ncomm)
   int tr_buf;                       // doubles per parity: (nwarps + nslot) * tr_k
   int tcache_w[BLK_MAX_WARPS];      // double2 offset of warp w's cache slice
+  int omc;                          // gradient kernel: first TMEM slot of the Omega basis cache (the warp's
+                                    // strips of Lc_0..Lc_{J-1}, then L0_b of the current pulse), -1: none
   signed char perm[QAL_BLK_MAX_ROWS];      // packed row -> natural index (-1 pad)
   unsigned char weight[QAL_BLK_MAX_ROWS];  // 0 pad, 1, 2
   signed char inv[64];                     // natural index -> packed row (-1 not stored)
@@ -149,6 +151,7 @@ struct BlkDev {
 bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot = 1, bool whole_c2 = false,
             bool whole_c3 = false, int tslots = BLK_TSLOTS) {
   memset(&D, 0, sizeof(D));
+  D.omc = -1;
   D.ngroups = p.ngroups;
   D.packed = p.packed;
   D.d = p.d;
@@ -785,6 +788,25 @@ __device__ __forceinline__ void bt_load(BR<C, R, RE>& s, uint32_t addr) {
 template <int C, int R, bool RE>
 __device__ __forceinline__ void bt_axpy(BR<C, R, RE>& acc, double a, uint32_t addr) {
   if (a == 0.0) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t v[4 * C], w[4 * C];
+    tm_ld_plane<C>(addr + (RE ? 4 : 8) * C * r, v);
+    if constexpr (!RE) tm_ld_plane<C>(addr + 8 * C * r + 4 * C, w);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      acc.re[r][i] = fma(a, __hiloint2double(static_cast<int>(v[2 * i + 1]), static_cast<int>(v[2 * i])), acc.re[r][i]);
+      if constexpr (!RE)
+        acc.im[r][i] =
+            fma(a, __hiloint2double(static_cast<int>(w[2 * i + 1]), static_cast<int>(w[2 * i])), acc.im[r][i]);
+    }
+  }
+}
+
+// acc += a * strip(addr) for every a (no zero shortcut: the arithmetic of baxpy_nat, term for term)
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bt_fma(BR<C, R, RE>& acc, double a, uint32_t addr) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t v[4 * C], w[4 * C];
@@ -1862,8 +1884,12 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const int nodes = (G.mode == 1) ? 2 : 1;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   uint32_t ph = 0;
+  // this slot's items: the contiguous range [lo, hi) (consecutive slices of a pulse, so the pulse's L0_b
+  // strip is loaded once per pulse, not per item); every warp of the slot runs the same sequence
+  const int sid = blockIdx.x * D.nslot + x.slot, nsl = gridDim.x * D.nslot;
+  const int lo = (int)((long long)items * sid / nsl), hi = (int)((long long)items * (sid + 1) / nsl);
   auto prefetch = [&](int it) {   // group leader: bulk-copy X_{k+1} -> SN, P_k -> SD of item `it`
-    if (leader && it < items) {
+    if (leader && it < hi) {
       fence_proxy_async();
       tma_grp_img(sm + 2 * IM, X_img + (size_t)it * stride + 2 * x.off, C, &bars[0], RE);
       tma_grp_img(sm, P_img + (size_t)it * stride + 2 * x.off, C, &bars[1], RE);
@@ -1871,24 +1897,55 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   };
   // the control values of item `it` into L1 ahead of its Omega build (one line per warp)
   auto prefetch_u = [&](int it) {
-    if (L.lane == 0 && it < items)
+    if (L.lane == 0 && it < hi)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(G.u + (size_t)it * nodes * B.J));
   };
   BR<C, R, RE> A, acc, Om;
-  // this slot's item stream: items item0, item0 + istride, ...
-  const int item0 = blockIdx.x * D.nslot + x.slot, istride = gridDim.x * D.nslot;
   const int w0 = x.slot * D.swarps;   // first warp of the slot (trace sum, flags)
-  prefetch(item0);
-  prefetch_u(item0 + istride);
+  prefetch(lo);
+  prefetch_u(lo + 1);
+  // Omega basis cache (D.omc >= 0: no commutator terms): the warp's strips of Lc_j in TMEM slots omc + j
+  // (once per launch) and of L0_b in slot omc + J (once per pulse), so the per-item Omega build reads TMEM
+  // instead of the L2 (the same fma sequence as bbuild_omega, term for term)
+  const bool omc = D.omc >= 0 && B.ncomm == 0;
+  const uint32_t tso = D.tstride[L.w];
+  const uint32_t TL0 = tm + (uint32_t)(D.omc + B.J) * tso;
+  long long cur_b = -1;
+  if (omc) {
+    for (int j = 0; j < B.J; ++j) {
+      bload_nat(Om, B.Lc + (size_t)j * B.packed + x.off, x, L);
+      bt_store(tm + (uint32_t)(D.omc + j) * tso, Om);
+    }
+  }
+  auto build = [&](int it) {
+    const int b = it / N, k = it % N;
+    if (!omc) {
+      bbuild_omega(Om, B, G, b, k, x, L);
+      return;
+    }
+    const long long key = B.L0_stride ? b : 0;
+    if (key != cur_b) {
+      bload_nat(Om, B.L0 + (size_t)b * B.L0_stride + x.off, x, L);
+      bt_store(TL0, Om);
+      cur_b = key;
+    }
+    const double* u = G.u + ((size_t)b * G.count + k) * nodes * B.J;
+    bzero(Om);
+    bt_fma(Om, G.h, TL0);
+    for (int j = 0; j < B.J; ++j) {
+      const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * B.J + j);
+      bt_fma(Om, 0.5 * G.h * (v1 + v2), tm + (uint32_t)(D.omc + j) * tso);
+    }
+  };
   // the forward's (m, s) code of an item, loaded with its Omega one item ahead (an L2 round trip that the
   // dual pass of the current item hides)
   auto code_of = [&](int it) -> unsigned short {
     return scheme ? __ldg(scheme + ((size_t)(it / N) * N + it % N) * D.ngroups + x.g) : (unsigned short)0;
   };
   unsigned short code = 0;
-  if (item0 < items) {
-    bbuild_omega(Om, B, G, item0 / N, item0 % N, x, L);
-    code = code_of(item0);
+  if (lo < hi) {
+    build(lo);
+    code = code_of(lo);
   }
   if (cache) {   // PWC trace basis: the warp's own entries B_m[c][row] x row weight, once per launch
     for (int mm = 0; mm < B.J; ++mm)
@@ -1947,7 +2004,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     }
   };
   int idx = 0;
-  for (int item = item0; item < items; item += istride, ++idx) {
+  for (int item = lo; item < hi; ++item, ++idx) {
     const int b = item / N, k = item % N;
     QAL_DCHECK(b < batch && k < N);
     bcopy(A, Om);
@@ -1956,21 +2013,20 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
                                                ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
                                                bad_sh + (idx & 3), scheme, code, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
-    const int nx = item + istride;
+    const int nx = item + 1;
     slot_sync(D, x.slot);   // every warp of the slot done with this item's images; previous traces complete
     prefetch(nx);
-    prefetch_u(nx + istride);
-    if (L.w == w0 && idx > 0) finish(item - istride, red_tr + (size_t)(par ^ 1) * D.tr_buf, (idx - 1) & 3);
-    if (nx < items) {
-      bbuild_omega(Om, B, G, nx / N, nx % N, x, L);
+    prefetch_u(nx + 1);
+    if (L.w == w0 && idx > 0) finish(item - 1, red_tr + (size_t)(par ^ 1) * D.tr_buf, (idx - 1) & 3);
+    if (nx < hi) {
+      build(nx);
       code = code_of(nx);
     }
     double* rt = red_tr + (size_t)par * D.tr_buf;
     blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
   }
   slot_sync(D, x.slot);   // the last item's traces complete
-  if (L.w == w0 && idx > 0)
-    finish(item0 + (idx - 1) * istride, red_tr + (size_t)((idx - 1) & 1) * D.tr_buf, (idx - 1) & 3);
+  if (L.w == w0 && idx > 0) finish(hi - 1, red_tr + (size_t)((idx - 1) & 1) * D.tr_buf, (idx - 1) & 3);
 }
 
 // FC == 0: any mix of roles (runtime dispatch); else every warp runs role <FC, FR, FKS, FRE> and the
@@ -2425,7 +2481,7 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
     const int need = (items + l.D.nslot - 1) / l.D.nslot;
     const int grid = std::min(need, l.per_sm * num_sms());
     l.fn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, B, G, O, items, tmem_cols_for(l.D), prof_counter(ST_BLK_EXPM),
-                                                prof_counter(ST_BLK_PREFIX));
+                                                prof_counter(ST_BLK_FOLD));
     ++launch_counter();
     return cudaGetLastError();
   });
@@ -2509,9 +2565,8 @@ cudaError_t launch_blk_chains(const qal_block_plan& p, int batch, int N, const d
     const int grid = (batch + l.D.nslot - 1) / l.D.nslot;
     if (l.prefix)
       l.pfn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, batch, N, U_img, P_img, lam, prof_counter(ST_BLK_PREFIX));
-    else
-      l.cfn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, batch, N, U_img, V, Cseed, X_img,
-                                                  prof_counter(ST_BLK_SUFFIX));
+    else   // flops counted under the stage that times this launch (the concurrent pair is one record)
+      l.cfn<<<grid, 32 * l.D.nwarps, l.bytes, s>>>(l.D, batch, N, U_img, V, Cseed, X_img, prof_counter(stage));
     ++launch_counter();
     return cudaGetLastError();
   });
@@ -2545,8 +2600,10 @@ struct GradLaunch {
   size_t bytes;
   int per_sm;
 };
-static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g) {
-  if (!to_dev(p, g.D, gmask, ns)) return false;
+static bool grad_layout_t(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g,
+                          int tslots) {
+  if (!to_dev(p, g.D, gmask, ns, false, false, tslots)) return false;
+  if (tslots > BLK_TSLOTS) g.D.omc = BLK_TSLOTS;
   int base = grp_smem_doubles(g.D, per_grad);
   g.D.tr_k = std::max(1, B.J + B.ncomm);
   g.D.tr_buf = (g.D.nwarps + g.D.nslot) * g.D.tr_k;
@@ -2565,6 +2622,19 @@ static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const B
     }
   }
   return g.per_sm > 0;
+}
+// + the Omega basis cache in TMEM (J + 1 more strip slots per warp) when the build has no commutator terms
+// and the cache costs no co-resident CTA (-DQAL_BLK_NO_OMC: never, experiment builds)
+constexpr int BLK_OMC_MAXJ = 3;
+static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g) {
+  if (!grad_layout_t(p, gmask, ns, B, g, BLK_TSLOTS)) return false;
+#ifndef QAL_BLK_NO_OMC
+  GradLaunch t;
+  if (B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && grad_layout_t(p, gmask, ns, B, t, BLK_TSLOTS + B.J + 1) &&
+      t.per_sm >= g.per_sm)
+    g = t;
+#endif
+  return true;
 }
 
 cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const BlkBasis& B, const SliceGrid& G,

@@ -98,7 +98,7 @@ cudaError_t ensure_smem(const void* fn, size_t bytes);
 
 // profiling window (qal_profile_begin/end): stage ids as in qal.h
 enum { ST_LIOUV = 0, ST_COMM, ST_EXPM, ST_TREE, ST_FID, ST_PREFIX, ST_SUFFIX, ST_GRAD, ST_DENSE_GEMM,
-       ST_BLK_EXPM, ST_BLK_TREE, ST_BLK_PREFIX, ST_BLK_SUFFIX, ST_BLK_GRAD, ST_BLK_GEMM, NSTAGE };
+       ST_BLK_EXPM, ST_BLK_TREE, ST_BLK_PREFIX, ST_BLK_SUFFIX, ST_BLK_GRAD, ST_BLK_GEMM, ST_BLK_FOLD, NSTAGE };
 unsigned long long* prof_counter(int stage);   // device counter slot or nullptr
 void prof_pre(int stage, cudaStream_t st);      // record start event (no-op when off)
 void prof_post(int stage, cudaStream_t st);     // record end event

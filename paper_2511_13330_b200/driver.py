@@ -84,6 +84,7 @@ class PulseBatch:
             self.sub = min(sub_batch, self.B)
             self.ws_bytes = qal.block_workspace_bytes(self.plan, op, self.sub, self.N)
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=dev)
+        self._pipe = None
 
     def _s(self):
         s = torch.cuda.current_stream() if self.stream is None else self.stream
@@ -97,15 +98,26 @@ class PulseBatch:
         qal._check(rc, "qal_build_liouvillian")
         return lib.qal_last_launch_count()
 
-    def step(self):
+    def subs(self):
+        """The sub-batches (first pulse, pulses) one step runs, in order."""
+        return [(b0, min(self.sub, self.B - b0)) for b0 in range(0, self.B, self.sub)]
+
+    def step(self, hooks=None):
+        """One step on the device-resident inputs.  `hooks` (step_host's copy pipeline): an object with
+        after_basis(), before_sub(i, b0, nb) and after_sub(i, b0, nb), called as the work is enqueued."""
         lib = qal.load()
         st = self._s()
+        if hooks is not None:
+            hooks.before_basis()
         launches = self._build_basis()
+        if hooks is not None:
+            hooks.after_basis()
         if self.structure == "blocks":
-            return self._step_blocks(lib, st, launches)
+            return self._step_blocks(lib, st, launches, hooks)
         plane = self.n * self.n
-        for b0 in range(0, self.B, self.sub):
-            nb = min(self.sub, self.B - b0)
+        for i, (b0, nb) in enumerate(self.subs()):
+            if hooks is not None:
+                hooks.before_sub(i, b0, nb)
             rc = lib.qal_fidelity_grad(
                 self.d, nb, self.N, self.T, self.order, qal.QAL_CTRL_PWC, self.J,
                 ctypes.c_void_p(self.u.data_ptr() + b0 * self.N * self.J * 8),
@@ -115,17 +127,20 @@ class PulseBatch:
                 None, ctypes.c_void_p(self.status.data_ptr() + b0 * 4), _p(self.ws), self.ws_bytes, st)
             qal._check(rc, "qal_fidelity_grad")
             launches += lib.qal_last_launch_count()
+            if hooks is not None:
+                hooks.after_sub(i, b0, nb)
         self.launches = launches
         return self.F, self.grad
 
-    def _step_blocks(self, lib, st, launches):
+    def _step_blocks(self, lib, st, launches, hooks=None):
         pl = ctypes.byref(self.plan)
         for src, dst in ((self.L0, self.L0p), (self.Lc, self.Lcp)):
             qal._check(lib.qal_block_pack(pl, src.shape[0], _p(src), _p(dst), None, st), "qal_block_pack")
             launches += lib.qal_last_launch_count()
         P = self.plan.packed
-        for b0 in range(0, self.B, self.sub):
-            nb = min(self.sub, self.B - b0)
+        for i, (b0, nb) in enumerate(self.subs()):
+            if hooks is not None:
+                hooks.before_sub(i, b0, nb)
             rc = lib.qal_block_fidelity_grad(
                 pl, nb, self.N, self.T, self.order, qal.QAL_CTRL_PWC, self.J,
                 ctypes.c_void_p(self.u.data_ptr() + b0 * self.N * self.J * 8),
@@ -135,6 +150,8 @@ class PulseBatch:
                 None, ctypes.c_void_p(self.status.data_ptr() + b0 * 4), _p(self.ws), self.ws_bytes, st)
             qal._check(rc, "qal_block_fidelity_grad")
             launches += lib.qal_last_launch_count()
+            if hooks is not None:
+                hooks.after_sub(i, b0, nb)
         # the structure check of this step's operators, per pulse (after the calls above, which reset
         # their status slices on entry): L0_b -> status[b]; a shared L_j -> every pulse
         qal._check(lib.qal_block_check(pl, self.B, _p(self.L0), 0, _p(self.status), self.B, st), "qal_block_check")
@@ -145,10 +162,96 @@ class PulseBatch:
         self.launches = launches
         return self.F, self.grad
 
+    def step_host(self, hH0, hu, hF, hg):
+        """One step from pinned host inputs to pinned host results (the end-to-end call): H0 [B][d][d]
+        and u [B][N][J] are copied in, F [B] and grad [B][N][J] copied out, all on two copy streams that
+        overlap the compute: sub-batch i's controls go in as soon as the previous step's sub-batch i is done
+        with them (so step s + 1's inputs stream in under step s), its results go out as soon as it is done
+        (under sub-batch i + 1).  The next step's compute is not held back by this step's last copy-out;
+        `host_fence()` orders the caller's stream after it (an event recorded there afterwards marks the
+        results in host memory) and `synchronize_host()` waits for it on the host."""
+        if self._pipe is None:
+            self._pipe = _CopyPipeline(self)
+        return self._pipe.run(hH0, hu, hF, hg)
+
+    def host_fence(self):
+        """Order the caller's stream after the last step_host's copy-out."""
+        if self._pipe is not None:
+            self._pipe.fence()
+
+    def synchronize_host(self):
+        """Wait until the last step_host's results are in host memory."""
+        self.host_fence()
+        (torch.cuda.current_stream() if self.stream is None else self.stream).synchronize()
+
     def structure_ok(self) -> bool:
         """False if the last step's device check found an operator coupling two blocks of the plan
         (those pulses carry QAL_ERR_STRUCTURE in `status`; synchronises)."""
         return self.structure == "dense" or not bool((self.status == qal.QAL_ERR_STRUCTURE).any())
+
+
+class _CopyPipeline:
+    """PulseBatch.step_host's copy streams and the events that order them against the compute stream
+    (across steps: a buffer is overwritten only after its previous reader is done)."""
+
+    def __init__(self, eng):
+        self.eng = eng
+        dev = eng.u.device
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        n = len(eng.subs())
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        self.h0_in, self.h0_free = ev(), ev()              # H0 copied in / basis build done with it
+        self.u_in = [ev() for _ in range(n)]               # sub-batch i's controls copied in
+        self.u_free = [ev() for _ in range(n)]             # sub-batch i's compute done (u read, F / grad written)
+        self.out_done = [ev() for _ in range(n)]           # sub-batch i's results copied out
+        self.started = False
+
+    def run(self, hH0, hu, hF, hg):
+        eng = self.eng
+        comp = torch.cuda.current_stream() if eng.stream is None else eng.stream
+        first = not self.started
+        self.started = True
+        subs = eng.subs()
+        with torch.cuda.stream(self.h2d):
+            if not first:
+                self.h2d.wait_event(self.h0_free)
+            eng.H0.copy_(hH0, non_blocking=True)
+            self.h0_in.record(self.h2d)
+            for i, (b0, nb) in enumerate(subs):
+                if not first:
+                    self.h2d.wait_event(self.u_free[i])
+                eng.u[b0:b0 + nb].copy_(hu[b0:b0 + nb], non_blocking=True)
+                self.u_in[i].record(self.h2d)
+        pipe = self
+
+        class Hooks:
+            def before_basis(self):
+                comp.wait_event(pipe.h0_in)
+
+            def after_basis(self):
+                pipe.h0_free.record(comp)
+
+            def before_sub(self, i, b0, nb):
+                comp.wait_event(pipe.u_in[i])
+                if not first:
+                    comp.wait_event(pipe.out_done[i])      # F / grad of sub-batch i copied out last step
+
+            def after_sub(self, i, b0, nb):
+                pipe.u_free[i].record(comp)
+                with torch.cuda.stream(pipe.d2h):
+                    pipe.d2h.wait_event(pipe.u_free[i])
+                    hF[b0:b0 + nb].copy_(eng.F[b0:b0 + nb], non_blocking=True)
+                    if eng.grad is not None and hg is not None:
+                        hg[b0:b0 + nb].copy_(eng.grad[b0:b0 + nb], non_blocking=True)
+                    pipe.out_done[i].record(pipe.d2h)
+
+        eng.step(hooks=Hooks())
+        return hF, hg
+
+    def fence(self):
+        comp = torch.cuda.current_stream() if self.eng.stream is None else self.eng.stream
+        comp.wait_event(self.out_done[len(self.eng.subs()) - 1])
 
 
 def shard_range(total: int, world: int, rank: int):

@@ -28,14 +28,15 @@ QAL_BLK_SETS_DEFAULT, QAL_BLK_SETS_FUSED, QAL_BLK_SETS_PAIRS = 0, 1, 2
 QAL_MAX_CTRL = 8
 STAGES = ["liouvillian", "commutators", "expm_fold", "tree", "fidelity", "prefix_chain", "suffix_chain",
           "grad_slices", "dense_gemm", "blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain",
-          "blk_grad_slices", "blk_gemm"]
+          "blk_grad_slices", "blk_gemm", "blk_fold"]
 # stages whose device counter holds algorithmic FLOPs (coherence-block path), not product counts
-FLOP_STAGES = {"blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain", "blk_grad_slices", "blk_gemm"}
+FLOP_STAGES = {"blk_expm_fold", "blk_tree", "blk_prefix_chain", "blk_suffix_chain", "blk_grad_slices", "blk_gemm", "blk_fold"}
 KERNELS = {"liouvillian": "k_liouvillian", "commutators": "k_commutators", "expm_fold": "k_expm_fold",
            "tree": "k_tree_level", "fidelity": "k_fidelity", "prefix_chain": "k_prefix_chain",
            "suffix_chain": "k_suffix_chain", "grad_slices": "k_grad_slices", "dense_gemm": "k_dense_gemm",
            "blk_expm_fold": "k_blk_expm_fold", "blk_tree": "k_blk_tree_level", "blk_prefix_chain": "k_blk_prefix_chain",
-           "blk_suffix_chain": "k_blk_suffix_chain", "blk_grad_slices": "k_blk_grad_slices", "blk_gemm": "k_bb_gemm"}
+           "blk_suffix_chain": "k_blk_suffix_chain", "blk_grad_slices": "k_blk_grad_slices", "blk_gemm": "k_bb_gemm",
+           "blk_fold": "k_blk_expm_fold"}
 
 _EXPORTS = {
     "qal_abi_version": (ctypes.c_int, []),
