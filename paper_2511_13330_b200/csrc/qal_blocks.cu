@@ -75,6 +75,12 @@ constexpr int BLK_TSLOTS = BLK_TMEM_SCR ? 8 : 4;       // TMEM strip slots per w
 #endif
 constexpr bool BLK_SPLIT_ACC = QAL_BLK_SPLIT_ACC != 0;
 constexpr int BLK_MAX_TASKS = 3;
+// gradient pass: consecutive items (slices of a pulse) per run of a slot's item sequence (0: one contiguous
+// range per slot)
+#ifndef QAL_BLK_GRAD_RUN
+#define QAL_BLK_GRAD_RUN 16
+#endif
+constexpr int BLK_GRAD_RUN = QAL_BLK_GRAD_RUN;
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
 #endif
@@ -1884,12 +1890,22 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const int nodes = (G.mode == 1) ? 2 : 1;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   uint32_t ph = 0;
-  // this slot's items: the contiguous range [lo, hi) (consecutive slices of a pulse, so the pulse's L0_b
-  // strip is loaded once per pulse, not per item); every warp of the slot runs the same sequence
+  // this slot's items: runs of BLK_GRAD_RUN consecutive items (slices of one pulse, so the pulse's L0_b
+  // strip is loaded once per run), the runs dealt round robin over the slots of the grid (the slots in
+  // flight then read a compact window of the image workspace); BLK_GRAD_RUN = 0: one contiguous range per
+  // slot.  Every warp of the slot runs the same sequence; item_at(j) = the slot's j-th item or -1.
   const int sid = blockIdx.x * D.nslot + x.slot, nsl = gridDim.x * D.nslot;
-  const int lo = (int)((long long)items * sid / nsl), hi = (int)((long long)items * (sid + 1) / nsl);
+  auto item_at = [&](long long j) -> int {
+    if constexpr (BLK_GRAD_RUN == 0) {
+      const long long lo = (long long)items * sid / nsl, hi = (long long)items * (sid + 1) / nsl;
+      return lo + j < hi ? (int)(lo + j) : -1;
+    } else {
+      const long long it = ((j / BLK_GRAD_RUN) * nsl + sid) * BLK_GRAD_RUN + j % BLK_GRAD_RUN;
+      return it < items ? (int)it : -1;
+    }
+  };
   auto prefetch = [&](int it) {   // group leader: bulk-copy X_{k+1} -> SN, P_k -> SD of item `it`
-    if (leader && it < hi) {
+    if (leader && it >= 0) {
       fence_proxy_async();
       tma_grp_img(sm + 2 * IM, X_img + (size_t)it * stride + 2 * x.off, C, &bars[0], RE);
       tma_grp_img(sm, P_img + (size_t)it * stride + 2 * x.off, C, &bars[1], RE);
@@ -1897,13 +1913,14 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   };
   // the control values of item `it` into L1 ahead of its Omega build (one line per warp)
   auto prefetch_u = [&](int it) {
-    if (L.lane == 0 && it < hi)
+    if (L.lane == 0 && it >= 0)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(G.u + (size_t)it * nodes * B.J));
   };
   BR<C, R, RE> A, acc, Om;
   const int w0 = x.slot * D.swarps;   // first warp of the slot (trace sum, flags)
-  prefetch(lo);
-  prefetch_u(lo + 1);
+  const int first = item_at(0);
+  prefetch(first);
+  prefetch_u(item_at(1));
   // Omega basis cache (D.omc >= 0: no commutator terms): the warp's strips of Lc_j in TMEM slots omc + j
   // (once per launch) and of L0_b in slot omc + J (once per pulse), so the per-item Omega build reads TMEM
   // instead of the L2 (the same fma sequence as bbuild_omega, term for term)
@@ -1943,9 +1960,9 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     return scheme ? __ldg(scheme + ((size_t)(it / N) * N + it % N) * D.ngroups + x.g) : (unsigned short)0;
   };
   unsigned short code = 0;
-  if (lo < hi) {
-    build(lo);
-    code = code_of(lo);
+  if (first >= 0) {
+    build(first);
+    code = code_of(first);
   }
   if (cache) {   // PWC trace basis: the warp's own entries B_m[c][row] x row weight, once per launch
     for (int mm = 0; mm < B.J; ++mm)
@@ -2004,7 +2021,8 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     }
   };
   int idx = 0;
-  for (int item = lo; item < hi; ++item, ++idx) {
+  int prev = -1;
+  for (int item = first; item >= 0; prev = item, item = item_at(idx + 1), ++idx) {
     const int b = item / N, k = item % N;
     QAL_DCHECK(b < batch && k < N);
     bcopy(A, Om);
@@ -2013,12 +2031,12 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
                                                ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
                                                bad_sh + (idx & 3), scheme, code, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
-    const int nx = item + 1;
+    const int nx = item_at(idx + 1);
     slot_sync(D, x.slot);   // every warp of the slot done with this item's images; previous traces complete
     prefetch(nx);
-    prefetch_u(nx + 1);
-    if (L.w == w0 && idx > 0) finish(item - 1, red_tr + (size_t)(par ^ 1) * D.tr_buf, (idx - 1) & 3);
-    if (nx < hi) {
+    prefetch_u(item_at(idx + 2));
+    if (L.w == w0 && idx > 0) finish(prev, red_tr + (size_t)(par ^ 1) * D.tr_buf, (idx - 1) & 3);
+    if (nx >= 0) {
       build(nx);
       code = code_of(nx);
     }
@@ -2026,7 +2044,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
   }
   slot_sync(D, x.slot);   // the last item's traces complete
-  if (L.w == w0 && idx > 0) finish(hi - 1, red_tr + (size_t)((idx - 1) & 1) * D.tr_buf, (idx - 1) & 3);
+  if (L.w == w0 && idx > 0) finish(prev, red_tr + (size_t)((idx - 1) & 1) * D.tr_buf, (idx - 1) & 3);
 }
 
 // FC == 0: any mix of roles (runtime dispatch); else every warp runs role <FC, FR, FKS, FRE> and the
