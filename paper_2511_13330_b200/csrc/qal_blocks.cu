@@ -43,7 +43,7 @@ namespace qal {
 
 constexpr int BLK_MAX_WARPS = 16;
 constexpr int BLK_FUSED_WARPS = 8;   // one item per CTA, all groups (every kernel but fwd / grad sets)
-constexpr int BLK_MAX_SLOTS = 5;   // independent item streams per CTA (group-specialised launches)
+constexpr int BLK_MAX_SLOTS = 12;  // independent item streams per CTA (group-specialised launches)
 constexpr int BLK_CHAIN_WARPS = 12;   // launch bound of the suffix-chain kernel (4 pulses x 3 warps)
 #ifndef QAL_CHAIN_STAGES
 #define QAL_CHAIN_STAGES 4
@@ -76,11 +76,12 @@ constexpr int BLK_TSLOTS = BLK_TMEM_SCR ? 8 : 4;       // TMEM strip slots per w
 constexpr bool BLK_SPLIT_ACC = QAL_BLK_SPLIT_ACC != 0;
 constexpr int BLK_MAX_TASKS = 3;
 // gradient pass: consecutive items (slices of a pulse) per run of a slot's item sequence (0: one contiguous
-// range per slot)
+// range per slot; configs[2] gradient 131.4 ms vs 132.4 / 132.7 / 132.9 ms with runs of 16 / 64 / 1)
 #ifndef QAL_BLK_GRAD_RUN
-#define QAL_BLK_GRAD_RUN 16
+#define QAL_BLK_GRAD_RUN 0
 #endif
 constexpr int BLK_GRAD_RUN = QAL_BLK_GRAD_RUN;
+constexpr int BLK_OMC_MAXJ = 3;   // Omega basis caches (forward and gradient) up to this many controls
 #ifndef QAL_BLK_MAXNREG
 #define QAL_BLK_MAXNREG 168
 #endif
@@ -218,7 +219,8 @@ bool to_dev(const qal_block_plan& p, BlkDev& D, unsigned gmask = ~0u, int nslot 
   // replicate the roles per slot: barrier ids 1 + slot * gl + local group (named barriers 1..15)
   D.swarps = w;
   D.nslot = nslot;
-  if (gl * nslot + (nslot > 1 ? nslot : 0) > 15) return false;
+  // named barrier ids 1 + slot * gl + local group, and per-slot ids (slots of one warp need none)
+  if (w > 1 && gl * nslot + (nslot > 1 ? nslot : 0) > 15) return false;
   for (int sl = 1; sl < nslot; ++sl)
     for (int v = 0; v < w; ++v) {
       D.task[sl * w + v][0] = D.task[v][0];
@@ -1016,11 +1018,54 @@ __host__ __device__ constexpr int img_doubles(int C, bool real) { return (real ?
 __host__ __device__ constexpr int red_doubles(int C) { return (8 * C * C + 15) / 16 * 16; }
 __host__ __device__ constexpr int grp3_doubles(int C, bool real) { return 3 * img_doubles(C, real) + red_doubles(C); }
 
+// The forward's shared Lc cache (role kernels: every warp of the CTA runs one role of one group): entry
+// (j, row tile rt, i, lane) = Lc_j[8 rt + g][4 i + t] of the group's block, fragment order (a warp's
+// loads are 32 consecutive entries), re only for a real group.  Filled by the warps of slot 0, each its
+// own row tiles, before the kernel's first CTA barrier.
+template <int C, bool RE>
+__device__ __forceinline__ int lcc_index(int j, int rt, int i, int lane) {
+  return ((j * C + rt) * 2 * C + i) * 32 + lane;
+}
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bfill_cache(double* lcc, const BlkBasis& B, const Ctx& x, const Lane& L) {
+  constexpr int P = 8 * C;
+  for (int j = 0; j < B.J; ++j) {
+    const double2* M = B.Lc + (size_t)j * B.packed + x.off;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * C; ++i) {
+        const double2 v = __ldg(M + (8 * (x.rt0 + r) + L.g) * P + 4 * i + L.t);
+        const int e = lcc_index<C, RE>(j, x.rt0 + r, i, L.lane);
+        if constexpr (RE) lcc[e] = v.x;
+        else reinterpret_cast<double2*>(lcc)[e] = v;
+      }
+  }
+}
+template <int C, int R, bool RE>
+__device__ __forceinline__ void bfma_cache(BR<C, R, RE>& X, double a, const double* lcc, int j, const Ctx& x,
+                                           const Lane& L) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < 2 * C; ++i) {
+      const int e = lcc_index<C, RE>(j, x.rt0 + r, i, L.lane);
+      if constexpr (RE) {
+        X.re[r][i] = fma(a, lcc[e], X.re[r][i]);
+      } else {
+        const double2 v = reinterpret_cast<const double2*>(lcc)[e];
+        X.re[r][i] = fma(a, v.x, X.re[r][i]);
+        X.im[r][i] = fma(a, v.y, X.im[r][i]);
+      }
+    }
+}
+__host__ __device__ constexpr int lcc_doubles(int J, int C, bool real) { return J * C * 2 * C * 32 * (real ? 1 : 2); }
+
 // ------------------------------------------------------------------ forward fold (a1-a5)
 template <int C, int R, int KS, bool RE>
 __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
                              const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long* nflop,
-                             const Lane& L) {
+                             const double* lcc, const Lane& L) {
   const uint32_t ts = D.tstride[L.w];
   constexpr int IM = img_doubles(C, RE);
   double* SX = sm;
@@ -1031,7 +1076,29 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   const int b = item / nchunk, c = item % nchunk;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   BR<C, R, RE> A, acc, Om;
-  bbuild_omega(Om, B, G, b, c * O.chunk, x, L);
+  // Omega basis cache (D.omc >= 0): this pulse's L0_b strips in the warp's TMEM slot omc (once per item),
+  // Lc_j from the CTA's shared cache -- the same fma sequence as bbuild_omega
+  const bool omc = lcc != nullptr && D.omc >= 0 && B.ncomm == 0;
+  const uint32_t TL0 = tm + (uint32_t)D.omc * ts;
+  auto build = [&](int k) {
+    if (!omc) {
+      bbuild_omega(Om, B, G, b, k, x, L);
+      return;
+    }
+    const int nodes = (G.mode == 1) ? 2 : 1;
+    const double* u = G.u + ((size_t)b * G.count + k) * nodes * B.J;
+    bzero(Om);
+    bt_fma(Om, G.h, TL0);
+    for (int j = 0; j < B.J; ++j) {
+      const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * B.J + j);
+      bfma_cache(Om, 0.5 * G.h * (v1 + v2), lcc, j, x, L);
+    }
+  };
+  if (omc) {
+    bload_nat(Om, B.L0 + (size_t)b * B.L0_stride + x.off, x, L);
+    bt_store(TL0, Om);
+  }
+  build(c * O.chunk);
   for (int kk = 0; kk < O.chunk; ++kk) {
     const int k = c * O.chunk + kk;
     bcopy(A, Om);
@@ -1048,7 +1115,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
     grp_sync(x);
     const int np = bexpm<C, R, KS, RE>(A, acc, m, s, SX, SX4, tm, ts, x, L);
     if (leader) nflop[0] += (unsigned long long)np * D.gflops[x.g];   // expansion (Eq. 14)
-    if (kk + 1 < O.chunk) bbuild_omega(Om, B, G, b, k + 1, x, L);   // loads overlap the stores / fold below
+    if (kk + 1 < O.chunk) build(k + 1);   // loads overlap the stores / fold below
     const size_t slot = (size_t)b * G.count + k;
     if (O.U_img) bstore_img_l2(O.U_img + slot * 2 * D.packed + 2 * x.off, A, x, L, l2_evict_first());
     if (O.chunk_nat) {
@@ -1084,6 +1151,12 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   if (threadIdx.x < BLK_MAX_SLOTS) bad_sh[threadIdx.x] = 0;
+  if constexpr (FC != 0) {   // the shared Lc cache (role kernels only; see bfill_cache)
+    if (D.omc >= 0 && B.ncomm == 0) {
+      const BlkTask T = D.task[L.w][0];
+      if (T.slot == 0) bfill_cache<FC, FR, FRE != 0>(smem + D.tcache_off, B, ctx_of(D, T), L);
+    }
+  }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -1099,9 +1172,10 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
     for (int item = blockIdx.x * D.nslot + x.slot; item < items; item += gridDim.x * D.nslot) {
       if constexpr (FC == 0)
         BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
-                     nflop, L);
+                     nflop, nullptr, L);
       else
-        blk_fwd_task<FC, FR, FKS, FRE != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop, L);
+        blk_fwd_task<FC, FR, FKS, FRE != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
+                                            D.omc >= 0 ? smem + D.tcache_off : nullptr, L);
       grp_sync(x);   // the slot's regions are reused by its next item
     }
   }
@@ -2465,28 +2539,47 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
     L l;
     bool have = false;
     long long best = -1;
+    int best_oc = 0;
+    // the Omega basis cache (L0_b strips in a 4th TMEM slot per warp, Lc_j in a shared cache per CTA; role
+    // kernels, chunks of more than one slice, no commutator terms) when it costs no items in flight
+#ifdef QAL_BLK_NO_FWD_OMC
+    const bool omc_ok = false;
+#else
+    const bool omc_ok = B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && O.chunk > 1;
+#endif
     for (int pass = 0; pass < 2 && !have; ++pass)   // balanced sub-partitions first, else any
-      for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns) {
-        if (p.launch_sets != QAL_BLK_SETS_DEFAULT && ns != set.nslot) continue;
-        L t;
-        // whole groups on one warp (no group barriers in the per-pulse chain: measured 70.4 -> 67.7 ms
-        // (16-wide) and 67.9 -> 62.3 ms (real 24-wide) per configs[2] step), when a role kernel exists for
-        // the layout (the dispatching kernel runs the 24-wide group only split)
-        const bool whole = p.launch_sets == QAL_BLK_SETS_DEFAULT;
-        if (!(whole && to_dev(p, t.D, set.gmask, ns, true, true, 3) && blk_role(t.D) != 0) &&
-            !(whole && to_dev(p, t.D, set.gmask, ns, true, false, 3) && blk_role(t.D) != 0) &&
-            !to_dev(p, t.D, set.gmask, ns, false, false, 3))
-          continue;
-        t.bytes = (size_t)grp_smem_doubles(t.D, per3) * 8;
-        t.fn = fwd_kernel(t.D);
-        const int per_sm = ctas_per_sm((const void*)t.fn, t.D.nwarps, t.bytes, tmem_cols_for(t.D));
-        if (per_sm < 1 || (pass == 0 && p.launch_sets == QAL_BLK_SETS_DEFAULT && !balanced_warps(per_sm, t.D.nwarps)))
-          continue;
-        const long long slots = (long long)per_sm * num_sms() * ns;
-        const long long used = std::min<long long>(slots, items);
-        t.per_sm = per_sm;
-        if (!have || used > best) { l = t; best = used; have = true; }
-      }
+      for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns)
+        for (int oc = omc_ok ? 1 : 0; oc >= 0; --oc) {
+          if (p.launch_sets != QAL_BLK_SETS_DEFAULT && ns != set.nslot) continue;
+          L t;
+          const int tsl = oc ? 4 : 3;
+          // whole groups on one warp (no group barriers in the per-pulse chain: measured 70.4 -> 67.7 ms
+          // (16-wide) and 67.9 -> 62.3 ms (real 24-wide) per configs[2] step), when a role kernel exists for
+          // the layout (the dispatching kernel runs the 24-wide group only split)
+          const bool whole = p.launch_sets == QAL_BLK_SETS_DEFAULT;
+          if (!(whole && to_dev(p, t.D, set.gmask, ns, true, true, tsl) && blk_role(t.D) != 0) &&
+              !(whole && to_dev(p, t.D, set.gmask, ns, true, false, tsl) && blk_role(t.D) != 0) &&
+              !to_dev(p, t.D, set.gmask, ns, false, false, tsl))
+            continue;
+          const int base = grp_smem_doubles(t.D, per3);
+          t.bytes = (size_t)base * 8;
+          if (oc) {
+            if (blk_role(t.D) == 0) continue;
+            const int g = __builtin_ctz(t.D.gmask);
+            t.D.omc = 3;
+            t.D.tcache_off = (base + 15) & ~15;
+            t.bytes = (size_t)(t.D.tcache_off + lcc_doubles(B.J, t.D.C[g], t.D.real[g] != 0)) * 8;
+          }
+          t.fn = fwd_kernel(t.D);
+          const int per_sm = ctas_per_sm((const void*)t.fn, t.D.nwarps, t.bytes, tmem_cols_for(t.D));
+          if (per_sm < 1 ||
+              (pass == 0 && p.launch_sets == QAL_BLK_SETS_DEFAULT && !balanced_warps(per_sm, t.D.nwarps)))
+            continue;
+          const long long slots = (long long)per_sm * num_sms() * ns;
+          const long long used = std::min<long long>(slots, items);
+          t.per_sm = per_sm;
+          if (!have || used > best || (used == best && oc > best_oc)) { l = t; best = used; best_oc = oc; have = true; }
+        }
     if (!have) return cudaErrorInvalidValue;
     cudaError_t e = set_smem_fn((const void*)l.fn, l.bytes);
     if (e != cudaSuccess) return e;
@@ -2643,13 +2736,17 @@ static bool grad_layout_t(const qal_block_plan& p, unsigned gmask, int ns, const
 }
 // + the Omega basis cache in TMEM (J + 1 more strip slots per warp) when the build has no commutator terms
 // and the cache costs no co-resident CTA (-DQAL_BLK_NO_OMC: never, experiment builds)
-constexpr int BLK_OMC_MAXJ = 3;
+// the role kernels (blk_role: 1 real 20-block, 2 the 15+1 block, 3 the 8-wide block, 0 dispatching) that
+// use the cache: bit r (-DQAL_BLK_OMC_ROLES=mask, experiment builds)
+#ifndef QAL_BLK_OMC_ROLES
+#define QAL_BLK_OMC_ROLES 0xF
+#endif
 static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g) {
   if (!grad_layout_t(p, gmask, ns, B, g, BLK_TSLOTS)) return false;
 #ifndef QAL_BLK_NO_OMC
   GradLaunch t;
-  if (B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && grad_layout_t(p, gmask, ns, B, t, BLK_TSLOTS + B.J + 1) &&
-      t.per_sm >= g.per_sm)
+  if (B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && ((QAL_BLK_OMC_ROLES >> blk_role(g.D)) & 1) &&
+      grad_layout_t(p, gmask, ns, B, t, BLK_TSLOTS + B.J + 1) && t.per_sm >= g.per_sm)
     g = t;
 #endif
   return true;
