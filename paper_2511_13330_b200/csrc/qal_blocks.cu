@@ -1062,7 +1062,7 @@ __device__ __forceinline__ void bfma_cache(BR<C, R, RE>& X, double a, const doub
 __host__ __device__ constexpr int lcc_doubles(int J, int C, bool real) { return J * C * 2 * C * 32 * (real ? 1 : 2); }
 
 // ------------------------------------------------------------------ forward fold (a1-a5)
-template <int C, int R, int KS, bool RE>
+template <int C, int R, int KS, bool RE, bool OMC = false>
 __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
                              const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long* nflop,
                              const double* lcc, const Lane& L) {
@@ -1076,12 +1076,14 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   const int b = item / nchunk, c = item % nchunk;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   BR<C, R, RE> A, acc, Om;
-  // Omega basis cache (D.omc >= 0): this pulse's L0_b strips in the warp's TMEM slot omc (once per item),
-  // Lc_j from the CTA's shared cache -- the same fma sequence as bbuild_omega
-  const bool omc = lcc != nullptr && D.omc >= 0 && B.ncomm == 0;
-  const uint32_t TL0 = tm + (uint32_t)D.omc * ts;
+  // Omega basis cache (OMC: the launcher chose it, D.omc >= 0, no commutator terms): this pulse's L0_b
+  // strips in the warp's TMEM slot omc (once per item), Lc_j from the CTA's shared cache -- the same fma
+  // sequence as bbuild_omega.  A compile-time choice: the kernels without the cache (NODES mode with
+  // commutator terms, one-slice chunks) keep the plain build's code (as a runtime flag it cost them 5%).
+  constexpr bool omc = OMC;
+  const uint32_t TL0 = tm + (uint32_t)(OMC ? D.omc : 0) * ts;
   auto build = [&](int k) {
-    if (!omc) {
+    if constexpr (!omc) {
       bbuild_omega(Om, B, G, b, k, x, L);
       return;
     }
@@ -1094,7 +1096,7 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
       bfma_cache(Om, 0.5 * G.h * (v1 + v2), lcc, j, x, L);
     }
   };
-  if (omc) {
+  if constexpr (omc) {
     bload_nat(Om, B.L0 + (size_t)b * B.L0_stride + x.off, x, L);
     bt_store(TL0, Om);
   }
@@ -1140,7 +1142,8 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   if (O.chunk_nat) bstore_nat(O.chunk_nat + ((size_t)b * nchunk + c) * D.packed + x.off, A, x, L);
 }
 
-template <int FC, int FR, int FKS, int FRE>   // as k_blk_grad_slices: FC == 0 any roles
+// FOMC: with the Omega basis cache (role kernels only)
+template <int FC, int FR, int FKS, int FRE, int FOMC = 0>   // as k_blk_grad_slices: FC == 0 any roles
 __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
                                                                           BlkFwdOut O, int items, int tmem_cols,
                                                                           unsigned long long* ctr,
@@ -1151,11 +1154,9 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   if (threadIdx.x < BLK_MAX_SLOTS) bad_sh[threadIdx.x] = 0;
-  if constexpr (FC != 0) {   // the shared Lc cache (role kernels only; see bfill_cache)
-    if (D.omc >= 0 && B.ncomm == 0) {
-      const BlkTask T = D.task[L.w][0];
-      if (T.slot == 0) bfill_cache<FC, FR, FRE != 0>(smem + D.tcache_off, B, ctx_of(D, T), L);
-    }
+  if constexpr (FC != 0 && FOMC != 0) {   // the shared Lc cache (see bfill_cache)
+    const BlkTask T = D.task[L.w][0];
+    if (T.slot == 0) bfill_cache<FC, FR, FRE != 0>(smem + D.tcache_off, B, ctx_of(D, T), L);
   }
   tmem_fence_before();
   __syncthreads();
@@ -1174,8 +1175,8 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
         BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
                      nflop, nullptr, L);
       else
-        blk_fwd_task<FC, FR, FKS, FRE != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
-                                            D.omc >= 0 ? smem + D.tcache_off : nullptr, L);
+        blk_fwd_task<FC, FR, FKS, FRE != 0, FOMC != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
+                                                       FOMC != 0 ? smem + D.tcache_off : nullptr, L);
       grp_sync(x);   // the slot's regions are reused by its next item
     }
   }
@@ -2371,6 +2372,15 @@ static PrefixKernel prefix_kernel(const BlkDev& D) {
   }
 }
 static FwdKernel fwd_kernel(const BlkDev& D) {
+  if (D.omc >= 0)   // with the Omega basis cache (launch_blk_expm_fold sets omc for role kernels only)
+    switch (blk_role(D)) {
+      case 1: return k_blk_expm_fold<3, 1, 5, 1, 1>;
+      case 2: return k_blk_expm_fold<2, 1, 4, 0, 1>;
+      case 3: return k_blk_expm_fold<1, 1, 2, 0, 1>;
+      case 4: return k_blk_expm_fold<2, 2, 4, 0, 1>;
+      case 5: return k_blk_expm_fold<3, 3, 5, 1, 1>;
+      default: return nullptr;
+    }
   switch (blk_role(D)) {
     case 1: return k_blk_expm_fold<3, 1, 5, 1>;
     case 2: return k_blk_expm_fold<2, 1, 4, 0>;
