@@ -97,6 +97,19 @@ constexpr int BLK_OMC_MAXJ = 3;   // Omega basis caches (forward and gradient) u
 #endif
 #define BLK_ROLE_MAXNREG(FC) \
   ((FC) == 1 ? QAL_BLK_MAXNREG_C1 : (FC) == 2 ? QAL_BLK_MAXNREG_C2 : (FC) == 3 ? QAL_BLK_MAXNREG_C3 : QAL_BLK_MAXNREG)
+// the gradient role kernels' own caps (default: the role's cap)
+#ifndef QAL_BLK_GRAD_MAXNREG_C1
+#define QAL_BLK_GRAD_MAXNREG_C1 QAL_BLK_MAXNREG_C1
+#endif
+#ifndef QAL_BLK_GRAD_MAXNREG_C2
+#define QAL_BLK_GRAD_MAXNREG_C2 QAL_BLK_MAXNREG_C2
+#endif
+#ifndef QAL_BLK_GRAD_MAXNREG_C3
+#define QAL_BLK_GRAD_MAXNREG_C3 QAL_BLK_MAXNREG_C3
+#endif
+#define BLK_GRAD_MAXNREG(FC)                                                               \
+  ((FC) == 1 ? QAL_BLK_GRAD_MAXNREG_C1 : (FC) == 2 ? QAL_BLK_GRAD_MAXNREG_C2 : (FC) == 3 ? QAL_BLK_GRAD_MAXNREG_C3 \
+                                                                                          : QAL_BLK_MAXNREG)
 
 __device__ __forceinline__ unsigned dyn_smem_bytes() {
   unsigned v;
@@ -1950,7 +1963,7 @@ __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& 
 // next item's Omega (basis loads in flight during the traces) and this item's per-warp traces.  The
 // trace buffers are double-buffered by item parity and the non-finite flags kept four deep, so one slot
 // barrier per item suffices.
-template <int C, int R, int KS, bool RE>
+template <int C, int R, int KS, bool RE, bool OMC = false>
 __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, const SliceGrid& G,
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
                               double* __restrict__ grad, int* __restrict__ status, const Ctx& x,
@@ -1996,14 +2009,15 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const int first = item_at(0);
   prefetch(first);
   prefetch_u(item_at(1));
-  // Omega basis cache (D.omc >= 0: no commutator terms): the warp's strips of Lc_j in TMEM slots omc + j
-  // (once per launch) and of L0_b in slot omc + J (once per pulse), so the per-item Omega build reads TMEM
-  // instead of the L2 (the same fma sequence as bbuild_omega, term for term)
-  const bool omc = D.omc >= 0 && B.ncomm == 0;
+  // Omega basis cache (OMC: the launcher chose it, D.omc >= 0, no commutator terms; a compile-time variant
+  // of the role kernels, as in the forward): the warp's strips of Lc_j in TMEM slots omc + j (once per
+  // launch) and of L0_b in slot omc + J (once per pulse), so the per-item Omega build reads TMEM instead of
+  // the L2 (the same fma sequence as bbuild_omega, term for term)
+  constexpr bool omc = OMC;
   const uint32_t tso = D.tstride[L.w];
-  const uint32_t TL0 = tm + (uint32_t)(D.omc + B.J) * tso;
+  const uint32_t TL0 = tm + (uint32_t)((OMC ? D.omc : 0) + B.J) * tso;
   long long cur_b = -1;
-  if (omc) {
+  if constexpr (omc) {
     for (int j = 0; j < B.J; ++j) {
       bload_nat(Om, B.Lc + (size_t)j * B.packed + x.off, x, L);
       bt_store(tm + (uint32_t)(D.omc + j) * tso, Om);
@@ -2011,7 +2025,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   }
   auto build = [&](int it) {
     const int b = it / N, k = it % N;
-    if (!omc) {
+    if constexpr (!omc) {
       bbuild_omega(Om, B, G, b, k, x, L);
       return;
     }
@@ -2124,8 +2138,8 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
 
 // FC == 0: any mix of roles (runtime dispatch); else every warp runs role <FC, FR, FKS, FRE> and the
 // kernel is compiled for that role alone (its own register count: a light role gets more warps per SM)
-template <int FC, int FR, int FKS, int FRE>
-__global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B, SliceGrid G,
+template <int FC, int FR, int FKS, int FRE, int FOMC = 0>   // FOMC: with the Omega basis cache (role kernels)
+__global__ void __maxnreg__(BLK_GRAD_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, int batch, BlkBasis B, SliceGrid G,
                                                                const double* __restrict__ P_img,
                                                                const double* __restrict__ X_img,
                                                                double* __restrict__ grad, int* __restrict__ status,
@@ -2163,8 +2177,9 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
     BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status,
                  x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, scheme, nflop, L);
   else
-    blk_grad_loop<FC, FR, FKS, FRE != 0>(D, batch, B, G, P_img, X_img, grad, status, x, sm, bars[x.bar], tm,
-                                          bad_sh[x.slot], red_tr, gscale, accum, cache, scheme, nflop, L);
+    blk_grad_loop<FC, FR, FKS, FRE != 0, FOMC != 0>(D, batch, B, G, P_img, X_img, grad, status, x, sm, bars[x.bar],
+                                                     tm, bad_sh[x.slot], red_tr, gscale, accum, cache, scheme,
+                                                     nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
   tmem_fence_before();
   __syncthreads();
@@ -2336,6 +2351,16 @@ using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, con
 using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*,
                            unsigned long long*);
 static GradKernel grad_kernel(const BlkDev& D) {
+  if (D.omc >= 0)   // with the Omega basis cache (grad_layout sets omc for role kernels only)
+    switch (blk_role(D)) {
+      case 1: return k_blk_grad_slices<3, 1, 5, 1, 1>;
+      case 2: return k_blk_grad_slices<2, 1, 4, 0, 1>;
+      case 3: return k_blk_grad_slices<1, 1, 2, 0, 1>;
+#ifdef QAL_BLK_ROLE_2_2
+      case 4: return k_blk_grad_slices<2, 2, 4, 0, 1>;
+#endif
+      default: return nullptr;
+    }
   switch (blk_role(D)) {
     case 1: return k_blk_grad_slices<3, 1, 5, 1>;
     case 2: return k_blk_grad_slices<2, 1, 4, 0>;
@@ -2749,13 +2774,15 @@ static bool grad_layout_t(const qal_block_plan& p, unsigned gmask, int ns, const
 // the role kernels (blk_role: 1 real 20-block, 2 the 15+1 block, 3 the 8-wide block, 0 dispatching) that
 // use the cache: bit r (-DQAL_BLK_OMC_ROLES=mask, experiment builds)
 #ifndef QAL_BLK_OMC_ROLES
-#define QAL_BLK_OMC_ROLES 0xF
+#define QAL_BLK_OMC_ROLES 0xE
 #endif
 static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g) {
   if (!grad_layout_t(p, gmask, ns, B, g, BLK_TSLOTS)) return false;
 #ifndef QAL_BLK_NO_OMC
   GradLaunch t;
-  if (B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && ((QAL_BLK_OMC_ROLES >> blk_role(g.D)) & 1) &&
+  const int role = blk_role(g.D);
+  const bool role_ok = role >= 1 && role <= 3 && ((QAL_BLK_OMC_ROLES >> role) & 1);
+  if (B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && role_ok &&
       grad_layout_t(p, gmask, ns, B, t, BLK_TSLOTS + B.J + 1) && t.per_sm >= g.per_sm)
     g = t;
 #endif
