@@ -701,27 +701,35 @@ __device__ __forceinline__ void baxpy_nat(BR<C, R, RE>& X, double a, const doubl
 // Omega_k strips of the group from the packed generator basis (a1-a3, as build_omega).  (Measured: issuing
 // the loads of three basis matrices before their FMAs gave nothing -- 18.2M vs 18.5M slices/s on
 // configs[2] -- the L2 latency of the basis is hidden by the other warps of the SM.)
-template <int C, int R, bool RE>
+// PW2: piecewise-constant controls with J = 2 and no commutator terms; NC2: node-sampled controls with J = 2
+// and the commutator basis (3 terms) -- both checked by the launcher: the loops unroll
+template <int C, int R, bool RE, bool PW2 = false, bool NC2 = false>
 __device__ __forceinline__ void bbuild_omega(BR<C, R, RE>& X, const BlkBasis& B, const SliceGrid& G, int b, int k,
                                              const Ctx& x, const Lane& L) {
-  const int J = B.J;
-  const int nodes = (G.mode == 1) ? 2 : 1;
+  constexpr bool J2 = PW2 || NC2;
+  const int J = J2 ? 2 : B.J;
+  const int nodes = PW2 ? 1 : NC2 ? 2 : (G.mode == 1) ? 2 : 1;
   const double* u = G.u + ((size_t)b * G.count + k) * nodes * J;
   bzero(X);
   baxpy_nat(X, G.h, B.L0 + (size_t)b * B.L0_stride + x.off, x, L);
-  for (int j = 0; j < J; ++j) {
+#pragma unroll(J2 ? 2 : 1)
+  for (int j = 0; j < (J2 ? 2 : J); ++j) {
     const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * J + j);
     baxpy_nat(X, 0.5 * G.h * (v1 + v2), B.Lc + (size_t)j * B.packed + x.off, x, L);
   }
-  if (B.ncomm > 0) {
+  if constexpr (PW2) return;
+  if (NC2 || B.ncomm > 0) {
     const double2* Cb = B.Lcomm + (size_t)b * B.Lcomm_stride + x.off;
-    for (int j = 0; j < J; ++j) {
+#pragma unroll(J2 ? 2 : 1)
+    for (int j = 0; j < (J2 ? 2 : J); ++j) {
       const double v1 = __ldg(u + j), v2 = __ldg(u + J + j);
       baxpy_nat(X, -G.c4 * (v2 - v1), Cb + (size_t)j * B.packed, x, L);
     }
     int p = J;
-    for (int a = 0; a < J; ++a)
-      for (int c = a + 1; c < J; ++c, ++p) {
+#pragma unroll(J2 ? 2 : 1)
+    for (int a = 0; a < (J2 ? 2 : J); ++a)
+#pragma unroll(J2 ? 2 : 1)
+      for (int c = a + 1; c < (J2 ? 2 : J); ++c, ++p) {
         const double coef = -G.c4 * (__ldg(u + a) * __ldg(u + J + c) - __ldg(u + c) * __ldg(u + J + a));
         baxpy_nat(X, coef, Cb + (size_t)p * B.packed, x, L);
       }
@@ -1075,7 +1083,10 @@ __device__ __forceinline__ void bfma_cache(BR<C, R, RE>& X, double a, const doub
 __host__ __device__ constexpr int lcc_doubles(int J, int C, bool real) { return J * C * 2 * C * 32 * (real ? 1 : 2); }
 
 // ------------------------------------------------------------------ forward fold (a1-a5)
-template <int C, int R, int KS, bool RE, bool OMC = false>
+// VAR (compile-time variants of the role kernels, chosen by the launcher): bit 0 = the Omega basis cache,
+// bit 2 = piecewise-constant controls with J = 2 (the control loop unrolls), as in blk_grad_loop, bit 3 =
+// node-sampled controls with J = 2 and the commutator basis (configs[3])
+template <int C, int R, int KS, bool RE, int VAR = 0>
 __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid& G, const BlkFwdOut& O, int item,
                              const Ctx& x, double* sm, uint32_t tm, int* bad, unsigned long long* nflop,
                              const double* lcc, const Lane& L) {
@@ -1093,19 +1104,22 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   // strips in the warp's TMEM slot omc (once per item), Lc_j from the CTA's shared cache -- the same fma
   // sequence as bbuild_omega.  A compile-time choice: the kernels without the cache (NODES mode with
   // commutator terms, one-slice chunks) keep the plain build's code (as a runtime flag it cost them 5%).
+  constexpr bool OMC = (VAR & 1) != 0, PW2 = (VAR & 4) != 0, NC2 = (VAR & 8) != 0;
   constexpr bool omc = OMC;
   const uint32_t TL0 = tm + (uint32_t)(OMC ? D.omc : 0) * ts;
   auto build = [&](int k) {
     if constexpr (!omc) {
-      bbuild_omega(Om, B, G, b, k, x, L);
+      bbuild_omega<C, R, RE, PW2, NC2>(Om, B, G, b, k, x, L);
       return;
     }
-    const int nodes = (G.mode == 1) ? 2 : 1;
-    const double* u = G.u + ((size_t)b * G.count + k) * nodes * B.J;
+    const int nodes = PW2 ? 1 : (G.mode == 1) ? 2 : 1;
+    const int BJ = PW2 ? 2 : B.J;
+    const double* u = G.u + ((size_t)b * G.count + k) * nodes * BJ;
     bzero(Om);
     bt_fma(Om, G.h, TL0);
-    for (int j = 0; j < B.J; ++j) {
-      const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * B.J + j);
+#pragma unroll(PW2 ? 2 : 1)
+    for (int j = 0; j < (PW2 ? 2 : BJ); ++j) {
+      const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * BJ + j);
       bfma_cache(Om, 0.5 * G.h * (v1 + v2), lcc, j, x, L);
     }
   };
@@ -1155,7 +1169,8 @@ __device__ void blk_fwd_task(const BlkDev& D, const BlkBasis& B, const SliceGrid
   if (O.chunk_nat) bstore_nat(O.chunk_nat + ((size_t)b * nchunk + c) * D.packed + x.off, A, x, L);
 }
 
-// FOMC: with the Omega basis cache (role kernels only)
+// FOMC: the role kernels' variant bits (blk_fwd_task): 0 none, 1 the Omega basis cache, 4 / 5 J = 2 PWC controls
+// without / with the cache
 template <int FC, int FR, int FKS, int FRE, int FOMC = 0>   // as k_blk_grad_slices: FC == 0 any roles
 __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkBasis B, SliceGrid G,
                                                                           BlkFwdOut O, int items, int tmem_cols,
@@ -1167,7 +1182,7 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
   const Lane L = lane_id();
   if (L.w == 0) blk_tmem_alloc(&tmem_base_sh, tmem_cols);
   if (threadIdx.x < BLK_MAX_SLOTS) bad_sh[threadIdx.x] = 0;
-  if constexpr (FC != 0 && FOMC != 0) {   // the shared Lc cache (see bfill_cache)
+  if constexpr (FC != 0 && (FOMC & 1) != 0) {   // the shared Lc cache (see bfill_cache)
     const BlkTask T = D.task[L.w][0];
     if (T.slot == 0) bfill_cache<FC, FR, FRE != 0>(smem + D.tcache_off, B, ctx_of(D, T), L);
   }
@@ -1188,8 +1203,8 @@ __global__ void __maxnreg__(BLK_ROLE_MAXNREG(FC)) k_blk_expm_fold(BlkDev D, BlkB
         BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_fwd_task, D, B, G, O, item, x, sm, tm, &bad_sh[x.slot],
                      nflop, nullptr, L);
       else
-        blk_fwd_task<FC, FR, FKS, FRE != 0, FOMC != 0>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
-                                                       FOMC != 0 ? smem + D.tcache_off : nullptr, L);
+        blk_fwd_task<FC, FR, FKS, FRE != 0, FOMC>(D, B, G, O, item, x, sm, tm, &bad_sh[x.slot], nflop,
+                                                  (FOMC & 1) != 0 ? smem + D.tcache_off : nullptr, L);
       grp_sync(x);   // the slot's regions are reused by its next item
     }
   }
@@ -1666,7 +1681,7 @@ constexpr int BLK_TRC_MAXJ = 2;   // PWC trace-basis cache in shared memory up t
 // Dual-number evaluation of the forward scheme for one group (qal_grad.cu k_grad_slices, P-wide);
 // leaves W = L_exp(Omega, G) in A and returns the product count.  SD, SV, SN: group images
 // (SN holds X_{k+1}, TMA-prefetched); tm: the warp's 4 TMEM slots.
-template <int C, int R, int KS, bool RE>
+template <int C, int R, int KS, bool RE, bool SCH = false>   // SCH: the forward's (m, s) codes are there (scheme != 0)
 __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc, const BlkBasis& B, const SliceGrid& G,
                                              int b, int k, const Ctx& x, double* SD, double* SV, double* SN,
                                              uint64_t* barN, uint64_t* barP, uint32_t& ph, double* red, double* sX,
@@ -1702,12 +1717,16 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
   // A holds Omega_k on entry (built one item ahead by the caller).  (m, s): the forward pass's choice for
   // this (pulse, slice, group) when it was kept (no norm, no group barrier here), else the same rule
   int m, s;
-  if (scheme) {
+  if constexpr (SCH) {
     if (!scheme_decode(code, m, s) && L.lane == 0) *bad = 1;
   } else {
-    const double nrm = bnorm1(A, red, x, L);
-    choose_scheme_blk(nrm, m, s);
-    if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+    if (scheme) {
+      if (!scheme_decode(code, m, s) && L.lane == 0) *bad = 1;
+    } else {
+      const double nrm = bnorm1(A, red, x, L);
+      choose_scheme_blk(nrm, m, s);
+      if (!(nrm <= 1e300) && L.lane == 0) *bad = 1;
+    }
   }
   const double sc = ldexp(1.0, -s);
   bscale(A, sc);
@@ -1910,13 +1929,15 @@ __device__ __forceinline__ int blk_dual_expm(BR<C, R, RE>& A, BR<C, R, RE>& acc,
 }
 
 // weighted traces Re Tr(W_g B_m,g) over the warp's rows, added to the warp's partial sums
-template <int C, int R, bool RE>
+// TRC: the cache is there (cache != 0); KJ > 0: K = KJ traces (unrolled: their shuffle reductions overlap)
+template <int C, int R, bool RE, bool TRC = false, int KJ = 0>
 __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& D, const BlkBasis& B, int b, const Ctx& x,
                                            double* tr, bool first, const double2* cache, const Lane& L) {
   constexpr int P = 8 * C;
-  const int K = B.J + B.ncomm;
-  if (cache) {   // PWC: the warp's weighted basis values B_m[c][row], staged once in shared memory
-    for (int mm = 0; mm < K; ++mm) {
+  const int K = KJ > 0 ? KJ : B.J + B.ncomm;
+  if (TRC || cache) {   // PWC: the warp's weighted basis values B_m[c][row], staged once in shared memory
+#pragma unroll(KJ > 0 ? KJ : 1)
+    for (int mm = 0; mm < (KJ > 0 ? KJ : K); ++mm) {
       double v = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -1932,6 +1953,7 @@ __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& 
     }
     return;
   }
+  if constexpr (TRC) return;
   for (int mm = 0; mm < K; ++mm) {
     const double2* Bm = (mm < B.J) ? B.Lc + (size_t)mm * B.packed
                                    : B.Lcomm + (size_t)b * B.Lcomm_stride + (size_t)(mm - B.J) * B.packed;
@@ -1963,7 +1985,9 @@ __device__ __forceinline__ void blk_traces(const BR<C, R, RE>& W, const BlkDev& 
 // next item's Omega (basis loads in flight during the traces) and this item's per-warp traces.  The
 // trace buffers are double-buffered by item parity and the non-finite flags kept four deep, so one slot
 // barrier per item suffices.
-template <int C, int R, int KS, bool RE, bool OMC = false>
+// VAR (compile-time variants of the role kernels, chosen by the launcher): bit 0 = the Omega basis cache and
+// the forward's stored (m, s) codes (scheme != 0), bit 1 = the PWC trace-basis cache (cache != 0)
+template <int C, int R, int KS, bool RE, int VAR = 0>
 __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, const SliceGrid& G,
                               const double* __restrict__ P_img, const double* __restrict__ X_img,
                               double* __restrict__ grad, int* __restrict__ status, const Ctx& x,
@@ -1974,8 +1998,12 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   const size_t stride = 2 * (size_t)D.packed;
   const int N = G.count;
   const int items = batch * N;
-  const int K = B.J + B.ncomm;
-  const int nodes = (G.mode == 1) ? 2 : 1;
+  // PW2 (VAR bit 2): piecewise-constant controls with J = 2 (the launcher checked G.mode == 0, B.J == 2, no
+  // commutator terms): the control loops unroll
+  constexpr bool PW2 = (VAR & 4) != 0;
+  const int BJ = PW2 ? 2 : B.J;
+  const int K = PW2 ? 2 : B.J + B.ncomm;
+  const int nodes = PW2 ? 1 : (G.mode == 1) ? 2 : 1;
   const bool leader = (x.rt0 == 0 && L.lane == 0);
   uint32_t ph = 0;
   // this slot's items: runs of BLK_GRAD_RUN consecutive items (slices of one pulse, so the pulse's L0_b
@@ -2002,7 +2030,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   // the control values of item `it` into L1 ahead of its Omega build (one line per warp)
   auto prefetch_u = [&](int it) {
     if (L.lane == 0 && it >= 0)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(G.u + (size_t)it * nodes * B.J));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(G.u + (size_t)it * nodes * BJ));
   };
   BR<C, R, RE> A, acc, Om;
   const int w0 = x.slot * D.swarps;   // first warp of the slot (trace sum, flags)
@@ -2013,12 +2041,14 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   // of the role kernels, as in the forward): the warp's strips of Lc_j in TMEM slots omc + j (once per
   // launch) and of L0_b in slot omc + J (once per pulse), so the per-item Omega build reads TMEM instead of
   // the L2 (the same fma sequence as bbuild_omega, term for term)
+  constexpr bool OMC = (VAR & 1) != 0, TRC = (VAR & 2) != 0;
   constexpr bool omc = OMC;
   const uint32_t tso = D.tstride[L.w];
-  const uint32_t TL0 = tm + (uint32_t)((OMC ? D.omc : 0) + B.J) * tso;
+  const uint32_t TL0 = tm + (uint32_t)((OMC ? D.omc : 0) + BJ) * tso;
   long long cur_b = -1;
   if constexpr (omc) {
-    for (int j = 0; j < B.J; ++j) {
+#pragma unroll(PW2 ? 2 : 1)
+    for (int j = 0; j < (PW2 ? 2 : BJ); ++j) {
       bload_nat(Om, B.Lc + (size_t)j * B.packed + x.off, x, L);
       bt_store(tm + (uint32_t)(D.omc + j) * tso, Om);
     }
@@ -2026,7 +2056,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
   auto build = [&](int it) {
     const int b = it / N, k = it % N;
     if constexpr (!omc) {
-      bbuild_omega(Om, B, G, b, k, x, L);
+      bbuild_omega<C, R, RE, false, (VAR & 8) != 0>(Om, B, G, b, k, x, L);
       return;
     }
     const long long key = B.L0_stride ? b : 0;
@@ -2035,17 +2065,19 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
       bt_store(TL0, Om);
       cur_b = key;
     }
-    const double* u = G.u + ((size_t)b * G.count + k) * nodes * B.J;
+    const double* u = G.u + ((size_t)b * G.count + k) * nodes * BJ;
     bzero(Om);
     bt_fma(Om, G.h, TL0);
-    for (int j = 0; j < B.J; ++j) {
-      const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * B.J + j);
+#pragma unroll(PW2 ? 2 : 1)
+    for (int j = 0; j < (PW2 ? 2 : BJ); ++j) {
+      const double v1 = __ldg(u + j), v2 = __ldg(u + (nodes - 1) * BJ + j);
       bt_fma(Om, 0.5 * G.h * (v1 + v2), tm + (uint32_t)(D.omc + j) * tso);
     }
   };
   // the forward's (m, s) code of an item, loaded with its Omega one item ahead (an L2 round trip that the
   // dual pass of the current item hides)
   auto code_of = [&](int it) -> unsigned short {
+    if constexpr (OMC) return __ldg(scheme + ((size_t)(it / N) * N + it % N) * D.ngroups + x.g);
     return scheme ? __ldg(scheme + ((size_t)(it / N) * N + it % N) * D.ngroups + x.g) : (unsigned short)0;
   };
   unsigned short code = 0;
@@ -2054,7 +2086,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     code = code_of(first);
   }
   if (cache) {   // PWC trace basis: the warp's own entries B_m[c][row] x row weight, once per launch
-    for (int mm = 0; mm < B.J; ++mm)
+    for (int mm = 0; mm < BJ; ++mm)
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -2079,9 +2111,9 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     __syncwarp();
     if (L.lane == 0) {
       const double* T = Tsum;
-      const int J = B.J;
+      const int J = BJ;
       const double inv_d2 = gscale;   // 1/d^2 for the fidelity, 1 for a general cotangent
-      if (G.mode == 0) {
+      if (PW2 || G.mode == 0) {
         double* gg = grad + ((size_t)b * N + k) * J;
         for (int j = 0; j < J; ++j) gg[j] = (accum ? gg[j] : 0.0) + G.h * T[j] * inv_d2;
       } else {
@@ -2116,7 +2148,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
     QAL_DCHECK(b < batch && k < N);
     bcopy(A, Om);
     const int par = idx & 1;   // item parity: double-buffered traces
-    const int np = blk_dual_expm<C, R, KS, RE>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
+    const int np = blk_dual_expm<C, R, KS, RE, OMC>(A, acc, B, G, b, k, x, sm, sm + IM, sm + 2 * IM, &bars[0], &bars[1],
                                                ph, sm + 3 * IM, sm + 3 * IM + red_doubles(C), tm, D.tstride[L.w],
                                                bad_sh + (idx & 3), scheme, code, L);
     if (leader) nflop += (unsigned long long)np * D.gflops[x.g];
@@ -2130,7 +2162,7 @@ __device__ void blk_grad_loop(const BlkDev& D, int batch, const BlkBasis& B, con
       code = code_of(nx);
     }
     double* rt = red_tr + (size_t)par * D.tr_buf;
-    blk_traces<C, R, RE>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
+    blk_traces<C, R, RE, TRC, PW2 ? 2 : 0>(A, D, B, b, x, rt + L.w * D.tr_k, true, cache, L);
   }
   slot_sync(D, x.slot);   // the last item's traces complete
   if (L.w == w0 && idx > 0) finish(prev, red_tr + (size_t)((idx - 1) & 1) * D.tr_buf, (idx - 1) & 3);
@@ -2177,7 +2209,7 @@ __global__ void __maxnreg__(BLK_GRAD_MAXNREG(FC)) k_blk_grad_slices(BlkDev D, in
     BLK_DISPATCH(D.C[x.g], T.R, x.ks, D.real[x.g], blk_grad_loop, D, batch, B, G, P_img, X_img, grad, status,
                  x, sm, bars[x.bar], tm, bad_sh[x.slot], red_tr, gscale, accum, cache, scheme, nflop, L);
   else
-    blk_grad_loop<FC, FR, FKS, FRE != 0, FOMC != 0>(D, batch, B, G, P_img, X_img, grad, status, x, sm, bars[x.bar],
+    blk_grad_loop<FC, FR, FKS, FRE != 0, FOMC>(D, batch, B, G, P_img, X_img, grad, status, x, sm, bars[x.bar],
                                                      tm, bad_sh[x.slot], red_tr, gscale, accum, cache, scheme,
                                                      nflop, L);
   if (ctr && nflop) atomicAdd(ctr, nflop);
@@ -2350,15 +2382,35 @@ using GradKernel = void (*)(BlkDev, int, BlkBasis, SliceGrid, const double*, con
                             int, int, const unsigned short*, unsigned long long*);
 using FwdKernel = void (*)(BlkDev, BlkBasis, SliceGrid, BlkFwdOut, int, int, unsigned long long*,
                            unsigned long long*);
-static GradKernel grad_kernel(const BlkDev& D) {
-  if (D.omc >= 0)   // with the Omega basis cache (grad_layout sets omc for role kernels only)
+static GradKernel grad_kernel(const BlkDev& D, bool pw2, bool nc2) {
+  // the variants with the Omega basis cache + stored (m, s) codes (grad_layout sets omc for role kernels
+  // only, and only when the codes are there), with the PWC trace-basis cache as well when the layout has it
+  if (nc2 && D.omc < 0)   // node-sampled controls, J = 2, commutator basis: the Omega build unrolled
+    switch (blk_role(D)) {
+      case 1: return k_blk_grad_slices<3, 1, 5, 1, 8>;
+      case 2: return k_blk_grad_slices<2, 1, 4, 0, 8>;
+      case 3: return k_blk_grad_slices<1, 1, 2, 0, 8>;
+      default: break;
+    }
+  if (D.omc >= 0 && D.tcache_off >= 0 && pw2)   // + piecewise-constant controls with J = 2 (unrolled)
+    switch (blk_role(D)) {
+      case 1: return k_blk_grad_slices<3, 1, 5, 1, 7>;
+      case 2: return k_blk_grad_slices<2, 1, 4, 0, 7>;
+      case 3: return k_blk_grad_slices<1, 1, 2, 0, 7>;
+      default: break;
+    }
+  if (D.omc >= 0 && D.tcache_off >= 0)
+    switch (blk_role(D)) {
+      case 1: return k_blk_grad_slices<3, 1, 5, 1, 3>;
+      case 2: return k_blk_grad_slices<2, 1, 4, 0, 3>;
+      case 3: return k_blk_grad_slices<1, 1, 2, 0, 3>;
+      default: break;
+    }
+  if (D.omc >= 0)
     switch (blk_role(D)) {
       case 1: return k_blk_grad_slices<3, 1, 5, 1, 1>;
       case 2: return k_blk_grad_slices<2, 1, 4, 0, 1>;
       case 3: return k_blk_grad_slices<1, 1, 2, 0, 1>;
-#ifdef QAL_BLK_ROLE_2_2
-      case 4: return k_blk_grad_slices<2, 2, 4, 0, 1>;
-#endif
       default: return nullptr;
     }
   switch (blk_role(D)) {
@@ -2396,7 +2448,34 @@ static PrefixKernel prefix_kernel(const BlkDev& D) {
     default: return k_blk_prefix_chain<0, 0, 0, 0>;
   }
 }
-static FwdKernel fwd_kernel(const BlkDev& D) {
+static FwdKernel fwd_kernel(const BlkDev& D, bool pw2, bool nc2) {
+  if (nc2 && D.omc < 0)   // node-sampled controls, J = 2, commutator basis
+    switch (blk_role(D)) {
+      case 1: return k_blk_expm_fold<3, 1, 5, 1, 8>;
+      case 2: return k_blk_expm_fold<2, 1, 4, 0, 8>;
+      case 3: return k_blk_expm_fold<1, 1, 2, 0, 8>;
+      case 4: return k_blk_expm_fold<2, 2, 4, 0, 8>;
+      case 5: return k_blk_expm_fold<3, 3, 5, 1, 8>;
+      default: break;
+    }
+  if (D.omc >= 0 && pw2)   // the Omega basis cache with piecewise-constant controls, J = 2 (unrolled)
+    switch (blk_role(D)) {
+      case 1: return k_blk_expm_fold<3, 1, 5, 1, 5>;
+      case 2: return k_blk_expm_fold<2, 1, 4, 0, 5>;
+      case 3: return k_blk_expm_fold<1, 1, 2, 0, 5>;
+      case 4: return k_blk_expm_fold<2, 2, 4, 0, 5>;
+      case 5: return k_blk_expm_fold<3, 3, 5, 1, 5>;
+      default: return nullptr;
+    }
+  if (pw2)   // piecewise-constant controls, J = 2, no cache
+    switch (blk_role(D)) {
+      case 1: return k_blk_expm_fold<3, 1, 5, 1, 4>;
+      case 2: return k_blk_expm_fold<2, 1, 4, 0, 4>;
+      case 3: return k_blk_expm_fold<1, 1, 2, 0, 4>;
+      case 4: return k_blk_expm_fold<2, 2, 4, 0, 4>;
+      case 5: return k_blk_expm_fold<3, 3, 5, 1, 4>;
+      default: break;
+    }
   if (D.omc >= 0)   // with the Omega basis cache (launch_blk_expm_fold sets omc for role kernels only)
     switch (blk_role(D)) {
       case 1: return k_blk_expm_fold<3, 1, 5, 1, 1>;
@@ -2605,7 +2684,7 @@ cudaError_t launch_blk_expm_fold(const qal_block_plan& p, int batch, const BlkBa
             t.D.tcache_off = (base + 15) & ~15;
             t.bytes = (size_t)(t.D.tcache_off + lcc_doubles(B.J, t.D.C[g], t.D.real[g] != 0)) * 8;
           }
-          t.fn = fwd_kernel(t.D);
+          t.fn = fwd_kernel(t.D, G.mode == 0 && B.J == 2 && B.ncomm == 0, G.mode == 1 && B.J == 2 && B.ncomm == 3);
           const int per_sm = ctas_per_sm((const void*)t.fn, t.D.nwarps, t.bytes, tmem_cols_for(t.D));
           if (per_sm < 1 ||
               (pass == 0 && p.launch_sets == QAL_BLK_SETS_DEFAULT && !balanced_warps(per_sm, t.D.nwarps)))
@@ -2747,7 +2826,7 @@ struct GradLaunch {
   int per_sm;
 };
 static bool grad_layout_t(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g,
-                          int tslots) {
+                          int tslots, bool pw2, bool nc2) {
   if (!to_dev(p, g.D, gmask, ns, false, false, tslots)) return false;
   if (tslots > BLK_TSLOTS) g.D.omc = BLK_TSLOTS;
   int base = grp_smem_doubles(g.D, per_grad);
@@ -2756,15 +2835,17 @@ static bool grad_layout_t(const qal_block_plan& p, unsigned gmask, int ns, const
   g.D.tr_off = (base + 15) & ~15;
   base = g.D.tr_off + 2 * g.D.tr_buf;
   g.D.tcache_off = -1;
-  g.fn = grad_kernel(g.D);
+  g.fn = grad_kernel(g.D, pw2, nc2);
   g.bytes = (size_t)base * 8;
   g.per_sm = ctas_per_sm((const void*)g.fn, g.D.nwarps, g.bytes, tmem_cols_for(g.D));
   if (B.ncomm == 0 && B.J <= BLK_TRC_MAXJ) {
     BlkDev trial = g.D;
     const size_t with = (size_t)grad_cache_layout(trial, B.J, base) * 8;
-    if (ctas_per_sm((const void*)g.fn, g.D.nwarps, with, tmem_cols_for(g.D)) >= g.per_sm) {
+    const GradKernel fn2 = grad_kernel(trial, pw2, nc2);   // (its own variant: the register count may differ)
+    if (ctas_per_sm((const void*)fn2, g.D.nwarps, with, tmem_cols_for(g.D)) >= g.per_sm) {
       g.D = trial;
       g.bytes = with;
+      g.fn = fn2;
     }
   }
   return g.per_sm > 0;
@@ -2776,14 +2857,17 @@ static bool grad_layout_t(const qal_block_plan& p, unsigned gmask, int ns, const
 #ifndef QAL_BLK_OMC_ROLES
 #define QAL_BLK_OMC_ROLES 0xE
 #endif
-static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g) {
-  if (!grad_layout_t(p, gmask, ns, B, g, BLK_TSLOTS)) return false;
+static bool grad_layout(const qal_block_plan& p, unsigned gmask, int ns, const BlkBasis& B, GradLaunch& g,
+                        bool have_scheme, bool pwc) {
+  const bool pw2 = pwc && B.J == 2 && B.ncomm == 0;
+  const bool nc2 = !pwc && B.J == 2 && B.ncomm == 3;
+  if (!grad_layout_t(p, gmask, ns, B, g, BLK_TSLOTS, pw2, nc2)) return false;
 #ifndef QAL_BLK_NO_OMC
   GradLaunch t;
   const int role = blk_role(g.D);
-  const bool role_ok = role >= 1 && role <= 3 && ((QAL_BLK_OMC_ROLES >> role) & 1);
+  const bool role_ok = have_scheme && role >= 1 && role <= 3 && ((QAL_BLK_OMC_ROLES >> role) & 1);
   if (B.ncomm == 0 && B.J >= 1 && B.J <= BLK_OMC_MAXJ && role_ok &&
-      grad_layout_t(p, gmask, ns, B, t, BLK_TSLOTS + B.J + 1) && t.per_sm >= g.per_sm)
+      grad_layout_t(p, gmask, ns, B, t, BLK_TSLOTS + B.J + 1, pw2, nc2) && t.per_sm >= g.per_sm)
     g = t;
 #endif
   return true;
@@ -2805,13 +2889,13 @@ cudaError_t launch_blk_grad_slices(const qal_block_plan& p, int batch, const Blk
       for (int pass = 0; pass < 2 && !have; ++pass)   // balanced sub-partitions first, else any
         for (int ns = 1; ns <= BLK_MAX_SLOTS; ++ns) {
           GradLaunch t;
-          if (!grad_layout(p, set.gmask, ns, B, t)) continue;
+          if (!grad_layout(p, set.gmask, ns, B, t, scheme != nullptr, G.mode == 0)) continue;
           const int wt = pass == 0 ? balanced_warps(t.per_sm, t.D.nwarps) : t.per_sm * t.D.nwarps;
           if (wt > best) { g = t; best = wt; }
         }
       have = best > 0;
     } else {
-      have = grad_layout(p, set.gmask, set.nslot, B, g);
+      have = grad_layout(p, set.gmask, set.nslot, B, g, scheme != nullptr, G.mode == 0);
     }
     if (!have) return cudaErrorInvalidValue;
     cudaError_t e = set_smem_fn((const void*)g.fn, g.bytes);

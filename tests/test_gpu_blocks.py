@@ -509,3 +509,56 @@ def test_block_gradient_degenerate_and_ragged_sizes(torch_cuda, qal, oracle, bat
         Fr, gr, _ = oracle.gradient(rL0, rLc, p.u[b], p.T, p.N, p.V)
         assert abs(F[b] - Fr) / abs(Fr) <= TOL_PROP
         assert relfro(g[b], gr) <= TOL_GRAD
+
+
+def _with_controls(p, J):
+    """The cfg0 problem with J control Hamiltonians: the first one only, or the two exchange terms plus a
+    third S_z-conserving one (the 1-3 exchange), with seeded piecewise-constant amplitudes."""
+    import dataclasses
+    sx = np.array([[0, 1], [1, 0]], dtype=complex)
+    sy = np.array([[0, -1j], [1j, 0]], dtype=complex)
+    sz = np.array([[1, 0], [0, -1]], dtype=complex)
+    i2 = np.eye(2, dtype=complex)
+    if J == 1:
+        Hc = p.Hc[:1].copy()
+    else:
+        H13 = sum(np.kron(np.kron(s, i2), s) for s in (sx, sy, sz)) / 4.0
+        Hc = np.concatenate([p.Hc, H13[None]], axis=0)
+    rng = np.random.default_rng(1234 + J)
+    u = rng.uniform(0.0, 2 * np.pi * 0.05, size=(1, p.N, J))
+    return dataclasses.replace(p, Hc=Hc, u=u)
+
+
+@pytest.mark.parametrize("J", [1, 3])
+def test_block_gradient_other_control_counts(torch_cuda, qal, oracle, J):
+    """The gradient role kernels are compiled in variants (Omega basis cache + stored (m, s) codes, PWC
+    trace-basis cache, J = 2 unrolled); J = 1 takes the variant without the unrolled loops and J = 3 the one
+    without the trace-basis cache.  Same parity bar as J = 2."""
+    torch = torch_cuda
+    p = _with_controls(qi.cfg0(N=24, T=100.0 * 24 / 256), J)
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Fr, gr, Lam = oracle.gradient(rL0, rLc, p.u[0], p.T, p.N, p.V)
+    F, g, Lp = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, p.u), p.T, p.N, dev(torch, p.V),
+                                           want_Lambda=True)
+    assert g.shape == (1, p.N, J)
+    assert relfro(qal.qal_block_unpack(plan, Lp)[0].cpu().numpy(), Lam) <= TOL_PROP
+    assert abs(F.item() - Fr) <= TOL_PROP * max(abs(Fr), 1e-3)
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD, relfro(g[0].cpu().numpy(), gr)
+
+
+def test_nodes_mode_order2_block_gradient(torch_cuda, qal, oracle):
+    """Node-sampled controls at Magnus order 2 (no commutator terms): the cached-basis variants with two
+    control values per slice."""
+    torch = torch_cuda
+    p = qi.cfg3()
+    N, T = 48, 200.0
+    u = oracle.sines_nodes(p.sines, p.u_max, N, T)[None]
+    plan, L0p, Lcp, _ = packed_basis(torch, qal, p)
+    rL0, rLc = oracle.build_liouvillian(p.H0[0], p.Hc, p.C)
+    Fr, gr, _ = oracle.gradient(rL0, rLc, u[0], T, N, p.V, mode=1, order=2)
+    F, g, _ = qal.qal_block_fidelity_grad(plan, L0p, Lcp, dev(torch, u), T, N, dev(torch, p.V), ctrl_mode=1,
+                                          magnus_order=2)
+    assert abs(F.item() - Fr) / abs(Fr) <= TOL_PROP
+    assert g.shape == (1, N, 2, 2)
+    assert relfro(g[0].cpu().numpy(), gr) <= TOL_GRAD
